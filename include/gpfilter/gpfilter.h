@@ -1,0 +1,108 @@
+/* gpfilter.h -- B200 drop-in for the Gauss-polynomial bilateral filter path.
+ *
+ * This header declares the C ABI that libgpfilter_b200.so exports. Every
+ * entry point keeps the name, argument meaning, status codes and error
+ * behaviour of the reference library's public header, so a caller written
+ * against the reference binds to this library unchanged for the GPF path.
+ * Each declaration cites the reference interface it replaces
+ * (/root/reference/proj/include/gpfilter/gpfilter.h, "ref.h" below).
+ *
+ * Only the hot path and the handles/params/errors it needs are provided.
+ * The exact filter, Taylor baseline, direct Gaussian, kernel evaluators,
+ * metrics and PGM I/O stay in the reference library.
+ */
+#ifndef GPFILTER_B200_GPFILTER_H
+#define GPFILTER_B200_GPFILTER_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* Status codes: same numeric values as ref.h:18-29. */
+typedef enum gpf_status {
+  GPF_OK = 0,
+  GPF_ERR_INVALID_ARGUMENT = 1,
+  GPF_ERR_IO = 2,
+  GPF_ERR_SIGMA_TOO_SMALL = 3,
+  GPF_ERR_PGM_BAD_MAGIC = 4,
+  GPF_ERR_PGM_BAD_DIMS = 5,
+  GPF_ERR_PGM_BAD_MAXVAL = 6,
+  GPF_ERR_PGM_TRUNCATED = 7,
+  GPF_ERR_PGM_BAD_PIXEL = 8,
+  GPF_ERR_UNKNOWN = 9 /* also: CUDA runtime failures (detail in gpf_last_error) */
+} gpf_status;
+
+/* ref.h:31-39 */
+const char* gpf_status_name(gpf_status status);
+const char* gpf_last_error(void); /* thread-local detail of the last failure */
+const char* gpf_version(void);
+
+/* Opaque row-major width*height grid of doubles (ref.h:45-58). */
+typedef struct gpf_image gpf_image;
+gpf_status gpf_image_create(int width, int height, gpf_image** out); /* zero-filled, w,h >= 1 */
+void gpf_image_destroy(gpf_image* img);                               /* NULL is a no-op */
+int gpf_image_width(const gpf_image* img);                            /* 0 for NULL */
+int gpf_image_height(const gpf_image* img);
+double* gpf_image_data(gpf_image* img);                               /* NULL for NULL */
+const double* gpf_image_cdata(const gpf_image* img);
+
+/* Parameters (ref.h:64-90); identical layout and defaults. */
+typedef enum gpf_boundary {
+  GPF_BOUNDARY_REPLICATE = 0,
+  GPF_BOUNDARY_REFLECT = 1,
+  GPF_BOUNDARY_ZERO = 2
+} gpf_boundary;
+
+typedef enum gpf_backend {
+  GPF_BACKEND_DIRECT = 0,   /* not provided on the GPU: returns GPF_ERR_INVALID_ARGUMENT */
+  GPF_BACKEND_RECURSIVE = 1 /* the O(1) Deriche path, sigma_s >= 0.5 */
+} gpf_backend;
+
+typedef struct gpf_spatial_params {
+  double sigma_s;     /* > 0 */
+  int window_radius;  /* <= 0 selects ceil(3 sigma_s); unused by the recursive path */
+  gpf_boundary boundary; /* validated; the recursive path always uses the
+                            replicate steady state, as the reference does */
+  double kernel_scale;   /* > 0 */
+} gpf_spatial_params;
+
+typedef struct gpf_range_params {
+  double sigma_r; /* > 0 */
+  int degree;     /* polynomial degree N >= 0 (N+2 filtered planes) */
+} gpf_range_params;
+
+void gpf_spatial_params_init(gpf_spatial_params* sp); /* 2 / auto / replicate / 1.0 */
+void gpf_range_params_init(gpf_range_params* rp);     /* 30 / 20 */
+
+/* The hot path (replaces ref.h:100-107, proj/src/capi.cpp:176-192).
+ * Validation and status mapping follow the reference: NULL in/sp/rp/out ->
+ * INVALID_ARGUMENT; *out is set to NULL before work starts; bad backend or
+ * boundary enum, sigma_s <= 0, kernel_scale <= 0, sigma_r <= 0, degree < 0 ->
+ * INVALID_ARGUMENT (detail names the field); sigma_s < 0.5 ->
+ * GPF_ERR_SIGMA_TOO_SMALL with "direct" in the detail. fallback_count may be
+ * NULL and is written only on success. Pixels with |Q| <= 1e-8 (reference
+ * units, proj/src/core/bilateral.hpp:85) keep their input value. */
+gpf_status gpf_filter_gpf(const gpf_image* in, const gpf_spatial_params* sp,
+                          const gpf_range_params* rp, gpf_backend backend,
+                          int centering, long long* fallback_count,
+                          gpf_image** out);
+
+/* Spatial recursive Gaussian alone (ref.h:118-119, proj/src/capi.cpp:219-228):
+ * same Deriche filter, output scaled by kernel_mass_1d(sigma_s)^2*kernel_scale. */
+gpf_status gpf_gaussian_recursive(const gpf_image* in, double sigma_s,
+                                  double kernel_scale, gpf_image** out);
+
+/* Thread-count plumbing (ref.h:165-168). Kept for ABI compatibility; the
+ * value is recorded but device work is always deterministic and identical
+ * for every count. */
+gpf_status gpf_set_num_threads(int n);
+int gpf_get_num_threads(void);
+
+#ifdef __cplusplus
+} /* extern "C" */
+#endif
+
+#endif /* GPFILTER_B200_GPFILTER_H */

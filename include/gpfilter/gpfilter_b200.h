@@ -1,0 +1,55 @@
+/* gpfilter_b200.h -- device-resident batched entry points (B200 extension).
+ *
+ * The reference ABI (gpfilter.h) moves one double image through host memory
+ * per call. Throughput users keep fp32 frames resident in HBM and filter a
+ * batch per call; these entries expose exactly that, with the same parameter
+ * structs, validation and status codes as gpf_filter_gpf.
+ *
+ * A plan binds (width, height, sigma_s, kernel_scale, sigma_r, degree,
+ * centering) to one CUDA device and owns the device workspace (the N+2
+ * intermediate planes, carries and per-frame scalars). Plans are not shared
+ * between concurrent callers; create one per thread/stream.
+ */
+#ifndef GPFILTER_B200_EXT_H
+#define GPFILTER_B200_EXT_H
+
+#include "gpfilter/gpfilter.h"
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct gpf_b200_plan gpf_b200_plan;
+
+/* Validates like gpf_filter_gpf (backend is implied recursive) and allocates
+ * the workspace on `device` (-1 = current device). */
+gpf_status gpf_b200_plan_create(int width, int height, const gpf_spatial_params* sp,
+                                const gpf_range_params* rp, int centering, int device,
+                                gpf_b200_plan** out);
+void gpf_b200_plan_destroy(gpf_b200_plan* plan);
+
+/* Bytes of device workspace held by the plan. */
+size_t gpf_b200_plan_workspace_bytes(const gpf_b200_plan* plan);
+
+/* Kernel launches enqueued per frame (for launch accounting in benchmarks). */
+int gpf_b200_plan_launches_per_frame(const gpf_b200_plan* plan);
+
+/* Filters `count` contiguous fp32 frames (each width*height, row-major) that
+ * live in device memory. d_out may not alias d_in. d_fallbacks (device
+ * memory, `count` long longs, may be NULL) receives per-frame fallback
+ * counts. Work is enqueued on `stream` (a cudaStream_t, NULL = legacy
+ * default stream); the call returns without synchronising. */
+gpf_status gpf_b200_filter_f32(gpf_b200_plan* plan, const float* d_in, float* d_out,
+                               int count, long long* d_fallbacks, void* stream);
+
+/* Same, from host memory to host memory: copies each frame in, filters,
+ * copies the result and the fallback counts back, and synchronises `stream`
+ * before returning. h_fallbacks (host, `count` entries) may be NULL. */
+gpf_status gpf_b200_filter_f32_host(gpf_b200_plan* plan, const float* h_in, float* h_out,
+                                    int count, long long* h_fallbacks, void* stream);
+
+#ifdef __cplusplus
+} /* extern "C" */
+#endif
+
+#endif /* GPFILTER_B200_EXT_H */

@@ -1,0 +1,13 @@
+"""B200-native Gauss-polynomial O(1) bilateral filter (arXiv 1505.00077 GPF path).
+
+The compute path is libgpfilter_b200.so (hand-written sm_100a kernels behind a
+C ABI that mirrors the reference's gpf_filter_gpf). This package is the thin
+host-side binding; it never computes the filter on the CPU.
+"""
+from ._lib import LIB_PATH, build  # noqa: F401
+from .gpf import (GpfError, Image, Plan, gpf_filter_gpf, gpf_gaussian_recursive,  # noqa: F401
+                  get_num_threads, range_params, set_num_threads, spatial_params)
+
+__all__ = ["GpfError", "Image", "Plan", "gpf_filter_gpf", "gpf_gaussian_recursive",
+           "range_params", "spatial_params", "set_num_threads", "get_num_threads", "build",
+           "LIB_PATH"]

@@ -1,0 +1,98 @@
+"""ctypes binding of libgpfilter_b200.so (the in-tree C-ABI library).
+
+There is no Python or CPU compute path behind these bindings: if the shared
+library is missing or cannot be loaded, importing this module raises.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+import subprocess
+
+PKG_DIR = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(PKG_DIR, "libgpfilter_b200.so")
+
+# gpf_status values (include/gpfilter/gpfilter.h)
+GPF_OK = 0
+GPF_ERR_INVALID_ARGUMENT = 1
+GPF_ERR_IO = 2
+GPF_ERR_SIGMA_TOO_SMALL = 3
+GPF_ERR_UNKNOWN = 9
+
+GPF_BOUNDARY_REPLICATE, GPF_BOUNDARY_REFLECT, GPF_BOUNDARY_ZERO = 0, 1, 2
+GPF_BACKEND_DIRECT, GPF_BACKEND_RECURSIVE = 0, 1
+
+# Every symbol include/gpfilter/*.h declares.
+EXPORTED = (
+    "gpf_status_name", "gpf_last_error", "gpf_version",
+    "gpf_image_create", "gpf_image_destroy", "gpf_image_width", "gpf_image_height",
+    "gpf_image_data", "gpf_image_cdata",
+    "gpf_spatial_params_init", "gpf_range_params_init",
+    "gpf_filter_gpf", "gpf_gaussian_recursive",
+    "gpf_set_num_threads", "gpf_get_num_threads",
+    "gpf_b200_plan_create", "gpf_b200_plan_destroy", "gpf_b200_plan_workspace_bytes",
+    "gpf_b200_plan_launches_per_frame", "gpf_b200_filter_f32", "gpf_b200_filter_f32_host",
+)
+
+
+class SpatialParams(C.Structure):
+    """gpf_spatial_params (reference gpfilter.h:75-80)."""
+    _fields_ = [("sigma_s", C.c_double), ("window_radius", C.c_int),
+                ("boundary", C.c_int), ("kernel_scale", C.c_double)]
+
+
+class RangeParams(C.Structure):
+    """gpf_range_params (reference gpfilter.h:82-85)."""
+    _fields_ = [("sigma_r", C.c_double), ("degree", C.c_int)]
+
+
+def build() -> None:
+    """Compile libgpfilter_b200.so for sm_100a (nvcc cross-compiles; no GPU needed)."""
+    subprocess.run(["make", "-s", "-C", PKG_DIR], check=True)
+
+
+def _declare(lib: C.CDLL) -> C.CDLL:
+    vp, dp = C.c_void_p, C.POINTER(C.c_double)
+    pvp = C.POINTER(vp)
+    lib.gpf_status_name.restype = C.c_char_p
+    lib.gpf_status_name.argtypes = [C.c_int]
+    lib.gpf_last_error.restype = C.c_char_p
+    lib.gpf_version.restype = C.c_char_p
+    lib.gpf_image_create.argtypes = [C.c_int, C.c_int, pvp]
+    lib.gpf_image_destroy.argtypes = [vp]
+    lib.gpf_image_width.argtypes = [vp]
+    lib.gpf_image_height.argtypes = [vp]
+    lib.gpf_image_data.restype = dp
+    lib.gpf_image_data.argtypes = [vp]
+    lib.gpf_image_cdata.restype = dp
+    lib.gpf_image_cdata.argtypes = [vp]
+    lib.gpf_spatial_params_init.argtypes = [C.POINTER(SpatialParams)]
+    lib.gpf_range_params_init.argtypes = [C.POINTER(RangeParams)]
+    lib.gpf_filter_gpf.argtypes = [vp, C.POINTER(SpatialParams), C.POINTER(RangeParams), C.c_int,
+                                   C.c_int, C.POINTER(C.c_longlong), pvp]
+    lib.gpf_gaussian_recursive.argtypes = [vp, C.c_double, C.c_double, pvp]
+    lib.gpf_set_num_threads.argtypes = [C.c_int]
+    lib.gpf_b200_plan_create.argtypes = [C.c_int, C.c_int, C.POINTER(SpatialParams),
+                                         C.POINTER(RangeParams), C.c_int, C.c_int, pvp]
+    lib.gpf_b200_plan_destroy.argtypes = [vp]
+    lib.gpf_b200_plan_workspace_bytes.restype = C.c_size_t
+    lib.gpf_b200_plan_workspace_bytes.argtypes = [vp]
+    lib.gpf_b200_plan_launches_per_frame.argtypes = [vp]
+    lib.gpf_b200_filter_f32.argtypes = [vp, vp, vp, C.c_int, vp, vp]
+    lib.gpf_b200_filter_f32_host.argtypes = [vp, vp, vp, C.c_int, C.POINTER(C.c_longlong), vp]
+    return lib
+
+
+_LIB: C.CDLL | None = None
+
+
+def lib() -> C.CDLL:
+    """The loaded library. Raises (never falls back) if it is absent."""
+    global _LIB
+    if _LIB is None:
+        if not os.path.exists(LIB_PATH):
+            raise ImportError(
+                f"{LIB_PATH} is missing: build it with __graft_entry__.build() or "
+                f"`make -C {PKG_DIR}` (there is no CPU fallback)")
+        _LIB = _declare(C.CDLL(LIB_PATH))
+    return _LIB

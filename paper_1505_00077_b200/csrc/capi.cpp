@@ -1,0 +1,355 @@
+// C ABI of libgpfilter_b200 (include/gpfilter/gpfilter.h, gpfilter_b200.h).
+//
+// Mirrors the reference's proj/src/capi.cpp for the GPF path: same validation
+// order and messages (to_spatial 65-80, to_backend 82-88, SpatialParams /
+// RangeParams validate, spatial.cpp:25-35 / range_kernel.cpp:22-29,
+// recursive_gaussian's SigmaTooSmallError, spatial.cpp:222-230), thread-local
+// last error (capi.cpp:28-33), *out = NULL before work, fallback_count written
+// only on success. There is no CPU compute path: every filter call runs the
+// sm_100a kernels, and a missing device is an error.
+#include <cmath>
+#include <cstring>
+#include <atomic>
+#include <memory>
+#include <mutex>
+#include <new>
+#include <string>
+#include <vector>
+
+#include <cuda_runtime.h>
+
+#include "gpf_internal.h"
+#include "gpfilter/gpfilter.h"
+#include "gpfilter/gpfilter_b200.h"
+
+struct gpf_image {
+  int w, h;
+  std::vector<double> data;
+};
+
+struct gpf_b200_plan {
+  gpfb::Plan plan;
+  unsigned long long* d_fb = nullptr;  // per-frame counters (grown on demand)
+  int d_fb_cap = 0;
+  float* d_stage_in = nullptr;         // host-entry staging (one frame)
+  float* d_stage_out = nullptr;
+};
+
+namespace {
+
+thread_local std::string g_last_error;
+std::atomic<int> g_threads{1};
+
+gpf_status fail(gpf_status s, const std::string& msg) {
+  g_last_error = msg;
+  return s;
+}
+
+void cuda_check(cudaError_t e, const char* what) {
+  if (e != cudaSuccess) throw gpfb::Error{GPF_ERR_UNKNOWN, std::string(what) + ": " + cudaGetErrorString(e)};
+}
+
+template <typename Fn>
+gpf_status guarded(Fn&& fn) {
+  try {
+    fn();
+    return GPF_OK;
+  } catch (const gpfb::Error& e) {
+    return fail(static_cast<gpf_status>(e.status), e.msg);
+  } catch (const std::bad_alloc&) {
+    return fail(GPF_ERR_UNKNOWN, "std::bad_alloc");
+  } catch (const std::exception& e) {
+    return fail(GPF_ERR_UNKNOWN, e.what());
+  }
+}
+
+[[noreturn]] void invalid(const std::string& m) { throw gpfb::Error{GPF_ERR_INVALID_ARGUMENT, m}; }
+
+// Validation of the GPF path, in the reference's order.
+gpfb::Params validate(int w, int h, const gpf_spatial_params& sp, const gpf_range_params& rp,
+                      gpf_backend backend, int centering) {
+  // to_spatial (capi.cpp:65-80): boundary enum checked even though unused.
+  if (sp.boundary != GPF_BOUNDARY_REPLICATE && sp.boundary != GPF_BOUNDARY_REFLECT &&
+      sp.boundary != GPF_BOUNDARY_ZERO)
+    invalid("boundary must be replicate, reflect, or zero");
+  // to_backend (capi.cpp:82-88)
+  if (backend != GPF_BACKEND_DIRECT && backend != GPF_BACKEND_RECURSIVE)
+    invalid("backend must be direct or recursive");
+  // SpatialParams::validate (spatial.cpp:25-35)
+  const int radius = sp.window_radius > 0 ? sp.window_radius : gpfb::default_window_radius(sp.sigma_s);
+  if (!(sp.sigma_s > 0.0)) invalid("SpatialParams: sigma_s must be > 0");
+  if (radius < 1) invalid("SpatialParams: window_radius must be >= 1");
+  if (!(sp.kernel_scale > 0.0)) invalid("SpatialParams: kernel_scale must be > 0");
+  // RangeParams::validate (range_kernel.cpp:22-29)
+  if (!(rp.sigma_r > 0.0)) invalid("RangeParams: sigma_r must be > 0");
+  if (rp.degree < 0) invalid("RangeParams: degree must be >= 0");
+  if (backend == GPF_BACKEND_DIRECT)
+    invalid("the direct (windowed) backend is not provided by the B200 library; "
+            "use GPF_BACKEND_RECURSIVE");
+  // recursive_gaussian (spatial.cpp:222-230)
+  if (sp.sigma_s < 0.5)
+    throw gpfb::Error{GPF_ERR_SIGMA_TOO_SMALL,
+                      "recursive_gaussian: sigma_s < 0.5 is not supported; use the direct backend"};
+  if (rp.degree + 2 > gpfb::kMaxPlanes)
+    invalid("RangeParams: degree must be <= 62 in the B200 library");
+  if (w < 1 || h < 1) invalid("Image dimensions must be >= 1");
+  gpfb::Params p;
+  p.width = w;
+  p.height = h;
+  p.sigma_s = sp.sigma_s;
+  p.kernel_scale = sp.kernel_scale;
+  p.sigma_r = rp.sigma_r;
+  p.degree = rp.degree;
+  p.centering = centering != 0 ? 1 : 0;
+  return p;
+}
+
+int current_device() {
+  int n = 0;
+  if (cudaGetDeviceCount(&n) != cudaSuccess || n == 0) {
+    cudaGetLastError();
+    throw gpfb::Error{GPF_ERR_UNKNOWN, "no CUDA device available (the B200 library has no CPU path)"};
+  }
+  int d = 0;
+  cuda_check(cudaGetDevice(&d), "cudaGetDevice");
+  return d;
+}
+
+// RAII device buffer
+struct DevBuf {
+  void* p = nullptr;
+  explicit DevBuf(size_t n) { cuda_check(cudaMalloc(&p, n), "cudaMalloc"); }
+  ~DevBuf() { cudaFree(p); }
+  DevBuf(const DevBuf&) = delete;
+  DevBuf& operator=(const DevBuf&) = delete;
+};
+
+struct PlanGuard {
+  gpfb::Plan plan;
+  bool live = false;
+  ~PlanGuard() {
+    if (live) gpfb::plan_free(plan);
+  }
+};
+
+}  // namespace
+
+extern "C" {
+
+const char* gpf_status_name(gpf_status status) {
+  switch (status) {
+    case GPF_OK: return "GPF_OK";
+    case GPF_ERR_INVALID_ARGUMENT: return "GPF_ERR_INVALID_ARGUMENT";
+    case GPF_ERR_IO: return "GPF_ERR_IO";
+    case GPF_ERR_SIGMA_TOO_SMALL: return "GPF_ERR_SIGMA_TOO_SMALL";
+    case GPF_ERR_PGM_BAD_MAGIC: return "GPF_ERR_PGM_BAD_MAGIC";
+    case GPF_ERR_PGM_BAD_DIMS: return "GPF_ERR_PGM_BAD_DIMS";
+    case GPF_ERR_PGM_BAD_MAXVAL: return "GPF_ERR_PGM_BAD_MAXVAL";
+    case GPF_ERR_PGM_TRUNCATED: return "GPF_ERR_PGM_TRUNCATED";
+    case GPF_ERR_PGM_BAD_PIXEL: return "GPF_ERR_PGM_BAD_PIXEL";
+    case GPF_ERR_UNKNOWN: return "GPF_ERR_UNKNOWN";
+  }
+  return "GPF_ERR_UNKNOWN";
+}
+
+const char* gpf_last_error(void) { return g_last_error.c_str(); }
+
+const char* gpf_version(void) { return "1.0.0-b200"; }
+
+gpf_status gpf_image_create(int width, int height, gpf_image** out) {
+  if (out == nullptr) return fail(GPF_ERR_INVALID_ARGUMENT, "out is null");
+  *out = nullptr;
+  if (width < 1 || height < 1) return fail(GPF_ERR_INVALID_ARGUMENT, "Image dimensions must be >= 1");
+  return guarded([&] {
+    *out = new gpf_image{width, height, std::vector<double>((size_t)width * height, 0.0)};
+  });
+}
+
+void gpf_image_destroy(gpf_image* img) { delete img; }
+int gpf_image_width(const gpf_image* img) { return img ? img->w : 0; }
+int gpf_image_height(const gpf_image* img) { return img ? img->h : 0; }
+double* gpf_image_data(gpf_image* img) { return img ? img->data.data() : nullptr; }
+const double* gpf_image_cdata(const gpf_image* img) { return img ? img->data.data() : nullptr; }
+
+void gpf_spatial_params_init(gpf_spatial_params* sp) {
+  if (!sp) return;
+  sp->sigma_s = 2.0;
+  sp->window_radius = 0;
+  sp->boundary = GPF_BOUNDARY_REPLICATE;
+  sp->kernel_scale = 1.0;
+}
+
+void gpf_range_params_init(gpf_range_params* rp) {
+  if (!rp) return;
+  rp->sigma_r = 30.0;
+  rp->degree = 20;
+}
+
+gpf_status gpf_filter_gpf(const gpf_image* in, const gpf_spatial_params* sp,
+                          const gpf_range_params* rp, gpf_backend backend, int centering,
+                          long long* fallback_count, gpf_image** out) {
+  if (in == nullptr || sp == nullptr || rp == nullptr || out == nullptr)
+    return fail(GPF_ERR_INVALID_ARGUMENT, "null argument");
+  *out = nullptr;
+  return guarded([&] {
+    const gpfb::Params p = validate(in->w, in->h, *sp, *rp, backend, centering);
+    const int dev = current_device();
+    const size_t n = (size_t)p.width * p.height;
+    PlanGuard g;
+    gpfb::plan_init(g.plan, p, dev);
+    g.live = true;
+    DevBuf din(n * sizeof(double)), dout(n * sizeof(double)), dfb(sizeof(unsigned long long));
+    cudaStream_t st;
+    cuda_check(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking), "cudaStreamCreate");
+    struct StreamGuard {
+      cudaStream_t s;
+      ~StreamGuard() { cudaStreamDestroy(s); }
+    } sg{st};
+    cuda_check(cudaMemcpyAsync(din.p, in->data.data(), n * sizeof(double), cudaMemcpyHostToDevice, st),
+               "cudaMemcpyAsync(H2D)");
+    cuda_check(cudaMemsetAsync(dfb.p, 0, sizeof(unsigned long long), st), "cudaMemsetAsync");
+    gpfb::run_frame_f64(g.plan, static_cast<const double*>(din.p), static_cast<double*>(dout.p),
+                        static_cast<unsigned long long*>(dfb.p), st);
+    auto* res = new gpf_image{p.width, p.height, std::vector<double>(n)};
+    std::unique_ptr<gpf_image> hold(res);
+    unsigned long long fb = 0;
+    cuda_check(cudaMemcpyAsync(res->data.data(), dout.p, n * sizeof(double), cudaMemcpyDeviceToHost, st),
+               "cudaMemcpyAsync(D2H)");
+    cuda_check(cudaMemcpyAsync(&fb, dfb.p, sizeof(fb), cudaMemcpyDeviceToHost, st), "cudaMemcpyAsync(D2H)");
+    cuda_check(cudaStreamSynchronize(st), "cudaStreamSynchronize");
+    if (fallback_count != nullptr) *fallback_count = static_cast<long long>(fb);
+    *out = hold.release();
+  });
+}
+
+gpf_status gpf_gaussian_recursive(const gpf_image* in, double sigma_s, double kernel_scale,
+                                  gpf_image** out) {
+  if (in == nullptr || out == nullptr) return fail(GPF_ERR_INVALID_ARGUMENT, "null argument");
+  *out = nullptr;
+  return guarded([&] {
+    // spatial.cpp:222-230
+    if (!(sigma_s > 0.0) || !(kernel_scale > 0.0))
+      invalid("recursive_gaussian: sigma_s and kernel_scale must be > 0");
+    if (sigma_s < 0.5)
+      throw gpfb::Error{GPF_ERR_SIGMA_TOO_SMALL,
+                        "recursive_gaussian: sigma_s < 0.5 is not supported; use the direct backend"};
+    current_device();
+    const size_t n = (size_t)in->w * in->h;
+    DevBuf din(n * sizeof(double)), dout(n * sizeof(double)), dtmp(n * sizeof(double));
+    cuda_check(cudaMemcpy(din.p, in->data.data(), n * sizeof(double), cudaMemcpyHostToDevice), "H2D");
+    const double mass = gpfb::kernel_mass_1d(sigma_s, gpfb::default_window_radius(sigma_s));
+    gpfb::run_gaussian_f64(static_cast<const double*>(din.p), static_cast<double*>(dout.p),
+                           static_cast<double*>(dtmp.p), in->w, in->h, sigma_s,
+                           mass * mass * kernel_scale, nullptr);
+    auto* res = new gpf_image{in->w, in->h, std::vector<double>(n)};
+    std::unique_ptr<gpf_image> hold(res);
+    cuda_check(cudaMemcpy(res->data.data(), dout.p, n * sizeof(double), cudaMemcpyDeviceToHost), "D2H");
+    *out = hold.release();
+  });
+}
+
+gpf_status gpf_set_num_threads(int n) {
+  if (n < 1) return fail(GPF_ERR_INVALID_ARGUMENT, "thread count must be >= 1");
+  g_threads.store(n);
+  return GPF_OK;
+}
+
+int gpf_get_num_threads(void) { return g_threads.load(); }
+
+// ---------------------------------------------------------------- B200 plans
+gpf_status gpf_b200_plan_create(int width, int height, const gpf_spatial_params* sp,
+                                const gpf_range_params* rp, int centering, int device,
+                                gpf_b200_plan** out) {
+  if (sp == nullptr || rp == nullptr || out == nullptr)
+    return fail(GPF_ERR_INVALID_ARGUMENT, "null argument");
+  *out = nullptr;
+  return guarded([&] {
+    const gpfb::Params p = validate(width, height, *sp, *rp, GPF_BACKEND_RECURSIVE, centering);
+    int dev = current_device();
+    if (device >= 0) {
+      cuda_check(cudaSetDevice(device), "cudaSetDevice");
+      dev = device;
+    }
+    auto* pl = new gpf_b200_plan();
+    std::unique_ptr<gpf_b200_plan> hold(pl);
+    gpfb::plan_init(pl->plan, p, dev);
+    *out = hold.release();
+  });
+}
+
+void gpf_b200_plan_destroy(gpf_b200_plan* plan) {
+  if (!plan) return;
+  int prev = 0;
+  cudaGetDevice(&prev);
+  cudaSetDevice(plan->plan.device);
+  gpfb::plan_free(plan->plan);
+  cudaFree(plan->d_fb);
+  cudaFree(plan->d_stage_in);
+  cudaFree(plan->d_stage_out);
+  cudaSetDevice(prev);
+  delete plan;
+}
+
+size_t gpf_b200_plan_workspace_bytes(const gpf_b200_plan* plan) { return plan ? plan->plan.bytes : 0; }
+
+int gpf_b200_plan_launches_per_frame(const gpf_b200_plan* plan) {
+  return plan ? plan->plan.launches_per_frame : 0;
+}
+
+gpf_status gpf_b200_filter_f32(gpf_b200_plan* plan, const float* d_in, float* d_out, int count,
+                               long long* d_fallbacks, void* stream) {
+  if (plan == nullptr || d_in == nullptr || d_out == nullptr)
+    return fail(GPF_ERR_INVALID_ARGUMENT, "null argument");
+  if (count < 0) return fail(GPF_ERR_INVALID_ARGUMENT, "count must be >= 0");
+  return guarded([&] {
+    cuda_check(cudaSetDevice(plan->plan.device), "cudaSetDevice");
+    auto st = static_cast<cudaStream_t>(stream);
+    const size_t npx = (size_t)plan->plan.p.width * plan->plan.p.height;
+    auto* fb = reinterpret_cast<unsigned long long*>(d_fallbacks);
+    if (fb) cuda_check(cudaMemsetAsync(fb, 0, sizeof(long long) * count, st), "cudaMemsetAsync");
+    else if (plan->d_fb_cap < 1) {
+      cuda_check(cudaMalloc(&plan->d_fb, sizeof(unsigned long long)), "cudaMalloc");
+      plan->d_fb_cap = 1;
+    }
+    for (int f = 0; f < count; ++f)
+      gpfb::run_frame_f32(plan->plan, d_in + f * npx, d_out + f * npx, fb ? fb + f : plan->d_fb, st);
+  });
+}
+
+gpf_status gpf_b200_filter_f32_host(gpf_b200_plan* plan, const float* h_in, float* h_out, int count,
+                                    long long* h_fallbacks, void* stream) {
+  if (plan == nullptr || h_in == nullptr || h_out == nullptr)
+    return fail(GPF_ERR_INVALID_ARGUMENT, "null argument");
+  if (count < 0) return fail(GPF_ERR_INVALID_ARGUMENT, "count must be >= 0");
+  return guarded([&] {
+    cuda_check(cudaSetDevice(plan->plan.device), "cudaSetDevice");
+    auto st = static_cast<cudaStream_t>(stream);
+    const size_t npx = (size_t)plan->plan.p.width * plan->plan.p.height;
+    if (!plan->d_stage_in) {
+      cuda_check(cudaMalloc(&plan->d_stage_in, npx * sizeof(float)), "cudaMalloc");
+      cuda_check(cudaMalloc(&plan->d_stage_out, npx * sizeof(float)), "cudaMalloc");
+    }
+    if (plan->d_fb_cap < count) {
+      cudaFree(plan->d_fb);
+      cuda_check(cudaMalloc(&plan->d_fb, sizeof(unsigned long long) * std::max(count, 1)), "cudaMalloc");
+      plan->d_fb_cap = std::max(count, 1);
+    }
+    cuda_check(cudaMemsetAsync(plan->d_fb, 0, sizeof(unsigned long long) * count, st), "memset");
+    for (int f = 0; f < count; ++f) {
+      cuda_check(cudaMemcpyAsync(plan->d_stage_in, h_in + f * npx, npx * sizeof(float),
+                                 cudaMemcpyHostToDevice, st), "H2D");
+      gpfb::run_frame_f32(plan->plan, plan->d_stage_in, plan->d_stage_out, plan->d_fb + f, st);
+      cuda_check(cudaMemcpyAsync(h_out + f * npx, plan->d_stage_out, npx * sizeof(float),
+                                 cudaMemcpyDeviceToHost, st), "D2H");
+    }
+    std::vector<unsigned long long> fb(count);
+    if (count > 0)
+      cuda_check(cudaMemcpyAsync(fb.data(), plan->d_fb, sizeof(unsigned long long) * count,
+                                 cudaMemcpyDeviceToHost, st), "D2H");
+    cuda_check(cudaStreamSynchronize(st), "cudaStreamSynchronize");
+    if (h_fallbacks)
+      for (int f = 0; f < count; ++f) h_fallbacks[f] = static_cast<long long>(fb[f]);
+  });
+}
+
+}  // extern "C"

@@ -1,0 +1,134 @@
+// Host-side filter constants (fp64), see gpf_internal.h.
+#include <cmath>
+#include <complex>
+
+#include "gpf_internal.h"
+
+namespace gpfb {
+
+using cd = std::complex<double>;
+
+// proj/src/core/spatial.cpp:14-16
+int default_window_radius(double sigma_s) { return static_cast<int>(std::ceil(3.0 * sigma_s)); }
+
+// proj/src/core/spatial.cpp:43-50 (same summation order)
+double kernel_mass_1d(double sigma_s, int radius) {
+  double mass = 0.0;
+  for (int k = -radius; k <= radius; ++k)
+    mass += std::exp(-(static_cast<double>(k) * k) / (2.0 * sigma_s * sigma_s));
+  return mass;
+}
+
+namespace {
+
+struct Deriche {
+  double nc[4], na[4], d[4];
+};
+
+// The reference's 4th-order Deriche fit, proj/src/core/spatial.cpp:140-181:
+// causal numerator nc, anticausal numerator na, shared denominator d, both
+// numerators normalised to exact unit DC gain.
+Deriche deriche(double s) {
+  const double a1 = 1.6800, c1 = 3.7350, l1 = 1.7830, w1 = 0.6318;
+  const double a2 = -0.6803, c2 = -0.2598, l2 = 1.7230, w2 = 1.9970;
+  const double e1 = std::exp(-l1 / s), e2 = std::exp(-l2 / s);
+  const double cw1 = std::cos(w1 / s), sw1 = std::sin(w1 / s);
+  const double cw2 = std::cos(w2 / s), sw2 = std::sin(w2 / s);
+  Deriche k{};
+  k.nc[0] = a1 + a2;
+  k.nc[1] = e2 * (c2 * sw2 - (a2 + 2.0 * a1) * cw2) + e1 * (c1 * sw1 - (2.0 * a2 + a1) * cw1);
+  k.nc[2] = 2.0 * e1 * e2 * ((a1 + a2) * cw2 * cw1 - c1 * cw2 * sw1 - c2 * cw1 * sw2) +
+            a2 * e1 * e1 + a1 * e2 * e2;
+  k.nc[3] = e2 * e1 * e1 * (c2 * sw2 - a2 * cw2) + e1 * e2 * e2 * (c1 * sw1 - a1 * cw1);
+  k.d[0] = -2.0 * e2 * cw2 - 2.0 * e1 * cw1;
+  k.d[1] = 4.0 * cw2 * cw1 * e1 * e2 + e1 * e1 + e2 * e2;
+  k.d[2] = -2.0 * cw1 * e1 * e2 * e2 - 2.0 * cw2 * e2 * e1 * e1;
+  k.d[3] = e1 * e1 * e2 * e2;
+  for (int i = 0; i < 3; ++i) k.na[i] = k.nc[i + 1] - k.d[i] * k.nc[0];
+  k.na[3] = -k.d[3] * k.nc[0];
+  double num = 0.0, den = 1.0;
+  for (int i = 0; i < 4; ++i) {
+    num += k.nc[i] + k.na[i];
+    den += k.d[i];
+  }
+  const double dc = num / den;
+  for (int i = 0; i < 4; ++i) {
+    k.nc[i] /= dc;
+    k.na[i] /= dc;
+  }
+  return k;
+}
+
+cd poly3(const double c[4], cd q) { return c[0] + q * (c[1] + q * (c[2] + q * c[3])); }
+
+}  // namespace
+
+void deriche_coeffs_f64(double sigma, double nc[4], double na[4], double d[4]) {
+  const Deriche k = deriche(sigma);
+  for (int i = 0; i < 4; ++i) {
+    nc[i] = k.nc[i];
+    na[i] = k.na[i];
+    d[i] = k.d[i];
+  }
+}
+
+FilterConsts make_filter_consts(double s) {
+  const Deriche k = deriche(s);
+  // Denominator 1 + d0 q + d1 q^2 + d2 q^3 + d3 q^4 = prod_j (1 - p_j q) with
+  // p = e^{-l/s} e^{+-i w/s} (the damped cosines of spatial.cpp:186-216).
+  const cd p[4] = {std::polar(std::exp(-1.7830 / s), 0.6318 / s),
+                   std::polar(std::exp(-1.7230 / s), 1.9970 / s),
+                   std::polar(std::exp(-1.7830 / s), -0.6318 / s),
+                   std::polar(std::exp(-1.7230 / s), -1.9970 / s)};
+  FilterConsts fc{};
+  for (int sec = 0; sec < 2; ++sec) {
+    const cd pk = p[sec];
+    const cd q = 1.0 / pk;
+    cd den = 1.0;
+    for (int j = 0; j < 4; ++j)
+      if (j != sec) den *= (1.0 - p[j] * q);
+    // causal: sum_m nc_m z^-m / D(z^-1); residue at z^-1 = q
+    const cd A = 2.0 * poly3(k.nc, q) / den;
+    // anticausal: z * sum_m na_m z^m / D(z), expanded as sum_k B_k z/(1 - p_k z)
+    const cd B = 2.0 * poly3(k.na, q) / den;
+    const cd g = 1.0 / (1.0 - pk);
+    fc.pr[sec] = static_cast<float>(pk.real());
+    fc.pi[sec] = static_cast<float>(pk.imag());
+    fc.ar[sec] = static_cast<float>(A.real());
+    fc.ai[sec] = static_cast<float>(A.imag());
+    fc.br[sec] = static_cast<float>(B.real());
+    fc.bi[sec] = static_cast<float>(B.imag());
+    fc.gr[sec] = static_cast<float>(g.real());
+    fc.gi[sec] = static_cast<float>(g.imag());
+  }
+  return fc;
+}
+
+RangeConsts make_range_consts(const Params& p) {
+  RangeConsts rc{};
+  rc.sigma_r = p.sigma_r;
+  rc.inv_sr = 1.0 / p.sigma_r;
+  rc.inv2s2 = 1.0 / (2.0 * p.sigma_r * p.sigma_r);
+  rc.degree = p.degree;
+  rc.planes = p.degree + 2;
+  rc.pairs = (rc.planes + 1) / 2;
+  rc.centering = p.centering;
+  // Plane scaling s_n = s0 - k n. |F_n| = |H^n exp(-H^2/2)| <= (n/e)^(n/2);
+  // pick the smallest k that keeps the last (padded) plane at or below 2^s0.
+  const int n_max = 2 * rc.pairs - 1;
+  const double lb = n_max > 0 ? 0.5 * n_max * std::log2(n_max / std::exp(1.0)) : 0.0;
+  int k = static_cast<int>(std::ceil(lb / std::max(1, n_max)));
+  if (k < 1) k = 1;
+  const int s0 = 100;
+  rc.e_scale = std::ldexp(1.0, s0);
+  rc.h_step = static_cast<float>(std::ldexp(1.0, -k));
+  rc.c0 = static_cast<float>(std::ldexp(1.0, -s0));
+  rc.p_scale = static_cast<float>(std::ldexp(1.0, k));
+  for (int n = 0; n < kMaxPlanes; ++n)
+    rc.w_step[n] = static_cast<float>(std::ldexp(1.0, k) / (n + 1));
+  const double mass = kernel_mass_1d(p.sigma_s, default_window_radius(p.sigma_s));
+  rc.q_thresh = static_cast<float>(1e-8 / (mass * mass * p.kernel_scale));
+  return rc;
+}
+
+}  // namespace gpfb

@@ -1,0 +1,100 @@
+// Internal interfaces of libgpfilter_b200: filter constants, plan and launchers.
+#pragma once
+
+#include <cstddef>
+#include <cstdint>
+#include <string>
+
+#include <cuda_runtime.h>
+
+namespace gpfb {
+
+constexpr int kMaxPlanes = 64;  // N+2 <= 64  (degree <= 62)
+
+// Per-call constants of the filter, computed on the host in fp64 from the
+// reference's own Deriche coefficients (proj/src/core/spatial.cpp:140-181) and
+// passed by value to every kernel.
+//
+// The 4th-order causal/anticausal recurrences of deriche_line
+// (proj/src/core/spatial.cpp:186-216) are realised as two complex first-order
+// sections each (partial-fraction expansion over the conjugate pole pairs):
+//   causal      w_k[i]   = x[i]   + p_k w_k[i-1],   y+[i] = sum_k Re(A_k w_k[i])
+//   anticausal  v_k[i]   = x[i+1] + p_k v_k[i+1],   y-[i] = sum_k Re(B_k v_k[i])
+// (A_k, B_k already carry the factor 2 of the conjugate pair.) Same transfer
+// function, far better conditioned in fp32 than the direct form. The replicate
+// steady-state warm start of the reference is w_k[-1] = x[0]/(1-p_k) and
+// v_k[n-1] = x[n-1]/(1-p_k).
+struct FilterConsts {
+  float pr[2], pi[2];  // poles (upper half plane)
+  float ar[2], ai[2];  // causal residues (x2)
+  float br[2], bi[2];  // anticausal residues (x2)
+  float gr[2], gi[2];  // 1/(1-p): warm-start gain
+};
+
+// Range / plane constants. Plane n holds F_n * 2^{s_n}, s_n = s0 - k*n, so
+// that every significant plane value stays in the fp32 normal range (the
+// exp(-h^2/2 sr^2) factor alone underflows fp32 for |h| > 13.2 sr).
+struct RangeConsts {
+  double inv_sr;      // 1/sigma_r
+  double inv2s2;      // 1/(2 sigma_r^2)  (same expression as bilateral.cpp:92)
+  double sigma_r;
+  double e_scale;     // 2^s0
+  float h_step;       // 2^-k      (chain multiplier factor)
+  float c0;           // 2^-s0     (weight of plane 0)
+  float p_scale;      // 2^k       (P uses planes n+1)
+  float w_step[kMaxPlanes];  // 2^k/(n+1): c_{n+1} = c_n * H * w_step[n]
+  float q_thresh;     // kQMin / (mass^2 * kernel_scale)  (bilateral.hpp:85)
+  int planes;         // N + 2
+  int pairs;          // ceil(planes / 2)
+  int degree;         // N
+  int centering;      // 0 / 1 (mean)
+};
+
+struct Params {
+  int width = 0, height = 0;
+  double sigma_s = 2.0, kernel_scale = 1.0, sigma_r = 30.0;
+  int degree = 20, centering = 1;
+};
+
+// Host-side constant builders (coeffs.cpp).
+FilterConsts make_filter_consts(double sigma_s);
+RangeConsts make_range_consts(const Params& p);
+double kernel_mass_1d(double sigma_s, int radius);
+int default_window_radius(double sigma_s);
+
+// Device workspace + launch plan for one (w, h, params) on one device.
+struct Plan {
+  Params p;
+  FilterConsts fc;
+  RangeConsts rc;
+  int device = 0;
+  // workspace
+  float* planes_v = nullptr;   // [pairs][h][w] float2  (after the column pass)
+  float* planes_b = nullptr;   // [pairs][h][w] float2  (after the row pass)
+  double* d_scalars = nullptr; // [2] t_c + spare
+  double* d_partials = nullptr;// mean partials (2 doubles per block)
+  size_t bytes = 0;
+  int mean_blocks = 0;
+  int launches_per_frame = 0;
+};
+
+// Status-carrying error used inside the library.
+struct Error {
+  int status;  // gpf_status value
+  std::string msg;
+};
+
+void plan_init(Plan& plan, const Params& p, int device);  // throws Error
+void plan_free(Plan& plan);
+// Enqueue one frame: in (fp32 or fp64) -> out (fp32 or fp64). fallbacks: device counter (+=).
+void run_frame_f32(Plan& plan, const float* d_in, float* d_out, unsigned long long* d_fb,
+                   cudaStream_t st);
+void run_frame_f64(Plan& plan, const double* d_in, double* d_out, unsigned long long* d_fb,
+                   cudaStream_t st);
+// Single-plane recursive Gaussian (gpf_gaussian_recursive), fp64 in/out.
+void run_gaussian_f64(const double* d_in, double* d_out, double* d_tmp, int w, int h,
+                      double sigma_s, double scale, cudaStream_t st);
+// The reference's normalised Deriche coefficients (spatial.cpp:140-181), fp64.
+void deriche_coeffs_f64(double sigma, double nc[4], double na[4], double d[4]);
+
+}  // namespace gpfb

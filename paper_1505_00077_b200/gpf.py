@@ -1,0 +1,172 @@
+"""Host-side mirror of the reference's GPF interface over the B200 C ABI.
+
+``gpf_filter_gpf`` follows ``gpf_filter_gpf`` of the reference C ABI
+(proj/include/gpfilter/gpfilter.h:100-107, proj/src/capi.cpp:176-192): same
+parameter structs and defaults, same status codes; a non-OK status raises
+``GpfError`` carrying the status and the library's ``gpf_last_error`` text.
+
+``Plan`` is the batched device-resident entry (gpfilter_b200.h): fp32 frames
+already in HBM, addressed by raw device pointers or torch CUDA tensors.
+"""
+from __future__ import annotations
+
+import ctypes as C
+
+import numpy as np
+
+from . import _lib
+from ._lib import (GPF_BACKEND_DIRECT, GPF_BACKEND_RECURSIVE, GPF_BOUNDARY_REFLECT,  # noqa: F401
+                   GPF_BOUNDARY_REPLICATE, GPF_BOUNDARY_ZERO, RangeParams, SpatialParams)
+
+
+class GpfError(RuntimeError):
+    def __init__(self, status: int, detail: str):
+        self.status = status
+        self.detail = detail
+        name = _lib.lib().gpf_status_name(status).decode()
+        super().__init__(f"{name}: {detail}")
+
+
+def _check(status: int) -> None:
+    if status != _lib.GPF_OK:
+        raise GpfError(status, _lib.lib().gpf_last_error().decode())
+
+
+def spatial_params(sigma_s: float = 2.0, window_radius: int = 0,
+                   boundary: int = GPF_BOUNDARY_REPLICATE,
+                   kernel_scale: float = 1.0) -> SpatialParams:
+    sp = SpatialParams()
+    _lib.lib().gpf_spatial_params_init(C.byref(sp))
+    sp.sigma_s, sp.window_radius, sp.boundary, sp.kernel_scale = (
+        sigma_s, window_radius, boundary, kernel_scale)
+    return sp
+
+
+def range_params(sigma_r: float = 30.0, degree: int = 20) -> RangeParams:
+    rp = RangeParams()
+    _lib.lib().gpf_range_params_init(C.byref(rp))
+    rp.sigma_r, rp.degree = sigma_r, degree
+    return rp
+
+
+class Image:
+    """Owning handle of a gpf_image (row-major doubles)."""
+
+    def __init__(self, handle: C.c_void_p):
+        self.h = handle
+
+    @classmethod
+    def from_array(cls, a: np.ndarray) -> "Image":
+        a = np.asarray(a, dtype=np.float64)
+        if a.ndim != 2:
+            raise ValueError("image must be 2-D (height, width)")
+        hdl = C.c_void_p()
+        _check(_lib.lib().gpf_image_create(a.shape[1], a.shape[0], C.byref(hdl)))
+        img = cls(hdl)
+        img.view()[...] = a
+        return img
+
+    @property
+    def shape(self):
+        L = _lib.lib()
+        return (L.gpf_image_height(self.h), L.gpf_image_width(self.h))
+
+    def view(self) -> np.ndarray:
+        h, w = self.shape
+        ptr = _lib.lib().gpf_image_data(self.h)
+        return np.ctypeslib.as_array(ptr, shape=(h * w,)).reshape(h, w)
+
+    def numpy(self) -> np.ndarray:
+        return self.view().copy()
+
+    def __del__(self):
+        if getattr(self, "h", None):
+            _lib.lib().gpf_image_destroy(self.h)
+            self.h = None
+
+
+def gpf_filter_gpf(img: np.ndarray, sp: SpatialParams | None = None, rp: RangeParams | None = None,
+                   backend: int = GPF_BACKEND_RECURSIVE, centering: int = 1):
+    """Constant-time Gauss-polynomial bilateral filter on the GPU.
+
+    Returns ``(out, fallback_count)``; raises GpfError on a non-OK status.
+    """
+    sp = sp or spatial_params()
+    rp = rp or range_params()
+    src = Image.from_array(img)
+    out = C.c_void_p()
+    fb = C.c_longlong(-1)
+    _check(_lib.lib().gpf_filter_gpf(src.h, C.byref(sp), C.byref(rp), backend, centering,
+                                     C.byref(fb), C.byref(out)))
+    res = Image(out)
+    return res.numpy(), fb.value
+
+
+def gpf_gaussian_recursive(img: np.ndarray, sigma_s: float, kernel_scale: float = 1.0) -> np.ndarray:
+    """Single-plane recursive Gaussian (reference gpf_gaussian_recursive)."""
+    src = Image.from_array(img)
+    out = C.c_void_p()
+    _check(_lib.lib().gpf_gaussian_recursive(src.h, sigma_s, kernel_scale, C.byref(out)))
+    return Image(out).numpy()
+
+
+def set_num_threads(n: int) -> None:
+    _check(_lib.lib().gpf_set_num_threads(n))
+
+
+def get_num_threads() -> int:
+    return _lib.lib().gpf_get_num_threads()
+
+
+def _ptr(x) -> int:
+    if isinstance(x, int):
+        return x
+    if hasattr(x, "data_ptr"):
+        return x.data_ptr()
+    raise TypeError("expected a device pointer (int) or a torch CUDA tensor")
+
+
+class Plan:
+    """Device workspace for filtering fp32 frames of one size/parameter set."""
+
+    def __init__(self, width: int, height: int, sigma_s: float, sigma_r: float, degree: int = 20,
+                 kernel_scale: float = 1.0, centering: int = 1, device: int = -1):
+        self.width, self.height = width, height
+        sp = spatial_params(sigma_s, kernel_scale=kernel_scale)
+        rp = range_params(sigma_r, degree)
+        self.h = C.c_void_p()
+        _check(_lib.lib().gpf_b200_plan_create(width, height, C.byref(sp), C.byref(rp),
+                                               centering, device, C.byref(self.h)))
+
+    @property
+    def workspace_bytes(self) -> int:
+        return _lib.lib().gpf_b200_plan_workspace_bytes(self.h)
+
+    @property
+    def launches_per_frame(self) -> int:
+        return _lib.lib().gpf_b200_plan_launches_per_frame(self.h)
+
+    def filter_device(self, d_in, d_out, count: int = 1, d_fallbacks=None, stream: int = 0) -> None:
+        """Enqueue `count` frames (device fp32 in -> device fp32 out) on `stream`."""
+        fb = _ptr(d_fallbacks) if d_fallbacks is not None else None
+        _check(_lib.lib().gpf_b200_filter_f32(self.h, _ptr(d_in), _ptr(d_out), count, fb, stream))
+
+    def filter_host(self, h_in: np.ndarray, h_out: np.ndarray | None = None, stream: int = 0):
+        """Host fp32 frames -> host fp32 frames (copies inside). Returns (out, fallbacks)."""
+        a = np.ascontiguousarray(h_in, dtype=np.float32)
+        count = a.size // (self.width * self.height)
+        if count * self.width * self.height != a.size:
+            raise ValueError("input size is not a whole number of frames")
+        out = h_out if h_out is not None else np.empty_like(a)
+        fb = (C.c_longlong * max(count, 1))()
+        _check(_lib.lib().gpf_b200_filter_f32_host(self.h, a.ctypes.data, out.ctypes.data, count,
+                                                   fb, stream))
+        return out, list(fb)[:count]
+
+    def close(self) -> None:
+        if getattr(self, "h", None):
+            _lib.lib().gpf_b200_plan_destroy(self.h)
+            self.h = None
+
+    def __del__(self):
+        self.close()

@@ -1,0 +1,151 @@
+"""CPU: the C-ABI library loads, exports every declared symbol, and validates
+arguments exactly like the reference C ABI (no device needed: validation runs
+before any device work). Mirrors proj/tests/test_capi.cpp for the GPF path.
+"""
+import ctypes as C
+import os
+import re
+
+import numpy as np
+import pytest
+
+from paper_1505_00077_b200 import _lib, gpf
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def declared_functions():
+    names = set()
+    for hdr in ("gpfilter.h", "gpfilter_b200.h"):
+        text = open(os.path.join(ROOT, "include", "gpfilter", hdr)).read()
+        text = re.sub(r"/\*.*?\*/", "", text, flags=re.S)
+        names |= set(re.findall(r"\b(gpf_\w+)\s*\(", text))
+    return names
+
+
+def test_library_exports_every_declared_symbol():
+    L = _lib.lib()
+    decl = declared_functions()
+    assert decl == set(_lib.EXPORTED)
+    for name in decl:
+        assert hasattr(L, name), name
+
+
+def test_version_and_status_names():
+    L = _lib.lib()
+    assert L.gpf_version().decode().startswith("1.0.0")
+    assert L.gpf_status_name(0) == b"GPF_OK"
+    assert L.gpf_status_name(3) == b"GPF_ERR_SIGMA_TOO_SMALL"
+    assert L.gpf_status_name(9) == b"GPF_ERR_UNKNOWN"
+
+
+def test_parameter_defaults():
+    sp, rp = _lib.SpatialParams(), _lib.RangeParams()
+    _lib.lib().gpf_spatial_params_init(C.byref(sp))
+    _lib.lib().gpf_range_params_init(C.byref(rp))
+    assert (sp.sigma_s, sp.window_radius, sp.boundary, sp.kernel_scale) == (2.0, 0, 0, 1.0)
+    assert (rp.sigma_r, rp.degree) == (30.0, 20)
+    _lib.lib().gpf_spatial_params_init(None)  # NULL is a no-op
+    _lib.lib().gpf_range_params_init(None)
+
+
+def test_image_lifecycle_and_null_safety():
+    L = _lib.lib()
+    h = C.c_void_p(1)
+    assert L.gpf_image_create(0, 5, C.byref(h)) == _lib.GPF_ERR_INVALID_ARGUMENT
+    assert h.value is None
+    assert len(L.gpf_last_error()) > 0
+    assert L.gpf_image_create(4, 4, None) == _lib.GPF_ERR_INVALID_ARGUMENT
+    assert L.gpf_image_create(3, 2, C.byref(h)) == 0
+    assert (L.gpf_image_width(h), L.gpf_image_height(h)) == (3, 2)
+    data = np.ctypeslib.as_array(L.gpf_image_data(h), shape=(6,))
+    assert (data == 0).all()
+    L.gpf_image_destroy(h)
+    L.gpf_image_destroy(None)
+    assert L.gpf_image_width(None) == 0 and L.gpf_image_height(None) == 0
+    assert not L.gpf_image_data(None) and not L.gpf_image_cdata(None)
+
+
+def _call(img, sp, rp, backend=1, centering=1, out_ptr=True):
+    L = _lib.lib()
+    src = gpf.Image.from_array(img)
+    out = C.c_void_p(1)
+    fb = C.c_longlong(-7)
+    st = L.gpf_filter_gpf(src.h, C.byref(sp) if sp is not None else None,
+                          C.byref(rp) if rp is not None else None, backend, centering,
+                          C.byref(fb), C.byref(out) if out_ptr else None)
+    return st, out, fb, L.gpf_last_error().decode()
+
+
+@pytest.mark.parametrize("case,status,needle", [
+    (dict(sigma_s=-1.0), 1, "sigma_s"),
+    (dict(sigma_s=0.0), 1, "sigma_s"),
+    (dict(kernel_scale=0.0), 1, "kernel_scale"),
+    (dict(sigma_r=0.0), 1, "sigma_r"),
+    (dict(degree=-1), 1, "degree"),
+    (dict(degree=63), 1, "degree"),
+    (dict(boundary=9), 1, "boundary"),
+    (dict(backend=7), 1, "backend"),
+    (dict(backend=0), 1, "direct"),
+    (dict(sigma_s=0.49), 3, "direct"),
+    (dict(sigma_s=0.3), 3, "direct"),
+])
+def test_validation_statuses(case, status, needle):
+    sp = gpf.spatial_params(case.get("sigma_s", 2.0), boundary=case.get("boundary", 0),
+                            kernel_scale=case.get("kernel_scale", 1.0))
+    rp = gpf.range_params(case.get("sigma_r", 30.0), case.get("degree", 20))
+    st, out, fb, msg = _call(np.zeros((8, 8)), sp, rp, backend=case.get("backend", 1))
+    assert st == status
+    assert needle in msg
+    assert out.value is None          # *out set to NULL before work
+    assert fb.value == -7             # fallback_count untouched on error
+
+
+def test_null_arguments():
+    sp, rp = gpf.spatial_params(), gpf.range_params()
+    for args in [(sp, None), (None, rp)]:
+        st, _, _, msg = _call(np.zeros((4, 4)), *args)
+        assert st == 1 and msg == "null argument"
+    st, _, _, _ = _call(np.zeros((4, 4)), sp, rp, out_ptr=False)
+    assert st == 1
+    L = _lib.lib()
+    out = C.c_void_p()
+    assert L.gpf_filter_gpf(None, C.byref(sp), C.byref(rp), 1, 1, None, C.byref(out)) == 1
+
+
+def test_gaussian_recursive_validation():
+    L = _lib.lib()
+    src = gpf.Image.from_array(np.ones((8, 8)))
+    out = C.c_void_p()
+    assert L.gpf_gaussian_recursive(src.h, 0.3, 1.0, C.byref(out)) == 3
+    assert "direct" in L.gpf_last_error().decode()
+    assert L.gpf_gaussian_recursive(src.h, -1.0, 1.0, C.byref(out)) == 1
+    assert L.gpf_gaussian_recursive(None, 2.0, 1.0, C.byref(out)) == 1
+
+
+def test_thread_count_plumbing():
+    L = _lib.lib()
+    assert L.gpf_get_num_threads() == 1
+    assert L.gpf_set_num_threads(0) == 1
+    assert L.gpf_get_num_threads() == 1
+    assert L.gpf_set_num_threads(4) == 0
+    assert L.gpf_get_num_threads() == 4
+    assert L.gpf_set_num_threads(1) == 0
+
+
+def test_plan_validation():
+    with pytest.raises(gpf.GpfError) as e:
+        gpf.Plan(64, 64, 0.4, 30.0)
+    assert e.value.status == 3
+    with pytest.raises(gpf.GpfError) as e:
+        gpf.Plan(0, 64, 2.0, 30.0)
+    assert e.value.status == 1
+
+
+def test_no_cpu_fallback_without_device():
+    import torch
+    if torch.cuda.is_available():
+        pytest.skip("device present")
+    with pytest.raises(gpf.GpfError) as e:
+        gpf.gpf_filter_gpf(np.full((8, 8), 3.0))
+    assert e.value.status == 9 and "no CUDA device" in e.value.detail
