@@ -28,6 +28,11 @@ gpf_status gpf_b200_plan_create(int width, int height, const gpf_spatial_params*
                                 gpf_b200_plan** out);
 void gpf_b200_plan_destroy(gpf_b200_plan* plan);
 
+/* Re-sizes the workspace to hold `frames` frames, so that gpf_b200_filter_f32
+ * filters up to that many frames per kernel launch (default 1). Frame-level
+ * batching is what fills the 148 SMs for small frames (e.g. 3840x2160). */
+gpf_status gpf_b200_plan_set_batch(gpf_b200_plan* plan, int frames);
+
 /* Bytes of device workspace held by the plan. */
 size_t gpf_b200_plan_workspace_bytes(const gpf_b200_plan* plan);
 

@@ -30,7 +30,8 @@ EXPORTED = (
     "gpf_spatial_params_init", "gpf_range_params_init",
     "gpf_filter_gpf", "gpf_gaussian_recursive",
     "gpf_set_num_threads", "gpf_get_num_threads",
-    "gpf_b200_plan_create", "gpf_b200_plan_destroy", "gpf_b200_plan_workspace_bytes",
+    "gpf_b200_plan_create", "gpf_b200_plan_destroy", "gpf_b200_plan_set_batch",
+    "gpf_b200_plan_workspace_bytes",
     "gpf_b200_plan_launches_per_frame", "gpf_b200_filter_f32", "gpf_b200_filter_f32_host",
 )
 
@@ -75,6 +76,7 @@ def _declare(lib: C.CDLL) -> C.CDLL:
     lib.gpf_b200_plan_create.argtypes = [C.c_int, C.c_int, C.POINTER(SpatialParams),
                                          C.POINTER(RangeParams), C.c_int, C.c_int, pvp]
     lib.gpf_b200_plan_destroy.argtypes = [vp]
+    lib.gpf_b200_plan_set_batch.argtypes = [vp, C.c_int]
     lib.gpf_b200_plan_workspace_bytes.restype = C.c_size_t
     lib.gpf_b200_plan_workspace_bytes.argtypes = [vp]
     lib.gpf_b200_plan_launches_per_frame.argtypes = [vp]

@@ -208,8 +208,8 @@ gpf_status gpf_filter_gpf(const gpf_image* in, const gpf_spatial_params* sp,
     cuda_check(cudaMemcpyAsync(din.p, in->data.data(), n * sizeof(double), cudaMemcpyHostToDevice, st),
                "cudaMemcpyAsync(H2D)");
     cuda_check(cudaMemsetAsync(dfb.p, 0, sizeof(unsigned long long), st), "cudaMemsetAsync");
-    gpfb::run_frame_f64(g.plan, static_cast<const double*>(din.p), static_cast<double*>(dout.p),
-                        static_cast<unsigned long long*>(dfb.p), st);
+    gpfb::run_frames_f64(g.plan, static_cast<const double*>(din.p), static_cast<double*>(dout.p), 1,
+                         static_cast<unsigned long long*>(dfb.p), st);
     auto* res = new gpf_image{p.width, p.height, std::vector<double>(n)};
     std::unique_ptr<gpf_image> hold(res);
     unsigned long long fb = 0;
@@ -290,6 +290,19 @@ void gpf_b200_plan_destroy(gpf_b200_plan* plan) {
   delete plan;
 }
 
+gpf_status gpf_b200_plan_set_batch(gpf_b200_plan* plan, int frames) {
+  if (plan == nullptr) return fail(GPF_ERR_INVALID_ARGUMENT, "null argument");
+  if (frames < 1) return fail(GPF_ERR_INVALID_ARGUMENT, "frames must be >= 1");
+  return guarded([&] {
+    cuda_check(cudaSetDevice(plan->plan.device), "cudaSetDevice");
+    cuda_check(cudaDeviceSynchronize(), "cudaDeviceSynchronize");
+    const gpfb::Params p = plan->plan.p;
+    const int dev = plan->plan.device;
+    gpfb::plan_free(plan->plan);
+    gpfb::plan_init(plan->plan, p, dev, frames);
+  });
+}
+
 size_t gpf_b200_plan_workspace_bytes(const gpf_b200_plan* plan) { return plan ? plan->plan.bytes : 0; }
 
 int gpf_b200_plan_launches_per_frame(const gpf_b200_plan* plan) {
@@ -306,13 +319,17 @@ gpf_status gpf_b200_filter_f32(gpf_b200_plan* plan, const float* d_in, float* d_
     auto st = static_cast<cudaStream_t>(stream);
     const size_t npx = (size_t)plan->plan.p.width * plan->plan.p.height;
     auto* fb = reinterpret_cast<unsigned long long*>(d_fallbacks);
+    const int B = plan->plan.batch;
     if (fb) cuda_check(cudaMemsetAsync(fb, 0, sizeof(long long) * count, st), "cudaMemsetAsync");
-    else if (plan->d_fb_cap < 1) {
-      cuda_check(cudaMalloc(&plan->d_fb, sizeof(unsigned long long)), "cudaMalloc");
-      plan->d_fb_cap = 1;
+    else if (plan->d_fb_cap < B) {
+      cudaFree(plan->d_fb);
+      cuda_check(cudaMalloc(&plan->d_fb, sizeof(unsigned long long) * B), "cudaMalloc");
+      plan->d_fb_cap = B;
     }
-    for (int f = 0; f < count; ++f)
-      gpfb::run_frame_f32(plan->plan, d_in + f * npx, d_out + f * npx, fb ? fb + f : plan->d_fb, st);
+    for (int f = 0; f < count; f += B) {
+      const int n = std::min(B, count - f);
+      gpfb::run_frames_f32(plan->plan, d_in + f * npx, d_out + f * npx, n, fb ? fb + f : plan->d_fb, st);
+    }
   });
 }
 
@@ -338,7 +355,7 @@ gpf_status gpf_b200_filter_f32_host(gpf_b200_plan* plan, const float* h_in, floa
     for (int f = 0; f < count; ++f) {
       cuda_check(cudaMemcpyAsync(plan->d_stage_in, h_in + f * npx, npx * sizeof(float),
                                  cudaMemcpyHostToDevice, st), "H2D");
-      gpfb::run_frame_f32(plan->plan, plan->d_stage_in, plan->d_stage_out, plan->d_fb + f, st);
+      gpfb::run_frames_f32(plan->plan, plan->d_stage_in, plan->d_stage_out, 1, plan->d_fb + f, st);
       cuda_check(cudaMemcpyAsync(h_out + f * npx, plan->d_stage_out, npx * sizeof(float),
                                  cudaMemcpyDeviceToHost, st), "D2H");
     }

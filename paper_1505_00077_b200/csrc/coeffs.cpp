@@ -1,4 +1,5 @@
 // Host-side filter constants (fp64), see gpf_internal.h.
+#include <algorithm>
 #include <cmath>
 #include <complex>
 
@@ -102,6 +103,29 @@ FilterConsts make_filter_consts(double s) {
     fc.gi[sec] = static_cast<float>(g.imag());
   }
   return fc;
+}
+
+TileConsts make_tile_consts(double s, int width, int height) {
+  const cd p[2] = {std::polar(std::exp(-1.7830 / s), 0.6318 / s),
+                   std::polar(std::exp(-1.7230 / s), 1.9970 / s)};
+  TileConsts tc{};
+  const int last_y = height - (height - 1) / kTile * kTile;  // rows in the last row chunk
+  const int last_x = width - (width - 1) / kTile * kTile;    // columns in the last strip
+  for (int k = 0; k < 2; ++k) {
+    for (int j = 0; j < kTile; ++j) {
+      const cd w = std::pow(p[k], j);
+      tc.wr[k][j] = static_cast<float>(w.real());
+      tc.wi[k][j] = static_cast<float>(w.imag());
+    }
+    const cd pt = std::pow(p[k], kTile), py = std::pow(p[k], last_y), px = std::pow(p[k], last_x);
+    tc.pTr[k] = static_cast<float>(pt.real());
+    tc.pTi[k] = static_cast<float>(pt.imag());
+    tc.pYr[k] = static_cast<float>(py.real());
+    tc.pYi[k] = static_cast<float>(py.imag());
+    tc.pXr[k] = static_cast<float>(px.real());
+    tc.pXi[k] = static_cast<float>(px.imag());
+  }
+  return tc;
 }
 
 RangeConsts make_range_consts(const Params& p) {

@@ -10,6 +10,7 @@
 namespace gpfb {
 
 constexpr int kMaxPlanes = 64;  // N+2 <= 64  (degree <= 62)
+constexpr int kTile = 32;       // rows per column-pass chunk == columns per row-pass chunk
 
 // Per-call constants of the filter, computed on the host in fp64 from the
 // reference's own Deriche coefficients (proj/src/core/spatial.cpp:140-181) and
@@ -29,6 +30,16 @@ struct FilterConsts {
   float ar[2], ai[2];  // causal residues (x2)
   float br[2], bi[2];  // anticausal residues (x2)
   float gr[2], gi[2];  // 1/(1-p): warm-start gain
+};
+
+// Tile constants for exact anticausal carries between chunks of kTile
+// samples: the carry entering a chunk from the far side is
+//   C = sum_{j < L} p^j x[j]  +  p^L C_next        (L = chunk length)
+struct TileConsts {
+  float wr[2][kTile], wi[2][kTile];  // p_k^j, j < kTile
+  float pTr[2], pTi[2];              // p_k^kTile
+  float pYr[2], pYi[2];              // p_k^(rows in the last row chunk)
+  float pXr[2], pXi[2];              // p_k^(columns in the last column strip)
 };
 
 // Range / plane constants. Plane n holds F_n * 2^{s_n}, s_n = s0 - k*n, so
@@ -58,24 +69,32 @@ struct Params {
 
 // Host-side constant builders (coeffs.cpp).
 FilterConsts make_filter_consts(double sigma_s);
+TileConsts make_tile_consts(double sigma_s, int width, int height);
 RangeConsts make_range_consts(const Params& p);
 double kernel_mass_1d(double sigma_s, int radius);
 int default_window_radius(double sigma_s);
+// The reference's normalised Deriche coefficients (spatial.cpp:140-181), fp64.
+void deriche_coeffs_f64(double sigma, double nc[4], double na[4], double d[4]);
 
 // Device workspace + launch plan for one (w, h, params) on one device.
 struct Plan {
   Params p;
   FilterConsts fc;
+  TileConsts tc;
   RangeConsts rc;
   int device = 0;
-  // workspace
-  float* planes_v = nullptr;   // [pairs][h][w] float2  (after the column pass)
-  float* planes_b = nullptr;   // [pairs][h][w] float2  (after the row pass)
-  double* d_scalars = nullptr; // [2] t_c + spare
-  double* d_partials = nullptr;// mean partials (2 doubles per block)
+  int batch = 0;       // frames per launch the workspace holds
+  int ny = 0, nx = 0;  // row chunks / column strips of kTile
+  // workspace (per frame slot)
+  float2* V = nullptr;      // [batch][pairs][w][h]   column-pass output, transposed
+  float4* CA = nullptr;     // [batch][ny][pairs][w][2] column anticausal carries
+  float4* AH = nullptr;     // [batch][nx][pairs][h][2] row aggregates per strip
+  float4* CH = nullptr;     // [batch][nx][pairs][h][2] row anticausal carries
+  double* scalars = nullptr;   // [batch][2]  t_c
+  double* partials = nullptr;  // [batch][mean_blocks][2]
   size_t bytes = 0;
   int mean_blocks = 0;
-  int launches_per_frame = 0;
+  int launches_per_frame = 0;  // kernels per launch group (independent of batch)
 };
 
 // Status-carrying error used inside the library.
@@ -84,17 +103,16 @@ struct Error {
   std::string msg;
 };
 
-void plan_init(Plan& plan, const Params& p, int device);  // throws Error
+void plan_init(Plan& plan, const Params& p, int device, int batch = 1);  // throws Error
 void plan_free(Plan& plan);
-// Enqueue one frame: in (fp32 or fp64) -> out (fp32 or fp64). fallbacks: device counter (+=).
-void run_frame_f32(Plan& plan, const float* d_in, float* d_out, unsigned long long* d_fb,
-                   cudaStream_t st);
-void run_frame_f64(Plan& plan, const double* d_in, double* d_out, unsigned long long* d_fb,
-                   cudaStream_t st);
+// Enqueue `count` contiguous frames (count <= plan.batch): in -> out; per-frame
+// fallback counters d_fb[count] are incremented (caller zeroes them).
+void run_frames_f32(Plan& plan, const float* d_in, float* d_out, int count,
+                    unsigned long long* d_fb, cudaStream_t st);
+void run_frames_f64(Plan& plan, const double* d_in, double* d_out, int count,
+                    unsigned long long* d_fb, cudaStream_t st);
 // Single-plane recursive Gaussian (gpf_gaussian_recursive), fp64 in/out.
 void run_gaussian_f64(const double* d_in, double* d_out, double* d_tmp, int w, int h,
                       double sigma_s, double scale, cudaStream_t st);
-// The reference's normalised Deriche coefficients (spatial.cpp:140-181), fp64.
-void deriche_coeffs_f64(double sigma, double nc[4], double na[4], double d[4]);
 
 }  // namespace gpfb

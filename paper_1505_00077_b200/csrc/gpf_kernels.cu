@@ -1,17 +1,34 @@
 // sm_100a kernels of the Gauss-polynomial bilateral filter (GPF) hot path.
 //
 // Reference path (proj/src/core/bilateral.cpp:150-158, gpf()):
-//   t_c = mean(f)                                   -> k_mean_*        (K0)
-//   N+2 planes F_n = H^n exp(-h^2/2sr^2), each
-//   filtered by the separable Deriche IIR           -> k_colpass       (K1, columns)
-//                                                      k_rowpass       (K2, rows)
-//   Q = sum c G Fbar_n, P = sum c G Fbar_{n+1},
-//   out = sr P/Q + t_c, |Q| <= 1e-8 -> input        -> k_combine       (K3)
+//   t_c = mean(f)                                  -> k_mean_partial/final (K0)
+//   N+2 planes F_n = H^n exp(-h^2/2sr^2), each filtered by the separable
+//   4th-order Deriche IIR (spatial.cpp:220-251):
+//     column carries from f                        -> k_col_carry   (K1)
+//     column pass (fused plane generator)          -> k_colpass     (K2)
+//     row carries (scan of K2's strip aggregates)  -> k_row_scan    (K3)
+//     row pass + P/Q recombination + normalise     -> k_rowpass     (K4)
+//   Q = sum c G Fbar_n, P = sum c G Fbar_{n+1}, out = sr P/Q + t_c,
+//   |Q| <= 1e-8 -> input (bilateral.cpp:117-148)
 //
-// Data layout in HBM: plane pair g (planes 2g, 2g+1) of the intermediate is a
-// row-major float2 image [pairs][h][w]; one thread owns one (line, pair).
+// Threads own (line, plane pair): a CTA is 32 lines x `pairs` warps. Both
+// passes sweep their lines in chunks of kTile samples: the causal recurrence
+// runs on across chunks; the anticausal one restarts every chunk from an exact
+// carry (the anticausal state at the chunk's far end), so a chunk's two
+// directions combine in registers and every intermediate plane crosses HBM
+// exactly once (written by K2, read by K4).
+//
+// HBM layouts (per frame):
+//   V  [pairs][w][h_pad] float2   column-pass output, TRANSPOSED so that the
+//                                 row pass reads 32 consecutive rows per load
+//   CA [ny][pairs][w]   2xfloat4  column anticausal carries (from f, K1)
+//   AH [nx][pairs][h]   2xfloat4  per-strip row aggregates sum_i p^i V (K2)
+//   CH [nx][pairs][h]   2xfloat4  row anticausal carries (K3)
+#include <algorithm>
+
 #include <cuda_runtime.h>
 
+#include "device_common.cuh"
 #include "gpf_internal.h"
 
 namespace gpfb {
@@ -62,6 +79,8 @@ template <typename T>
 __global__ void __launch_bounds__(kMeanThreads) k_mean_partial(const T* __restrict__ in,
                                                                long long n,
                                                                double* __restrict__ partials) {
+  in += (size_t)blockIdx.y * n;
+  partials += (size_t)blockIdx.y * gridDim.x * 2;
   double hi = 0.0, lo = 0.0;
   const long long stride = (long long)gridDim.x * kMeanThreads;
   for (long long i = (long long)blockIdx.x * kMeanThreads + threadIdx.x; i < n; i += stride) {
@@ -81,251 +100,360 @@ __global__ void __launch_bounds__(kMeanThreads) k_mean_final(const double* __res
                                                              int nblocks, long long n,
                                                              int centering,
                                                              double* __restrict__ scalars) {
+  partials += (size_t)blockIdx.x * nblocks * 2;
   double hi = 0.0, lo = 0.0;
   for (int b = threadIdx.x; b < nblocks; b += kMeanThreads)
     dd_add(hi, lo, partials[2 * b], partials[2 * b + 1]);
   block_dd_reduce(hi, lo);
-  if (threadIdx.x == 0) scalars[0] = centering ? (hi + lo) / static_cast<double>(n) : 0.0;
+  if (threadIdx.x == 0)
+    scalars[2 * blockIdx.x] = centering ? (hi + lo) / static_cast<double>(n) : 0.0;
 }
 
 // ----------------------------------------------------------------------------
-// Plane generation (bilateral.cpp:92-101 and the F <- H F recursion of
-// step(), bilateral.cpp:117-120): for pixel value f,
-//   h = f - t_c, H = h / sr, E = exp(-h^2 / 2 sr^2)      (fp64, like the ref)
-//   plane n (scaled) = E 2^s0 * (H 2^-k)^n              (fp32 chain)
+// cp.async helpers (LDGSTS): global -> shared without staging in registers.
 // ----------------------------------------------------------------------------
-struct PixelRange {
-  float es;  // E * 2^s0
-  float m;   // H * 2^-k
-};
-
-__device__ __forceinline__ PixelRange pixel_range(double f, double t_c, const RangeConsts& rc) {
-  const double h = f - t_c;
-  PixelRange r;
-  r.es = static_cast<float>(exp(-(h * h) * rc.inv2s2) * rc.e_scale);
-  r.m = static_cast<float>(h * rc.inv_sr) * rc.h_step;
-  return r;
+__device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
+  const unsigned s = static_cast<unsigned>(__cvta_generic_to_shared(smem));
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(s), "l"(gmem));
 }
-
-// planes (2g, 2g+1) of a pixel: es * m^(2g), es * m^(2g+1). g is warp-uniform.
-__device__ __forceinline__ float2 pair_values(const PixelRange& r, int g) {
-  float base = r.m * r.m, acc = r.es;
-  for (int e = g; e; e >>= 1) {
-    if (e & 1) acc *= base;
-    base *= base;
-  }
-  return make_float2(acc, acc * r.m);
+template <int BYTES>
+__device__ __forceinline__ void cp_async_zfill(void* smem, const void* gmem, bool valid) {
+  const unsigned s = static_cast<unsigned>(__cvta_generic_to_shared(smem));
+  asm volatile("cp.async.ca.shared.global [%0], [%1], %2, %3;\n" ::"r"(s), "l"(gmem), "n"(BYTES),
+               "r"(valid ? BYTES : 0));
 }
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::); }
+__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_group 0;\n" ::); }
 
-// ----------------------------------------------------------------------------
-// One complex first-order section pair for two planes (see FilterConsts).
-// ----------------------------------------------------------------------------
-struct PairState {
-  float wr[2][2], wi[2][2];  // [plane][section]
-};
-
-__device__ __forceinline__ void warm_start(PairState& s, float2 x, const FilterConsts& fc) {
-#pragma unroll
-  for (int k = 0; k < 2; ++k) {
-    s.wr[0][k] = x.x * fc.gr[k];
-    s.wi[0][k] = x.x * fc.gi[k];
-    s.wr[1][k] = x.y * fc.gr[k];
-    s.wi[1][k] = x.y * fc.gi[k];
-  }
-}
-
-// w <- p w + x
-__device__ __forceinline__ void advance(PairState& s, float2 x, const FilterConsts& fc) {
-#pragma unroll
-  for (int k = 0; k < 2; ++k) {
-#pragma unroll
-    for (int q = 0; q < 2; ++q) {
-      const float xv = q == 0 ? x.x : x.y;
-      const float nr = fmaf(fc.pr[k], s.wr[q][k], fmaf(-fc.pi[k], s.wi[q][k], xv));
-      const float ni = fmaf(fc.pr[k], s.wi[q][k], fc.pi[k] * s.wr[q][k]);
-      s.wr[q][k] = nr;
-      s.wi[q][k] = ni;
-    }
-  }
-}
-
-// sum_k Re(c_k w_k) with residues (cr, ci)
-__device__ __forceinline__ float2 emit(const PairState& s, const float* cr, const float* ci) {
-  float2 o;
-  o.x = fmaf(cr[0], s.wr[0][0], fmaf(-ci[0], s.wi[0][0], fmaf(cr[1], s.wr[0][1], -ci[1] * s.wi[0][1])));
-  o.y = fmaf(cr[0], s.wr[1][0], fmaf(-ci[0], s.wi[1][0], fmaf(cr[1], s.wr[1][1], -ci[1] * s.wi[1][1])));
-  return o;
-}
-
-// ----------------------------------------------------------------------------
-// K1: column pass (deriche_line over columns, spatial.cpp:240-243), fused with
-// the plane generator. Thread = (column x, plane pair g); block = 32 columns x
-// pairs. Causal sweep writes its output, anticausal sweep adds to it.
-// ----------------------------------------------------------------------------
+// f tile: the 32x32 image block at (x0, y0) into ftile[32 rows][33], zero
+// outside the image. Issued by the whole CTA; caller commits/waits.
 template <typename Tin>
-__global__ void k_colpass(const Tin* __restrict__ in, float2* __restrict__ planes,
-                          const double* __restrict__ scalars, int w, int h,
-                          FilterConsts fc, RangeConsts rc) {
-  const int x = blockIdx.x * 32 + threadIdx.x;
-  const int g = threadIdx.y;
-  if (x >= w) return;
-  const double t_c = scalars[0];
-  float2* out = planes + (size_t)g * h * w + x;
+__device__ __forceinline__ void issue_f_tile(Tin* ftile, const Tin* __restrict__ in, int w, int h,
+                                             int x0, int y0) {
+  const int nthr = blockDim.x * blockDim.y;
+  const int tid = threadIdx.y * 32 + threadIdx.x;
+  for (int p = tid; p < 1024; p += nthr) {
+    const int r = p >> 5, c = p & 31;
+    const bool ok = (y0 + r < h) && (x0 + c < w);
+    const Tin* src = ok ? in + (size_t)(y0 + r) * w + x0 + c : in;
+    cp_async_zfill<sizeof(Tin)>(ftile + r * 33 + c, src, ok);
+  }
+}
 
-  PairState s;
-  {
-    const float2 x0 = pair_values(pixel_range(static_cast<double>(in[x]), t_c, rc), g);
-    warm_start(s, x0, fc);
-  }
-  for (int y = 0; y < h; ++y) {
-    const float2 xv = pair_values(pixel_range(static_cast<double>(in[(size_t)y * w + x]), t_c, rc), g);
-    advance(s, xv, fc);
-    out[(size_t)y * w] = emit(s, fc.ar, fc.ai);
-  }
-  {
-    const float2 xl = pair_values(pixel_range(static_cast<double>(in[(size_t)(h - 1) * w + x]), t_c, rc), g);
-    warm_start(s, xl, fc);
-  }
-  for (int y = h - 1; y >= 0; --y) {
-    const float2 a = emit(s, fc.br, fc.bi);
-    float2 o = out[(size_t)y * w];
-    o.x += a.x;
-    o.y += a.y;
-    out[(size_t)y * w] = o;
-    if (y > 0) {
-      const float2 xv = pair_values(pixel_range(static_cast<double>(in[(size_t)y * w + x]), t_c, rc), g);
-      advance(s, xv, fc);
-    }
+// Producer: range terms (es, m) of a 32x32 pixel block from the smem f tile,
+// computed once per pixel and shared by the `pairs` warps.
+template <typename Tin>
+__device__ __forceinline__ void produce_terms(float2 (*prod)[32], const Tin* ftile, double t_c,
+                                              const RangeConsts& rc) {
+  const int nthr = blockDim.x * blockDim.y;
+  const int tid = threadIdx.y * 32 + threadIdx.x;
+  for (int p = tid; p < 1024; p += nthr) {
+    const int j = p >> 5, c = p & 31;
+    prod[j][c] = pixel_terms(static_cast<double>(ftile[j * 33 + c]), t_c, rc);
   }
 }
 
 // ----------------------------------------------------------------------------
-// K2: row pass (deriche_line over rows, spatial.cpp:235-239) on the
-// intermediate planes. Thread = (row y, pair g).
+// K1: exact anticausal carries of the column pass, computed from f.
+// Thread (column x, pair g) walks its column bottom-up over row chunks:
+//   carry(last)   = x[h-1] / (1-p)                       (replicate, spatial.cpp:204-206)
+//   carry(c - 1)  = sum_{j<L_c} p^j x[y0_c + j] + p^{L_c} carry(c)
+// where carry(c) is the anticausal state at the last row of chunk c.
 // ----------------------------------------------------------------------------
-__global__ void k_rowpass(const float2* __restrict__ src, float2* __restrict__ dst, int w, int h,
-                          FilterConsts fc) {
+template <int MAXT, typename Tin>
+__global__ void __launch_bounds__(MAXT, 1) k_col_carry(const Tin* __restrict__ in_all,
+                                                    const double* __restrict__ scalars,
+                                                    float4* __restrict__ CA_all, int w, int h,
+                                                    int ny, FilterConsts fc, TileConsts tc,
+                                                    RangeConsts rc) {
+  __shared__ float2 prod[kTile][32];
+  __shared__ Tin ftile[2][32 * 33];
+  const int f = blockIdx.y, lane = threadIdx.x, g = threadIdx.y, pairs = blockDim.y;
+  const int x0 = blockIdx.x * 32, x = x0 + lane;
+  const Tin* in = in_all + (size_t)f * w * h;
+  float4* CA = CA_all + (size_t)f * ny * pairs * w * 2;
+  const double t_c = scalars[2 * f];
+  PairState C;
+  ps_zero(C);
+  issue_f_tile(ftile[(ny - 1) & 1], in, w, h, x0, (ny - 1) * kTile);
+  cp_async_commit();
+  for (int cy = ny - 1; cy >= 0; --cy) {
+    const int y0 = cy * kTile, rows = min(kTile, h - y0);
+    cp_async_wait_all();
+    __syncthreads();
+    if (cy > 0) {
+      issue_f_tile(ftile[(cy - 1) & 1], in, w, h, x0, y0 - kTile);
+      cp_async_commit();
+    }
+    produce_terms(prod, ftile[cy & 1], t_c, rc);
+    __syncthreads();
+    if (x < w) {
+      if (cy == ny - 1) ps_set_gain(C, pair_planes(prod[rows - 1][lane], g), fc);
+      ps_store(CA + ((size_t)cy * pairs + g) * w * 2 + (size_t)x * 2, C);
+      if (cy > 0) {
+        PairState agg;
+        ps_zero(agg);
+#pragma unroll 8
+        for (int j = 0; j < rows; ++j)
+          ps_accum(agg, pair_planes(prod[j][lane], g), tc.wr[0][j], tc.wi[0][j], tc.wr[1][j],
+                   tc.wi[1][j]);
+        if (cy == ny - 1) ps_chain(C, agg, tc.pYr, tc.pYi);
+        else ps_chain(C, agg, tc.pTr, tc.pTi);
+      }
+    }
+    __syncthreads();
+  }
+}
+
+// ----------------------------------------------------------------------------
+// K2: column pass (deriche_line over columns, spatial.cpp:240-243), fused with
+// the plane generator. Per row chunk: anticausal sweep from the K1 carry into
+// a register buffer, causal sweep (state carried from the previous chunk)
+// adds it and stages the chunk in smem; the staged chunk is written to V
+// transposed and reduced into the row-pass strip aggregates AH.
+// ----------------------------------------------------------------------------
+template <int MAXT, typename Tin>
+__global__ void __launch_bounds__(MAXT, 1) k_colpass(const Tin* __restrict__ in_all,
+                                                  const double* __restrict__ scalars,
+                                                  const float4* __restrict__ CA_all,
+                                                  float2* __restrict__ V_all,
+                                                  float4* __restrict__ AH_all, int w, int h,
+                                                  int h_pad, int ny, int nx, FilterConsts fc,
+                                                  TileConsts tc, RangeConsts rc) {
+  extern __shared__ float4 smem4[];
+  float2(*prod)[32] = reinterpret_cast<float2(*)[32]>(smem4);
+  // stage[g][c][33]: column c's 32 rows of pair g (row dim padded to 33)
+  float2* stage = reinterpret_cast<float2*>(smem4) + kTile * 32;
+  Tin* ftiles = reinterpret_cast<Tin*>(stage + (size_t)blockDim.y * 32 * 33);  // [2][32*33]
+  const int f = blockIdx.y, lane = threadIdx.x, g = threadIdx.y, pairs = blockDim.y;
+  const int strip = blockIdx.x, x0 = strip * 32, x = x0 + lane;
+  const int cols = min(32, w - x0);
+  const Tin* in = in_all + (size_t)f * w * h;
+  const float4* CA = CA_all + (size_t)f * ny * pairs * w * 2;
+  float2* V = V_all + (size_t)f * pairs * w * h_pad;
+  float4* AH = AH_all + (size_t)f * nx * pairs * h * 2;
+  const double t_c = scalars[2 * f];
+  PairState cs;  // causal state, carried across chunks
+  ps_zero(cs);
+  issue_f_tile(ftiles, in, w, h, x0, 0);
+  cp_async_commit();
+  for (int cy = 0; cy < ny; ++cy) {
+    const int y0 = cy * kTile, rows = min(kTile, h - y0);
+    cp_async_wait_all();
+    __syncthreads();
+    if (cy + 1 < ny) {
+      issue_f_tile(ftiles + ((cy + 1) & 1) * 32 * 33, in, w, h, x0, y0 + kTile);
+      cp_async_commit();
+    }
+    produce_terms(prod, ftiles + (cy & 1) * 32 * 33, t_c, rc);
+    __syncthreads();
+    if (x < w) {
+      PairState as;
+      ps_load(as, CA + ((size_t)cy * pairs + g) * w * 2 + (size_t)x * 2);
+      float2 buf[kTile];
+#pragma unroll
+      for (int j = kTile - 1; j >= 0; --j) {
+        if (j < rows) {
+          buf[j] = ps_emit(as, fc.br, fc.bi);
+          ps_advance(as, pair_planes(prod[j][lane], g), fc);
+        }
+      }
+      float2* st = stage + ((size_t)g * 32 + lane) * 33;
+#pragma unroll
+      for (int j = 0; j < kTile; ++j) {
+        if (j < rows) {
+          const float2 xv = pair_planes(prod[j][lane], g);
+          if (cy == 0 && j == 0) ps_set_gain(cs, xv, fc);
+          ps_advance(cs, xv, fc);
+          const float2 o = ps_emit(cs, fc.ar, fc.ai);
+          st[j] = make_float2(o.x + buf[j].x, o.y + buf[j].y);
+        }
+      }
+    }
+    __syncthreads();
+    // write-out: warp handles (gg, c) rows of the stage; lanes = rows
+    const int warp = g, nwarps = pairs;
+    if (lane < rows)
+      for (int q = warp; q < pairs * 32; q += nwarps) {
+        const int gg = q >> 5, c = q & 31;
+        if (c < cols) V[((size_t)gg * w + x0 + c) * h_pad + y0 + lane] = stage[((size_t)gg * 32 + c) * 33 + lane];
+      }
+    // strip aggregates for the row pass: thread (pair g, row lane)
+    if (lane < rows) {
+      PairState agg;
+      ps_zero(agg);
+      const float2* sg = stage + (size_t)g * 32 * 33 + lane;
+#pragma unroll 8
+      for (int c = 0; c < cols; ++c)
+        ps_accum(agg, sg[c * 33], tc.wr[0][c], tc.wi[0][c], tc.wr[1][c], tc.wi[1][c]);
+      ps_store(AH + ((size_t)strip * pairs + g) * h * 2 + (size_t)(y0 + lane) * 2, agg);
+    }
+    __syncthreads();
+  }
+}
+
+// ----------------------------------------------------------------------------
+// K3: row anticausal carries: suffix scan of the strip aggregates.
+//   carry(last strip) = V[w-1] / (1-p)
+//   carry(b - 1)      = AH[b] + p^{L_b} carry(b)
+// ----------------------------------------------------------------------------
+__global__ void __launch_bounds__(1024) k_row_scan(const float2* __restrict__ V_all,
+                                                   const float4* __restrict__ AH_all,
+                                                   float4* __restrict__ CH_all, int w, int h,
+                                                   int h_pad, int nx, FilterConsts fc,
+                                                   TileConsts tc) {
+  const int f = blockIdx.y, g = threadIdx.y, pairs = blockDim.y;
   const int y = blockIdx.x * 32 + threadIdx.x;
-  const int g = threadIdx.y;
   if (y >= h) return;
-  const float2* row = src + ((size_t)g * h + y) * w;
-  float2* orow = dst + ((size_t)g * h + y) * w;
-  PairState s;
-  warm_start(s, row[0], fc);
-  for (int x = 0; x < w; ++x) {
-    advance(s, row[x], fc);
-    orow[x] = emit(s, fc.ar, fc.ai);
-  }
-  warm_start(s, row[w - 1], fc);
-  for (int x = w - 1; x >= 0; --x) {
-    const float2 a = emit(s, fc.br, fc.bi);
-    float2 o = orow[x];
-    o.x += a.x;
-    o.y += a.y;
-    orow[x] = o;
-    if (x > 0) advance(s, row[x], fc);
+  const float2* V = V_all + (size_t)f * pairs * w * h_pad;
+  const float4* AH = AH_all + (size_t)f * nx * pairs * h * 2;
+  float4* CH = CH_all + (size_t)f * nx * pairs * h * 2;
+  PairState C;
+  ps_set_gain(C, V[((size_t)g * w + (w - 1)) * h_pad + y], fc);
+  const size_t sstride = (size_t)pairs * h * 2;
+  const size_t off = (size_t)g * h * 2 + (size_t)y * 2;
+  ps_store(CH + (size_t)(nx - 1) * sstride + off, C);
+  for (int b = nx - 1; b >= 1; --b) {
+    PairState agg;
+    ps_load(agg, AH + (size_t)b * sstride + off);
+    if (b == nx - 1) ps_chain(C, agg, tc.pXr, tc.pXi);
+    else ps_chain(C, agg, tc.pTr, tc.pTi);
+    ps_store(CH + (size_t)(b - 1) * sstride + off, C);
   }
 }
 
 // ----------------------------------------------------------------------------
-// K3: P/Q recombination and normalisation (bilateral.cpp:117-126, 139-146):
-//   Q = sum_{n<=N} c_n Fbar_n, P = sum_{n<=N} c_n Fbar_{n+1}, c_n = H^n/n!
-// (scaled by 2^-s_n so c_n Fbar_n,scaled is in reference units / S), then
-// out = sr P/Q + t_c, or the input where |Q| <= 1e-8/S.
+// K4: row pass (deriche_line over rows, spatial.cpp:235-239) on V, fused with
+// the P/Q recombination and normalisation (bilateral.cpp:117-148).
+// Thread (row lane, pair g). Strips of 32 columns are double-buffered into
+// smem with cp.async; per strip: anticausal sweep from the K3 carry, causal
+// sweep (carried), Fbar written back in place, then every pixel of the strip
+// contracts its N+2 planes:
+//   Q = sum_{n<=N} c_n Fbar_n,  P = sum_{n<=N} c_n Fbar_{n+1},  c_n = H^n/n!
+// (weights and planes carry compensating 2^{-+s_n} scalings).
 // ----------------------------------------------------------------------------
-template <typename Tin, typename Tout>
-__global__ void k_combine(const Tin* __restrict__ in, const float2* __restrict__ planes,
-                          Tout* __restrict__ out, const double* __restrict__ scalars,
-                          unsigned long long* __restrict__ fb_count, int w, int h,
-                          RangeConsts rc) {
-  const long long npx = (long long)w * h;
-  const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
-  int fell = 0;
-  if (i < npx) {
-    const double t_c = scalars[0];
-    const double f = static_cast<double>(in[i]);
-    const float H = static_cast<float>((f - t_c) * rc.inv_sr);
-    float c = rc.c0, P = 0.f, Q = 0.f;
-    float2 cur = planes[i];
-    for (int g = 0; g < rc.pairs; ++g) {
-      const int n = 2 * g;
-      const float2 nxt = (g + 1 < rc.pairs) ? planes[(size_t)(g + 1) * npx + i] : make_float2(0.f, 0.f);
-      if (n <= rc.degree) {
-        Q = fmaf(c, cur.x, Q);
-        P = fmaf(c, cur.y, P);
-        c = c * (H * rc.w_step[n]);
-      }
-      if (n + 1 <= rc.degree) {
-        Q = fmaf(c, cur.y, Q);
-        P = fmaf(c, nxt.x, P);
-        c = c * (H * rc.w_step[n + 1]);
-      }
-      cur = nxt;
+template <int MAXT, typename Tin, typename Tout>
+__global__ void __launch_bounds__(MAXT, 1) k_rowpass(const Tin* __restrict__ in_all,
+                                                  const double* __restrict__ scalars,
+                                                  const float2* __restrict__ V_all,
+                                                  const float4* __restrict__ CH_all,
+                                                  Tout* __restrict__ out_all,
+                                                  unsigned long long* __restrict__ fb_all, int w,
+                                                  int h, int h_pad, int nx, FilterConsts fc,
+                                                  RangeConsts rc) {
+  extern __shared__ float4 smem4[];
+  const int f = blockIdx.y, lane = threadIdx.x, g = threadIdx.y, pairs = blockDim.y;
+  const int nthr = 32 * pairs, tid = g * 32 + lane;
+  const int y0 = blockIdx.x * 32, y = y0 + lane;
+  const int rows = min(32, h - y0);
+  const size_t tile_elems = (size_t)pairs * 32 * 32;  // float2 per buffer: [g][x][32 rows]
+  float2* tiles = reinterpret_cast<float2*>(smem4);
+  Tin* ftiles = reinterpret_cast<Tin*>(tiles + 2 * tile_elems);  // [2][32 rows][33]
+  Tout* otile = reinterpret_cast<Tout*>(ftiles + 2 * 32 * 33);    // [32 rows][33]
+  __shared__ unsigned fb_shared;
+  if (tid == 0) fb_shared = 0;
+
+  const Tin* in = in_all + (size_t)f * w * h;
+  Tout* out = out_all + (size_t)f * w * h;
+  const float2* V = V_all + (size_t)f * pairs * w * h_pad;
+  const float4* CH = CH_all + (size_t)f * nx * pairs * h * 2;
+  const double t_c = scalars[2 * f];
+
+  // issue the V tile of strip b into buffer `buf`: 16-byte copies of
+  // [g][x][32 rows] (rows padded to h_pad, so always in bounds)
+  auto issue_tile = [&](int b, int buf) {
+    const int xs = b * 32, ncol = min(32, w - xs);
+    float2* dst = tiles + (size_t)buf * tile_elems;
+    const int nchunk = pairs * 32 * 16;  // 16-byte chunks per buffer
+    for (int q = tid; q < nchunk; q += nthr) {
+      const int gg = q >> 9, c = (q >> 4) & 31, part = q & 15;
+      if (c < ncol)
+        cp_async16(dst + ((size_t)gg * 32 + c) * 32 + part * 2,
+                   V + ((size_t)gg * w + xs + c) * h_pad + y0 + part * 2);
     }
-    double o;
-    if (!(fabsf(Q) > rc.q_thresh)) {
-      o = f;
-      fell = 1;
-    } else {
-      o = rc.sigma_r * ((static_cast<double>(P) * rc.p_scale) / static_cast<double>(Q)) + t_c;
+    issue_f_tile(ftiles + buf * 32 * 33, in, w, h, xs, y0);
+    cp_async_commit();
+  };
+
+  issue_tile(0, 0);
+  PairState cs;
+  ps_zero(cs);
+  unsigned my_fb = 0;
+  for (int b = 0; b < nx; ++b) {
+    const int cur = b & 1, xs = b * 32, cols = min(32, w - xs);
+    const Tin* ftile = ftiles + cur * 32 * 33;
+    cp_async_wait_all();
+    __syncthreads();
+    if (b + 1 < nx) issue_tile(b + 1, cur ^ 1);
+    float2* tl = tiles + (size_t)cur * tile_elems + (size_t)g * 32 * 32 + lane;  // [x*32]
+    if (lane < rows) {
+      PairState as;
+      ps_load(as, CH + ((size_t)b * pairs + g) * h * 2 + (size_t)y * 2);
+      float2 buf[32];
+#pragma unroll
+      for (int c = 31; c >= 0; --c) {
+        if (c < cols) {
+          buf[c] = ps_emit(as, fc.br, fc.bi);
+          ps_advance(as, tl[c * 32], fc);
+        }
+      }
+#pragma unroll
+      for (int c = 0; c < 32; ++c) {
+        if (c < cols) {
+          const float2 xv = tl[c * 32];
+          if (b == 0 && c == 0) ps_set_gain(cs, xv, fc);
+          ps_advance(cs, xv, fc);
+          const float2 o = ps_emit(cs, fc.ar, fc.ai);
+          tl[c * 32] = make_float2(o.x + buf[c].x, o.y + buf[c].y);
+        }
+      }
     }
-    out[i] = static_cast<Tout>(o);
+    __syncthreads();
+    // contraction: pixel (row r = p & 31, col c = p >> 5)
+    const float2* tb = tiles + (size_t)cur * tile_elems;
+    for (int p = tid; p < 1024; p += nthr) {
+      const int r = p & 31, c = p >> 5;
+      if (r < rows && c < cols) {
+        const double fv = static_cast<double>(ftile[r * 33 + c]);
+        const float Hf = static_cast<float>((fv - t_c) * rc.inv_sr);
+        float cc = rc.c0, P = 0.f, Q = 0.f;
+        float2 curv = tb[(size_t)c * 32 + r];
+        for (int gg = 0; gg < pairs; ++gg) {
+          const int n = 2 * gg;
+          const float2 nxt = (gg + 1 < pairs) ? tb[((size_t)(gg + 1) * 32 + c) * 32 + r]
+                                              : make_float2(0.f, 0.f);
+          if (n <= rc.degree) {
+            Q = fmaf(cc, curv.x, Q);
+            P = fmaf(cc, curv.y, P);
+            cc = cc * (Hf * rc.w_step[n]);
+          }
+          if (n + 1 <= rc.degree) {
+            Q = fmaf(cc, curv.y, Q);
+            P = fmaf(cc, nxt.x, P);
+            cc = cc * (Hf * rc.w_step[n + 1]);
+          }
+          curv = nxt;
+        }
+        double o;
+        if (!(fabsf(Q) > rc.q_thresh)) {
+          o = fv;
+          ++my_fb;
+        } else {
+          o = rc.sigma_r * ((static_cast<double>(P) * rc.p_scale) / static_cast<double>(Q)) + t_c;
+        }
+        otile[r * 33 + c] = static_cast<Tout>(o);
+      }
+    }
+    __syncthreads();
+    for (int p = tid; p < 1024; p += nthr) {
+      const int r = p >> 5, c = p & 31;
+      if (r < rows && c < cols) out[(size_t)(y0 + r) * w + xs + c] = otile[r * 33 + c];
+    }
   }
-  const unsigned ballot = __ballot_sync(0xffffffffu, fell);
-  if ((threadIdx.x & 31) == 0 && ballot) atomicAdd(fb_count, (unsigned long long)__popc(ballot));
+  if (my_fb) atomicAdd(&fb_shared, my_fb);
+  __syncthreads();
+  if (tid == 0 && fb_shared) atomicAdd(fb_all + f, (unsigned long long)fb_shared);
 }
-
-// ----------------------------------------------------------------------------
-// Host launchers
-// ----------------------------------------------------------------------------
-static void check(cudaError_t e, const char* what) {
-  if (e != cudaSuccess) throw Error{9, std::string(what) + ": " + cudaGetErrorString(e)};
-}
-
-void plan_init(Plan& plan, const Params& p, int device) {
-  plan.p = p;
-  plan.device = device;
-  plan.fc = make_filter_consts(p.sigma_s);
-  plan.rc = make_range_consts(p);
-  const size_t npx = (size_t)p.width * p.height;
-  const size_t plane_bytes = (size_t)plan.rc.pairs * npx * sizeof(float2);
-  plan.mean_blocks = (int)std::min<size_t>((npx + kMeanThreads - 1) / kMeanThreads, 148 * 8);
-  if (plan.mean_blocks < 1) plan.mean_blocks = 1;
-  check(cudaMalloc(&plan.planes_v, plane_bytes), "cudaMalloc(planes_v)");
-  check(cudaMalloc(&plan.planes_b, plane_bytes), "cudaMalloc(planes_b)");
-  check(cudaMalloc(&plan.d_scalars, 4 * sizeof(double)), "cudaMalloc(scalars)");
-  check(cudaMalloc(&plan.d_partials, 2 * sizeof(double) * plan.mean_blocks), "cudaMalloc(partials)");
-  plan.bytes = 2 * plane_bytes + 4 * sizeof(double) + 2 * sizeof(double) * plan.mean_blocks;
-  plan.launches_per_frame = 5;
-}
-
-void plan_free(Plan& plan) {
-  cudaFree(plan.planes_v);
-  cudaFree(plan.planes_b);
-  cudaFree(plan.d_scalars);
-  cudaFree(plan.d_partials);
-  plan.planes_v = plan.planes_b = nullptr;
-  plan.d_scalars = plan.d_partials = nullptr;
-}
-
-template <typename Tin, typename Tout>
-static void run_frame(Plan& plan, const Tin* d_in, Tout* d_out, unsigned long long* d_fb,
-                      cudaStream_t st) {
-  const int w = plan.p.width, h = plan.p.height;
-  const long long npx = (long long)w * h;
-  k_mean_partial<Tin><<<plan.mean_blocks, kMeanThreads, 0, st>>>(d_in, npx, plan.d_partials);
-  k_mean_final<<<1, kMeanThreads, 0, st>>>(plan.d_partials, plan.mean_blocks, npx,
-                                           plan.rc.centering, plan.d_scalars);
-  const dim3 blk(32, plan.rc.pairs);
-  float2* pv = reinterpret_cast<float2*>(plan.planes_v);
-  float2* pb = reinterpret_cast<float2*>(plan.planes_b);
-  k_colpass<Tin><<<(w + 31) / 32, blk, 0, st>>>(d_in, pv, plan.d_scalars, w, h, plan.fc, plan.rc);
-  k_rowpass<<<(h + 31) / 32, blk, 0, st>>>(pv, pb, w, h, plan.fc);
-  k_combine<Tin, Tout><<<(unsigned)((npx + 255) / 256), 256, 0, st>>>(
-      d_in, pb, d_out, plan.d_scalars, d_fb, w, h, plan.rc);
-  check(cudaGetLastError(), "kernel launch");
-}
-
 
 // ----------------------------------------------------------------------------
 // gpf_gaussian_recursive (proj/src/capi.cpp:219-228 -> spatial.cpp:220-251):
@@ -394,24 +522,132 @@ __global__ void k_gauss_cols(const double* __restrict__ tmp, double* __restrict_
   for (int y = 0; y < h; ++y) out[(size_t)y * w + x] = m_(out[(size_t)y * w + x], scale);
 }
 
+// ----------------------------------------------------------------------------
+// Host side
+// ----------------------------------------------------------------------------
+static void check(cudaError_t e, const char* what) {
+  if (e != cudaSuccess) throw Error{9, std::string(what) + ": " + cudaGetErrorString(e)};
+}
+
+template <typename Tin>
+static size_t colpass_smem(int pairs) {
+  return sizeof(float2) * (kTile * 32 + (size_t)pairs * 32 * 33) + sizeof(Tin) * 2 * 32 * 33;
+}
+template <typename Tin, typename Tout>
+static size_t rowpass_smem(int pairs) {
+  return sizeof(float2) * 2 * (size_t)pairs * 32 * 32 + sizeof(Tin) * 2 * 32 * 33 +
+         sizeof(Tout) * 32 * 33;
+}
+
 void run_gaussian_f64(const double* d_in, double* d_out, double* d_tmp, int w, int h,
                       double sigma_s, double scale, cudaStream_t st) {
   DericheD k;
   deriche_coeffs_f64(sigma_s, k.nc, k.na, k.d);
-  cudaMemsetAsync(d_out, 0, sizeof(double) * (size_t)w * h, st);
+  check(cudaMemsetAsync(d_out, 0, sizeof(double) * (size_t)w * h, st), "cudaMemsetAsync");
   k_gauss_rows<<<(h + 127) / 128, 128, 0, st>>>(d_in, d_tmp, w, h, k);
   k_gauss_cols<<<(w + 127) / 128, 128, 0, st>>>(d_tmp, d_out, w, h, k, scale);
   check(cudaGetLastError(), "kernel launch");
 }
 
-void run_frame_f32(Plan& plan, const float* d_in, float* d_out, unsigned long long* d_fb,
-                   cudaStream_t st) {
-  run_frame<float, float>(plan, d_in, d_out, d_fb, st);
+void plan_init(Plan& plan, const Params& p, int device, int batch) {
+  plan.p = p;
+  plan.device = device;
+  plan.batch = std::max(1, batch);
+  plan.fc = make_filter_consts(p.sigma_s);
+  plan.tc = make_tile_consts(p.sigma_s, p.width, p.height);
+  plan.rc = make_range_consts(p);
+  const int pairs = plan.rc.pairs;
+  if (rowpass_smem<double, double>(pairs) > 227 * 1024 || colpass_smem<double>(pairs) > 227 * 1024)
+    throw Error{1, "RangeParams: degree must be <= 48 in the B200 library"};
+  const int w = p.width, h = p.height, B = plan.batch;
+  plan.ny = (h + kTile - 1) / kTile;
+  plan.nx = (w + kTile - 1) / kTile;
+  const int h_pad = plan.ny * kTile;
+  const size_t npx = (size_t)w * h;
+  plan.mean_blocks = (int)std::min<size_t>((npx + kMeanThreads - 1) / kMeanThreads, 148 * 4);
+  if (plan.mean_blocks < 1) plan.mean_blocks = 1;
+  const size_t vb = sizeof(float2) * B * (size_t)pairs * w * h_pad;
+  const size_t cab = sizeof(float4) * 2 * B * (size_t)plan.ny * pairs * w;
+  const size_t ahb = sizeof(float4) * 2 * B * (size_t)plan.nx * pairs * h;
+  plan.V = nullptr;
+  plan.CA = plan.AH = plan.CH = nullptr;
+  plan.scalars = plan.partials = nullptr;
+  try {
+    check(cudaMalloc(&plan.V, vb), "cudaMalloc(V)");
+    check(cudaMalloc(&plan.CA, cab), "cudaMalloc(CA)");
+    check(cudaMalloc(&plan.AH, ahb), "cudaMalloc(AH)");
+    check(cudaMalloc(&plan.CH, ahb), "cudaMalloc(CH)");
+    check(cudaMalloc(&plan.scalars, sizeof(double) * 2 * B), "cudaMalloc(scalars)");
+    check(cudaMalloc(&plan.partials, sizeof(double) * 2 * B * plan.mean_blocks), "cudaMalloc(partials)");
+  } catch (...) {
+    plan_free(plan);
+    throw;
+  }
+  plan.bytes = vb + cab + 2 * ahb + sizeof(double) * 2 * B * (1 + plan.mean_blocks);
+  plan.launches_per_frame = 6;
 }
 
-void run_frame_f64(Plan& plan, const double* d_in, double* d_out, unsigned long long* d_fb,
-                   cudaStream_t st) {
-  run_frame<double, double>(plan, d_in, d_out, d_fb, st);
+void plan_free(Plan& plan) {
+  cudaFree(plan.V);
+  cudaFree(plan.CA);
+  cudaFree(plan.AH);
+  cudaFree(plan.CH);
+  cudaFree(plan.scalars);
+  cudaFree(plan.partials);
+  plan.V = nullptr;
+  plan.CA = plan.AH = plan.CH = nullptr;
+  plan.scalars = plan.partials = nullptr;
+}
+
+// MAXT = the CTA size bound the kernels are compiled for (32 x pairs threads):
+// 384 -> up to 168 registers/thread (N <= 22), 512 -> 128 (N <= 30), 1024 -> 64.
+template <int MAXT, typename Tin, typename Tout>
+static void launch_passes(Plan& plan, const Tin* d_in, Tout* d_out, int count,
+                          unsigned long long* d_fb, cudaStream_t st) {
+  const int w = plan.p.width, h = plan.p.height, pairs = plan.rc.pairs;
+  const int h_pad = plan.ny * kTile;
+  check(cudaFuncSetAttribute(k_colpass<MAXT, Tin>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             (int)colpass_smem<Tin>(pairs)),
+        "cudaFuncSetAttribute");
+  check(cudaFuncSetAttribute(k_rowpass<MAXT, Tin, Tout>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             (int)rowpass_smem<Tin, Tout>(pairs)),
+        "cudaFuncSetAttribute");
+  const dim3 blk(32, pairs);
+  k_col_carry<MAXT, Tin><<<dim3(plan.nx, count), blk, 0, st>>>(d_in, plan.scalars, plan.CA, w, h,
+                                                               plan.ny, plan.fc, plan.tc, plan.rc);
+  k_colpass<MAXT, Tin><<<dim3(plan.nx, count), blk, colpass_smem<Tin>(pairs), st>>>(
+      d_in, plan.scalars, plan.CA, plan.V, plan.AH, w, h, h_pad, plan.ny, plan.nx, plan.fc, plan.tc,
+      plan.rc);
+  k_row_scan<<<dim3(plan.ny, count), blk, 0, st>>>(plan.V, plan.AH, plan.CH, w, h, h_pad, plan.nx,
+                                                   plan.fc, plan.tc);
+  k_rowpass<MAXT, Tin, Tout><<<dim3(plan.ny, count), blk, rowpass_smem<Tin, Tout>(pairs), st>>>(
+      d_in, plan.scalars, plan.V, plan.CH, d_out, d_fb, w, h, h_pad, plan.nx, plan.fc, plan.rc);
+}
+
+template <typename Tin, typename Tout>
+static void run_frames(Plan& plan, const Tin* d_in, Tout* d_out, int count,
+                       unsigned long long* d_fb, cudaStream_t st) {
+  if (count <= 0) return;
+  if (count > plan.batch) throw Error{1, "batch larger than the plan's workspace"};
+  const long long npx = (long long)plan.p.width * plan.p.height;
+  k_mean_partial<Tin><<<dim3(plan.mean_blocks, count), kMeanThreads, 0, st>>>(d_in, npx, plan.partials);
+  k_mean_final<<<count, kMeanThreads, 0, st>>>(plan.partials, plan.mean_blocks, npx,
+                                               plan.rc.centering, plan.scalars);
+  const int nthr = 32 * plan.rc.pairs;
+  if (nthr <= 384) launch_passes<384>(plan, d_in, d_out, count, d_fb, st);
+  else if (nthr <= 512) launch_passes<512>(plan, d_in, d_out, count, d_fb, st);
+  else launch_passes<1024>(plan, d_in, d_out, count, d_fb, st);
+  check(cudaGetLastError(), "kernel launch");
+}
+
+void run_frames_f32(Plan& plan, const float* d_in, float* d_out, int count,
+                    unsigned long long* d_fb, cudaStream_t st) {
+  run_frames<float, float>(plan, d_in, d_out, count, d_fb, st);
+}
+
+void run_frames_f64(Plan& plan, const double* d_in, double* d_out, int count,
+                    unsigned long long* d_fb, cudaStream_t st) {
+  run_frames<double, double>(plan, d_in, d_out, count, d_fb, st);
 }
 
 }  // namespace gpfb

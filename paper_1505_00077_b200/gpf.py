@@ -130,13 +130,15 @@ class Plan:
     """Device workspace for filtering fp32 frames of one size/parameter set."""
 
     def __init__(self, width: int, height: int, sigma_s: float, sigma_r: float, degree: int = 20,
-                 kernel_scale: float = 1.0, centering: int = 1, device: int = -1):
+                 kernel_scale: float = 1.0, centering: int = 1, device: int = -1, batch: int = 1):
         self.width, self.height = width, height
         sp = spatial_params(sigma_s, kernel_scale=kernel_scale)
         rp = range_params(sigma_r, degree)
         self.h = C.c_void_p()
         _check(_lib.lib().gpf_b200_plan_create(width, height, C.byref(sp), C.byref(rp),
                                                centering, device, C.byref(self.h)))
+        if batch > 1:
+            _check(_lib.lib().gpf_b200_plan_set_batch(self.h, batch))
 
     @property
     def workspace_bytes(self) -> int:
