@@ -62,6 +62,8 @@ Deriche deriche(double s) {
 
 cd poly3(const double c[4], cd q) { return c[0] + q * (c[1] + q * (c[2] + q * c[3])); }
 
+float2 dup(double v) { return make_float2(static_cast<float>(v), static_cast<float>(v)); }
+
 }  // namespace
 
 void deriche_coeffs_f64(double sigma, double nc[4], double na[4], double d[4]) {
@@ -93,14 +95,15 @@ FilterConsts make_filter_consts(double s) {
     // anticausal: z * sum_m na_m z^m / D(z), expanded as sum_k B_k z/(1 - p_k z)
     const cd B = 2.0 * poly3(k.na, q) / den;
     const cd g = 1.0 / (1.0 - pk);
-    fc.pr[sec] = static_cast<float>(pk.real());
-    fc.pi[sec] = static_cast<float>(pk.imag());
-    fc.ar[sec] = static_cast<float>(A.real());
-    fc.ai[sec] = static_cast<float>(A.imag());
-    fc.br[sec] = static_cast<float>(B.real());
-    fc.bi[sec] = static_cast<float>(B.imag());
-    fc.gr[sec] = static_cast<float>(g.real());
-    fc.gi[sec] = static_cast<float>(g.imag());
+    fc.pr2[sec] = dup(pk.real());
+    fc.pi2[sec] = dup(pk.imag());
+    fc.npi2[sec] = dup(-pk.imag());
+    fc.ar2[sec] = dup(A.real());
+    fc.nai2[sec] = dup(-A.imag());
+    fc.br2[sec] = dup(B.real());
+    fc.nbi2[sec] = dup(-B.imag());
+    fc.gr2[sec] = dup(g.real());
+    fc.gi2[sec] = dup(g.imag());
   }
   return fc;
 }
@@ -114,16 +117,16 @@ TileConsts make_tile_consts(double s, int width, int height) {
   for (int k = 0; k < 2; ++k) {
     for (int j = 0; j < kTile; ++j) {
       const cd w = std::pow(p[k], j);
-      tc.wr[k][j] = static_cast<float>(w.real());
-      tc.wi[k][j] = static_cast<float>(w.imag());
+      tc.wr2[k][j] = dup(w.real());
+      tc.wi2[k][j] = dup(w.imag());
     }
     const cd pt = std::pow(p[k], kTile), py = std::pow(p[k], last_y), px = std::pow(p[k], last_x);
-    tc.pTr[k] = static_cast<float>(pt.real());
-    tc.pTi[k] = static_cast<float>(pt.imag());
-    tc.pYr[k] = static_cast<float>(py.real());
-    tc.pYi[k] = static_cast<float>(py.imag());
-    tc.pXr[k] = static_cast<float>(px.real());
-    tc.pXi[k] = static_cast<float>(px.imag());
+    tc.pTr2[k] = dup(pt.real());
+    tc.pTi2[k] = dup(pt.imag());
+    tc.pYr2[k] = dup(py.real());
+    tc.pYi2[k] = dup(py.imag());
+    tc.pXr2[k] = dup(px.real());
+    tc.pXi2[k] = dup(px.imag());
   }
   return tc;
 }
@@ -145,6 +148,8 @@ RangeConsts make_range_consts(const Params& p) {
   if (k < 1) k = 1;
   const int s0 = 100;
   rc.e_scale = std::ldexp(1.0, s0);
+  rc.e_log2 = s0;
+  rc.exp2_k = 1.4426950408889634 / (2.0 * p.sigma_r * p.sigma_r);
   rc.h_step = static_cast<float>(std::ldexp(1.0, -k));
   rc.c0 = static_cast<float>(std::ldexp(1.0, -s0));
   rc.p_scale = static_cast<float>(std::ldexp(1.0, k));

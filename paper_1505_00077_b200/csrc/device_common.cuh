@@ -1,4 +1,9 @@
 // Device helpers shared by the GPF kernels.
+//
+// A thread owns one line and one PAIR of planes (2g, 2g+1); the two planes
+// travel together as the .x/.y halves of float2 values, so every recurrence
+// step is issued as packed fp32x2 instructions (FFMA2 on sm_100a: two FMAs
+// per issue slot).
 #pragma once
 
 #include <cuda_runtime.h>
@@ -7,113 +12,114 @@
 
 namespace gpfb {
 
+__device__ __forceinline__ float2 f2(float v) { return make_float2(v, v); }
+__device__ __forceinline__ float2 fma2(float2 a, float2 b, float2 c) { return __ffma2_rn(a, b, c); }
+__device__ __forceinline__ float2 mul2(float2 a, float2 b) { return __fmul2_rn(a, b); }
+__device__ __forceinline__ float2 add2(float2 a, float2 b) { return __fadd2_rn(a, b); }
+
 // ---------------------------------------------------------------- prologue
 // Per-pixel range terms (bilateral.cpp:92-101), fp64 like the reference:
 //   h = f - t_c,  H = h/sr,  E = exp(-h^2 / 2 sr^2)
 // packed for the fp32 plane chain: es = E 2^s0, m = H 2^-k, so that
 // plane n (scaled by 2^{s0 - k n}) = es * m^n.
+//
+// es = 2^(s0 - h^2 log2(e) / 2sr^2): the exponent is formed and split into an
+// integer and a fraction |r| <= 1/2 in fp64 (so large arguments lose nothing),
+// 2^r comes from a degree-7 polynomial in fp32 (truncation 5e-9, ~1 ulp), and
+// the integer part is applied as two exact power-of-two scalings. Same
+// accuracy class as rounding the fp64 exp() to fp32, at a third of the cost.
+__device__ __forceinline__ float exp2_frac(float r) {  // 2^r, |r| <= 0.5
+  float p = 1.5252733804059841e-05f;                    // ln2^7/7!
+  p = fmaf(p, r, 1.5403530393381606e-04f);              // ln2^6/6!
+  p = fmaf(p, r, 1.3333558146428443e-03f);              // ln2^5/5!
+  p = fmaf(p, r, 9.6181291076284772e-03f);              // ln2^4/4!
+  p = fmaf(p, r, 5.5504108664821580e-02f);              // ln2^3/3!
+  p = fmaf(p, r, 2.4022650695910071e-01f);              // ln2^2/2!
+  p = fmaf(p, r, 6.9314718055994531e-01f);              // ln2
+  return fmaf(p, r, 1.0f);
+}
+
 __device__ __forceinline__ float2 pixel_terms(double f, double t_c, const RangeConsts& rc) {
   const double h = f - t_c;
+  const double a = fma(-(h * h), rc.exp2_k, rc.e_log2);  // s0 - h^2 log2(e)/(2 sr^2)
+  const double n = rint(a);
+  const float pr = exp2_frac(static_cast<float>(a - n));
+  const int ni = max(static_cast<int>(n), -252);
+  const int k1 = max(ni, -126), k2 = ni - k1;  // both exponents in the normal range
   float2 r;
-  r.x = static_cast<float>(exp(-(h * h) * rc.inv2s2) * rc.e_scale);
+  r.x = (pr * __int_as_float((k1 + 127) << 23)) * __int_as_float((k2 + 127) << 23);
   r.y = static_cast<float>(h * rc.inv_sr) * rc.h_step;
   return r;
 }
 
-// Planes (2g, 2g+1) of a pixel from its terms; g is warp-uniform.
-__device__ __forceinline__ float2 pair_planes(float2 t, int g) {
-  float base = t.y * t.y, acc = t.x;
-  for (int e = g; e; e >>= 1) {
-    if (e & 1) acc *= base;
-    base *= base;
-  }
-  return make_float2(acc, acc * t.y);
-}
-
 // ------------------------------------------------------- IIR section state
-// Two complex first-order sections (k) for the two planes (q) of a pair.
+// Two complex first-order sections k; each component packs the two planes.
 struct PairState {
-  float wr[2][2], wi[2][2];  // [plane q][section k]
+  float2 wr[2], wi[2];
 };
 
+__device__ __forceinline__ void ps_zero(PairState& s) {
+  s.wr[0] = s.wr[1] = s.wi[0] = s.wi[1] = make_float2(0.f, 0.f);
+}
+
+// replicate steady state: w = x / (1 - p)
 __device__ __forceinline__ void ps_set_gain(PairState& s, float2 x, const FilterConsts& fc) {
 #pragma unroll
   for (int k = 0; k < 2; ++k) {
-    s.wr[0][k] = x.x * fc.gr[k];
-    s.wi[0][k] = x.x * fc.gi[k];
-    s.wr[1][k] = x.y * fc.gr[k];
-    s.wi[1][k] = x.y * fc.gi[k];
+    s.wr[k] = mul2(x, fc.gr2[k]);
+    s.wi[k] = mul2(x, fc.gi2[k]);
   }
 }
 
-// w <- p w + x
+// w <- p w + x   (4 FFMA2/FMUL2 per section for both planes)
 __device__ __forceinline__ void ps_advance(PairState& s, float2 x, const FilterConsts& fc) {
 #pragma unroll
   for (int k = 0; k < 2; ++k) {
-#pragma unroll
-    for (int q = 0; q < 2; ++q) {
-      const float xv = q == 0 ? x.x : x.y;
-      const float nr = fmaf(fc.pr[k], s.wr[q][k], fmaf(-fc.pi[k], s.wi[q][k], xv));
-      const float ni = fmaf(fc.pr[k], s.wi[q][k], fc.pi[k] * s.wr[q][k]);
-      s.wr[q][k] = nr;
-      s.wi[q][k] = ni;
-    }
+    const float2 nr = fma2(fc.pr2[k], s.wr[k], fma2(fc.npi2[k], s.wi[k], x));
+    const float2 ni = fma2(fc.pr2[k], s.wi[k], mul2(fc.pi2[k], s.wr[k]));
+    s.wr[k] = nr;
+    s.wi[k] = ni;
   }
 }
 
-// sum_k Re(c_k w_k)
-__device__ __forceinline__ float2 ps_emit(const PairState& s, const float* cr, const float* ci) {
-  float2 o;
-  o.x = fmaf(cr[0], s.wr[0][0], fmaf(-ci[0], s.wi[0][0], fmaf(cr[1], s.wr[0][1], -ci[1] * s.wi[0][1])));
-  o.y = fmaf(cr[0], s.wr[1][0], fmaf(-ci[0], s.wi[1][0], fmaf(cr[1], s.wr[1][1], -ci[1] * s.wi[1][1])));
-  return o;
+// sum_k Re(c_k w_k) = sum_k (cr_k wr_k - ci_k wi_k); ncr = -ci pre-negated
+__device__ __forceinline__ float2 ps_emit(const PairState& s, const float2* cr, const float2* nci) {
+  return fma2(cr[0], s.wr[0], fma2(nci[0], s.wi[0], fma2(cr[1], s.wr[1], mul2(nci[1], s.wi[1]))));
 }
 
-// Carry record: the 8 floats of a PairState, stored as two float4.
+// Carry record: the 8 floats of a PairState as two float4.
 __device__ __forceinline__ void ps_store(float4* dst, const PairState& s) {
-  dst[0] = make_float4(s.wr[0][0], s.wi[0][0], s.wr[0][1], s.wi[0][1]);
-  dst[1] = make_float4(s.wr[1][0], s.wi[1][0], s.wr[1][1], s.wi[1][1]);
+  dst[0] = make_float4(s.wr[0].x, s.wr[0].y, s.wi[0].x, s.wi[0].y);
+  dst[1] = make_float4(s.wr[1].x, s.wr[1].y, s.wi[1].x, s.wi[1].y);
 }
 
 __device__ __forceinline__ void ps_load(PairState& s, const float4* src) {
   const float4 a = src[0], b = src[1];
-  s.wr[0][0] = a.x; s.wi[0][0] = a.y; s.wr[0][1] = a.z; s.wi[0][1] = a.w;
-  s.wr[1][0] = b.x; s.wi[1][0] = b.y; s.wr[1][1] = b.z; s.wi[1][1] = b.w;
+  s.wr[0] = make_float2(a.x, a.y);
+  s.wi[0] = make_float2(a.z, a.w);
+  s.wr[1] = make_float2(b.x, b.y);
+  s.wi[1] = make_float2(b.z, b.w);
 }
 
-// s <- agg + P s  with P = p^L per section (complex), applied to both planes.
-__device__ __forceinline__ void ps_chain(PairState& s, const PairState& agg, const float* plr,
-                                         const float* pli) {
+// s <- agg + P s  with P = p^L per section (complex, duplicated pairs)
+__device__ __forceinline__ void ps_chain(PairState& s, const PairState& agg, const float2* plr,
+                                         const float2* pli) {
 #pragma unroll
   for (int k = 0; k < 2; ++k) {
-#pragma unroll
-    for (int q = 0; q < 2; ++q) {
-      const float nr = fmaf(plr[k], s.wr[q][k], fmaf(-pli[k], s.wi[q][k], agg.wr[q][k]));
-      const float ni = fmaf(plr[k], s.wi[q][k], fmaf(pli[k], s.wr[q][k], agg.wi[q][k]));
-      s.wr[q][k] = nr;
-      s.wi[q][k] = ni;
-    }
+    const float2 nr = fma2(plr[k], s.wr[k], fma2(make_float2(-pli[k].x, -pli[k].y), s.wi[k], agg.wr[k]));
+    const float2 ni = fma2(plr[k], s.wi[k], fma2(pli[k], s.wr[k], agg.wi[k]));
+    s.wr[k] = nr;
+    s.wi[k] = ni;
   }
 }
 
-// agg += w_j x  (complex weight per section, real input per plane)
-__device__ __forceinline__ void ps_accum(PairState& a, float2 x, float w0r, float w0i, float w1r,
-                                         float w1i) {
-  a.wr[0][0] = fmaf(w0r, x.x, a.wr[0][0]);
-  a.wi[0][0] = fmaf(w0i, x.x, a.wi[0][0]);
-  a.wr[1][0] = fmaf(w0r, x.y, a.wr[1][0]);
-  a.wi[1][0] = fmaf(w0i, x.y, a.wi[1][0]);
-  a.wr[0][1] = fmaf(w1r, x.x, a.wr[0][1]);
-  a.wi[0][1] = fmaf(w1i, x.x, a.wi[0][1]);
-  a.wr[1][1] = fmaf(w1r, x.y, a.wr[1][1]);
-  a.wi[1][1] = fmaf(w1i, x.y, a.wi[1][1]);
-}
-
-__device__ __forceinline__ void ps_zero(PairState& s) {
-#pragma unroll
-  for (int q = 0; q < 2; ++q)
-#pragma unroll
-    for (int k = 0; k < 2; ++k) s.wr[q][k] = s.wi[q][k] = 0.f;
+// agg += w x with complex weight (w_k = wr_k + i wi_k) per section
+__device__ __forceinline__ void ps_accum(PairState& a, float2 x, float2 w0r, float2 w0i, float2 w1r,
+                                         float2 w1i) {
+  a.wr[0] = fma2(w0r, x, a.wr[0]);
+  a.wi[0] = fma2(w0i, x, a.wi[0]);
+  a.wr[1] = fma2(w1r, x, a.wr[1]);
+  a.wi[1] = fma2(w1i, x, a.wi[1]);
 }
 
 }  // namespace gpfb

@@ -25,21 +25,23 @@ constexpr int kTile = 32;       // rows per column-pass chunk == columns per row
 // function, far better conditioned in fp32 than the direct form. The replicate
 // steady-state warm start of the reference is w_k[-1] = x[0]/(1-p_k) and
 // v_k[n-1] = x[n-1]/(1-p_k).
+// Every coefficient is stored duplicated as (c, c) so that it feeds packed
+// fp32x2 instructions directly (the two halves are the two planes of a pair).
 struct FilterConsts {
-  float pr[2], pi[2];  // poles (upper half plane)
-  float ar[2], ai[2];  // causal residues (x2)
-  float br[2], bi[2];  // anticausal residues (x2)
-  float gr[2], gi[2];  // 1/(1-p): warm-start gain
+  float2 pr2[2], pi2[2], npi2[2];  // poles p_k (upper half plane), -Im p_k
+  float2 ar2[2], nai2[2];          // causal residues A_k (x2): Re, -Im
+  float2 br2[2], nbi2[2];          // anticausal residues B_k (x2): Re, -Im
+  float2 gr2[2], gi2[2];           // 1/(1-p_k): warm-start gain
 };
 
 // Tile constants for exact anticausal carries between chunks of kTile
 // samples: the carry entering a chunk from the far side is
 //   C = sum_{j < L} p^j x[j]  +  p^L C_next        (L = chunk length)
 struct TileConsts {
-  float wr[2][kTile], wi[2][kTile];  // p_k^j, j < kTile
-  float pTr[2], pTi[2];              // p_k^kTile
-  float pYr[2], pYi[2];              // p_k^(rows in the last row chunk)
-  float pXr[2], pXi[2];              // p_k^(columns in the last column strip)
+  float2 wr2[2][kTile], wi2[2][kTile];  // p_k^j, j < kTile
+  float2 pTr2[2], pTi2[2];              // p_k^kTile
+  float2 pYr2[2], pYi2[2];              // p_k^(rows in the last row chunk)
+  float2 pXr2[2], pXi2[2];              // p_k^(columns in the last column strip)
 };
 
 // Range / plane constants. Plane n holds F_n * 2^{s_n}, s_n = s0 - k*n, so
@@ -50,6 +52,8 @@ struct RangeConsts {
   double inv2s2;      // 1/(2 sigma_r^2)  (same expression as bilateral.cpp:92)
   double sigma_r;
   double e_scale;     // 2^s0
+  double e_log2;      // s0
+  double exp2_k;      // log2(e) / (2 sigma_r^2)
   float h_step;       // 2^-k      (chain multiplier factor)
   float c0;           // 2^-s0     (weight of plane 0)
   float p_scale;      // 2^k       (P uses planes n+1)

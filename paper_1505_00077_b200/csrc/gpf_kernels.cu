@@ -140,16 +140,25 @@ __device__ __forceinline__ void issue_f_tile(Tin* ftile, const Tin* __restrict__
   }
 }
 
-// Producer: range terms (es, m) of a 32x32 pixel block from the smem f tile,
-// computed once per pixel and shared by the `pairs` warps.
+// Producer: all planes of a 32x32 pixel block into buf[pair][col][33 rows]
+// (float2 = planes 2g, 2g+1), computed once per pixel from the smem f tile
+// and shared by the `pairs` warps. Plane chain in fp32:
+//   x_0 = E 2^s0,  x_{n+1} = x_n * (H 2^-k)      (bilateral.cpp:97-101, 117-120)
 template <typename Tin>
-__device__ __forceinline__ void produce_terms(float2 (*prod)[32], const Tin* ftile, double t_c,
-                                              const RangeConsts& rc) {
-  const int nthr = blockDim.x * blockDim.y;
+__device__ __forceinline__ void produce_planes(float2* buf, const Tin* ftile, double t_c,
+                                               const RangeConsts& rc) {
+  const int nthr = blockDim.x * blockDim.y, pairs = blockDim.y;
   const int tid = threadIdx.y * 32 + threadIdx.x;
   for (int p = tid; p < 1024; p += nthr) {
     const int j = p >> 5, c = p & 31;
-    prod[j][c] = pixel_terms(static_cast<double>(ftile[j * 33 + c]), t_c, rc);
+    const float2 t = pixel_terms(static_cast<double>(ftile[j * 33 + c]), t_c, rc);
+    float x = t.x;
+    float2* dst = buf + c * 33 + j;
+    for (int gg = 0; gg < pairs; ++gg) {
+      const float x1 = x * t.y;
+      dst[gg * 32 * 33] = make_float2(x, x1);
+      x = x1 * t.y;
+    }
   }
 }
 
@@ -162,69 +171,74 @@ __device__ __forceinline__ void produce_terms(float2 (*prod)[32], const Tin* fti
 // ----------------------------------------------------------------------------
 template <int MAXT, typename Tin>
 __global__ void __launch_bounds__(MAXT, 1) k_col_carry(const Tin* __restrict__ in_all,
-                                                    const double* __restrict__ scalars,
-                                                    float4* __restrict__ CA_all, int w, int h,
-                                                    int ny, FilterConsts fc, TileConsts tc,
-                                                    RangeConsts rc) {
-  __shared__ float2 prod[kTile][32];
-  __shared__ Tin ftile[2][32 * 33];
+                                                       const double* __restrict__ scalars,
+                                                       float4* __restrict__ CA_all, int w, int h,
+                                                       int ny, FilterConsts fc, TileConsts tc,
+                                                       RangeConsts rc) {
+  extern __shared__ float4 smem4[];
+  float2* buf = reinterpret_cast<float2*>(smem4);                               // [pairs][32][33]
+  Tin* ftiles = reinterpret_cast<Tin*>(buf + (size_t)blockDim.y * 32 * 33);  // [2][32*33]
   const int f = blockIdx.y, lane = threadIdx.x, g = threadIdx.y, pairs = blockDim.y;
   const int x0 = blockIdx.x * 32, x = x0 + lane;
   const Tin* in = in_all + (size_t)f * w * h;
   float4* CA = CA_all + (size_t)f * ny * pairs * w * 2;
   const double t_c = scalars[2 * f];
+  const float2* mine = buf + ((size_t)g * 32 + lane) * 33;
   PairState C;
   ps_zero(C);
-  issue_f_tile(ftile[(ny - 1) & 1], in, w, h, x0, (ny - 1) * kTile);
+  issue_f_tile(ftiles + ((ny - 1) & 1) * 32 * 33, in, w, h, x0, (ny - 1) * kTile);
   cp_async_commit();
   for (int cy = ny - 1; cy >= 0; --cy) {
     const int y0 = cy * kTile, rows = min(kTile, h - y0);
     cp_async_wait_all();
     __syncthreads();
     if (cy > 0) {
-      issue_f_tile(ftile[(cy - 1) & 1], in, w, h, x0, y0 - kTile);
+      issue_f_tile(ftiles + ((cy - 1) & 1) * 32 * 33, in, w, h, x0, y0 - kTile);
       cp_async_commit();
     }
-    produce_terms(prod, ftile[cy & 1], t_c, rc);
+    produce_planes(buf, ftiles + (cy & 1) * 32 * 33, t_c, rc);
     __syncthreads();
     if (x < w) {
-      if (cy == ny - 1) ps_set_gain(C, pair_planes(prod[rows - 1][lane], g), fc);
+      if (cy == ny - 1) ps_set_gain(C, mine[rows - 1], fc);
       ps_store(CA + ((size_t)cy * pairs + g) * w * 2 + (size_t)x * 2, C);
       if (cy > 0) {
         PairState agg;
         ps_zero(agg);
-#pragma unroll 8
-        for (int j = 0; j < rows; ++j)
-          ps_accum(agg, pair_planes(prod[j][lane], g), tc.wr[0][j], tc.wi[0][j], tc.wr[1][j],
-                   tc.wi[1][j]);
-        if (cy == ny - 1) ps_chain(C, agg, tc.pYr, tc.pYi);
-        else ps_chain(C, agg, tc.pTr, tc.pTi);
+        if (rows == kTile) {
+#pragma unroll
+          for (int j = 0; j < kTile; ++j)
+            ps_accum(agg, mine[j], tc.wr2[0][j], tc.wi2[0][j], tc.wr2[1][j], tc.wi2[1][j]);
+        } else {
+          for (int j = 0; j < rows; ++j)
+            ps_accum(agg, mine[j], tc.wr2[0][j], tc.wi2[0][j], tc.wr2[1][j], tc.wi2[1][j]);
+        }
+        if (cy == ny - 1) ps_chain(C, agg, tc.pYr2, tc.pYi2);
+        else ps_chain(C, agg, tc.pTr2, tc.pTi2);
       }
     }
-    __syncthreads();
   }
 }
 
 // ----------------------------------------------------------------------------
 // K2: column pass (deriche_line over columns, spatial.cpp:240-243), fused with
-// the plane generator. Per row chunk: anticausal sweep from the K1 carry into
-// a register buffer, causal sweep (state carried from the previous chunk)
-// adds it and stages the chunk in smem; the staged chunk is written to V
-// transposed and reduced into the row-pass strip aggregates AH.
+// the plane generator. Per row chunk: the producer writes every plane of the
+// 32x32 block to smem; each thread lifts its pair's 32 inputs into registers,
+// runs the anticausal sweep from the K1 carry (outputs in place in smem),
+// then the causal sweep (state carried across chunks) which adds and leaves
+// the final values in place. The chunk is then written to V transposed and
+// reduced into the row-pass strip aggregates AH.
 // ----------------------------------------------------------------------------
 template <int MAXT, typename Tin>
 __global__ void __launch_bounds__(MAXT, 1) k_colpass(const Tin* __restrict__ in_all,
-                                                  const double* __restrict__ scalars,
-                                                  const float4* __restrict__ CA_all,
-                                                  float2* __restrict__ V_all,
-                                                  float4* __restrict__ AH_all, int w, int h,
-                                                  int h_pad, int ny, int nx, FilterConsts fc,
-                                                  TileConsts tc, RangeConsts rc) {
+                                                     const double* __restrict__ scalars,
+                                                     const float4* __restrict__ CA_all,
+                                                     float2* __restrict__ V_all,
+                                                     float4* __restrict__ AH_all, int w, int h,
+                                                     int h_pad, int ny, int nx, FilterConsts fc,
+                                                     TileConsts tc, RangeConsts rc) {
   extern __shared__ float4 smem4[];
-  float2(*prod)[32] = reinterpret_cast<float2(*)[32]>(smem4);
-  // stage[g][c][33]: column c's 32 rows of pair g (row dim padded to 33)
-  float2* stage = reinterpret_cast<float2*>(smem4) + kTile * 32;
-  Tin* ftiles = reinterpret_cast<Tin*>(stage + (size_t)blockDim.y * 32 * 33);  // [2][32*33]
+  float2* buf = reinterpret_cast<float2*>(smem4);                               // [pairs][32][33]
+  Tin* ftiles = reinterpret_cast<Tin*>(buf + (size_t)blockDim.y * 32 * 33);  // [2][32*33]
   const int f = blockIdx.y, lane = threadIdx.x, g = threadIdx.y, pairs = blockDim.y;
   const int strip = blockIdx.x, x0 = strip * 32, x = x0 + lane;
   const int cols = min(32, w - x0);
@@ -233,6 +247,7 @@ __global__ void __launch_bounds__(MAXT, 1) k_colpass(const Tin* __restrict__ in_
   float2* V = V_all + (size_t)f * pairs * w * h_pad;
   float4* AH = AH_all + (size_t)f * nx * pairs * h * 2;
   const double t_c = scalars[2 * f];
+  float2* mine = buf + ((size_t)g * 32 + lane) * 33;
   PairState cs;  // causal state, carried across chunks
   ps_zero(cs);
   issue_f_tile(ftiles, in, w, h, x0, 0);
@@ -245,50 +260,66 @@ __global__ void __launch_bounds__(MAXT, 1) k_colpass(const Tin* __restrict__ in_
       issue_f_tile(ftiles + ((cy + 1) & 1) * 32 * 33, in, w, h, x0, y0 + kTile);
       cp_async_commit();
     }
-    produce_terms(prod, ftiles + (cy & 1) * 32 * 33, t_c, rc);
+    produce_planes(buf, ftiles + (cy & 1) * 32 * 33, t_c, rc);
     __syncthreads();
     if (x < w) {
       PairState as;
       ps_load(as, CA + ((size_t)cy * pairs + g) * w * 2 + (size_t)x * 2);
-      float2 buf[kTile];
+      float2 xr[kTile];
 #pragma unroll
-      for (int j = kTile - 1; j >= 0; --j) {
-        if (j < rows) {
-          buf[j] = ps_emit(as, fc.br, fc.bi);
-          ps_advance(as, pair_planes(prod[j][lane], g), fc);
+      for (int j = 0; j < kTile; ++j) xr[j] = mine[j];
+      if (cy == 0) ps_set_gain(cs, xr[0], fc);
+      if (rows == kTile) {  // full chunk: branch-free sweeps
+#pragma unroll
+        for (int j = kTile - 1; j >= 0; --j) {
+          mine[j] = ps_emit(as, fc.br2, fc.nbi2);
+          ps_advance(as, xr[j], fc);
         }
-      }
-      float2* st = stage + ((size_t)g * 32 + lane) * 33;
 #pragma unroll
-      for (int j = 0; j < kTile; ++j) {
-        if (j < rows) {
-          const float2 xv = pair_planes(prod[j][lane], g);
-          if (cy == 0 && j == 0) ps_set_gain(cs, xv, fc);
-          ps_advance(cs, xv, fc);
-          const float2 o = ps_emit(cs, fc.ar, fc.ai);
-          st[j] = make_float2(o.x + buf[j].x, o.y + buf[j].y);
+        for (int j = 0; j < kTile; ++j) {
+          ps_advance(cs, xr[j], fc);
+          mine[j] = add2(ps_emit(cs, fc.ar2, fc.nai2), mine[j]);
+        }
+      } else {  // last, partial chunk: predicated (keeps xr in registers)
+#pragma unroll
+        for (int j = kTile - 1; j >= 0; --j) {
+          if (j < rows) {
+            mine[j] = ps_emit(as, fc.br2, fc.nbi2);
+            ps_advance(as, xr[j], fc);
+          }
+        }
+#pragma unroll
+        for (int j = 0; j < kTile; ++j) {
+          if (j < rows) {
+            ps_advance(cs, xr[j], fc);
+            mine[j] = add2(ps_emit(cs, fc.ar2, fc.nai2), mine[j]);
+          }
         }
       }
     }
     __syncthreads();
-    // write-out: warp handles (gg, c) rows of the stage; lanes = rows
-    const int warp = g, nwarps = pairs;
-    if (lane < rows)
-      for (int q = warp; q < pairs * 32; q += nwarps) {
-        const int gg = q >> 5, c = q & 31;
-        if (c < cols) V[((size_t)gg * w + x0 + c) * h_pad + y0 + lane] = stage[((size_t)gg * 32 + c) * 33 + lane];
-      }
+    // write-out: warp g writes its pair's 32 columns; lanes = rows
+    if (lane < rows) {
+      float2* vdst = V + ((size_t)g * w + x0) * h_pad + y0 + lane;
+      const float2* src = buf + (size_t)g * 32 * 33 + lane;
+#pragma unroll 8
+      for (int c = 0; c < cols; ++c) vdst[(size_t)c * h_pad] = src[c * 33];
+    }
     // strip aggregates for the row pass: thread (pair g, row lane)
     if (lane < rows) {
       PairState agg;
       ps_zero(agg);
-      const float2* sg = stage + (size_t)g * 32 * 33 + lane;
-#pragma unroll 8
-      for (int c = 0; c < cols; ++c)
-        ps_accum(agg, sg[c * 33], tc.wr[0][c], tc.wi[0][c], tc.wr[1][c], tc.wi[1][c]);
+      const float2* sg = buf + (size_t)g * 32 * 33 + lane;
+      if (cols == 32) {
+#pragma unroll
+        for (int c = 0; c < 32; ++c)
+          ps_accum(agg, sg[c * 33], tc.wr2[0][c], tc.wi2[0][c], tc.wr2[1][c], tc.wi2[1][c]);
+      } else {
+        for (int c = 0; c < cols; ++c)
+          ps_accum(agg, sg[c * 33], tc.wr2[0][c], tc.wi2[0][c], tc.wr2[1][c], tc.wi2[1][c]);
+      }
       ps_store(AH + ((size_t)strip * pairs + g) * h * 2 + (size_t)(y0 + lane) * 2, agg);
     }
-    __syncthreads();
   }
 }
 
@@ -316,8 +347,8 @@ __global__ void __launch_bounds__(1024) k_row_scan(const float2* __restrict__ V_
   for (int b = nx - 1; b >= 1; --b) {
     PairState agg;
     ps_load(agg, AH + (size_t)b * sstride + off);
-    if (b == nx - 1) ps_chain(C, agg, tc.pXr, tc.pXi);
-    else ps_chain(C, agg, tc.pTr, tc.pTi);
+    if (b == nx - 1) ps_chain(C, agg, tc.pXr2, tc.pXi2);
+    else ps_chain(C, agg, tc.pTr2, tc.pTi2);
     ps_store(CH + (size_t)(b - 1) * sstride + off, C);
   }
 }
@@ -334,13 +365,13 @@ __global__ void __launch_bounds__(1024) k_row_scan(const float2* __restrict__ V_
 // ----------------------------------------------------------------------------
 template <int MAXT, typename Tin, typename Tout>
 __global__ void __launch_bounds__(MAXT, 1) k_rowpass(const Tin* __restrict__ in_all,
-                                                  const double* __restrict__ scalars,
-                                                  const float2* __restrict__ V_all,
-                                                  const float4* __restrict__ CH_all,
-                                                  Tout* __restrict__ out_all,
-                                                  unsigned long long* __restrict__ fb_all, int w,
-                                                  int h, int h_pad, int nx, FilterConsts fc,
-                                                  RangeConsts rc) {
+                                                     const double* __restrict__ scalars,
+                                                     const float2* __restrict__ V_all,
+                                                     const float4* __restrict__ CH_all,
+                                                     Tout* __restrict__ out_all,
+                                                     unsigned long long* __restrict__ fb_all,
+                                                     int w, int h, int h_pad, int nx, int nbuf,
+                                                     FilterConsts fc, RangeConsts rc) {
   extern __shared__ float4 smem4[];
   const int f = blockIdx.y, lane = threadIdx.x, g = threadIdx.y, pairs = blockDim.y;
   const int nthr = 32 * pairs, tid = g * 32 + lane;
@@ -348,8 +379,8 @@ __global__ void __launch_bounds__(MAXT, 1) k_rowpass(const Tin* __restrict__ in_
   const int rows = min(32, h - y0);
   const size_t tile_elems = (size_t)pairs * 32 * 32;  // float2 per buffer: [g][x][32 rows]
   float2* tiles = reinterpret_cast<float2*>(smem4);
-  Tin* ftiles = reinterpret_cast<Tin*>(tiles + 2 * tile_elems);  // [2][32 rows][33]
-  Tout* otile = reinterpret_cast<Tout*>(ftiles + 2 * 32 * 33);    // [32 rows][33]
+  Tin* ftiles = reinterpret_cast<Tin*>(tiles + nbuf * tile_elems);  // [nbuf][32 rows][33]
+  Tout* otile = reinterpret_cast<Tout*>(ftiles + nbuf * 32 * 33);    // [32 rows][33]
   __shared__ unsigned fb_shared;
   if (tid == 0) fb_shared = 0;
 
@@ -359,11 +390,11 @@ __global__ void __launch_bounds__(MAXT, 1) k_rowpass(const Tin* __restrict__ in_
   const float4* CH = CH_all + (size_t)f * nx * pairs * h * 2;
   const double t_c = scalars[2 * f];
 
-  // issue the V tile of strip b into buffer `buf`: 16-byte copies of
+  // issue the V tile of strip b into buffer `bi`: 16-byte copies of
   // [g][x][32 rows] (rows padded to h_pad, so always in bounds)
-  auto issue_tile = [&](int b, int buf) {
+  auto issue_tile = [&](int b, int bi) {
     const int xs = b * 32, ncol = min(32, w - xs);
-    float2* dst = tiles + (size_t)buf * tile_elems;
+    float2* dst = tiles + (size_t)bi * tile_elems;
     const int nchunk = pairs * 32 * 16;  // 16-byte chunks per buffer
     for (int q = tid; q < nchunk; q += nthr) {
       const int gg = q >> 9, c = (q >> 4) & 31, part = q & 15;
@@ -371,7 +402,7 @@ __global__ void __launch_bounds__(MAXT, 1) k_rowpass(const Tin* __restrict__ in_
         cp_async16(dst + ((size_t)gg * 32 + c) * 32 + part * 2,
                    V + ((size_t)gg * w + xs + c) * h_pad + y0 + part * 2);
     }
-    issue_f_tile(ftiles + buf * 32 * 33, in, w, h, xs, y0);
+    issue_f_tile(ftiles + bi * 32 * 33, in, w, h, xs, y0);
     cp_async_commit();
   };
 
@@ -380,71 +411,82 @@ __global__ void __launch_bounds__(MAXT, 1) k_rowpass(const Tin* __restrict__ in_
   ps_zero(cs);
   unsigned my_fb = 0;
   for (int b = 0; b < nx; ++b) {
-    const int cur = b & 1, xs = b * 32, cols = min(32, w - xs);
+    const int cur = nbuf == 2 ? (b & 1) : 0, xs = b * 32, cols = min(32, w - xs);
     const Tin* ftile = ftiles + cur * 32 * 33;
     cp_async_wait_all();
     __syncthreads();
-    if (b + 1 < nx) issue_tile(b + 1, cur ^ 1);
+    if (nbuf == 2 && b + 1 < nx) issue_tile(b + 1, cur ^ 1);  // double buffer: overlap
     float2* tl = tiles + (size_t)cur * tile_elems + (size_t)g * 32 * 32 + lane;  // [x*32]
     if (lane < rows) {
       PairState as;
       ps_load(as, CH + ((size_t)b * pairs + g) * h * 2 + (size_t)y * 2);
-      float2 buf[32];
+      float2 ybuf[32];
+      if (cols == 32) {
 #pragma unroll
-      for (int c = 31; c >= 0; --c) {
-        if (c < cols) {
-          buf[c] = ps_emit(as, fc.br, fc.bi);
+        for (int c = 31; c >= 0; --c) {
+          ybuf[c] = ps_emit(as, fc.br2, fc.nbi2);
           ps_advance(as, tl[c * 32], fc);
         }
-      }
+        if (b == 0) ps_set_gain(cs, tl[0], fc);
 #pragma unroll
-      for (int c = 0; c < 32; ++c) {
-        if (c < cols) {
-          const float2 xv = tl[c * 32];
-          if (b == 0 && c == 0) ps_set_gain(cs, xv, fc);
-          ps_advance(cs, xv, fc);
-          const float2 o = ps_emit(cs, fc.ar, fc.ai);
-          tl[c * 32] = make_float2(o.x + buf[c].x, o.y + buf[c].y);
+        for (int c = 0; c < 32; ++c) {
+          ps_advance(cs, tl[c * 32], fc);
+          tl[c * 32] = add2(ps_emit(cs, fc.ar2, fc.nai2), ybuf[c]);
+        }
+      } else {
+#pragma unroll
+        for (int c = 31; c >= 0; --c) {
+          if (c < cols) {
+            ybuf[c] = ps_emit(as, fc.br2, fc.nbi2);
+            ps_advance(as, tl[c * 32], fc);
+          }
+        }
+        if (b == 0) ps_set_gain(cs, tl[0], fc);
+#pragma unroll
+        for (int c = 0; c < 32; ++c) {
+          if (c < cols) {
+            ps_advance(cs, tl[c * 32], fc);
+            tl[c * 32] = add2(ps_emit(cs, fc.ar2, fc.nai2), ybuf[c]);
+          }
         }
       }
     }
     __syncthreads();
-    // contraction: pixel (row r = p & 31, col c = p >> 5)
+    // contraction: pixel (row r = p & 31, col c = p >> 5); (Q, P) packed
     const float2* tb = tiles + (size_t)cur * tile_elems;
     for (int p = tid; p < 1024; p += nthr) {
       const int r = p & 31, c = p >> 5;
       if (r < rows && c < cols) {
         const double fv = static_cast<double>(ftile[r * 33 + c]);
         const float Hf = static_cast<float>((fv - t_c) * rc.inv_sr);
-        float cc = rc.c0, P = 0.f, Q = 0.f;
-        float2 curv = tb[(size_t)c * 32 + r];
-        for (int gg = 0; gg < pairs; ++gg) {
-          const int n = 2 * gg;
-          const float2 nxt = (gg + 1 < pairs) ? tb[((size_t)(gg + 1) * 32 + c) * 32 + r]
-                                              : make_float2(0.f, 0.f);
-          if (n <= rc.degree) {
-            Q = fmaf(cc, curv.x, Q);
-            P = fmaf(cc, curv.y, P);
-            cc = cc * (Hf * rc.w_step[n]);
-          }
-          if (n + 1 <= rc.degree) {
-            Q = fmaf(cc, curv.y, Q);
-            P = fmaf(cc, nxt.x, P);
-            cc = cc * (Hf * rc.w_step[n + 1]);
-          }
-          curv = nxt;
+        float cc = rc.c0;
+        float2 qp = make_float2(0.f, 0.f);  // (Q, P)
+        const float2* col = tb + (size_t)c * 32 + r;
+        float2 cur2 = col[0];
+        // pairs g with both n = 2g and 2g+1 <= N; pair `full` always exists
+        const int full = (rc.degree + 1) >> 1;
+#pragma unroll 4
+        for (int gg = 0; gg < full; ++gg) {
+          const float2 nxt = col[(size_t)(gg + 1) * 1024];
+          qp = fma2(f2(cc), cur2, qp);
+          cc = cc * (Hf * rc.w_step[2 * gg]);
+          qp = fma2(f2(cc), make_float2(cur2.y, nxt.x), qp);
+          cc = cc * (Hf * rc.w_step[2 * gg + 1]);
+          cur2 = nxt;
         }
+        if (!(rc.degree & 1)) qp = fma2(f2(cc), cur2, qp);  // n = N (even N)
         double o;
-        if (!(fabsf(Q) > rc.q_thresh)) {
+        if (!(fabsf(qp.x) > rc.q_thresh)) {
           o = fv;
           ++my_fb;
         } else {
-          o = rc.sigma_r * ((static_cast<double>(P) * rc.p_scale) / static_cast<double>(Q)) + t_c;
+          o = rc.sigma_r * ((static_cast<double>(qp.y) * rc.p_scale) / static_cast<double>(qp.x)) + t_c;
         }
         otile[r * 33 + c] = static_cast<Tout>(o);
       }
     }
     __syncthreads();
+    if (nbuf == 1 && b + 1 < nx) issue_tile(b + 1, 0);  // single buffer (large N)
     for (int p = tid; p < 1024; p += nthr) {
       const int r = p >> 5, c = p & 31;
       if (r < rows && c < cols) out[(size_t)(y0 + r) * w + xs + c] = otile[r * 33 + c];
@@ -531,12 +573,16 @@ static void check(cudaError_t e, const char* what) {
 
 template <typename Tin>
 static size_t colpass_smem(int pairs) {
-  return sizeof(float2) * (kTile * 32 + (size_t)pairs * 32 * 33) + sizeof(Tin) * 2 * 32 * 33;
+  return sizeof(float2) * (size_t)pairs * 32 * 33 + sizeof(Tin) * 2 * 32 * 33;
 }
 template <typename Tin, typename Tout>
-static size_t rowpass_smem(int pairs) {
-  return sizeof(float2) * 2 * (size_t)pairs * 32 * 32 + sizeof(Tin) * 2 * 32 * 33 +
+static size_t rowpass_smem(int pairs, int nbuf) {
+  return (sizeof(float2) * (size_t)pairs * 32 * 32 + sizeof(Tin) * 32 * 33) * nbuf +
          sizeof(Tout) * 32 * 33;
+}
+template <typename Tin, typename Tout>
+static int rowpass_nbuf(int pairs) {
+  return rowpass_smem<Tin, Tout>(pairs, 2) <= 227 * 1024 ? 2 : 1;
 }
 
 void run_gaussian_f64(const double* d_in, double* d_out, double* d_tmp, int w, int h,
@@ -557,7 +603,7 @@ void plan_init(Plan& plan, const Params& p, int device, int batch) {
   plan.tc = make_tile_consts(p.sigma_s, p.width, p.height);
   plan.rc = make_range_consts(p);
   const int pairs = plan.rc.pairs;
-  if (rowpass_smem<double, double>(pairs) > 227 * 1024 || colpass_smem<double>(pairs) > 227 * 1024)
+  if (rowpass_smem<double, double>(pairs, 1) > 227 * 1024 || colpass_smem<double>(pairs) > 227 * 1024)
     throw Error{1, "RangeParams: degree must be <= 48 in the B200 library"};
   const int w = p.width, h = p.height, B = plan.batch;
   plan.ny = (h + kTile - 1) / kTile;
@@ -606,22 +652,25 @@ static void launch_passes(Plan& plan, const Tin* d_in, Tout* d_out, int count,
                           unsigned long long* d_fb, cudaStream_t st) {
   const int w = plan.p.width, h = plan.p.height, pairs = plan.rc.pairs;
   const int h_pad = plan.ny * kTile;
-  check(cudaFuncSetAttribute(k_colpass<MAXT, Tin>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             (int)colpass_smem<Tin>(pairs)),
+  const int csm = (int)colpass_smem<Tin>(pairs);
+  const int nbuf = rowpass_nbuf<Tin, Tout>(pairs);
+  const int rsm = (int)rowpass_smem<Tin, Tout>(pairs, nbuf);
+  check(cudaFuncSetAttribute(k_col_carry<MAXT, Tin>, cudaFuncAttributeMaxDynamicSharedMemorySize, csm),
         "cudaFuncSetAttribute");
-  check(cudaFuncSetAttribute(k_rowpass<MAXT, Tin, Tout>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             (int)rowpass_smem<Tin, Tout>(pairs)),
+  check(cudaFuncSetAttribute(k_colpass<MAXT, Tin>, cudaFuncAttributeMaxDynamicSharedMemorySize, csm),
+        "cudaFuncSetAttribute");
+  check(cudaFuncSetAttribute(k_rowpass<MAXT, Tin, Tout>, cudaFuncAttributeMaxDynamicSharedMemorySize, rsm),
         "cudaFuncSetAttribute");
   const dim3 blk(32, pairs);
-  k_col_carry<MAXT, Tin><<<dim3(plan.nx, count), blk, 0, st>>>(d_in, plan.scalars, plan.CA, w, h,
-                                                               plan.ny, plan.fc, plan.tc, plan.rc);
-  k_colpass<MAXT, Tin><<<dim3(plan.nx, count), blk, colpass_smem<Tin>(pairs), st>>>(
+  k_col_carry<MAXT, Tin><<<dim3(plan.nx, count), blk, csm, st>>>(d_in, plan.scalars, plan.CA, w, h,
+                                                                 plan.ny, plan.fc, plan.tc, plan.rc);
+  k_colpass<MAXT, Tin><<<dim3(plan.nx, count), blk, csm, st>>>(
       d_in, plan.scalars, plan.CA, plan.V, plan.AH, w, h, h_pad, plan.ny, plan.nx, plan.fc, plan.tc,
       plan.rc);
   k_row_scan<<<dim3(plan.ny, count), blk, 0, st>>>(plan.V, plan.AH, plan.CH, w, h, h_pad, plan.nx,
                                                    plan.fc, plan.tc);
-  k_rowpass<MAXT, Tin, Tout><<<dim3(plan.ny, count), blk, rowpass_smem<Tin, Tout>(pairs), st>>>(
-      d_in, plan.scalars, plan.V, plan.CH, d_out, d_fb, w, h, h_pad, plan.nx, plan.fc, plan.rc);
+  k_rowpass<MAXT, Tin, Tout><<<dim3(plan.ny, count), blk, rsm, st>>>(
+      d_in, plan.scalars, plan.V, plan.CH, d_out, d_fb, w, h, h_pad, plan.nx, nbuf, plan.fc, plan.rc);
 }
 
 template <typename Tin, typename Tout>
