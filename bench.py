@@ -1,0 +1,352 @@
+#!/usr/bin/env python3
+"""Benchmark of the B200 GPF hot path (BASELINE.json metric: Mpixel/s of the
+sigma_s-independent Gauss-polynomial bilateral filter, and % of roofline).
+
+Workload (BASELINE config 3): one 8192x8192 fp32 frame of the seeded
+generator (1024 rectangles, noise 10), sigma_r 30, N = 20, recursive backend,
+mean centering; a STEP filters it at every sigma_s of the sweep
+{2, 5, 10, 20, 50} (5 frames = 335.5 Mpixel per GPU), one plan and stream per
+sigma_s. Inputs are 256 MiB per frame (> 126 MB L2), so no L2 flush is needed.
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl b200|reference]
+
+N > 1 runs one process per GPU under torch.distributed.run (weak scaling:
+every rank filters its own frame sweep; no collective on the data path);
+time = max over ranks of the CUDA-event time of the K steps.
+
+--impl reference times the reference's own CPU implementation
+(oracle/_ref/libgpfilter_ref.so, compiled unmodified from the reference
+sources; the oracle port if that build is absent) on the box's host cores, on
+a bounded sample of the same workload (one 1024x1024 frame of the generator at
+each sigma_s per step).
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import tempfile
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "Mpixel/s of Gauss-poly bilateral (sigma_s-independent) and % of HBM/FP32 roofline"
+UNIT = "Mpixel/s"
+CFG_ID = 3
+SAMPLE_W = SAMPLE_H = 1024
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", choices=["b200", "reference"], default="b200")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    return ap.parse_args()
+
+
+def dist_env():
+    return (int(os.environ.get("RANK", 0)), int(os.environ.get("WORLD_SIZE", 1)),
+            int(os.environ.get("LOCAL_RANK", 0)))
+
+
+def relaunch_under_torchrun(args):
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
+           f"--nproc-per-node={args.gpus}", "--master-addr", "127.0.0.1", "--master-port", "29531",
+           os.path.abspath(__file__)] + sys.argv[1:]
+    sys.exit(subprocess.call(cmd))
+
+
+# ------------------------------------------------------------------ clocks
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled during the timed region."""
+    FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
+              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+              "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu: int):
+        self.gpu = gpu
+        self.proc = None
+        self.path = None
+
+    def start(self):
+        fd, self.path = tempfile.mkstemp(suffix=".csv")
+        os.close(fd)
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.gpu), f"--query-gpu={self.FIELDS}",
+                 "--format=csv,noheader,nounits", "-lms", "50"],
+                stdout=open(self.path, "w"), stderr=subprocess.DEVNULL)
+        except OSError:
+            self.proc = None
+        time.sleep(0.3)
+
+    def stop(self) -> dict:
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        time.sleep(0.1)
+        self.proc.terminate()
+        self.proc.wait()
+        sm, smax, reasons = [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for line in open(self.path):
+            parts = [p.strip() for p in line.split(",")]
+            if len(parts) < 7:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                smax.append(float(parts[1]))
+            except ValueError:
+                continue
+            for n, v in zip(names, parts[3:7]):
+                if v.lower().startswith("active"):
+                    reasons.add(n)
+        os.unlink(self.path)
+        # samples under load: the timed region keeps the GPU busy throughout
+        return {"sm_mhz": statistics.median(sm) if sm else None,
+                "sm_max_mhz": max(smax) if smax else None,
+                "samples": len(sm), "reasons": sorted(reasons)}
+
+
+# ------------------------------------------------------------- CPU leg
+def cpu_threads() -> int:
+    try:
+        return len(os.sched_getaffinity(0))
+    except AttributeError:
+        return os.cpu_count() or 1
+
+
+def cpu_reference_run(sigmas, sigma_r, degree, steps, threads):
+    """Times the reference CPU implementation on the bounded sample; returns
+    (Mpix/s, seconds per step, kind)."""
+    import numpy as np
+
+    from oracle.oracle import LIB_REF, Oracle, Reference
+    from paper_1505_00077_b200 import synth
+    img = synth.rects_image(SAMPLE_W, SAMPLE_H, 16, 10.0, CFG_ID * 1000 + 7).astype(np.float64)
+    if os.path.exists(LIB_REF):
+        ref = Reference()
+        ref.set_num_threads(threads)
+        kind = "reference"
+
+        def one(ss):
+            st, _, _ = ref.gpf(img, ss, sigma_r, degree)
+            assert st == 0
+    else:
+        orc = Oracle()
+        kind = "port"
+
+        def one(ss):
+            orc.gpf(img, ss, sigma_r, degree, threads=threads)
+    times = []
+    for _ in range(steps):
+        t0 = time.perf_counter()
+        for ss in sigmas:
+            one(ss)
+        times.append(time.perf_counter() - t0)
+    per_step = statistics.median(times)
+    return len(sigmas) * SAMPLE_W * SAMPLE_H / per_step / 1e6, per_step, kind
+
+
+def algorithmic_bytes_per_px(pairs: int) -> dict:
+    """HBM bytes each stage must move per pixel (fp32 frames, N+2 = 2*pairs
+    planes, carries every 32 samples: 32 B per (pair, line, chunk))."""
+    return {"mean": 4, "col_carry": 4 + pairs, "colpass": 4 + 10 * pairs, "row_scan": 2 * pairs,
+            "rowpass": 9 * pairs + 8}
+
+
+# ------------------------------------------------------------- B200 leg
+def bench_b200(args):
+    import numpy as np
+    import torch
+
+    from paper_1505_00077_b200 import gpf, synth
+
+    rank, world, local = dist_env()
+    torch.cuda.set_device(local)
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    cfg = synth.CONFIGS[CFG_ID]
+    W, H, sigmas, sr, N = cfg.width, cfg.height, cfg.sigma_s, cfg.sigma_r, cfg.degree
+    img = synth.make(cfg)
+    px = W * H
+    d_in = torch.from_numpy(img).cuda()
+    plans = [gpf.Plan(W, H, s, sr, N) for s in sigmas]
+    outs = [torch.empty_like(d_in) for _ in sigmas]
+    d_fb = torch.zeros(len(sigmas), dtype=torch.int64, device="cuda")
+    streams = [torch.cuda.Stream() for _ in sigmas]
+    main = torch.cuda.current_stream()
+
+    def step():
+        for i, (plan, out, st) in enumerate(zip(plans, outs, streams)):
+            st.wait_stream(main)
+            plan.filter_device(d_in, out, 1, d_fb[i:i + 1], st.cuda_stream)
+        for st in streams:
+            main.wait_stream(st)
+
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+    if world > 1:
+        torch.distributed.barrier()
+    torch.cuda.synchronize()
+    clocks = ClockSampler(local)
+    clocks.start()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(main)
+    for _ in range(args.steps):
+        step()
+    e1.record(main)
+    torch.cuda.synchronize()
+    ms = e0.elapsed_time(e1)
+    clk = clocks.stop()
+    if world > 1:
+        t = torch.tensor([ms], device="cuda")
+        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+        ms = float(t.item())
+        torch.distributed.barrier()
+    ms_step = ms / args.steps
+    frames = len(sigmas)
+    value = world * frames * px / (ms_step / 1e3) / 1e6
+    fallbacks = d_fb.cpu().tolist()
+
+    # sigma_s independence: each plan alone on one stream
+    per_sigma = {}
+    for s, plan, out in zip(sigmas, plans, outs):
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        plan.filter_device(d_in, out, 1, None, main.cuda_stream)
+        a.record(main)
+        for _ in range(3):
+            plan.filter_device(d_in, out, 1, None, main.cuda_stream)
+        b.record(main)
+        torch.cuda.synchronize()
+        per_sigma[f"{s:g}"] = round(a.elapsed_time(b) / 3, 4)
+
+    # per-stage timing of one plan (sigma_s = 5) on one stream: dominant kernel
+    p5 = plans[sigmas.index(5.0)]
+    p5.set_profiling(True)
+    reps = max(3, min(args.steps, 10))
+    for _ in range(reps):
+        p5.filter_device(d_in, outs[0], 1, None, main.cuda_stream)
+    torch.cuda.synchronize()
+    stage_ms = {k: v / reps for k, v in p5.stage_times().items()}
+    p5.set_profiling(False)
+    pairs = (N + 3) // 2
+    bpp = algorithmic_bytes_per_px(pairs)
+    dom = max(stage_ms, key=stage_ms.get)
+    peaks = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json"))) if os.path.exists(
+        os.path.join(ROOT, "MEASURED_PEAKS.json")) else {}
+    hbm_peak = peaks.get("hbm_gbs", 6650.0)
+    achieved = bpp[dom] * px / (stage_ms[dom] / 1e3) / 1e9
+    traffic = None
+    tpath = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+    if os.path.exists(tpath):
+        t = json.load(open(tpath))
+        if t.get("width") == W and t.get("height") == H and dom in t.get("bytes_per_launch", {}):
+            traffic = t["bytes_per_launch"][dom]
+    # whole-step view against the SURVEY 8(d) model: 8(N+2)+12 B/px at HBM peak
+    model_bpp = 8 * (N + 2) + 12
+    model_frac = (model_bpp * px * frames / (ms_step / 1e3) / 1e9) / hbm_peak
+
+    # end to end through the C ABI: pinned host fp32 in -> host fp32 out
+    h_in = torch.from_numpy(img).pin_memory()
+    h_out = torch.empty_like(h_in).pin_memory()
+    h_in_np, h_out_np = h_in.numpy(), h_out.numpy()
+    for plan in plans:
+        plan.filter_host(h_in_np, h_out_np)
+    e2e_steps = max(2, min(args.steps, 5))
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    for _ in range(e2e_steps):
+        for plan in plans:
+            plan.filter_host(h_in_np, h_out_np)
+    e2e_s = (time.perf_counter() - t0) / e2e_steps
+    if world > 1:
+        t = torch.tensor([e2e_s], device="cuda")
+        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+        e2e_s = float(t.item())
+    e2e = {"value": round(world * frames * px / e2e_s / 1e6, 1), "unit": UNIT,
+           "h2d_bytes_per_step": frames * px * 4, "d2h_bytes_per_step": frames * px * 4 + frames * 8,
+           "api": "gpf_b200_filter_f32_host (pinned host fp32 in/out, one call per sigma_s)"}
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        thr = cpu_threads()
+        v, sec, kind = cpu_reference_run(sigmas, sr, N, 1, thr)
+        cpu = {"value": round(v, 3), "unit": UNIT, "cores": thr, "kind": kind,
+               "sample": f"{SAMPLE_W}x{SAMPLE_H} generator frame at sigma_s {list(sigmas)}, "
+                         f"sigma_r {sr}, N {N} ({sec:.1f} s of CPU work)"}
+
+    launches = args.steps * frames * plans[0].launches_per_frame
+    line = {
+        "metric": METRIC, "value": round(value, 1), "unit": UNIT, "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms_step, 4),
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "fp32",
+        "data": "synthetic (seeded generator, SURVEY.md 8(d))",
+        "config": {"workload": f"C3: {W}x{H} fp32 rects1024 noise10, sigma_r {sr}, N {N}, "
+                               f"sigma_s sweep {list(sigmas)} = {frames} frames/step/GPU",
+                   "frames_per_step_per_gpu": frames, "pixels_per_frame": px,
+                   "l2": "inputs larger than L2 (256 MiB per frame, 126 MB L2); no flush",
+                   "parallelism": f"frame replicas x{world}, no collective"},
+        "sigma_s_ms_per_frame": per_sigma,
+        "stage_ms_per_frame": {k: round(v, 4) for k, v in stage_ms.items()},
+        "roofline": {"bound": "hbm", "kernel": dom, "achieved": round(achieved, 1),
+                     "peak": hbm_peak, "unit": "GB/s", "frac": round(achieved / hbm_peak, 4),
+                     "traffic": traffic, "algorithmic_bytes_per_px": bpp[dom],
+                     "peak_source": "MEASURED_PEAKS.json hbm_gbs (burst copy)",
+                     "step_model_frac": round(model_frac, 4),
+                     "step_model": f"SURVEY 8(d): {model_bpp} B/px at HBM peak"},
+        "e2e": e2e,
+        "cpu_baseline": cpu,
+        "gpu_launches": launches,
+        "fallbacks": fallbacks,
+        "clocks": clk,
+    }
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        torch.distributed.destroy_process_group()
+
+
+def bench_reference(args):
+    rank, world, _ = dist_env()
+    if rank != 0:
+        return
+    from paper_1505_00077_b200 import synth
+    cfg = synth.CONFIGS[CFG_ID]
+    thr = cpu_threads()
+    cpu_reference_run(cfg.sigma_s, cfg.sigma_r, cfg.degree, args.warmup, thr) if args.warmup else None
+    v, sec, kind = cpu_reference_run(cfg.sigma_s, cfg.sigma_r, cfg.degree, args.steps, thr)
+    line = {
+        "impl": "reference", "metric": METRIC, "value": round(v, 3), "unit": UNIT, "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(sec * 1e3, 1),
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "fp64",
+        "data": "synthetic (seeded generator, SURVEY.md 8(d))",
+        "config": {"workload": f"C3 sample: {SAMPLE_W}x{SAMPLE_H} generator frame, sigma_r "
+                               f"{cfg.sigma_r}, N {cfg.degree}, sigma_s sweep {list(cfg.sigma_s)}",
+                   "parallelism": f"{thr} host threads (gpf_set_num_threads)"},
+        "cpu_baseline": {"value": round(v, 3), "unit": UNIT, "cores": thr, "kind": kind,
+                         "sample": f"{SAMPLE_W}x{SAMPLE_H} x {len(cfg.sigma_s)} sigma_s per step"},
+        "e2e": {"value": round(v, 3), "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+def main():
+    args = parse()
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        relaunch_under_torchrun(args)
+    if args.impl == "reference":
+        bench_reference(args)
+    else:
+        bench_b200(args)
+
+
+if __name__ == "__main__":
+    main()

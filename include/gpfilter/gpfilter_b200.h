@@ -33,6 +33,14 @@ void gpf_b200_plan_destroy(gpf_b200_plan* plan);
  * batching is what fills the 148 SMs for small frames (e.g. 3840x2160). */
 gpf_status gpf_b200_plan_set_batch(gpf_b200_plan* plan, int frames);
 
+/* Per-stage timing for benchmarks: when enabled, every launch group records
+ * CUDA events between its kernels on the launching stream. stage_times
+ * synchronises those events and returns, per stage (0 mean, 1 column
+ * carries, 2 column pass, 3 row-carry scan, 4 row pass + contraction), the
+ * milliseconds accumulated since profiling was (re)enabled. */
+gpf_status gpf_b200_plan_set_profiling(gpf_b200_plan* plan, int enable);
+int gpf_b200_plan_stage_times(gpf_b200_plan* plan, float* ms, int max_stages);
+
 /* Bytes of device workspace held by the plan. */
 size_t gpf_b200_plan_workspace_bytes(const gpf_b200_plan* plan);
 

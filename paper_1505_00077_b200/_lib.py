@@ -31,7 +31,7 @@ EXPORTED = (
     "gpf_filter_gpf", "gpf_gaussian_recursive",
     "gpf_set_num_threads", "gpf_get_num_threads",
     "gpf_b200_plan_create", "gpf_b200_plan_destroy", "gpf_b200_plan_set_batch",
-    "gpf_b200_plan_workspace_bytes",
+    "gpf_b200_plan_set_profiling", "gpf_b200_plan_stage_times", "gpf_b200_plan_workspace_bytes",
     "gpf_b200_plan_launches_per_frame", "gpf_b200_filter_f32", "gpf_b200_filter_f32_host",
 )
 
@@ -77,6 +77,8 @@ def _declare(lib: C.CDLL) -> C.CDLL:
                                          C.POINTER(RangeParams), C.c_int, C.c_int, pvp]
     lib.gpf_b200_plan_destroy.argtypes = [vp]
     lib.gpf_b200_plan_set_batch.argtypes = [vp, C.c_int]
+    lib.gpf_b200_plan_set_profiling.argtypes = [vp, C.c_int]
+    lib.gpf_b200_plan_stage_times.argtypes = [vp, C.POINTER(C.c_float), C.c_int]
     lib.gpf_b200_plan_workspace_bytes.restype = C.c_size_t
     lib.gpf_b200_plan_workspace_bytes.argtypes = [vp]
     lib.gpf_b200_plan_launches_per_frame.argtypes = [vp]

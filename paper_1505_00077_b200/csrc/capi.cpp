@@ -282,6 +282,7 @@ void gpf_b200_plan_destroy(gpf_b200_plan* plan) {
   int prev = 0;
   cudaGetDevice(&prev);
   cudaSetDevice(plan->plan.device);
+  gpfb::stage_reset(plan->plan);
   gpfb::plan_free(plan->plan);
   cudaFree(plan->d_fb);
   cudaFree(plan->d_stage_in);
@@ -301,6 +302,24 @@ gpf_status gpf_b200_plan_set_batch(gpf_b200_plan* plan, int frames) {
     gpfb::plan_free(plan->plan);
     gpfb::plan_init(plan->plan, p, dev, frames);
   });
+}
+
+gpf_status gpf_b200_plan_set_profiling(gpf_b200_plan* plan, int enable) {
+  if (plan == nullptr) return fail(GPF_ERR_INVALID_ARGUMENT, "null argument");
+  return guarded([&] {
+    gpfb::stage_reset(plan->plan);
+    plan->plan.profile = enable != 0;
+  });
+}
+
+int gpf_b200_plan_stage_times(gpf_b200_plan* plan, float* ms, int max_stages) {
+  if (plan == nullptr || ms == nullptr || max_stages <= 0) return 0;
+  try {
+    return gpfb::stage_times(plan->plan, ms, max_stages);
+  } catch (const gpfb::Error& e) {
+    fail(static_cast<gpf_status>(e.status), e.msg);
+    return 0;
+  }
 }
 
 size_t gpf_b200_plan_workspace_bytes(const gpf_b200_plan* plan) { return plan ? plan->plan.bytes : 0; }

@@ -99,7 +99,17 @@ struct Plan {
   size_t bytes = 0;
   int mean_blocks = 0;
   int launches_per_frame = 0;  // kernels per launch group (independent of batch)
+  // optional per-stage timing: events recorded on the launching stream
+  bool profile = false;
+  struct StageTimer* timer = nullptr;
 };
+
+// Stage ids for the profiling hook.
+enum Stage { kStageMean = 0, kStageColCarry, kStageColPass, kStageRowScan, kStageRowPass, kNumStages };
+void stage_mark(Plan& plan, int stage, cudaStream_t st);  // records "stage begins"
+void stage_end(Plan& plan, cudaStream_t st);              // records "last stage ends"
+int stage_times(Plan& plan, float* ms, int max_stages);   // accumulated ms per stage; syncs
+void stage_reset(Plan& plan);
 
 // Status-carrying error used inside the library.
 struct Error {

@@ -25,6 +25,7 @@
 //   AH [nx][pairs][h]   2xfloat4  per-strip row aggregates sum_i p^i V (K2)
 //   CH [nx][pairs][h]   2xfloat4  row anticausal carries (K3)
 #include <algorithm>
+#include <vector>
 
 #include <cuda_runtime.h>
 
@@ -170,7 +171,7 @@ __device__ __forceinline__ void produce_planes(float2* buf, const Tin* ftile, do
 // where carry(c) is the anticausal state at the last row of chunk c.
 // ----------------------------------------------------------------------------
 template <int MAXT, typename Tin>
-__global__ void __launch_bounds__(MAXT, 1) k_col_carry(const Tin* __restrict__ in_all,
+__global__ void __launch_bounds__(MAXT, 2) k_col_carry(const Tin* __restrict__ in_all,
                                                        const double* __restrict__ scalars,
                                                        float4* __restrict__ CA_all, int w, int h,
                                                        int ny, FilterConsts fc, TileConsts tc,
@@ -252,6 +253,10 @@ __global__ void __launch_bounds__(MAXT, 1) k_colpass(const Tin* __restrict__ in_
   ps_zero(cs);
   issue_f_tile(ftiles, in, w, h, x0, 0);
   cp_async_commit();
+  // anticausal carries, prefetched one chunk ahead
+  const float4* ca_ptr = CA + (size_t)g * w * 2 + (size_t)min(x, w - 1) * 2;
+  const size_t ca_stride = (size_t)pairs * w * 2;
+  float4 ca0 = __ldg(ca_ptr), ca1 = __ldg(ca_ptr + 1);
   for (int cy = 0; cy < ny; ++cy) {
     const int y0 = cy * kTile, rows = min(kTile, h - y0);
     cp_async_wait_all();
@@ -261,10 +266,17 @@ __global__ void __launch_bounds__(MAXT, 1) k_colpass(const Tin* __restrict__ in_
       cp_async_commit();
     }
     produce_planes(buf, ftiles + (cy & 1) * 32 * 33, t_c, rc);
+    PairState as;
+    as.wr[0] = make_float2(ca0.x, ca0.y);
+    as.wi[0] = make_float2(ca0.z, ca0.w);
+    as.wr[1] = make_float2(ca1.x, ca1.y);
+    as.wi[1] = make_float2(ca1.z, ca1.w);
+    if (cy + 1 < ny) {
+      ca0 = __ldg(ca_ptr + (size_t)(cy + 1) * ca_stride);
+      ca1 = __ldg(ca_ptr + (size_t)(cy + 1) * ca_stride + 1);
+    }
     __syncthreads();
     if (x < w) {
-      PairState as;
-      ps_load(as, CA + ((size_t)cy * pairs + g) * w * 2 + (size_t)x * 2);
       float2 xr[kTile];
 #pragma unroll
       for (int j = 0; j < kTile; ++j) xr[j] = mine[j];
@@ -353,149 +365,11 @@ __global__ void __launch_bounds__(1024) k_row_scan(const float2* __restrict__ V_
   }
 }
 
-// ----------------------------------------------------------------------------
-// K4: row pass (deriche_line over rows, spatial.cpp:235-239) on V, fused with
-// the P/Q recombination and normalisation (bilateral.cpp:117-148).
-// Thread (row lane, pair g). Strips of 32 columns are double-buffered into
-// smem with cp.async; per strip: anticausal sweep from the K3 carry, causal
-// sweep (carried), Fbar written back in place, then every pixel of the strip
-// contracts its N+2 planes:
-//   Q = sum_{n<=N} c_n Fbar_n,  P = sum_{n<=N} c_n Fbar_{n+1},  c_n = H^n/n!
-// (weights and planes carry compensating 2^{-+s_n} scalings).
-// ----------------------------------------------------------------------------
-template <int MAXT, typename Tin, typename Tout>
-__global__ void __launch_bounds__(MAXT, 1) k_rowpass(const Tin* __restrict__ in_all,
-                                                     const double* __restrict__ scalars,
-                                                     const float2* __restrict__ V_all,
-                                                     const float4* __restrict__ CH_all,
-                                                     Tout* __restrict__ out_all,
-                                                     unsigned long long* __restrict__ fb_all,
-                                                     int w, int h, int h_pad, int nx, int nbuf,
-                                                     FilterConsts fc, RangeConsts rc) {
-  extern __shared__ float4 smem4[];
-  const int f = blockIdx.y, lane = threadIdx.x, g = threadIdx.y, pairs = blockDim.y;
-  const int nthr = 32 * pairs, tid = g * 32 + lane;
-  const int y0 = blockIdx.x * 32, y = y0 + lane;
-  const int rows = min(32, h - y0);
-  const size_t tile_elems = (size_t)pairs * 32 * 32;  // float2 per buffer: [g][x][32 rows]
-  float2* tiles = reinterpret_cast<float2*>(smem4);
-  Tin* ftiles = reinterpret_cast<Tin*>(tiles + nbuf * tile_elems);  // [nbuf][32 rows][33]
-  Tout* otile = reinterpret_cast<Tout*>(ftiles + nbuf * 32 * 33);    // [32 rows][33]
-  __shared__ unsigned fb_shared;
-  if (tid == 0) fb_shared = 0;
+}  // namespace gpfb
 
-  const Tin* in = in_all + (size_t)f * w * h;
-  Tout* out = out_all + (size_t)f * w * h;
-  const float2* V = V_all + (size_t)f * pairs * w * h_pad;
-  const float4* CH = CH_all + (size_t)f * nx * pairs * h * 2;
-  const double t_c = scalars[2 * f];
+#include "rowpass.cuh"
 
-  // issue the V tile of strip b into buffer `bi`: 16-byte copies of
-  // [g][x][32 rows] (rows padded to h_pad, so always in bounds)
-  auto issue_tile = [&](int b, int bi) {
-    const int xs = b * 32, ncol = min(32, w - xs);
-    float2* dst = tiles + (size_t)bi * tile_elems;
-    const int nchunk = pairs * 32 * 16;  // 16-byte chunks per buffer
-    for (int q = tid; q < nchunk; q += nthr) {
-      const int gg = q >> 9, c = (q >> 4) & 31, part = q & 15;
-      if (c < ncol)
-        cp_async16(dst + ((size_t)gg * 32 + c) * 32 + part * 2,
-                   V + ((size_t)gg * w + xs + c) * h_pad + y0 + part * 2);
-    }
-    issue_f_tile(ftiles + bi * 32 * 33, in, w, h, xs, y0);
-    cp_async_commit();
-  };
-
-  issue_tile(0, 0);
-  PairState cs;
-  ps_zero(cs);
-  unsigned my_fb = 0;
-  for (int b = 0; b < nx; ++b) {
-    const int cur = nbuf == 2 ? (b & 1) : 0, xs = b * 32, cols = min(32, w - xs);
-    const Tin* ftile = ftiles + cur * 32 * 33;
-    cp_async_wait_all();
-    __syncthreads();
-    if (nbuf == 2 && b + 1 < nx) issue_tile(b + 1, cur ^ 1);  // double buffer: overlap
-    float2* tl = tiles + (size_t)cur * tile_elems + (size_t)g * 32 * 32 + lane;  // [x*32]
-    if (lane < rows) {
-      PairState as;
-      ps_load(as, CH + ((size_t)b * pairs + g) * h * 2 + (size_t)y * 2);
-      float2 ybuf[32];
-      if (cols == 32) {
-#pragma unroll
-        for (int c = 31; c >= 0; --c) {
-          ybuf[c] = ps_emit(as, fc.br2, fc.nbi2);
-          ps_advance(as, tl[c * 32], fc);
-        }
-        if (b == 0) ps_set_gain(cs, tl[0], fc);
-#pragma unroll
-        for (int c = 0; c < 32; ++c) {
-          ps_advance(cs, tl[c * 32], fc);
-          tl[c * 32] = add2(ps_emit(cs, fc.ar2, fc.nai2), ybuf[c]);
-        }
-      } else {
-#pragma unroll
-        for (int c = 31; c >= 0; --c) {
-          if (c < cols) {
-            ybuf[c] = ps_emit(as, fc.br2, fc.nbi2);
-            ps_advance(as, tl[c * 32], fc);
-          }
-        }
-        if (b == 0) ps_set_gain(cs, tl[0], fc);
-#pragma unroll
-        for (int c = 0; c < 32; ++c) {
-          if (c < cols) {
-            ps_advance(cs, tl[c * 32], fc);
-            tl[c * 32] = add2(ps_emit(cs, fc.ar2, fc.nai2), ybuf[c]);
-          }
-        }
-      }
-    }
-    __syncthreads();
-    // contraction: pixel (row r = p & 31, col c = p >> 5); (Q, P) packed
-    const float2* tb = tiles + (size_t)cur * tile_elems;
-    for (int p = tid; p < 1024; p += nthr) {
-      const int r = p & 31, c = p >> 5;
-      if (r < rows && c < cols) {
-        const double fv = static_cast<double>(ftile[r * 33 + c]);
-        const float Hf = static_cast<float>((fv - t_c) * rc.inv_sr);
-        float cc = rc.c0;
-        float2 qp = make_float2(0.f, 0.f);  // (Q, P)
-        const float2* col = tb + (size_t)c * 32 + r;
-        float2 cur2 = col[0];
-        // pairs g with both n = 2g and 2g+1 <= N; pair `full` always exists
-        const int full = (rc.degree + 1) >> 1;
-#pragma unroll 4
-        for (int gg = 0; gg < full; ++gg) {
-          const float2 nxt = col[(size_t)(gg + 1) * 1024];
-          qp = fma2(f2(cc), cur2, qp);
-          cc = cc * (Hf * rc.w_step[2 * gg]);
-          qp = fma2(f2(cc), make_float2(cur2.y, nxt.x), qp);
-          cc = cc * (Hf * rc.w_step[2 * gg + 1]);
-          cur2 = nxt;
-        }
-        if (!(rc.degree & 1)) qp = fma2(f2(cc), cur2, qp);  // n = N (even N)
-        double o;
-        if (!(fabsf(qp.x) > rc.q_thresh)) {
-          o = fv;
-          ++my_fb;
-        } else {
-          o = rc.sigma_r * ((static_cast<double>(qp.y) * rc.p_scale) / static_cast<double>(qp.x)) + t_c;
-        }
-        otile[r * 33 + c] = static_cast<Tout>(o);
-      }
-    }
-    __syncthreads();
-    if (nbuf == 1 && b + 1 < nx) issue_tile(b + 1, 0);  // single buffer (large N)
-    for (int p = tid; p < 1024; p += nthr) {
-      const int r = p >> 5, c = p & 31;
-      if (r < rows && c < cols) out[(size_t)(y0 + r) * w + xs + c] = otile[r * 33 + c];
-    }
-  }
-  if (my_fb) atomicAdd(&fb_shared, my_fb);
-  __syncthreads();
-  if (tid == 0 && fb_shared) atomicAdd(fb_all + f, (unsigned long long)fb_shared);
-}
+namespace gpfb {
 
 // ----------------------------------------------------------------------------
 // gpf_gaussian_recursive (proj/src/capi.cpp:219-228 -> spatial.cpp:220-251):
@@ -576,13 +450,8 @@ static size_t colpass_smem(int pairs) {
   return sizeof(float2) * (size_t)pairs * 32 * 33 + sizeof(Tin) * 2 * 32 * 33;
 }
 template <typename Tin, typename Tout>
-static size_t rowpass_smem(int pairs, int nbuf) {
-  return (sizeof(float2) * (size_t)pairs * 32 * 32 + sizeof(Tin) * 32 * 33) * nbuf +
-         sizeof(Tout) * 32 * 33;
-}
-template <typename Tin, typename Tout>
-static int rowpass_nbuf(int pairs) {
-  return rowpass_smem<Tin, Tout>(pairs, 2) <= 227 * 1024 ? 2 : 1;
+static size_t rowpass_smem(int pairs) {
+  return sizeof(float2) * (size_t)pairs * 32 * 32 + sizeof(Tin) * 32 * 33 + sizeof(Tout) * 32 * 33;
 }
 
 void run_gaussian_f64(const double* d_in, double* d_out, double* d_tmp, int w, int h,
@@ -603,7 +472,7 @@ void plan_init(Plan& plan, const Params& p, int device, int batch) {
   plan.tc = make_tile_consts(p.sigma_s, p.width, p.height);
   plan.rc = make_range_consts(p);
   const int pairs = plan.rc.pairs;
-  if (rowpass_smem<double, double>(pairs, 1) > 227 * 1024 || colpass_smem<double>(pairs) > 227 * 1024)
+  if (rowpass_smem<double, double>(pairs) > 227 * 1024 || colpass_smem<double>(pairs) > 227 * 1024)
     throw Error{1, "RangeParams: degree must be <= 48 in the B200 library"};
   const int w = p.width, h = p.height, B = plan.batch;
   plan.ny = (h + kTile - 1) / kTile;
@@ -653,24 +522,31 @@ static void launch_passes(Plan& plan, const Tin* d_in, Tout* d_out, int count,
   const int w = plan.p.width, h = plan.p.height, pairs = plan.rc.pairs;
   const int h_pad = plan.ny * kTile;
   const int csm = (int)colpass_smem<Tin>(pairs);
-  const int nbuf = rowpass_nbuf<Tin, Tout>(pairs);
-  const int rsm = (int)rowpass_smem<Tin, Tout>(pairs, nbuf);
+  const int rsm = (int)rowpass_smem<Tin, Tout>(pairs);
   check(cudaFuncSetAttribute(k_col_carry<MAXT, Tin>, cudaFuncAttributeMaxDynamicSharedMemorySize, csm),
         "cudaFuncSetAttribute");
   check(cudaFuncSetAttribute(k_colpass<MAXT, Tin>, cudaFuncAttributeMaxDynamicSharedMemorySize, csm),
         "cudaFuncSetAttribute");
   check(cudaFuncSetAttribute(k_rowpass<MAXT, Tin, Tout>, cudaFuncAttributeMaxDynamicSharedMemorySize, rsm),
         "cudaFuncSetAttribute");
+  check(cudaFuncSetAttribute(k_rowpass<MAXT, Tin, Tout>, cudaFuncAttributePreferredSharedMemoryCarveout,
+                             cudaSharedmemCarveoutMaxShared),
+        "cudaFuncSetAttribute");
   const dim3 blk(32, pairs);
+  stage_mark(plan, kStageColCarry, st);
   k_col_carry<MAXT, Tin><<<dim3(plan.nx, count), blk, csm, st>>>(d_in, plan.scalars, plan.CA, w, h,
                                                                  plan.ny, plan.fc, plan.tc, plan.rc);
+  stage_mark(plan, kStageColPass, st);
   k_colpass<MAXT, Tin><<<dim3(plan.nx, count), blk, csm, st>>>(
       d_in, plan.scalars, plan.CA, plan.V, plan.AH, w, h, h_pad, plan.ny, plan.nx, plan.fc, plan.tc,
       plan.rc);
+  stage_mark(plan, kStageRowScan, st);
   k_row_scan<<<dim3(plan.ny, count), blk, 0, st>>>(plan.V, plan.AH, plan.CH, w, h, h_pad, plan.nx,
                                                    plan.fc, plan.tc);
+  stage_mark(plan, kStageRowPass, st);
   k_rowpass<MAXT, Tin, Tout><<<dim3(plan.ny, count), blk, rsm, st>>>(
-      d_in, plan.scalars, plan.V, plan.CH, d_out, d_fb, w, h, h_pad, plan.nx, nbuf, plan.fc, plan.rc);
+      d_in, plan.scalars, plan.V, plan.CH, d_out, d_fb, w, h, h_pad, plan.nx, plan.fc, plan.rc);
+  stage_end(plan, st);
 }
 
 template <typename Tin, typename Tout>
@@ -679,14 +555,64 @@ static void run_frames(Plan& plan, const Tin* d_in, Tout* d_out, int count,
   if (count <= 0) return;
   if (count > plan.batch) throw Error{1, "batch larger than the plan's workspace"};
   const long long npx = (long long)plan.p.width * plan.p.height;
+  stage_mark(plan, kStageMean, st);
   k_mean_partial<Tin><<<dim3(plan.mean_blocks, count), kMeanThreads, 0, st>>>(d_in, npx, plan.partials);
   k_mean_final<<<count, kMeanThreads, 0, st>>>(plan.partials, plan.mean_blocks, npx,
                                                plan.rc.centering, plan.scalars);
   const int nthr = 32 * plan.rc.pairs;
-  if (nthr <= 384) launch_passes<384>(plan, d_in, d_out, count, d_fb, st);
+  if (nthr <= 352) launch_passes<352>(plan, d_in, d_out, count, d_fb, st);  // N <= 20
+  else if (nthr <= 384) launch_passes<384>(plan, d_in, d_out, count, d_fb, st);
   else if (nthr <= 512) launch_passes<512>(plan, d_in, d_out, count, d_fb, st);
   else launch_passes<1024>(plan, d_in, d_out, count, d_fb, st);
   check(cudaGetLastError(), "kernel launch");
+}
+
+// ---------------------------------------------------------------- profiling
+struct StageTimer {
+  struct Mark {
+    int stage;
+    cudaEvent_t ev;
+  };
+  std::vector<Mark> marks;  // in record order; stage -1 = end marker
+  float acc[kNumStages] = {};
+  int launches[kNumStages] = {};
+};
+
+void stage_mark(Plan& plan, int stage, cudaStream_t st) {
+  if (!plan.profile) return;
+  if (!plan.timer) plan.timer = new StageTimer();
+  cudaEvent_t e;
+  check(cudaEventCreate(&e), "cudaEventCreate");
+  check(cudaEventRecord(e, st), "cudaEventRecord");
+  plan.timer->marks.push_back({stage, e});
+}
+
+void stage_end(Plan& plan, cudaStream_t st) { stage_mark(plan, -1, st); }
+
+int stage_times(Plan& plan, float* ms, int max_stages) {
+  StageTimer* t = plan.timer;
+  if (t) {
+    for (size_t i = 0; i + 1 < t->marks.size(); ++i) {
+      if (t->marks[i].stage < 0) continue;
+      check(cudaEventSynchronize(t->marks[i + 1].ev), "cudaEventSynchronize");
+      float e = 0.f;
+      check(cudaEventElapsedTime(&e, t->marks[i].ev, t->marks[i + 1].ev), "cudaEventElapsedTime");
+      t->acc[t->marks[i].stage] += e;
+      t->launches[t->marks[i].stage] += 1;
+    }
+    for (auto& m : t->marks) cudaEventDestroy(m.ev);
+    t->marks.clear();
+  }
+  const int n = std::min(max_stages, static_cast<int>(kNumStages));
+  for (int i = 0; i < n; ++i) ms[i] = t ? t->acc[i] : 0.f;
+  return n;
+}
+
+void stage_reset(Plan& plan) {
+  if (!plan.timer) return;
+  for (auto& m : plan.timer->marks) cudaEventDestroy(m.ev);
+  delete plan.timer;
+  plan.timer = nullptr;
 }
 
 void run_frames_f32(Plan& plan, const float* d_in, float* d_out, int count,

@@ -140,6 +140,18 @@ class Plan:
         if batch > 1:
             _check(_lib.lib().gpf_b200_plan_set_batch(self.h, batch))
 
+    STAGES = ("mean", "col_carry", "colpass", "row_scan", "rowpass")
+
+    def set_profiling(self, enable: bool) -> None:
+        """Record CUDA events between this plan's kernels (per-stage timing)."""
+        _check(_lib.lib().gpf_b200_plan_set_profiling(self.h, 1 if enable else 0))
+
+    def stage_times(self) -> dict:
+        """Milliseconds per stage accumulated since profiling was enabled (syncs)."""
+        buf = (C.c_float * len(self.STAGES))()
+        n = _lib.lib().gpf_b200_plan_stage_times(self.h, buf, len(self.STAGES))
+        return {self.STAGES[i]: float(buf[i]) for i in range(n)}
+
     @property
     def workspace_bytes(self) -> int:
         return _lib.lib().gpf_b200_plan_workspace_bytes(self.h)
