@@ -25,8 +25,10 @@
 //   AH [nx][pairs][h]   2xfloat4  per-strip row aggregates sum_i p^i V (K2)
 //   CH [nx][pairs][h]   2xfloat4  row anticausal carries (K3)
 #include <algorithm>
+#include <string>
 #include <vector>
 
+#include <cudaTypedefs.h>
 #include <cuda_runtime.h>
 
 #include "device_common.cuh"
@@ -265,7 +267,9 @@ __global__ void __launch_bounds__(MAXT, 1) k_colpass(const Tin* __restrict__ in_
       issue_f_tile(ftiles + ((cy + 1) & 1) * 32 * 33, in, w, h, x0, y0 + kTile);
       cp_async_commit();
     }
+#ifndef GPF_DIAG_COL_NO_PROD
     produce_planes(buf, ftiles + (cy & 1) * 32 * 33, t_c, rc);
+#endif
     PairState as;
     as.wr[0] = make_float2(ca0.x, ca0.y);
     as.wi[0] = make_float2(ca0.z, ca0.w);
@@ -276,7 +280,11 @@ __global__ void __launch_bounds__(MAXT, 1) k_colpass(const Tin* __restrict__ in_
       ca1 = __ldg(ca_ptr + (size_t)(cy + 1) * ca_stride + 1);
     }
     __syncthreads();
+#ifdef GPF_DIAG_COL_NO_SWEEP
+    if (x < 0) {
+#else
     if (x < w) {
+#endif
       float2 xr[kTile];
 #pragma unroll
       for (int j = 0; j < kTile; ++j) xr[j] = mine[j];
@@ -311,14 +319,20 @@ __global__ void __launch_bounds__(MAXT, 1) k_colpass(const Tin* __restrict__ in_
     }
     __syncthreads();
     // write-out: warp g writes its pair's 32 columns; lanes = rows
+#ifndef GPF_DIAG_COL_NO_WRITE
     if (lane < rows) {
       float2* vdst = V + ((size_t)g * w + x0) * h_pad + y0 + lane;
       const float2* src = buf + (size_t)g * 32 * 33 + lane;
 #pragma unroll 8
       for (int c = 0; c < cols; ++c) vdst[(size_t)c * h_pad] = src[c * 33];
     }
+#endif
     // strip aggregates for the row pass: thread (pair g, row lane)
+#ifdef GPF_DIAG_COL_NO_HDOT
+    if (lane < 0) {
+#else
     if (lane < rows) {
+#endif
       PairState agg;
       ps_zero(agg);
       const float2* sg = buf + (size_t)g * 32 * 33 + lane;
@@ -450,8 +464,10 @@ static size_t colpass_smem(int pairs) {
   return sizeof(float2) * (size_t)pairs * 32 * 33 + sizeof(Tin) * 2 * 32 * 33;
 }
 template <typename Tin, typename Tout>
-static size_t rowpass_smem(int pairs) {
-  return sizeof(float2) * (size_t)pairs * 32 * 32 + sizeof(Tin) * 32 * 33 + sizeof(Tout) * 32 * 33;
+static int rowpass_nbuf(int pairs) {  // deepest V ring that fits in 227 KB (0: none)
+  for (int nb = kRowBufsMax; nb >= 2; --nb)
+    if (rowpass_smem_bytes<Tin, Tout>(pairs, nb) <= 227 * 1024) return nb;
+  return 0;
 }
 
 void run_gaussian_f64(const double* d_in, double* d_out, double* d_tmp, int w, int h,
@@ -472,7 +488,7 @@ void plan_init(Plan& plan, const Params& p, int device, int batch) {
   plan.tc = make_tile_consts(p.sigma_s, p.width, p.height);
   plan.rc = make_range_consts(p);
   const int pairs = plan.rc.pairs;
-  if (rowpass_smem<double, double>(pairs) > 227 * 1024 || colpass_smem<double>(pairs) > 227 * 1024)
+  if (rowpass_nbuf<double, double>(pairs) == 0 || colpass_smem<double>(pairs) > 227 * 1024)
     throw Error{1, "RangeParams: degree must be <= 48 in the B200 library"};
   const int w = p.width, h = p.height, B = plan.batch;
   plan.ny = (h + kTile - 1) / kTile;
@@ -500,6 +516,29 @@ void plan_init(Plan& plan, const Params& p, int device, int batch) {
   }
   plan.bytes = vb + cab + 2 * ahb + sizeof(double) * 2 * B * (1 + plan.mean_blocks);
   plan.launches_per_frame = 6;
+  // TMA tensor map of V for the row pass: fp32 dims (inner first)
+  // {2*h_pad, w, pairs, batch}, box {64 (= 32 rows), 32 columns, pairs, 1}
+  static PFN_cuTensorMapEncodeTiled_v12000 encode = nullptr;
+  if (!encode) {
+    cudaDriverEntryPointQueryResult q;
+    check(cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", reinterpret_cast<void**>(&encode),
+                                  cudaEnableDefault, &q),
+          "cudaGetDriverEntryPoint(cuTensorMapEncodeTiled)");
+    if (q != cudaDriverEntryPointSuccess || !encode)
+      throw Error{9, "cuTensorMapEncodeTiled unavailable"};
+  }
+  const cuuint64_t dims[4] = {(cuuint64_t)2 * h_pad, (cuuint64_t)w, (cuuint64_t)pairs, (cuuint64_t)B};
+  const cuuint64_t strides[3] = {(cuuint64_t)2 * h_pad * 4, (cuuint64_t)2 * h_pad * 4 * w,
+                                 (cuuint64_t)2 * h_pad * 4 * w * pairs};
+  const cuuint32_t box[4] = {2 * kRowBand, 32, (cuuint32_t)pairs, 1};
+  const cuuint32_t estr[4] = {1, 1, 1, 1};
+  const CUresult r = encode(&plan.vmap, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, plan.V, dims, strides, box,
+                            estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                            CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) {
+    plan_free(plan);
+    throw Error{9, "cuTensorMapEncodeTiled failed (" + std::to_string((int)r) + ")"};
+  }
 }
 
 void plan_free(Plan& plan) {
@@ -522,15 +561,16 @@ static void launch_passes(Plan& plan, const Tin* d_in, Tout* d_out, int count,
   const int w = plan.p.width, h = plan.p.height, pairs = plan.rc.pairs;
   const int h_pad = plan.ny * kTile;
   const int csm = (int)colpass_smem<Tin>(pairs);
-  const int rsm = (int)rowpass_smem<Tin, Tout>(pairs);
+  const int nbuf = rowpass_nbuf<Tin, Tout>(pairs);
+  const int rsm = (int)rowpass_smem_bytes<Tin, Tout>(pairs, nbuf);
   check(cudaFuncSetAttribute(k_col_carry<MAXT, Tin>, cudaFuncAttributeMaxDynamicSharedMemorySize, csm),
         "cudaFuncSetAttribute");
   check(cudaFuncSetAttribute(k_colpass<MAXT, Tin>, cudaFuncAttributeMaxDynamicSharedMemorySize, csm),
         "cudaFuncSetAttribute");
-  check(cudaFuncSetAttribute(k_rowpass<MAXT, Tin, Tout>, cudaFuncAttributeMaxDynamicSharedMemorySize, rsm),
-        "cudaFuncSetAttribute");
-  check(cudaFuncSetAttribute(k_rowpass<MAXT, Tin, Tout>, cudaFuncAttributePreferredSharedMemoryCarveout,
-                             cudaSharedmemCarveoutMaxShared),
+  // row-pass CTA: (pairs+1)/2 sweep warps + kAux aux warps
+  constexpr int RMAXT = MAXT <= 384 ? 384 : 640;
+  check(cudaFuncSetAttribute(k_rowpass<RMAXT, Tin, Tout>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             rsm),
         "cudaFuncSetAttribute");
   const dim3 blk(32, pairs);
   stage_mark(plan, kStageColCarry, st);
@@ -544,8 +584,10 @@ static void launch_passes(Plan& plan, const Tin* d_in, Tout* d_out, int count,
   k_row_scan<<<dim3(plan.ny, count), blk, 0, st>>>(plan.V, plan.AH, plan.CH, w, h, h_pad, plan.nx,
                                                    plan.fc, plan.tc);
   stage_mark(plan, kStageRowPass, st);
-  k_rowpass<MAXT, Tin, Tout><<<dim3(plan.ny, count), blk, rsm, st>>>(
-      d_in, plan.scalars, plan.V, plan.CH, d_out, d_fb, w, h, h_pad, plan.nx, plan.fc, plan.rc);
+  k_rowpass<RMAXT, Tin, Tout><<<dim3((h + kRowBand - 1) / kRowBand, count),
+                                dim3(32, (pairs + 1) / 2 + kAux), rsm, st>>>(
+      d_in, plan.scalars, plan.CH, d_out, d_fb, w, h, plan.nx, pairs, nbuf, plan.fc, plan.rc,
+      plan.vmap);
   stage_end(plan, st);
 }
 
