@@ -255,25 +255,48 @@ def bench_b200(args):
     model_frac = (model_bpp * px * frames / (ms_step / 1e3) / 1e9) / hbm_peak
 
     # end to end through the C ABI: pinned host fp32 in -> host fp32 out
+    # One host thread per sigma_s plan (the C call releases the GIL; each plan
+    # owns its streams), so one frame's upload/download overlaps the others'
+    # compute. Every step still moves its input H2D and its output D2H.
+    import threading
     h_in = torch.from_numpy(img).pin_memory()
-    h_out = torch.empty_like(h_in).pin_memory()
-    h_in_np, h_out_np = h_in.numpy(), h_out.numpy()
-    for plan in plans:
-        plan.filter_host(h_in_np, h_out_np)
+    h_in_np = h_in.numpy()
+    h_outs = [torch.empty_like(h_in).pin_memory() for _ in plans]
+    h_outs_np = [o.numpy() for o in h_outs]
     e2e_steps = max(2, min(args.steps, 5))
+
+    def host_run(n):
+        errs = []
+
+        def worker(plan, o):
+            try:
+                for _ in range(n):
+                    plan.filter_host(h_in_np, o)
+            except Exception as e:  # surfaced below
+                errs.append(e)
+        ths = [threading.Thread(target=worker, args=(p, o)) for p, o in zip(plans, h_outs_np)]
+        t0 = time.perf_counter()
+        for t in ths:
+            t.start()
+        for t in ths:
+            t.join()
+        if errs:
+            raise errs[0]
+        return time.perf_counter() - t0
+
+    host_run(1)
     torch.cuda.synchronize()
-    t0 = time.perf_counter()
-    for _ in range(e2e_steps):
-        for plan in plans:
-            plan.filter_host(h_in_np, h_out_np)
-    e2e_s = (time.perf_counter() - t0) / e2e_steps
+    if world > 1:
+        torch.distributed.barrier()
+    e2e_s = host_run(e2e_steps) / e2e_steps
     if world > 1:
         t = torch.tensor([e2e_s], device="cuda")
         torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
         e2e_s = float(t.item())
     e2e = {"value": round(world * frames * px / e2e_s / 1e6, 1), "unit": UNIT,
            "h2d_bytes_per_step": frames * px * 4, "d2h_bytes_per_step": frames * px * 4 + frames * 8,
-           "api": "gpf_b200_filter_f32_host (pinned host fp32 in/out, one call per sigma_s)"}
+           "api": "gpf_b200_filter_f32_host (pinned host fp32 in/out, one call per sigma_s per step, "
+                   f"{frames} host threads, one per sigma_s plan)"}
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:

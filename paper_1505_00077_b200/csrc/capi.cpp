@@ -31,8 +31,15 @@ struct gpf_b200_plan {
   gpfb::Plan plan;
   unsigned long long* d_fb = nullptr;  // per-frame counters (grown on demand)
   int d_fb_cap = 0;
-  float* d_stage_in = nullptr;         // host-entry staging (one frame)
-  float* d_stage_out = nullptr;
+  // Host-entry pipeline: two staging slots; compute on the plan's stream (or
+  // the caller's), H2D / D2H on the device's shared copy streams, so frame f+1
+  // uploads while f computes and f-1 downloads.
+  float* d_stage_in[2] = {nullptr, nullptr};
+  float* d_stage_out[2] = {nullptr, nullptr};
+  cudaStream_t s_comp = nullptr;
+  cudaEvent_t in_ready[2] = {}, computed[2] = {}, out_free[2] = {};
+  unsigned long long* h_fb = nullptr;  // pinned readback of the counters
+  int h_fb_cap = 0;
 };
 
 namespace {
@@ -131,6 +138,29 @@ struct PlanGuard {
     if (live) gpfb::plan_free(plan);
   }
 };
+
+// Host<->device copy streams shared by every plan on a device. One FIFO per
+// direction means concurrent host-entry calls (several plans, several host
+// threads) upload one frame at a time at full link speed instead of sharing
+// the link and then all computing / downloading at once; the calls then
+// stagger and the frames' copies overlap each other's compute. Never freed
+// (they live as long as the process's CUDA context).
+struct CopyStreams {
+  cudaStream_t h2d = nullptr, d2h = nullptr;
+};
+
+CopyStreams copy_streams(int device) {
+  static std::mutex mu;
+  static std::vector<CopyStreams> per_dev;
+  std::lock_guard<std::mutex> lock(mu);
+  if ((int)per_dev.size() <= device) per_dev.resize(device + 1);
+  CopyStreams& cs = per_dev[device];
+  if (!cs.h2d) {
+    cuda_check(cudaStreamCreateWithFlags(&cs.h2d, cudaStreamNonBlocking), "cudaStreamCreate");
+    cuda_check(cudaStreamCreateWithFlags(&cs.d2h, cudaStreamNonBlocking), "cudaStreamCreate");
+  }
+  return cs;
+}
 
 }  // namespace
 
@@ -285,8 +315,15 @@ void gpf_b200_plan_destroy(gpf_b200_plan* plan) {
   gpfb::stage_reset(plan->plan);
   gpfb::plan_free(plan->plan);
   cudaFree(plan->d_fb);
-  cudaFree(plan->d_stage_in);
-  cudaFree(plan->d_stage_out);
+  for (int s = 0; s < 2; ++s) {
+    cudaFree(plan->d_stage_in[s]);
+    cudaFree(plan->d_stage_out[s]);
+    if (plan->in_ready[s]) cudaEventDestroy(plan->in_ready[s]);
+    if (plan->computed[s]) cudaEventDestroy(plan->computed[s]);
+    if (plan->out_free[s]) cudaEventDestroy(plan->out_free[s]);
+  }
+  if (plan->s_comp) cudaStreamDestroy(plan->s_comp);
+  cudaFreeHost(plan->h_fb);
   cudaSetDevice(prev);
   delete plan;
 }
@@ -359,32 +396,67 @@ gpf_status gpf_b200_filter_f32_host(gpf_b200_plan* plan, const float* h_in, floa
   if (count < 0) return fail(GPF_ERR_INVALID_ARGUMENT, "count must be >= 0");
   return guarded([&] {
     cuda_check(cudaSetDevice(plan->plan.device), "cudaSetDevice");
-    auto st = static_cast<cudaStream_t>(stream);
-    const size_t npx = (size_t)plan->plan.p.width * plan->plan.p.height;
-    if (!plan->d_stage_in) {
-      cuda_check(cudaMalloc(&plan->d_stage_in, npx * sizeof(float)), "cudaMalloc");
-      cuda_check(cudaMalloc(&plan->d_stage_out, npx * sizeof(float)), "cudaMalloc");
+    if (!plan->s_comp) {
+      const unsigned fl = cudaStreamNonBlocking;
+      cuda_check(cudaStreamCreateWithFlags(&plan->s_comp, fl), "cudaStreamCreate");
+      for (int s = 0; s < 2; ++s) {
+        cuda_check(cudaEventCreateWithFlags(&plan->in_ready[s], cudaEventDisableTiming), "event");
+        cuda_check(cudaEventCreateWithFlags(&plan->computed[s], cudaEventDisableTiming), "event");
+        cuda_check(cudaEventCreateWithFlags(&plan->out_free[s], cudaEventDisableTiming), "event");
+      }
     }
+    // Null stream -> the plan's own non-blocking stream, so that host threads
+    // driving different plans overlap instead of serialising on stream 0.
+    auto st = stream ? static_cast<cudaStream_t>(stream) : plan->s_comp;
+    const CopyStreams cs = copy_streams(plan->plan.device);
+    const size_t npx = (size_t)plan->plan.p.width * plan->plan.p.height;
+    const int slots = count > 1 ? 2 : 1;
+    for (int s = 0; s < slots; ++s)
+      if (!plan->d_stage_in[s]) {
+        cuda_check(cudaMalloc(&plan->d_stage_in[s], npx * sizeof(float)), "cudaMalloc");
+        cuda_check(cudaMalloc(&plan->d_stage_out[s], npx * sizeof(float)), "cudaMalloc");
+      }
     if (plan->d_fb_cap < count) {
       cudaFree(plan->d_fb);
       cuda_check(cudaMalloc(&plan->d_fb, sizeof(unsigned long long) * std::max(count, 1)), "cudaMalloc");
       plan->d_fb_cap = std::max(count, 1);
     }
-    cuda_check(cudaMemsetAsync(plan->d_fb, 0, sizeof(unsigned long long) * count, st), "memset");
-    for (int f = 0; f < count; ++f) {
-      cuda_check(cudaMemcpyAsync(plan->d_stage_in, h_in + f * npx, npx * sizeof(float),
-                                 cudaMemcpyHostToDevice, st), "H2D");
-      gpfb::run_frames_f32(plan->plan, plan->d_stage_in, plan->d_stage_out, 1, plan->d_fb + f, st);
-      cuda_check(cudaMemcpyAsync(h_out + f * npx, plan->d_stage_out, npx * sizeof(float),
-                                 cudaMemcpyDeviceToHost, st), "D2H");
+    if (plan->h_fb_cap < count) {
+      cudaFreeHost(plan->h_fb);
+      plan->h_fb = nullptr;
+      plan->h_fb_cap = 0;
+      cuda_check(cudaMallocHost(&plan->h_fb, sizeof(unsigned long long) * count), "cudaMallocHost");
+      plan->h_fb_cap = count;
     }
-    std::vector<unsigned long long> fb(count);
+    cuda_check(cudaMemsetAsync(plan->d_fb, 0, sizeof(unsigned long long) * count, st), "memset");
+    // The staging slots belong to this plan and its previous host-entry call has
+    // completed, so the first uploads need no wait (a wait here would also hold
+    // up other plans' uploads queued behind this one on the shared stream).
+    for (int f = 0; f < count; ++f) {
+      const int s = f % slots;
+      // slot s is reused by frame f: its input is free once frame f-2 computed,
+      // its output once frame f-2 downloaded.
+      if (f >= slots) cuda_check(cudaStreamWaitEvent(cs.h2d, plan->computed[s], 0), "wait");
+      cuda_check(cudaMemcpyAsync(plan->d_stage_in[s], h_in + f * npx, npx * sizeof(float),
+                                 cudaMemcpyHostToDevice, cs.h2d), "H2D");
+      cuda_check(cudaEventRecord(plan->in_ready[s], cs.h2d), "cudaEventRecord");
+      cuda_check(cudaStreamWaitEvent(st, plan->in_ready[s], 0), "wait");
+      if (f >= slots) cuda_check(cudaStreamWaitEvent(st, plan->out_free[s], 0), "wait");
+      gpfb::run_frames_f32(plan->plan, plan->d_stage_in[s], plan->d_stage_out[s], 1, plan->d_fb + f, st);
+      cuda_check(cudaEventRecord(plan->computed[s], st), "cudaEventRecord");
+      cuda_check(cudaStreamWaitEvent(cs.d2h, plan->computed[s], 0), "wait");
+      cuda_check(cudaMemcpyAsync(h_out + f * npx, plan->d_stage_out[s], npx * sizeof(float),
+                                 cudaMemcpyDeviceToHost, cs.d2h), "D2H");
+      cuda_check(cudaEventRecord(plan->out_free[s], cs.d2h), "cudaEventRecord");
+    }
     if (count > 0)
-      cuda_check(cudaMemcpyAsync(fb.data(), plan->d_fb, sizeof(unsigned long long) * count,
+      cuda_check(cudaMemcpyAsync(plan->h_fb, plan->d_fb, sizeof(unsigned long long) * count,
                                  cudaMemcpyDeviceToHost, st), "D2H");
+    // this call's last download is the last event on out_free[(count-1)%slots]
+    if (count > 0) cuda_check(cudaEventSynchronize(plan->out_free[(count - 1) % slots]), "sync");
     cuda_check(cudaStreamSynchronize(st), "cudaStreamSynchronize");
     if (h_fallbacks)
-      for (int f = 0; f < count; ++f) h_fallbacks[f] = static_cast<long long>(fb[f]);
+      for (int f = 0; f < count; ++f) h_fallbacks[f] = static_cast<long long>(plan->h_fb[f]);
   });
 }
 

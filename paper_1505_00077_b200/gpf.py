@@ -172,6 +172,8 @@ class Plan:
         if count * self.width * self.height != a.size:
             raise ValueError("input size is not a whole number of frames")
         out = h_out if h_out is not None else np.empty_like(a)
+        if out.dtype != np.float32 or out.size != a.size or not out.flags.c_contiguous:
+            raise ValueError("h_out must be a C-contiguous float32 array of the input's size")
         fb = (C.c_longlong * max(count, 1))()
         _check(_lib.lib().gpf_b200_filter_f32_host(self.h, a.ctypes.data, out.ctypes.data, count,
                                                    fb, stream))

@@ -117,17 +117,40 @@ def test_full_size_c1_and_plan_path(gpu, oracle):
 def test_device_batch_matches_host_entry(gpu):
     import torch
     cfg = synth.scaled(synth.CONFIGS[3], 256, 192)
-    frames = np.stack([synth.rects_image(256, 192, 8, 10.0, s) for s in (1, 2, 3)])
+    # 5 frames: the host entry's two staging slots are each reused
+    frames = np.stack([synth.rects_image(256, 192, 8, 10.0, s) for s in (1, 2, 3, 4, 5)])
     plan = gpu.Plan(256, 192, 5.0, 30.0, 20)
     host_out, host_fb = plan.filter_host(frames)
     d_in = torch.from_numpy(frames).cuda()
     d_out = torch.empty_like(d_in)
-    d_fb = torch.zeros(3, dtype=torch.int64, device="cuda")
-    plan.filter_device(d_in, d_out, 3, d_fb, torch.cuda.current_stream().cuda_stream)
+    d_fb = torch.zeros(5, dtype=torch.int64, device="cuda")
+    plan.filter_device(d_in, d_out, 5, d_fb, torch.cuda.current_stream().cuda_stream)
     torch.cuda.synchronize()
     np.testing.assert_array_equal(d_out.cpu().numpy(), host_out)
     assert d_fb.cpu().tolist() == host_fb
     del cfg
+
+
+def test_host_entry_concurrent_plans(gpu):
+    """Plans driven from several host threads at once (each on its own
+    streams, as bench.py's e2e leg does) give the sequential results."""
+    import threading
+    img = synth.rects_image(320, 256, 8, 10.0, 21)
+    sig = (2.0, 5.0, 10.0, 20.0)
+    plans = [gpu.Plan(320, 256, s, 30.0, 20) for s in sig]
+    seq = [p.filter_host(np.stack([img, img]))[0] for p in plans]
+    outs = [np.empty_like(x) for x in seq]
+
+    def work(p, o):
+        for _ in range(3):
+            p.filter_host(np.stack([img, img]), o)
+    ths = [threading.Thread(target=work, args=(p, o)) for p, o in zip(plans, outs)]
+    for t in ths:
+        t.start()
+    for t in ths:
+        t.join()
+    for a, b in zip(seq, outs):
+        np.testing.assert_array_equal(a, b)
 
 
 def test_determinism(gpu):
