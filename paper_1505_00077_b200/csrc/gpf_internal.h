@@ -95,7 +95,8 @@ struct Plan {
   float4* CA = nullptr;     // [batch][ny][pairs][w][2] column anticausal carries
   float4* AH = nullptr;     // [batch][nx][pairs][h][2] row aggregates per strip
   float4* CH = nullptr;     // [batch][nx][pairs][h][2] row anticausal carries
-  alignas(64) CUtensorMap vmap;  // TMA map of V: fp32 [batch][pairs][w][2*h_pad]
+  alignas(64) CUtensorMap vmap;    // TMA map of V: fp32 [batch][pairs][w][2*h_pad] (row-pass loads)
+  alignas(64) CUtensorMap vstore;  // TMA map of V for the column pass's staged chunk stores
   double* scalars = nullptr;   // [batch][2]  t_c
   double* partials = nullptr;  // [batch][mean_blocks][2]
   size_t bytes = 0;

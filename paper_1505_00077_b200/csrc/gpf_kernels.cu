@@ -33,6 +33,7 @@
 
 #include "device_common.cuh"
 #include "gpf_internal.h"
+#include "sync.cuh"
 
 namespace gpfb {
 
@@ -147,20 +148,36 @@ __device__ __forceinline__ void issue_f_tile(Tin* ftile, const Tin* __restrict__
 // (float2 = planes 2g, 2g+1), computed once per pixel from the smem f tile
 // and shared by the `pairs` warps. Plane chain in fp32:
 //   x_0 = E 2^s0,  x_{n+1} = x_n * (H 2^-k)      (bilateral.cpp:97-101, 117-120)
+// A thread takes up to three pixels (1024 / (32 pairs) <= 3 for N <= 20) and
+// runs their chains interleaved, so the dependent multiplies overlap.
 template <typename Tin>
 __device__ __forceinline__ void produce_planes(float2* buf, const Tin* ftile, double t_c,
                                                const RangeConsts& rc) {
   const int nthr = blockDim.x * blockDim.y, pairs = blockDim.y;
   const int tid = threadIdx.y * 32 + threadIdx.x;
-  for (int p = tid; p < 1024; p += nthr) {
-    const int j = p >> 5, c = p & 31;
-    const float2 t = pixel_terms(static_cast<double>(ftile[j * 33 + c]), t_c, rc);
-    float x = t.x;
-    float2* dst = buf + c * 33 + j;
+  for (int p0 = tid; p0 < 1024; p0 += 3 * nthr) {
+    float x[3], m[3];
+    float2* dst[3];
+    bool ok[3];
+#pragma unroll
+    for (int k = 0; k < 3; ++k) {
+      const int pk = p0 + k * nthr;
+      ok[k] = pk < 1024;
+      const int pp = ok[k] ? pk : p0;
+      const int j = pp >> 5, c = pp & 31;
+      const float2 t = pixel_terms(static_cast<double>(ftile[j * 33 + c]), t_c, rc);
+      x[k] = t.x;
+      m[k] = t.y;
+      dst[k] = buf + c * 33 + j;
+    }
+#pragma unroll 2
     for (int gg = 0; gg < pairs; ++gg) {
-      const float x1 = x * t.y;
-      dst[gg * 32 * 33] = make_float2(x, x1);
-      x = x1 * t.y;
+#pragma unroll
+      for (int k = 0; k < 3; ++k) {
+        const float x1 = x[k] * m[k];
+        if (ok[k]) dst[k][gg * 32 * 33] = make_float2(x[k], x1);
+        x[k] = x1 * m[k];
+      }
     }
   }
 }
@@ -224,13 +241,229 @@ __global__ void __launch_bounds__(MAXT, 2) k_col_carry(const Tin* __restrict__ i
 
 // ----------------------------------------------------------------------------
 // K2: column pass (deriche_line over columns, spatial.cpp:240-243), fused with
-// the plane generator. Per row chunk: the producer writes every plane of the
-// 32x32 block to smem; each thread lifts its pair's 32 inputs into registers,
-// runs the anticausal sweep from the K1 carry (outputs in place in smem),
-// then the causal sweep (state carried across chunks) which adds and leaves
-// the final values in place. The chunk is then written to V transposed and
-// reduced into the row-pass strip aggregates AH.
+// the plane generator.
+//
+// k_colpass_tma (N <= 24): per 32x32 chunk the producer writes every plane
+// straight into a staging tile laid out exactly as one TMA box of V --
+// [pair][16-row half][column][16 rows x float2], 128B-swizzled -- so that
+// lanes = 32 columns touch 16-B chunks conflict-free when a thread moves two
+// rows at once. Each thread lifts its column's 32 inputs into registers, runs
+// the anticausal sweep from the K1 carry and then the causal sweep (state
+// carried across chunks), both in place in the stage; one elected thread
+// then writes the whole chunk with a single tensor store. Two stages
+// alternate, so the store of chunk k drains while chunk k+1 is produced and
+// swept. The chunk is finally reduced into the row-pass strip aggregates AH.
+//
+// k_colpass (larger N, where two stages do not fit): same sweeps on a padded
+// [pair][column][33] tile, written to V by the warps.
 // ----------------------------------------------------------------------------
+constexpr int kStageAlign = 1024;  // SWIZZLE_128B atoms repeat every 1024 B
+
+// float2 element (column of base_col, row j) of a stage tile; cm = column % 8
+__device__ __forceinline__ float* stage_at(float* base_col, int j, int cm) {
+  return base_col + (j >> 4) * 1024 + ((((j & 15) >> 1) ^ cm) << 2) + (j & 1) * 2;
+}
+
+// Producer into a stage tile for the pair group starting at plane n0 = 2*pair0:
+// item = (column, row pair); 512 items over the CTA's threads, four pixels
+// (two items) in flight per thread. x_{n0} = es m^{n0} is reached through the
+// planes x_4, x_8, ... (each in range by the plane scaling), then the chain
+// runs over the group's planes.
+template <typename Tin>
+__device__ __forceinline__ void produce_group(float* stage, const Tin* ftile, double t_c,
+                                              const RangeConsts& rc, int pair0, int npairs) {
+  const int nthr = blockDim.x * blockDim.y;
+  const int tid = threadIdx.y * 32 + threadIdx.x;
+  for (int i0 = tid; i0 < 512; i0 += 2 * nthr) {
+    float x[4], m[4];
+    float4* dst[2];
+    bool ok[2];
+#pragma unroll
+    for (int k = 0; k < 2; ++k) {
+      const int ik = i0 + k * nthr;
+      ok[k] = ik < 512;
+      const int it = ok[k] ? ik : i0;
+      const int c = it & 31, j = (it >> 5) * 2;  // rows j, j+1
+      const float2 ta = pixel_terms(static_cast<double>(ftile[j * 33 + c]), t_c, rc);
+      const float2 tb = pixel_terms(static_cast<double>(ftile[(j + 1) * 33 + c]), t_c, rc);
+      x[2 * k] = ta.x;
+      m[2 * k] = ta.y;
+      x[2 * k + 1] = tb.x;
+      m[2 * k + 1] = tb.y;
+      dst[k] = reinterpret_cast<float4*>(stage_at(stage + c * 32, j, c & 7));
+    }
+    if (pair0 > 0) {
+      float m4[4];
+#pragma unroll
+      for (int e = 0; e < 4; ++e) {
+        m4[e] = m[e] * m[e];
+        m4[e] *= m4[e];
+      }
+      for (int n = 0; n < 2 * pair0; n += 4) {
+#pragma unroll
+        for (int e = 0; e < 4; ++e) x[e] *= m4[e];
+      }
+    }
+#pragma unroll 2
+    for (int gg = 0; gg < npairs; ++gg) {
+#pragma unroll
+      for (int k = 0; k < 2; ++k) {
+        const float a1 = x[2 * k] * m[2 * k], b1 = x[2 * k + 1] * m[2 * k + 1];
+        if (ok[k]) dst[k][gg * 512] = make_float4(x[2 * k], a1, x[2 * k + 1], b1);
+        x[2 * k] = a1 * m[2 * k];
+        x[2 * k + 1] = b1 * m[2 * k + 1];
+      }
+    }
+  }
+}
+
+// One CTA = 32 columns x kColGroup pairs (pair group blockIdx.z); several
+// CTAs share an SM so one's producer / H-dot phases overlap another's sweeps.
+constexpr int kColGroup = 4;
+
+template <typename Tin>
+__global__ void __launch_bounds__(32 * kColGroup, 3) k_colpass_tma(
+    const Tin* __restrict__ in_all, const double* __restrict__ scalars,
+    const float4* __restrict__ CA_all, float4* __restrict__ AH_all, int w, int h, int ny, int nx,
+    int pairs, FilterConsts fc, TileConsts tc, RangeConsts rc,
+    const __grid_constant__ CUtensorMap vstore) {
+  extern __shared__ float4 smem4[];
+  const int f = blockIdx.y, lane = threadIdx.x, gl = threadIdx.y;
+  const int tid = gl * 32 + lane;
+  const int pair0 = blockIdx.z * kColGroup, npairs = min(kColGroup, pairs - pair0);
+  const int g = pair0 + gl;           // this warp's pair
+  const bool active = gl < npairs;
+  // smem: [2 stages x kColGroup x 8 KB, 1024-aligned][2 f tiles]. The alignment
+  // is an offset from the smem base (not integer arithmetic on the pointer) so
+  // the compiler keeps the accesses in the shared window (LDS/STS).
+  float* stages = reinterpret_cast<float*>(reinterpret_cast<char*>(smem4) +
+                                           ((kStageAlign - smem_u32(smem4)) & (kStageAlign - 1)));
+  constexpr int kStageFloats = kColGroup * 2048;
+  Tin* ftiles = reinterpret_cast<Tin*>(stages + 2 * kStageFloats);  // [2][32*33]
+  const int strip = blockIdx.x, x0 = strip * 32, x = x0 + lane;
+  const int cols = min(32, w - x0);
+  const Tin* in = in_all + (size_t)f * w * h;
+  const float4* CA = CA_all + (size_t)f * ny * pairs * w * 2;
+  float4* AH = AH_all + (size_t)f * nx * pairs * h * 2;
+  const double t_c = scalars[2 * f];
+  const int cm = lane & 7;
+  const int col_off = (gl * 64 + lane) * 32;  // this thread's column, half 0
+  // H-dots: thread (pair, row lane) reads column c at hd_off + c*32 + ((hq ^ (c%8)) << 2)
+  const int hq = (lane & 15) >> 1;
+  const int hd_off = (gl * 64 + (lane >> 4) * 32) * 32 + (lane & 1) * 2;
+  PairState cs;  // causal state, carried across chunks
+  ps_zero(cs);
+  issue_f_tile(ftiles, in, w, h, x0, 0);
+  cp_async_commit();
+  // anticausal carries, prefetched one chunk ahead
+  const float4* ca_ptr = CA + (size_t)min(g, pairs - 1) * w * 2 + (size_t)min(x, w - 1) * 2;
+  const size_t ca_stride = (size_t)pairs * w * 2;
+  float4 ca0 = __ldg(ca_ptr), ca1 = __ldg(ca_ptr + 1);
+  for (int cy = 0; cy < ny; ++cy) {
+    const int y0 = cy * kTile, rows = min(kTile, h - y0);
+    float* stage = stages + (cy & 1) * kStageFloats;
+    cp_async_wait_all();
+    if (tid == 0 && cy >= 2) {  // the store of chunk cy-2 (same stage) has read it
+      asm volatile("cp.async.bulk.wait_group.read 1;\n" ::: "memory");
+    }
+    __syncthreads();
+    if (cy + 1 < ny) {
+      issue_f_tile(ftiles + ((cy + 1) & 1) * 32 * 33, in, w, h, x0, y0 + kTile);
+      cp_async_commit();
+    }
+#ifndef GPF_DIAG_NO_PROD
+    produce_group(stage, ftiles + (cy & 1) * 32 * 33, t_c, rc, pair0, npairs);
+#endif
+    PairState as;
+    as.wr[0] = make_float2(ca0.x, ca0.y);
+    as.wi[0] = make_float2(ca0.z, ca0.w);
+    as.wr[1] = make_float2(ca1.x, ca1.y);
+    as.wi[1] = make_float2(ca1.z, ca1.w);
+    if (cy + 1 < ny) {
+      ca0 = __ldg(ca_ptr + (size_t)(cy + 1) * ca_stride);
+      ca1 = __ldg(ca_ptr + (size_t)(cy + 1) * ca_stride + 1);
+    }
+    __syncthreads();
+    float* mcol = stage + col_off;
+    if (active && x < w) {
+      float2 xr[kTile];
+#pragma unroll
+      for (int j = 0; j < kTile; j += 2) {
+        const float4 v = *reinterpret_cast<const float4*>(stage_at(mcol, j, cm));
+        xr[j] = make_float2(v.x, v.y);
+        xr[j + 1] = make_float2(v.z, v.w);
+      }
+      if (cy == 0) ps_set_gain(cs, xr[0], fc);
+      if (rows == kTile) {  // full chunk: branch-free sweeps, two rows per smem access
+#pragma unroll
+        for (int j = kTile - 1; j >= 0; j -= 2) {
+          const float2 yb = ps_emit(as, fc.br2, fc.nbi2);
+          ps_advance(as, xr[j], fc);
+          const float2 ya = ps_emit(as, fc.br2, fc.nbi2);
+          ps_advance(as, xr[j - 1], fc);
+          *reinterpret_cast<float4*>(stage_at(mcol, j - 1, cm)) = make_float4(ya.x, ya.y, yb.x, yb.y);
+        }
+#pragma unroll
+        for (int j = 0; j < kTile; j += 2) {
+          float4* p = reinterpret_cast<float4*>(stage_at(mcol, j, cm));
+          const float4 an = *p;
+          ps_advance(cs, xr[j], fc);
+          const float2 ya = add2(ps_emit(cs, fc.ar2, fc.nai2), make_float2(an.x, an.y));
+          ps_advance(cs, xr[j + 1], fc);
+          const float2 yb = add2(ps_emit(cs, fc.ar2, fc.nai2), make_float2(an.z, an.w));
+          *p = make_float4(ya.x, ya.y, yb.x, yb.y);
+        }
+      } else {  // last, partial chunk: predicated (keeps xr in registers)
+#pragma unroll
+        for (int j = kTile - 1; j >= 0; --j) {
+          if (j < rows) {
+            *reinterpret_cast<float2*>(stage_at(mcol, j, cm)) = ps_emit(as, fc.br2, fc.nbi2);
+            ps_advance(as, xr[j], fc);
+          }
+        }
+#pragma unroll
+        for (int j = 0; j < kTile; ++j) {
+          if (j < rows) {
+            float2* p = reinterpret_cast<float2*>(stage_at(mcol, j, cm));
+            ps_advance(cs, xr[j], fc);
+            *p = add2(ps_emit(cs, fc.ar2, fc.nai2), *p);
+          }
+        }
+      }
+    }
+    fence_proxy_async();  // stage writes -> visible to the TMA store
+    __syncthreads();
+#ifndef GPF_DIAG_NO_STORE
+    if (tid == 0) {  // pairs past the last one fall outside the tensor and are clipped
+      tma_store_5d(&vstore, 0, x0, y0 >> 4, pair0, f, stage);
+      bulk_commit();
+    }
+#endif
+    // strip aggregates for the row pass: thread (pair, row lane)
+#ifdef GPF_DIAG_NO_HDOT
+    if (lane < 0) {
+#else
+    if (active && lane < rows) {
+#endif
+      PairState agg;
+      ps_zero(agg);
+      const float* sb = stage + hd_off;
+      if (cols == 32) {
+#pragma unroll
+        for (int c = 0; c < 32; ++c)
+          ps_accum(agg, *reinterpret_cast<const float2*>(sb + c * 32 + ((hq ^ (c & 7)) << 2)),
+                   tc.wr2[0][c], tc.wi2[0][c], tc.wr2[1][c], tc.wi2[1][c]);
+      } else {
+        for (int c = 0; c < cols; ++c)
+          ps_accum(agg, *reinterpret_cast<const float2*>(sb + c * 32 + ((hq ^ (c & 7)) << 2)),
+                   tc.wr2[0][c], tc.wi2[0][c], tc.wr2[1][c], tc.wi2[1][c]);
+      }
+      ps_store(AH + ((size_t)strip * pairs + g) * h * 2 + (size_t)(y0 + lane) * 2, agg);
+    }
+  }
+  if (tid == 0) bulk_wait_all();  // V complete before the CTA retires
+}
+
 template <int MAXT, typename Tin>
 __global__ void __launch_bounds__(MAXT, 1) k_colpass(const Tin* __restrict__ in_all,
                                                      const double* __restrict__ scalars,
@@ -255,7 +488,6 @@ __global__ void __launch_bounds__(MAXT, 1) k_colpass(const Tin* __restrict__ in_
   ps_zero(cs);
   issue_f_tile(ftiles, in, w, h, x0, 0);
   cp_async_commit();
-  // anticausal carries, prefetched one chunk ahead
   const float4* ca_ptr = CA + (size_t)g * w * 2 + (size_t)min(x, w - 1) * 2;
   const size_t ca_stride = (size_t)pairs * w * 2;
   float4 ca0 = __ldg(ca_ptr), ca1 = __ldg(ca_ptr + 1);
@@ -267,9 +499,7 @@ __global__ void __launch_bounds__(MAXT, 1) k_colpass(const Tin* __restrict__ in_
       issue_f_tile(ftiles + ((cy + 1) & 1) * 32 * 33, in, w, h, x0, y0 + kTile);
       cp_async_commit();
     }
-#ifndef GPF_DIAG_COL_NO_PROD
     produce_planes(buf, ftiles + (cy & 1) * 32 * 33, t_c, rc);
-#endif
     PairState as;
     as.wr[0] = make_float2(ca0.x, ca0.y);
     as.wi[0] = make_float2(ca0.z, ca0.w);
@@ -280,70 +510,41 @@ __global__ void __launch_bounds__(MAXT, 1) k_colpass(const Tin* __restrict__ in_
       ca1 = __ldg(ca_ptr + (size_t)(cy + 1) * ca_stride + 1);
     }
     __syncthreads();
-#ifdef GPF_DIAG_COL_NO_SWEEP
-    if (x < 0) {
-#else
     if (x < w) {
-#endif
       float2 xr[kTile];
 #pragma unroll
       for (int j = 0; j < kTile; ++j) xr[j] = mine[j];
       if (cy == 0) ps_set_gain(cs, xr[0], fc);
-      if (rows == kTile) {  // full chunk: branch-free sweeps
 #pragma unroll
-        for (int j = kTile - 1; j >= 0; --j) {
+      for (int j = kTile - 1; j >= 0; --j) {
+        if (j < rows) {
           mine[j] = ps_emit(as, fc.br2, fc.nbi2);
           ps_advance(as, xr[j], fc);
         }
+      }
 #pragma unroll
-        for (int j = 0; j < kTile; ++j) {
+      for (int j = 0; j < kTile; ++j) {
+        if (j < rows) {
           ps_advance(cs, xr[j], fc);
           mine[j] = add2(ps_emit(cs, fc.ar2, fc.nai2), mine[j]);
-        }
-      } else {  // last, partial chunk: predicated (keeps xr in registers)
-#pragma unroll
-        for (int j = kTile - 1; j >= 0; --j) {
-          if (j < rows) {
-            mine[j] = ps_emit(as, fc.br2, fc.nbi2);
-            ps_advance(as, xr[j], fc);
-          }
-        }
-#pragma unroll
-        for (int j = 0; j < kTile; ++j) {
-          if (j < rows) {
-            ps_advance(cs, xr[j], fc);
-            mine[j] = add2(ps_emit(cs, fc.ar2, fc.nai2), mine[j]);
-          }
         }
       }
     }
     __syncthreads();
     // write-out: warp g writes its pair's 32 columns; lanes = rows
-#ifndef GPF_DIAG_COL_NO_WRITE
     if (lane < rows) {
       float2* vdst = V + ((size_t)g * w + x0) * h_pad + y0 + lane;
       const float2* src = buf + (size_t)g * 32 * 33 + lane;
 #pragma unroll 8
-      for (int c = 0; c < cols; ++c) vdst[(size_t)c * h_pad] = src[c * 33];
+      for (int c = 0; c < cols; ++c, vdst += h_pad) *vdst = src[c * 33];
     }
-#endif
     // strip aggregates for the row pass: thread (pair g, row lane)
-#ifdef GPF_DIAG_COL_NO_HDOT
-    if (lane < 0) {
-#else
     if (lane < rows) {
-#endif
       PairState agg;
       ps_zero(agg);
       const float2* sg = buf + (size_t)g * 32 * 33 + lane;
-      if (cols == 32) {
-#pragma unroll
-        for (int c = 0; c < 32; ++c)
-          ps_accum(agg, sg[c * 33], tc.wr2[0][c], tc.wi2[0][c], tc.wr2[1][c], tc.wi2[1][c]);
-      } else {
-        for (int c = 0; c < cols; ++c)
-          ps_accum(agg, sg[c * 33], tc.wr2[0][c], tc.wi2[0][c], tc.wr2[1][c], tc.wi2[1][c]);
-      }
+      for (int c = 0; c < cols; ++c)
+        ps_accum(agg, sg[c * 33], tc.wr2[0][c], tc.wi2[0][c], tc.wr2[1][c], tc.wi2[1][c]);
       ps_store(AH + ((size_t)strip * pairs + g) * h * 2 + (size_t)(y0 + lane) * 2, agg);
     }
   }
@@ -460,8 +661,12 @@ static void check(cudaError_t e, const char* what) {
 }
 
 template <typename Tin>
-static size_t colpass_smem(int pairs) {
+static size_t colpass_smem(int pairs) {  // k_colpass and k_col_carry
   return sizeof(float2) * (size_t)pairs * 32 * 33 + sizeof(Tin) * 2 * 32 * 33;
+}
+template <typename Tin>
+static size_t colpass_tma_smem() {  // two stages of a pair group + f tiles + alignment slack
+  return kStageAlign + sizeof(float) * 2 * kColGroup * 2048 + sizeof(Tin) * 2 * 32 * 33;
 }
 template <typename Tin, typename Tout>
 static int rowpass_nbuf(int pairs) {  // deepest V ring that fits in 227 KB (0: none)
@@ -539,6 +744,23 @@ void plan_init(Plan& plan, const Params& p, int device, int batch) {
     plan_free(plan);
     throw Error{9, "cuTensorMapEncodeTiled failed (" + std::to_string((int)r) + ")"};
   }
+  // Column-pass chunk store: V viewed as fp32 {32 floats = 16 rows, column,
+  // 16-row half, pair, frame} (the half stride, 128 B, is inside the column
+  // stride), box {32, 32 columns, 2 halves, kColGroup pairs, 1} = one 32x32 chunk of
+  // every pair; smem side [pair][half][column][128 B], 128B-swizzled.
+  const cuuint64_t sdims[5] = {32, (cuuint64_t)w, (cuuint64_t)h_pad / 16, (cuuint64_t)pairs,
+                               (cuuint64_t)B};
+  const cuuint64_t sstrides[4] = {(cuuint64_t)2 * h_pad * 4, 128, (cuuint64_t)2 * h_pad * 4 * w,
+                                  (cuuint64_t)2 * h_pad * 4 * w * pairs};
+  const cuuint32_t sbox[5] = {32, 32, 2, (cuuint32_t)kColGroup, 1};
+  const cuuint32_t sestr[5] = {1, 1, 1, 1, 1};
+  const CUresult r2 = encode(&plan.vstore, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 5, plan.V, sdims, sstrides,
+                             sbox, sestr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                             CU_TENSOR_MAP_L2_PROMOTION_NONE, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r2 != CUDA_SUCCESS) {
+    plan_free(plan);
+    throw Error{9, "cuTensorMapEncodeTiled (store) failed (" + std::to_string((int)r2) + ")"};
+  }
 }
 
 void plan_free(Plan& plan) {
@@ -561,11 +783,13 @@ static void launch_passes(Plan& plan, const Tin* d_in, Tout* d_out, int count,
   const int w = plan.p.width, h = plan.p.height, pairs = plan.rc.pairs;
   const int h_pad = plan.ny * kTile;
   const int csm = (int)colpass_smem<Tin>(pairs);
+  // TMA-store column pass in pair groups (the large-N builds keep the padded one)
+  constexpr bool kCanStage = MAXT <= 512;
+  const bool staged = kCanStage;
+  const int psm = (int)(staged ? colpass_tma_smem<Tin>() : colpass_smem<Tin>(pairs));
   const int nbuf = rowpass_nbuf<Tin, Tout>(pairs);
   const int rsm = (int)rowpass_smem_bytes<Tin, Tout>(pairs, nbuf);
   check(cudaFuncSetAttribute(k_col_carry<MAXT, Tin>, cudaFuncAttributeMaxDynamicSharedMemorySize, csm),
-        "cudaFuncSetAttribute");
-  check(cudaFuncSetAttribute(k_colpass<MAXT, Tin>, cudaFuncAttributeMaxDynamicSharedMemorySize, csm),
         "cudaFuncSetAttribute");
   // row-pass CTA: (pairs+1)/2 sweep warps + kAux aux warps
   constexpr int RMAXT = MAXT <= 384 ? 384 : 640;
@@ -577,9 +801,21 @@ static void launch_passes(Plan& plan, const Tin* d_in, Tout* d_out, int count,
   k_col_carry<MAXT, Tin><<<dim3(plan.nx, count), blk, csm, st>>>(d_in, plan.scalars, plan.CA, w, h,
                                                                  plan.ny, plan.fc, plan.tc, plan.rc);
   stage_mark(plan, kStageColPass, st);
-  k_colpass<MAXT, Tin><<<dim3(plan.nx, count), blk, csm, st>>>(
-      d_in, plan.scalars, plan.CA, plan.V, plan.AH, w, h, h_pad, plan.ny, plan.nx, plan.fc, plan.tc,
-      plan.rc);
+  if constexpr (kCanStage) {
+    check(cudaFuncSetAttribute(k_colpass_tma<Tin>, cudaFuncAttributeMaxDynamicSharedMemorySize, psm),
+          "cudaFuncSetAttribute");
+    const int groups = (pairs + kColGroup - 1) / kColGroup;
+    k_colpass_tma<Tin><<<dim3(plan.nx, count, groups), dim3(32, kColGroup), psm, st>>>(
+        d_in, plan.scalars, plan.CA, plan.AH, w, h, plan.ny, plan.nx, pairs, plan.fc, plan.tc, plan.rc,
+        plan.vstore);
+  }
+  if (!staged) {
+    check(cudaFuncSetAttribute(k_colpass<MAXT, Tin>, cudaFuncAttributeMaxDynamicSharedMemorySize, psm),
+          "cudaFuncSetAttribute");
+    k_colpass<MAXT, Tin><<<dim3(plan.nx, count), blk, psm, st>>>(d_in, plan.scalars, plan.CA, plan.V,
+                                                                 plan.AH, w, h, h_pad, plan.ny, plan.nx,
+                                                                 plan.fc, plan.tc, plan.rc);
+  }
   stage_mark(plan, kStageRowScan, st);
   k_row_scan<<<dim3(plan.ny, count), blk, 0, st>>>(plan.V, plan.AH, plan.CH, w, h, h_pad, plan.nx,
                                                    plan.fc, plan.tc);
