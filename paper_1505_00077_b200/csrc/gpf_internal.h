@@ -95,8 +95,11 @@ struct Plan {
   float4* CA = nullptr;     // [batch][ny][pairs][w][2] column anticausal carries
   float4* AH = nullptr;     // [batch][nx][pairs][h][2] row aggregates per strip
   float4* CH = nullptr;     // [batch][nx][pairs][h][2] row anticausal carries
+  float2* EM = nullptr;     // [batch][h][w_pad] per-pixel plane seeds (E 2^s0, H 2^-k) from K1
+  int w_pad = 0;            // EM row pitch in pixels (even: TMA strides are 16-B multiples)
   alignas(64) CUtensorMap vmap;    // TMA map of V: fp32 [batch][pairs][w][2*h_pad] (row-pass loads)
   alignas(64) CUtensorMap vstore;  // TMA map of V for the column pass's staged chunk stores
+  alignas(64) CUtensorMap emmap;   // TMA map of EM: 32x32-pixel tiles for the column pass
   double* scalars = nullptr;   // [batch][2]  t_c
   double* partials = nullptr;  // [batch][mean_blocks][2]
   size_t bytes = 0;

@@ -152,7 +152,8 @@ __device__ __forceinline__ void issue_f_tile(Tin* ftile, const Tin* __restrict__
 // runs their chains interleaved, so the dependent multiplies overlap.
 template <typename Tin>
 __device__ __forceinline__ void produce_planes(float2* buf, const Tin* ftile, double t_c,
-                                               const RangeConsts& rc) {
+                                               const RangeConsts& rc, float2* em = nullptr,
+                                               int em_pitch = 0, int em_rows = 0, int em_cols = 0) {
   const int nthr = blockDim.x * blockDim.y, pairs = blockDim.y;
   const int tid = threadIdx.y * 32 + threadIdx.x;
   for (int p0 = tid; p0 < 1024; p0 += 3 * nthr) {
@@ -169,6 +170,8 @@ __device__ __forceinline__ void produce_planes(float2* buf, const Tin* ftile, do
       x[k] = t.x;
       m[k] = t.y;
       dst[k] = buf + c * 33 + j;
+      // K1 hands the per-pixel seeds to the column pass (coalesced: lanes = columns)
+      if (em && ok[k] && j < em_rows && c < em_cols) em[(size_t)j * em_pitch + c] = t;
     }
 #pragma unroll 2
     for (int gg = 0; gg < pairs; ++gg) {
@@ -192,9 +195,10 @@ __device__ __forceinline__ void produce_planes(float2* buf, const Tin* ftile, do
 template <int MAXT, typename Tin>
 __global__ void __launch_bounds__(MAXT, 2) k_col_carry(const Tin* __restrict__ in_all,
                                                        const double* __restrict__ scalars,
-                                                       float4* __restrict__ CA_all, int w, int h,
-                                                       int ny, FilterConsts fc, TileConsts tc,
-                                                       RangeConsts rc) {
+                                                       float4* __restrict__ CA_all,
+                                                       float2* __restrict__ EM_all, int w, int h,
+                                                       int w_pad, int ny, FilterConsts fc,
+                                                       TileConsts tc, RangeConsts rc) {
   extern __shared__ float4 smem4[];
   float2* buf = reinterpret_cast<float2*>(smem4);                               // [pairs][32][33]
   Tin* ftiles = reinterpret_cast<Tin*>(buf + (size_t)blockDim.y * 32 * 33);  // [2][32*33]
@@ -216,7 +220,8 @@ __global__ void __launch_bounds__(MAXT, 2) k_col_carry(const Tin* __restrict__ i
       issue_f_tile(ftiles + ((cy - 1) & 1) * 32 * 33, in, w, h, x0, y0 - kTile);
       cp_async_commit();
     }
-    produce_planes(buf, ftiles + (cy & 1) * 32 * 33, t_c, rc);
+    produce_planes(buf, ftiles + (cy & 1) * 32 * 33, t_c, rc,
+                   EM_all + ((size_t)f * h + y0) * w_pad + x0, w_pad, rows, min(32, w - x0));
     __syncthreads();
     if (x < w) {
       if (cy == ny - 1) ps_set_gain(C, mine[rows - 1], fc);
@@ -264,28 +269,23 @@ __device__ __forceinline__ float* stage_at(float* base_col, int j, int cm) {
   return base_col + (j >> 4) * 1024 + ((((j & 15) >> 1) ^ cm) << 2) + (j & 1) * 2;
 }
 
-// Producer into a stage tile for the pair group starting at plane n0 = 2*pair0:
-// item = (column, row pair); 512 items over the CTA's threads, four pixels
-// (two items) in flight per thread. x_{n0} = es m^{n0} is reached through the
-// planes x_4, x_8, ... (each in range by the plane scaling), then the chain
-// runs over the group's planes.
-template <typename Tin>
-__device__ __forceinline__ void produce_group(float* stage, const Tin* ftile, double t_c,
-                                              const RangeConsts& rc, int pair0, int npairs) {
+// Producer into a stage tile for the pair group starting at plane n0 = 2*pair0,
+// from the per-pixel seeds (es, m) K1 left in HBM (em tile [32 rows][32]):
+// item = (column, row pair), two items (four pixels) in flight per thread.
+// x_{n0} = es m^{n0} is reached through the planes x_4, x_8, ... (each in
+// range by the plane scaling), then the chain runs over the group's planes.
+__device__ __forceinline__ void produce_group(float* stage, const float2* emt, int pair0,
+                                              int npairs) {
   const int nthr = blockDim.x * blockDim.y;
   const int tid = threadIdx.y * 32 + threadIdx.x;
   for (int i0 = tid; i0 < 512; i0 += 2 * nthr) {
     float x[4], m[4];
     float4* dst[2];
-    bool ok[2];
 #pragma unroll
     for (int k = 0; k < 2; ++k) {
-      const int ik = i0 + k * nthr;
-      ok[k] = ik < 512;
-      const int it = ok[k] ? ik : i0;
+      const int it = i0 + k * nthr;  // 512 = 2 * 2 * 128 items: always valid for 4-warp CTAs
       const int c = it & 31, j = (it >> 5) * 2;  // rows j, j+1
-      const float2 ta = pixel_terms(static_cast<double>(ftile[j * 33 + c]), t_c, rc);
-      const float2 tb = pixel_terms(static_cast<double>(ftile[(j + 1) * 33 + c]), t_c, rc);
+      const float2 ta = emt[j * 32 + c], tb = emt[(j + 1) * 32 + c];
       x[2 * k] = ta.x;
       m[2 * k] = ta.y;
       x[2 * k + 1] = tb.x;
@@ -309,7 +309,7 @@ __device__ __forceinline__ void produce_group(float* stage, const Tin* ftile, do
 #pragma unroll
       for (int k = 0; k < 2; ++k) {
         const float a1 = x[2 * k] * m[2 * k], b1 = x[2 * k + 1] * m[2 * k + 1];
-        if (ok[k]) dst[k][gg * 512] = make_float4(x[2 * k], a1, x[2 * k + 1], b1);
+        dst[k][gg * 512] = make_float4(x[2 * k], a1, x[2 * k + 1], b1);
         x[2 * k] = a1 * m[2 * k];
         x[2 * k + 1] = b1 * m[2 * k + 1];
       }
@@ -321,40 +321,47 @@ __device__ __forceinline__ void produce_group(float* stage, const Tin* ftile, do
 // CTAs share an SM so one's producer / H-dot phases overlap another's sweeps.
 constexpr int kColGroup = 4;
 
-template <typename Tin>
 __global__ void __launch_bounds__(32 * kColGroup, 3) k_colpass_tma(
-    const Tin* __restrict__ in_all, const double* __restrict__ scalars,
     const float4* __restrict__ CA_all, float4* __restrict__ AH_all, int w, int h, int ny, int nx,
-    int pairs, FilterConsts fc, TileConsts tc, RangeConsts rc,
-    const __grid_constant__ CUtensorMap vstore) {
+    int pairs, int groups, FilterConsts fc, TileConsts tc,
+    const __grid_constant__ CUtensorMap emmap, const __grid_constant__ CUtensorMap vstore) {
   extern __shared__ float4 smem4[];
+  __shared__ uint64_t em_full;
   const int f = blockIdx.y, lane = threadIdx.x, gl = threadIdx.y;
   const int tid = gl * 32 + lane;
-  const int pair0 = blockIdx.z * kColGroup, npairs = min(kColGroup, pairs - pair0);
+  // pair group fastest in the grid: a strip's groups run together and share
+  // its EM tiles in L2
+  const int strip = blockIdx.x / groups, grp = blockIdx.x - strip * groups;
+  const int pair0 = grp * kColGroup, npairs = min(kColGroup, pairs - pair0);
   const int g = pair0 + gl;           // this warp's pair
   const bool active = gl < npairs;
-  // smem: [2 stages x kColGroup x 8 KB, 1024-aligned][2 f tiles]. The alignment
-  // is an offset from the smem base (not integer arithmetic on the pointer) so
-  // the compiler keeps the accesses in the shared window (LDS/STS).
+  // smem: [2 stages x kColGroup x 8 KB, 1024-aligned][EM tile 8 KB]. The
+  // alignment is an offset from the smem base (not integer arithmetic on the
+  // pointer) so the compiler keeps the accesses in the shared window.
   float* stages = reinterpret_cast<float*>(reinterpret_cast<char*>(smem4) +
                                            ((kStageAlign - smem_u32(smem4)) & (kStageAlign - 1)));
   constexpr int kStageFloats = kColGroup * 2048;
-  Tin* ftiles = reinterpret_cast<Tin*>(stages + 2 * kStageFloats);  // [2][32*33]
-  const int strip = blockIdx.x, x0 = strip * 32, x = x0 + lane;
+  float2* emt = reinterpret_cast<float2*>(stages + 2 * kStageFloats);  // [32][32]
+  const int x0 = strip * 32, x = x0 + lane;
   const int cols = min(32, w - x0);
-  const Tin* in = in_all + (size_t)f * w * h;
   const float4* CA = CA_all + (size_t)f * ny * pairs * w * 2;
   float4* AH = AH_all + (size_t)f * nx * pairs * h * 2;
-  const double t_c = scalars[2 * f];
   const int cm = lane & 7;
   const int col_off = (gl * 64 + lane) * 32;  // this thread's column, half 0
   // H-dots: thread (pair, row lane) reads column c at hd_off + c*32 + ((hq ^ (c%8)) << 2)
   const int hq = (lane & 15) >> 1;
   const int hd_off = (gl * 64 + (lane >> 4) * 32) * 32 + (lane & 1) * 2;
+  if (tid == 0) {
+    mbar_init(&em_full, 1);
+    mbar_fence_init();
+  }
+  __syncthreads();
+  if (tid == 0) {
+    mbar_arrive_expect_tx(&em_full, 32 * 32 * sizeof(float2));
+    tma_load_3d(emt, &emmap, 2 * x0, 0, f, &em_full);
+  }
   PairState cs;  // causal state, carried across chunks
   ps_zero(cs);
-  issue_f_tile(ftiles, in, w, h, x0, 0);
-  cp_async_commit();
   // anticausal carries, prefetched one chunk ahead
   const float4* ca_ptr = CA + (size_t)min(g, pairs - 1) * w * 2 + (size_t)min(x, w - 1) * 2;
   const size_t ca_stride = (size_t)pairs * w * 2;
@@ -362,17 +369,13 @@ __global__ void __launch_bounds__(32 * kColGroup, 3) k_colpass_tma(
   for (int cy = 0; cy < ny; ++cy) {
     const int y0 = cy * kTile, rows = min(kTile, h - y0);
     float* stage = stages + (cy & 1) * kStageFloats;
-    cp_async_wait_all();
     if (tid == 0 && cy >= 2) {  // the store of chunk cy-2 (same stage) has read it
       asm volatile("cp.async.bulk.wait_group.read 1;\n" ::: "memory");
     }
     __syncthreads();
-    if (cy + 1 < ny) {
-      issue_f_tile(ftiles + ((cy + 1) & 1) * 32 * 33, in, w, h, x0, y0 + kTile);
-      cp_async_commit();
-    }
+    mbar_wait(&em_full, cy & 1);  // this chunk's seeds have landed
 #ifndef GPF_DIAG_NO_PROD
-    produce_group(stage, ftiles + (cy & 1) * 32 * 33, t_c, rc, pair0, npairs);
+    produce_group(stage, emt, pair0, npairs);
 #endif
     PairState as;
     as.wr[0] = make_float2(ca0.x, ca0.y);
@@ -384,6 +387,10 @@ __global__ void __launch_bounds__(32 * kColGroup, 3) k_colpass_tma(
       ca1 = __ldg(ca_ptr + (size_t)(cy + 1) * ca_stride + 1);
     }
     __syncthreads();
+    if (tid == 0 && cy + 1 < ny) {  // the EM tile is free again: fetch the next chunk's
+      mbar_arrive_expect_tx(&em_full, 32 * 32 * sizeof(float2));
+      tma_load_3d(emt, &emmap, 2 * x0, y0 + kTile, f, &em_full);
+    }
     float* mcol = stage + col_off;
     if (active && x < w) {
       float2 xr[kTile];
@@ -664,9 +671,8 @@ template <typename Tin>
 static size_t colpass_smem(int pairs) {  // k_colpass and k_col_carry
   return sizeof(float2) * (size_t)pairs * 32 * 33 + sizeof(Tin) * 2 * 32 * 33;
 }
-template <typename Tin>
-static size_t colpass_tma_smem() {  // two stages of a pair group + f tiles + alignment slack
-  return kStageAlign + sizeof(float) * 2 * kColGroup * 2048 + sizeof(Tin) * 2 * 32 * 33;
+static size_t colpass_tma_smem() {  // two stages of a pair group + EM tile + alignment slack
+  return kStageAlign + sizeof(float) * 2 * kColGroup * 2048 + sizeof(float2) * 32 * 32;
 }
 template <typename Tin, typename Tout>
 static int rowpass_nbuf(int pairs) {  // deepest V ring that fits in 227 KB (0: none)
@@ -705,10 +711,14 @@ void plan_init(Plan& plan, const Params& p, int device, int batch) {
   const size_t vb = sizeof(float2) * B * (size_t)pairs * w * h_pad;
   const size_t cab = sizeof(float4) * 2 * B * (size_t)plan.ny * pairs * w;
   const size_t ahb = sizeof(float4) * 2 * B * (size_t)plan.nx * pairs * h;
+  plan.w_pad = (w + 1) & ~1;
+  const size_t emb = sizeof(float2) * B * (size_t)h * plan.w_pad;
   plan.V = nullptr;
   plan.CA = plan.AH = plan.CH = nullptr;
+  plan.EM = nullptr;
   plan.scalars = plan.partials = nullptr;
   try {
+    check(cudaMalloc(&plan.EM, emb), "cudaMalloc(EM)");
     check(cudaMalloc(&plan.V, vb), "cudaMalloc(V)");
     check(cudaMalloc(&plan.CA, cab), "cudaMalloc(CA)");
     check(cudaMalloc(&plan.AH, ahb), "cudaMalloc(AH)");
@@ -719,7 +729,7 @@ void plan_init(Plan& plan, const Params& p, int device, int batch) {
     plan_free(plan);
     throw;
   }
-  plan.bytes = vb + cab + 2 * ahb + sizeof(double) * 2 * B * (1 + plan.mean_blocks);
+  plan.bytes = vb + cab + 2 * ahb + emb + sizeof(double) * 2 * B * (1 + plan.mean_blocks);
   plan.launches_per_frame = 6;
   // TMA tensor map of V for the row pass: fp32 dims (inner first)
   // {2*h_pad, w, pairs, batch}, box {64 (= 32 rows), 32 columns, pairs, 1}
@@ -761,6 +771,19 @@ void plan_init(Plan& plan, const Params& p, int device, int batch) {
     plan_free(plan);
     throw Error{9, "cuTensorMapEncodeTiled (store) failed (" + std::to_string((int)r2) + ")"};
   }
+  // EM seeds for the column pass: fp32 {2*w_pad, h, batch}, box {64 (= 32
+  // pixels), 32 rows, 1}; out-of-image pixels read as zero.
+  const cuuint64_t edims[3] = {(cuuint64_t)2 * w, (cuuint64_t)h, (cuuint64_t)B};
+  const cuuint64_t estrides[2] = {(cuuint64_t)8 * plan.w_pad, (cuuint64_t)8 * plan.w_pad * h};
+  const cuuint32_t ebox[3] = {64, 32, 1};
+  const cuuint32_t eestr[3] = {1, 1, 1};
+  const CUresult r3 = encode(&plan.emmap, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, plan.EM, edims, estrides,
+                             ebox, eestr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                             CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r3 != CUDA_SUCCESS) {
+    plan_free(plan);
+    throw Error{9, "cuTensorMapEncodeTiled (EM) failed (" + std::to_string((int)r3) + ")"};
+  }
 }
 
 void plan_free(Plan& plan) {
@@ -768,10 +791,12 @@ void plan_free(Plan& plan) {
   cudaFree(plan.CA);
   cudaFree(plan.AH);
   cudaFree(plan.CH);
+  cudaFree(plan.EM);
   cudaFree(plan.scalars);
   cudaFree(plan.partials);
   plan.V = nullptr;
   plan.CA = plan.AH = plan.CH = nullptr;
+  plan.EM = nullptr;
   plan.scalars = plan.partials = nullptr;
 }
 
@@ -786,7 +811,7 @@ static void launch_passes(Plan& plan, const Tin* d_in, Tout* d_out, int count,
   // TMA-store column pass in pair groups (the large-N builds keep the padded one)
   constexpr bool kCanStage = MAXT <= 512;
   const bool staged = kCanStage;
-  const int psm = (int)(staged ? colpass_tma_smem<Tin>() : colpass_smem<Tin>(pairs));
+  const int psm = (int)(staged ? colpass_tma_smem() : colpass_smem<Tin>(pairs));
   const int nbuf = rowpass_nbuf<Tin, Tout>(pairs);
   const int rsm = (int)rowpass_smem_bytes<Tin, Tout>(pairs, nbuf);
   check(cudaFuncSetAttribute(k_col_carry<MAXT, Tin>, cudaFuncAttributeMaxDynamicSharedMemorySize, csm),
@@ -798,15 +823,15 @@ static void launch_passes(Plan& plan, const Tin* d_in, Tout* d_out, int count,
         "cudaFuncSetAttribute");
   const dim3 blk(32, pairs);
   stage_mark(plan, kStageColCarry, st);
-  k_col_carry<MAXT, Tin><<<dim3(plan.nx, count), blk, csm, st>>>(d_in, plan.scalars, plan.CA, w, h,
-                                                                 plan.ny, plan.fc, plan.tc, plan.rc);
+  k_col_carry<MAXT, Tin><<<dim3(plan.nx, count), blk, csm, st>>>(
+      d_in, plan.scalars, plan.CA, plan.EM, w, h, plan.w_pad, plan.ny, plan.fc, plan.tc, plan.rc);
   stage_mark(plan, kStageColPass, st);
   if constexpr (kCanStage) {
-    check(cudaFuncSetAttribute(k_colpass_tma<Tin>, cudaFuncAttributeMaxDynamicSharedMemorySize, psm),
+    check(cudaFuncSetAttribute(k_colpass_tma, cudaFuncAttributeMaxDynamicSharedMemorySize, psm),
           "cudaFuncSetAttribute");
     const int groups = (pairs + kColGroup - 1) / kColGroup;
-    k_colpass_tma<Tin><<<dim3(plan.nx, count, groups), dim3(32, kColGroup), psm, st>>>(
-        d_in, plan.scalars, plan.CA, plan.AH, w, h, plan.ny, plan.nx, pairs, plan.fc, plan.tc, plan.rc,
+    k_colpass_tma<<<dim3(plan.nx * groups, count), dim3(32, kColGroup), psm, st>>>(
+        plan.CA, plan.AH, w, h, plan.ny, plan.nx, pairs, groups, plan.fc, plan.tc, plan.emmap,
         plan.vstore);
   }
   if (!staged) {
