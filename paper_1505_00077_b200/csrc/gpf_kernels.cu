@@ -19,8 +19,12 @@
 // exactly once (written by K2, read by K4).
 //
 // HBM layouts (per frame):
-//   V  [pairs][w][h_pad] float2   column-pass output, TRANSPOSED so that the
-//                                 row pass reads 32 consecutive rows per load
+//   V  [pairs][h_pad/16][w][16]   column-pass output, BAND-MAJOR float2: the
+//                                 16 rows of one column within a 16-row band
+//                                 are 128 B, and a band's columns follow each
+//                                 other, so a 32-column strip of a band is 4 KB
+//                                 contiguous for both the writer (K2) and the
+//                                 reader (K4)
 //   CA [ny][pairs][w]   2xfloat4  column anticausal carries (from f, K1)
 //   AH [nx][pairs][h]   2xfloat4  per-strip row aggregates sum_i p^i V (K2)
 //   CH [nx][pairs][h]   2xfloat4  row anticausal carries (K3)
@@ -401,24 +405,32 @@ __global__ void __launch_bounds__(32 * kColGroup, 3) k_colpass_tma(
         xr[j + 1] = make_float2(v.z, v.w);
       }
       if (cy == 0) ps_set_gain(cs, xr[0], fc);
-      if (rows == kTile) {  // full chunk: branch-free sweeps, two rows per smem access
+      if (rows == kTile) {
+        // full chunk: both directions in one branch-free loop (two independent
+        // recurrences per step), two rows per smem access. Step t runs the
+        // anticausal sections at rows 31-t, 30-t and the causal ones at rows
+        // t, t+1; first-half outputs park in the stage, second-half outputs
+        // add the other direction's parked value.
 #pragma unroll
-        for (int j = kTile - 1; j >= 0; j -= 2) {
+        for (int t = 0; t < kTile; t += 2) {
           const float2 yb = ps_emit(as, fc.br2, fc.nbi2);
-          ps_advance(as, xr[j], fc);
+          ps_advance(as, xr[31 - t], fc);
+          ps_advance(cs, xr[t], fc);
+          const float2 yc0 = ps_emit(cs, fc.ar2, fc.nai2);
           const float2 ya = ps_emit(as, fc.br2, fc.nbi2);
-          ps_advance(as, xr[j - 1], fc);
-          *reinterpret_cast<float4*>(stage_at(mcol, j - 1, cm)) = make_float4(ya.x, ya.y, yb.x, yb.y);
-        }
-#pragma unroll
-        for (int j = 0; j < kTile; j += 2) {
-          float4* p = reinterpret_cast<float4*>(stage_at(mcol, j, cm));
-          const float4 an = *p;
-          ps_advance(cs, xr[j], fc);
-          const float2 ya = add2(ps_emit(cs, fc.ar2, fc.nai2), make_float2(an.x, an.y));
-          ps_advance(cs, xr[j + 1], fc);
-          const float2 yb = add2(ps_emit(cs, fc.ar2, fc.nai2), make_float2(an.z, an.w));
-          *p = make_float4(ya.x, ya.y, yb.x, yb.y);
+          ps_advance(as, xr[30 - t], fc);
+          ps_advance(cs, xr[t + 1], fc);
+          const float2 yc1 = ps_emit(cs, fc.ar2, fc.nai2);
+          float4* pa = reinterpret_cast<float4*>(stage_at(mcol, 30 - t, cm));
+          float4* pc = reinterpret_cast<float4*>(stage_at(mcol, t, cm));
+          if (t < kTile / 2) {
+            *pa = make_float4(ya.x, ya.y, yb.x, yb.y);
+            *pc = make_float4(yc0.x, yc0.y, yc1.x, yc1.y);
+          } else {
+            const float4 qa = *pa, qc = *pc;
+            *pa = make_float4(ya.x + qa.x, ya.y + qa.y, yb.x + qa.z, yb.y + qa.w);
+            *pc = make_float4(yc0.x + qc.x, yc0.y + qc.y, yc1.x + qc.z, yc1.y + qc.w);
+          }
         }
       } else {  // last, partial chunk: predicated (keeps xr in registers)
 #pragma unroll
@@ -540,10 +552,12 @@ __global__ void __launch_bounds__(MAXT, 1) k_colpass(const Tin* __restrict__ in_
     __syncthreads();
     // write-out: warp g writes its pair's 32 columns; lanes = rows
     if (lane < rows) {
-      float2* vdst = V + ((size_t)g * w + x0) * h_pad + y0 + lane;
+      // band-major: element (g, row y, column x) at ((g*nb + y/16)*w + x)*16 + y%16
+      const int y = y0 + lane;
+      float2* vdst = V + (((size_t)g * (h_pad >> 4) + (y >> 4)) * w + x0) * 16 + (y & 15);
       const float2* src = buf + (size_t)g * 32 * 33 + lane;
 #pragma unroll 8
-      for (int c = 0; c < cols; ++c, vdst += h_pad) *vdst = src[c * 33];
+      for (int c = 0; c < cols; ++c, vdst += 16) *vdst = src[c * 33];
     }
     // strip aggregates for the row pass: thread (pair g, row lane)
     if (lane < rows) {
@@ -574,7 +588,7 @@ __global__ void __launch_bounds__(1024) k_row_scan(const float2* __restrict__ V_
   const float4* AH = AH_all + (size_t)f * nx * pairs * h * 2;
   float4* CH = CH_all + (size_t)f * nx * pairs * h * 2;
   PairState C;
-  ps_set_gain(C, V[((size_t)g * w + (w - 1)) * h_pad + y], fc);
+  ps_set_gain(C, V[(((size_t)g * (h_pad >> 4) + (y >> 4)) * w + (w - 1)) * 16 + (y & 15)], fc);
   const size_t sstride = (size_t)pairs * h * 2;
   const size_t off = (size_t)g * h * 2 + (size_t)y * 2;
   ps_store(CH + (size_t)(nx - 1) * sstride + off, C);
@@ -731,8 +745,8 @@ void plan_init(Plan& plan, const Params& p, int device, int batch) {
   }
   plan.bytes = vb + cab + 2 * ahb + emb + sizeof(double) * 2 * B * (1 + plan.mean_blocks);
   plan.launches_per_frame = 6;
-  // TMA tensor map of V for the row pass: fp32 dims (inner first)
-  // {2*h_pad, w, pairs, batch}, box {64 (= 32 rows), 32 columns, pairs, 1}
+  // TMA tensor maps of the band-major V: fp32 dims (inner first)
+  // {32 = 16 rows x 2 planes, w, h_pad/16 bands, pairs, batch}.
   static PFN_cuTensorMapEncodeTiled_v12000 encode = nullptr;
   if (!encode) {
     cudaDriverEntryPointQueryResult q;
@@ -742,30 +756,26 @@ void plan_init(Plan& plan, const Params& p, int device, int batch) {
     if (q != cudaDriverEntryPointSuccess || !encode)
       throw Error{9, "cuTensorMapEncodeTiled unavailable"};
   }
-  const cuuint64_t dims[4] = {(cuuint64_t)2 * h_pad, (cuuint64_t)w, (cuuint64_t)pairs, (cuuint64_t)B};
-  const cuuint64_t strides[3] = {(cuuint64_t)2 * h_pad * 4, (cuuint64_t)2 * h_pad * 4 * w,
-                                 (cuuint64_t)2 * h_pad * 4 * w * pairs};
-  const cuuint32_t box[4] = {2 * kRowBand, 32, (cuuint32_t)pairs, 1};
-  const cuuint32_t estr[4] = {1, 1, 1, 1};
-  const CUresult r = encode(&plan.vmap, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, plan.V, dims, strides, box,
+  const cuuint64_t nb = (cuuint64_t)h_pad / 16;
+  const cuuint64_t dims[5] = {32, (cuuint64_t)w, nb, (cuuint64_t)pairs, (cuuint64_t)B};
+  const cuuint64_t strides[4] = {128, (cuuint64_t)128 * w, (cuuint64_t)128 * w * nb,
+                                 (cuuint64_t)128 * w * nb * pairs};
+  const cuuint32_t estr[5] = {1, 1, 1, 1, 1};
+  // row pass: box {32, 32 columns, 1 band, pairs, 1} -> smem [pair][column][16 rows]
+  const cuuint32_t box[5] = {32, 32, 1, (cuuint32_t)pairs, 1};
+  const CUresult r = encode(&plan.vmap, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 5, plan.V, dims, strides, box,
                             estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
                             CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   if (r != CUDA_SUCCESS) {
     plan_free(plan);
     throw Error{9, "cuTensorMapEncodeTiled failed (" + std::to_string((int)r) + ")"};
   }
-  // Column-pass chunk store: V viewed as fp32 {32 floats = 16 rows, column,
-  // 16-row half, pair, frame} (the half stride, 128 B, is inside the column
-  // stride), box {32, 32 columns, 2 halves, kColGroup pairs, 1} = one 32x32 chunk of
-  // every pair; smem side [pair][half][column][128 B], 128B-swizzled.
-  const cuuint64_t sdims[5] = {32, (cuuint64_t)w, (cuuint64_t)h_pad / 16, (cuuint64_t)pairs,
-                               (cuuint64_t)B};
-  const cuuint64_t sstrides[4] = {(cuuint64_t)2 * h_pad * 4, 128, (cuuint64_t)2 * h_pad * 4 * w,
-                                  (cuuint64_t)2 * h_pad * 4 * w * pairs};
+  // column-pass chunk store: box {32, 32 columns, 2 bands, kColGroup pairs, 1}
+  // = one 32x32 chunk of a pair group; smem [pair][band][column][128 B],
+  // 128B-swizzled.
   const cuuint32_t sbox[5] = {32, 32, 2, (cuuint32_t)kColGroup, 1};
-  const cuuint32_t sestr[5] = {1, 1, 1, 1, 1};
-  const CUresult r2 = encode(&plan.vstore, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 5, plan.V, sdims, sstrides,
-                             sbox, sestr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+  const CUresult r2 = encode(&plan.vstore, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 5, plan.V, dims, strides,
+                             sbox, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
                              CU_TENSOR_MAP_L2_PROMOTION_NONE, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   if (r2 != CUDA_SUCCESS) {
     plan_free(plan);
@@ -845,10 +855,20 @@ static void launch_passes(Plan& plan, const Tin* d_in, Tout* d_out, int count,
   k_row_scan<<<dim3(plan.ny, count), blk, 0, st>>>(plan.V, plan.AH, plan.CH, w, h, h_pad, plan.nx,
                                                    plan.fc, plan.tc);
   stage_mark(plan, kStageRowPass, st);
-  k_rowpass<RMAXT, Tin, Tout><<<dim3((h + kRowBand - 1) / kRowBand, count),
-                                dim3(32, (pairs + 1) / 2 + kAux), rsm, st>>>(
-      d_in, plan.scalars, plan.CH, d_out, d_fb, w, h, plan.nx, pairs, nbuf, plan.fc, plan.rc,
-      plan.vmap);
+  if (pairs <= 12) {
+    const int r2sm = (int)rowpass2_smem_bytes<Tin, Tout>(pairs);
+    // the default degree (N = 20, reference RangeParams) has a fully static build
+    auto k = plan.rc.degree == 20 ? k_rowpass2<Tin, Tout, 20> : k_rowpass2<Tin, Tout, 0>;
+    check(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, r2sm),
+          "cudaFuncSetAttribute");
+    k<<<dim3((h + kRowBand - 1) / kRowBand, count), dim3(32, (pairs + 1) / 2), r2sm, st>>>(
+        d_in, plan.scalars, plan.CH, d_out, d_fb, w, h, plan.nx, pairs, plan.fc, plan.rc, plan.vmap);
+  } else {
+    k_rowpass<RMAXT, Tin, Tout><<<dim3((h + kRowBand - 1) / kRowBand, count),
+                                  dim3(32, (pairs + 1) / 2 + kAux), rsm, st>>>(
+        d_in, plan.scalars, plan.CH, d_out, d_fb, w, h, plan.nx, pairs, nbuf, plan.fc, plan.rc,
+        plan.vmap);
+  }
   stage_end(plan, st);
 }
 

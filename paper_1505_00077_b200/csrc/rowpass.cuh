@@ -101,25 +101,33 @@ __global__ void __launch_bounds__(MAXT, 1) k_rowpass(const Tin* __restrict__ in_
       // element [g][c][r] of slot s at tl[c * kRowBand]
       float2* tl = T + (size_t)s * tile_elems + (size_t)gl * 32 * kRowBand + r;
       mbar_wait(&full[s], (b / nbuf) & 1);
-      float2 ybuf[32];
+      if (b == 0) ps_set_gain(cs, tl[0], fc);
       if (cols == 32) {
-        // (an empty asm with a memory clobber every 4 columns stops the
-        // compiler from hoisting all 32 smem loads into registers at once)
+        // Both directions in one loop (two independent recurrences per step):
+        // step t runs the anticausal section at column 31-t and the causal one
+        // at column t. Outputs of the first half wait in registers; from
+        // t = 16 on each column's other half is ready and the sum is written.
+        float2 ya_hi[16], yc_lo[16];  // ya[16..31], yc[0..15]
 #pragma unroll
-        for (int c = 31; c >= 0; --c) {
-          if ((c & 3) == 3) asm volatile("" ::: "memory");
-          ybuf[c] = ps_emit(as, fc.br2, fc.nbi2);
-          ps_advance(as, tl[c * kRowBand], fc);
-        }
-        if (b == 0) ps_set_gain(cs, tl[0], fc);
-#pragma unroll
-        for (int c = 0; c < 32; ++c) {
-          if ((c & 3) == 0) asm volatile("" ::: "memory");
-          ps_advance(cs, tl[c * kRowBand], fc);
-          const float2 o = add2(ps_emit(cs, fc.ar2, fc.nai2), ybuf[c]);
-          if (live) tl[c * kRowBand] = o;
+        for (int t = 0; t < 32; ++t) {
+          const int ca = 31 - t, cc = t;
+          const float2 ya = ps_emit(as, fc.br2, fc.nbi2);
+          const float2 xa = tl[ca * kRowBand], xc = tl[cc * kRowBand];
+          ps_advance(as, xa, fc);
+          ps_advance(cs, xc, fc);
+          const float2 yc = ps_emit(cs, fc.ar2, fc.nai2);
+          if (t < 16) {
+            ya_hi[ca - 16] = ya;
+            yc_lo[cc] = yc;
+          } else {
+            if (live) {
+              tl[ca * kRowBand] = add2(ya, yc_lo[ca]);
+              tl[cc * kRowBand] = add2(yc, ya_hi[cc - 16]);
+            }
+          }
         }
       } else {  // last, partial strip
+        float2 ybuf[32];
 #pragma unroll
         for (int c = 31; c >= 0; --c) {
           if (c < cols) {
@@ -127,7 +135,6 @@ __global__ void __launch_bounds__(MAXT, 1) k_rowpass(const Tin* __restrict__ in_
             ps_advance(as, tl[c * kRowBand], fc);
           }
         }
-        if (b == 0) ps_set_gain(cs, tl[0], fc);
 #pragma unroll
         for (int c = 0; c < 32; ++c) {
           if (c < cols) {
@@ -154,7 +161,7 @@ __global__ void __launch_bounds__(MAXT, 1) k_rowpass(const Tin* __restrict__ in_
     if (atid == 0) {
       fence_proxy_async();
       mbar_arrive_expect_tx(&full[s], (uint32_t)(tile_elems * sizeof(float2)));
-      tma_load_4d(T + (size_t)s * tile_elems, &vmap, 2 * y0, xs, 0, f, &full[s]);
+      tma_load_5d(T + (size_t)s * tile_elems, &vmap, 0, xs, y0 / kRowBand, 0, f, &full[s]);
     }
     Tin* Fs = F + s * kRowBand * 33;
     for (int p = atid; p < kRowBand * 32; p += nat) {
@@ -237,6 +244,285 @@ __global__ void __launch_bounds__(MAXT, 1) k_rowpass(const Tin* __restrict__ in_
     named_bar(1, nat);  // slot s and O are free again
     if (b + nbuf < nx) load_strip(b + nbuf, s);
   }
+  for (int o = 16; o; o >>= 1) my_fb += __shfl_xor_sync(0xffffffffu, my_fb, o);
+  if (lane == 0 && my_fb) atomicAdd(fb_all + f, (unsigned long long)my_fb);
+}
+
+}  // namespace gpfb
+
+namespace gpfb {
+
+// ----------------------------------------------------------------------------
+// k_rowpass2 (pairs <= 12): no warp specialisation. A CTA of ceil(pairs/2)
+// warps owns kRowBand rows; per 32-column strip it
+//   1. waits for the strip's V box (TMA, 2-slot ring) and sweeps both
+//      directions in one interleaved loop (half-warp per pair, lane = row),
+//      Fbar in place;
+//   2. contracts every pixel over all planes into an output tile;
+//   3. writes the tile out coalesced and refills the slot with strip b+2.
+// Two CTAs share an SM, so one's contraction / write-out / load phases
+// overlap the other's FMA-bound sweeps.
+// ----------------------------------------------------------------------------
+constexpr int kRow2Slots = 2;
+constexpr int kRow2MaxN = 22;  // pairs <= 12
+
+template <typename Tin, typename Tout>
+__host__ __device__ constexpr size_t rowpass2_smem_bytes(int pairs) {
+  return sizeof(float2) * (size_t)pairs * 32 * kRowBand * kRow2Slots +
+         sizeof(Tin) * kRowBand * 33 * kRow2Slots + sizeof(Tout) * kRowBand * 33 +
+         kRow2Slots * sizeof(uint64_t) + 16;
+}
+
+// Contraction of kPx pixels per thread (pixel p -> row p & 15, column p >> 4),
+// their chains interleaved. Plane m adds (c_m, c_{m-1}) F_m to (Q, P); the
+// weight pair advances componentwise, (c_{m+1}, c_m) = (c_m, c_{m-1}) * H
+// (w_m, w_{m-1}): three packed instructions per plane. Plane 0 is Q-only,
+// plane N+1 P-only (bilateral.cpp:117-148). Returns the fallback count.
+template <int kPx, int NFIX, typename Tin, typename Tout>
+__device__ __forceinline__ unsigned contract_px(const float2* Ts, const Tin* Fs, Tout* O, int p0,
+                                                int nthr, int rows, int cols, const RangeConsts& rc,
+                                                double t_c, float sr_f, float tc_hi, float tc_lo) {
+  unsigned nfb = 0;
+  const int nN = NFIX > 0 ? NFIX : rc.degree;  // planes 0..N+1
+  float Hf[kPx];
+  float2 qp[kPx], W[kPx], cur[kPx];
+  int off[kPx];
+#pragma unroll
+  for (int k = 0; k < kPx; ++k) {
+    const int p = min(p0 + k * nthr, kRowBand * 32 - 1);
+    off[k] = (p >> 4) * kRowBand + (p & (kRowBand - 1));  // [col][row]
+    // H as the column pass formed it (pixel_terms): fp64 difference, fp32 H
+    Hf[k] = static_cast<float>((static_cast<double>(Fs[(p & 15) * 33 + (p >> 4)]) - t_c) * rc.inv_sr);
+    cur[k] = Ts[off[k]];  // (F_0, F_1)
+    qp[k] = make_float2(rc.c0 * cur[k].x, 0.f);                // plane 0
+    W[k] = make_float2(rc.c0 * (Hf[k] * rc.w_step[0]), rc.c0);  // (c_1, c_0)
+  }
+  // planes m = 1 .. N: odd m is .y of the pair in cur, even m opens the next
+  // pair. Unrolled to N (static build) or to kRow2MaxN with an early exit, so
+  // smem offsets and weight constants are immediates.
+#pragma unroll
+  for (int m = 1; m <= (NFIX > 0 ? NFIX : kRow2MaxN); m += 2) {
+    if (m > nN) break;
+#pragma unroll
+    for (int k = 0; k < kPx; ++k) {
+      qp[k] = fma2(W[k], f2(cur[k].y), qp[k]);
+      W[k] = mul2(W[k], mul2(f2(Hf[k]), rc.w_pair[m]));
+    }
+    if (m + 1 > nN) break;
+#pragma unroll
+    for (int k = 0; k < kPx; ++k) {
+      cur[k] = Ts[off[k] + ((m + 1) >> 1) * 32 * kRowBand];
+      qp[k] = fma2(W[k], f2(cur[k].x), qp[k]);
+      W[k] = mul2(W[k], mul2(f2(Hf[k]), rc.w_pair[m + 1]));
+    }
+  }
+  // plane N+1: P only, weight c_N (= W.y after the last advance)
+  if (nN & 1) {  // N+1 even: .x of a pair not loaded yet
+#pragma unroll
+    for (int k = 0; k < kPx; ++k)
+      qp[k].y = fmaf(W[k].y, Ts[off[k] + ((nN + 1) >> 1) * 32 * kRowBand].x, qp[k].y);
+  } else {  // N+1 odd: .y of the pair in cur (N = 0: pair 0)
+#pragma unroll
+    for (int k = 0; k < kPx; ++k) qp[k].y = fmaf(W[k].y, cur[k].y, qp[k].y);
+  }
+  // out = sr P/Q + t_c (bilateral.cpp:139-147); |Q| <= threshold -> input.
+  // fp32 output: fp32 quotient (|error| <= sr |P/Q| 2^-22 < 1e-4 on [0, 255]);
+  // fp64 output keeps the fp64 quotient.
+#pragma unroll
+  for (int k = 0; k < kPx; ++k) {
+    const int p = p0 + k * nthr;
+    const int pr = p & (kRowBand - 1), pc = p >> 4;
+    if (p < kRowBand * 32 && pr < rows && pc < cols) {
+      Tout o;
+      if (!(fabsf(qp[k].x) > rc.q_thresh)) {
+        o = static_cast<Tout>(Fs[pr * 33 + pc]);
+        ++nfb;
+      } else if constexpr (sizeof(Tout) == sizeof(float)) {
+        // fast quotient (2 ulp) inside its range; |Q| > threshold >> 2^-126 here
+        const float num = qp[k].y * rc.p_scale, den = qp[k].x;
+        const float q = fabsf(den) < 1e37f ? __fdividef(num, den) : num / den;
+        o = fmaf(sr_f, q, tc_hi) + tc_lo;
+      } else {
+        o = rc.sigma_r * ((static_cast<double>(qp[k].y) * rc.p_scale) / static_cast<double>(qp[k].x)) +
+            t_c;
+      }
+      O[pr * 33 + pc] = o;
+    }
+  }
+  return nfb;
+}
+
+// NFIX > 0: the degree N is a compile-time constant (the default N = 20 build);
+// NFIX = 0: runtime N (<= kRow2MaxN).
+template <typename Tin, typename Tout, int NFIX>
+__global__ void __launch_bounds__(192, 2) k_rowpass2(const Tin* __restrict__ in_all,
+                                                      const double* __restrict__ scalars,
+                                                      const float4* __restrict__ CH_all,
+                                                      Tout* __restrict__ out_all,
+                                                      unsigned long long* __restrict__ fb_all,
+                                                      int w, int h, int nx, int pairs,
+                                                      FilterConsts fc, RangeConsts rc,
+                                                      const __grid_constant__ CUtensorMap vmap) {
+  extern __shared__ float4 smem4[];
+  const int f = blockIdx.y, lane = threadIdx.x, warp = threadIdx.y;
+  const int tid = warp * 32 + lane, nthr = blockDim.x * blockDim.y;
+  const int y0 = blockIdx.x * kRowBand;
+  const int rows = min(kRowBand, h - y0);
+  const size_t tile_elems = (size_t)pairs * 32 * kRowBand;  // float2 per slot: [g][c][16 rows]
+  float2* T = reinterpret_cast<float2*>(smem4);
+  Tin* F = reinterpret_cast<Tin*>(T + kRow2Slots * tile_elems);       // [slot][16 rows][33]
+  Tout* O = reinterpret_cast<Tout*>(F + kRow2Slots * kRowBand * 33);  // [16 rows][33]
+  uint64_t* full = reinterpret_cast<uint64_t*>(
+      (reinterpret_cast<uintptr_t>(O + kRowBand * 33) + 15) & ~uintptr_t(15));
+  const Tin* in = in_all + (size_t)f * w * h;
+  Tout* out = out_all + (size_t)f * w * h;
+  const double t_c = scalars[2 * f];
+
+  // V box of strip b into slot s (TMA, completion on full[s]) and its f tile
+  // (one cp.async group per thread, waited before the contraction)
+  auto load_strip = [&](int b, int s) {
+    const int xs = b * 32, ncol = min(32, w - xs);
+    if (tid == 0) {
+      fence_proxy_async();
+      mbar_arrive_expect_tx(&full[s], (uint32_t)(tile_elems * sizeof(float2)));
+      tma_load_5d(T + (size_t)s * tile_elems, &vmap, 0, xs, y0 / kRowBand, 0, f, &full[s]);
+    }
+    Tin* Fs = F + s * kRowBand * 33;
+    for (int p = tid; p < kRowBand * 32; p += nthr) {
+      const int r = p >> 5, c = p & 31;
+      const bool ok = r < rows && c < ncol;
+      cp_async_zfill<sizeof(Tin)>(Fs + r * 33 + c, ok ? in + (size_t)(y0 + r) * w + xs + c : in, ok);
+    }
+    cp_async_commit();
+  };
+
+  if (tid == 0) {
+    for (int s = 0; s < kRow2Slots; ++s) mbar_init(&full[s], 1);
+    mbar_fence_init();
+  }
+  __syncthreads();
+  for (int s = 0; s < kRow2Slots && s < nx; ++s) load_strip(s, s);
+
+  // sweep role: half-warp per pair, lane = row
+  const int r = lane & (kRowBand - 1);
+  const int g = 2 * warp + (lane >> 4);
+  const bool live = g < pairs;
+  const int gl = live ? g : pairs - 1;
+  const int yr = min(y0 + r, h - 1);
+  const float4* CH = CH_all + (size_t)f * nx * pairs * h * 2 + (size_t)gl * h * 2 + (size_t)yr * 2;
+  const size_t ch_stride = (size_t)pairs * h * 2;
+  float4 c0 = __ldg(CH), c1 = __ldg(CH + 1);
+  PairState cs;
+  ps_zero(cs);
+  unsigned my_fb = 0;
+  const float sr_f = static_cast<float>(rc.sigma_r);
+  const float tc_hi = static_cast<float>(t_c), tc_lo = static_cast<float>(t_c - tc_hi);
+#ifdef GPF_DIAG_CLOCKS
+  long long tph[6] = {0, 0, 0, 0, 0, 0};  // wait V, sweep, f+bar, contract, bar+write, bar+load
+  long long tq = clock64();
+#define GPF_TICK(i) { const long long tn = clock64(); tph[i] += tn - tq; tq = tn; }
+#else
+#define GPF_TICK(i)
+#endif
+
+  for (int b = 0; b < nx; ++b) {
+    const int s = b & 1, xs = b * 32, cols = min(32, w - xs);
+    PairState as;
+    as.wr[0] = make_float2(c0.x, c0.y);
+    as.wi[0] = make_float2(c0.z, c0.w);
+    as.wr[1] = make_float2(c1.x, c1.y);
+    as.wi[1] = make_float2(c1.z, c1.w);
+    if (b + 1 < nx) {
+      c0 = __ldg(CH + (size_t)(b + 1) * ch_stride);
+      c1 = __ldg(CH + (size_t)(b + 1) * ch_stride + 1);
+    }
+    // ---- 1. sweeps (element [g][c][r] of slot s at tl[c * kRowBand])
+    float2* tl = T + (size_t)s * tile_elems + (size_t)gl * 32 * kRowBand + r;
+    GPF_TICK(5);
+    mbar_wait(&full[s], (b >> 1) & 1);
+    GPF_TICK(0);
+    if (b == 0) ps_set_gain(cs, tl[0], fc);
+    if (cols == 32) {
+      // both directions in one loop: step t runs the anticausal sections at
+      // column 31-t and the causal ones at column t; first-half outputs wait
+      // in registers, second-half outputs add them and are written in place
+      float2 ya_hi[16], yc_lo[16];  // ya[16..31], yc[0..15]
+#pragma unroll
+      for (int t = 0; t < 32; ++t) {
+        if ((t & 1) == 1) asm volatile("" ::: "memory");
+        const int ca = 31 - t, cc = t;
+        const float2 ya = ps_emit(as, fc.br2, fc.nbi2);
+        const float2 xa = tl[ca * kRowBand], xc = tl[cc * kRowBand];
+        ps_advance(as, xa, fc);
+        ps_advance(cs, xc, fc);
+        const float2 yc = ps_emit(cs, fc.ar2, fc.nai2);
+        if (t < 16) {
+          ya_hi[ca - 16] = ya;
+          yc_lo[cc] = yc;
+        } else if (live) {
+          tl[ca * kRowBand] = add2(ya, yc_lo[ca]);
+          tl[cc * kRowBand] = add2(yc, ya_hi[cc - 16]);
+        }
+      }
+    } else {  // last, partial strip
+      float2 ybuf[32];
+#pragma unroll
+      for (int c = 31; c >= 0; --c) {
+        if (c < cols) {
+          ybuf[c] = ps_emit(as, fc.br2, fc.nbi2);
+          ps_advance(as, tl[c * kRowBand], fc);
+        }
+      }
+#pragma unroll
+      for (int c = 0; c < 32; ++c) {
+        if (c < cols) {
+          ps_advance(cs, tl[c * kRowBand], fc);
+          const float2 o = add2(ps_emit(cs, fc.ar2, fc.nai2), ybuf[c]);
+          if (live) tl[c * kRowBand] = o;
+        }
+      }
+    }
+    GPF_TICK(1);
+    // this strip's f tile: the newer group (strip b+1) may stay in flight
+    if (b + 1 < nx) asm volatile("cp.async.wait_group 1;\n" ::: "memory");
+    else asm volatile("cp.async.wait_group 0;\n" ::: "memory");
+    __syncthreads();
+    GPF_TICK(2);
+    // ---- 2. contraction: pixel p -> (row p & 15, col p >> 4); three pixels
+    // per thread with interleaved (independent) chains. Plane m adds
+    // (c_m, c_{m-1}) F_m to (Q, P); the weight pair advances componentwise,
+    // (c_{m+1}, c_m) = (c_m, c_{m-1}) * H (w_m, w_{m-1}): three packed
+    // instructions per plane. Plane 0 is Q-only, plane N+1 is P-only.
+    const float2* Ts = T + (size_t)s * tile_elems;
+    const Tin* Fs = F + s * kRowBand * 33;
+    for (int p0 = tid; p0 < kRowBand * 32; p0 += nthr * 3) {
+      // pixels per thread for this warp (warp-uniform: no work on pixels past the strip)
+      const int wb = p0 - lane;
+      if (wb + 2 * nthr + 31 < kRowBand * 32)
+        my_fb += contract_px<3, NFIX>(Ts, Fs, O, p0, nthr, rows, cols, rc, t_c, sr_f, tc_hi, tc_lo);
+      else if (wb + nthr < kRowBand * 32)
+        my_fb += contract_px<2, NFIX>(Ts, Fs, O, p0, nthr, rows, cols, rc, t_c, sr_f, tc_hi, tc_lo);
+      else
+        my_fb += contract_px<1, NFIX>(Ts, Fs, O, p0, nthr, rows, cols, rc, t_c, sr_f, tc_hi, tc_lo);
+    }
+    GPF_TICK(3);
+    __syncthreads();
+    // ---- 3. write-out (row segments of 32, coalesced) and refill the slot
+    for (int p = tid; p < kRowBand * 32; p += nthr) {
+      const int pr = p >> 5, pc = p & 31;
+      if (pr < rows && pc < cols) out[(size_t)(y0 + pr) * w + xs + pc] = O[pr * 33 + pc];
+    }
+    GPF_TICK(4);
+    __syncthreads();  // slot s, its f tile and O are free again
+    if (b + kRow2Slots < nx) load_strip(b + kRow2Slots, s);
+  }
+#ifdef GPF_DIAG_CLOCKS
+  if ((blockIdx.x == 100 || blockIdx.x == 101 || blockIdx.x == 400) && (tid == 0 || tid == 160))
+    printf("cta %d tid %d: waitV %lld sweep %lld fbar %lld contract %lld write %lld load %lld (per strip)\n",
+           blockIdx.x, tid, tph[0] / nx, tph[1] / nx, tph[2] / nx, tph[3] / nx, tph[4] / nx,
+           tph[5] / nx);
+#endif
+#undef GPF_TICK
   for (int o = 16; o; o >>= 1) my_fb += __shfl_xor_sync(0xffffffffu, my_fb, o);
   if (lane == 0 && my_fb) atomicAdd(fb_all + f, (unsigned long long)my_fb);
 }
