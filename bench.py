@@ -155,8 +155,14 @@ def cpu_reference_run(sigmas, sigma_r, degree, steps, threads):
 
 def algorithmic_bytes_per_px(pairs: int) -> dict:
     """HBM bytes each stage must move per pixel (fp32 frames, N+2 = 2*pairs
-    planes, carries every 32 samples: 32 B per (pair, line, chunk))."""
-    return {"mean": 4, "col_carry": 4 + pairs, "colpass": 4 + 10 * pairs, "row_scan": 2 * pairs,
+    planes; carries every 32 samples: 32 B per (pair, line, chunk) = pairs B/px).
+      mean       f                                   4
+      col_carry  f in; CA + EM (plane seeds) out     4 + pairs + 8
+      colpass    EM + CA in; V + AH out              8 + pairs + 8 pairs + pairs
+      row_scan   AH in, CH out                       2 pairs
+      rowpass    V + CH + f in; out                  8 pairs + pairs + 4 + 4
+    (ncu dram__bytes of each launch agree to within 3%: profiles/r01_v17_traffic.csv)"""
+    return {"mean": 4, "col_carry": 12 + pairs, "colpass": 8 + 10 * pairs, "row_scan": 2 * pairs,
             "rowpass": 9 * pairs + 8}
 
 
@@ -250,9 +256,12 @@ def bench_b200(args):
         t = json.load(open(tpath))
         if t.get("width") == W and t.get("height") == H and dom in t.get("bytes_per_launch", {}):
             traffic = t["bytes_per_launch"][dom]
-    # whole-step view against the SURVEY 8(d) model: 8(N+2)+12 B/px at HBM peak
+    # whole-step view against the SURVEY 8(d) model: 8(N+2)+12 B/px at HBM peak,
+    # and against this design's own traffic (sum of the stages above)
     model_bpp = 8 * (N + 2) + 12
     model_frac = (model_bpp * px * frames / (ms_step / 1e3) / 1e9) / hbm_peak
+    design_bpp = sum(bpp.values())
+    design_frac = (design_bpp * px * frames / (ms_step / 1e3) / 1e9) / hbm_peak
 
     # end to end through the C ABI: pinned host fp32 in -> host fp32 out
     # One host thread per sigma_s plan (the C call releases the GIL; each plan
@@ -324,7 +333,9 @@ def bench_b200(args):
                      "traffic": traffic, "algorithmic_bytes_per_px": bpp[dom],
                      "peak_source": "MEASURED_PEAKS.json hbm_gbs (burst copy)",
                      "step_model_frac": round(model_frac, 4),
-                     "step_model": f"SURVEY 8(d): {model_bpp} B/px at HBM peak"},
+                     "step_model": f"SURVEY 8(d): {model_bpp} B/px at HBM peak",
+                     "step_design_frac": round(design_frac, 4),
+                     "step_design": f"all stages: {design_bpp} B/px at HBM peak"},
         "e2e": e2e,
         "cpu_baseline": cpu,
         "gpu_launches": launches,
