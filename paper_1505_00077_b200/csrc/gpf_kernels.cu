@@ -483,6 +483,127 @@ __global__ void __launch_bounds__(32 * kColGroup, 3) k_colpass_tma(
   if (tid == 0) bulk_wait_all();  // V complete before the CTA retires
 }
 
+// ----------------------------------------------------------------------------
+// K1a: per-pixel plane seeds EM = (E 2^s0, H 2^-k) (pixel_terms), written once
+// per frame and read by the grouped carry and column passes via TMA.
+// ----------------------------------------------------------------------------
+template <typename Tin>
+__global__ void __launch_bounds__(256) k_seed(const Tin* __restrict__ in_all,
+                                              const double* __restrict__ scalars,
+                                              float2* __restrict__ EM_all, int w, int h, int w_pad,
+                                              RangeConsts rc) {
+  const int f = blockIdx.z, x = blockIdx.x * 256 + threadIdx.x;
+  if (x >= w) return;
+  const Tin* in = in_all + (size_t)f * w * h;
+  float2* EM = EM_all + (size_t)f * h * w_pad;
+  const double t_c = scalars[2 * f];
+  for (int y = blockIdx.y; y < h; y += gridDim.y)
+    EM[(size_t)y * w_pad + x] = pixel_terms(static_cast<double>(in[(size_t)y * w + x]), t_c, rc);
+}
+
+// ----------------------------------------------------------------------------
+// K1b: exact anticausal carries of the column pass (same recursion as
+// k_col_carry) in pair groups: one CTA = 32 columns x kColGroup pairs. Per row
+// chunk (bottom-up) each thread holds eight pixels' seeds (es, m) -- loaded from
+// EM one chunk ahead, so the L2/HBM latency hides behind the current chunk's
+// dot products -- and builds the group's planes into a padded [pair][col][33]
+// tile; each thread (column, pair) then reduces its 32 rows into its carry
+// chain. 34 KB of smem and <= 64 registers: six CTAs per SM, so a frame's
+// 3 x (w/32) CTAs are resident in one wave.
+// ----------------------------------------------------------------------------
+__global__ void __launch_bounds__(32 * kColGroup, 6) k_col_carry_tma(
+    const float2* __restrict__ EM_all, float4* __restrict__ CA_all, int w, int h, int w_pad,
+    int ny, int pairs, int groups, FilterConsts fc, TileConsts tc) {
+  extern __shared__ float4 smem4[];
+  float2* buf = reinterpret_cast<float2*>(smem4);  // [kColGroup][32][33]
+  const int f = blockIdx.y, lane = threadIdx.x, gl = threadIdx.y;
+  const int tid = gl * 32 + lane;
+  const int strip = blockIdx.x / groups, grp = blockIdx.x - strip * groups;
+  const int pair0 = grp * kColGroup, npairs = min(kColGroup, pairs - pair0);
+  const int g = pair0 + gl;
+  const bool active = gl < npairs;
+  const int x0 = strip * 32, x = x0 + lane;
+  const float2* EM = EM_all + (size_t)f * h * w_pad;
+  float4* CA = CA_all + (size_t)f * ny * pairs * w * 2;
+  const float2* mine = buf + ((size_t)gl * 32 + lane) * 33;
+  // producer items: pixel (row gl + 4 k, column lane) for k = 0..7
+  constexpr int kItems = 32 / kColGroup;  // 8 rows per thread
+  const int xc = min(x, w - 1);           // out-of-image columns repeat the last (unused)
+  const size_t row_step = (size_t)kColGroup * w_pad;
+  float2 seed[kItems];
+  auto fetch = [&](int y0, int rows) {
+    const float2* src = EM + (size_t)(y0 + gl) * w_pad + xc;
+    if (rows == kTile) {
+#pragma unroll
+      for (int k = 0; k < kItems; ++k) seed[k] = __ldg(src + k * row_step);
+    } else {
+#pragma unroll
+      for (int k = 0; k < kItems; ++k)
+        seed[k] = gl + kColGroup * k < rows ? __ldg(src + k * row_step) : make_float2(0.f, 0.f);
+    }
+  };
+  fetch((ny - 1) * kTile, min(kTile, h - (ny - 1) * kTile));
+  PairState C;
+  ps_zero(C);
+  for (int cy = ny - 1; cy >= 0; --cy) {
+    const int y0 = cy * kTile, rows = min(kTile, h - y0);
+    // planes of the group for this thread's eight pixels
+    {
+      float xv[kItems], m[kItems];
+#pragma unroll
+      for (int k = 0; k < kItems; ++k) {
+        xv[k] = seed[k].x;
+        m[k] = seed[k].y;
+      }
+      if (pair0 > 0) {
+        float m4[kItems];
+#pragma unroll
+        for (int k = 0; k < kItems; ++k) {
+          m4[k] = m[k] * m[k];
+          m4[k] *= m4[k];
+        }
+        for (int n = 0; n < 2 * pair0; n += 4) {
+#pragma unroll
+          for (int k = 0; k < kItems; ++k) xv[k] *= m4[k];
+        }
+      }
+      float2* dst = buf + lane * 33 + gl;  // column lane, row gl + 4k
+#pragma unroll
+      for (int gg = 0; gg < kColGroup; ++gg) {
+        if (gg < npairs) {
+#pragma unroll
+          for (int k = 0; k < kItems; ++k) {
+            const float x1 = xv[k] * m[k];
+            dst[gg * 32 * 33 + kColGroup * k] = make_float2(xv[k], x1);
+            xv[k] = x1 * m[k];
+          }
+        }
+      }
+    }
+    if (cy > 0) fetch(y0 - kTile, kTile);  // next chunk's seeds, in flight during the dots
+    __syncthreads();
+    if (active && x < w) {
+      if (cy == ny - 1) ps_set_gain(C, mine[rows - 1], fc);
+      ps_store(CA + ((size_t)cy * pairs + g) * w * 2 + (size_t)x * 2, C);
+      if (cy > 0) {
+        PairState agg;
+        ps_zero(agg);
+        if (rows == kTile) {
+#pragma unroll
+          for (int j = 0; j < kTile; ++j)
+            ps_accum(agg, mine[j], tc.wr2[0][j], tc.wi2[0][j], tc.wr2[1][j], tc.wi2[1][j]);
+        } else {
+          for (int j = 0; j < rows; ++j)
+            ps_accum(agg, mine[j], tc.wr2[0][j], tc.wi2[0][j], tc.wr2[1][j], tc.wi2[1][j]);
+        }
+        if (cy == ny - 1) ps_chain(C, agg, tc.pYr2, tc.pYi2);
+        else ps_chain(C, agg, tc.pTr2, tc.pTi2);
+      }
+    }
+    __syncthreads();  // the tile is rebuilt for the next chunk
+  }
+}
+
 template <int MAXT, typename Tin>
 __global__ void __launch_bounds__(MAXT, 1) k_colpass(const Tin* __restrict__ in_all,
                                                      const double* __restrict__ scalars,
@@ -744,7 +865,8 @@ void plan_init(Plan& plan, const Params& p, int device, int batch) {
     throw;
   }
   plan.bytes = vb + cab + 2 * ahb + emb + sizeof(double) * 2 * B * (1 + plan.mean_blocks);
-  plan.launches_per_frame = 6;
+  // mean (2), [seed,] carries, column pass, row scan, row pass
+  plan.launches_per_frame = 32 * pairs <= 512 ? 7 : 6;
   // TMA tensor maps of the band-major V: fp32 dims (inner first)
   // {32 = 16 rows x 2 planes, w, h_pad/16 bands, pairs, batch}.
   static PFN_cuTensorMapEncodeTiled_v12000 encode = nullptr;
@@ -832,14 +954,25 @@ static void launch_passes(Plan& plan, const Tin* d_in, Tout* d_out, int count,
                              rsm),
         "cudaFuncSetAttribute");
   const dim3 blk(32, pairs);
+  const int groups = (pairs + kColGroup - 1) / kColGroup;
   stage_mark(plan, kStageColCarry, st);
-  k_col_carry<MAXT, Tin><<<dim3(plan.nx, count), blk, csm, st>>>(
-      d_in, plan.scalars, plan.CA, plan.EM, w, h, plan.w_pad, plan.ny, plan.fc, plan.tc, plan.rc);
+  if constexpr (kCanStage) {
+    // seeds once per pixel, then the carries in pair groups
+    k_seed<Tin><<<dim3((w + 255) / 256, std::min(h, 1024), count), 256, 0, st>>>(
+        d_in, plan.scalars, plan.EM, w, h, plan.w_pad, plan.rc);
+    const int ksm = (int)(sizeof(float2) * kColGroup * 32 * 33);
+    check(cudaFuncSetAttribute(k_col_carry_tma, cudaFuncAttributeMaxDynamicSharedMemorySize, ksm),
+          "cudaFuncSetAttribute");
+    k_col_carry_tma<<<dim3(plan.nx * groups, count), dim3(32, kColGroup), ksm, st>>>(
+        plan.EM, plan.CA, w, h, plan.w_pad, plan.ny, pairs, groups, plan.fc, plan.tc);
+  } else {
+    k_col_carry<MAXT, Tin><<<dim3(plan.nx, count), blk, csm, st>>>(
+        d_in, plan.scalars, plan.CA, plan.EM, w, h, plan.w_pad, plan.ny, plan.fc, plan.tc, plan.rc);
+  }
   stage_mark(plan, kStageColPass, st);
   if constexpr (kCanStage) {
     check(cudaFuncSetAttribute(k_colpass_tma, cudaFuncAttributeMaxDynamicSharedMemorySize, psm),
           "cudaFuncSetAttribute");
-    const int groups = (pairs + kColGroup - 1) / kColGroup;
     k_colpass_tma<<<dim3(plan.nx * groups, count), dim3(32, kColGroup), psm, st>>>(
         plan.CA, plan.AH, w, h, plan.ny, plan.nx, pairs, groups, plan.fc, plan.tc, plan.emmap,
         plan.vstore);
