@@ -47,6 +47,9 @@ def parse():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", choices=["b200", "reference"], default="b200")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--workload", choices=["c3", "c4"], default="c3",
+                    help="c3 (default, the metric's config): 8192^2 sigma_s sweep, replicas per GPU; "
+                         "c4: 64 frames x 3 channels of 3840x2160 sharded across the GPUs")
     return ap.parse_args()
 
 
@@ -166,6 +169,37 @@ def algorithmic_bytes_per_px(pairs: int) -> dict:
             "rowpass": 9 * pairs + 8}
 
 
+def algorithmic_flops_per_px(pairs: int) -> dict:
+    """FP32 FLOPs each stage must issue per pixel (FMA = 2), P = plane pairs.
+    One IIR step of one plane: two complex sections advanced (3 FMA + 1 MUL
+    each) and emitted (3 FMA + 1 MUL for both) = 21; both directions + the
+    sum = 43, i.e. 86 per pair. Strip/chunk dot products: 4 FMA per plane.
+      carries    seeds ~20 + per pair: planes 2 MUL, dots 16          18 P + 20
+      colpass    per pair: planes 2, sweeps 86, row dots 16          104 P
+      row_scan   per pair: one chain step per 32 pixels              ~P
+      rowpass    per pair: sweeps 86, contraction 16 (8 per plane)   102 P + 10"""
+    return {"mean": 1, "col_carry": 18 * pairs + 20, "colpass": 104 * pairs, "row_scan": pairs,
+            "rowpass": 102 * pairs + 10}
+
+
+def fp32_peak_tflops(peaks: dict) -> float:
+    """Nominal FP32 FMA peak: 148 SMs x 128 FMA/clk x 2 FLOP x max SM clock."""
+    return 148 * 128 * 2 * peaks.get("sm_max_mhz", 1965.0) * 1e6 / 1e12
+
+
+def roofline_of(px: int, ms: float, bpp: int, fpp: int, hbm_gbs: float, fp32_tf: float) -> dict:
+    """Achieved vs the slower of HBM bytes and FP32 FLOPs (north_star)."""
+    t_hbm = bpp * px / (hbm_gbs * 1e9)
+    t_fp = fpp * px / (fp32_tf * 1e12)
+    if t_hbm >= t_fp:
+        ach = bpp * px / (ms / 1e3) / 1e9
+        return {"bound": "hbm", "achieved": round(ach, 1), "peak": hbm_gbs, "unit": "GB/s",
+                "frac": round(ach / hbm_gbs, 4)}
+    ach = fpp * px / (ms / 1e3) / 1e12
+    return {"bound": "fp32", "achieved": round(ach, 2), "peak": round(fp32_tf, 1), "unit": "TFLOP/s",
+            "frac": round(ach / fp32_tf, 4)}
+
+
 # ------------------------------------------------------------- B200 leg
 def bench_b200(args):
     import numpy as np
@@ -245,23 +279,35 @@ def bench_b200(args):
     p5.set_profiling(False)
     pairs = (N + 3) // 2
     bpp = algorithmic_bytes_per_px(pairs)
+    fpp = algorithmic_flops_per_px(pairs)
     dom = max(stage_ms, key=stage_ms.get)
     peaks = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json"))) if os.path.exists(
         os.path.join(ROOT, "MEASURED_PEAKS.json")) else {}
     hbm_peak = peaks.get("hbm_gbs", 6650.0)
-    achieved = bpp[dom] * px / (stage_ms[dom] / 1e3) / 1e9
+    fp32_tf = fp32_peak_tflops(peaks)
     traffic = None
     tpath = os.path.join(ROOT, "profiles", "ncu_traffic.json")
     if os.path.exists(tpath):
         t = json.load(open(tpath))
         if t.get("width") == W and t.get("height") == H and dom in t.get("bytes_per_launch", {}):
             traffic = t["bytes_per_launch"][dom]
-    # whole-step view against the SURVEY 8(d) model: 8(N+2)+12 B/px at HBM peak,
-    # and against this design's own traffic (sum of the stages above)
-    model_bpp = 8 * (N + 2) + 12
+    roof = roofline_of(px, stage_ms[dom], bpp[dom], fpp[dom], hbm_peak, fp32_tf)
+    fp_k = fpp[dom] * px / (stage_ms[dom] / 1e3) / 1e12
+    # whole step: all stages' bytes and FLOPs against the same peaks
+    design_bpp, design_fpp = sum(bpp.values()), sum(fpp.values())
+    step = roofline_of(px * frames, ms_step, design_bpp, design_fpp, hbm_peak, fp32_tf)
+    model_bpp = 8 * (N + 2) + 12  # SURVEY 8(d) streaming model
     model_frac = (model_bpp * px * frames / (ms_step / 1e3) / 1e9) / hbm_peak
-    design_bpp = sum(bpp.values())
-    design_frac = (design_bpp * px * frames / (ms_step / 1e3) / 1e9) / hbm_peak
+    roofline = dict(roof, kernel=dom, traffic=traffic, algorithmic_bytes_per_px=bpp[dom],
+                    algorithmic_flops_per_px=fpp[dom],
+                    fp32={"achieved_tflops": round(fp_k, 2), "peak_tflops": round(fp32_tf, 1),
+                          "frac": round(fp_k / fp32_tf, 4),
+                          "peak_source": "nominal 148 SM x 128 FMA/clk x 2 x sm_max_mhz"},
+                    peak_source="MEASURED_PEAKS.json hbm_gbs (burst copy)",
+                    step=dict(step, bytes_per_px=design_bpp, flops_per_px=design_fpp,
+                              what="all stages of the step, slower of HBM bytes and FP32 FLOPs"),
+                    step_model_frac=round(model_frac, 4),
+                    step_model=f"SURVEY 8(d): {model_bpp} B/px at HBM peak")
 
     # end to end through the C ABI: pinned host fp32 in -> host fp32 out
     # One host thread per sigma_s plan (the C call releases the GIL; each plan
@@ -328,18 +374,164 @@ def bench_b200(args):
                    "parallelism": f"frame replicas x{world}, no collective"},
         "sigma_s_ms_per_frame": per_sigma,
         "stage_ms_per_frame": {k: round(v, 4) for k, v in stage_ms.items()},
-        "roofline": {"bound": "hbm", "kernel": dom, "achieved": round(achieved, 1),
-                     "peak": hbm_peak, "unit": "GB/s", "frac": round(achieved / hbm_peak, 4),
-                     "traffic": traffic, "algorithmic_bytes_per_px": bpp[dom],
-                     "peak_source": "MEASURED_PEAKS.json hbm_gbs (burst copy)",
-                     "step_model_frac": round(model_frac, 4),
-                     "step_model": f"SURVEY 8(d): {model_bpp} B/px at HBM peak",
-                     "step_design_frac": round(design_frac, 4),
-                     "step_design": f"all stages: {design_bpp} B/px at HBM peak"},
+        "roofline": roofline,
         "e2e": e2e,
         "cpu_baseline": cpu,
         "gpu_launches": launches,
         "fallbacks": fallbacks,
+        "clocks": clk,
+    }
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        torch.distributed.destroy_process_group()
+
+
+# ------------------------------------------------------------- C4 frame batch
+def build_c4_frames(d_in, first: int, cfg):
+    """Problems first .. first+len(d_in)-1 of C4 (problem i = frame i // 3,
+    channel i % 3) on the device: the synth gradient + the channel's rectangle
+    layer drifted 4 px per frame + N(0, noise^2) (torch-seeded per problem),
+    clipped to [0, 255]."""
+    import numpy as np
+    import torch
+
+    from paper_1505_00077_b200 import synth
+    H, W = cfg.height, cfg.width
+    base = cfg.cid * 1000
+    layers = [torch.from_numpy(synth._rect_layer(np.random.default_rng(base + c), W, H, 48)).float().cuda()
+              for c in range(cfg.channels)]
+    x = torch.arange(W, device="cuda", dtype=torch.float32) / max(1, W - 1)
+    y = torch.arange(H, device="cuda", dtype=torch.float32) / max(1, H - 1)
+    grad = 32.0 * (x[None, :] + y[:, None])
+    g = torch.Generator(device="cuda")
+    for k in range(d_in.shape[0]):
+        i = first + k
+        fr, ch = divmod(i, cfg.channels)
+        dx = min(4 * fr, W)
+        img = grad.clone()
+        img[:, dx:] += layers[ch][:, :W - dx]
+        g.manual_seed(base + fr * 3 + ch + 500)
+        img += cfg.noise * torch.randn((H, W), generator=g, device="cuda")
+        d_in[k] = img.clamp_(0.0, 255.0)
+
+
+def bench_c4(args):
+    import torch
+
+    from paper_1505_00077_b200 import gpf, shard, synth
+
+    rank, world, local = dist_env()
+    torch.cuda.set_device(local)
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    cfg = synth.CONFIGS[4]
+    W, H, ss, sr, N = cfg.width, cfg.height, cfg.sigma_s[0], cfg.sigma_r, cfg.degree
+    n_items = cfg.frames * cfg.channels
+    first, stop = shard.shard_range(n_items, rank, world)
+    n_loc = stop - first
+    px = W * H
+    d_in = torch.empty((max(n_loc, 1), H, W), dtype=torch.float32, device="cuda")
+    build_c4_frames(d_in[:n_loc], first, cfg)
+    d_out = torch.empty_like(d_in)
+    d_fb = torch.zeros(max(n_loc, 1), dtype=torch.int64, device="cuda")
+    plan = gpf.Plan(W, H, ss, sr, N, batch=max(1, min(n_loc, 8)))
+    st = torch.cuda.current_stream()
+
+    def step():
+        if n_loc:
+            plan.filter_device(d_in, d_out, n_loc, d_fb, st.cuda_stream)
+
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+    if world > 1:
+        torch.distributed.barrier()
+    torch.cuda.synchronize()
+    clocks = ClockSampler(local)
+    clocks.start()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(st)
+    for _ in range(args.steps):
+        step()
+    e1.record(st)
+    torch.cuda.synchronize()
+    ms_local = e0.elapsed_time(e1)
+    clk = clocks.stop()
+    if world > 1:
+        torch.distributed.barrier()
+    secs, fallbacks = shard.reduce_job(ms_local / 1e3, d_fb[:n_loc].cpu().tolist(), n_items, rank,
+                                       world, device="cuda")
+    ms_step = secs * 1e3 / args.steps
+    value = n_items * px / (ms_step / 1e3) / 1e6
+
+    # per-stage timing of one frame (dominant kernel) and the roofline
+    plan.set_profiling(True)
+    reps = 3
+    for _ in range(reps):
+        plan.filter_device(d_in, d_out, 1, None, st.cuda_stream)
+    torch.cuda.synchronize()
+    stage_ms = {k: v / reps for k, v in plan.stage_times().items()}
+    plan.set_profiling(False)
+    pairs = (N + 3) // 2
+    bpp, fpp = algorithmic_bytes_per_px(pairs), algorithmic_flops_per_px(pairs)
+    dom = max(stage_ms, key=stage_ms.get)
+    peaks = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json"))) if os.path.exists(
+        os.path.join(ROOT, "MEASURED_PEAKS.json")) else {}
+    hbm_peak, fp32_tf = peaks.get("hbm_gbs", 6650.0), fp32_peak_tflops(peaks)
+    roof = roofline_of(px, stage_ms[dom], bpp[dom], fpp[dom], hbm_peak, fp32_tf)
+    step_roof = roofline_of(n_items * px, ms_step, sum(bpp.values()), sum(fpp.values()),
+                            hbm_peak * world, fp32_tf * world)
+    roofline = dict(roof, kernel=dom, traffic=None, algorithmic_bytes_per_px=bpp[dom],
+                    algorithmic_flops_per_px=fpp[dom],
+                    peak_source="MEASURED_PEAKS.json hbm_gbs (burst copy)",
+                    step=dict(step_roof, what=f"whole job on {world} GPU(s), peaks x {world}"))
+
+    # end to end: this rank's frames from pinned host memory through the
+    # pipelined host entry (H2D of frame f+1 overlaps compute of f), every step
+    h_in = d_in[:max(n_loc, 1)].cpu().pin_memory()
+    h_out = torch.empty_like(h_in).pin_memory()
+    h_in_np, h_out_np = h_in.numpy(), h_out.numpy()
+    if n_loc:
+        plan.filter_host(h_in_np[:n_loc], h_out_np[:n_loc])
+    torch.cuda.synchronize()
+    if world > 1:
+        torch.distributed.barrier()
+    e2e_steps = max(1, min(args.steps, 3))
+    t0 = time.perf_counter()
+    for _ in range(e2e_steps):
+        if n_loc:
+            plan.filter_host(h_in_np[:n_loc], h_out_np[:n_loc])
+    e2e_s, _ = shard.reduce_job((time.perf_counter() - t0) / e2e_steps, [0] * n_loc, n_items, rank,
+                                world, device="cuda")
+    e2e = {"value": round(n_items * px / e2e_s / 1e6, 1), "unit": UNIT,
+           "h2d_bytes_per_step": n_items * px * 4, "d2h_bytes_per_step": n_items * (px * 4 + 8),
+           "api": "gpf_b200_filter_f32_host (pinned host fp32 in/out, all local frames per call, "
+                  "H2D/compute/D2H pipelined inside)"}
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        thr = cpu_threads()
+        v, sec, kind = cpu_reference_run((ss,), sr, N, 1, thr)
+        cpu = {"value": round(v, 3), "unit": UNIT, "cores": thr, "kind": kind,
+               "sample": f"{SAMPLE_W}x{SAMPLE_H} generator frame at sigma_s {ss}, sigma_r {sr}, N {N} "
+                         f"({sec:.1f} s of CPU work)"}
+    line = {
+        "metric": METRIC, "value": round(value, 1), "unit": UNIT, "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms_step, 4),
+        "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "fp32",
+        "data": "synthetic (C4 generator on device: drifting rectangles + seeded noise)",
+        "config": {"workload": f"C4: {cfg.frames} frames x {cfg.channels} channels of {W}x{H} fp32, "
+                               f"sigma_s {ss}, sigma_r {sr}, N {N}; {n_items} independent problems "
+                               f"sharded contiguously ({shard.shard_sizes(n_items, world)})",
+                   "l2": "inputs larger than L2 (33 MB per problem x %d per GPU); no flush" % n_loc,
+                   "parallelism": f"frame shards x{world}, no collective on the data path"},
+        "stage_ms_per_frame": {k: round(v, 4) for k, v in stage_ms.items()},
+        "roofline": roofline,
+        "e2e": e2e,
+        "cpu_baseline": cpu,
+        "gpu_launches": args.steps * n_loc * plan.launches_per_frame,
+        "fallbacks_total": int(sum(fallbacks)),
         "clocks": clk,
     }
     if rank == 0:
@@ -353,16 +545,17 @@ def bench_reference(args):
     if rank != 0:
         return
     from paper_1505_00077_b200 import synth
-    cfg = synth.CONFIGS[CFG_ID]
+    cfg = synth.CONFIGS[4 if args.workload == "c4" else CFG_ID]
     thr = cpu_threads()
     cpu_reference_run(cfg.sigma_s, cfg.sigma_r, cfg.degree, args.warmup, thr) if args.warmup else None
     v, sec, kind = cpu_reference_run(cfg.sigma_s, cfg.sigma_r, cfg.degree, args.steps, thr)
     line = {
         "impl": "reference", "metric": METRIC, "value": round(v, 3), "unit": UNIT, "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(sec * 1e3, 1),
-        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "fp64",
+        "higher_is_better": True, "scaling": "strong" if args.workload == "c4" else "weak",
+        "vs_baseline": None, "dtype": "fp64",
         "data": "synthetic (seeded generator, SURVEY.md 8(d))",
-        "config": {"workload": f"C3 sample: {SAMPLE_W}x{SAMPLE_H} generator frame, sigma_r "
+        "config": {"workload": f"C{cfg.cid} sample: {SAMPLE_W}x{SAMPLE_H} generator frame, sigma_r "
                                f"{cfg.sigma_r}, N {cfg.degree}, sigma_s sweep {list(cfg.sigma_s)}",
                    "parallelism": f"{thr} host threads (gpf_set_num_threads)"},
         "cpu_baseline": {"value": round(v, 3), "unit": UNIT, "cores": thr, "kind": kind,
@@ -378,6 +571,8 @@ def main():
         relaunch_under_torchrun(args)
     if args.impl == "reference":
         bench_reference(args)
+    elif args.workload == "c4":
+        bench_c4(args)
     else:
         bench_b200(args)
 
