@@ -29,6 +29,7 @@
 //   AH [nx][pairs][h]   2xfloat4  per-strip row aggregates sum_i p^i V (K2)
 //   CH [nx][pairs][h]   2xfloat4  row anticausal carries (K3)
 #include <algorithm>
+#include <cstring>
 #include <string>
 #include <vector>
 
@@ -826,6 +827,34 @@ void run_gaussian_f64(const double* d_in, double* d_out, double* d_tmp, int w, i
   check(cudaGetLastError(), "kernel launch");
 }
 
+static PFN_cuTensorMapEncodeTiled_v12000 tensor_map_encoder() {
+  static PFN_cuTensorMapEncodeTiled_v12000 encode = nullptr;
+  if (!encode) {
+    cudaDriverEntryPointQueryResult q;
+    check(cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", reinterpret_cast<void**>(&encode),
+                                  cudaEnableDefault, &q),
+          "cudaGetDriverEntryPoint(cuTensorMapEncodeTiled)");
+    if (q != cudaDriverEntryPointSuccess || !encode)
+      throw Error{9, "cuTensorMapEncodeTiled unavailable"};
+  }
+  return encode;
+}
+
+// Output frames fp32 {w, h, count}, box {32 columns, 16 rows, 1}, 128B-swizzled
+// (the row pass's output tile); requires w % 4 == 0 and a 16-B aligned base.
+static void encode_out_map(CUtensorMap* m, void* d_out, int w, int h, int count) {
+  const cuuint64_t dims[3] = {(cuuint64_t)w, (cuuint64_t)h, (cuuint64_t)count};
+  const cuuint64_t strides[2] = {(cuuint64_t)4 * w, (cuuint64_t)4 * w * h};
+  const cuuint32_t box[3] = {32, (cuuint32_t)kRowBand, 1};
+  const cuuint32_t estr[3] = {1, 1, 1};
+  const CUresult r = tensor_map_encoder()(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, d_out, dims, strides,
+                                          box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                                          CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_NONE,
+                                          CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS)
+    throw Error{9, "cuTensorMapEncodeTiled (output) failed (" + std::to_string((int)r) + ")"};
+}
+
 void plan_init(Plan& plan, const Params& p, int device, int batch) {
   plan.p = p;
   plan.device = device;
@@ -869,15 +898,7 @@ void plan_init(Plan& plan, const Params& p, int device, int batch) {
   plan.launches_per_frame = 32 * pairs <= 512 ? 7 : 6;
   // TMA tensor maps of the band-major V: fp32 dims (inner first)
   // {32 = 16 rows x 2 planes, w, h_pad/16 bands, pairs, batch}.
-  static PFN_cuTensorMapEncodeTiled_v12000 encode = nullptr;
-  if (!encode) {
-    cudaDriverEntryPointQueryResult q;
-    check(cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", reinterpret_cast<void**>(&encode),
-                                  cudaEnableDefault, &q),
-          "cudaGetDriverEntryPoint(cuTensorMapEncodeTiled)");
-    if (q != cudaDriverEntryPointSuccess || !encode)
-      throw Error{9, "cuTensorMapEncodeTiled unavailable"};
-  }
+  const auto encode = tensor_map_encoder();
   const cuuint64_t nb = (cuuint64_t)h_pad / 16;
   const cuuint64_t dims[5] = {32, (cuuint64_t)w, nb, (cuuint64_t)pairs, (cuuint64_t)B};
   const cuuint64_t strides[4] = {128, (cuuint64_t)128 * w, (cuuint64_t)128 * w * nb,
@@ -990,12 +1011,23 @@ static void launch_passes(Plan& plan, const Tin* d_in, Tout* d_out, int count,
   stage_mark(plan, kStageRowPass, st);
   if (pairs <= 12) {
     const int r2sm = (int)rowpass2_smem_bytes<Tin, Tout>(pairs);
+    // fp32 output with 16-B rows: TMA output store (tensor map of this call's d_out)
+    const bool otma = sizeof(Tout) == 4 && (w % 4) == 0 &&
+                      (reinterpret_cast<uintptr_t>(d_out) % 16) == 0;
+    alignas(64) CUtensorMap omap;
+    std::memset(&omap, 0, sizeof(omap));
+    if (otma) encode_out_map(&omap, d_out, w, h, count);
     // the default degree (N = 20, reference RangeParams) has a fully static build
-    auto k = plan.rc.degree == 20 ? k_rowpass2<Tin, Tout, 20> : k_rowpass2<Tin, Tout, 0>;
+    const bool n20 = plan.rc.degree == 20;
+    auto k = n20 ? k_rowpass2<Tin, Tout, 20, false> : k_rowpass2<Tin, Tout, 0, false>;
+    if constexpr (sizeof(Tout) == 4) {
+      if (otma) k = n20 ? k_rowpass2<Tin, Tout, 20, true> : k_rowpass2<Tin, Tout, 0, true>;
+    }
     check(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, r2sm),
           "cudaFuncSetAttribute");
     k<<<dim3((h + kRowBand - 1) / kRowBand, count), dim3(32, (pairs + 1) / 2), r2sm, st>>>(
-        d_in, plan.scalars, plan.CH, d_out, d_fb, w, h, plan.nx, pairs, plan.fc, plan.rc, plan.vmap);
+        d_in, plan.scalars, plan.CH, d_out, d_fb, w, h, plan.nx, pairs, plan.fc, plan.rc, plan.vmap,
+        omap);
   } else {
     k_rowpass<RMAXT, Tin, Tout><<<dim3((h + kRowBand - 1) / kRowBand, count),
                                   dim3(32, (pairs + 1) / 2 + kAux), rsm, st>>>(

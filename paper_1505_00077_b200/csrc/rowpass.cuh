@@ -268,9 +268,10 @@ constexpr int kRow2MaxN = 22;  // pairs <= 12
 
 template <typename Tin, typename Tout>
 __host__ __device__ constexpr size_t rowpass2_smem_bytes(int pairs) {
+  // V ring | f tiles | padded output tile | mbarriers | 1024-aligned swizzled output tile
   return sizeof(float2) * (size_t)pairs * 32 * kRowBand * kRow2Slots +
          sizeof(Tin) * kRowBand * 33 * kRow2Slots + sizeof(Tout) * kRowBand * 33 +
-         kRow2Slots * sizeof(uint64_t) + 16;
+         kRow2Slots * sizeof(uint64_t) + 16 + 1024 + sizeof(float) * kRowBand * 32;
 }
 
 // Contraction of kPx pixels per thread (pixel p -> row p & 15, column p >> 4),
@@ -278,7 +279,9 @@ __host__ __device__ constexpr size_t rowpass2_smem_bytes(int pairs) {
 // weight pair advances componentwise, (c_{m+1}, c_m) = (c_m, c_{m-1}) * H
 // (w_m, w_{m-1}): three packed instructions per plane. Plane 0 is Q-only,
 // plane N+1 P-only (bilateral.cpp:117-148). Returns the fallback count.
-template <int kPx, int NFIX, typename Tin, typename Tout>
+// OSW: write into the 128B-swizzled [16][32] fp32 tile of the TMA output store
+// (element (r, c) at r*32 + (((c/4) ^ (r%8)) * 4) + c%4) instead of the padded O.
+template <int kPx, int NFIX, bool OSW, typename Tin, typename Tout>
 __device__ __forceinline__ unsigned contract_px(const float2* Ts, const Tin* Fs, Tout* O, int p0,
                                                 int nthr, int rows, int cols, const RangeConsts& rc,
                                                 double t_c, float sr_f, float tc_hi, float tc_lo) {
@@ -332,11 +335,11 @@ __device__ __forceinline__ unsigned contract_px(const float2* Ts, const Tin* Fs,
   for (int k = 0; k < kPx; ++k) {
     const int p = p0 + k * nthr;
     const int pr = p & (kRowBand - 1), pc = p >> 4;
-    if (p < kRowBand * 32 && pr < rows && pc < cols) {
+    if (p < kRowBand * 32 && (OSW || (pr < rows && pc < cols))) {  // the TMA store clips
       Tout o;
       if (!(fabsf(qp[k].x) > rc.q_thresh)) {
         o = static_cast<Tout>(Fs[pr * 33 + pc]);
-        ++nfb;
+        if (pr < rows && pc < cols) ++nfb;
       } else if constexpr (sizeof(Tout) == sizeof(float)) {
         // fast quotient (2 ulp) inside its range; |Q| > threshold >> 2^-126 here
         const float num = qp[k].y * rc.p_scale, den = qp[k].x;
@@ -346,7 +349,8 @@ __device__ __forceinline__ unsigned contract_px(const float2* Ts, const Tin* Fs,
         o = rc.sigma_r * ((static_cast<double>(qp[k].y) * rc.p_scale) / static_cast<double>(qp[k].x)) +
             t_c;
       }
-      O[pr * 33 + pc] = o;
+      if constexpr (OSW) O[pr * 32 + ((((pc >> 2) ^ (pr & 7))) << 2) + (pc & 3)] = o;
+      else O[pr * 33 + pc] = o;
     }
   }
   return nfb;
@@ -354,7 +358,11 @@ __device__ __forceinline__ unsigned contract_px(const float2* Ts, const Tin* Fs,
 
 // NFIX > 0: the degree N is a compile-time constant (the default N = 20 build);
 // NFIX = 0: runtime N (<= kRow2MaxN).
-template <typename Tin, typename Tout, int NFIX>
+// OTMA (fp32 output, width % 4 == 0): the contraction fills a 128B-swizzled
+// [16][32] tile and one thread stores it with a TMA tensor store (`omap` =
+// the caller's output), which drains under the next strip's sweeps; else the
+// warps write the tile out row by row.
+template <typename Tin, typename Tout, int NFIX, bool OTMA>
 __global__ void __launch_bounds__(192, 2) k_rowpass2(const Tin* __restrict__ in_all,
                                                       const double* __restrict__ scalars,
                                                       const float4* __restrict__ CH_all,
@@ -362,7 +370,8 @@ __global__ void __launch_bounds__(192, 2) k_rowpass2(const Tin* __restrict__ in_
                                                       unsigned long long* __restrict__ fb_all,
                                                       int w, int h, int nx, int pairs,
                                                       FilterConsts fc, RangeConsts rc,
-                                                      const __grid_constant__ CUtensorMap vmap) {
+                                                      const __grid_constant__ CUtensorMap vmap,
+                                                      const __grid_constant__ CUtensorMap omap) {
   extern __shared__ float4 smem4[];
   const int f = blockIdx.y, lane = threadIdx.x, warp = threadIdx.y;
   const int tid = warp * 32 + lane, nthr = blockDim.x * blockDim.y;
@@ -374,6 +383,13 @@ __global__ void __launch_bounds__(192, 2) k_rowpass2(const Tin* __restrict__ in_
   Tout* O = reinterpret_cast<Tout*>(F + kRow2Slots * kRowBand * 33);  // [16 rows][33]
   uint64_t* full = reinterpret_cast<uint64_t*>(
       (reinterpret_cast<uintptr_t>(O + kRowBand * 33) + 15) & ~uintptr_t(15));
+  // swizzled output tile, 1024-aligned in the shared window (offset from the base)
+  float* O2;
+  {
+    char* base = reinterpret_cast<char*>(smem4);
+    const uint32_t a = smem_u32(full + kRow2Slots);
+    O2 = reinterpret_cast<float*>(base + (((a + 1023u) & ~1023u) - smem_u32(base)));
+  }
   const Tin* in = in_all + (size_t)f * w * h;
   Tout* out = out_all + (size_t)f * w * h;
   const double t_c = scalars[2 * f];
@@ -486,6 +502,7 @@ __global__ void __launch_bounds__(192, 2) k_rowpass2(const Tin* __restrict__ in_
     // this strip's f tile: the newer group (strip b+1) may stay in flight
     if (b + 1 < nx) asm volatile("cp.async.wait_group 1;\n" ::: "memory");
     else asm volatile("cp.async.wait_group 0;\n" ::: "memory");
+    if (OTMA && tid == 0) bulk_wait_read_all();  // the previous strip's store has left O2
     __syncthreads();
     GPF_TICK(2);
     // ---- 2. contraction: pixel p -> (row p & 15, col p >> 4); three pixels
@@ -498,24 +515,36 @@ __global__ void __launch_bounds__(192, 2) k_rowpass2(const Tin* __restrict__ in_
     for (int p0 = tid; p0 < kRowBand * 32; p0 += nthr * 3) {
       // pixels per thread for this warp (warp-uniform: no work on pixels past the strip)
       const int wb = p0 - lane;
+      Tout* Od = OTMA ? reinterpret_cast<Tout*>(O2) : O;
       if (wb + 2 * nthr + 31 < kRowBand * 32)
-        my_fb += contract_px<3, NFIX>(Ts, Fs, O, p0, nthr, rows, cols, rc, t_c, sr_f, tc_hi, tc_lo);
+        my_fb += contract_px<3, NFIX, OTMA>(Ts, Fs, Od, p0, nthr, rows, cols, rc, t_c, sr_f, tc_hi, tc_lo);
       else if (wb + nthr < kRowBand * 32)
-        my_fb += contract_px<2, NFIX>(Ts, Fs, O, p0, nthr, rows, cols, rc, t_c, sr_f, tc_hi, tc_lo);
+        my_fb += contract_px<2, NFIX, OTMA>(Ts, Fs, Od, p0, nthr, rows, cols, rc, t_c, sr_f, tc_hi, tc_lo);
       else
-        my_fb += contract_px<1, NFIX>(Ts, Fs, O, p0, nthr, rows, cols, rc, t_c, sr_f, tc_hi, tc_lo);
+        my_fb += contract_px<1, NFIX, OTMA>(Ts, Fs, Od, p0, nthr, rows, cols, rc, t_c, sr_f, tc_hi, tc_lo);
     }
     GPF_TICK(3);
-    __syncthreads();
-    // ---- 3. write-out (row segments of 32, coalesced) and refill the slot
-    for (int p = tid; p < kRowBand * 32; p += nthr) {
-      const int pr = p >> 5, pc = p & 31;
-      if (pr < rows && pc < cols) out[(size_t)(y0 + pr) * w + xs + pc] = O[pr * 33 + pc];
+    if constexpr (OTMA) {
+      fence_proxy_async();  // O2 writes -> visible to the TMA store
+      __syncthreads();      // slot s, its f tile are free; O2 is complete
+      if (tid == 0) {
+        tma_store_3d(&omap, xs, y0, f, O2);  // clipped to the image
+        bulk_commit();
+      }
+      GPF_TICK(4);
+    } else {
+      __syncthreads();
+      // ---- 3. write-out (row segments of 32, coalesced)
+      for (int p = tid; p < kRowBand * 32; p += nthr) {
+        const int pr = p >> 5, pc = p & 31;
+        if (pr < rows && pc < cols) out[(size_t)(y0 + pr) * w + xs + pc] = O[pr * 33 + pc];
+      }
+      GPF_TICK(4);
+      __syncthreads();  // slot s, its f tile and O are free again
     }
-    GPF_TICK(4);
-    __syncthreads();  // slot s, its f tile and O are free again
     if (b + kRow2Slots < nx) load_strip(b + kRow2Slots, s);
   }
+  if (OTMA && tid == 0) bulk_wait_all();  // the output is complete before the CTA retires
 #ifdef GPF_DIAG_CLOCKS
   if ((blockIdx.x == 100 || blockIdx.x == 101 || blockIdx.x == 400) && (tid == 0 || tid == 160))
     printf("cta %d tid %d: waitV %lld sweep %lld fbar %lld contract %lld write %lld load %lld (per strip)\n",

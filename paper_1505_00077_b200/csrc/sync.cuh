@@ -96,6 +96,13 @@ __device__ __forceinline__ void tma_store_5d(const void* tmap, int c0, int c1, i
       "r"(c0), "r"(c1), "r"(c2), "r"(c3), "r"(c4), "r"(smem_u32(src))
       : "memory");
 }
+// 3-D tensor-map tile store (TMA) shared -> global, tracked by bulk groups.
+__device__ __forceinline__ void tma_store_3d(const void* tmap, int c0, int c1, int c2, const void* src) {
+  asm volatile(
+      "cp.async.bulk.tensor.3d.global.shared::cta.bulk_group [%0, {%1, %2, %3}], [%4];\n" ::"l"(tmap),
+      "r"(c0), "r"(c1), "r"(c2), "r"(smem_u32(src))
+      : "memory");
+}
 __device__ __forceinline__ void bulk_commit() { asm volatile("cp.async.bulk.commit_group;\n" ::: "memory"); }
 // Source smem of every committed bulk store has been read (may be reused).
 __device__ __forceinline__ void bulk_wait_read_all() {
