@@ -326,7 +326,15 @@ __device__ __forceinline__ void produce_group(float* stage, const float2* emt, i
 // CTAs share an SM so one's producer / H-dot phases overlap another's sweeps.
 constexpr int kColGroup = 4;
 
-__global__ void __launch_bounds__(32 * kColGroup, 3) k_colpass_tma(
+#ifndef GPF_COL_STAGES
+#define GPF_COL_STAGES 1
+#endif
+#ifndef GPF_COL_CTAS
+#define GPF_COL_CTAS 4
+#endif
+constexpr int kColStages = GPF_COL_STAGES;  // staging tiles per CTA (1: store drains under the H-dots)
+
+__global__ void __launch_bounds__(32 * kColGroup, GPF_COL_CTAS) k_colpass_tma(
     const float4* __restrict__ CA_all, float4* __restrict__ AH_all, int w, int h, int ny, int nx,
     int pairs, int groups, FilterConsts fc, TileConsts tc,
     const __grid_constant__ CUtensorMap emmap, const __grid_constant__ CUtensorMap vstore) {
@@ -346,7 +354,7 @@ __global__ void __launch_bounds__(32 * kColGroup, 3) k_colpass_tma(
   float* stages = reinterpret_cast<float*>(reinterpret_cast<char*>(smem4) +
                                            ((kStageAlign - smem_u32(smem4)) & (kStageAlign - 1)));
   constexpr int kStageFloats = kColGroup * 2048;
-  float2* emt = reinterpret_cast<float2*>(stages + 2 * kStageFloats);  // [32][32]
+  float2* emt = reinterpret_cast<float2*>(stages + kColStages * kStageFloats);  // [32][32]
   const int x0 = strip * 32, x = x0 + lane;
   const int cols = min(32, w - x0);
   const float4* CA = CA_all + (size_t)f * ny * pairs * w * 2;
@@ -373,9 +381,10 @@ __global__ void __launch_bounds__(32 * kColGroup, 3) k_colpass_tma(
   float4 ca0 = __ldg(ca_ptr), ca1 = __ldg(ca_ptr + 1);
   for (int cy = 0; cy < ny; ++cy) {
     const int y0 = cy * kTile, rows = min(kTile, h - y0);
-    float* stage = stages + (cy & 1) * kStageFloats;
-    if (tid == 0 && cy >= 2) {  // the store of chunk cy-2 (same stage) has read it
-      asm volatile("cp.async.bulk.wait_group.read 1;\n" ::: "memory");
+    float* stage = stages + (kColStages == 2 ? (cy & 1) : 0) * kStageFloats;
+    if (tid == 0 && cy >= kColStages) {  // the store of chunk cy-kColStages (same stage) has read it
+      if constexpr (kColStages == 2) asm volatile("cp.async.bulk.wait_group.read 1;\n" ::: "memory");
+      else asm volatile("cp.async.bulk.wait_group.read 0;\n" ::: "memory");
     }
     __syncthreads();
     mbar_wait(&em_full, cy & 1);  // this chunk's seeds have landed
@@ -807,8 +816,8 @@ template <typename Tin>
 static size_t colpass_smem(int pairs) {  // k_colpass and k_col_carry
   return sizeof(float2) * (size_t)pairs * 32 * 33 + sizeof(Tin) * 2 * 32 * 33;
 }
-static size_t colpass_tma_smem() {  // two stages of a pair group + EM tile + alignment slack
-  return kStageAlign + sizeof(float) * 2 * kColGroup * 2048 + sizeof(float2) * 32 * 32;
+static size_t colpass_tma_smem() {  // stages of a pair group + EM tile + alignment slack
+  return kStageAlign + sizeof(float) * kColStages * kColGroup * 2048 + sizeof(float2) * 32 * 32;
 }
 template <typename Tin, typename Tout>
 static int rowpass_nbuf(int pairs) {  // deepest V ring that fits in 227 KB (0: none)
