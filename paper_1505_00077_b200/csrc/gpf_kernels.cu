@@ -92,7 +92,25 @@ __global__ void __launch_bounds__(kMeanThreads) k_mean_partial(const T* __restri
   partials += (size_t)blockIdx.y * gridDim.x * 2;
   double hi = 0.0, lo = 0.0;
   const long long stride = (long long)gridDim.x * kMeanThreads;
-  for (long long i = (long long)blockIdx.x * kMeanThreads + threadIdx.x; i < n; i += stride) {
+  long long i0 = 0;
+  if (sizeof(T) == 4 && (reinterpret_cast<uintptr_t>(in) & 15) == 0) {
+    // four pixels per 16-B load; two_sum keeps every add's rounding error
+    const float4* in4 = reinterpret_cast<const float4*>(in);
+    const long long n4 = n / 4;
+    for (long long i = (long long)blockIdx.x * kMeanThreads + threadIdx.x; i < n4; i += stride) {
+      const float4 v = __ldg(in4 + i);
+      const double e4[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        double s, e;
+        two_sum(hi, e4[k], s, e);
+        hi = s;
+        lo += e;
+      }
+    }
+    i0 = n4 * 4;
+  }
+  for (long long i = i0 + (long long)blockIdx.x * kMeanThreads + threadIdx.x; i < n; i += stride) {
     double s, e;
     two_sum(hi, static_cast<double>(in[i]), s, e);
     hi = s;
@@ -502,13 +520,26 @@ __global__ void __launch_bounds__(256) k_seed(const Tin* __restrict__ in_all,
                                               const double* __restrict__ scalars,
                                               float2* __restrict__ EM_all, int w, int h, int w_pad,
                                               RangeConsts rc) {
-  const int f = blockIdx.z, x = blockIdx.x * 256 + threadIdx.x;
+  // four pixels per thread: one 16-B load of f (fp32, w % 4 == 0), two 16-B stores
+  const int f = blockIdx.z, x = (blockIdx.x * 256 + threadIdx.x) * 4;
   if (x >= w) return;
   const Tin* in = in_all + (size_t)f * w * h;
   float2* EM = EM_all + (size_t)f * h * w_pad;
   const double t_c = scalars[2 * f];
-  for (int y = blockIdx.y; y < h; y += gridDim.y)
-    EM[(size_t)y * w_pad + x] = pixel_terms(static_cast<double>(in[(size_t)y * w + x]), t_c, rc);
+  const bool vec = sizeof(Tin) == 4 && (w & 3) == 0 && x + 4 <= w;
+  for (int y = blockIdx.y; y < h; y += gridDim.y) {
+    const Tin* src = in + (size_t)y * w + x;
+    float2* dst = EM + (size_t)y * w_pad + x;
+    if (vec) {
+      const float4 v = __ldg(reinterpret_cast<const float4*>(src));
+      const float2 a = pixel_terms(v.x, t_c, rc), b = pixel_terms(v.y, t_c, rc);
+      const float2 c = pixel_terms(v.z, t_c, rc), d = pixel_terms(v.w, t_c, rc);
+      reinterpret_cast<float4*>(dst)[0] = make_float4(a.x, a.y, b.x, b.y);
+      reinterpret_cast<float4*>(dst)[1] = make_float4(c.x, c.y, d.x, d.y);
+    } else {
+      for (int k = 0; k < 4 && x + k < w; ++k) dst[k] = pixel_terms(static_cast<double>(src[k]), t_c, rc);
+    }
+  }
 }
 
 // ----------------------------------------------------------------------------
@@ -988,7 +1019,7 @@ static void launch_passes(Plan& plan, const Tin* d_in, Tout* d_out, int count,
   stage_mark(plan, kStageColCarry, st);
   if constexpr (kCanStage) {
     // seeds once per pixel, then the carries in pair groups
-    k_seed<Tin><<<dim3((w + 255) / 256, std::min(h, 1024), count), 256, 0, st>>>(
+    k_seed<Tin><<<dim3((w + 1023) / 1024, std::min(h, 1024), count), 256, 0, st>>>(
         d_in, plan.scalars, plan.EM, w, h, plan.w_pad, plan.rc);
     const int ksm = (int)(sizeof(float2) * kColGroup * 32 * 33);
     check(cudaFuncSetAttribute(k_col_carry_tma, cudaFuncAttributeMaxDynamicSharedMemorySize, ksm),
