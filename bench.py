@@ -17,8 +17,8 @@ time = max over ranks of the CUDA-event time of the K steps.
 --impl reference times the reference's own CPU implementation
 (oracle/_ref/libgpfilter_ref.so, compiled unmodified from the reference
 sources; the oracle port if that build is absent) on the box's host cores, on
-a bounded sample of the same workload (one 1024x1024 frame of the generator at
-each sigma_s per step).
+a bounded sample of the same workload (one 2048x2048 frame of the generator at
+each sigma_s per step, ~5 s on 16 cores).
 """
 from __future__ import annotations
 
@@ -37,7 +37,7 @@ sys.path.insert(0, ROOT)
 METRIC = "Mpixel/s of Gauss-poly bilateral (sigma_s-independent) and % of HBM/FP32 roofline"
 UNIT = "Mpixel/s"
 CFG_ID = 3
-SAMPLE_W = SAMPLE_H = 1024
+SAMPLE_W = SAMPLE_H = 2048  # 5 sigma_s x 4.2 MP: ~5 s per pass of the reference on 16 cores
 
 
 def parse():
@@ -356,10 +356,10 @@ def bench_b200(args):
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         thr = cpu_threads()
-        v, sec, kind = cpu_reference_run(sigmas, sr, N, 1, thr)
+        v, sec, kind = cpu_reference_run(sigmas, sr, N, 2, thr)
         cpu = {"value": round(v, 3), "unit": UNIT, "cores": thr, "kind": kind,
                "sample": f"{SAMPLE_W}x{SAMPLE_H} generator frame at sigma_s {list(sigmas)}, "
-                         f"sigma_r {sr}, N {N} ({sec:.1f} s of CPU work)"}
+                         f"sigma_r {sr}, N {N}; median of 2 passes of {sec:.1f} s of CPU work"}
 
     launches = args.steps * frames * plans[0].launches_per_frame
     line = {
@@ -512,7 +512,7 @@ def bench_c4(args):
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         thr = cpu_threads()
-        v, sec, kind = cpu_reference_run((ss,), sr, N, 1, thr)
+        v, sec, kind = cpu_reference_run((ss,), sr, N, 3, thr)
         cpu = {"value": round(v, 3), "unit": UNIT, "cores": thr, "kind": kind,
                "sample": f"{SAMPLE_W}x{SAMPLE_H} generator frame at sigma_s {ss}, sigma_r {sr}, N {N} "
                          f"({sec:.1f} s of CPU work)"}
