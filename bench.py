@@ -223,10 +223,23 @@ def bench_b200(args):
     streams = [torch.cuda.Stream() for _ in sigmas]
     main = torch.cuda.current_stream()
 
+    # The five sigma_s frames run concurrently on five streams. (GPF_BENCH_CHAIN=1
+    # instead chains them -- frame j starts when frame j-1's column half is done,
+    # via gpf_b200_filter_f32_ev -- measured slower: 12.0 vs 13.8 Gpix/s.)
+    pipelined = os.environ.get("GPF_BENCH_CHAIN", "0") == "1"
+    front = [torch.cuda.Event() for _ in sigmas]
+    for ev, st in zip(front, streams):
+        ev.record(st)  # creates the events
+    chain = {"prev": None}
+
     def step():
         for i, (plan, out, st) in enumerate(zip(plans, outs, streams)):
             st.wait_stream(main)
-            plan.filter_device(d_in, out, 1, d_fb[i:i + 1], st.cuda_stream)
+            if pipelined and chain["prev"] is not None:
+                st.wait_event(chain["prev"])
+            plan.filter_device(d_in, out, 1, d_fb[i:i + 1], st.cuda_stream,
+                               front[i].cuda_event if pipelined else None)
+            chain["prev"] = front[i]
         for st in streams:
             main.wait_stream(st)
 

@@ -55,6 +55,15 @@ int gpf_b200_plan_launches_per_frame(const gpf_b200_plan* plan);
 gpf_status gpf_b200_filter_f32(gpf_b200_plan* plan, const float* d_in, float* d_out,
                                int count, long long* d_fallbacks, void* stream);
 
+/* Same as gpf_b200_filter_f32, and records `front_done` (a cudaEvent_t) on
+ * `stream` once the column half of the last frame (mean, seeds, column
+ * carries, column pass) has been enqueued: waiting on it lets the caller start
+ * another frame's column half while this frame's row half (row carries, row
+ * pass) runs, so HBM-heavy and FMA-heavy kernels of different frames overlap. */
+gpf_status gpf_b200_filter_f32_ev(gpf_b200_plan* plan, const float* d_in, float* d_out,
+                                  int count, long long* d_fallbacks, void* stream,
+                                  void* front_done);
+
 /* Same, from host memory to host memory: copies each frame in, filters,
  * copies the result and the fallback counts back, and synchronises `stream`
  * before returning. h_fallbacks (host, `count` entries) may be NULL. */

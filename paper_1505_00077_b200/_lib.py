@@ -32,7 +32,8 @@ EXPORTED = (
     "gpf_set_num_threads", "gpf_get_num_threads",
     "gpf_b200_plan_create", "gpf_b200_plan_destroy", "gpf_b200_plan_set_batch",
     "gpf_b200_plan_set_profiling", "gpf_b200_plan_stage_times", "gpf_b200_plan_workspace_bytes",
-    "gpf_b200_plan_launches_per_frame", "gpf_b200_filter_f32", "gpf_b200_filter_f32_host",
+    "gpf_b200_plan_launches_per_frame", "gpf_b200_filter_f32", "gpf_b200_filter_f32_ev",
+    "gpf_b200_filter_f32_host",
 )
 
 
@@ -83,6 +84,7 @@ def _declare(lib: C.CDLL) -> C.CDLL:
     lib.gpf_b200_plan_workspace_bytes.argtypes = [vp]
     lib.gpf_b200_plan_launches_per_frame.argtypes = [vp]
     lib.gpf_b200_filter_f32.argtypes = [vp, vp, vp, C.c_int, vp, vp]
+    lib.gpf_b200_filter_f32_ev.argtypes = [vp, vp, vp, C.c_int, vp, vp, vp]
     lib.gpf_b200_filter_f32_host.argtypes = [vp, vp, vp, C.c_int, C.POINTER(C.c_longlong), vp]
     return lib
 

@@ -365,8 +365,8 @@ int gpf_b200_plan_launches_per_frame(const gpf_b200_plan* plan) {
   return plan ? plan->plan.launches_per_frame : 0;
 }
 
-gpf_status gpf_b200_filter_f32(gpf_b200_plan* plan, const float* d_in, float* d_out, int count,
-                               long long* d_fallbacks, void* stream) {
+gpf_status gpf_b200_filter_f32_ev(gpf_b200_plan* plan, const float* d_in, float* d_out, int count,
+                                  long long* d_fallbacks, void* stream, void* front_done) {
   if (plan == nullptr || d_in == nullptr || d_out == nullptr)
     return fail(GPF_ERR_INVALID_ARGUMENT, "null argument");
   if (count < 0) return fail(GPF_ERR_INVALID_ARGUMENT, "count must be >= 0");
@@ -382,11 +382,21 @@ gpf_status gpf_b200_filter_f32(gpf_b200_plan* plan, const float* d_in, float* d_
       cuda_check(cudaMalloc(&plan->d_fb, sizeof(unsigned long long) * B), "cudaMalloc");
       plan->d_fb_cap = B;
     }
+    struct Reset {  // the event belongs to this call only
+      gpfb::Plan& p;
+      ~Reset() { p.front_done = nullptr; }
+    } reset{plan->plan};
     for (int f = 0; f < count; f += B) {
       const int n = std::min(B, count - f);
+      plan->plan.front_done = f + n >= count ? static_cast<cudaEvent_t>(front_done) : nullptr;
       gpfb::run_frames_f32(plan->plan, d_in + f * npx, d_out + f * npx, n, fb ? fb + f : plan->d_fb, st);
     }
   });
+}
+
+gpf_status gpf_b200_filter_f32(gpf_b200_plan* plan, const float* d_in, float* d_out, int count,
+                               long long* d_fallbacks, void* stream) {
+  return gpf_b200_filter_f32_ev(plan, d_in, d_out, count, d_fallbacks, stream, nullptr);
 }
 
 gpf_status gpf_b200_filter_f32_host(gpf_b200_plan* plan, const float* h_in, float* h_out, int count,

@@ -106,6 +106,8 @@ struct Plan {
   size_t bytes = 0;
   int mean_blocks = 0;
   int launches_per_frame = 0;  // kernels per launch group (independent of batch)
+  // optional event recorded after the column pass (set per call by the C ABI)
+  cudaEvent_t front_done = nullptr;
   // optional per-stage timing: events recorded on the launching stream
   bool profile = false;
   struct StageTimer* timer = nullptr;

@@ -397,6 +397,13 @@ __global__ void __launch_bounds__(32 * kColGroup, GPF_COL_CTAS) k_colpass_tma(
   const float4* ca_ptr = CA + (size_t)min(g, pairs - 1) * w * 2 + (size_t)min(x, w - 1) * 2;
   const size_t ca_stride = (size_t)pairs * w * 2;
   float4 ca0 = __ldg(ca_ptr), ca1 = __ldg(ca_ptr + 1);
+#ifdef GPF_DIAG_CLOCKS
+  long long tph[6] = {0, 0, 0, 0, 0, 0};  // barA, waitEM, produce, barB, sweep, barC+store+hdot
+  long long tq = clock64();
+#define GPF_TICK(i) { const long long tn = clock64(); tph[i] += tn - tq; tq = tn; }
+#else
+#define GPF_TICK(i)
+#endif
   for (int cy = 0; cy < ny; ++cy) {
     const int y0 = cy * kTile, rows = min(kTile, h - y0);
     float* stage = stages + (kColStages == 2 ? (cy & 1) : 0) * kStageFloats;
@@ -405,10 +412,13 @@ __global__ void __launch_bounds__(32 * kColGroup, GPF_COL_CTAS) k_colpass_tma(
       else asm volatile("cp.async.bulk.wait_group.read 0;\n" ::: "memory");
     }
     __syncthreads();
+    GPF_TICK(0);
     mbar_wait(&em_full, cy & 1);  // this chunk's seeds have landed
+    GPF_TICK(1);
 #ifndef GPF_DIAG_NO_PROD
     produce_group(stage, emt, pair0, npairs);
 #endif
+    GPF_TICK(2);
     PairState as;
     as.wr[0] = make_float2(ca0.x, ca0.y);
     as.wi[0] = make_float2(ca0.z, ca0.w);
@@ -419,6 +429,7 @@ __global__ void __launch_bounds__(32 * kColGroup, GPF_COL_CTAS) k_colpass_tma(
       ca1 = __ldg(ca_ptr + (size_t)(cy + 1) * ca_stride + 1);
     }
     __syncthreads();
+    GPF_TICK(3);
     if (tid == 0 && cy + 1 < ny) {  // the EM tile is free again: fetch the next chunk's
       mbar_arrive_expect_tx(&em_full, 32 * 32 * sizeof(float2));
       tma_load_3d(emt, &emmap, 2 * x0, y0 + kTile, f, &em_full);
@@ -478,6 +489,7 @@ __global__ void __launch_bounds__(32 * kColGroup, GPF_COL_CTAS) k_colpass_tma(
         }
       }
     }
+    GPF_TICK(4);
     fence_proxy_async();  // stage writes -> visible to the TMA store
     __syncthreads();
 #ifndef GPF_DIAG_NO_STORE
@@ -507,7 +519,14 @@ __global__ void __launch_bounds__(32 * kColGroup, GPF_COL_CTAS) k_colpass_tma(
       }
       ps_store(AH + ((size_t)strip * pairs + g) * h * 2 + (size_t)(y0 + lane) * 2, agg);
     }
+    GPF_TICK(5);
   }
+#ifdef GPF_DIAG_CLOCKS
+  if ((blockIdx.x == 300 || blockIdx.x == 301) && (tid == 0 || tid == 96))
+    printf("colpass cta %d tid %d: barA %lld waitEM %lld produce %lld barB %lld sweep %lld rest %lld (per chunk)\n",
+           blockIdx.x, tid, tph[0] / ny, tph[1] / ny, tph[2] / ny, tph[3] / ny, tph[4] / ny, tph[5] / ny);
+#endif
+#undef GPF_TICK
   if (tid == 0) bulk_wait_all();  // V complete before the CTA retires
 }
 
@@ -1045,6 +1064,7 @@ static void launch_passes(Plan& plan, const Tin* d_in, Tout* d_out, int count,
                                                                  plan.AH, w, h, h_pad, plan.ny, plan.nx,
                                                                  plan.fc, plan.tc, plan.rc);
   }
+  if (plan.front_done) check(cudaEventRecord(plan.front_done, st), "cudaEventRecord");
   stage_mark(plan, kStageRowScan, st);
   k_row_scan<<<dim3(plan.ny, count), blk, 0, st>>>(plan.V, plan.AH, plan.CH, w, h, h_pad, plan.nx,
                                                    plan.fc, plan.tc);

@@ -160,10 +160,14 @@ class Plan:
     def launches_per_frame(self) -> int:
         return _lib.lib().gpf_b200_plan_launches_per_frame(self.h)
 
-    def filter_device(self, d_in, d_out, count: int = 1, d_fallbacks=None, stream: int = 0) -> None:
-        """Enqueue `count` frames (device fp32 in -> device fp32 out) on `stream`."""
+    def filter_device(self, d_in, d_out, count: int = 1, d_fallbacks=None, stream: int = 0,
+                      front_done: int | None = None) -> None:
+        """Enqueue `count` frames (device fp32 in -> device fp32 out) on `stream`.
+        `front_done` (a cudaEvent_t handle, e.g. torch.cuda.Event().cuda_event)
+        is recorded once the last frame's column half is enqueued."""
         fb = _ptr(d_fallbacks) if d_fallbacks is not None else None
-        _check(_lib.lib().gpf_b200_filter_f32(self.h, _ptr(d_in), _ptr(d_out), count, fb, stream))
+        _check(_lib.lib().gpf_b200_filter_f32_ev(self.h, _ptr(d_in), _ptr(d_out), count, fb, stream,
+                                                 front_done))
 
     def filter_host(self, h_in: np.ndarray, h_out: np.ndarray | None = None, stream: int = 0):
         """Host fp32 frames -> host fp32 frames (copies inside). Returns (out, fallbacks)."""
