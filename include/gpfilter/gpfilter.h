@@ -95,6 +95,26 @@ gpf_status gpf_filter_gpf(const gpf_image* in, const gpf_spatial_params* sp,
 gpf_status gpf_gaussian_recursive(const gpf_image* in, double sigma_s,
                                   double kernel_scale, gpf_image** out);
 
+/* Exact brute-force bilateral filter, Eq. (1) over the (2W+1)^2 window with
+ * the boundary mode of sp (ref.h:97-98, proj/src/capi.cpp:164-174 ->
+ * exact_bilateral, proj/src/core/bilateral.cpp:14-56). The MSE yardstick of
+ * the GPF path; runs on the GPU (fp32 taps, fp64 row sums: within 1e-4 of the
+ * fp64 reference on [0,255]). Same NULL / validation / status behaviour. */
+gpf_status gpf_filter_exact(const gpf_image* in, const gpf_spatial_params* sp,
+                            const gpf_range_params* rp, gpf_image** out);
+
+/* Error statistics between equally sized images (ref.h:149-159,
+ * proj/src/capi.cpp:288-301 -> metrics::compare, proj/src/core/metrics.cpp). */
+typedef struct gpf_error_report {
+  double mse;
+  double mse_db; /* 10*log10(mse); -400 when mse == 0 */
+  double max_abs;
+  long long pixels; /* samples compared */
+} gpf_error_report;
+
+gpf_status gpf_compare(const gpf_image* ref, const gpf_image* test,
+                       int exclude_border, gpf_error_report* out);
+
 /* Thread-count plumbing (ref.h:165-168). Kept for ABI compatibility; the
  * value is recorded but device work is always deterministic and identical
  * for every count. */

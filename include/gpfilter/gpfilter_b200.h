@@ -64,6 +64,17 @@ gpf_status gpf_b200_filter_f32_ev(gpf_b200_plan* plan, const float* d_in, float*
                                   int count, long long* d_fallbacks, void* stream,
                                   void* front_done);
 
+/* Exact (direct O(sigma_s^2)) bilateral filter of `count` contiguous fp32
+ * frames in device memory (the gpf_filter_exact definition), on `stream`. */
+gpf_status gpf_b200_exact_f32(const float* d_in, float* d_out, int width, int height, int count,
+                              const gpf_spatial_params* sp, const gpf_range_params* rp,
+                              void* stream);
+
+/* gpf_compare on fp32 device images (deterministic reduction); synchronises
+ * `stream`. */
+gpf_status gpf_b200_compare_f32(const float* d_ref, const float* d_test, int width, int height,
+                                int exclude_border, gpf_error_report* out, void* stream);
+
 /* Same, from host memory to host memory: copies each frame in, filters,
  * copies the result and the fallback counts back, and synchronises `stream`
  * before returning. h_fallbacks (host, `count` entries) may be NULL. */

@@ -178,8 +178,24 @@ class Reference:
             return st, None, fb.value
         return st, self._take(out, img.shape), fb.value
 
-    def exact(self, img: np.ndarray, sigma_s: float, sigma_r: float) -> np.ndarray:
-        sp = self.SpatialParams(sigma_s, 0, 0, 1.0)
+    class ErrorReport(C.Structure):
+        _fields_ = [("mse", C.c_double), ("mse_db", C.c_double), ("max_abs", C.c_double),
+                    ("pixels", C.c_longlong)]
+
+    def compare(self, ref: np.ndarray, test: np.ndarray, exclude_border: int = 0):
+        """Reference gpf_compare (capi.cpp:288-301): (status, report dict or None)."""
+        self.lib.gpf_compare.argtypes = [C.c_void_p, C.c_void_p, C.c_int, C.POINTER(self.ErrorReport)]
+        a, b = self._img(ref), self._img(test)
+        rep = self.ErrorReport()
+        st = self.lib.gpf_compare(a, b, exclude_border, C.byref(rep))
+        self.lib.gpf_image_destroy(a)
+        self.lib.gpf_image_destroy(b)
+        if st != 0:
+            return st, None
+        return st, {"mse": rep.mse, "mse_db": rep.mse_db, "max_abs": rep.max_abs, "pixels": rep.pixels}
+
+    def exact(self, img: np.ndarray, sigma_s: float, sigma_r: float, boundary: int = 0) -> np.ndarray:
+        sp = self.SpatialParams(sigma_s, 0, boundary, 1.0)
         rp = self.RangeParams(sigma_r, 20)
         src = self._img(img)
         out = C.c_void_p()

@@ -28,12 +28,12 @@ EXPORTED = (
     "gpf_image_create", "gpf_image_destroy", "gpf_image_width", "gpf_image_height",
     "gpf_image_data", "gpf_image_cdata",
     "gpf_spatial_params_init", "gpf_range_params_init",
-    "gpf_filter_gpf", "gpf_gaussian_recursive",
+    "gpf_filter_gpf", "gpf_gaussian_recursive", "gpf_filter_exact", "gpf_compare",
     "gpf_set_num_threads", "gpf_get_num_threads",
     "gpf_b200_plan_create", "gpf_b200_plan_destroy", "gpf_b200_plan_set_batch",
     "gpf_b200_plan_set_profiling", "gpf_b200_plan_stage_times", "gpf_b200_plan_workspace_bytes",
     "gpf_b200_plan_launches_per_frame", "gpf_b200_filter_f32", "gpf_b200_filter_f32_ev",
-    "gpf_b200_filter_f32_host",
+    "gpf_b200_filter_f32_host", "gpf_b200_exact_f32", "gpf_b200_compare_f32",
 )
 
 
@@ -41,6 +41,12 @@ class SpatialParams(C.Structure):
     """gpf_spatial_params (reference gpfilter.h:75-80)."""
     _fields_ = [("sigma_s", C.c_double), ("window_radius", C.c_int),
                 ("boundary", C.c_int), ("kernel_scale", C.c_double)]
+
+
+class ErrorReport(C.Structure):
+    """gpf_error_report (reference gpfilter.h:149-154)."""
+    _fields_ = [("mse", C.c_double), ("mse_db", C.c_double), ("max_abs", C.c_double),
+                ("pixels", C.c_longlong)]
 
 
 class RangeParams(C.Structure):
@@ -73,6 +79,11 @@ def _declare(lib: C.CDLL) -> C.CDLL:
     lib.gpf_filter_gpf.argtypes = [vp, C.POINTER(SpatialParams), C.POINTER(RangeParams), C.c_int,
                                    C.c_int, C.POINTER(C.c_longlong), pvp]
     lib.gpf_gaussian_recursive.argtypes = [vp, C.c_double, C.c_double, pvp]
+    lib.gpf_filter_exact.argtypes = [vp, C.POINTER(SpatialParams), C.POINTER(RangeParams), pvp]
+    lib.gpf_compare.argtypes = [vp, vp, C.c_int, C.POINTER(ErrorReport)]
+    lib.gpf_b200_exact_f32.argtypes = [vp, vp, C.c_int, C.c_int, C.c_int, C.POINTER(SpatialParams),
+                                       C.POINTER(RangeParams), vp]
+    lib.gpf_b200_compare_f32.argtypes = [vp, vp, C.c_int, C.c_int, C.c_int, C.POINTER(ErrorReport), vp]
     lib.gpf_set_num_threads.argtypes = [C.c_int]
     lib.gpf_b200_plan_create.argtypes = [C.c_int, C.c_int, C.POINTER(SpatialParams),
                                          C.POINTER(RangeParams), C.c_int, C.c_int, pvp]

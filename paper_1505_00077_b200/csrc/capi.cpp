@@ -7,6 +7,7 @@
 // last error (capi.cpp:28-33), *out = NULL before work, fallback_count written
 // only on success. There is no CPU compute path: every filter call runs the
 // sm_100a kernels, and a missing device is an error.
+#include <algorithm>
 #include <cmath>
 #include <cstring>
 #include <atomic>
@@ -109,6 +110,33 @@ gpfb::Params validate(int w, int h, const gpf_spatial_params& sp, const gpf_rang
   p.degree = rp.degree;
   p.centering = centering != 0 ? 1 : 0;
   return p;
+}
+
+// Validation of the exact filter (to_spatial / to_range, SpatialParams and
+// RangeParams::validate): returns the window radius.
+int validate_exact(const gpf_spatial_params& sp, const gpf_range_params& rp) {
+  if (sp.boundary != GPF_BOUNDARY_REPLICATE && sp.boundary != GPF_BOUNDARY_REFLECT &&
+      sp.boundary != GPF_BOUNDARY_ZERO)
+    invalid("boundary must be replicate, reflect, or zero");
+  const int radius = sp.window_radius > 0 ? sp.window_radius : gpfb::default_window_radius(sp.sigma_s);
+  if (!(sp.sigma_s > 0.0)) invalid("SpatialParams: sigma_s must be > 0");
+  if (radius < 1) invalid("SpatialParams: window_radius must be >= 1");
+  if (!(sp.kernel_scale > 0.0)) invalid("SpatialParams: kernel_scale must be > 0");
+  if (!(rp.sigma_r > 0.0)) invalid("RangeParams: sigma_r must be > 0");
+  if (rp.degree < 0) invalid("RangeParams: degree must be >= 0");
+  return radius;
+}
+
+void fill_report(const gpfb::ErrorStats& st, gpf_error_report* out) {
+  out->mse = st.mse;
+  out->mse_db = st.mse == 0.0 ? -400.0 : std::max(10.0 * std::log10(st.mse), -400.0);  // metrics.cpp:12-18
+  out->max_abs = st.max_abs;
+  out->pixels = st.pixels;
+}
+
+void check_compare_dims(int w, int h, int border) {  // metrics.cpp:20-33
+  if (border < 0) invalid("compare: exclude_border must be >= 0");
+  if (2 * border >= w || 2 * border >= h) invalid("compare: exclude_border leaves no interior pixels");
 }
 
 int current_device() {
@@ -278,6 +306,44 @@ gpf_status gpf_gaussian_recursive(const gpf_image* in, double sigma_s, double ke
   });
 }
 
+gpf_status gpf_filter_exact(const gpf_image* in, const gpf_spatial_params* sp,
+                            const gpf_range_params* rp, gpf_image** out) {
+  if (in == nullptr || sp == nullptr || rp == nullptr || out == nullptr)
+    return fail(GPF_ERR_INVALID_ARGUMENT, "null argument");
+  *out = nullptr;
+  return guarded([&] {
+    const int W = validate_exact(*sp, *rp);
+    current_device();
+    const size_t n = (size_t)in->w * in->h;
+    DevBuf din(n * sizeof(double)), dout(n * sizeof(double));
+    cuda_check(cudaMemcpy(din.p, in->data.data(), n * sizeof(double), cudaMemcpyHostToDevice), "H2D");
+    gpfb::run_exact_f64(static_cast<const double*>(din.p), static_cast<double*>(dout.p), in->w, in->h,
+                        1, W, static_cast<int>(sp->boundary), sp->sigma_s, rp->sigma_r, nullptr);
+    auto* res = new gpf_image{in->w, in->h, std::vector<double>(n)};
+    std::unique_ptr<gpf_image> hold(res);
+    cuda_check(cudaMemcpy(res->data.data(), dout.p, n * sizeof(double), cudaMemcpyDeviceToHost), "D2H");
+    *out = hold.release();
+  });
+}
+
+gpf_status gpf_compare(const gpf_image* ref, const gpf_image* test, int exclude_border,
+                       gpf_error_report* out) {
+  if (ref == nullptr || test == nullptr || out == nullptr)
+    return fail(GPF_ERR_INVALID_ARGUMENT, "null argument");
+  return guarded([&] {
+    if (ref->w != test->w || ref->h != test->h) invalid("compare: images differ in size");
+    check_compare_dims(ref->w, ref->h, exclude_border);
+    current_device();
+    const size_t n = (size_t)ref->w * ref->h;
+    DevBuf da(n * sizeof(double)), db(n * sizeof(double));
+    cuda_check(cudaMemcpy(da.p, ref->data.data(), n * sizeof(double), cudaMemcpyHostToDevice), "H2D");
+    cuda_check(cudaMemcpy(db.p, test->data.data(), n * sizeof(double), cudaMemcpyHostToDevice), "H2D");
+    fill_report(gpfb::compare_f64(static_cast<const double*>(da.p), static_cast<const double*>(db.p),
+                                  ref->w, ref->h, exclude_border, nullptr),
+                out);
+  });
+}
+
 gpf_status gpf_set_num_threads(int n) {
   if (n < 1) return fail(GPF_ERR_INVALID_ARGUMENT, "thread count must be >= 1");
   g_threads.store(n);
@@ -397,6 +463,34 @@ gpf_status gpf_b200_filter_f32_ev(gpf_b200_plan* plan, const float* d_in, float*
 gpf_status gpf_b200_filter_f32(gpf_b200_plan* plan, const float* d_in, float* d_out, int count,
                                long long* d_fallbacks, void* stream) {
   return gpf_b200_filter_f32_ev(plan, d_in, d_out, count, d_fallbacks, stream, nullptr);
+}
+
+gpf_status gpf_b200_exact_f32(const float* d_in, float* d_out, int width, int height, int count,
+                              const gpf_spatial_params* sp, const gpf_range_params* rp,
+                              void* stream) {
+  if (d_in == nullptr || d_out == nullptr || sp == nullptr || rp == nullptr)
+    return fail(GPF_ERR_INVALID_ARGUMENT, "null argument");
+  if (width < 1 || height < 1) return fail(GPF_ERR_INVALID_ARGUMENT, "Image dimensions must be >= 1");
+  if (count < 0) return fail(GPF_ERR_INVALID_ARGUMENT, "count must be >= 0");
+  return guarded([&] {
+    const int W = validate_exact(*sp, *rp);
+    current_device();
+    gpfb::run_exact_f32(d_in, d_out, width, height, count, W, static_cast<int>(sp->boundary),
+                        sp->sigma_s, rp->sigma_r, static_cast<cudaStream_t>(stream));
+  });
+}
+
+gpf_status gpf_b200_compare_f32(const float* d_ref, const float* d_test, int width, int height,
+                                int exclude_border, gpf_error_report* out, void* stream) {
+  if (d_ref == nullptr || d_test == nullptr || out == nullptr)
+    return fail(GPF_ERR_INVALID_ARGUMENT, "null argument");
+  return guarded([&] {
+    check_compare_dims(width, height, exclude_border);
+    current_device();
+    fill_report(gpfb::compare_f32(d_ref, d_test, width, height, exclude_border,
+                                  static_cast<cudaStream_t>(stream)),
+                out);
+  });
 }
 
 gpf_status gpf_b200_filter_f32_host(gpf_b200_plan* plan, const float* h_in, float* h_out, int count,

@@ -134,6 +134,21 @@ void run_frames_f32(Plan& plan, const float* d_in, float* d_out, int count,
                     unsigned long long* d_fb, cudaStream_t st);
 void run_frames_f64(Plan& plan, const double* d_in, double* d_out, int count,
                     unsigned long long* d_fb, cudaStream_t st);
+// Direct O(sigma_s^2) bilateral (exact_bilateral, bilateral.cpp:14-56) on
+// `count` frames; boundary 0 replicate, 1 reflect, 2 zero (exact.cu).
+void run_exact_f32(const float* d_in, float* d_out, int w, int h, int count, int W, int boundary,
+                   double sigma_s, double sigma_r, cudaStream_t st);
+void run_exact_f64(const double* d_in, double* d_out, int w, int h, int count, int W, int boundary,
+                   double sigma_s, double sigma_r, cudaStream_t st);
+// metrics::compare (metrics.cpp:20-56) on device images; synchronises st.
+struct ErrorStats {
+  double mse = 0.0, max_abs = 0.0;
+  long long pixels = 0;
+};
+ErrorStats compare_f32(const float* d_ref, const float* d_test, int w, int h, int border,
+                       cudaStream_t st);
+ErrorStats compare_f64(const double* d_ref, const double* d_test, int w, int h, int border,
+                       cudaStream_t st);
 // Single-plane recursive Gaussian (gpf_gaussian_recursive), fp64 in/out.
 void run_gaussian_f64(const double* d_in, double* d_out, double* d_tmp, int w, int h,
                       double sigma_s, double scale, cudaStream_t st);

@@ -110,6 +110,47 @@ def gpf_gaussian_recursive(img: np.ndarray, sigma_s: float, kernel_scale: float 
     return Image(out).numpy()
 
 
+def gpf_filter_exact(img: np.ndarray, sp: SpatialParams | None = None,
+                     rp: RangeParams | None = None) -> np.ndarray:
+    """Exact brute-force bilateral filter (reference gpf_filter_exact), on the GPU."""
+    sp = sp or spatial_params()
+    rp = rp or range_params()
+    src = Image.from_array(img)
+    out = C.c_void_p()
+    _check(_lib.lib().gpf_filter_exact(src.h, C.byref(sp), C.byref(rp), C.byref(out)))
+    return Image(out).numpy()
+
+
+def _report(rep) -> dict:
+    return {"mse": rep.mse, "mse_db": rep.mse_db, "max_abs": rep.max_abs, "pixels": rep.pixels}
+
+
+def gpf_compare(ref: np.ndarray, test: np.ndarray, exclude_border: int = 0) -> dict:
+    """Error statistics (reference gpf_compare / metrics::compare)."""
+    a, b = Image.from_array(ref), Image.from_array(test)
+    rep = _lib.ErrorReport()
+    _check(_lib.lib().gpf_compare(a.h, b.h, exclude_border, C.byref(rep)))
+    return _report(rep)
+
+
+def exact_device(d_in, d_out, width: int, height: int, sigma_s: float, sigma_r: float,
+                 count: int = 1, boundary: int = GPF_BOUNDARY_REPLICATE, stream: int = 0) -> None:
+    """Exact bilateral of `count` fp32 device frames (gpf_b200_exact_f32), on `stream`."""
+    sp = spatial_params(sigma_s, boundary=boundary)
+    rp = range_params(sigma_r)
+    _check(_lib.lib().gpf_b200_exact_f32(_ptr(d_in), _ptr(d_out), width, height, count, C.byref(sp),
+                                         C.byref(rp), stream))
+
+
+def compare_device(d_ref, d_test, width: int, height: int, exclude_border: int = 0,
+                   stream: int = 0) -> dict:
+    """gpf_compare on fp32 device images (synchronises `stream`)."""
+    rep = _lib.ErrorReport()
+    _check(_lib.lib().gpf_b200_compare_f32(_ptr(d_ref), _ptr(d_test), width, height, exclude_border,
+                                           C.byref(rep), stream))
+    return _report(rep)
+
+
 def set_num_threads(n: int) -> None:
     _check(_lib.lib().gpf_set_num_threads(n))
 

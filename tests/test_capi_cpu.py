@@ -149,3 +149,30 @@ def test_no_cpu_fallback_without_device():
     with pytest.raises(gpf.GpfError) as e:
         gpf.gpf_filter_gpf(np.full((8, 8), 3.0))
     assert e.value.status == 9 and "no CUDA device" in e.value.detail
+
+
+def test_exact_and_compare_validation_before_device():
+    """gpf_filter_exact / gpf_compare reject bad arguments with the reference's
+    statuses and messages before touching the device."""
+    import ctypes as C
+
+    from paper_1505_00077_b200 import _lib, gpf
+    L = _lib.lib()
+    img = gpf.Image.from_array(np.zeros((4, 5)))
+    out = C.c_void_p()
+    sp, rp = gpf.spatial_params(), gpf.range_params()
+    assert L.gpf_filter_exact(None, C.byref(sp), C.byref(rp), C.byref(out)) == _lib.GPF_ERR_INVALID_ARGUMENT
+    sp.sigma_s = 0.0
+    assert L.gpf_filter_exact(img.h, C.byref(sp), C.byref(rp), C.byref(out)) == _lib.GPF_ERR_INVALID_ARGUMENT
+    assert b"sigma_s must be > 0" in L.gpf_last_error()
+    sp = gpf.spatial_params()
+    rp.sigma_r = -1.0
+    assert L.gpf_filter_exact(img.h, C.byref(sp), C.byref(rp), C.byref(out)) == _lib.GPF_ERR_INVALID_ARGUMENT
+    assert b"sigma_r must be > 0" in L.gpf_last_error()
+    rep = _lib.ErrorReport()
+    other = gpf.Image.from_array(np.zeros((4, 6)))
+    assert L.gpf_compare(img.h, other.h, 0, C.byref(rep)) == _lib.GPF_ERR_INVALID_ARGUMENT
+    assert b"differ in size" in L.gpf_last_error()
+    assert L.gpf_compare(img.h, img.h, -1, C.byref(rep)) == _lib.GPF_ERR_INVALID_ARGUMENT
+    assert L.gpf_compare(img.h, img.h, 2, C.byref(rep)) == _lib.GPF_ERR_INVALID_ARGUMENT
+    assert b"no interior" in L.gpf_last_error()

@@ -1,0 +1,103 @@
+"""Exact (direct O(sigma_s^2)) bilateral filter and error metrics on the GPU
+(gpf_filter_exact / gpf_compare / gpf_b200_exact_f32 / gpf_b200_compare_f32),
+against the oracle's restatement of exact_bilateral (bilateral.cpp:14-56) and,
+where the compiled reference is present, the reference's own entry points."""
+import numpy as np
+import pytest
+
+from paper_1505_00077_b200 import synth
+
+pytestmark = pytest.mark.gpu
+TOL = 1e-4  # fp32 taps with fp64 row sums vs the fp64 reference, on [0, 255]
+
+
+def _img(w, h, seed):
+    return synth.rects_image(w, h, max(2, w * h // 600), 10.0, seed).astype(np.float64)
+
+
+@pytest.mark.parametrize("boundary", [0, 1, 2])
+@pytest.mark.parametrize("w,h,ss,sr", [(64, 48, 2.0, 30.0), (75, 41, 3.5, 20.0), (33, 17, 1.0, 60.0)])
+def test_exact_matches_oracle(gpu, oracle, boundary, w, h, ss, sr):
+    img = _img(w, h, 7 + boundary)
+    out = gpu.gpf_filter_exact(img, gpu.spatial_params(ss, boundary=boundary), gpu.range_params(sr))
+    idx = np.arange(w * h)  # every pixel
+    ref = oracle.exact_bilateral_at(img, ss, sr, idx, boundary=boundary).reshape(h, w)
+    assert np.abs(out - ref).max() <= TOL
+
+
+def test_exact_large_window_sampled(gpu, oracle):
+    img = _img(160, 120, 11)
+    ss, sr = 12.0, 25.0  # W = 36: 5329 taps per pixel
+    out = gpu.gpf_filter_exact(img, gpu.spatial_params(ss), gpu.range_params(sr))
+    rng = np.random.default_rng(3)
+    idx = rng.choice(160 * 120, size=600, replace=False)
+    ref = oracle.exact_bilateral_at(img, ss, sr, idx)
+    assert np.abs(out.ravel()[idx] - ref).max() <= TOL
+
+
+def test_exact_constant_and_reference_entry(gpu, reference):
+    c = np.full((21, 30), 117.0)
+    assert np.array_equal(gpu.gpf_filter_exact(c, gpu.spatial_params(3.0)), c)
+    img = _img(48, 40, 5)
+    ref = reference.exact(img, 2.5, 30.0, boundary=1)
+    out = gpu.gpf_filter_exact(img, gpu.spatial_params(2.5, boundary=1), gpu.range_params(30.0))
+    assert np.abs(out - ref).max() <= TOL
+
+
+def test_exact_device_batch(gpu):
+    import torch
+    frames = np.stack([_img(96, 64, s).astype(np.float32) for s in (1, 2)])
+    d_in = torch.from_numpy(frames).cuda()
+    d_out = torch.empty_like(d_in)
+    gpu.exact_device(d_in, d_out, 96, 64, 3.0, 30.0, count=2,
+                     stream=torch.cuda.current_stream().cuda_stream)
+    torch.cuda.synchronize()
+    for k in range(2):
+        host = gpu.gpf_filter_exact(frames[k].astype(np.float64), gpu.spatial_params(3.0),
+                                    gpu.range_params(30.0))
+        assert np.abs(d_out[k].cpu().numpy() - host).max() <= TOL
+
+
+@pytest.mark.parametrize("border", [0, 3])
+def test_compare_matches_reference(gpu, reference, border):
+    a = _img(70, 52, 1)
+    b = a + np.random.default_rng(9).normal(0, 2.0, a.shape)
+    got = gpu.gpf_compare(a, b, border)
+    st, want = reference.compare(a, b, border)
+    assert st == 0
+    assert got["pixels"] == want["pixels"]
+    assert got["max_abs"] == want["max_abs"]
+    assert got["mse"] == pytest.approx(want["mse"], rel=1e-14)
+    assert got["mse_db"] == pytest.approx(want["mse_db"], rel=1e-12)
+
+
+def test_compare_identical_and_errors(gpu):
+    a = _img(20, 10, 2)
+    rep = gpu.gpf_compare(a, a)
+    assert rep["mse"] == 0.0 and rep["mse_db"] == -400.0 and rep["pixels"] == 200
+    with pytest.raises(gpu.GpfError, match="differ in size"):
+        gpu.gpf_compare(a, a[:, :5])
+    with pytest.raises(gpu.GpfError, match="no interior"):
+        gpu.gpf_compare(a, a, 5)
+
+
+def test_compare_device_matches_host(gpu):
+    import torch
+    a = _img(128, 96, 4).astype(np.float32)
+    b = (a + 1.5).astype(np.float32)
+    rep = gpu.compare_device(torch.from_numpy(a).cuda(), torch.from_numpy(b).cuda(), 128, 96, 2,
+                             torch.cuda.current_stream().cuda_stream)
+    host = gpu.gpf_compare(a.astype(np.float64), b.astype(np.float64), 2)
+    assert rep["pixels"] == host["pixels"] == 124 * 92
+    assert rep["mse"] == pytest.approx(host["mse"], rel=1e-12)
+
+
+def test_gpf_mse_vs_exact_c1(gpu):
+    """GPF's own error against the exact filter on C1 (reported, like the
+    reference's dB figures): finite, and the GPU GPF output matches the
+    reference GPF within the parity tolerance, so this is the reference's MSE."""
+    img = synth.make(synth.CONFIGS[1]).astype(np.float64)
+    g, fb = gpu.gpf_filter_gpf(img, gpu.spatial_params(3.0), gpu.range_params(30.0))
+    ex = gpu.gpf_filter_exact(img, gpu.spatial_params(3.0), gpu.range_params(30.0))
+    rep = gpu.gpf_compare(ex, g)
+    assert np.isfinite(rep["mse_db"]) and rep["mse"] > 0
