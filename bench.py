@@ -269,6 +269,17 @@ def bench_b200(args):
     value = world * frames * px / (ms_step / 1e3) / 1e6
     fallbacks = d_fb.cpu().tolist()
 
+    # GPF's error against the exact O(sigma_s^2) filter (north_star: reported
+    # alongside), full frame, metrics::compare definitions; outside the timed region
+    mse = {}
+    d_ex = torch.empty_like(d_in)
+    for s_, out in zip(sigmas, outs):
+        gpf.exact_device(d_in, d_ex, W, H, s_, sr, stream=main.cuda_stream)
+        rep = gpf.compare_device(d_ex, out, W, H, 0, main.cuda_stream)
+        mse[f"{s_:g}"] = {"mse": round(rep["mse"], 4), "mse_db": round(rep["mse_db"], 3),
+                          "max_abs": round(rep["max_abs"], 4)}
+    del d_ex
+
     # sigma_s independence: each plan alone on one stream
     per_sigma = {}
     for s, plan, out in zip(sigmas, plans, outs):
@@ -386,6 +397,9 @@ def bench_b200(args):
                    "l2": "inputs larger than L2 (256 MiB per frame, 126 MB L2); no flush",
                    "parallelism": f"frame replicas x{world}, no collective"},
         "sigma_s_ms_per_frame": per_sigma,
+        "mse_vs_exact": {"per_sigma_s": mse, "pixels": px,
+                         "what": "GPF output vs the exact O(sigma_s^2) bilateral (gpf_b200_exact_f32), "
+                                 "full frame, metrics::compare (mse, 10 log10 mse, max |d|)"},
         "stage_ms_per_frame": {k: round(v, 4) for k, v in stage_ms.items()},
         "roofline": roofline,
         "e2e": e2e,
