@@ -194,3 +194,21 @@ def test_degenerate_shapes(gpu, oracle):
         out, fb = run(gpu, img, 2.0, 30.0)
         assert fb == rfb
         assert np.abs(out - ref).max() <= TOL, shape
+
+
+@pytest.mark.parametrize("degree", [2, 3, 10, 19, 21, 22, 23, 24, 25, 31, 48])
+def test_degree_sweep_kernel_variants(gpu, oracle, degree):
+    """Every kernel variant the degree selects (static N = 20 row pass, runtime-N
+    row pass up to N = 22, warp-specialised row pass above; staged column pass
+    groups up to N = 24, padded column pass above) against the oracle, on an
+    odd-sized frame (partial chunks, strips and bands)."""
+    img = synth.rects_image(152, 77, 8, 10.0, 40 + degree).astype(np.float64)
+    ref, rfb, _ = oracle.gpf(img, 4.0, 45.0, degree)
+    out, fb = run(gpu, img, 4.0, 45.0, degree)
+    assert fb == rfb
+    assert np.abs(out - ref).max() <= TOL
+    # fp32 plan entry (the fast-path kernels for fp32 output) on the same frame
+    plan = gpu.Plan(152, 77, 4.0, 45.0, degree)
+    o32, fbs = plan.filter_host(img.astype(np.float32))
+    assert fbs == [rfb]
+    assert np.abs(o32 - ref).max() <= TOL
