@@ -232,17 +232,24 @@ def bench_b200(args):
         ev.record(st)  # creates the events
     chain = {"prev": None}
 
+    # A step enqueues the five frames; steps follow each other on the streams
+    # without a join in between (the timed region is still bracketed by a
+    # device-wide synchronize), so one frame's tail overlaps the next step.
+    join_each_step = os.environ.get("GPF_BENCH_JOIN", "0") == "1"
+
     def step():
         for i, (plan, out, st) in enumerate(zip(plans, outs, streams)):
-            st.wait_stream(main)
             if pipelined and chain["prev"] is not None:
                 st.wait_event(chain["prev"])
             plan.filter_device(d_in, out, 1, d_fb[i:i + 1], st.cuda_stream,
                                front[i].cuda_event if pipelined else None)
             chain["prev"] = front[i]
-        for st in streams:
-            main.wait_stream(st)
+        if join_each_step:
+            for st in streams:
+                main.wait_stream(st)
 
+    for st in streams:
+        st.wait_stream(main)
     for _ in range(args.warmup):
         step()
     torch.cuda.synchronize()
@@ -253,8 +260,12 @@ def bench_b200(args):
     clocks.start()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e0.record(main)
+    for st in streams:
+        st.wait_stream(main)  # every stream starts after e0
     for _ in range(args.steps):
         step()
+    for st in streams:
+        main.wait_stream(st)  # e1 after every stream's last frame
     e1.record(main)
     torch.cuda.synchronize()
     ms = e0.elapsed_time(e1)
@@ -470,6 +481,8 @@ def bench_c4(args):
         if n_loc:
             plan.filter_device(d_in, d_out, n_loc, d_fb, st.cuda_stream)
 
+    for st in streams:
+        st.wait_stream(main)
     for _ in range(args.warmup):
         step()
     torch.cuda.synchronize()
