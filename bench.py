@@ -47,6 +47,8 @@ def parse():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", choices=["b200", "reference"], default="b200")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-mse", action="store_true",
+                    help="skip the (untimed) MSE-vs-exact report, e.g. for ncu launch lists")
     ap.add_argument("--workload", choices=["c3", "c4"], default="c3",
                     help="c3 (default, the metric's config): 8192^2 sigma_s sweep, replicas per GPU; "
                          "c4: 64 frames x 3 channels of 3840x2160 sharded across the GPUs")
@@ -284,7 +286,7 @@ def bench_b200(args):
     # alongside), full frame, metrics::compare definitions; outside the timed region
     mse = {}
     d_ex = torch.empty_like(d_in)
-    for s_, out in zip(sigmas, outs):
+    for s_, out in zip(sigmas, [] if args.no_mse else outs):
         gpf.exact_device(d_in, d_ex, W, H, s_, sr, stream=main.cuda_stream)
         rep = gpf.compare_device(d_ex, out, W, H, 0, main.cuda_stream)
         mse[f"{s_:g}"] = {"mse": round(rep["mse"], 4), "mse_db": round(rep["mse_db"], 3),
