@@ -114,12 +114,12 @@ TileConsts make_tile_consts(double s, int width, int height) {
   TileConsts tc{};
   const int last_y = height - (height - 1) / kTile * kTile;  // rows in the last row chunk
   const int last_x = width - (width - 1) / kTile * kTile;    // columns in the last strip
+  for (int j = 0; j < kTile; ++j) {
+    const cd w0 = std::pow(p[0], j), w1 = std::pow(p[1], j);
+    tc.w4[j] = make_float4(static_cast<float>(w0.real()), static_cast<float>(w0.imag()),
+                           static_cast<float>(w1.real()), static_cast<float>(w1.imag()));
+  }
   for (int k = 0; k < 2; ++k) {
-    for (int j = 0; j < kTile; ++j) {
-      const cd w = std::pow(p[k], j);
-      tc.wr2[k][j] = dup(w.real());
-      tc.wi2[k][j] = dup(w.imag());
-    }
     const cd pt = std::pow(p[k], kTile), py = std::pow(p[k], last_y), px = std::pow(p[k], last_x);
     tc.pTr2[k] = dup(pt.real());
     tc.pTi2[k] = dup(pt.imag());

@@ -113,13 +113,14 @@ __device__ __forceinline__ void ps_chain(PairState& s, const PairState& agg, con
   }
 }
 
-// agg += w x with complex weight (w_k = wr_k + i wi_k) per section
-__device__ __forceinline__ void ps_accum(PairState& a, float2 x, float2 w0r, float2 w0i, float2 w1r,
-                                         float2 w1i) {
-  a.wr[0] = fma2(w0r, x, a.wr[0]);
-  a.wi[0] = fma2(w0i, x, a.wi[0]);
-  a.wr[1] = fma2(w1r, x, a.wr[1]);
-  a.wi[1] = fma2(w1i, x, a.wi[1]);
+// agg += w x with complex weight (w_k = wr_k + i wi_k) per section, the
+// weights as scalars (w.x, w.y, w.z, w.w) = (wr_0, wi_0, wr_1, wi_1): the
+// packed FMAs take them as broadcast operands, four per 16-B constant load.
+__device__ __forceinline__ void ps_accum(PairState& a, float2 x, const float4& w) {
+  a.wr[0] = fma2(x, f2(w.x), a.wr[0]);
+  a.wi[0] = fma2(x, f2(w.y), a.wi[0]);
+  a.wr[1] = fma2(x, f2(w.z), a.wr[1]);
+  a.wi[1] = fma2(x, f2(w.w), a.wi[1]);
 }
 
 }  // namespace gpfb

@@ -39,7 +39,7 @@ struct FilterConsts {
 // samples: the carry entering a chunk from the far side is
 //   C = sum_{j < L} p^j x[j]  +  p^L C_next        (L = chunk length)
 struct TileConsts {
-  float2 wr2[2][kTile], wi2[2][kTile];  // p_k^j, j < kTile
+  float4 w4[kTile];                     // (Re p_0^j, Im p_0^j, Re p_1^j, Im p_1^j), j < kTile
   float2 pTr2[2], pTi2[2];              // p_k^kTile
   float2 pYr2[2], pYi2[2];              // p_k^(rows in the last row chunk)
   float2 pXr2[2], pXi2[2];              // p_k^(columns in the last column strip)

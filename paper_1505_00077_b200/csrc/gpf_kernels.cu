@@ -255,10 +255,10 @@ __global__ void __launch_bounds__(MAXT, 2) k_col_carry(const Tin* __restrict__ i
         if (rows == kTile) {
 #pragma unroll
           for (int j = 0; j < kTile; ++j)
-            ps_accum(agg, mine[j], tc.wr2[0][j], tc.wi2[0][j], tc.wr2[1][j], tc.wi2[1][j]);
+            ps_accum(agg, mine[j], tc.w4[j]);
         } else {
           for (int j = 0; j < rows; ++j)
-            ps_accum(agg, mine[j], tc.wr2[0][j], tc.wi2[0][j], tc.wr2[1][j], tc.wi2[1][j]);
+            ps_accum(agg, mine[j], tc.w4[j]);
         }
         if (cy == ny - 1) ps_chain(C, agg, tc.pYr2, tc.pYi2);
         else ps_chain(C, agg, tc.pTr2, tc.pTi2);
@@ -510,12 +510,10 @@ __global__ void __launch_bounds__(32 * kColGroup, GPF_COL_CTAS) k_colpass_tma(
       if (cols == 32) {
 #pragma unroll
         for (int c = 0; c < 32; ++c)
-          ps_accum(agg, *reinterpret_cast<const float2*>(sb + c * 32 + ((hq ^ (c & 7)) << 2)),
-                   tc.wr2[0][c], tc.wi2[0][c], tc.wr2[1][c], tc.wi2[1][c]);
+          ps_accum(agg, *reinterpret_cast<const float2*>(sb + c * 32 + ((hq ^ (c & 7)) << 2)), tc.w4[c]);
       } else {
         for (int c = 0; c < cols; ++c)
-          ps_accum(agg, *reinterpret_cast<const float2*>(sb + c * 32 + ((hq ^ (c & 7)) << 2)),
-                   tc.wr2[0][c], tc.wi2[0][c], tc.wr2[1][c], tc.wi2[1][c]);
+          ps_accum(agg, *reinterpret_cast<const float2*>(sb + c * 32 + ((hq ^ (c & 7)) << 2)), tc.w4[c]);
       }
       ps_store(AH + ((size_t)strip * pairs + g) * h * 2 + (size_t)(y0 + lane) * 2, agg);
     }
@@ -651,10 +649,10 @@ __global__ void __launch_bounds__(32 * kColGroup, 6) k_col_carry_tma(
         if (rows == kTile) {
 #pragma unroll
           for (int j = 0; j < kTile; ++j)
-            ps_accum(agg, mine[j], tc.wr2[0][j], tc.wi2[0][j], tc.wr2[1][j], tc.wi2[1][j]);
+            ps_accum(agg, mine[j], tc.w4[j]);
         } else {
           for (int j = 0; j < rows; ++j)
-            ps_accum(agg, mine[j], tc.wr2[0][j], tc.wi2[0][j], tc.wr2[1][j], tc.wi2[1][j]);
+            ps_accum(agg, mine[j], tc.w4[j]);
         }
         if (cy == ny - 1) ps_chain(C, agg, tc.pYr2, tc.pYi2);
         else ps_chain(C, agg, tc.pTr2, tc.pTi2);
@@ -746,7 +744,7 @@ __global__ void __launch_bounds__(MAXT, 1) k_colpass(const Tin* __restrict__ in_
       ps_zero(agg);
       const float2* sg = buf + (size_t)g * 32 * 33 + lane;
       for (int c = 0; c < cols; ++c)
-        ps_accum(agg, sg[c * 33], tc.wr2[0][c], tc.wi2[0][c], tc.wr2[1][c], tc.wi2[1][c]);
+        ps_accum(agg, sg[c * 33], tc.w4[c]);
       ps_store(AH + ((size_t)strip * pairs + g) * h * 2 + (size_t)(y0 + lane) * 2, agg);
     }
   }
