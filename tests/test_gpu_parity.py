@@ -212,3 +212,16 @@ def test_degree_sweep_kernel_variants(gpu, oracle, degree):
     o32, fbs = plan.filter_host(img.astype(np.float32))
     assert fbs == [rfb]
     assert np.abs(o32 - ref).max() <= TOL
+
+
+@pytest.mark.parametrize("w,h", [(65536, 9), (7, 40000), (4100, 33), (33, 4100)])
+def test_extreme_aspect_ratios(gpu, oracle, w, h):
+    """Very wide / very tall frames: grid dimensions, partial chunks, strips and
+    bands at every edge, through both entries."""
+    img = synth.rects_image(w, h, 6, 10.0, 77).astype(np.float64)
+    ref, rfb, _ = oracle.gpf(img, 3.0, 30.0, 20, threads=8)
+    out, fb = run(gpu, img, 3.0, 30.0)
+    assert fb == rfb and np.abs(out - ref).max() <= TOL
+    plan = gpu.Plan(w, h, 3.0, 30.0, 20)
+    o32, fbs = plan.filter_host(img.astype(np.float32))
+    assert fbs == [rfb] and np.abs(o32 - ref).max() <= TOL
