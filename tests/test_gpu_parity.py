@@ -225,3 +225,26 @@ def test_extreme_aspect_ratios(gpu, oracle, w, h):
     plan = gpu.Plan(w, h, 3.0, 30.0, 20)
     o32, fbs = plan.filter_host(img.astype(np.float32))
     assert fbs == [rfb] and np.abs(o32 - ref).max() <= TOL
+
+
+def test_huge_frame_index_range(gpu):
+    """16384^2 (V holds 3e9 float2: past 32-bit element indices): a constant
+    frame stays exactly constant, and vertical flipping commutes with the
+    filter (the replicate boundary and the Deriche pair are symmetric)."""
+    import torch
+    n = 16384
+    plan = gpu.Plan(n, n, 6.0, 30.0, 20)
+    s = torch.cuda.current_stream().cuda_stream
+    c = torch.full((n, n), 93.0, device="cuda")
+    out = torch.empty_like(c)
+    plan.filter_device(c, out, 1, None, s)
+    torch.cuda.synchronize()
+    assert torch.equal(out, c)
+    g = torch.Generator(device="cuda").manual_seed(5)
+    x = (torch.rand((n, n), generator=g, device="cuda") * 255.0).round_()
+    y = torch.empty_like(x)
+    yf = torch.empty_like(x)
+    plan.filter_device(x, y, 1, None, s)
+    plan.filter_device(torch.flip(x, [0]).contiguous(), yf, 1, None, s)
+    torch.cuda.synchronize()
+    assert (torch.flip(yf, [0]) - y).abs().max().item() <= 1e-3
