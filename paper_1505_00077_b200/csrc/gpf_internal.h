@@ -59,7 +59,6 @@ struct RangeConsts {
   float c0;           // 2^-s0     (weight of plane 0)
   float p_scale;      // 2^k       (P uses planes n+1)
   float w_step[kMaxPlanes];  // 2^k/(n+1): c_{n+1} = c_n * H * w_step[n]
-  float2 w_pair[kMaxPlanes]; // (w_step[m], w_step[m-1]): (c_{m+1}, c_m) = (c_m, c_{m-1}) * H w_pair[m]
   float q_thresh;     // kQMin / (mass^2 * kernel_scale)  (bilateral.hpp:85)
   int planes;         // N + 2
   int pairs;          // ceil(planes / 2)
