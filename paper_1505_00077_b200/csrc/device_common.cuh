@@ -87,6 +87,13 @@ __device__ __forceinline__ float2 ps_emit(const PairState& s, const float2* cr, 
   return fma2(cr[0], s.wr[0], fma2(nci[0], s.wi[0], fma2(cr[1], s.wr[1], mul2(nci[1], s.wi[1]))));
 }
 
+// init + sum_k Re(c_k w_k): the emit seeded with a value to add (one FMA
+// instead of the MUL at the head of the chain and a separate add)
+__device__ __forceinline__ float2 ps_emit_acc(const PairState& s, const float2* cr, const float2* nci,
+                                              float2 init) {
+  return fma2(cr[0], s.wr[0], fma2(nci[0], s.wi[0], fma2(cr[1], s.wr[1], fma2(nci[1], s.wi[1], init))));
+}
+
 // Carry record: the 8 floats of a PairState as two float4.
 __device__ __forceinline__ void ps_store(float4* dst, const PairState& s) {
   dst[0] = make_float4(s.wr[0].x, s.wr[0].y, s.wi[0].x, s.wi[0].y);

@@ -452,23 +452,31 @@ __global__ void __launch_bounds__(32 * kColGroup, GPF_COL_CTAS) k_colpass_tma(
         // add the other direction's parked value.
 #pragma unroll
         for (int t = 0; t < kTile; t += 2) {
-          const float2 yb = ps_emit(as, fc.br2, fc.nbi2);
-          ps_advance(as, xr[31 - t], fc);
-          ps_advance(cs, xr[t], fc);
-          const float2 yc0 = ps_emit(cs, fc.ar2, fc.nai2);
-          const float2 ya = ps_emit(as, fc.br2, fc.nbi2);
-          ps_advance(as, xr[30 - t], fc);
-          ps_advance(cs, xr[t + 1], fc);
-          const float2 yc1 = ps_emit(cs, fc.ar2, fc.nai2);
           float4* pa = reinterpret_cast<float4*>(stage_at(mcol, 30 - t, cm));
           float4* pc = reinterpret_cast<float4*>(stage_at(mcol, t, cm));
           if (t < kTile / 2) {
+            const float2 yb = ps_emit(as, fc.br2, fc.nbi2);
+            ps_advance(as, xr[31 - t], fc);
+            ps_advance(cs, xr[t], fc);
+            const float2 yc0 = ps_emit(cs, fc.ar2, fc.nai2);
+            const float2 ya = ps_emit(as, fc.br2, fc.nbi2);
+            ps_advance(as, xr[30 - t], fc);
+            ps_advance(cs, xr[t + 1], fc);
+            const float2 yc1 = ps_emit(cs, fc.ar2, fc.nai2);
             *pa = make_float4(ya.x, ya.y, yb.x, yb.y);
             *pc = make_float4(yc0.x, yc0.y, yc1.x, yc1.y);
-          } else {
+          } else {  // the other direction's parked values seed the emits
             const float4 qa = *pa, qc = *pc;
-            *pa = make_float4(ya.x + qa.x, ya.y + qa.y, yb.x + qa.z, yb.y + qa.w);
-            *pc = make_float4(yc0.x + qc.x, yc0.y + qc.y, yc1.x + qc.z, yc1.y + qc.w);
+            const float2 yb = ps_emit_acc(as, fc.br2, fc.nbi2, make_float2(qa.z, qa.w));
+            ps_advance(as, xr[31 - t], fc);
+            ps_advance(cs, xr[t], fc);
+            const float2 yc0 = ps_emit_acc(cs, fc.ar2, fc.nai2, make_float2(qc.x, qc.y));
+            const float2 ya = ps_emit_acc(as, fc.br2, fc.nbi2, make_float2(qa.x, qa.y));
+            ps_advance(as, xr[30 - t], fc);
+            ps_advance(cs, xr[t + 1], fc);
+            const float2 yc1 = ps_emit_acc(cs, fc.ar2, fc.nai2, make_float2(qc.z, qc.w));
+            *pa = make_float4(ya.x, ya.y, yb.x, yb.y);
+            *pc = make_float4(yc0.x, yc0.y, yc1.x, yc1.y);
           }
         }
       } else {  // last, partial chunk: predicated (keeps xr in registers)

@@ -481,17 +481,23 @@ __global__ void __launch_bounds__(192, 2) k_rowpass2(const Tin* __restrict__ in_
       for (int t = 0; t < 32; ++t) {
         if ((t & 1) == 1) asm volatile("" ::: "memory");
         const int ca = 31 - t, cc = t;
-        const float2 ya = ps_emit(as, fc.br2, fc.nbi2);
-        const float2 xa = tl[ca * kRowBand], xc = tl[cc * kRowBand];
-        ps_advance(as, xa, fc);
-        ps_advance(cs, xc, fc);
-        const float2 yc = ps_emit(cs, fc.ar2, fc.nai2);
         if (t < 16) {
+          const float2 ya = ps_emit(as, fc.br2, fc.nbi2);
+          const float2 xa = tl[ca * kRowBand], xc = tl[cc * kRowBand];
+          ps_advance(as, xa, fc);
+          ps_advance(cs, xc, fc);
           ya_hi[ca - 16] = ya;
-          yc_lo[cc] = yc;
-        } else if (live) {
-          tl[ca * kRowBand] = add2(ya, yc_lo[ca]);
-          tl[cc * kRowBand] = add2(yc, ya_hi[cc - 16]);
+          yc_lo[cc] = ps_emit(cs, fc.ar2, fc.nai2);
+        } else {  // the other direction's parked value seeds the emit
+          const float2 ya = ps_emit_acc(as, fc.br2, fc.nbi2, yc_lo[ca]);
+          const float2 xa = tl[ca * kRowBand], xc = tl[cc * kRowBand];
+          ps_advance(as, xa, fc);
+          ps_advance(cs, xc, fc);
+          const float2 yc = ps_emit_acc(cs, fc.ar2, fc.nai2, ya_hi[cc - 16]);
+          if (live) {
+            tl[ca * kRowBand] = ya;
+            tl[cc * kRowBand] = yc;
+          }
         }
       }
     } else {  // last, partial strip
