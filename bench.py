@@ -172,16 +172,17 @@ def algorithmic_bytes_per_px(pairs: int) -> dict:
 
 
 def algorithmic_flops_per_px(pairs: int) -> dict:
-    """FP32 FLOPs each stage must issue per pixel (FMA = 2), P = plane pairs.
-    One IIR step of one plane: two complex sections advanced (3 FMA + 1 MUL
-    each) and emitted (3 FMA + 1 MUL for both) = 21; both directions + the
-    sum = 43, i.e. 86 per pair. Strip/chunk dot products: 4 FMA per plane.
+    """FP32 FLOPs each stage issues per pixel (FMA = 2), P = plane pairs.
+    One IIR step of one plane: two complex sections advanced (3 FMA each in
+    the sweep basis) and emitted (3 FMA + 1 MUL for both) = 19; both
+    directions = 38, plus the folded sum ~ 39, i.e. 78 per pair. Strip/chunk
+    dot products: 4 FMA per plane. Contraction: 2 FMA + 2 MUL per plane.
       carries    seeds ~20 + per pair: planes 2 MUL, dots 16          18 P + 20
-      colpass    per pair: planes 2, sweeps 86, row dots 16          104 P
+      colpass    per pair: planes 2, sweeps 78, row dots 16           96 P
       row_scan   per pair: one chain step per 32 pixels              ~P
-      rowpass    per pair: sweeps 86, contraction 16 (8 per plane)   102 P + 10"""
-    return {"mean": 1, "col_carry": 18 * pairs + 20, "colpass": 104 * pairs, "row_scan": pairs,
-            "rowpass": 102 * pairs + 10}
+      rowpass    per pair: sweeps 78, contraction 12                  90 P + 10"""
+    return {"mean": 1, "col_carry": 18 * pairs + 20, "colpass": 96 * pairs, "row_scan": pairs,
+            "rowpass": 90 * pairs + 10}
 
 
 def fp32_peak_tflops(peaks: dict) -> float:

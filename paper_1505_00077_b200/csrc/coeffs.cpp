@@ -96,14 +96,16 @@ FilterConsts make_filter_consts(double s) {
     const cd B = 2.0 * poly3(k.na, q) / den;
     const cd g = 1.0 / (1.0 - pk);
     fc.pr2[sec] = dup(pk.real());
-    fc.pi2[sec] = dup(pk.imag());
-    fc.npi2[sec] = dup(-pk.imag());
     fc.ar2[sec] = dup(A.real());
-    fc.nai2[sec] = dup(-A.imag());
     fc.br2[sec] = dup(B.real());
-    fc.nbi2[sec] = dup(-B.imag());
     fc.gr2[sec] = dup(g.real());
     fc.gi2[sec] = dup(g.imag());
+    const double si = pk.imag();
+    fc.nps2[sec] = dup(-si * si);
+    fc.sai2[sec] = dup(-A.imag() * si);
+    fc.sbi2[sec] = dup(-B.imag() * si);
+    fc.gs2[sec] = dup(g.imag() / si);
+    fc.ips2[sec] = dup(1.0 / si);
   }
   return fc;
 }

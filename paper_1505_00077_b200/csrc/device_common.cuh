@@ -62,7 +62,7 @@ __device__ __forceinline__ void ps_zero(PairState& s) {
   s.wr[0] = s.wr[1] = s.wi[0] = s.wi[1] = make_float2(0.f, 0.f);
 }
 
-// replicate steady state: w = x / (1 - p)
+// replicate steady state, standard basis (carry chains): w = x / (1 - p)
 __device__ __forceinline__ void ps_set_gain(PairState& s, float2 x, const FilterConsts& fc) {
 #pragma unroll
   for (int k = 0; k < 2; ++k) {
@@ -71,18 +71,37 @@ __device__ __forceinline__ void ps_set_gain(PairState& s, float2 x, const Filter
   }
 }
 
-// w <- p w + x   (4 FFMA2/FMUL2 per section for both planes)
+// Sweep-basis state (FilterConsts: wi holds v^ = Im(w) / Im(p)):
+//   w <- p w + x  as  Re w' = Re p Re w - (Im p)^2 v^ + x,  v^' = Re p v^ + Re w
+// three FFMA2 per section for both planes.
 __device__ __forceinline__ void ps_advance(PairState& s, float2 x, const FilterConsts& fc) {
 #pragma unroll
   for (int k = 0; k < 2; ++k) {
-    const float2 nr = fma2(fc.pr2[k], s.wr[k], fma2(fc.npi2[k], s.wi[k], x));
-    const float2 ni = fma2(fc.pr2[k], s.wi[k], mul2(fc.pi2[k], s.wr[k]));
+    const float2 nr = fma2(fc.pr2[k], s.wr[k], fma2(fc.nps2[k], s.wi[k], x));
+    const float2 ni = fma2(fc.pr2[k], s.wi[k], s.wr[k]);
     s.wr[k] = nr;
     s.wi[k] = ni;
   }
 }
 
-// sum_k Re(c_k w_k) = sum_k (cr_k wr_k - ci_k wi_k); ncr = -ci pre-negated
+// replicate steady state in the sweep basis: w = x / (1 - p)
+__device__ __forceinline__ void ps_set_gain_sweep(PairState& s, float2 x, const FilterConsts& fc) {
+#pragma unroll
+  for (int k = 0; k < 2; ++k) {
+    s.wr[k] = mul2(x, fc.gr2[k]);
+    s.wi[k] = mul2(x, fc.gs2[k]);
+  }
+}
+
+// a carry record (standard basis, 2 float4) as a sweep-basis state
+__device__ __forceinline__ void ps_from_carry(PairState& s, float4 c0, float4 c1, const FilterConsts& fc) {
+  s.wr[0] = make_float2(c0.x, c0.y);
+  s.wi[0] = mul2(make_float2(c0.z, c0.w), fc.ips2[0]);
+  s.wr[1] = make_float2(c1.x, c1.y);
+  s.wi[1] = mul2(make_float2(c1.z, c1.w), fc.ips2[1]);
+}
+
+// sum_k Re(c_k w_k): with the sweep basis the weights are (Re c_k, -Im c_k Im p_k)
 __device__ __forceinline__ float2 ps_emit(const PairState& s, const float2* cr, const float2* nci) {
   return fma2(cr[0], s.wr[0], fma2(nci[0], s.wi[0], fma2(cr[1], s.wr[1], mul2(nci[1], s.wi[1]))));
 }

@@ -29,10 +29,17 @@ constexpr int kTile = 32;       // rows per column-pass chunk == columns per row
 // Every coefficient is stored duplicated as (c, c) so that it feeds packed
 // fp32x2 instructions directly (the two halves are the two planes of a pair).
 struct FilterConsts {
-  float2 pr2[2], pi2[2], npi2[2];  // poles p_k (upper half plane), -Im p_k
-  float2 ar2[2], nai2[2];          // causal residues A_k (x2): Re, -Im
-  float2 br2[2], nbi2[2];          // anticausal residues B_k (x2): Re, -Im
+  float2 pr2[2];                   // Re p_k (poles in the upper half plane)
+  float2 ar2[2], br2[2];           // Re of the causal / anticausal residues A_k, B_k (x2)
   float2 gr2[2], gi2[2];           // 1/(1-p_k): warm-start gain
+  // Sweep basis: the imaginary part of each section state is kept as
+  // v^ = Im(w) / Im(p), which turns the advance into three FMAs per section
+  //   Re w' = Re p Re w - (Im p)^2 v^ + x,   v^' = Re p v^ + Re w
+  // (a diagonal similarity transform: same conditioning as the complex form).
+  float2 nps2[2];                  // -(Im p_k)^2
+  float2 sai2[2], sbi2[2];         // -Im(A_k) Im(p_k), -Im(B_k) Im(p_k): emit weights of v^
+  float2 gs2[2];                   // Im(1/(1-p_k)) / Im(p_k): warm start of v^
+  float2 ips2[2];                  // 1 / Im(p_k): carry (standard basis) -> v^
 };
 
 // Tile constants for exact anticausal carries between chunks of kTile

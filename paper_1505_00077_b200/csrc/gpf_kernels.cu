@@ -420,10 +420,7 @@ __global__ void __launch_bounds__(32 * kColGroup, GPF_COL_CTAS) k_colpass_tma(
 #endif
     GPF_TICK(2);
     PairState as;
-    as.wr[0] = make_float2(ca0.x, ca0.y);
-    as.wi[0] = make_float2(ca0.z, ca0.w);
-    as.wr[1] = make_float2(ca1.x, ca1.y);
-    as.wi[1] = make_float2(ca1.z, ca1.w);
+    ps_from_carry(as, ca0, ca1, fc);
     if (cy + 1 < ny) {
       ca0 = __ldg(ca_ptr + (size_t)(cy + 1) * ca_stride);
       ca1 = __ldg(ca_ptr + (size_t)(cy + 1) * ca_stride + 1);
@@ -443,7 +440,7 @@ __global__ void __launch_bounds__(32 * kColGroup, GPF_COL_CTAS) k_colpass_tma(
         xr[j] = make_float2(v.x, v.y);
         xr[j + 1] = make_float2(v.z, v.w);
       }
-      if (cy == 0) ps_set_gain(cs, xr[0], fc);
+      if (cy == 0) ps_set_gain_sweep(cs, xr[0], fc);
       if (rows == kTile) {
         // full chunk: both directions in one branch-free loop (two independent
         // recurrences per step), two rows per smem access. Step t runs the
@@ -455,26 +452,26 @@ __global__ void __launch_bounds__(32 * kColGroup, GPF_COL_CTAS) k_colpass_tma(
           float4* pa = reinterpret_cast<float4*>(stage_at(mcol, 30 - t, cm));
           float4* pc = reinterpret_cast<float4*>(stage_at(mcol, t, cm));
           if (t < kTile / 2) {
-            const float2 yb = ps_emit(as, fc.br2, fc.nbi2);
+            const float2 yb = ps_emit(as, fc.br2, fc.sbi2);
             ps_advance(as, xr[31 - t], fc);
             ps_advance(cs, xr[t], fc);
-            const float2 yc0 = ps_emit(cs, fc.ar2, fc.nai2);
-            const float2 ya = ps_emit(as, fc.br2, fc.nbi2);
+            const float2 yc0 = ps_emit(cs, fc.ar2, fc.sai2);
+            const float2 ya = ps_emit(as, fc.br2, fc.sbi2);
             ps_advance(as, xr[30 - t], fc);
             ps_advance(cs, xr[t + 1], fc);
-            const float2 yc1 = ps_emit(cs, fc.ar2, fc.nai2);
+            const float2 yc1 = ps_emit(cs, fc.ar2, fc.sai2);
             *pa = make_float4(ya.x, ya.y, yb.x, yb.y);
             *pc = make_float4(yc0.x, yc0.y, yc1.x, yc1.y);
           } else {  // the other direction's parked values seed the emits
             const float4 qa = *pa, qc = *pc;
-            const float2 yb = ps_emit_acc(as, fc.br2, fc.nbi2, make_float2(qa.z, qa.w));
+            const float2 yb = ps_emit_acc(as, fc.br2, fc.sbi2, make_float2(qa.z, qa.w));
             ps_advance(as, xr[31 - t], fc);
             ps_advance(cs, xr[t], fc);
-            const float2 yc0 = ps_emit_acc(cs, fc.ar2, fc.nai2, make_float2(qc.x, qc.y));
-            const float2 ya = ps_emit_acc(as, fc.br2, fc.nbi2, make_float2(qa.x, qa.y));
+            const float2 yc0 = ps_emit_acc(cs, fc.ar2, fc.sai2, make_float2(qc.x, qc.y));
+            const float2 ya = ps_emit_acc(as, fc.br2, fc.sbi2, make_float2(qa.x, qa.y));
             ps_advance(as, xr[30 - t], fc);
             ps_advance(cs, xr[t + 1], fc);
-            const float2 yc1 = ps_emit_acc(cs, fc.ar2, fc.nai2, make_float2(qc.z, qc.w));
+            const float2 yc1 = ps_emit_acc(cs, fc.ar2, fc.sai2, make_float2(qc.z, qc.w));
             *pa = make_float4(ya.x, ya.y, yb.x, yb.y);
             *pc = make_float4(yc0.x, yc0.y, yc1.x, yc1.y);
           }
@@ -483,7 +480,7 @@ __global__ void __launch_bounds__(32 * kColGroup, GPF_COL_CTAS) k_colpass_tma(
 #pragma unroll
         for (int j = kTile - 1; j >= 0; --j) {
           if (j < rows) {
-            *reinterpret_cast<float2*>(stage_at(mcol, j, cm)) = ps_emit(as, fc.br2, fc.nbi2);
+            *reinterpret_cast<float2*>(stage_at(mcol, j, cm)) = ps_emit(as, fc.br2, fc.sbi2);
             ps_advance(as, xr[j], fc);
           }
         }
@@ -492,7 +489,7 @@ __global__ void __launch_bounds__(32 * kColGroup, GPF_COL_CTAS) k_colpass_tma(
           if (j < rows) {
             float2* p = reinterpret_cast<float2*>(stage_at(mcol, j, cm));
             ps_advance(cs, xr[j], fc);
-            *p = add2(ps_emit(cs, fc.ar2, fc.nai2), *p);
+            *p = add2(ps_emit(cs, fc.ar2, fc.sai2), *p);
           }
         }
       }
@@ -707,10 +704,7 @@ __global__ void __launch_bounds__(MAXT, 1) k_colpass(const Tin* __restrict__ in_
     }
     produce_planes(buf, ftiles + (cy & 1) * 32 * 33, t_c, rc);
     PairState as;
-    as.wr[0] = make_float2(ca0.x, ca0.y);
-    as.wi[0] = make_float2(ca0.z, ca0.w);
-    as.wr[1] = make_float2(ca1.x, ca1.y);
-    as.wi[1] = make_float2(ca1.z, ca1.w);
+    ps_from_carry(as, ca0, ca1, fc);
     if (cy + 1 < ny) {
       ca0 = __ldg(ca_ptr + (size_t)(cy + 1) * ca_stride);
       ca1 = __ldg(ca_ptr + (size_t)(cy + 1) * ca_stride + 1);
@@ -720,11 +714,11 @@ __global__ void __launch_bounds__(MAXT, 1) k_colpass(const Tin* __restrict__ in_
       float2 xr[kTile];
 #pragma unroll
       for (int j = 0; j < kTile; ++j) xr[j] = mine[j];
-      if (cy == 0) ps_set_gain(cs, xr[0], fc);
+      if (cy == 0) ps_set_gain_sweep(cs, xr[0], fc);
 #pragma unroll
       for (int j = kTile - 1; j >= 0; --j) {
         if (j < rows) {
-          mine[j] = ps_emit(as, fc.br2, fc.nbi2);
+          mine[j] = ps_emit(as, fc.br2, fc.sbi2);
           ps_advance(as, xr[j], fc);
         }
       }
@@ -732,7 +726,7 @@ __global__ void __launch_bounds__(MAXT, 1) k_colpass(const Tin* __restrict__ in_
       for (int j = 0; j < kTile; ++j) {
         if (j < rows) {
           ps_advance(cs, xr[j], fc);
-          mine[j] = add2(ps_emit(cs, fc.ar2, fc.nai2), mine[j]);
+          mine[j] = add2(ps_emit(cs, fc.ar2, fc.sai2), mine[j]);
         }
       }
     }

@@ -90,10 +90,7 @@ __global__ void __launch_bounds__(MAXT, 1) k_rowpass(const Tin* __restrict__ in_
     for (int b = 0; b < nx; ++b) {
       const int s = b % nbuf, cols = min(32, w - b * 32);
       PairState as;
-      as.wr[0] = make_float2(c0.x, c0.y);
-      as.wi[0] = make_float2(c0.z, c0.w);
-      as.wr[1] = make_float2(c1.x, c1.y);
-      as.wi[1] = make_float2(c1.z, c1.w);
+      ps_from_carry(as, c0, c1, fc);
       if (b + 1 < nx) {
         c0 = __ldg(CH + (size_t)(b + 1) * ch_stride);
         c1 = __ldg(CH + (size_t)(b + 1) * ch_stride + 1);
@@ -101,7 +98,7 @@ __global__ void __launch_bounds__(MAXT, 1) k_rowpass(const Tin* __restrict__ in_
       // element [g][c][r] of slot s at tl[c * kRowBand]
       float2* tl = T + (size_t)s * tile_elems + (size_t)gl * 32 * kRowBand + r;
       mbar_wait(&full[s], (b / nbuf) & 1);
-      if (b == 0) ps_set_gain(cs, tl[0], fc);
+      if (b == 0) ps_set_gain_sweep(cs, tl[0], fc);
       if (cols == 32) {
         // Both directions in one loop (two independent recurrences per step):
         // step t runs the anticausal section at column 31-t and the causal one
@@ -111,11 +108,11 @@ __global__ void __launch_bounds__(MAXT, 1) k_rowpass(const Tin* __restrict__ in_
 #pragma unroll
         for (int t = 0; t < 32; ++t) {
           const int ca = 31 - t, cc = t;
-          const float2 ya = ps_emit(as, fc.br2, fc.nbi2);
+          const float2 ya = ps_emit(as, fc.br2, fc.sbi2);
           const float2 xa = tl[ca * kRowBand], xc = tl[cc * kRowBand];
           ps_advance(as, xa, fc);
           ps_advance(cs, xc, fc);
-          const float2 yc = ps_emit(cs, fc.ar2, fc.nai2);
+          const float2 yc = ps_emit(cs, fc.ar2, fc.sai2);
           if (t < 16) {
             ya_hi[ca - 16] = ya;
             yc_lo[cc] = yc;
@@ -131,7 +128,7 @@ __global__ void __launch_bounds__(MAXT, 1) k_rowpass(const Tin* __restrict__ in_
 #pragma unroll
         for (int c = 31; c >= 0; --c) {
           if (c < cols) {
-            ybuf[c] = ps_emit(as, fc.br2, fc.nbi2);
+            ybuf[c] = ps_emit(as, fc.br2, fc.sbi2);
             ps_advance(as, tl[c * kRowBand], fc);
           }
         }
@@ -139,7 +136,7 @@ __global__ void __launch_bounds__(MAXT, 1) k_rowpass(const Tin* __restrict__ in_
         for (int c = 0; c < 32; ++c) {
           if (c < cols) {
             ps_advance(cs, tl[c * kRowBand], fc);
-            const float2 o = add2(ps_emit(cs, fc.ar2, fc.nai2), ybuf[c]);
+            const float2 o = add2(ps_emit(cs, fc.ar2, fc.sai2), ybuf[c]);
             if (live) tl[c * kRowBand] = o;
           }
         }
@@ -458,10 +455,7 @@ __global__ void __launch_bounds__(192, 2) k_rowpass2(const Tin* __restrict__ in_
   for (int b = 0; b < nx; ++b) {
     const int s = b & 1, xs = b * 32, cols = min(32, w - xs);
     PairState as;
-    as.wr[0] = make_float2(c0.x, c0.y);
-    as.wi[0] = make_float2(c0.z, c0.w);
-    as.wr[1] = make_float2(c1.x, c1.y);
-    as.wi[1] = make_float2(c1.z, c1.w);
+    ps_from_carry(as, c0, c1, fc);
     if (b + 1 < nx) {
       c0 = __ldg(CH + (size_t)(b + 1) * ch_stride);
       c1 = __ldg(CH + (size_t)(b + 1) * ch_stride + 1);
@@ -471,7 +465,7 @@ __global__ void __launch_bounds__(192, 2) k_rowpass2(const Tin* __restrict__ in_
     GPF_TICK(5);
     mbar_wait(&full[s], (b >> 1) & 1);
     GPF_TICK(0);
-    if (b == 0) ps_set_gain(cs, tl[0], fc);
+    if (b == 0) ps_set_gain_sweep(cs, tl[0], fc);
     if (cols == 32) {
       // both directions in one loop: step t runs the anticausal sections at
       // column 31-t and the causal ones at column t; first-half outputs wait
@@ -482,18 +476,18 @@ __global__ void __launch_bounds__(192, 2) k_rowpass2(const Tin* __restrict__ in_
         if ((t & 1) == 1) asm volatile("" ::: "memory");
         const int ca = 31 - t, cc = t;
         if (t < 16) {
-          const float2 ya = ps_emit(as, fc.br2, fc.nbi2);
+          const float2 ya = ps_emit(as, fc.br2, fc.sbi2);
           const float2 xa = tl[ca * kRowBand], xc = tl[cc * kRowBand];
           ps_advance(as, xa, fc);
           ps_advance(cs, xc, fc);
           ya_hi[ca - 16] = ya;
-          yc_lo[cc] = ps_emit(cs, fc.ar2, fc.nai2);
+          yc_lo[cc] = ps_emit(cs, fc.ar2, fc.sai2);
         } else {  // the other direction's parked value seeds the emit
-          const float2 ya = ps_emit_acc(as, fc.br2, fc.nbi2, yc_lo[ca]);
+          const float2 ya = ps_emit_acc(as, fc.br2, fc.sbi2, yc_lo[ca]);
           const float2 xa = tl[ca * kRowBand], xc = tl[cc * kRowBand];
           ps_advance(as, xa, fc);
           ps_advance(cs, xc, fc);
-          const float2 yc = ps_emit_acc(cs, fc.ar2, fc.nai2, ya_hi[cc - 16]);
+          const float2 yc = ps_emit_acc(cs, fc.ar2, fc.sai2, ya_hi[cc - 16]);
           if (live) {
             tl[ca * kRowBand] = ya;
             tl[cc * kRowBand] = yc;
@@ -505,7 +499,7 @@ __global__ void __launch_bounds__(192, 2) k_rowpass2(const Tin* __restrict__ in_
 #pragma unroll
       for (int c = 31; c >= 0; --c) {
         if (c < cols) {
-          ybuf[c] = ps_emit(as, fc.br2, fc.nbi2);
+          ybuf[c] = ps_emit(as, fc.br2, fc.sbi2);
           ps_advance(as, tl[c * kRowBand], fc);
         }
       }
@@ -513,7 +507,7 @@ __global__ void __launch_bounds__(192, 2) k_rowpass2(const Tin* __restrict__ in_
       for (int c = 0; c < 32; ++c) {
         if (c < cols) {
           ps_advance(cs, tl[c * kRowBand], fc);
-          const float2 o = add2(ps_emit(cs, fc.ar2, fc.nai2), ybuf[c]);
+          const float2 o = add2(ps_emit(cs, fc.ar2, fc.sai2), ybuf[c]);
           if (live) tl[c * kRowBand] = o;
         }
       }
