@@ -899,8 +899,8 @@ static PFN_cuTensorMapEncodeTiled_v12000 tensor_map_encoder() {
   return encode;
 }
 
-// Output frames fp32 {w, h, count}, box {32 columns, 16 rows, 1}, 128B-swizzled
-// (the row pass's output tile); requires w % 4 == 0 and a 16-B aligned base.
+// fp32 frames {w, h, count}, box {32 columns, 16 rows, 1}, 128B-swizzled: the
+// row pass's output tile and f tile; requires w % 4 == 0 and a 16-B aligned base.
 static void encode_out_map(CUtensorMap* m, void* d_out, int w, int h, int count) {
   const cuuint64_t dims[3] = {(cuuint64_t)w, (cuuint64_t)h, (cuuint64_t)count};
   const cuuint64_t strides[2] = {(cuuint64_t)4 * w, (cuuint64_t)4 * w * h};
@@ -1072,11 +1072,16 @@ static void launch_passes(Plan& plan, const Tin* d_in, Tout* d_out, int count,
   if (pairs <= 12) {
     const int r2sm = (int)rowpass2_smem_bytes<Tin, Tout>(pairs);
     // fp32 output with 16-B rows: TMA output store (tensor map of this call's d_out)
-    const bool otma = sizeof(Tout) == 4 && (w % 4) == 0 &&
-                      (reinterpret_cast<uintptr_t>(d_out) % 16) == 0;
-    alignas(64) CUtensorMap omap;
+    const bool otma = sizeof(Tout) == 4 && sizeof(Tin) == 4 && (w % 4) == 0 &&
+                      (reinterpret_cast<uintptr_t>(d_out) % 16) == 0 &&
+                      (reinterpret_cast<uintptr_t>(d_in) % 16) == 0;
+    alignas(64) CUtensorMap omap, imap;
     std::memset(&omap, 0, sizeof(omap));
-    if (otma) encode_out_map(&omap, d_out, w, h, count);
+    std::memset(&imap, 0, sizeof(imap));
+    if (otma) {
+      encode_out_map(&omap, d_out, w, h, count);
+      encode_out_map(&imap, const_cast<Tin*>(d_in), w, h, count);  // same box shape for the f tiles
+    }
     // the default degree (N = 20, reference RangeParams) has a fully static build
     const bool n20 = plan.rc.degree == 20;
     auto k = n20 ? k_rowpass2<Tin, Tout, 20, false> : k_rowpass2<Tin, Tout, 0, false>;
@@ -1087,7 +1092,7 @@ static void launch_passes(Plan& plan, const Tin* d_in, Tout* d_out, int count,
           "cudaFuncSetAttribute");
     k<<<dim3((h + kRowBand - 1) / kRowBand, count), dim3(32, (pairs + 1) / 2), r2sm, st>>>(
         d_in, plan.scalars, plan.CH, d_out, d_fb, w, h, plan.nx, pairs, plan.fc, plan.rc, plan.vmap,
-        omap);
+        omap, imap);
   } else {
     k_rowpass<RMAXT, Tin, Tout><<<dim3((h + kRowBand - 1) / kRowBand, count),
                                   dim3(32, (pairs + 1) / 2 + kAux), rsm, st>>>(

@@ -265,16 +265,24 @@ constexpr int kRow2MaxN = 22;  // pairs <= 12
 
 template <typename Tin, typename Tout>
 __host__ __device__ constexpr size_t rowpass2_smem_bytes(int pairs) {
-  // V ring | f tiles | padded output tile | mbarriers | 1024-aligned swizzled output tile
+  // V ring | f tiles | padded output tile | mbarriers | 1024-aligned swizzled
+  // output tile | swizzled f tiles (TMA path)
   return sizeof(float2) * (size_t)pairs * 32 * kRowBand * kRow2Slots +
          sizeof(Tin) * kRowBand * 33 * kRow2Slots + sizeof(Tout) * kRowBand * 33 +
-         kRow2Slots * sizeof(uint64_t) + 16 + 1024 + sizeof(float) * kRowBand * 32;
+         kRow2Slots * sizeof(uint64_t) + 16 + 1024 + sizeof(float) * kRowBand * 32 * (1 + kRow2Slots);
 }
 
 // Contraction of kPx pixels per thread (pixel p -> row p & 15, column p >> 4),
 // their chains interleaved. Plane m adds c_m F_m to Q and c_{m-1} F_m to P;
 // plane 0 is Q-only, plane N+1 P-only (bilateral.cpp:117-148). Returns the
 // fallback count.
+// f tile element (row r, column c): padded [16][33] (cp.async path) or the
+// 128B-swizzled [16][32] box of the TMA path
+template <bool SW>
+__device__ __forceinline__ int f_at(int r, int c) {
+  return SW ? r * 32 + ((((c >> 2) ^ (r & 7))) << 2) + (c & 3) : r * 33 + c;
+}
+
 // OSW: write into the 128B-swizzled [16][32] fp32 tile of the TMA output store
 // (element (r, c) at r*32 + (((c/4) ^ (r%8)) * 4) + c%4) instead of the padded O.
 template <int kPx, int NFIX, bool OSW, typename Tin, typename Tout>
@@ -291,7 +299,7 @@ __device__ __forceinline__ unsigned contract_px(const float2* Ts, const Tin* Fs,
     const int p = min(p0 + k * nthr, kRowBand * 32 - 1);
     off[k] = (p >> 4) * kRowBand + (p & (kRowBand - 1));  // [col][row]
     // H as the column pass formed it (pixel_terms): fp64 difference, fp32 H
-    Hf[k] = static_cast<float>((static_cast<double>(Fs[(p & 15) * 33 + (p >> 4)]) - t_c) * rc.inv_sr);
+    Hf[k] = static_cast<float>((static_cast<double>(Fs[f_at<OSW>(p & 15, p >> 4)]) - t_c) * rc.inv_sr);
     cur[k] = Ts[off[k]];  // (F_0, F_1)
     qp[k] = make_float2(rc.c0 * cur[k].x, 0.f);                // plane 0
     W[k] = make_float2(rc.c0 * (Hf[k] * rc.w_step[0]), rc.c0);  // (c_1, c_0)
@@ -349,7 +357,7 @@ __device__ __forceinline__ unsigned contract_px(const float2* Ts, const Tin* Fs,
     if (p < kRowBand * 32 && (OSW || (pr < rows && pc < cols))) {  // the TMA store clips
       Tout o;
       if (!(fabsf(qp[k].x) > rc.q_thresh)) {
-        o = static_cast<Tout>(Fs[pr * 33 + pc]);
+        o = static_cast<Tout>(Fs[f_at<OSW>(pr, pc)]);
         if (pr < rows && pc < cols) ++nfb;
       } else if constexpr (sizeof(Tout) == sizeof(float)) {
         // fast quotient (2 ulp) inside its range; |Q| > threshold >> 2^-126 here
@@ -382,7 +390,8 @@ __global__ void __launch_bounds__(192, 2) k_rowpass2(const Tin* __restrict__ in_
                                                       int w, int h, int nx, int pairs,
                                                       FilterConsts fc, RangeConsts rc,
                                                       const __grid_constant__ CUtensorMap vmap,
-                                                      const __grid_constant__ CUtensorMap omap) {
+                                                      const __grid_constant__ CUtensorMap omap,
+                                                      const __grid_constant__ CUtensorMap imap) {
   extern __shared__ float4 smem4[];
   const int f = blockIdx.y, lane = threadIdx.x, warp = threadIdx.y;
   const int tid = warp * 32 + lane, nthr = blockDim.x * blockDim.y;
@@ -401,26 +410,32 @@ __global__ void __launch_bounds__(192, 2) k_rowpass2(const Tin* __restrict__ in_
     const uint32_t a = smem_u32(full + kRow2Slots);
     O2 = reinterpret_cast<float*>(base + (((a + 1023u) & ~1023u) - smem_u32(base)));
   }
+  float* F2 = O2 + kRowBand * 32;  // [slot][16][32] swizzled f tiles (TMA path)
   const Tin* in = in_all + (size_t)f * w * h;
   Tout* out = out_all + (size_t)f * w * h;
   const double t_c = scalars[2 * f];
 
-  // V box of strip b into slot s (TMA, completion on full[s]) and its f tile
-  // (one cp.async group per thread, waited before the contraction)
+  // V box of strip b into slot s (TMA, completion on full[s]) and its f tile:
+  // TMA path -- a swizzled tensor box completing on the same barrier; else
+  // one cp.async group per thread, waited before the contraction
   auto load_strip = [&](int b, int s) {
     const int xs = b * 32, ncol = min(32, w - xs);
     if (tid == 0) {
       fence_proxy_async();
-      mbar_arrive_expect_tx(&full[s], (uint32_t)(tile_elems * sizeof(float2)));
+      mbar_arrive_expect_tx(&full[s], (uint32_t)(tile_elems * sizeof(float2) +
+                                                 (OTMA ? sizeof(float) * kRowBand * 32 : 0)));
       tma_load_5d(T + (size_t)s * tile_elems, &vmap, 0, xs, y0 / kRowBand, 0, f, &full[s]);
+      if constexpr (OTMA) tma_load_3d(F2 + s * kRowBand * 32, &imap, xs, y0, f, &full[s]);
     }
-    Tin* Fs = F + s * kRowBand * 33;
-    for (int p = tid; p < kRowBand * 32; p += nthr) {
-      const int r = p >> 5, c = p & 31;
-      const bool ok = r < rows && c < ncol;
-      cp_async_zfill<sizeof(Tin)>(Fs + r * 33 + c, ok ? in + (size_t)(y0 + r) * w + xs + c : in, ok);
+    if constexpr (!OTMA) {
+      Tin* Fs = F + s * kRowBand * 33;
+      for (int p = tid; p < kRowBand * 32; p += nthr) {
+        const int r = p >> 5, c = p & 31;
+        const bool ok = r < rows && c < ncol;
+        cp_async_zfill<sizeof(Tin)>(Fs + r * 33 + c, ok ? in + (size_t)(y0 + r) * w + xs + c : in, ok);
+      }
+      cp_async_commit();
     }
-    cp_async_commit();
   };
 
   if (tid == 0) {
@@ -514,8 +529,10 @@ __global__ void __launch_bounds__(192, 2) k_rowpass2(const Tin* __restrict__ in_
     }
     GPF_TICK(1);
     // this strip's f tile: the newer group (strip b+1) may stay in flight
-    if (b + 1 < nx) asm volatile("cp.async.wait_group 1;\n" ::: "memory");
-    else asm volatile("cp.async.wait_group 0;\n" ::: "memory");
+    if constexpr (!OTMA) {
+      if (b + 1 < nx) asm volatile("cp.async.wait_group 1;\n" ::: "memory");
+      else asm volatile("cp.async.wait_group 0;\n" ::: "memory");
+    }
     if (OTMA && tid == 0) bulk_wait_read_all();  // the previous strip's store has left O2
     __syncthreads();
     GPF_TICK(2);
@@ -525,7 +542,7 @@ __global__ void __launch_bounds__(192, 2) k_rowpass2(const Tin* __restrict__ in_
     // (c_{m+1}, c_m) = (c_m, c_{m-1}) * H (w_m, w_{m-1}): three packed
     // instructions per plane. Plane 0 is Q-only, plane N+1 is P-only.
     const float2* Ts = T + (size_t)s * tile_elems;
-    const Tin* Fs = F + s * kRowBand * 33;
+    const Tin* Fs = OTMA ? reinterpret_cast<const Tin*>(F2 + s * kRowBand * 32) : F + s * kRowBand * 33;
     for (int p0 = tid; p0 < kRowBand * 32; p0 += nthr * 3) {
       // pixels per thread for this warp (warp-uniform: no work on pixels past the strip)
       const int wb = p0 - lane;
