@@ -95,6 +95,16 @@ gpf_status gpf_filter_gpf(const gpf_image* in, const gpf_spatial_params* sp,
 gpf_status gpf_gaussian_recursive(const gpf_image* in, double sigma_s,
                                   double kernel_scale, gpf_image** out);
 
+/* Taylor-polynomial baseline of degree rp->degree, truncation order
+ * K = degree / 2 (ref.h:109-113, proj/src/capi.cpp:194-207 -> taylor_bilateral,
+ * proj/src/core/bilateral.cpp:160-220): the 2K+2 moment images f^m smoothed by
+ * the recursive Gaussian and recombined per pixel; fp64 on the GPU, bitwise
+ * equal to the reference. Same NULL / validation / status behaviour and
+ * fallback rule as gpf_filter_gpf; GPF_BACKEND_DIRECT is rejected. */
+gpf_status gpf_filter_taylor(const gpf_image* in, const gpf_spatial_params* sp,
+                             const gpf_range_params* rp, gpf_backend backend,
+                             long long* fallback_count, gpf_image** out);
+
 /* Exact brute-force bilateral filter, Eq. (1) over the (2W+1)^2 window with
  * the boundary mode of sp (ref.h:97-98, proj/src/capi.cpp:164-174 ->
  * exact_bilateral, proj/src/core/bilateral.cpp:14-56). The MSE yardstick of

@@ -194,6 +194,23 @@ class Reference:
             return st, None
         return st, {"mse": rep.mse, "mse_db": rep.mse_db, "max_abs": rep.max_abs, "pixels": rep.pixels}
 
+    def taylor(self, img: np.ndarray, sigma_s: float, sigma_r: float, degree: int = 20,
+               backend: int = 1):
+        """Reference gpf_filter_taylor (capi.cpp:194-207): (status, out or None, fallbacks)."""
+        self.lib.gpf_filter_taylor.argtypes = [C.c_void_p, C.c_void_p, C.c_void_p, C.c_int,
+                                               C.POINTER(C.c_longlong), C.POINTER(C.c_void_p)]
+        sp = self.SpatialParams(sigma_s, 0, 0, 1.0)
+        rp = self.RangeParams(sigma_r, degree)
+        src = self._img(img)
+        out = C.c_void_p()
+        fb = C.c_longlong(-1)
+        st = self.lib.gpf_filter_taylor(src, C.byref(sp), C.byref(rp), backend, C.byref(fb),
+                                        C.byref(out))
+        self.lib.gpf_image_destroy(src)
+        if st != 0:
+            return st, None, fb.value
+        return st, self._take(out, img.shape), fb.value
+
     def exact(self, img: np.ndarray, sigma_s: float, sigma_r: float, boundary: int = 0) -> np.ndarray:
         sp = self.SpatialParams(sigma_s, 0, boundary, 1.0)
         rp = self.RangeParams(sigma_r, 20)

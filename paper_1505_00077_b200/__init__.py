@@ -6,10 +6,10 @@ host-side binding; it never computes the filter on the CPU.
 """
 from ._lib import LIB_PATH, build  # noqa: F401
 from .gpf import (GpfError, Image, Plan, compare_device, exact_device, gpf_compare,  # noqa: F401
-                  gpf_filter_exact, gpf_filter_gpf, gpf_gaussian_recursive, get_num_threads,
+                  gpf_filter_exact, gpf_filter_gpf, gpf_filter_taylor, gpf_gaussian_recursive, get_num_threads,
                   range_params, set_num_threads, spatial_params)
 
 __all__ = ["GpfError", "Image", "Plan", "gpf_filter_gpf", "gpf_gaussian_recursive",
-           "gpf_filter_exact", "gpf_compare", "exact_device", "compare_device",
+           "gpf_filter_exact", "gpf_filter_taylor", "gpf_compare", "exact_device", "compare_device",
            "range_params", "spatial_params", "set_num_threads", "get_num_threads", "build",
            "LIB_PATH"]

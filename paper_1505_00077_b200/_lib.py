@@ -29,6 +29,7 @@ EXPORTED = (
     "gpf_image_data", "gpf_image_cdata",
     "gpf_spatial_params_init", "gpf_range_params_init",
     "gpf_filter_gpf", "gpf_gaussian_recursive", "gpf_filter_exact", "gpf_compare",
+    "gpf_filter_taylor",
     "gpf_set_num_threads", "gpf_get_num_threads",
     "gpf_b200_plan_create", "gpf_b200_plan_destroy", "gpf_b200_plan_set_batch",
     "gpf_b200_plan_set_profiling", "gpf_b200_plan_stage_times", "gpf_b200_plan_workspace_bytes",
@@ -80,6 +81,8 @@ def _declare(lib: C.CDLL) -> C.CDLL:
                                    C.c_int, C.POINTER(C.c_longlong), pvp]
     lib.gpf_gaussian_recursive.argtypes = [vp, C.c_double, C.c_double, pvp]
     lib.gpf_filter_exact.argtypes = [vp, C.POINTER(SpatialParams), C.POINTER(RangeParams), pvp]
+    lib.gpf_filter_taylor.argtypes = [vp, C.POINTER(SpatialParams), C.POINTER(RangeParams), C.c_int,
+                                      C.POINTER(C.c_longlong), pvp]
     lib.gpf_compare.argtypes = [vp, vp, C.c_int, C.POINTER(ErrorReport)]
     lib.gpf_b200_exact_f32.argtypes = [vp, vp, C.c_int, C.c_int, C.c_int, C.POINTER(SpatialParams),
                                        C.POINTER(RangeParams), vp]

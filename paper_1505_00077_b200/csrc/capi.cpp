@@ -306,6 +306,31 @@ gpf_status gpf_gaussian_recursive(const gpf_image* in, double sigma_s, double ke
   });
 }
 
+gpf_status gpf_filter_taylor(const gpf_image* in, const gpf_spatial_params* sp,
+                             const gpf_range_params* rp, gpf_backend backend,
+                             long long* fallback_count, gpf_image** out) {
+  if (in == nullptr || sp == nullptr || rp == nullptr || out == nullptr)
+    return fail(GPF_ERR_INVALID_ARGUMENT, "null argument");
+  *out = nullptr;
+  return guarded([&] {
+    const gpfb::Params p = validate(in->w, in->h, *sp, *rp, backend, 0);
+    current_device();
+    const size_t n = (size_t)in->w * in->h;
+    DevBuf din(n * sizeof(double)), dout(n * sizeof(double)), dfb(sizeof(unsigned long long));
+    cuda_check(cudaMemcpy(din.p, in->data.data(), n * sizeof(double), cudaMemcpyHostToDevice), "H2D");
+    gpfb::run_taylor_f64(static_cast<const double*>(din.p), static_cast<double*>(dout.p), in->w, in->h,
+                         p.sigma_s, p.kernel_scale, p.sigma_r, p.degree,
+                         static_cast<unsigned long long*>(dfb.p), nullptr);
+    auto* res = new gpf_image{in->w, in->h, std::vector<double>(n)};
+    std::unique_ptr<gpf_image> hold(res);
+    unsigned long long fb = 0;
+    cuda_check(cudaMemcpy(res->data.data(), dout.p, n * sizeof(double), cudaMemcpyDeviceToHost), "D2H");
+    cuda_check(cudaMemcpy(&fb, dfb.p, sizeof(fb), cudaMemcpyDeviceToHost), "D2H");
+    if (fallback_count) *fallback_count = static_cast<long long>(fb);
+    *out = hold.release();
+  });
+}
+
 gpf_status gpf_filter_exact(const gpf_image* in, const gpf_spatial_params* sp,
                             const gpf_range_params* rp, gpf_image** out) {
   if (in == nullptr || sp == nullptr || rp == nullptr || out == nullptr)

@@ -155,6 +155,11 @@ ErrorStats compare_f32(const float* d_ref, const float* d_test, int w, int h, in
                        cudaStream_t st);
 ErrorStats compare_f64(const double* d_ref, const double* d_test, int w, int h, int border,
                        cudaStream_t st);
+// Taylor-polynomial baseline (taylor_bilateral, bilateral.cpp:160-220), fp64,
+// bitwise equal to the reference; *d_fb receives the fallback count (taylor.cu).
+void run_taylor_f64(const double* d_in, double* d_out, int w, int h, double sigma_s,
+                    double kernel_scale, double sigma_r, int degree, unsigned long long* d_fb,
+                    cudaStream_t st);
 // Single-plane recursive Gaussian (gpf_gaussian_recursive), fp64 in/out.
 void run_gaussian_f64(const double* d_in, double* d_out, double* d_tmp, int w, int h,
                       double sigma_s, double scale, cudaStream_t st);

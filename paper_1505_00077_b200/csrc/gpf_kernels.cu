@@ -580,7 +580,7 @@ __global__ void __launch_bounds__(32 * kColGroup, 6) k_col_carry_tma(
   extern __shared__ float4 smem4[];
   float2* buf = reinterpret_cast<float2*>(smem4);  // [kColGroup][32][33]
   const int f = blockIdx.y, lane = threadIdx.x, gl = threadIdx.y;
-  const int tid = gl * 32 + lane;
+  // (no CTA-level thread index needed)
   const int strip = blockIdx.x / groups, grp = blockIdx.x - strip * groups;
   const int pair0 = grp * kColGroup, npairs = min(kColGroup, pairs - pair0);
   const int g = pair0 + gl;

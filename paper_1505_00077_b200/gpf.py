@@ -110,6 +110,20 @@ def gpf_gaussian_recursive(img: np.ndarray, sigma_s: float, kernel_scale: float 
     return Image(out).numpy()
 
 
+def gpf_filter_taylor(img: np.ndarray, sp: SpatialParams | None = None, rp: RangeParams | None = None,
+                      backend: int = GPF_BACKEND_RECURSIVE):
+    """Taylor-polynomial baseline (reference gpf_filter_taylor), on the GPU.
+    Returns ``(out, fallback_count)``."""
+    sp = sp or spatial_params()
+    rp = rp or range_params()
+    src = Image.from_array(img)
+    out = C.c_void_p()
+    fb = C.c_longlong(-1)
+    _check(_lib.lib().gpf_filter_taylor(src.h, C.byref(sp), C.byref(rp), backend, C.byref(fb),
+                                        C.byref(out)))
+    return Image(out).numpy(), fb.value
+
+
 def gpf_filter_exact(img: np.ndarray, sp: SpatialParams | None = None,
                      rp: RangeParams | None = None) -> np.ndarray:
     """Exact brute-force bilateral filter (reference gpf_filter_exact), on the GPU."""
