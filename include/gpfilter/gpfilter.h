@@ -131,6 +131,19 @@ gpf_status gpf_compare(const gpf_image* ref, const gpf_image* test,
 gpf_status gpf_set_num_threads(int n);
 int gpf_get_num_threads(void);
 
+/* PGM I/O (ref.h:171-186, proj/src/capi.cpp:311-349):
+ * binary (P5) or ASCII (P2), maxval 255. Parse failures return one of the
+ * GPF_ERR_PGM_* codes and gpf_last_error() names the byte offset; file errors
+ * return GPF_ERR_IO. Writing produces "P5\n<w> <h>\n255\n" with samples
+ * clamped to [0, 255] and rounded half away from zero. */
+gpf_status gpf_read_pgm(const char* path, gpf_image** out);
+gpf_status gpf_decode_pgm(const uint8_t* bytes, size_t size, gpf_image** out);
+gpf_status gpf_write_pgm(const gpf_image* img, const char* path);
+gpf_status gpf_encode_pgm(const gpf_image* img, uint8_t** bytes, size_t* size);
+
+/* Releases a buffer returned by gpf_encode_pgm. */
+void gpf_free_bytes(uint8_t* bytes);
+
 #ifdef __cplusplus
 } /* extern "C" */
 #endif

@@ -221,5 +221,31 @@ class Reference:
         assert st == 0
         return self._take(out, img.shape)
 
+    def decode_pgm(self, data: bytes):
+        """Reference gpf_decode_pgm: (status, array or None, last_error)."""
+        self.lib.gpf_decode_pgm.argtypes = [C.c_void_p, C.c_size_t, C.POINTER(C.c_void_p)]
+        self.lib.gpf_image_width.argtypes = [C.c_void_p]
+        self.lib.gpf_image_height.argtypes = [C.c_void_p]
+        buf = C.create_string_buffer(data, len(data))
+        out = C.c_void_p()
+        st = self.lib.gpf_decode_pgm(buf, len(data), C.byref(out))
+        if st != 0:
+            return st, None, self.last_error()
+        w, h = self.lib.gpf_image_width(out), self.lib.gpf_image_height(out)
+        return st, self._take(out, (h, w)), ""
+
+    def encode_pgm(self, img: np.ndarray) -> bytes:
+        self.lib.gpf_encode_pgm.argtypes = [C.c_void_p, C.POINTER(C.POINTER(C.c_uint8)),
+                                            C.POINTER(C.c_size_t)]
+        self.lib.gpf_free_bytes.argtypes = [C.POINTER(C.c_uint8)]
+        src = self._img(img)
+        p = C.POINTER(C.c_uint8)()
+        n = C.c_size_t()
+        assert self.lib.gpf_encode_pgm(src, C.byref(p), C.byref(n)) == 0
+        out = bytes(p[:n.value])
+        self.lib.gpf_free_bytes(p)
+        self.lib.gpf_image_destroy(src)
+        return out
+
     def last_error(self) -> str:
         return self.lib.gpf_last_error().decode()

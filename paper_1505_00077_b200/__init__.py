@@ -4,6 +4,7 @@ The compute path is libgpfilter_b200.so (hand-written sm_100a kernels behind a
 C ABI that mirrors the reference's gpf_filter_gpf). This package is the thin
 host-side binding; it never computes the filter on the CPU.
 """
+from . import gpf  # noqa: F401
 from ._lib import LIB_PATH, build  # noqa: F401
 from .gpf import (GpfError, Image, Plan, compare_device, exact_device, gpf_compare,  # noqa: F401
                   gpf_filter_exact, gpf_filter_gpf, gpf_filter_taylor, gpf_gaussian_recursive, get_num_threads,

@@ -17,6 +17,8 @@ GPF_OK = 0
 GPF_ERR_INVALID_ARGUMENT = 1
 GPF_ERR_IO = 2
 GPF_ERR_SIGMA_TOO_SMALL = 3
+GPF_ERR_PGM_BAD_MAGIC, GPF_ERR_PGM_BAD_DIMS, GPF_ERR_PGM_BAD_MAXVAL = 4, 5, 6
+GPF_ERR_PGM_TRUNCATED, GPF_ERR_PGM_BAD_PIXEL = 7, 8
 GPF_ERR_UNKNOWN = 9
 
 GPF_BOUNDARY_REPLICATE, GPF_BOUNDARY_REFLECT, GPF_BOUNDARY_ZERO = 0, 1, 2
@@ -29,7 +31,8 @@ EXPORTED = (
     "gpf_image_data", "gpf_image_cdata",
     "gpf_spatial_params_init", "gpf_range_params_init",
     "gpf_filter_gpf", "gpf_gaussian_recursive", "gpf_filter_exact", "gpf_compare",
-    "gpf_filter_taylor",
+    "gpf_filter_taylor", "gpf_read_pgm", "gpf_decode_pgm", "gpf_write_pgm", "gpf_encode_pgm",
+    "gpf_free_bytes",
     "gpf_set_num_threads", "gpf_get_num_threads",
     "gpf_b200_plan_create", "gpf_b200_plan_destroy", "gpf_b200_plan_set_batch",
     "gpf_b200_plan_set_profiling", "gpf_b200_plan_stage_times", "gpf_b200_plan_workspace_bytes",
@@ -81,6 +84,11 @@ def _declare(lib: C.CDLL) -> C.CDLL:
                                    C.c_int, C.POINTER(C.c_longlong), pvp]
     lib.gpf_gaussian_recursive.argtypes = [vp, C.c_double, C.c_double, pvp]
     lib.gpf_filter_exact.argtypes = [vp, C.POINTER(SpatialParams), C.POINTER(RangeParams), pvp]
+    lib.gpf_read_pgm.argtypes = [C.c_char_p, pvp]
+    lib.gpf_decode_pgm.argtypes = [C.c_void_p, C.c_size_t, pvp]
+    lib.gpf_write_pgm.argtypes = [vp, C.c_char_p]
+    lib.gpf_encode_pgm.argtypes = [vp, C.POINTER(C.POINTER(C.c_uint8)), C.POINTER(C.c_size_t)]
+    lib.gpf_free_bytes.argtypes = [C.POINTER(C.c_uint8)]
     lib.gpf_filter_taylor.argtypes = [vp, C.POINTER(SpatialParams), C.POINTER(RangeParams), C.c_int,
                                       C.POINTER(C.c_longlong), pvp]
     lib.gpf_compare.argtypes = [vp, vp, C.c_int, C.POINTER(ErrorReport)]

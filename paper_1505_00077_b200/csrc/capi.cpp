@@ -21,6 +21,7 @@
 
 #include "gpf_internal.h"
 #include "gpfilter/gpfilter.h"
+#include "pgm.h"
 #include "gpfilter/gpfilter_b200.h"
 
 struct gpf_image {
@@ -368,6 +369,49 @@ gpf_status gpf_compare(const gpf_image* ref, const gpf_image* test, int exclude_
                 out);
   });
 }
+
+// ----------------------------------------------------------------- PGM I/O
+namespace {
+void deliver_pgm(gpfb::pgm::Decoded&& d, gpf_image** out) {
+  *out = new gpf_image{d.w, d.h, std::move(d.pixels)};
+}
+}  // namespace
+
+gpf_status gpf_read_pgm(const char* path, gpf_image** out) {
+  if (path == nullptr || out == nullptr) return fail(GPF_ERR_INVALID_ARGUMENT, "null argument");
+  *out = nullptr;
+  return guarded([&] {
+    const std::vector<uint8_t> bytes = gpfb::pgm::read_file(path);
+    deliver_pgm(gpfb::pgm::decode(bytes.data(), bytes.size()), out);
+  });
+}
+
+gpf_status gpf_decode_pgm(const uint8_t* bytes, size_t size, gpf_image** out) {
+  if (bytes == nullptr || out == nullptr) return fail(GPF_ERR_INVALID_ARGUMENT, "null argument");
+  *out = nullptr;
+  return guarded([&] { deliver_pgm(gpfb::pgm::decode(bytes, size), out); });
+}
+
+gpf_status gpf_write_pgm(const gpf_image* img, const char* path) {
+  if (img == nullptr || path == nullptr) return fail(GPF_ERR_INVALID_ARGUMENT, "null argument");
+  return guarded([&] { gpfb::pgm::write_file(path, gpfb::pgm::encode(img->data.data(), img->w, img->h)); });
+}
+
+gpf_status gpf_encode_pgm(const gpf_image* img, uint8_t** bytes, size_t* size) {
+  if (img == nullptr || bytes == nullptr || size == nullptr)
+    return fail(GPF_ERR_INVALID_ARGUMENT, "null argument");
+  *bytes = nullptr;
+  *size = 0;
+  return guarded([&] {
+    const std::vector<uint8_t> buf = gpfb::pgm::encode(img->data.data(), img->w, img->h);
+    auto* mem = new uint8_t[buf.size()];
+    std::memcpy(mem, buf.data(), buf.size());
+    *bytes = mem;
+    *size = buf.size();
+  });
+}
+
+void gpf_free_bytes(uint8_t* bytes) { delete[] bytes; }
 
 gpf_status gpf_set_num_threads(int n) {
   if (n < 1) return fail(GPF_ERR_INVALID_ARGUMENT, "thread count must be >= 1");

@@ -165,6 +165,36 @@ def compare_device(d_ref, d_test, width: int, height: int, exclude_border: int =
     return _report(rep)
 
 
+def read_pgm(path: str) -> np.ndarray:
+    """gpf_read_pgm: P5/P2 file -> float64 array (raises GpfError with the PGM status)."""
+    out = C.c_void_p()
+    _check(_lib.lib().gpf_read_pgm(path.encode(), C.byref(out)))
+    return Image(out).numpy()
+
+
+def decode_pgm(data: bytes) -> np.ndarray:
+    out = C.c_void_p()
+    buf = C.create_string_buffer(data, len(data))
+    _check(_lib.lib().gpf_decode_pgm(buf, len(data), C.byref(out)))
+    return Image(out).numpy()
+
+
+def encode_pgm(img: np.ndarray) -> bytes:
+    src = Image.from_array(img)
+    p = C.POINTER(C.c_uint8)()
+    n = C.c_size_t()
+    _check(_lib.lib().gpf_encode_pgm(src.h, C.byref(p), C.byref(n)))
+    try:
+        return bytes(p[:n.value])
+    finally:
+        _lib.lib().gpf_free_bytes(p)
+
+
+def write_pgm(img: np.ndarray, path: str) -> None:
+    src = Image.from_array(img)
+    _check(_lib.lib().gpf_write_pgm(src.h, path.encode()))
+
+
 def set_num_threads(n: int) -> None:
     _check(_lib.lib().gpf_set_num_threads(n))
 

@@ -1,0 +1,78 @@
+"""gpf_b200 command-line front end (filter / compare / bench; the reference
+CLI's flags and CSV protocol, proj/tools/gpf_cli.cpp). Argument errors run on
+CPU; the filtering runs are GPU tests."""
+import csv
+import os
+import subprocess
+
+import numpy as np
+import pytest
+
+from paper_1505_00077_b200 import synth
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+CLI = os.path.join(ROOT, "paper_1505_00077_b200", "gpf_b200")
+
+
+def run(*args):
+    return subprocess.run([CLI, *args], capture_output=True, text=True)
+
+
+@pytest.fixture(scope="module")
+def cli():
+    if not os.path.exists(CLI):
+        subprocess.run(["make", "-s", "-C", os.path.dirname(CLI)], check=True)
+    return CLI
+
+
+def test_cli_argument_errors(cli, tmp_path):
+    r = run("filter", "--input", "x.pgm")
+    assert r.returncode == 1 and "error: --output: is required" in r.stderr
+    r = run("filter", "--input", "x", "--output", "y", "--method", "median", "--sigma-s", "2",
+            "--sigma-r", "30")
+    assert r.returncode == 1 and "--method" in r.stderr
+    r = run("filter", "--input", str(tmp_path / "missing.pgm"), "--output", "y", "--method", "gpf",
+            "--sigma-s", "2", "--sigma-r", "30")
+    assert r.returncode == 1 and r.stderr.startswith("error: --input: cannot open")
+    r = run("bench", "--input", "x", "--method", "gpf", "--sigma-s-list", "2,-1", "--sigma-r", "30",
+            "--degree", "20", "--backend", "recursive", "--csv", "o.csv")
+    assert r.returncode == 1 and "--sigma-s-list" in r.stderr
+    r = run("kernel-error")
+    assert r.returncode == 1 and "not provided" in r.stderr
+    assert run("--version").stdout.strip().endswith("b200")
+
+
+@pytest.mark.gpu
+def test_cli_filter_compare_bench(cli, gpu, reference, tmp_path):
+    img = np.round(synth.rects_image(96, 64, 6, 10.0, 3)).astype(np.float64)
+    src = tmp_path / "in.pgm"
+    gpu.gpf.write_pgm(img, str(src))
+    out = tmp_path / "out.pgm"
+    r = run("filter", "--input", str(src), "--output", str(out), "--method", "gpf", "--sigma-s", "3",
+            "--sigma-r", "30")
+    assert r.returncode == 0, r.stderr
+    st, ref, _ = reference.gpf(img, 3.0, 30.0, 20)
+    want = np.frombuffer(reference.encode_pgm(ref)[-96 * 64:], np.uint8).astype(int)
+    got = np.frombuffer(out.read_bytes()[-96 * 64:], np.uint8).astype(int)
+    assert np.abs(got - want).max() <= 1 and (got == want).mean() > 0.999  # rounding ties only
+    ex = tmp_path / "ex.pgm"
+    assert run("filter", "--input", str(src), "--output", str(ex), "--method", "exact", "--sigma-s",
+               "2", "--sigma-r", "30").returncode == 0
+    r = run("compare", "--ref", str(ex), "--test", str(out), "--exclude-border", "2")
+    assert r.returncode == 0 and r.stdout.startswith("mse=")
+    fields = dict(kv.split("=") for kv in r.stdout.split())
+    rep = gpu.gpf_compare(gpu.gpf.read_pgm(str(ex)), gpu.gpf.read_pgm(str(out)), 2)
+    assert float(fields["mse"]) == pytest.approx(rep["mse"], rel=1e-12)
+    assert int(fields["pixels"]) == rep["pixels"] == 92 * 60
+    table = tmp_path / "bench.csv"
+    r = run("bench", "--input", str(src), "--method", "gpf,exact,taylor", "--sigma-s-list", "2,4.5",
+            "--sigma-r", "30", "--degree", "20", "--backend", "recursive", "--repeats", "2",
+            "--warmup", "1", "--csv", str(table))
+    assert r.returncode == 0, r.stderr
+    rows = list(csv.reader(open(table)))
+    assert rows[0] == ["method", "backend", "sigma_s", "sigma_r", "degree", "pixels", "repeats",
+                       "median_seconds"]
+    assert [(x[0], x[2]) for x in rows[1:]] == [("gpf", "2.0"), ("gpf", "4.5"), ("exact", "2.0"),
+                                              ("exact", "4.5"), ("taylor", "2.0"), ("taylor", "4.5")]
+    assert all(x[1] == "recursive" and x[3] == "30.0" and x[4] == "20" and x[5] == str(96 * 64)
+               and x[6] == "2" and float(x[7]) > 0 for x in rows[1:])
