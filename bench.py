@@ -162,12 +162,12 @@ def algorithmic_bytes_per_px(pairs: int) -> dict:
     """HBM bytes each stage must move per pixel (fp32 frames, N+2 = 2*pairs
     planes; carries every 32 samples: 32 B per (pair, line, chunk) = pairs B/px).
       mean       f                                   4
-      col_carry  f in; CA + EM (plane seeds) out     4 + pairs + 8
+      col_carry  seeds: f in, EM out; carries: EM in, CA out   4 + 8 + 8 + pairs
       colpass    EM + CA in; V + AH out              8 + pairs + 8 pairs + pairs
       row_scan   AH in, CH out                       2 pairs
       rowpass    V + CH + f in; out                  8 pairs + pairs + 4 + 4
-    (ncu dram__bytes of each launch agree to within 3%: profiles/r01_v17_traffic.csv)"""
-    return {"mean": 4, "col_carry": 12 + pairs, "colpass": 8 + 10 * pairs, "row_scan": 2 * pairs,
+    (ncu dram__bytes of each launch agree to within 3%: profiles/r01_v26_traffic.csv)"""
+    return {"mean": 4, "col_carry": 20 + pairs, "colpass": 8 + 10 * pairs, "row_scan": 2 * pairs,
             "rowpass": 9 * pairs + 8}
 
 
