@@ -484,8 +484,6 @@ def bench_c4(args):
         if n_loc:
             plan.filter_device(d_in, d_out, n_loc, d_fb, st.cuda_stream)
 
-    for st in streams:
-        st.wait_stream(main)
     for _ in range(args.warmup):
         step()
     torch.cuda.synchronize()
