@@ -17,7 +17,7 @@ def test_roofline_helpers():
     assert sum(bpp.values()) == 282 and bpp["rowpass"] == 107
     assert bench.fp32_peak_tflops({"sm_max_mhz": 1965.0}) == pytest.approx(74.4, abs=0.05)
     r = bench.roofline_of(1000, 1.0, 100, 10, 1000.0, 74.4)  # HBM-bound
-    assert r["bound"] == "hbm" and r["unit"] == "GB/s" and r["achieved"] == pytest.approx(100.0)
+    assert r["bound"] == "hbm" and r["unit"] == "GB/s" and r["achieved"] == pytest.approx(0.1)
     r = bench.roofline_of(1000, 1.0, 1, 10 ** 9, 1000.0, 74.4)  # FLOP-bound
     assert r["bound"] == "fp32" and r["unit"] == "TFLOP/s"
 
