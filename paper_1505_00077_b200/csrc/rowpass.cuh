@@ -424,7 +424,11 @@ __global__ void __launch_bounds__(192, 2) k_rowpass2(const Tin* __restrict__ in_
       fence_proxy_async();
       mbar_arrive_expect_tx(&full[s], (uint32_t)(tile_elems * sizeof(float2) +
                                                  (OTMA ? sizeof(float) * kRowBand * 32 : 0)));
+#ifdef GPF_DIAG_L2V  // diagnostic: V boxes from a small L2-resident region
+      tma_load_5d(T + (size_t)s * tile_elems, &vmap, 0, (b & 3) * 32, blockIdx.x & 1, 0, f, &full[s]);
+#else
       tma_load_5d(T + (size_t)s * tile_elems, &vmap, 0, xs, y0 / kRowBand, 0, f, &full[s]);
+#endif
       if constexpr (OTMA) tma_load_3d(F2 + s * kRowBand * 32, &imap, xs, y0, f, &full[s]);
     }
     if constexpr (!OTMA) {
@@ -481,7 +485,12 @@ __global__ void __launch_bounds__(192, 2) k_rowpass2(const Tin* __restrict__ in_
     mbar_wait(&full[s], (b >> 1) & 1);
     GPF_TICK(0);
     if (b == 0) ps_set_gain_sweep(cs, tl[0], fc);
-    if (cols == 32) {
+#ifdef GPF_DIAG_NO_SWEEP
+    constexpr bool kSweep = false;
+#else
+    constexpr bool kSweep = true;
+#endif
+    if (kSweep && cols == 32) {
       // both directions in one loop: step t runs the anticausal sections at
       // column 31-t and the causal ones at column t; first-half outputs wait
       // in registers, second-half outputs add them and are written in place
@@ -509,7 +518,7 @@ __global__ void __launch_bounds__(192, 2) k_rowpass2(const Tin* __restrict__ in_
           }
         }
       }
-    } else {  // last, partial strip
+    } else if (kSweep) {  // last, partial strip
       float2 ybuf[32];
 #pragma unroll
       for (int c = 31; c >= 0; --c) {
@@ -543,7 +552,11 @@ __global__ void __launch_bounds__(192, 2) k_rowpass2(const Tin* __restrict__ in_
     // instructions per plane. Plane 0 is Q-only, plane N+1 is P-only.
     const float2* Ts = T + (size_t)s * tile_elems;
     const Tin* Fs = OTMA ? reinterpret_cast<const Tin*>(F2 + s * kRowBand * 32) : F + s * kRowBand * 33;
+#ifdef GPF_DIAG_NO_CONTRACT
+    for (int p0 = tid; p0 < 0; p0 += nthr * 3) {
+#else
     for (int p0 = tid; p0 < kRowBand * 32; p0 += nthr * 3) {
+#endif
       // pixels per thread for this warp (warp-uniform: no work on pixels past the strip)
       const int wb = p0 - lane;
       Tout* Od = OTMA ? reinterpret_cast<Tout*>(O2) : O;
