@@ -157,6 +157,11 @@ RangeConsts make_range_consts(const Params& p) {
   rc.p_scale = static_cast<float>(std::ldexp(1.0, k));
   for (int n = 0; n < kMaxPlanes; ++n)
     rc.w_step[n] = static_cast<float>(std::ldexp(1.0, k) / (n + 1));
+  double kc = std::ldexp(1.0, -s0);  // c0
+  for (int n = 0; n < kMaxPlanes; ++n) {
+    rc.k_coef[n] = static_cast<float>(kc);
+    kc *= std::ldexp(1.0, k) / (n + 1);
+  }
   const double mass = kernel_mass_1d(p.sigma_s, default_window_radius(p.sigma_s));
   rc.q_thresh = static_cast<float>(1e-8 / (mass * mass * p.kernel_scale));
   return rc;

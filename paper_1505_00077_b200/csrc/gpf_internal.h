@@ -66,6 +66,7 @@ struct RangeConsts {
   float c0;           // 2^-s0     (weight of plane 0)
   float p_scale;      // 2^k       (P uses planes n+1)
   float w_step[kMaxPlanes];  // 2^k/(n+1): c_{n+1} = c_n * H * w_step[n]
+  float k_coef[kMaxPlanes];  // 2^-s0 2^{kn} / n!: c_n = H^n k_coef[n] (Horner contraction)
   float q_thresh;     // kQMin / (mass^2 * kernel_scale)  (bilateral.hpp:85)
   int planes;         // N + 2
   int pairs;          // ceil(planes / 2)

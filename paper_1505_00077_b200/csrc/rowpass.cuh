@@ -292,7 +292,6 @@ __device__ __forceinline__ unsigned contract_px(const float2* Ts, const Tin* Fs,
   unsigned nfb = 0;
   const int nN = NFIX > 0 ? NFIX : rc.degree;  // planes 0..N+1
   float Hf[kPx];
-  float2 qp[kPx], W[kPx], cur[kPx];
   int off[kPx];
 #pragma unroll
   for (int k = 0; k < kPx; ++k) {
@@ -300,53 +299,44 @@ __device__ __forceinline__ unsigned contract_px(const float2* Ts, const Tin* Fs,
     off[k] = (p >> 4) * kRowBand + (p & (kRowBand - 1));  // [col][row]
     // H as the column pass formed it (pixel_terms): fp64 difference, fp32 H
     Hf[k] = static_cast<float>((static_cast<double>(Fs[f_at<OSW>(p & 15, p >> 4)]) - t_c) * rc.inv_sr);
-    cur[k] = Ts[off[k]];  // (F_0, F_1)
-    qp[k] = make_float2(rc.c0 * cur[k].x, 0.f);                // plane 0
-    W[k] = make_float2(rc.c0 * (Hf[k] * rc.w_step[0]), rc.c0);  // (c_1, c_0)
   }
-  // planes m = 1 .. N (odd m: .y of the pair in cur, even m opens the next
-  // pair), unrolled to N (static build) or to kRow2MaxN with an early exit so
-  // smem offsets and weight constants are immediates. Scalar form -- four
-  // single-lane FP32 ops per plane, 4 pipe cycles against 6 for the packed
-  // (c_m, c_{m-1}) pair form (measured 3 % faster row pass):
-  //   Q += c_m F_m,  P += c_{m-1} F_m,  c_{m+1} = c_m (H w_m)
-  float cq[kPx], cp[kPx];
-#pragma unroll
-  for (int k = 0; k < kPx; ++k) {
-    cq[k] = W[k].x;
-    cp[k] = W[k].y;
-  }
-#pragma unroll
-  for (int m = 1; m <= (NFIX > 0 ? NFIX : kRow2MaxN); m += 2) {
-    if (m > nN) break;
+  // Q = sum_{n<=N} c_n F_n and P = sum_{n<=N} c_n F_{n+1} with c_n = H^n k_n
+  // share the coefficient polynomial: Horner in H over n = N..0 on the pair
+  //   (Q, P) <- (Q, P) H + k_n (F_n, F_{n+1}),
+  // one packed multiply and one packed FMA per plane. (F_n, F_{n+1}) is plane
+  // pair n/2 for even n; for odd n it straddles two pairs (lo.y, hi.x). Every
+  // partial sum is a tail of the same series in unscaled units (k_n F_n =
+  // F_n-bar / n!), so no intermediate leaves the range the forward sum uses.
+  // Unrolled to N (static build) or to kRow2MaxN with a guard, so smem
+  // offsets and the k_n are immediates.
+  constexpr int kTop = NFIX > 0 ? NFIX : kRow2MaxN;
+  float2 acc[kPx], hi[kPx];
+  {  // n = N
+    const float kn = rc.k_coef[nN];
 #pragma unroll
     for (int k = 0; k < kPx; ++k) {
-      qp[k].x = fmaf(cq[k], cur[k].y, qp[k].x);
-      qp[k].y = fmaf(cp[k], cur[k].y, qp[k].y);
-      cp[k] = cq[k];
-      cq[k] *= Hf[k] * rc.w_step[m];
-    }
-    if (m + 1 > nN) break;
-#pragma unroll
-    for (int k = 0; k < kPx; ++k) {
-      cur[k] = Ts[off[k] + ((m + 1) >> 1) * 32 * kRowBand];
-      qp[k].x = fmaf(cq[k], cur[k].x, qp[k].x);
-      qp[k].y = fmaf(cp[k], cur[k].x, qp[k].y);
-      cp[k] = cq[k];
-      cq[k] *= Hf[k] * rc.w_step[m + 1];
+      const float2 lo = Ts[off[k] + (nN >> 1) * 32 * kRowBand];
+      float2 t = lo;
+      if (nN & 1) t = make_float2(lo.y, Ts[off[k] + ((nN + 1) >> 1) * 32 * kRowBand].x);
+      acc[k] = mul2(t, f2(kn));
+      hi[k] = lo;
     }
   }
 #pragma unroll
-  for (int k = 0; k < kPx; ++k) W[k] = make_float2(cq[k], cp[k]);
-  // plane N+1: P only, weight c_N (= W.y after the last advance)
-  if (nN & 1) {  // N+1 even: .x of a pair not loaded yet
+  for (int n = kTop - 1; n >= 0; --n) {
+    if (n >= nN) continue;
+    const float kn = rc.k_coef[n];
 #pragma unroll
-    for (int k = 0; k < kPx; ++k)
-      qp[k].y = fmaf(W[k].y, Ts[off[k] + ((nN + 1) >> 1) * 32 * kRowBand].x, qp[k].y);
-  } else {  // N+1 odd: .y of the pair in cur (N = 0: pair 0)
-#pragma unroll
-    for (int k = 0; k < kPx; ++k) qp[k].y = fmaf(W[k].y, cur[k].y, qp[k].y);
+    for (int k = 0; k < kPx; ++k) {
+      const float2 lo = Ts[off[k] + (n >> 1) * 32 * kRowBand];
+      const float2 t = (n & 1) ? make_float2(lo.y, hi[k].x) : lo;
+      acc[k] = fma2(acc[k], f2(Hf[k]), mul2(t, f2(kn)));
+      hi[k] = lo;
+    }
   }
+  float2 qp[kPx];
+#pragma unroll
+  for (int k = 0; k < kPx; ++k) qp[k] = acc[k];
   // out = sr P/Q + t_c (bilateral.cpp:139-147); |Q| <= threshold -> input.
   // fp32 output: fp32 quotient (|error| <= sr |P/Q| 2^-22 < 1e-4 on [0, 255]);
   // fp64 output keeps the fp64 quotient.
