@@ -535,11 +535,9 @@ __global__ void __launch_bounds__(192, 2) k_rowpass2(const Tin* __restrict__ in_
     if (OTMA && tid == 0) bulk_wait_read_all();  // the previous strip's store has left O2
     __syncthreads();
     GPF_TICK(2);
-    // ---- 2. contraction: pixel p -> (row p & 15, col p >> 4); three pixels
-    // per thread with interleaved (independent) chains. Plane m adds
-    // (c_m, c_{m-1}) F_m to (Q, P); the weight pair advances componentwise,
-    // (c_{m+1}, c_m) = (c_m, c_{m-1}) * H (w_m, w_{m-1}): three packed
-    // instructions per plane. Plane 0 is Q-only, plane N+1 is P-only.
+    // ---- 2. contraction: pixel p -> (row p & 15, col p >> 4); up to three
+    // pixels per thread with interleaved (independent) Horner chains over the
+    // plane pairs (contract_px).
     const float2* Ts = T + (size_t)s * tile_elems;
     const Tin* Fs = OTMA ? reinterpret_cast<const Tin*>(F2 + s * kRowBand * 32) : F + s * kRowBand * 33;
 #ifdef GPF_DIAG_NO_CONTRACT
