@@ -10,7 +10,8 @@ import os
 import subprocess
 
 PKG_DIR = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(PKG_DIR, "libgpfilter_b200.so")
+# GPF_B200_LIB: an alternative build of the same library (A/B timing); there is no fallback
+LIB_PATH = os.environ.get("GPF_B200_LIB") or os.path.join(PKG_DIR, "libgpfilter_b200.so")
 
 # gpf_status values (include/gpfilter/gpfilter.h)
 GPF_OK = 0
