@@ -292,45 +292,48 @@ __device__ __forceinline__ float* stage_at(float* base_col, int j, int cm) {
   return base_col + (j >> 4) * 1024 + ((((j & 15) >> 1) ^ cm) << 2) + (j & 1) * 2;
 }
 
+constexpr int kColGroup = 4;  // pairs per column-pass CTA / carry warp
+
+// m2^pair0 for pair0 in {0, 4, 8, 12} (kColGroup = 4, pairs <= 16): straight-line
+// squarings and warp-uniform selects (shared by the producer and the carries)
+__device__ __forceinline__ float pow_group(float m2, int pair0) {
+  const float m4 = m2 * m2, m8 = m4 * m4;
+  float r = (pair0 & 4) ? m8 : 1.f;
+  if (pair0 & 8) r *= m8 * m8;
+  return r;
+}
+
 // Producer into a stage tile for the pair group starting at plane n0 = 2*pair0,
 // from the per-pixel seeds (es, m) K1 left in HBM (em tile [32 rows][32]):
-// item = (column, row pair), two items (four pixels) in flight per thread.
-// x_{n0} = es m^{n0} is reached through the planes x_4, x_8, ... (each in
-// range by the plane scaling), then the chain runs over the group's planes.
+// item = (column, row pair), four items (eight pixels) per thread in one
+// straight-line pass, so eight independent multiply chains are in flight.
+// x_{n0} = es m^{n0} by squarings, then the chain runs over the group's planes.
 __device__ __forceinline__ void produce_group(float* stage, const float2* emt, int pair0,
                                               int npairs) {
-  const int nthr = blockDim.x * blockDim.y;
+  constexpr int kIt = 4;  // 512 items = 4 x 128 threads (4-warp CTAs)
   const int tid = threadIdx.y * 32 + threadIdx.x;
-  for (int i0 = tid; i0 < 512; i0 += 2 * nthr) {
-    float x[4], m[4];
-    float4* dst[2];
+  float x[2 * kIt], m[2 * kIt];
+  float4* dst[kIt];
 #pragma unroll
-    for (int k = 0; k < 2; ++k) {
-      const int it = i0 + k * nthr;  // 512 = 2 * 2 * 128 items: always valid for 4-warp CTAs
-      const int c = it & 31, j = (it >> 5) * 2;  // rows j, j+1
-      const float2 ta = emt[j * 32 + c], tb = emt[(j + 1) * 32 + c];
-      x[2 * k] = ta.x;
-      m[2 * k] = ta.y;
-      x[2 * k + 1] = tb.x;
-      m[2 * k + 1] = tb.y;
-      dst[k] = reinterpret_cast<float4*>(stage_at(stage + c * 32, j, c & 7));
-    }
-    if (pair0 > 0) {
-      float m4[4];
+  for (int k = 0; k < kIt; ++k) {
+    const int it = tid + k * 128;
+    const int c = it & 31, j = (it >> 5) * 2;  // rows j, j+1
+    const float2 ta = emt[j * 32 + c], tb = emt[(j + 1) * 32 + c];
+    x[2 * k] = ta.x;
+    m[2 * k] = ta.y;
+    x[2 * k + 1] = tb.x;
+    m[2 * k + 1] = tb.y;
+    dst[k] = reinterpret_cast<float4*>(stage_at(stage + c * 32, j, c & 7));
+  }
+  if (pair0 > 0) {
 #pragma unroll
-      for (int e = 0; e < 4; ++e) {
-        m4[e] = m[e] * m[e];
-        m4[e] *= m4[e];
-      }
-      for (int n = 0; n < 2 * pair0; n += 4) {
+    for (int e = 0; e < 2 * kIt; ++e) x[e] *= pow_group(m[e] * m[e], pair0);
+  }
 #pragma unroll
-        for (int e = 0; e < 4; ++e) x[e] *= m4[e];
-      }
-    }
-#pragma unroll 2
-    for (int gg = 0; gg < npairs; ++gg) {
+  for (int gg = 0; gg < kColGroup; ++gg) {
+    if (gg < npairs) {
 #pragma unroll
-      for (int k = 0; k < 2; ++k) {
+      for (int k = 0; k < kIt; ++k) {
         const float a1 = x[2 * k] * m[2 * k], b1 = x[2 * k + 1] * m[2 * k + 1];
         dst[k][gg * 512] = make_float4(x[2 * k], a1, x[2 * k + 1], b1);
         x[2 * k] = a1 * m[2 * k];
@@ -342,7 +345,6 @@ __device__ __forceinline__ void produce_group(float* stage, const float2* emt, i
 
 // One CTA = 32 columns x kColGroup pairs (pair group blockIdx.z); several
 // CTAs share an SM so one's producer / H-dot phases overlap another's sweeps.
-constexpr int kColGroup = 4;
 
 #ifndef GPF_COL_STAGES
 #define GPF_COL_STAGES 1
@@ -578,14 +580,6 @@ __global__ void __launch_bounds__(256) k_seed(const Tin* __restrict__ in_all,
 // lane, 8 columns per warp -- or 4-/8-way row splits with shuffle reductions
 // are slower.)
 // ----------------------------------------------------------------------------
-// m2^pair0 for pair0 in {0, 4, 8, 12} (kColGroup = 4, pairs <= 16): straight-line
-// squarings and warp-uniform selects, so rows interleave freely
-__device__ __forceinline__ float pow_group(float m2, int pair0) {
-  const float m4 = m2 * m2, m8 = m4 * m4;
-  float r = (pair0 & 4) ? m8 : 1.f;
-  if (pair0 & 8) r *= m8 * m8;
-  return r;
-}
 
 __global__ void __launch_bounds__(32) k_col_carry_reg(const float2* __restrict__ EM_all,
                                                       float4* __restrict__ CA_all, int w, int h,
