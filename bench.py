@@ -477,7 +477,9 @@ def bench_c4(args):
     build_c4_frames(d_in[:n_loc], first, cfg)
     d_out = torch.empty_like(d_in)
     d_fb = torch.zeros(max(n_loc, 1), dtype=torch.int64, device="cuda")
-    plan = gpf.Plan(W, H, ss, sr, N, batch=max(1, min(n_loc, 8)))
+    # frames per launch: large batches keep every pass several waves deep (the
+    # single stream has no other work to fill a batch's tail)
+    plan = gpf.Plan(W, H, ss, sr, N, batch=max(1, min(n_loc, int(os.environ.get("GPF_C4_BATCH", "48")))))
     st = torch.cuda.current_stream()
 
     def step():
