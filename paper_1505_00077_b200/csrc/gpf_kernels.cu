@@ -434,7 +434,57 @@ __global__ void __launch_bounds__(32 * kColGroup, GPF_COL_CTAS) k_colpass_tma(
       tma_load_3d(emt, &emmap, 2 * x0, y0 + kTile, f, &em_full);
     }
     float* mcol = stage + col_off;
-    if (active && x < w) {
+    if (active && x < w && rows == kTile) {
+      // full chunk: both directions in one branch-free loop (two independent
+      // recurrences per step), two rows per smem access. Step t runs the
+      // anticausal sections at rows 31-t, 30-t and the causal ones at rows
+      // t, t+1. First-half outputs park in registers (pa: anticausal rows
+      // 16..31, pc: causal rows 0..15) and the inputs stay in the stage, so
+      // the second half re-reads its inputs there and writes each final
+      // output once, in place.
+      if (cy == 0) {
+        const float4 v0 = *reinterpret_cast<const float4*>(stage_at(mcol, 0, cm));
+        ps_set_gain_sweep(cs, make_float2(v0.x, v0.y), fc);
+      }
+      float2 pa[kTile / 2], pc[kTile / 2];
+#pragma unroll
+      for (int t = 0; t < kTile / 2; t += 2) {
+        const float4 va = *reinterpret_cast<const float4*>(stage_at(mcol, 30 - t, cm));
+        const float4 vc = *reinterpret_cast<const float4*>(stage_at(mcol, t, cm));
+        pa[15 - t] = ps_emit(as, fc.br2, fc.sbi2);  // row 31-t
+        ps_advance(as, make_float2(va.z, va.w), fc);
+        ps_advance(cs, make_float2(vc.x, vc.y), fc);
+        pc[t] = ps_emit(cs, fc.ar2, fc.sai2);  // row t
+        pa[14 - t] = ps_emit(as, fc.br2, fc.sbi2);  // row 30-t
+        ps_advance(as, make_float2(va.x, va.y), fc);
+        ps_advance(cs, make_float2(vc.z, vc.w), fc);
+        pc[t + 1] = ps_emit(cs, fc.ar2, fc.sai2);  // row t+1
+      }
+      // second half: anticausal rows 15-u, 14-u; causal rows 16+u, 17+u; the
+      // next step's inputs are read before this step's outputs are stored
+      float4 va = *reinterpret_cast<const float4*>(stage_at(mcol, 14, cm));
+      float4 vc = *reinterpret_cast<const float4*>(stage_at(mcol, 16, cm));
+#pragma unroll
+      for (int u = 0; u < kTile / 2; u += 2) {
+        float4 na = va, nc = vc;
+        if (u + 2 < kTile / 2) {
+          na = *reinterpret_cast<const float4*>(stage_at(mcol, 12 - u, cm));
+          nc = *reinterpret_cast<const float4*>(stage_at(mcol, 18 + u, cm));
+        }
+        const float2 yb = ps_emit_acc(as, fc.br2, fc.sbi2, pc[15 - u]);
+        ps_advance(as, make_float2(va.z, va.w), fc);
+        ps_advance(cs, make_float2(vc.x, vc.y), fc);
+        const float2 yc0 = ps_emit_acc(cs, fc.ar2, fc.sai2, pa[u]);
+        const float2 ya = ps_emit_acc(as, fc.br2, fc.sbi2, pc[14 - u]);
+        ps_advance(as, make_float2(va.x, va.y), fc);
+        ps_advance(cs, make_float2(vc.z, vc.w), fc);
+        const float2 yc1 = ps_emit_acc(cs, fc.ar2, fc.sai2, pa[u + 1]);
+        *reinterpret_cast<float4*>(stage_at(mcol, 14 - u, cm)) = make_float4(ya.x, ya.y, yb.x, yb.y);
+        *reinterpret_cast<float4*>(stage_at(mcol, 16 + u, cm)) = make_float4(yc0.x, yc0.y, yc1.x, yc1.y);
+        va = na;
+        vc = nc;
+      }
+    } else if (active && x < w) {
       float2 xr[kTile];
 #pragma unroll
       for (int j = 0; j < kTile; j += 2) {
@@ -443,42 +493,7 @@ __global__ void __launch_bounds__(32 * kColGroup, GPF_COL_CTAS) k_colpass_tma(
         xr[j + 1] = make_float2(v.z, v.w);
       }
       if (cy == 0) ps_set_gain_sweep(cs, xr[0], fc);
-      if (rows == kTile) {
-        // full chunk: both directions in one branch-free loop (two independent
-        // recurrences per step), two rows per smem access. Step t runs the
-        // anticausal sections at rows 31-t, 30-t and the causal ones at rows
-        // t, t+1; first-half outputs park in the stage, second-half outputs
-        // add the other direction's parked value.
-#pragma unroll
-        for (int t = 0; t < kTile; t += 2) {
-          float4* pa = reinterpret_cast<float4*>(stage_at(mcol, 30 - t, cm));
-          float4* pc = reinterpret_cast<float4*>(stage_at(mcol, t, cm));
-          if (t < kTile / 2) {
-            const float2 yb = ps_emit(as, fc.br2, fc.sbi2);
-            ps_advance(as, xr[31 - t], fc);
-            ps_advance(cs, xr[t], fc);
-            const float2 yc0 = ps_emit(cs, fc.ar2, fc.sai2);
-            const float2 ya = ps_emit(as, fc.br2, fc.sbi2);
-            ps_advance(as, xr[30 - t], fc);
-            ps_advance(cs, xr[t + 1], fc);
-            const float2 yc1 = ps_emit(cs, fc.ar2, fc.sai2);
-            *pa = make_float4(ya.x, ya.y, yb.x, yb.y);
-            *pc = make_float4(yc0.x, yc0.y, yc1.x, yc1.y);
-          } else {  // the other direction's parked values seed the emits
-            const float4 qa = *pa, qc = *pc;
-            const float2 yb = ps_emit_acc(as, fc.br2, fc.sbi2, make_float2(qa.z, qa.w));
-            ps_advance(as, xr[31 - t], fc);
-            ps_advance(cs, xr[t], fc);
-            const float2 yc0 = ps_emit_acc(cs, fc.ar2, fc.sai2, make_float2(qc.x, qc.y));
-            const float2 ya = ps_emit_acc(as, fc.br2, fc.sbi2, make_float2(qa.x, qa.y));
-            ps_advance(as, xr[30 - t], fc);
-            ps_advance(cs, xr[t + 1], fc);
-            const float2 yc1 = ps_emit_acc(cs, fc.ar2, fc.sai2, make_float2(qc.z, qc.w));
-            *pa = make_float4(ya.x, ya.y, yb.x, yb.y);
-            *pc = make_float4(yc0.x, yc0.y, yc1.x, yc1.y);
-          }
-        }
-      } else {  // last, partial chunk: predicated (keeps xr in registers)
+      {
 #pragma unroll
         for (int j = kTile - 1; j >= 0; --j) {
           if (j < rows) {
