@@ -106,6 +106,7 @@ struct Plan {
   float2* EM = nullptr;     // [batch][h][w_pad] per-pixel plane seeds (E 2^s0, H 2^-k) from K1
   int w_pad = 0;            // EM row pitch in pixels (even: TMA strides are 16-B multiples)
   alignas(64) CUtensorMap vmap;    // TMA map of V: fp32 [batch][pairs][w][2*h_pad] (row-pass loads)
+  alignas(64) CUtensorMap vmap8;   // same, 8-row x 33-column boxes (8-row-band row pass)
   alignas(64) CUtensorMap vstore;  // TMA map of V for the column pass's staged chunk stores
   alignas(64) CUtensorMap emmap;   // TMA map of EM: 32x32-pixel tiles for the column pass
   double* scalars = nullptr;   // [batch][2]  t_c

@@ -897,10 +897,10 @@ static PFN_cuTensorMapEncodeTiled_v12000 tensor_map_encoder() {
 
 // fp32 frames {w, h, count}, box {32 columns, 16 rows, 1}, 128B-swizzled: the
 // row pass's output tile and f tile; requires w % 4 == 0 and a 16-B aligned base.
-static void encode_out_map(CUtensorMap* m, void* d_out, int w, int h, int count) {
+static void encode_out_map(CUtensorMap* m, void* d_out, int w, int h, int count, int band_rows) {
   const cuuint64_t dims[3] = {(cuuint64_t)w, (cuuint64_t)h, (cuuint64_t)count};
   const cuuint64_t strides[2] = {(cuuint64_t)4 * w, (cuuint64_t)4 * w * h};
-  const cuuint32_t box[3] = {32, (cuuint32_t)kRowBand, 1};
+  const cuuint32_t box[3] = {32, (cuuint32_t)band_rows, 1};
   const cuuint32_t estr[3] = {1, 1, 1};
   const CUresult r = tensor_map_encoder()(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, d_out, dims, strides,
                                           box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
@@ -968,6 +968,15 @@ void plan_init(Plan& plan, const Params& p, int device, int batch) {
     plan_free(plan);
     throw Error{9, "cuTensorMapEncodeTiled failed (" + std::to_string((int)r) + ")"};
   }
+  // 8-row-band row pass: box {16 (= 8 rows x 2 planes), 33 columns, 1 band, pairs, 1}
+  const cuuint32_t box8[5] = {16, 33, 1, (cuuint32_t)pairs, 1};
+  const CUresult r8 = encode(&plan.vmap8, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 5, plan.V, dims, strides, box8,
+                             estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                             CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r8 != CUDA_SUCCESS) {
+    plan_free(plan);
+    throw Error{9, "cuTensorMapEncodeTiled (8-row V) failed (" + std::to_string((int)r8) + ")"};
+  }
   // column-pass chunk store: box {32, 32 columns, 2 bands, kColGroup pairs, 1}
   // = one 32x32 chunk of a pair group; smem [pair][band][column][128 B],
   // 128B-swizzled.
@@ -1010,6 +1019,10 @@ void plan_free(Plan& plan) {
 
 // MAXT = the CTA size bound the kernels are compiled for (32 x pairs threads):
 // 384 -> up to 168 registers/thread (N <= 22), 512 -> 128 (N <= 30), 1024 -> 64.
+#ifndef GPF_ROW_BAND
+#define GPF_ROW_BAND 16
+#endif
+
 template <int MAXT, typename Tin, typename Tout>
 static void launch_passes(Plan& plan, const Tin* d_in, Tout* d_out, int count,
                           unsigned long long* d_fb, cudaStream_t st) {
@@ -1063,7 +1076,8 @@ static void launch_passes(Plan& plan, const Tin* d_in, Tout* d_out, int count,
                                                    plan.fc, plan.tc);
   stage_mark(plan, kStageRowPass, st);
   if (pairs <= 12) {
-    const int r2sm = (int)rowpass2_smem_bytes<Tin, Tout>(pairs);
+    constexpr int RB = GPF_ROW_BAND;  // rows per row-pass CTA (16 or 8)
+    const int r2sm = (int)rowpass2_smem_bytes<Tin, Tout, RB>(pairs);
     // fp32 output with 16-B rows: TMA output store (tensor map of this call's d_out)
     const bool otma = sizeof(Tout) == 4 && sizeof(Tin) == 4 && (w % 4) == 0 &&
                       (reinterpret_cast<uintptr_t>(d_out) % 16) == 0 &&
@@ -1072,20 +1086,20 @@ static void launch_passes(Plan& plan, const Tin* d_in, Tout* d_out, int count,
     std::memset(&omap, 0, sizeof(omap));
     std::memset(&imap, 0, sizeof(imap));
     if (otma) {
-      encode_out_map(&omap, d_out, w, h, count);
-      encode_out_map(&imap, const_cast<Tin*>(d_in), w, h, count);  // same box shape for the f tiles
+      encode_out_map(&omap, d_out, w, h, count, RB);
+      encode_out_map(&imap, const_cast<Tin*>(d_in), w, h, count, RB);  // same box shape for the f tiles
     }
     // the default degree (N = 20, reference RangeParams) has a fully static build
     const bool n20 = plan.rc.degree == 20;
-    auto k = n20 ? k_rowpass2<Tin, Tout, 20, false> : k_rowpass2<Tin, Tout, 0, false>;
+    auto k = n20 ? k_rowpass2<Tin, Tout, 20, false, RB> : k_rowpass2<Tin, Tout, 0, false, RB>;
     if constexpr (sizeof(Tout) == 4) {
-      if (otma) k = n20 ? k_rowpass2<Tin, Tout, 20, true> : k_rowpass2<Tin, Tout, 0, true>;
+      if (otma) k = n20 ? k_rowpass2<Tin, Tout, 20, true, RB> : k_rowpass2<Tin, Tout, 0, true, RB>;
     }
     check(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, r2sm),
           "cudaFuncSetAttribute");
-    k<<<dim3((h + kRowBand - 1) / kRowBand, count), dim3(32, (pairs + 1) / 2), r2sm, st>>>(
-        d_in, plan.scalars, plan.CH, d_out, d_fb, w, h, plan.nx, pairs, plan.fc, plan.rc, plan.vmap,
-        omap, imap);
+    k<<<dim3((h + RB - 1) / RB, count), dim3(32, (pairs * RB + 31) / 32), r2sm, st>>>(
+        d_in, plan.scalars, plan.CH, d_out, d_fb, w, h, plan.nx, pairs, plan.fc, plan.rc,
+        RB == 8 ? plan.vmap8 : plan.vmap, omap, imap);
   } else {
     k_rowpass<RMAXT, Tin, Tout><<<dim3((h + kRowBand - 1) / kRowBand, count),
                                   dim3(32, (pairs + 1) / 2 + kAux), rsm, st>>>(

@@ -263,13 +263,20 @@ namespace gpfb {
 constexpr int kRow2Slots = 2;
 constexpr int kRow2MaxN = 22;  // pairs <= 12
 
-template <typename Tin, typename Tout>
+// Band height RB: 16 rows (half-warp per pair, 2 CTAs/SM) or 8 rows (quarter-warp
+// per pair, 4 CTAs/SM). The 8-row V box is 33 columns wide, so consecutive pairs
+// sit 64 B apart in the bank space and a warp's four 64-B pair segments of one
+// column are conflict-free (the 33rd column is loaded but unused).
+template <int RB>
+__host__ __device__ constexpr int row2_pair_cols() { return RB == 8 ? 33 : 32; }
+
+template <typename Tin, typename Tout, int RB = kRowBand>
 __host__ __device__ constexpr size_t rowpass2_smem_bytes(int pairs) {
   // V ring | f tiles | padded output tile | mbarriers | 1024-aligned swizzled
   // output tile | swizzled f tiles (TMA path)
-  return sizeof(float2) * (size_t)pairs * 32 * kRowBand * kRow2Slots +
-         sizeof(Tin) * kRowBand * 33 * kRow2Slots + sizeof(Tout) * kRowBand * 33 +
-         kRow2Slots * sizeof(uint64_t) + 16 + 1024 + sizeof(float) * kRowBand * 32 * (1 + kRow2Slots);
+  return (sizeof(float2) * (size_t)pairs * row2_pair_cols<RB>() * RB + 128) * kRow2Slots +
+         sizeof(Tin) * RB * 33 * kRow2Slots + sizeof(Tout) * RB * 33 +
+         kRow2Slots * sizeof(uint64_t) + 16 + 1024 + sizeof(float) * RB * 32 * (1 + kRow2Slots);
 }
 
 // Contraction of kPx pixels per thread (pixel p -> row p & 15, column p >> 4),
@@ -285,7 +292,7 @@ __device__ __forceinline__ int f_at(int r, int c) {
 
 // OSW: write into the 128B-swizzled [16][32] fp32 tile of the TMA output store
 // (element (r, c) at r*32 + (((c/4) ^ (r%8)) * 4) + c%4) instead of the padded O.
-template <int kPx, int NFIX, bool OSW, typename Tin, typename Tout>
+template <int kPx, int NFIX, bool OSW, int RB, typename Tin, typename Tout>
 __device__ __forceinline__ unsigned contract_px(const float2* Ts, const Tin* Fs, Tout* O, int p0,
                                                 int nthr, int rows, int cols, const RangeConsts& rc,
                                                 double t_c, float sr_f, float tc_hi, float tc_lo) {
@@ -295,10 +302,10 @@ __device__ __forceinline__ unsigned contract_px(const float2* Ts, const Tin* Fs,
   int off[kPx];
 #pragma unroll
   for (int k = 0; k < kPx; ++k) {
-    const int p = min(p0 + k * nthr, kRowBand * 32 - 1);
-    off[k] = (p >> 4) * kRowBand + (p & (kRowBand - 1));  // [col][row]
+    const int p = min(p0 + k * nthr, RB * 32 - 1);
+    off[k] = p;  // [col][row]: column p / RB, row p % RB
     // H as the column pass formed it (pixel_terms): fp64 difference, fp32 H
-    Hf[k] = static_cast<float>((static_cast<double>(Fs[f_at<OSW>(p & 15, p >> 4)]) - t_c) * rc.inv_sr);
+    Hf[k] = static_cast<float>((static_cast<double>(Fs[f_at<OSW>(p % RB, p / RB)]) - t_c) * rc.inv_sr);
   }
   // Q = sum_{n<=N} c_n F_n and P = sum_{n<=N} c_n F_{n+1} with c_n = H^n k_n
   // share the coefficient polynomial: Horner in H over n = N..0 on the pair
@@ -310,14 +317,15 @@ __device__ __forceinline__ unsigned contract_px(const float2* Ts, const Tin* Fs,
   // Unrolled to N (static build) or to kRow2MaxN with a guard, so smem
   // offsets and the k_n are immediates.
   constexpr int kTop = NFIX > 0 ? NFIX : kRow2MaxN;
+  constexpr int kPS = row2_pair_cols<RB>() * RB;  // float2 per pair in a slot
   float2 acc[kPx], hi[kPx];
   {  // n = N
     const float kn = rc.k_coef[nN];
 #pragma unroll
     for (int k = 0; k < kPx; ++k) {
-      const float2 lo = Ts[off[k] + (nN >> 1) * 32 * kRowBand];
+      const float2 lo = Ts[off[k] + (nN >> 1) * kPS];
       float2 t = lo;
-      if (nN & 1) t = make_float2(lo.y, Ts[off[k] + ((nN + 1) >> 1) * 32 * kRowBand].x);
+      if (nN & 1) t = make_float2(lo.y, Ts[off[k] + ((nN + 1) >> 1) * kPS].x);
       acc[k] = mul2(t, f2(kn));
       hi[k] = lo;
     }
@@ -328,7 +336,7 @@ __device__ __forceinline__ unsigned contract_px(const float2* Ts, const Tin* Fs,
     const float kn = rc.k_coef[n];
 #pragma unroll
     for (int k = 0; k < kPx; ++k) {
-      const float2 lo = Ts[off[k] + (n >> 1) * 32 * kRowBand];
+      const float2 lo = Ts[off[k] + (n >> 1) * kPS];
       const float2 t = (n & 1) ? make_float2(lo.y, hi[k].x) : lo;
       acc[k] = fma2(acc[k], f2(Hf[k]), mul2(t, f2(kn)));
       hi[k] = lo;
@@ -343,8 +351,8 @@ __device__ __forceinline__ unsigned contract_px(const float2* Ts, const Tin* Fs,
 #pragma unroll
   for (int k = 0; k < kPx; ++k) {
     const int p = p0 + k * nthr;
-    const int pr = p & (kRowBand - 1), pc = p >> 4;
-    if (p < kRowBand * 32 && (OSW || (pr < rows && pc < cols))) {  // the TMA store clips
+    const int pr = p % RB, pc = p / RB;
+    if (p < RB * 32 && (OSW || (pr < rows && pc < cols))) {  // the TMA store clips
       Tout o;
       if (!(fabsf(qp[k].x) > rc.q_thresh)) {
         o = static_cast<Tout>(Fs[f_at<OSW>(pr, pc)]);
@@ -371,8 +379,8 @@ __device__ __forceinline__ unsigned contract_px(const float2* Ts, const Tin* Fs,
 // [16][32] tile and one thread stores it with a TMA tensor store (`omap` =
 // the caller's output), which drains under the next strip's sweeps; else the
 // warps write the tile out row by row.
-template <typename Tin, typename Tout, int NFIX, bool OTMA>
-__global__ void __launch_bounds__(192, 2) k_rowpass2(const Tin* __restrict__ in_all,
+template <typename Tin, typename Tout, int NFIX, bool OTMA, int RB = kRowBand>
+__global__ void __launch_bounds__(RB == 8 ? 96 : 192, RB == 8 ? 4 : 2) k_rowpass2(const Tin* __restrict__ in_all,
                                                       const double* __restrict__ scalars,
                                                       const float4* __restrict__ CH_all,
                                                       Tout* __restrict__ out_all,
@@ -385,14 +393,16 @@ __global__ void __launch_bounds__(192, 2) k_rowpass2(const Tin* __restrict__ in_
   extern __shared__ float4 smem4[];
   const int f = blockIdx.y, lane = threadIdx.x, warp = threadIdx.y;
   const int tid = warp * 32 + lane, nthr = blockDim.x * blockDim.y;
-  const int y0 = blockIdx.x * kRowBand;
-  const int rows = min(kRowBand, h - y0);
-  const size_t tile_elems = (size_t)pairs * 32 * kRowBand;  // float2 per slot: [g][c][16 rows]
+  constexpr int PC = row2_pair_cols<RB>();  // columns per pair in a slot
+  const int y0 = blockIdx.x * RB;
+  const int rows = min(RB, h - y0);
+  const size_t tile_elems = (size_t)pairs * PC * RB;  // float2 per V box: [g][PC columns][RB rows]
+  const size_t slot_elems = (tile_elems + 15) & ~size_t(15);  // slots 128-B aligned (TMA)
   float2* T = reinterpret_cast<float2*>(smem4);
-  Tin* F = reinterpret_cast<Tin*>(T + kRow2Slots * tile_elems);       // [slot][16 rows][33]
-  Tout* O = reinterpret_cast<Tout*>(F + kRow2Slots * kRowBand * 33);  // [16 rows][33]
+  Tin* F = reinterpret_cast<Tin*>(T + kRow2Slots * slot_elems);  // [slot][RB rows][33]
+  Tout* O = reinterpret_cast<Tout*>(F + kRow2Slots * RB * 33);   // [RB rows][33]
   uint64_t* full = reinterpret_cast<uint64_t*>(
-      (reinterpret_cast<uintptr_t>(O + kRowBand * 33) + 15) & ~uintptr_t(15));
+      (reinterpret_cast<uintptr_t>(O + RB * 33) + 15) & ~uintptr_t(15));
   // swizzled output tile, 1024-aligned in the shared window (offset from the base)
   float* O2;
   {
@@ -400,7 +410,7 @@ __global__ void __launch_bounds__(192, 2) k_rowpass2(const Tin* __restrict__ in_
     const uint32_t a = smem_u32(full + kRow2Slots);
     O2 = reinterpret_cast<float*>(base + (((a + 1023u) & ~1023u) - smem_u32(base)));
   }
-  float* F2 = O2 + kRowBand * 32;  // [slot][16][32] swizzled f tiles (TMA path)
+  float* F2 = O2 + RB * 32;  // [slot][RB][32] swizzled f tiles (TMA path)
   const Tin* in = in_all + (size_t)f * w * h;
   Tout* out = out_all + (size_t)f * w * h;
   const double t_c = scalars[2 * f];
@@ -413,17 +423,18 @@ __global__ void __launch_bounds__(192, 2) k_rowpass2(const Tin* __restrict__ in_
     if (tid == 0) {
       fence_proxy_async();
       mbar_arrive_expect_tx(&full[s], (uint32_t)(tile_elems * sizeof(float2) +
-                                                 (OTMA ? sizeof(float) * kRowBand * 32 : 0)));
+                                                 (OTMA ? sizeof(float) * RB * 32 : 0)));
+      // V is band-major in 16-row bands: an 8-row band starts 0 or 16 floats into its band
 #ifdef GPF_DIAG_L2V  // diagnostic: V boxes from a small L2-resident region
-      tma_load_5d(T + (size_t)s * tile_elems, &vmap, 0, (b & 3) * 32, blockIdx.x & 1, 0, f, &full[s]);
+      tma_load_5d(T + (size_t)s * slot_elems, &vmap, 0, (b & 3) * 32, blockIdx.x & 1, 0, f, &full[s]);
 #else
-      tma_load_5d(T + (size_t)s * tile_elems, &vmap, 0, xs, y0 / kRowBand, 0, f, &full[s]);
+      tma_load_5d(T + (size_t)s * slot_elems, &vmap, (y0 & 15) * 2, xs, y0 >> 4, 0, f, &full[s]);
 #endif
-      if constexpr (OTMA) tma_load_3d(F2 + s * kRowBand * 32, &imap, xs, y0, f, &full[s]);
+      if constexpr (OTMA) tma_load_3d(F2 + s * RB * 32, &imap, xs, y0, f, &full[s]);
     }
     if constexpr (!OTMA) {
-      Tin* Fs = F + s * kRowBand * 33;
-      for (int p = tid; p < kRowBand * 32; p += nthr) {
+      Tin* Fs = F + s * RB * 33;
+      for (int p = tid; p < RB * 32; p += nthr) {
         const int r = p >> 5, c = p & 31;
         const bool ok = r < rows && c < ncol;
         cp_async_zfill<sizeof(Tin)>(Fs + r * 33 + c, ok ? in + (size_t)(y0 + r) * w + xs + c : in, ok);
@@ -439,9 +450,9 @@ __global__ void __launch_bounds__(192, 2) k_rowpass2(const Tin* __restrict__ in_
   __syncthreads();
   for (int s = 0; s < kRow2Slots && s < nx; ++s) load_strip(s, s);
 
-  // sweep role: half-warp per pair, lane = row
-  const int r = lane & (kRowBand - 1);
-  const int g = 2 * warp + (lane >> 4);
+  // sweep role: RB lanes per pair (half- or quarter-warp), lane = row
+  const int r = lane & (RB - 1);
+  const int g = (32 / RB) * warp + lane / RB;
   const bool live = g < pairs;
   const int gl = live ? g : pairs - 1;
   const int yr = min(y0 + r, h - 1);
@@ -469,8 +480,8 @@ __global__ void __launch_bounds__(192, 2) k_rowpass2(const Tin* __restrict__ in_
       c0 = __ldg(CH + (size_t)(b + 1) * ch_stride);
       c1 = __ldg(CH + (size_t)(b + 1) * ch_stride + 1);
     }
-    // ---- 1. sweeps (element [g][c][r] of slot s at tl[c * kRowBand])
-    float2* tl = T + (size_t)s * tile_elems + (size_t)gl * 32 * kRowBand + r;
+    // ---- 1. sweeps (element [g][c][r] of slot s at tl[c * RB])
+    float2* tl = T + (size_t)s * slot_elems + (size_t)gl * PC * RB + r;
     GPF_TICK(5);
     mbar_wait(&full[s], (b >> 1) & 1);
     GPF_TICK(0);
@@ -491,20 +502,20 @@ __global__ void __launch_bounds__(192, 2) k_rowpass2(const Tin* __restrict__ in_
         const int ca = 31 - t, cc = t;
         if (t < 16) {
           const float2 ya = ps_emit(as, fc.br2, fc.sbi2);
-          const float2 xa = tl[ca * kRowBand], xc = tl[cc * kRowBand];
+          const float2 xa = tl[ca * RB], xc = tl[cc * RB];
           ps_advance(as, xa, fc);
           ps_advance(cs, xc, fc);
           ya_hi[ca - 16] = ya;
           yc_lo[cc] = ps_emit(cs, fc.ar2, fc.sai2);
         } else {  // the other direction's parked value seeds the emit
           const float2 ya = ps_emit_acc(as, fc.br2, fc.sbi2, yc_lo[ca]);
-          const float2 xa = tl[ca * kRowBand], xc = tl[cc * kRowBand];
+          const float2 xa = tl[ca * RB], xc = tl[cc * RB];
           ps_advance(as, xa, fc);
           ps_advance(cs, xc, fc);
           const float2 yc = ps_emit_acc(cs, fc.ar2, fc.sai2, ya_hi[cc - 16]);
           if (live) {
-            tl[ca * kRowBand] = ya;
-            tl[cc * kRowBand] = yc;
+            tl[ca * RB] = ya;
+            tl[cc * RB] = yc;
           }
         }
       }
@@ -514,15 +525,15 @@ __global__ void __launch_bounds__(192, 2) k_rowpass2(const Tin* __restrict__ in_
       for (int c = 31; c >= 0; --c) {
         if (c < cols) {
           ybuf[c] = ps_emit(as, fc.br2, fc.sbi2);
-          ps_advance(as, tl[c * kRowBand], fc);
+          ps_advance(as, tl[c * RB], fc);
         }
       }
 #pragma unroll
       for (int c = 0; c < 32; ++c) {
         if (c < cols) {
-          ps_advance(cs, tl[c * kRowBand], fc);
+          ps_advance(cs, tl[c * RB], fc);
           const float2 o = add2(ps_emit(cs, fc.ar2, fc.sai2), ybuf[c]);
-          if (live) tl[c * kRowBand] = o;
+          if (live) tl[c * RB] = o;
         }
       }
     }
@@ -538,22 +549,22 @@ __global__ void __launch_bounds__(192, 2) k_rowpass2(const Tin* __restrict__ in_
     // ---- 2. contraction: pixel p -> (row p & 15, col p >> 4); up to three
     // pixels per thread with interleaved (independent) Horner chains over the
     // plane pairs (contract_px).
-    const float2* Ts = T + (size_t)s * tile_elems;
-    const Tin* Fs = OTMA ? reinterpret_cast<const Tin*>(F2 + s * kRowBand * 32) : F + s * kRowBand * 33;
+    const float2* Ts = T + (size_t)s * slot_elems;
+    const Tin* Fs = OTMA ? reinterpret_cast<const Tin*>(F2 + s * RB * 32) : F + s * RB * 33;
 #ifdef GPF_DIAG_NO_CONTRACT
     for (int p0 = tid; p0 < 0; p0 += nthr * 3) {
 #else
-    for (int p0 = tid; p0 < kRowBand * 32; p0 += nthr * 3) {
+    for (int p0 = tid; p0 < RB * 32; p0 += nthr * 3) {
 #endif
       // pixels per thread for this warp (warp-uniform: no work on pixels past the strip)
       const int wb = p0 - lane;
       Tout* Od = OTMA ? reinterpret_cast<Tout*>(O2) : O;
-      if (wb + 2 * nthr + 31 < kRowBand * 32)
-        my_fb += contract_px<3, NFIX, OTMA>(Ts, Fs, Od, p0, nthr, rows, cols, rc, t_c, sr_f, tc_hi, tc_lo);
-      else if (wb + nthr < kRowBand * 32)
-        my_fb += contract_px<2, NFIX, OTMA>(Ts, Fs, Od, p0, nthr, rows, cols, rc, t_c, sr_f, tc_hi, tc_lo);
+      if (wb + 2 * nthr + 31 < RB * 32)
+        my_fb += contract_px<3, NFIX, OTMA, RB>(Ts, Fs, Od, p0, nthr, rows, cols, rc, t_c, sr_f, tc_hi, tc_lo);
+      else if (wb + nthr < RB * 32)
+        my_fb += contract_px<2, NFIX, OTMA, RB>(Ts, Fs, Od, p0, nthr, rows, cols, rc, t_c, sr_f, tc_hi, tc_lo);
       else
-        my_fb += contract_px<1, NFIX, OTMA>(Ts, Fs, Od, p0, nthr, rows, cols, rc, t_c, sr_f, tc_hi, tc_lo);
+        my_fb += contract_px<1, NFIX, OTMA, RB>(Ts, Fs, Od, p0, nthr, rows, cols, rc, t_c, sr_f, tc_hi, tc_lo);
     }
     GPF_TICK(3);
     if constexpr (OTMA) {
@@ -567,7 +578,7 @@ __global__ void __launch_bounds__(192, 2) k_rowpass2(const Tin* __restrict__ in_
     } else {
       __syncthreads();
       // ---- 3. write-out (row segments of 32, coalesced)
-      for (int p = tid; p < kRowBand * 32; p += nthr) {
+      for (int p = tid; p < RB * 32; p += nthr) {
         const int pr = p >> 5, pc = p & 31;
         if (pr < rows && pc < cols) out[(size_t)(y0 + pr) * w + xs + pc] = O[pr * 33 + pc];
       }
