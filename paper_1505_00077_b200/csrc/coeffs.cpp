@@ -2,6 +2,7 @@
 #include <algorithm>
 #include <cmath>
 #include <complex>
+#include <string>
 
 #include "gpf_internal.h"
 
@@ -95,17 +96,32 @@ FilterConsts make_filter_consts(double s) {
     // anticausal: z * sum_m na_m z^m / D(z), expanded as sum_k B_k z/(1 - p_k z)
     const cd B = 2.0 * poly3(k.na, q) / den;
     const cd g = 1.0 / (1.0 - pk);
-    fc.pr2[sec] = dup(pk.real());
-    fc.ar2[sec] = dup(A.real());
-    fc.br2[sec] = dup(B.real());
+    const double pr = pk.real(), si = pk.imag();
+    fc.pr2[sec] = dup(pr);
     fc.gr2[sec] = dup(g.real());
     fc.gi2[sec] = dup(g.imag());
-    const double si = pk.imag();
-    fc.nps2[sec] = dup(-si * si);
-    fc.sai2[sec] = dup(-A.imag() * si);
-    fc.sbi2[sec] = dup(-B.imag() * si);
     fc.gs2[sec] = dup(g.imag() / si);
     fc.ips2[sec] = dup(1.0 / si);
+    // sweep bases (see FilterConsts): tau = Im R / Re R, clamped to |tau Im p| <= 1
+    auto basis = [&](const cd& R, float2* m11, float2* m12, float2* m22, double& tau) {
+      tau = R.imag() / R.real();
+      if (!(std::fabs(tau * si) <= 1.0)) tau = std::copysign(1.0 / si, tau);
+      m11[sec] = dup(pr - tau * si);
+      m22[sec] = dup(pr + tau * si);
+      m12[sec] = dup(-si * si * (1.0 + tau * tau));
+    };
+    double tc = 0.0, ta = 0.0;
+    basis(A, fc.cm11, fc.cm12, fc.cm22, tc);
+    basis(B, fc.am11, fc.am12, fc.am22, ta);
+    // Re(R w) = Re R u1 + Im p (Re R tau - Im R) u2
+    fc.ce[sec] = dup(A.real());
+    fc.ae[sec] = dup(B.real());
+    const double cv = si * (A.real() * tc - A.imag()), av = si * (B.real() * ta - B.imag());
+    if (std::fabs(cv) > 1e-12 * std::abs(A) || (sec == 0 && std::fabs(av) > 1e-12 * std::abs(B)))
+      throw Error{9, "sweep basis: unsupported residue (sigma_s " + std::to_string(s) + ")"};
+    if (sec == 1) fc.aev = dup(av);
+    fc.ntau_a[sec] = dup(-ta);
+    fc.cgu1[sec] = dup(g.real() - tc * g.imag());
   }
   return fc;
 }

@@ -71,46 +71,58 @@ __device__ __forceinline__ void ps_set_gain(PairState& s, float2 x, const Filter
   }
 }
 
-// Sweep-basis state (FilterConsts: wi holds v^ = Im(w) / Im(p)):
-//   w <- p w + x  as  Re w' = Re p Re w - (Im p)^2 v^ + x,  v^' = Re p v^ + Re w
+// Sweep-basis state (FilterConsts): wr holds u1, wi holds u2 per section.
+//   u2' = m22 u2 + u1,  u1' = m11 u1 + m12 u2 + x
 // three FFMA2 per section for both planes.
-__device__ __forceinline__ void ps_advance(PairState& s, float2 x, const FilterConsts& fc) {
+__device__ __forceinline__ void ps_adv(PairState& s, float2 x, const float2* m11, const float2* m12,
+                                       const float2* m22) {
 #pragma unroll
   for (int k = 0; k < 2; ++k) {
-    const float2 nr = fma2(fc.pr2[k], s.wr[k], fma2(fc.nps2[k], s.wi[k], x));
-    const float2 ni = fma2(fc.pr2[k], s.wi[k], s.wr[k]);
-    s.wr[k] = nr;
-    s.wi[k] = ni;
+    const float2 n2 = fma2(m22[k], s.wi[k], s.wr[k]);
+    const float2 n1 = fma2(m11[k], s.wr[k], fma2(m12[k], s.wi[k], x));
+    s.wr[k] = n1;
+    s.wi[k] = n2;
   }
 }
+__device__ __forceinline__ void ps_advance_c(PairState& s, float2 x, const FilterConsts& fc) {
+  ps_adv(s, x, fc.cm11, fc.cm12, fc.cm22);
+}
+__device__ __forceinline__ void ps_advance_a(PairState& s, float2 x, const FilterConsts& fc) {
+  ps_adv(s, x, fc.am11, fc.am12, fc.am22);
+}
 
-// replicate steady state in the sweep basis: w = x / (1 - p)
+// replicate steady state of the causal sweep: w = x / (1 - p) in its basis
 __device__ __forceinline__ void ps_set_gain_sweep(PairState& s, float2 x, const FilterConsts& fc) {
 #pragma unroll
   for (int k = 0; k < 2; ++k) {
-    s.wr[k] = mul2(x, fc.gr2[k]);
+    s.wr[k] = mul2(x, fc.cgu1[k]);
     s.wi[k] = mul2(x, fc.gs2[k]);
   }
 }
 
-// a carry record (standard basis, 2 float4) as a sweep-basis state
+// an anticausal carry record (standard basis, 2 float4) in the anticausal sweep basis
 __device__ __forceinline__ void ps_from_carry(PairState& s, float4 c0, float4 c1, const FilterConsts& fc) {
-  s.wr[0] = make_float2(c0.x, c0.y);
-  s.wi[0] = mul2(make_float2(c0.z, c0.w), fc.ips2[0]);
-  s.wr[1] = make_float2(c1.x, c1.y);
-  s.wi[1] = mul2(make_float2(c1.z, c1.w), fc.ips2[1]);
+  const float2 i0 = make_float2(c0.z, c0.w), i1 = make_float2(c1.z, c1.w);
+  s.wr[0] = fma2(fc.ntau_a[0], i0, make_float2(c0.x, c0.y));
+  s.wi[0] = mul2(i0, fc.ips2[0]);
+  s.wr[1] = fma2(fc.ntau_a[1], i1, make_float2(c1.x, c1.y));
+  s.wi[1] = mul2(i1, fc.ips2[1]);
 }
 
-// sum_k Re(c_k w_k): with the sweep basis the weights are (Re c_k, -Im c_k Im p_k)
-__device__ __forceinline__ float2 ps_emit(const PairState& s, const float2* cr, const float2* nci) {
-  return fma2(cr[0], s.wr[0], fma2(nci[0], s.wi[0], fma2(cr[1], s.wr[1], mul2(nci[1], s.wi[1]))));
+// outputs: causal sum_k Re A_k u1_k; anticausal sum_k Re B_k u1_k (+ the
+// section-1 u2 term, zero unless its basis was clamped). The _acc forms add
+// `init` (the other direction's parked value) inside the FMA chain.
+__device__ __forceinline__ float2 ps_emit_c(const PairState& s, const FilterConsts& fc) {
+  return fma2(fc.ce[1], s.wr[1], mul2(fc.ce[0], s.wr[0]));
 }
-
-// init + sum_k Re(c_k w_k): the emit seeded with a value to add (one FMA
-// instead of the MUL at the head of the chain and a separate add)
-__device__ __forceinline__ float2 ps_emit_acc(const PairState& s, const float2* cr, const float2* nci,
-                                              float2 init) {
-  return fma2(cr[0], s.wr[0], fma2(nci[0], s.wi[0], fma2(cr[1], s.wr[1], fma2(nci[1], s.wi[1], init))));
+__device__ __forceinline__ float2 ps_emit_c_acc(const PairState& s, const FilterConsts& fc, float2 init) {
+  return fma2(fc.ce[1], s.wr[1], fma2(fc.ce[0], s.wr[0], init));
+}
+__device__ __forceinline__ float2 ps_emit_a(const PairState& s, const FilterConsts& fc) {
+  return fma2(fc.ae[1], s.wr[1], fma2(fc.aev, s.wi[1], mul2(fc.ae[0], s.wr[0])));
+}
+__device__ __forceinline__ float2 ps_emit_a_acc(const PairState& s, const FilterConsts& fc, float2 init) {
+  return fma2(fc.ae[1], s.wr[1], fma2(fc.aev, s.wi[1], fma2(fc.ae[0], s.wr[0], init)));
 }
 
 // Carry record: the 8 floats of a PairState as two float4.

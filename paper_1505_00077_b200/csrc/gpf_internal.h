@@ -30,16 +30,25 @@ constexpr int kTile = 32;       // rows per column-pass chunk == columns per row
 // fp32x2 instructions directly (the two halves are the two planes of a pair).
 struct FilterConsts {
   float2 pr2[2];                   // Re p_k (poles in the upper half plane)
-  float2 ar2[2], br2[2];           // Re of the causal / anticausal residues A_k, B_k (x2)
-  float2 gr2[2], gi2[2];           // 1/(1-p_k): warm-start gain
-  // Sweep basis: the imaginary part of each section state is kept as
-  // v^ = Im(w) / Im(p), which turns the advance into three FMAs per section
-  //   Re w' = Re p Re w - (Im p)^2 v^ + x,   v^' = Re p v^ + Re w
-  // (a diagonal similarity transform: same conditioning as the complex form).
-  float2 nps2[2];                  // -(Im p_k)^2
-  float2 sai2[2], sbi2[2];         // -Im(A_k) Im(p_k), -Im(B_k) Im(p_k): emit weights of v^
-  float2 gs2[2];                   // Im(1/(1-p_k)) / Im(p_k): warm start of v^
-  float2 ips2[2];                  // 1 / Im(p_k): carry (standard basis) -> v^
+  float2 gr2[2], gi2[2];           // 1/(1-p_k): warm-start gain (standard basis, carry chains)
+  float2 ips2[2];                  // 1 / Im(p_k)
+  float2 gs2[2];                   // Im(1/(1-p_k)) / Im(p_k): warm start of u2
+  // Sweep basis, per direction D (causal c with residues A_k, anticausal a
+  // with B_k): u1 = Re w - tau Im w, u2 = Im w / Im p, with tau = Im R / Re R
+  // (R = A_k or B_k), so that the section's output Re(R w) = Re R * u1 and the
+  // emit costs one FMA per section. The advance stays three FMAs:
+  //   u2' = m22 u2 + u1,   u1' = m11 u1 + m12 u2 + x
+  //   m11 = Re p - tau Im p,  m22 = Re p + tau Im p,  m12 = -(Im p)^2 (1 + tau^2)
+  // (tau = 0 is the plain rescaled basis u2 = Im w / Im p). Only B_1 gets close
+  // to a zero real part (sigma_s in [0.96, 1.17]); there tau is clamped to
+  // |tau Im p| <= 1 and its emit keeps a u2 term (aev).
+  float2 cm11[2], cm12[2], cm22[2];  // causal advance
+  float2 am11[2], am12[2], am22[2];  // anticausal advance
+  float2 ce[2];                      // causal emit weights Re A_k
+  float2 ae[2];                      // anticausal emit weights Re B_k
+  float2 aev;                        // anticausal section-1 u2 weight (0 unless tau clamped)
+  float2 ntau_a[2];                  // -tau of the anticausal sections (carry -> u1)
+  float2 cgu1[2];                    // causal warm start of u1: Re g - tau Im g
 };
 
 // Tile constants for exact anticausal carries between chunks of kTile

@@ -451,14 +451,14 @@ __global__ void __launch_bounds__(32 * kColGroup, GPF_COL_CTAS) k_colpass_tma(
       for (int t = 0; t < kTile / 2; t += 2) {
         const float4 va = *reinterpret_cast<const float4*>(stage_at(mcol, 30 - t, cm));
         const float4 vc = *reinterpret_cast<const float4*>(stage_at(mcol, t, cm));
-        pa[15 - t] = ps_emit(as, fc.br2, fc.sbi2);  // row 31-t
-        ps_advance(as, make_float2(va.z, va.w), fc);
-        ps_advance(cs, make_float2(vc.x, vc.y), fc);
-        pc[t] = ps_emit(cs, fc.ar2, fc.sai2);  // row t
-        pa[14 - t] = ps_emit(as, fc.br2, fc.sbi2);  // row 30-t
-        ps_advance(as, make_float2(va.x, va.y), fc);
-        ps_advance(cs, make_float2(vc.z, vc.w), fc);
-        pc[t + 1] = ps_emit(cs, fc.ar2, fc.sai2);  // row t+1
+        pa[15 - t] = ps_emit_a(as, fc);  // row 31-t
+        ps_advance_a(as, make_float2(va.z, va.w), fc);
+        ps_advance_c(cs, make_float2(vc.x, vc.y), fc);
+        pc[t] = ps_emit_c(cs, fc);  // row t
+        pa[14 - t] = ps_emit_a(as, fc);  // row 30-t
+        ps_advance_a(as, make_float2(va.x, va.y), fc);
+        ps_advance_c(cs, make_float2(vc.z, vc.w), fc);
+        pc[t + 1] = ps_emit_c(cs, fc);  // row t+1
       }
       // second half: anticausal rows 15-u, 14-u; causal rows 16+u, 17+u; the
       // next step's inputs are read before this step's outputs are stored
@@ -471,14 +471,14 @@ __global__ void __launch_bounds__(32 * kColGroup, GPF_COL_CTAS) k_colpass_tma(
           na = *reinterpret_cast<const float4*>(stage_at(mcol, 12 - u, cm));
           nc = *reinterpret_cast<const float4*>(stage_at(mcol, 18 + u, cm));
         }
-        const float2 yb = ps_emit_acc(as, fc.br2, fc.sbi2, pc[15 - u]);
-        ps_advance(as, make_float2(va.z, va.w), fc);
-        ps_advance(cs, make_float2(vc.x, vc.y), fc);
-        const float2 yc0 = ps_emit_acc(cs, fc.ar2, fc.sai2, pa[u]);
-        const float2 ya = ps_emit_acc(as, fc.br2, fc.sbi2, pc[14 - u]);
-        ps_advance(as, make_float2(va.x, va.y), fc);
-        ps_advance(cs, make_float2(vc.z, vc.w), fc);
-        const float2 yc1 = ps_emit_acc(cs, fc.ar2, fc.sai2, pa[u + 1]);
+        const float2 yb = ps_emit_a_acc(as, fc, pc[15 - u]);
+        ps_advance_a(as, make_float2(va.z, va.w), fc);
+        ps_advance_c(cs, make_float2(vc.x, vc.y), fc);
+        const float2 yc0 = ps_emit_c_acc(cs, fc, pa[u]);
+        const float2 ya = ps_emit_a_acc(as, fc, pc[14 - u]);
+        ps_advance_a(as, make_float2(va.x, va.y), fc);
+        ps_advance_c(cs, make_float2(vc.z, vc.w), fc);
+        const float2 yc1 = ps_emit_c_acc(cs, fc, pa[u + 1]);
         *reinterpret_cast<float4*>(stage_at(mcol, 14 - u, cm)) = make_float4(ya.x, ya.y, yb.x, yb.y);
         *reinterpret_cast<float4*>(stage_at(mcol, 16 + u, cm)) = make_float4(yc0.x, yc0.y, yc1.x, yc1.y);
         va = na;
@@ -497,16 +497,16 @@ __global__ void __launch_bounds__(32 * kColGroup, GPF_COL_CTAS) k_colpass_tma(
 #pragma unroll
         for (int j = kTile - 1; j >= 0; --j) {
           if (j < rows) {
-            *reinterpret_cast<float2*>(stage_at(mcol, j, cm)) = ps_emit(as, fc.br2, fc.sbi2);
-            ps_advance(as, xr[j], fc);
+            *reinterpret_cast<float2*>(stage_at(mcol, j, cm)) = ps_emit_a(as, fc);
+            ps_advance_a(as, xr[j], fc);
           }
         }
 #pragma unroll
         for (int j = 0; j < kTile; ++j) {
           if (j < rows) {
             float2* p = reinterpret_cast<float2*>(stage_at(mcol, j, cm));
-            ps_advance(cs, xr[j], fc);
-            *p = add2(ps_emit(cs, fc.ar2, fc.sai2), *p);
+            ps_advance_c(cs, xr[j], fc);
+            *p = add2(ps_emit_c(cs, fc), *p);
           }
         }
       }
@@ -714,15 +714,15 @@ __global__ void __launch_bounds__(MAXT, 1) k_colpass(const Tin* __restrict__ in_
 #pragma unroll
       for (int j = kTile - 1; j >= 0; --j) {
         if (j < rows) {
-          mine[j] = ps_emit(as, fc.br2, fc.sbi2);
-          ps_advance(as, xr[j], fc);
+          mine[j] = ps_emit_a(as, fc);
+          ps_advance_a(as, xr[j], fc);
         }
       }
 #pragma unroll
       for (int j = 0; j < kTile; ++j) {
         if (j < rows) {
-          ps_advance(cs, xr[j], fc);
-          mine[j] = add2(ps_emit(cs, fc.ar2, fc.sai2), mine[j]);
+          ps_advance_c(cs, xr[j], fc);
+          mine[j] = add2(ps_emit_c(cs, fc), mine[j]);
         }
       }
     }

@@ -108,11 +108,11 @@ __global__ void __launch_bounds__(MAXT, 1) k_rowpass(const Tin* __restrict__ in_
 #pragma unroll
         for (int t = 0; t < 32; ++t) {
           const int ca = 31 - t, cc = t;
-          const float2 ya = ps_emit(as, fc.br2, fc.sbi2);
+          const float2 ya = ps_emit_a(as, fc);
           const float2 xa = tl[ca * kRowBand], xc = tl[cc * kRowBand];
-          ps_advance(as, xa, fc);
-          ps_advance(cs, xc, fc);
-          const float2 yc = ps_emit(cs, fc.ar2, fc.sai2);
+          ps_advance_a(as, xa, fc);
+          ps_advance_c(cs, xc, fc);
+          const float2 yc = ps_emit_c(cs, fc);
           if (t < 16) {
             ya_hi[ca - 16] = ya;
             yc_lo[cc] = yc;
@@ -128,15 +128,15 @@ __global__ void __launch_bounds__(MAXT, 1) k_rowpass(const Tin* __restrict__ in_
 #pragma unroll
         for (int c = 31; c >= 0; --c) {
           if (c < cols) {
-            ybuf[c] = ps_emit(as, fc.br2, fc.sbi2);
-            ps_advance(as, tl[c * kRowBand], fc);
+            ybuf[c] = ps_emit_a(as, fc);
+            ps_advance_a(as, tl[c * kRowBand], fc);
           }
         }
 #pragma unroll
         for (int c = 0; c < 32; ++c) {
           if (c < cols) {
-            ps_advance(cs, tl[c * kRowBand], fc);
-            const float2 o = add2(ps_emit(cs, fc.ar2, fc.sai2), ybuf[c]);
+            ps_advance_c(cs, tl[c * kRowBand], fc);
+            const float2 o = add2(ps_emit_c(cs, fc), ybuf[c]);
             if (live) tl[c * kRowBand] = o;
           }
         }
@@ -501,18 +501,18 @@ __global__ void __launch_bounds__(RB == 8 ? 96 : 192, RB == 8 ? 4 : 2) k_rowpass
         if ((t & 1) == 1) asm volatile("" ::: "memory");
         const int ca = 31 - t, cc = t;
         if (t < 16) {
-          const float2 ya = ps_emit(as, fc.br2, fc.sbi2);
+          const float2 ya = ps_emit_a(as, fc);
           const float2 xa = tl[ca * RB], xc = tl[cc * RB];
-          ps_advance(as, xa, fc);
-          ps_advance(cs, xc, fc);
+          ps_advance_a(as, xa, fc);
+          ps_advance_c(cs, xc, fc);
           ya_hi[ca - 16] = ya;
-          yc_lo[cc] = ps_emit(cs, fc.ar2, fc.sai2);
+          yc_lo[cc] = ps_emit_c(cs, fc);
         } else {  // the other direction's parked value seeds the emit
-          const float2 ya = ps_emit_acc(as, fc.br2, fc.sbi2, yc_lo[ca]);
+          const float2 ya = ps_emit_a_acc(as, fc, yc_lo[ca]);
           const float2 xa = tl[ca * RB], xc = tl[cc * RB];
-          ps_advance(as, xa, fc);
-          ps_advance(cs, xc, fc);
-          const float2 yc = ps_emit_acc(cs, fc.ar2, fc.sai2, ya_hi[cc - 16]);
+          ps_advance_a(as, xa, fc);
+          ps_advance_c(cs, xc, fc);
+          const float2 yc = ps_emit_c_acc(cs, fc, ya_hi[cc - 16]);
           if (live) {
             tl[ca * RB] = ya;
             tl[cc * RB] = yc;
@@ -524,15 +524,15 @@ __global__ void __launch_bounds__(RB == 8 ? 96 : 192, RB == 8 ? 4 : 2) k_rowpass
 #pragma unroll
       for (int c = 31; c >= 0; --c) {
         if (c < cols) {
-          ybuf[c] = ps_emit(as, fc.br2, fc.sbi2);
-          ps_advance(as, tl[c * RB], fc);
+          ybuf[c] = ps_emit_a(as, fc);
+          ps_advance_a(as, tl[c * RB], fc);
         }
       }
 #pragma unroll
       for (int c = 0; c < 32; ++c) {
         if (c < cols) {
-          ps_advance(cs, tl[c * RB], fc);
-          const float2 o = add2(ps_emit(cs, fc.ar2, fc.sai2), ybuf[c]);
+          ps_advance_c(cs, tl[c * RB], fc);
+          const float2 o = add2(ps_emit_c(cs, fc), ybuf[c]);
           if (live) tl[c * RB] = o;
         }
       }
