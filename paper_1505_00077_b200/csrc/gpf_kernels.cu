@@ -352,6 +352,12 @@ __device__ __forceinline__ void produce_group(float* stage, const float2* emt, i
 #ifndef GPF_COL_CTAS
 #define GPF_COL_CTAS 4
 #endif
+#ifndef GPF_COL_XREG
+#define GPF_COL_XREG 0
+#endif
+// GPF_COL_XREG: the full-chunk sweep keeps its inputs in registers for the
+// second half (no re-reads from the stage; needs ~166 registers, 3 CTAs/SM)
+constexpr bool kColXreg = GPF_COL_XREG != 0;
 constexpr int kColStages = GPF_COL_STAGES;  // staging tiles per CTA (1: store drains under the H-dots)
 
 __global__ void __launch_bounds__(32 * kColGroup, GPF_COL_CTAS) k_colpass_tma(
@@ -447,10 +453,15 @@ __global__ void __launch_bounds__(32 * kColGroup, GPF_COL_CTAS) k_colpass_tma(
         ps_set_gain_sweep(cs, make_float2(v0.x, v0.y), fc);
       }
       float2 pa[kTile / 2], pc[kTile / 2];
+      float4 xa[kColXreg ? kTile / 4 : 1], xc[kColXreg ? kTile / 4 : 1];  // inputs kept for the second half
 #pragma unroll
       for (int t = 0; t < kTile / 2; t += 2) {
         const float4 va = *reinterpret_cast<const float4*>(stage_at(mcol, 30 - t, cm));
         const float4 vc = *reinterpret_cast<const float4*>(stage_at(mcol, t, cm));
+        if constexpr (kColXreg) {
+          xa[t / 2] = va;  // rows 30-t, 31-t
+          xc[t / 2] = vc;  // rows t, t+1
+        }
         pa[15 - t] = ps_emit_a(as, fc);  // row 31-t
         ps_advance_a(as, make_float2(va.z, va.w), fc);
         ps_advance_c(cs, make_float2(vc.x, vc.y), fc);
@@ -462,14 +473,25 @@ __global__ void __launch_bounds__(32 * kColGroup, GPF_COL_CTAS) k_colpass_tma(
       }
       // second half: anticausal rows 15-u, 14-u; causal rows 16+u, 17+u; the
       // next step's inputs are read before this step's outputs are stored
-      float4 va = *reinterpret_cast<const float4*>(stage_at(mcol, 14, cm));
-      float4 vc = *reinterpret_cast<const float4*>(stage_at(mcol, 16, cm));
+      float4 va, vc;
+      if constexpr (kColXreg) {
+        va = xc[7];
+        vc = xa[7];
+      } else {
+        va = *reinterpret_cast<const float4*>(stage_at(mcol, 14, cm));
+        vc = *reinterpret_cast<const float4*>(stage_at(mcol, 16, cm));
+      }
 #pragma unroll
       for (int u = 0; u < kTile / 2; u += 2) {
         float4 na = va, nc = vc;
         if (u + 2 < kTile / 2) {
-          na = *reinterpret_cast<const float4*>(stage_at(mcol, 12 - u, cm));
-          nc = *reinterpret_cast<const float4*>(stage_at(mcol, 18 + u, cm));
+          if constexpr (kColXreg) {
+            na = xc[(12 - u) / 2];  // rows 12-u, 13-u
+            nc = xa[(12 - u) / 2];  // rows 18+u, 19+u
+          } else {
+            na = *reinterpret_cast<const float4*>(stage_at(mcol, 12 - u, cm));
+            nc = *reinterpret_cast<const float4*>(stage_at(mcol, 18 + u, cm));
+          }
         }
         const float2 yb = ps_emit_a_acc(as, fc, pc[15 - u]);
         ps_advance_a(as, make_float2(va.z, va.w), fc);
