@@ -173,16 +173,18 @@ def algorithmic_bytes_per_px(pairs: int) -> dict:
 
 def algorithmic_flops_per_px(pairs: int) -> dict:
     """FP32 FLOPs each stage issues per pixel (FMA = 2), P = plane pairs.
-    One IIR step of one plane: two complex sections advanced (3 FMA each in
-    the sweep basis) and emitted (3 FMA + 1 MUL for both) = 19; both
-    directions = 38, plus the folded sum ~ 39, i.e. 78 per pair. Strip/chunk
-    dot products: 4 FMA per plane. Contraction: 2 FMA + 2 MUL per plane.
+    One IIR step of one plane in the output-aligned section basis (DESIGN.md
+    section 3): two sections advanced, 3 FMA each, in each direction = 24;
+    emits (causal 1 MUL + 1 FMA, anticausal 1 MUL + 2 FMA, one MUL becoming an
+    FMA where the other direction's parked value is added) ~9; i.e. ~33 per
+    plane, 66 per pair. Strip/chunk dot products: 4 FMA per plane.
+    Contraction: 2 FMA + 2 MUL per plane.
       carries    seeds ~20 + per pair: planes 2 MUL, dots 16          18 P + 20
-      colpass    per pair: planes 2, sweeps 78, row dots 16           96 P
+      colpass    per pair: planes 2, sweeps 66, row dots 16           84 P
       row_scan   per pair: one chain step per 32 pixels              ~P
-      rowpass    per pair: sweeps 78, contraction 12                  90 P + 10"""
-    return {"mean": 1, "col_carry": 18 * pairs + 20, "colpass": 96 * pairs, "row_scan": pairs,
-            "rowpass": 90 * pairs + 10}
+      rowpass    per pair: sweeps 66, contraction 12                  78 P + 10"""
+    return {"mean": 1, "col_carry": 18 * pairs + 20, "colpass": 84 * pairs, "row_scan": pairs,
+            "rowpass": 78 * pairs + 10}
 
 
 def fp32_peak_tflops(peaks: dict) -> float:
