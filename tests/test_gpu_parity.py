@@ -248,3 +248,19 @@ def test_huge_frame_index_range(gpu):
     plan.filter_device(torch.flip(x, [0]).contiguous(), yf, 1, None, s)
     torch.cuda.synchronize()
     assert (torch.flip(yf, [0]) - y).abs().max().item() <= 1e-3
+
+
+@pytest.mark.parametrize("ss", [0.5, 0.75, 0.96, 1.0, 1.03, 1.07, 1.1, 1.17, 1.3, 1.6, 2.5, 100.0])
+def test_sigma_s_sweep_basis_edges(gpu, oracle, ss):
+    """The sweeps run each section in a basis aligned with its output (DESIGN.md 3);
+    one anticausal residue's real part crosses zero near sigma_s = 1.07, where that
+    basis is clamped and the emit keeps a second term. Parity across that window,
+    the smallest admissible sigma_s and a wide one."""
+    cfg = synth.scaled(synth.CONFIGS[1], 200, 152)
+    img = synth.make(cfg).astype(np.float64)
+    ref, rfb, _ = oracle.gpf(img, ss, 30.0, 20, threads=8)
+    out, fb = run(gpu, img, ss, 30.0)
+    assert fb == rfb
+    d = np.abs(out - ref).max()
+    print(f"sigma_s {ss}: max |gpu - oracle| {d:.2e}")
+    assert d <= TOL
