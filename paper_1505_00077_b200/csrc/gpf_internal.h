@@ -118,6 +118,7 @@ struct Plan {
   alignas(64) CUtensorMap vmap8;   // same, 8-row x 33-column boxes (8-row-band row pass)
   alignas(64) CUtensorMap vstore;  // TMA map of V for the column pass's staged chunk stores
   alignas(64) CUtensorMap emmap;   // TMA map of EM: 32x32-pixel tiles for the column pass
+  alignas(64) CUtensorMap emcmap;  // TMA map of EM: 64-column x 32-row tiles for the carry walk
   double* scalars = nullptr;   // [batch][2]  t_c
   double* partials = nullptr;  // [batch][mean_blocks][2]
   size_t bytes = 0;

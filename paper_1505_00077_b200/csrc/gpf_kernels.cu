@@ -685,6 +685,116 @@ __global__ void __launch_bounds__(32) k_col_carry_reg(const float2* __restrict__
   }
 }
 
+// K1b (TMA ring): the same carries, with each 32-row seed tile of a 64-column
+// strip brought into shared memory by TMA, kCarrySlots chunks ahead, instead
+// of a register prefetch of one chunk. CTA = 4 warps; warp wi takes columns
+// 16 wi .. 16 wi + 15 of the strip with the lane mapping of k_col_carry_reg
+// (half-warp = two pairs of the pair group). No register-resident seeds, so
+// four CTAs fit an SM, and HBM latency is covered by the ring depth.
+#ifndef GPF_CARRY_SLOTS
+#define GPF_CARRY_SLOTS 2
+#endif
+constexpr int kCarrySlots = GPF_CARRY_SLOTS;
+constexpr int kCarryCols = 64;  // columns per CTA (4 warps x 16)
+
+template <int GRP>
+__device__ __forceinline__ float2 carry_base(float2 s, int half, float& m2) {
+  // planes (2 pair0, 2 pair0 + 1) of a seed, pair0 = 4 GRP + 2 half:
+  // E m^{8 GRP + 4 half} by squarings (GRP warp-uniform, half per lane)
+  m2 = s.y * s.y;
+  const float m4 = m2 * m2;
+  float xb = s.x;
+  if constexpr (GRP >= 1) {
+    const float m8 = m4 * m4;
+    xb *= (GRP == 2 ? m8 * m8 : m8);
+  }
+  xb *= half ? m4 : 1.f;
+  return make_float2(xb, xb * s.y);
+}
+
+template <int GRP>
+__device__ __forceinline__ void carry_walk(float2* tiles, uint64_t* full,
+                                           float4* CA, const CUtensorMap* emcmap, int w, int h,
+                                           int ny, int pairs, int x0, int f, const FilterConsts& fc,
+                                           const TileConsts& tc) {
+  constexpr int kLanePairs = kColGroup / 2;
+  const int lane = threadIdx.x, wi = threadIdx.y, tid = wi * 32 + lane;
+  const int half = lane >> 4, col = wi * 16 + (lane & 15), x = x0 + col;
+  const int pair0 = GRP * kColGroup + half * kLanePairs;
+  const int npairs = min(kLanePairs, pairs - pair0);
+  const size_t pair_stride = (size_t)w * 2, chunk_stride = (size_t)pairs * w * 2;
+  float4* ca = CA + (size_t)x * 2;
+  PairState C[kLanePairs];
+  for (int k = 0; k < ny; ++k) {
+    const int cy = ny - 1 - k, s = k % kCarrySlots;
+    const float2* tile = tiles + (size_t)s * 32 * kCarryCols + col;  // [32 rows][64 columns]
+    mbar_wait(&full[s], (k / kCarrySlots) & 1);
+    if (k == 0) {  // replicate boundary: steady state of the bottom row
+      float m2;
+      const float2 p0 = carry_base<GRP>(tile[(h - 1 - cy * kTile) * kCarryCols], half, m2);
+      ps_set_gain(C[0], p0, fc);
+      ps_set_gain(C[1], mul2(p0, f2(m2)), fc);
+    }
+    if (x < w) {
+#pragma unroll
+      for (int gg = 0; gg < kLanePairs; ++gg)
+        if (gg < npairs) ps_store(ca + cy * chunk_stride + (pair0 + gg) * pair_stride, C[gg]);
+    }
+    if (cy == 0) break;
+    PairState agg[kLanePairs];
+#pragma unroll
+    for (int gg = 0; gg < kLanePairs; ++gg) ps_zero(agg[gg]);
+    // rows past the image (last, partial chunk) read as zero seeds (TMA fill):
+    // their planes vanish, so the loop is branch-free
+#pragma unroll
+    for (int j = 0; j < kTile; ++j) {
+      float m2;
+      const float2 p0 = carry_base<GRP>(tile[j * kCarryCols], half, m2);
+      ps_accum(agg[0], p0, tc.w4[j]);
+      ps_accum(agg[1], mul2(p0, f2(m2)), tc.w4[j]);
+    }
+    const bool last = k == 0;
+#pragma unroll
+    for (int gg = 0; gg < kLanePairs; ++gg)
+      ps_chain(C[gg], agg[gg], last ? tc.pYr2 : tc.pTr2, last ? tc.pYi2 : tc.pTi2);
+    __syncthreads();  // every warp is done with slot s
+    if (tid == 0 && k + kCarrySlots < ny) {
+      mbar_arrive_expect_tx(&full[s], 32 * kCarryCols * sizeof(float2));
+      tma_load_3d(tiles + (size_t)s * 32 * kCarryCols, emcmap, 2 * x0, (cy - kCarrySlots) * kTile, f,
+                  &full[s]);
+    }
+  }
+}
+
+__global__ void __launch_bounds__(128, GPF_CARRY_SLOTS == 2 ? 6 : 4) k_col_carry_tma(float4* __restrict__ CA_all, int w, int h,
+                                                          int ny, int pairs, int groups,
+                                                          FilterConsts fc, TileConsts tc,
+                                                          const __grid_constant__ CUtensorMap emcmap) {
+  extern __shared__ float4 smem4[];
+  __shared__ uint64_t full[kCarrySlots];
+  // [kCarrySlots][32][64] float2, 128-B aligned for TMA (offset from the smem base)
+  float2* tiles = reinterpret_cast<float2*>(reinterpret_cast<char*>(smem4) +
+                                            ((128u - smem_u32(smem4)) & 127u));
+  const int f = blockIdx.y, tid = threadIdx.y * 32 + threadIdx.x;
+  const int strip = blockIdx.x / groups, grp = blockIdx.x - strip * groups;
+  const int x0 = strip * kCarryCols;
+  if (tid == 0) {
+    for (int s = 0; s < kCarrySlots; ++s) mbar_init(&full[s], 1);
+    mbar_fence_init();
+  }
+  __syncthreads();
+  if (tid == 0) {
+    for (int k = 0; k < kCarrySlots && k < ny; ++k) {
+      mbar_arrive_expect_tx(&full[k], 32 * kCarryCols * sizeof(float2));
+      tma_load_3d(tiles + (size_t)k * 32 * kCarryCols, &emcmap, 2 * x0, (ny - 1 - k) * kTile, f, &full[k]);
+    }
+  }
+  float4* CA = CA_all + (size_t)f * ny * pairs * w * 2;
+  if (grp == 0) carry_walk<0>(tiles, full, CA, &emcmap, w, h, ny, pairs, x0, f, fc, tc);
+  else if (grp == 1) carry_walk<1>(tiles, full, CA, &emcmap, w, h, ny, pairs, x0, f, fc, tc);
+  else carry_walk<2>(tiles, full, CA, &emcmap, w, h, ny, pairs, x0, f, fc, tc);
+}
+
 template <int MAXT, typename Tin>
 __global__ void __launch_bounds__(MAXT, 1) k_colpass(const Tin* __restrict__ in_all,
                                                      const double* __restrict__ scalars,
@@ -1019,6 +1129,15 @@ void plan_init(Plan& plan, const Params& p, int device, int batch) {
   const CUresult r3 = encode(&plan.emmap, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, plan.EM, edims, estrides,
                              ebox, eestr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
                              CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  // EM seeds for the carry walk: box {128 (= 64 pixels), 32 rows, 1}
+  const cuuint32_t cbox[3] = {2 * kCarryCols, 32, 1};
+  const CUresult r4 = encode(&plan.emcmap, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, plan.EM, edims, estrides,
+                             cbox, eestr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                             CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r4 != CUDA_SUCCESS) {
+    plan_free(plan);
+    throw Error{9, "cuTensorMapEncodeTiled (EM carries) failed (" + std::to_string((int)r4) + ")"};
+  }
   if (r3 != CUDA_SUCCESS) {
     plan_free(plan);
     throw Error{9, "cuTensorMapEncodeTiled (EM) failed (" + std::to_string((int)r3) + ")"};
@@ -1043,6 +1162,9 @@ void plan_free(Plan& plan) {
 // 384 -> up to 168 registers/thread (N <= 22), 512 -> 128 (N <= 30), 1024 -> 64.
 #ifndef GPF_ROW_BAND
 #define GPF_ROW_BAND 16
+#endif
+#ifndef GPF_CARRY_TMA
+#define GPF_CARRY_TMA 1
 #endif
 
 template <int MAXT, typename Tin, typename Tout>
@@ -1071,8 +1193,19 @@ static void launch_passes(Plan& plan, const Tin* d_in, Tout* d_out, int count,
     // seeds once per pixel, then the carries in pair groups
     k_seed<Tin><<<dim3((w + 1023) / 1024, std::min(h, 1024), count), 256, 0, st>>>(
         d_in, plan.scalars, plan.EM, w, h, plan.w_pad, plan.rc);
+#ifndef GPF_DIAG_NO_CARRY  // diagnostic: skip the carries (wrong output; bench-mix cost)
+#if GPF_CARRY_TMA
+    if (groups <= 3) {
+      const int csm2 = (int)(sizeof(float2) * kCarrySlots * 32 * kCarryCols + 128);
+      check(cudaFuncSetAttribute(k_col_carry_tma, cudaFuncAttributeMaxDynamicSharedMemorySize, csm2),
+            "cudaFuncSetAttribute");
+      k_col_carry_tma<<<dim3((w + kCarryCols - 1) / kCarryCols * groups, count), dim3(32, 4), csm2, st>>>(
+          plan.CA, w, h, plan.ny, pairs, groups, plan.fc, plan.tc, plan.emcmap);
+    } else
+#endif
     k_col_carry_reg<<<dim3((w + 15) / 16 * groups, count), 32, 0, st>>>(
         plan.EM, plan.CA, w, h, plan.w_pad, plan.ny, pairs, groups, plan.fc, plan.tc);
+#endif
   } else {
     k_col_carry<MAXT, Tin><<<dim3(plan.nx, count), blk, csm, st>>>(
         d_in, plan.scalars, plan.CA, plan.EM, w, h, plan.w_pad, plan.ny, plan.fc, plan.tc, plan.rc);
@@ -1094,8 +1227,10 @@ static void launch_passes(Plan& plan, const Tin* d_in, Tout* d_out, int count,
   }
   if (plan.front_done) check(cudaEventRecord(plan.front_done, st), "cudaEventRecord");
   stage_mark(plan, kStageRowScan, st);
+#ifndef GPF_DIAG_NO_ROWSCAN  // diagnostic: skip the row scan (wrong output; bench-mix cost)
   k_row_scan<<<dim3(plan.ny, count), blk, 0, st>>>(plan.V, plan.AH, plan.CH, w, h, h_pad, plan.nx,
                                                    plan.fc, plan.tc);
+#endif
   stage_mark(plan, kStageRowPass, st);
   if (pairs <= 12) {
     constexpr int RB = GPF_ROW_BAND;  // rows per row-pass CTA (16 or 8)
