@@ -695,7 +695,11 @@ __global__ void __launch_bounds__(32) k_col_carry_reg(const float2* __restrict__
 #define GPF_CARRY_SLOTS 2
 #endif
 constexpr int kCarrySlots = GPF_CARRY_SLOTS;
-constexpr int kCarryCols = 64;  // columns per CTA (4 warps x 16)
+#ifndef GPF_CARRY_COLS
+#define GPF_CARRY_COLS 64
+#endif
+constexpr int kCarryCols = GPF_CARRY_COLS;  // columns per CTA (kCarryCols / 16 warps)
+constexpr int kCarryWarps = kCarryCols / 16;
 
 template <int GRP>
 __device__ __forceinline__ float2 carry_base(float2 s, int half, float& m2) {
@@ -727,7 +731,7 @@ __device__ __forceinline__ void carry_walk(float2* tiles, uint64_t* full,
   PairState C[kLanePairs];
   for (int k = 0; k < ny; ++k) {
     const int cy = ny - 1 - k, s = k % kCarrySlots;
-    const float2* tile = tiles + (size_t)s * 32 * kCarryCols + col;  // [32 rows][64 columns]
+    const float2* tile = tiles + (size_t)s * 32 * kCarryCols + col;  // [32 rows][kCarryCols columns]
     mbar_wait(&full[s], (k / kCarrySlots) & 1);
     if (k == 0) {  // replicate boundary: steady state of the bottom row
       float m2;
@@ -766,7 +770,7 @@ __device__ __forceinline__ void carry_walk(float2* tiles, uint64_t* full,
   }
 }
 
-__global__ void __launch_bounds__(128, GPF_CARRY_SLOTS == 2 ? 6 : 4) k_col_carry_tma(float4* __restrict__ CA_all, int w, int h,
+__global__ void __launch_bounds__(32 * kCarryWarps, (GPF_CARRY_SLOTS == 2 ? 6 : 4) * (4 / kCarryWarps)) k_col_carry_tma(float4* __restrict__ CA_all, int w, int h,
                                                           int ny, int pairs, int groups,
                                                           FilterConsts fc, TileConsts tc,
                                                           const __grid_constant__ CUtensorMap emcmap) {
@@ -1199,7 +1203,7 @@ static void launch_passes(Plan& plan, const Tin* d_in, Tout* d_out, int count,
       const int csm2 = (int)(sizeof(float2) * kCarrySlots * 32 * kCarryCols + 128);
       check(cudaFuncSetAttribute(k_col_carry_tma, cudaFuncAttributeMaxDynamicSharedMemorySize, csm2),
             "cudaFuncSetAttribute");
-      k_col_carry_tma<<<dim3((w + kCarryCols - 1) / kCarryCols * groups, count), dim3(32, 4), csm2, st>>>(
+      k_col_carry_tma<<<dim3((w + kCarryCols - 1) / kCarryCols * groups, count), dim3(32, kCarryWarps), csm2, st>>>(
           plan.CA, w, h, plan.ny, pairs, groups, plan.fc, plan.tc, plan.emcmap);
     } else
 #endif
