@@ -698,8 +698,12 @@ constexpr int kCarrySlots = GPF_CARRY_SLOTS;
 #ifndef GPF_CARRY_COLS
 #define GPF_CARRY_COLS 64
 #endif
-constexpr int kCarryCols = GPF_CARRY_COLS;  // columns per CTA (kCarryCols / 16 warps)
-constexpr int kCarryWarps = kCarryCols / 16;
+#ifndef GPF_CARRY_LP
+#define GPF_CARRY_LP 2
+#endif
+constexpr int kCarryLP = GPF_CARRY_LP;       // pairs per lane (2 or 4)
+constexpr int kCarryCols = GPF_CARRY_COLS;  // columns per CTA
+constexpr int kCarryWarps = kCarryCols / (8 * kCarryLP);
 
 template <int GRP>
 __device__ __forceinline__ float2 carry_base(float2 s, int half, float& m2) {
@@ -721,9 +725,13 @@ __device__ __forceinline__ void carry_walk(float2* tiles, uint64_t* full,
                                            float4* CA, const CUtensorMap* emcmap, int w, int h,
                                            int ny, int pairs, int x0, int f, const FilterConsts& fc,
                                            const TileConsts& tc) {
-  constexpr int kLanePairs = kColGroup / 2;
+  // kCarryLP pairs per lane: 2 (half-warp per two pairs, 16 columns per warp)
+  // or 4 (the whole group, 32 columns per warp: one power chain per seed)
+  constexpr int kLanePairs = kCarryLP;
+  constexpr int kWarpCols = 8 * kCarryLP;  // 16 or 32
   const int lane = threadIdx.x, wi = threadIdx.y, tid = wi * 32 + lane;
-  const int half = lane >> 4, col = wi * 16 + (lane & 15), x = x0 + col;
+  const int half = kCarryLP == 2 ? lane >> 4 : 0;
+  const int col = wi * kWarpCols + (lane & (kWarpCols - 1)), x = x0 + col;
   const int pair0 = GRP * kColGroup + half * kLanePairs;
   const int npairs = min(kLanePairs, pairs - pair0);
   const size_t pair_stride = (size_t)w * 2, chunk_stride = (size_t)pairs * w * 2;
@@ -735,9 +743,12 @@ __device__ __forceinline__ void carry_walk(float2* tiles, uint64_t* full,
     mbar_wait(&full[s], (k / kCarrySlots) & 1);
     if (k == 0) {  // replicate boundary: steady state of the bottom row
       float m2;
-      const float2 p0 = carry_base<GRP>(tile[(h - 1 - cy * kTile) * kCarryCols], half, m2);
-      ps_set_gain(C[0], p0, fc);
-      ps_set_gain(C[1], mul2(p0, f2(m2)), fc);
+      float2 pl = carry_base<GRP>(tile[(h - 1 - cy * kTile) * kCarryCols], half, m2);
+#pragma unroll
+      for (int gg = 0; gg < kLanePairs; ++gg) {
+        ps_set_gain(C[gg], pl, fc);
+        pl = mul2(pl, f2(m2));
+      }
     }
     if (x < w) {
 #pragma unroll
@@ -753,9 +764,12 @@ __device__ __forceinline__ void carry_walk(float2* tiles, uint64_t* full,
 #pragma unroll
     for (int j = 0; j < kTile; ++j) {
       float m2;
-      const float2 p0 = carry_base<GRP>(tile[j * kCarryCols], half, m2);
-      ps_accum(agg[0], p0, tc.w4[j]);
-      ps_accum(agg[1], mul2(p0, f2(m2)), tc.w4[j]);
+      float2 pl = carry_base<GRP>(tile[j * kCarryCols], half, m2);
+#pragma unroll
+      for (int gg = 0; gg < kLanePairs; ++gg) {
+        ps_accum(agg[gg], pl, tc.w4[j]);
+        if (gg + 1 < kLanePairs) pl = mul2(pl, f2(m2));
+      }
     }
     const bool last = k == 0;
 #pragma unroll
