@@ -491,7 +491,7 @@ __global__ void __launch_bounds__(RB == 8 ? 96 : 192, RB == 8 ? 4 : 2) k_rowpass
 #else
     constexpr bool kSweep = true;
 #endif
-    if (kSweep && cols == 32) {
+    if (kSweep && live && cols == 32) {  // a dead half-warp (odd P) idles: same issue, less power
       // both directions in one loop: step t runs the anticausal sections at
       // column 31-t and the causal ones at column t; first-half outputs wait
       // in registers, second-half outputs add them and are written in place
@@ -519,7 +519,7 @@ __global__ void __launch_bounds__(RB == 8 ? 96 : 192, RB == 8 ? 4 : 2) k_rowpass
           }
         }
       }
-    } else if (kSweep) {  // last, partial strip
+    } else if (kSweep && live) {  // last, partial strip
       float2 ybuf[32];
 #pragma unroll
       for (int c = 31; c >= 0; --c) {
