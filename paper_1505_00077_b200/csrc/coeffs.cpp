@@ -85,6 +85,7 @@ FilterConsts make_filter_consts(double s) {
                    std::polar(std::exp(-1.7830 / s), -0.6318 / s),
                    std::polar(std::exp(-1.7230 / s), -1.9970 / s)};
   FilterConsts fc{};
+  double are[2], bre[2], aev = 0.0;  // emit weights before normalisation
   for (int sec = 0; sec < 2; ++sec) {
     const cd pk = p[sec];
     const cd q = 1.0 / pk;
@@ -114,15 +115,23 @@ FilterConsts make_filter_consts(double s) {
     basis(A, fc.cm11, fc.cm12, fc.cm22, tc);
     basis(B, fc.am11, fc.am12, fc.am22, ta);
     // Re(R w) = Re R u1 + Im p (Re R tau - Im R) u2
-    fc.ce[sec] = dup(A.real());
-    fc.ae[sec] = dup(B.real());
+    are[sec] = A.real();
+    bre[sec] = B.real();
     const double cv = si * (A.real() * tc - A.imag()), av = si * (B.real() * ta - B.imag());
     if (std::fabs(cv) > 1e-12 * std::abs(A) || (sec == 0 && std::fabs(av) > 1e-12 * std::abs(B)))
       throw Error{9, "sweep basis: unsupported residue (sigma_s " + std::to_string(s) + ")"};
-    if (sec == 1) fc.aev = dup(av);
+    if (sec == 1) aev = av;
     fc.ntau_a[sec] = dup(-ta);
     fc.cgu1[sec] = dup(g.real() - tc * g.imag());
   }
+  // emit normalisation (see FilterConsts): S = Re A_0 > 0 for every sigma_s
+  const double S = are[0];
+  for (int sec = 0; sec < 2; ++sec) {
+    fc.ce[sec] = dup(are[sec] / S);
+    fc.ae[sec] = dup(bre[sec] / S);
+  }
+  fc.aev = dup(aev / S);
+  fc.seed_log2 = 2.0 * std::log2(S);
   return fc;
 }
 

@@ -112,11 +112,12 @@ __device__ __forceinline__ void ps_from_carry(PairState& s, float4 c0, float4 c1
 // outputs: causal sum_k Re A_k u1_k; anticausal sum_k Re B_k u1_k (+ the
 // section-1 u2 term, zero unless its basis was clamped). The _acc forms add
 // `init` (the other direction's parked value) inside the FMA chain.
+// (causal section-0 weight normalised to 1, FilterConsts::seed_log2)
 __device__ __forceinline__ float2 ps_emit_c(const PairState& s, const FilterConsts& fc) {
-  return fma2(fc.ce[1], s.wr[1], mul2(fc.ce[0], s.wr[0]));
+  return fma2(fc.ce[1], s.wr[1], s.wr[0]);
 }
 __device__ __forceinline__ float2 ps_emit_c_acc(const PairState& s, const FilterConsts& fc, float2 init) {
-  return fma2(fc.ce[1], s.wr[1], fma2(fc.ce[0], s.wr[0], init));
+  return fma2(fc.ce[1], s.wr[1], add2(s.wr[0], init));
 }
 __device__ __forceinline__ float2 ps_emit_a(const PairState& s, const FilterConsts& fc) {
   return fma2(fc.ae[1], s.wr[1], fma2(fc.aev, s.wi[1], mul2(fc.ae[0], s.wr[0])));

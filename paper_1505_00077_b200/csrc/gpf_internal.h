@@ -49,6 +49,11 @@ struct FilterConsts {
   float2 aev;                        // anticausal section-1 u2 weight (0 unless tau clamped)
   float2 ntau_a[2];                  // -tau of the anticausal sections (carry -> u1)
   float2 cgu1[2];                    // causal warm start of u1: Re g - tau Im g
+  // Emit normalisation: every emit weight is divided by S = Re A_0, so the
+  // causal section-0 weight is 1 (its emit needs no multiply). The column
+  // pass's input carries S^2 (plane seeds, RangeConsts::e_log2 += seed_log2)
+  // and its output S, so the row pass's input carries S and its output none.
+  double seed_log2;                  // log2(S^2), host side
 };
 
 // Tile constants for exact anticausal carries between chunks of kTile

@@ -1067,6 +1067,7 @@ void plan_init(Plan& plan, const Params& p, int device, int batch) {
   plan.fc = make_filter_consts(p.sigma_s);
   plan.tc = make_tile_consts(p.sigma_s, p.width, p.height);
   plan.rc = make_range_consts(p);
+  plan.rc.e_log2 += plan.fc.seed_log2;  // column-pass input carries S^2 (emit normalisation)
   const int pairs = plan.rc.pairs;
   if (rowpass_nbuf<double, double>(pairs) == 0 || colpass_smem<double>(pairs) > 227 * 1024)
     throw Error{1, "RangeParams: degree must be <= 48 in the B200 library"};
