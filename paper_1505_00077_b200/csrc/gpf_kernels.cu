@@ -360,6 +360,7 @@ __device__ __forceinline__ void produce_group(float* stage, const float2* emt, i
 constexpr bool kColXreg = GPF_COL_XREG != 0;
 constexpr int kColStages = GPF_COL_STAGES;  // staging tiles per CTA (1: store drains under the H-dots)
 
+template <bool AEV>
 __global__ void __launch_bounds__(32 * kColGroup, GPF_COL_CTAS) k_colpass_tma(
     const float4* __restrict__ CA_all, float4* __restrict__ AH_all, int w, int h, int ny, int nx,
     int pairs, int groups, FilterConsts fc, TileConsts tc,
@@ -462,11 +463,11 @@ __global__ void __launch_bounds__(32 * kColGroup, GPF_COL_CTAS) k_colpass_tma(
           xa[t / 2] = va;  // rows 30-t, 31-t
           xc[t / 2] = vc;  // rows t, t+1
         }
-        pa[15 - t] = ps_emit_a(as, fc);  // row 31-t
+        pa[15 - t] = ps_emit_a<AEV>(as, fc);  // row 31-t
         ps_advance_a(as, make_float2(va.z, va.w), fc);
         ps_advance_c(cs, make_float2(vc.x, vc.y), fc);
         pc[t] = ps_emit_c(cs, fc);  // row t
-        pa[14 - t] = ps_emit_a(as, fc);  // row 30-t
+        pa[14 - t] = ps_emit_a<AEV>(as, fc);  // row 30-t
         ps_advance_a(as, make_float2(va.x, va.y), fc);
         ps_advance_c(cs, make_float2(vc.z, vc.w), fc);
         pc[t + 1] = ps_emit_c(cs, fc);  // row t+1
@@ -493,11 +494,11 @@ __global__ void __launch_bounds__(32 * kColGroup, GPF_COL_CTAS) k_colpass_tma(
             nc = *reinterpret_cast<const float4*>(stage_at(mcol, 18 + u, cm));
           }
         }
-        const float2 yb = ps_emit_a_acc(as, fc, pc[15 - u]);
+        const float2 yb = ps_emit_a_acc<AEV>(as, fc, pc[15 - u]);
         ps_advance_a(as, make_float2(va.z, va.w), fc);
         ps_advance_c(cs, make_float2(vc.x, vc.y), fc);
         const float2 yc0 = ps_emit_c_acc(cs, fc, pa[u]);
-        const float2 ya = ps_emit_a_acc(as, fc, pc[14 - u]);
+        const float2 ya = ps_emit_a_acc<AEV>(as, fc, pc[14 - u]);
         ps_advance_a(as, make_float2(va.x, va.y), fc);
         ps_advance_c(cs, make_float2(vc.z, vc.w), fc);
         const float2 yc1 = ps_emit_c_acc(cs, fc, pa[u + 1]);
@@ -519,7 +520,7 @@ __global__ void __launch_bounds__(32 * kColGroup, GPF_COL_CTAS) k_colpass_tma(
 #pragma unroll
         for (int j = kTile - 1; j >= 0; --j) {
           if (j < rows) {
-            *reinterpret_cast<float2*>(stage_at(mcol, j, cm)) = ps_emit_a(as, fc);
+            *reinterpret_cast<float2*>(stage_at(mcol, j, cm)) = ps_emit_a<AEV>(as, fc);
             ps_advance_a(as, xr[j], fc);
           }
         }
@@ -1231,9 +1232,10 @@ static void launch_passes(Plan& plan, const Tin* d_in, Tout* d_out, int count,
   }
   stage_mark(plan, kStageColPass, st);
   if constexpr (kCanStage) {
-    check(cudaFuncSetAttribute(k_colpass_tma, cudaFuncAttributeMaxDynamicSharedMemorySize, psm),
+    auto kc = plan.fc.aev.x != 0.f ? k_colpass_tma<true> : k_colpass_tma<false>;
+    check(cudaFuncSetAttribute(kc, cudaFuncAttributeMaxDynamicSharedMemorySize, psm),
           "cudaFuncSetAttribute");
-    k_colpass_tma<<<dim3(plan.nx * groups, count), dim3(32, kColGroup), psm, st>>>(
+    kc<<<dim3(plan.nx * groups, count), dim3(32, kColGroup), psm, st>>>(
         plan.CA, plan.AH, w, h, plan.ny, plan.nx, pairs, groups, plan.fc, plan.tc, plan.emmap,
         plan.vstore);
   }
@@ -1267,9 +1269,14 @@ static void launch_passes(Plan& plan, const Tin* d_in, Tout* d_out, int count,
     }
     // the default degree (N = 20, reference RangeParams) has a fully static build
     const bool n20 = plan.rc.degree == 20;
-    auto k = n20 ? k_rowpass2<Tin, Tout, 20, false, RB> : k_rowpass2<Tin, Tout, 0, false, RB>;
+    // the clamped-basis u2 emit term only for sigma_s in [0.96, 1.17]
+    const bool aev = plan.fc.aev.x != 0.f;
+    auto k = n20 ? (aev ? k_rowpass2<Tin, Tout, 20, false, RB, true> : k_rowpass2<Tin, Tout, 20, false, RB, false>)
+                 : k_rowpass2<Tin, Tout, 0, false, RB, true>;
     if constexpr (sizeof(Tout) == 4) {
-      if (otma) k = n20 ? k_rowpass2<Tin, Tout, 20, true, RB> : k_rowpass2<Tin, Tout, 0, true, RB>;
+      if (otma)
+        k = n20 ? (aev ? k_rowpass2<Tin, Tout, 20, true, RB, true> : k_rowpass2<Tin, Tout, 20, true, RB, false>)
+                : k_rowpass2<Tin, Tout, 0, true, RB, true>;
     }
     check(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, r2sm),
           "cudaFuncSetAttribute");

@@ -379,7 +379,7 @@ __device__ __forceinline__ unsigned contract_px(const float2* Ts, const Tin* Fs,
 // [16][32] tile and one thread stores it with a TMA tensor store (`omap` =
 // the caller's output), which drains under the next strip's sweeps; else the
 // warps write the tile out row by row.
-template <typename Tin, typename Tout, int NFIX, bool OTMA, int RB = kRowBand>
+template <typename Tin, typename Tout, int NFIX, bool OTMA, int RB = kRowBand, bool AEV = true>
 __global__ void __launch_bounds__(RB == 8 ? 96 : 192, RB == 8 ? 4 : 2) k_rowpass2(const Tin* __restrict__ in_all,
                                                       const double* __restrict__ scalars,
                                                       const float4* __restrict__ CH_all,
@@ -501,14 +501,14 @@ __global__ void __launch_bounds__(RB == 8 ? 96 : 192, RB == 8 ? 4 : 2) k_rowpass
         if ((t & 1) == 1) asm volatile("" ::: "memory");
         const int ca = 31 - t, cc = t;
         if (t < 16) {
-          const float2 ya = ps_emit_a(as, fc);
+          const float2 ya = ps_emit_a<AEV>(as, fc);
           const float2 xa = tl[ca * RB], xc = tl[cc * RB];
           ps_advance_a(as, xa, fc);
           ps_advance_c(cs, xc, fc);
           ya_hi[ca - 16] = ya;
           yc_lo[cc] = ps_emit_c(cs, fc);
         } else {  // the other direction's parked value seeds the emit
-          const float2 ya = ps_emit_a_acc(as, fc, yc_lo[ca]);
+          const float2 ya = ps_emit_a_acc<AEV>(as, fc, yc_lo[ca]);
           const float2 xa = tl[ca * RB], xc = tl[cc * RB];
           ps_advance_a(as, xa, fc);
           ps_advance_c(cs, xc, fc);
@@ -524,7 +524,7 @@ __global__ void __launch_bounds__(RB == 8 ? 96 : 192, RB == 8 ? 4 : 2) k_rowpass
 #pragma unroll
       for (int c = 31; c >= 0; --c) {
         if (c < cols) {
-          ybuf[c] = ps_emit_a(as, fc);
+          ybuf[c] = ps_emit_a<AEV>(as, fc);
           ps_advance_a(as, tl[c * RB], fc);
         }
       }
