@@ -120,7 +120,9 @@ FilterConsts make_filter_consts(double s) {
     const double cv = si * (A.real() * tc - A.imag()), av = si * (B.real() * ta - B.imag());
     if (std::fabs(cv) > 1e-12 * std::abs(A) || (sec == 0 && std::fabs(av) > 1e-12 * std::abs(B)))
       throw Error{9, "sweep basis: unsupported residue (sigma_s " + std::to_string(s) + ")"};
-    if (sec == 1) aev = av;
+    // exactly zero unless B_1's basis was clamped (rounding leaves ~1e-18 otherwise),
+    // so the sweep kernels' no-u2-term instantiation is selected
+    if (sec == 1) aev = std::fabs(av) > 1e-12 * std::abs(B) ? av : 0.0;
     fc.ntau_a[sec] = dup(-ta);
     fc.cgu1[sec] = dup(g.real() - tc * g.imag());
   }
