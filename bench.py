@@ -175,16 +175,16 @@ def algorithmic_flops_per_px(pairs: int) -> dict:
     """FP32 FLOPs each stage issues per pixel (FMA = 2), P = plane pairs.
     One IIR step of one plane in the output-aligned section basis (DESIGN.md
     section 3): two sections advanced, 3 FMA each, in each direction = 24;
-    emits (causal 1 MUL + 1 FMA, anticausal 1 MUL + 2 FMA, one MUL becoming an
-    FMA where the other direction's parked value is added) ~9; i.e. ~33 per
-    plane, 66 per pair. Strip/chunk dot products: 4 FMA per plane.
-    Contraction: 2 FMA + 2 MUL per plane.
+    emits with normalised weights (causal 1 FMA, or ADD + FMA where the other
+    direction's parked value is added; anticausal MUL + FMA, or 2 FMA) ~6;
+    i.e. ~30 per plane, 60 per pair. Strip/chunk dot products: 4 FMA per
+    plane. Contraction: 2 FMA + 2 MUL per plane.
       carries    seeds ~20 + per pair: planes 2 MUL, dots 16          18 P + 20
-      colpass    per pair: planes 2, sweeps 66, row dots 16           84 P
+      colpass    per pair: planes 2, sweeps 60, row dots 16           78 P
       row_scan   per pair: one chain step per 32 pixels              ~P
-      rowpass    per pair: sweeps 66, contraction 12                  78 P + 10"""
-    return {"mean": 1, "col_carry": 18 * pairs + 20, "colpass": 84 * pairs, "row_scan": pairs,
-            "rowpass": 78 * pairs + 10}
+      rowpass    per pair: sweeps 60, contraction 12                  72 P + 10"""
+    return {"mean": 1, "col_carry": 18 * pairs + 20, "colpass": 78 * pairs, "row_scan": pairs,
+            "rowpass": 72 * pairs + 10}
 
 
 def fp32_peak_tflops(peaks: dict) -> float:
