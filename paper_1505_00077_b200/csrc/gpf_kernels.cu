@@ -4,15 +4,18 @@
 //   t_c = mean(f)                                  -> k_mean_partial/final (K0)
 //   N+2 planes F_n = H^n exp(-h^2/2sr^2), each filtered by the separable
 //   4th-order Deriche IIR (spatial.cpp:220-251):
-//     column carries from f                        -> k_col_carry   (K1)
-//     column pass (fused plane generator)          -> k_colpass     (K2)
+//     per-pixel plane seeds (E 2^s0, H 2^-k)       -> k_seed        (K1a)
+//     column carries from the seeds                -> k_col_carry_tma (K1b; k_col_carry_reg /
+//                                                     k_col_carry for larger N)
+//     column pass (fused plane generator)          -> k_colpass_tma (K2; k_colpass for N > 30)
 //     row carries (scan of K2's strip aggregates)  -> k_row_scan    (K3)
-//     row pass + P/Q recombination + normalise     -> k_rowpass     (K4)
+//     row pass + P/Q recombination + normalise     -> k_rowpass2    (K4; k_rowpass for N > 22)
 //   Q = sum c G Fbar_n, P = sum c G Fbar_{n+1}, out = sr P/Q + t_c,
 //   |Q| <= 1e-8 -> input (bilateral.cpp:117-148)
 //
-// Threads own (line, plane pair): a CTA is 32 lines x `pairs` warps. Both
-// passes sweep their lines in chunks of kTile samples: the causal recurrence
+// Threads own (line, plane pair). Both passes sweep their lines in chunks of
+// kTile samples, each complex section in its output-aligned basis
+// (FilterConsts, device_common.cuh): the causal recurrence
 // runs on across chunks; the anticausal one restarts every chunk from an exact
 // carry (the anticausal state at the chunk's far end), so a chunk's two
 // directions combine in registers and every intermediate plane crosses HBM

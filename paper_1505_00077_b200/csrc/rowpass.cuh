@@ -2,8 +2,9 @@
 // the P/Q recombination and normalisation (bilateral.cpp:117-148).
 // Included by gpf_kernels.cu.
 //
-// Warp-specialised TMA pipeline. A CTA owns kRowBand = 16 image rows and walks
-// them strip by strip (32 columns):
+// Two kernels: k_rowpass2 (N <= 22, the default path; further below) and the
+// warp-specialised k_rowpass for larger N, described here. A k_rowpass CTA
+// owns kRowBand = 16 image rows and walks them strip by strip (32 columns):
 //
 //   aux warps (kAux)    : f tile (cp.async) + V tile of strip b+nbuf (one TMA
 //                         box: 16 rows x 32 columns x all pairs) into ring slot
