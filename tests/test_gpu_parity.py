@@ -264,3 +264,18 @@ def test_sigma_s_sweep_basis_edges(gpu, oracle, ss):
     d = np.abs(out - ref).max()
     print(f"sigma_s {ss}: max |gpu - oracle| {d:.2e}")
     assert d <= TOL
+
+
+@pytest.mark.parametrize("sr,ss", [(3.0, 2.0), (3.0, 6.0), (5.0, 2.0), (5.0, 3.0)])
+def test_small_sigma_r(gpu, oracle, sr, ss):
+    """Small sigma_r (H = h / sigma_r up to ~85): planes F_n = H^n E span a huge
+    range across neighbouring pixels, the regime where fp32 rounding inside the
+    filter matters most (DESIGN.md 2). Within the bar down to sigma_r = 3;
+    sigma_r = 1 with sigma_s = 2 exceeds it (tools/small_sr_probe.py)."""
+    img = synth.rects_image(96, 64, 8, 10.0, 77).astype(np.float64)
+    ref, rfb, _ = oracle.gpf(img, ss, sr, 20, threads=4)
+    out, fb = run(gpu, img, ss, sr)
+    assert fb == rfb
+    dmax, din, rel, nout = split_report(out, ref, img)
+    print(f"sr {sr} ss {ss}: max {dmax:.2e} in-range {din:.2e} diverged px {nout}")
+    assert din <= TOL and rel <= 1e-2
