@@ -81,6 +81,42 @@ gpf_status gpf_b200_compare_f32(const float* d_ref, const float* d_test, int wid
 gpf_status gpf_b200_filter_f32_host(gpf_b200_plan* plan, const float* h_in, float* h_out,
                                     int count, long long* h_fallbacks, void* stream);
 
+/* ------------------------------------------------------------------------
+ * Precision of the fp64 drop-in entry gpf_filter_gpf.
+ *
+ *   FP32  the fp32 plane kernels (the throughput path of gpf_b200_filter_f32),
+ *         fp64 input/output and prologue. Held to max |out - reference| <= 1e-3
+ *         on [0,255] while max|H| = max(f_max - t_c, t_c - f_min) / sigma_r <=
+ *         gpf_b200_fp32_h_limit() and degree <= 48.
+ *   FP64  the reference's own fp64 arithmetic replayed on the GPU operation for
+ *         operation (only exp() is CUDA's rather than glibc's): follows the
+ *         reference also where its degree-N series is ill-conditioned and its
+ *         output leaves the input range (BASELINE C2/C5). Degree <= 62; about
+ *         (degree + 2) x 16 B of extra device memory per pixel.
+ *   AUTO  (default; environment GPF_B200_PRECISION=auto|fp32|fp64 sets the
+ *         initial mode) measures t_c, f_min and f_max on the device and runs
+ *         FP64 outside the FP32 envelope, FP32 inside it.
+ * The mode is process-global; gpf_b200_last_precision() reports (per calling
+ * thread) which one the last gpf_filter_gpf call ran, and
+ * gpf_b200_last_max_abs_h() the max|H| it measured (AUTO only, else 0).
+ * ---------------------------------------------------------------------- */
+typedef enum gpf_b200_precision {
+  GPF_B200_PRECISION_AUTO = 0,
+  GPF_B200_PRECISION_FP32 = 1,
+  GPF_B200_PRECISION_FP64 = 2
+} gpf_b200_precision;
+
+gpf_status gpf_b200_set_precision(int mode);
+int gpf_b200_get_precision(void);
+int gpf_b200_last_precision(void);
+double gpf_b200_last_max_abs_h(void);
+double gpf_b200_fp32_h_limit(void);
+
+/* gpf_filter_gpf keeps, per device, up to four fp32 plans (keyed by every
+ * filter parameter), the fp64 workspace and its device buffers between calls,
+ * so repeated calls allocate nothing. This frees all of it. */
+void gpf_b200_dropin_release(void);
+
 #ifdef __cplusplus
 } /* extern "C" */
 #endif

@@ -39,7 +39,12 @@ EXPORTED = (
     "gpf_b200_plan_set_profiling", "gpf_b200_plan_stage_times", "gpf_b200_plan_workspace_bytes",
     "gpf_b200_plan_launches_per_frame", "gpf_b200_filter_f32", "gpf_b200_filter_f32_ev",
     "gpf_b200_filter_f32_host", "gpf_b200_exact_f32", "gpf_b200_compare_f32",
+    "gpf_b200_set_precision", "gpf_b200_get_precision", "gpf_b200_last_precision",
+    "gpf_b200_last_max_abs_h", "gpf_b200_fp32_h_limit", "gpf_b200_dropin_release",
 )
+
+# gpf_b200_precision (include/gpfilter/gpfilter_b200.h)
+PRECISION_AUTO, PRECISION_FP32, PRECISION_FP64 = 0, 1, 2
 
 
 class SpatialParams(C.Structure):
@@ -61,7 +66,7 @@ class RangeParams(C.Structure):
 
 def build() -> None:
     """Compile libgpfilter_b200.so for sm_100a (nvcc cross-compiles; no GPU needed)."""
-    subprocess.run(["make", "-s", "-C", PKG_DIR], check=True)
+    subprocess.run(["make", "-s", "-j8", "-C", PKG_DIR], check=True)
 
 
 def _declare(lib: C.CDLL) -> C.CDLL:
@@ -109,6 +114,9 @@ def _declare(lib: C.CDLL) -> C.CDLL:
     lib.gpf_b200_filter_f32.argtypes = [vp, vp, vp, C.c_int, vp, vp]
     lib.gpf_b200_filter_f32_ev.argtypes = [vp, vp, vp, C.c_int, vp, vp, vp]
     lib.gpf_b200_filter_f32_host.argtypes = [vp, vp, vp, C.c_int, C.POINTER(C.c_longlong), vp]
+    lib.gpf_b200_set_precision.argtypes = [C.c_int]
+    lib.gpf_b200_last_max_abs_h.restype = C.c_double
+    lib.gpf_b200_fp32_h_limit.restype = C.c_double
     return lib
 
 

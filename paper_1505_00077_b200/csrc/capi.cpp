@@ -11,7 +11,10 @@
 #include <cmath>
 #include <cstring>
 #include <atomic>
+#include <map>
 #include <memory>
+#include <list>
+#include <cstdlib>
 #include <mutex>
 #include <new>
 #include <string>
@@ -24,9 +27,86 @@
 #include "pgm.h"
 #include "gpfilter/gpfilter_b200.h"
 
+// Image storage. Frames of 4 MiB and more live in page-locked host memory
+// (cudaMallocHost, recycled through a small pool) so that the drop-in entry's
+// copies run at full PCIe speed instead of through the driver's pageable
+// staging; smaller ones (and any image on a machine without a CUDA device) use
+// ordinary heap memory. The layout the caller sees is the reference's:
+// row-major doubles (proj/src/core/image.hpp:14-41).
+namespace {
+constexpr size_t kPinnedMinBytes = size_t(4) << 20;
+constexpr size_t kPinnedPoolBytes = size_t(8) << 30;
+
+struct HostPool {
+  std::mutex mu;
+  std::multimap<size_t, void*> free_blocks;  // bytes -> block
+  size_t pooled = 0;
+};
+HostPool& host_pool() {
+  static HostPool* p = new HostPool();  // never destroyed: blocks may outlive static teardown
+  return *p;
+}
+
+double* host_alloc(size_t n, bool& pinned) {
+  const size_t bytes = std::max<size_t>(n, 1) * sizeof(double);
+  pinned = false;
+  if (bytes >= kPinnedMinBytes) {
+    HostPool& hp = host_pool();
+    {
+      std::lock_guard<std::mutex> lock(hp.mu);
+      auto it = hp.free_blocks.lower_bound(bytes);
+      if (it != hp.free_blocks.end() && it->first <= 2 * bytes) {
+        void* b = it->second;
+        hp.pooled -= it->first;
+        hp.free_blocks.erase(it);
+        pinned = true;
+        // remember the block's real size in front of the data
+        return static_cast<double*>(b) + 1;
+      }
+    }
+    void* b = nullptr;
+    if (cudaMallocHost(&b, bytes + sizeof(double)) == cudaSuccess) {
+      *static_cast<size_t*>(b) = bytes;
+      pinned = true;
+      return static_cast<double*>(b) + 1;
+    }
+    cudaGetLastError();  // no device / pinned memory exhausted: pageable storage
+  }
+  auto* d = static_cast<double*>(std::malloc(bytes));
+  if (!d) throw std::bad_alloc();
+  return d;
+}
+
+void host_free(double* d, bool pinned) {
+  if (!d) return;
+  if (!pinned) {
+    std::free(d);
+    return;
+  }
+  void* b = d - 1;
+  const size_t bytes = *static_cast<size_t*>(b);
+  HostPool& hp = host_pool();
+  {
+    std::lock_guard<std::mutex> lock(hp.mu);
+    if (hp.pooled + bytes <= kPinnedPoolBytes) {
+      hp.free_blocks.emplace(bytes, b);
+      hp.pooled += bytes;
+      return;
+    }
+  }
+  cudaFreeHost(b);
+}
+}  // namespace
+
 struct gpf_image {
-  int w, h;
-  std::vector<double> data;
+  int w = 0, h = 0;
+  double* px = nullptr;
+  bool pinned = false;
+  gpf_image(int w_, int h_) : w(w_), h(h_) { px = host_alloc((size_t)w * h, pinned); }
+  ~gpf_image() { host_free(px, pinned); }
+  gpf_image(const gpf_image&) = delete;
+  gpf_image& operator=(const gpf_image&) = delete;
+  size_t n() const { return (size_t)w * h; }
 };
 
 struct gpf_b200_plan {
@@ -76,7 +156,7 @@ gpf_status guarded(Fn&& fn) {
 
 // Validation of the GPF path, in the reference's order.
 gpfb::Params validate(int w, int h, const gpf_spatial_params& sp, const gpf_range_params& rp,
-                      gpf_backend backend, int centering) {
+                      gpf_backend backend, int centering, int max_degree) {
   // to_spatial (capi.cpp:65-80): boundary enum checked even though unused.
   if (sp.boundary != GPF_BOUNDARY_REPLICATE && sp.boundary != GPF_BOUNDARY_REFLECT &&
       sp.boundary != GPF_BOUNDARY_ZERO)
@@ -99,8 +179,10 @@ gpfb::Params validate(int w, int h, const gpf_spatial_params& sp, const gpf_rang
   if (sp.sigma_s < 0.5)
     throw gpfb::Error{GPF_ERR_SIGMA_TOO_SMALL,
                       "recursive_gaussian: sigma_s < 0.5 is not supported; use the direct backend"};
-  if (rp.degree + 2 > gpfb::kMaxPlanes)
-    invalid("RangeParams: degree must be <= 62 in the B200 library");
+  if (rp.degree > max_degree)
+    invalid("RangeParams: degree must be <= " + std::to_string(max_degree) +
+            (max_degree == gpfb::kMaxDegreeF64 ? " in the B200 library"
+                                               : " for the fp32 plan entries of the B200 library"));
   if (w < 1 || h < 1) invalid("Image dimensions must be >= 1");
   gpfb::Params p;
   p.width = w;
@@ -220,15 +302,17 @@ gpf_status gpf_image_create(int width, int height, gpf_image** out) {
   *out = nullptr;
   if (width < 1 || height < 1) return fail(GPF_ERR_INVALID_ARGUMENT, "Image dimensions must be >= 1");
   return guarded([&] {
-    *out = new gpf_image{width, height, std::vector<double>((size_t)width * height, 0.0)};
+    auto* img = new gpf_image(width, height);
+    std::memset(img->px, 0, img->n() * sizeof(double));
+    *out = img;
   });
 }
 
 void gpf_image_destroy(gpf_image* img) { delete img; }
 int gpf_image_width(const gpf_image* img) { return img ? img->w : 0; }
 int gpf_image_height(const gpf_image* img) { return img ? img->h : 0; }
-double* gpf_image_data(gpf_image* img) { return img ? img->data.data() : nullptr; }
-const double* gpf_image_cdata(const gpf_image* img) { return img ? img->data.data() : nullptr; }
+double* gpf_image_data(gpf_image* img) { return img ? img->px : nullptr; }
+const double* gpf_image_cdata(const gpf_image* img) { return img ? img->px : nullptr; }
 
 void gpf_spatial_params_init(gpf_spatial_params* sp) {
   if (!sp) return;
@@ -251,36 +335,14 @@ gpf_status gpf_filter_gpf(const gpf_image* in, const gpf_spatial_params* sp,
     return fail(GPF_ERR_INVALID_ARGUMENT, "null argument");
   *out = nullptr;
   return guarded([&] {
-    const gpfb::Params p = validate(in->w, in->h, *sp, *rp, backend, centering);
-    const int dev = current_device();
-    const size_t n = (size_t)p.width * p.height;
-    PlanGuard g;
-    gpfb::plan_init(g.plan, p, dev);
-    g.live = true;
-    DevBuf din(n * sizeof(double)), dout(n * sizeof(double)), dfb(sizeof(unsigned long long));
-    cudaStream_t st;
-    cuda_check(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking), "cudaStreamCreate");
-    struct StreamGuard {
-      cudaStream_t s;
-      ~StreamGuard() { cudaStreamDestroy(s); }
-    } sg{st};
-    cuda_check(cudaMemcpyAsync(din.p, in->data.data(), n * sizeof(double), cudaMemcpyHostToDevice, st),
-               "cudaMemcpyAsync(H2D)");
-    cuda_check(cudaMemsetAsync(dfb.p, 0, sizeof(unsigned long long), st), "cudaMemsetAsync");
-    gpfb::run_frames_f64(g.plan, static_cast<const double*>(din.p), static_cast<double*>(dout.p), 1,
-                         static_cast<unsigned long long*>(dfb.p), st);
-    auto* res = new gpf_image{p.width, p.height, std::vector<double>(n)};
+    const gpfb::Params p = validate(in->w, in->h, *sp, *rp, backend, centering, gpfb::kMaxDegreeF64);
+    auto* res = new gpf_image(p.width, p.height);
     std::unique_ptr<gpf_image> hold(res);
-    unsigned long long fb = 0;
-    cuda_check(cudaMemcpyAsync(res->data.data(), dout.p, n * sizeof(double), cudaMemcpyDeviceToHost, st),
-               "cudaMemcpyAsync(D2H)");
-    cuda_check(cudaMemcpyAsync(&fb, dfb.p, sizeof(fb), cudaMemcpyDeviceToHost, st), "cudaMemcpyAsync(D2H)");
-    cuda_check(cudaStreamSynchronize(st), "cudaStreamSynchronize");
-    if (fallback_count != nullptr) *fallback_count = static_cast<long long>(fb);
+    const long long fb = gpfb::dropin_gpf(in->px, res->px, p);
+    if (fallback_count != nullptr) *fallback_count = fb;
     *out = hold.release();
   });
 }
-
 gpf_status gpf_gaussian_recursive(const gpf_image* in, double sigma_s, double kernel_scale,
                                   gpf_image** out) {
   if (in == nullptr || out == nullptr) return fail(GPF_ERR_INVALID_ARGUMENT, "null argument");
@@ -295,14 +357,14 @@ gpf_status gpf_gaussian_recursive(const gpf_image* in, double sigma_s, double ke
     current_device();
     const size_t n = (size_t)in->w * in->h;
     DevBuf din(n * sizeof(double)), dout(n * sizeof(double)), dtmp(n * sizeof(double));
-    cuda_check(cudaMemcpy(din.p, in->data.data(), n * sizeof(double), cudaMemcpyHostToDevice), "H2D");
+    cuda_check(cudaMemcpy(din.p, in->px, n * sizeof(double), cudaMemcpyHostToDevice), "H2D");
     const double mass = gpfb::kernel_mass_1d(sigma_s, gpfb::default_window_radius(sigma_s));
     gpfb::run_gaussian_f64(static_cast<const double*>(din.p), static_cast<double*>(dout.p),
                            static_cast<double*>(dtmp.p), in->w, in->h, sigma_s,
                            mass * mass * kernel_scale, nullptr);
-    auto* res = new gpf_image{in->w, in->h, std::vector<double>(n)};
+    auto* res = new gpf_image(in->w, in->h);
     std::unique_ptr<gpf_image> hold(res);
-    cuda_check(cudaMemcpy(res->data.data(), dout.p, n * sizeof(double), cudaMemcpyDeviceToHost), "D2H");
+    cuda_check(cudaMemcpy(res->px, dout.p, n * sizeof(double), cudaMemcpyDeviceToHost), "D2H");
     *out = hold.release();
   });
 }
@@ -314,18 +376,18 @@ gpf_status gpf_filter_taylor(const gpf_image* in, const gpf_spatial_params* sp,
     return fail(GPF_ERR_INVALID_ARGUMENT, "null argument");
   *out = nullptr;
   return guarded([&] {
-    const gpfb::Params p = validate(in->w, in->h, *sp, *rp, backend, 0);
+    const gpfb::Params p = validate(in->w, in->h, *sp, *rp, backend, 0, 1 << 20);
     current_device();
     const size_t n = (size_t)in->w * in->h;
     DevBuf din(n * sizeof(double)), dout(n * sizeof(double)), dfb(sizeof(unsigned long long));
-    cuda_check(cudaMemcpy(din.p, in->data.data(), n * sizeof(double), cudaMemcpyHostToDevice), "H2D");
+    cuda_check(cudaMemcpy(din.p, in->px, n * sizeof(double), cudaMemcpyHostToDevice), "H2D");
     gpfb::run_taylor_f64(static_cast<const double*>(din.p), static_cast<double*>(dout.p), in->w, in->h,
                          p.sigma_s, p.kernel_scale, p.sigma_r, p.degree,
                          static_cast<unsigned long long*>(dfb.p), nullptr);
-    auto* res = new gpf_image{in->w, in->h, std::vector<double>(n)};
+    auto* res = new gpf_image(in->w, in->h);
     std::unique_ptr<gpf_image> hold(res);
     unsigned long long fb = 0;
-    cuda_check(cudaMemcpy(res->data.data(), dout.p, n * sizeof(double), cudaMemcpyDeviceToHost), "D2H");
+    cuda_check(cudaMemcpy(res->px, dout.p, n * sizeof(double), cudaMemcpyDeviceToHost), "D2H");
     cuda_check(cudaMemcpy(&fb, dfb.p, sizeof(fb), cudaMemcpyDeviceToHost), "D2H");
     if (fallback_count) *fallback_count = static_cast<long long>(fb);
     *out = hold.release();
@@ -342,12 +404,12 @@ gpf_status gpf_filter_exact(const gpf_image* in, const gpf_spatial_params* sp,
     current_device();
     const size_t n = (size_t)in->w * in->h;
     DevBuf din(n * sizeof(double)), dout(n * sizeof(double));
-    cuda_check(cudaMemcpy(din.p, in->data.data(), n * sizeof(double), cudaMemcpyHostToDevice), "H2D");
+    cuda_check(cudaMemcpy(din.p, in->px, n * sizeof(double), cudaMemcpyHostToDevice), "H2D");
     gpfb::run_exact_f64(static_cast<const double*>(din.p), static_cast<double*>(dout.p), in->w, in->h,
                         1, W, static_cast<int>(sp->boundary), sp->sigma_s, rp->sigma_r, nullptr);
-    auto* res = new gpf_image{in->w, in->h, std::vector<double>(n)};
+    auto* res = new gpf_image(in->w, in->h);
     std::unique_ptr<gpf_image> hold(res);
-    cuda_check(cudaMemcpy(res->data.data(), dout.p, n * sizeof(double), cudaMemcpyDeviceToHost), "D2H");
+    cuda_check(cudaMemcpy(res->px, dout.p, n * sizeof(double), cudaMemcpyDeviceToHost), "D2H");
     *out = hold.release();
   });
 }
@@ -362,8 +424,8 @@ gpf_status gpf_compare(const gpf_image* ref, const gpf_image* test, int exclude_
     current_device();
     const size_t n = (size_t)ref->w * ref->h;
     DevBuf da(n * sizeof(double)), db(n * sizeof(double));
-    cuda_check(cudaMemcpy(da.p, ref->data.data(), n * sizeof(double), cudaMemcpyHostToDevice), "H2D");
-    cuda_check(cudaMemcpy(db.p, test->data.data(), n * sizeof(double), cudaMemcpyHostToDevice), "H2D");
+    cuda_check(cudaMemcpy(da.p, ref->px, n * sizeof(double), cudaMemcpyHostToDevice), "H2D");
+    cuda_check(cudaMemcpy(db.p, test->px, n * sizeof(double), cudaMemcpyHostToDevice), "H2D");
     fill_report(gpfb::compare_f64(static_cast<const double*>(da.p), static_cast<const double*>(db.p),
                                   ref->w, ref->h, exclude_border, nullptr),
                 out);
@@ -373,7 +435,9 @@ gpf_status gpf_compare(const gpf_image* ref, const gpf_image* test, int exclude_
 // ----------------------------------------------------------------- PGM I/O
 namespace {
 void deliver_pgm(gpfb::pgm::Decoded&& d, gpf_image** out) {
-  *out = new gpf_image{d.w, d.h, std::move(d.pixels)};
+  auto* img = new gpf_image(d.w, d.h);
+  std::memcpy(img->px, d.pixels.data(), img->n() * sizeof(double));
+  *out = img;
 }
 }  // namespace
 
@@ -394,7 +458,7 @@ gpf_status gpf_decode_pgm(const uint8_t* bytes, size_t size, gpf_image** out) {
 
 gpf_status gpf_write_pgm(const gpf_image* img, const char* path) {
   if (img == nullptr || path == nullptr) return fail(GPF_ERR_INVALID_ARGUMENT, "null argument");
-  return guarded([&] { gpfb::pgm::write_file(path, gpfb::pgm::encode(img->data.data(), img->w, img->h)); });
+  return guarded([&] { gpfb::pgm::write_file(path, gpfb::pgm::encode(img->px, img->w, img->h)); });
 }
 
 gpf_status gpf_encode_pgm(const gpf_image* img, uint8_t** bytes, size_t* size) {
@@ -403,7 +467,7 @@ gpf_status gpf_encode_pgm(const gpf_image* img, uint8_t** bytes, size_t* size) {
   *bytes = nullptr;
   *size = 0;
   return guarded([&] {
-    const std::vector<uint8_t> buf = gpfb::pgm::encode(img->data.data(), img->w, img->h);
+    const std::vector<uint8_t> buf = gpfb::pgm::encode(img->px, img->w, img->h);
     auto* mem = new uint8_t[buf.size()];
     std::memcpy(mem, buf.data(), buf.size());
     *bytes = mem;
@@ -412,6 +476,20 @@ gpf_status gpf_encode_pgm(const gpf_image* img, uint8_t** bytes, size_t* size) {
 }
 
 void gpf_free_bytes(uint8_t* bytes) { delete[] bytes; }
+
+gpf_status gpf_b200_set_precision(int mode) {
+  if (mode != GPF_B200_PRECISION_AUTO && mode != GPF_B200_PRECISION_FP32 &&
+      mode != GPF_B200_PRECISION_FP64)
+    return fail(GPF_ERR_INVALID_ARGUMENT, "precision must be AUTO, FP32 or FP64");
+  gpfb::set_precision(mode);
+  return GPF_OK;
+}
+
+int gpf_b200_get_precision(void) { return gpfb::get_precision(); }
+int gpf_b200_last_precision(void) { return gpfb::last_precision(); }
+double gpf_b200_last_max_abs_h(void) { return gpfb::last_max_abs_h(); }
+double gpf_b200_fp32_h_limit(void) { return gpfb::kH32Limit; }
+void gpf_b200_dropin_release(void) { gpfb::dropin_release(); }
 
 gpf_status gpf_set_num_threads(int n) {
   if (n < 1) return fail(GPF_ERR_INVALID_ARGUMENT, "thread count must be >= 1");
@@ -429,12 +507,15 @@ gpf_status gpf_b200_plan_create(int width, int height, const gpf_spatial_params*
     return fail(GPF_ERR_INVALID_ARGUMENT, "null argument");
   *out = nullptr;
   return guarded([&] {
-    const gpfb::Params p = validate(width, height, *sp, *rp, GPF_BACKEND_RECURSIVE, centering);
-    int dev = current_device();
-    if (device >= 0) {
-      cuda_check(cudaSetDevice(device), "cudaSetDevice");
-      dev = device;
-    }
+    const gpfb::Params p =
+        validate(width, height, *sp, *rp, GPF_BACKEND_RECURSIVE, centering, gpfb::kMaxDegreeF32);
+    const int prev = current_device();
+    const int dev = device >= 0 ? device : prev;
+    struct Restore {  // the caller's current device is left as it was
+      int d;
+      ~Restore() { cudaSetDevice(d); }
+    } restore{prev};
+    cuda_check(cudaSetDevice(dev), "cudaSetDevice");
     auto* pl = new gpf_b200_plan();
     std::unique_ptr<gpf_b200_plan> hold(pl);
     gpfb::plan_init(pl->plan, p, dev);
@@ -467,12 +548,23 @@ gpf_status gpf_b200_plan_set_batch(gpf_b200_plan* plan, int frames) {
   if (plan == nullptr) return fail(GPF_ERR_INVALID_ARGUMENT, "null argument");
   if (frames < 1) return fail(GPF_ERR_INVALID_ARGUMENT, "frames must be >= 1");
   return guarded([&] {
+    int prev = 0;
+    cuda_check(cudaGetDevice(&prev), "cudaGetDevice");
+    struct Restore {
+      int d;
+      ~Restore() { cudaSetDevice(d); }
+    } restore{prev};
     cuda_check(cudaSetDevice(plan->plan.device), "cudaSetDevice");
     cuda_check(cudaDeviceSynchronize(), "cudaDeviceSynchronize");
-    const gpfb::Params p = plan->plan.p;
-    const int dev = plan->plan.device;
+    // Build the new workspace first; the plan keeps its old one (and stays
+    // usable) if that fails, e.g. when the batch does not fit in HBM.
+    gpfb::Plan fresh;
+    gpfb::plan_init(fresh, plan->plan.p, plan->plan.device, frames);
+    fresh.profile = plan->plan.profile;
+    fresh.timer = plan->plan.timer;
+    plan->plan.timer = nullptr;
     gpfb::plan_free(plan->plan);
-    gpfb::plan_init(plan->plan, p, dev, frames);
+    plan->plan = fresh;
   });
 }
 

@@ -169,6 +169,7 @@ RangeConsts make_range_consts(const Params& p) {
   rc.planes = p.degree + 2;
   rc.pairs = (rc.planes + 1) / 2;
   rc.centering = p.centering;
+  rc.tc_fixed = p.tc_fixed;
   // Plane scaling s_n = s0 - k n. |F_n| = |H^n exp(-H^2/2)| <= (n/e)^(n/2);
   // pick the smallest k that keeps the last (padded) plane at or below 2^s0.
   const int n_max = 2 * rc.pairs - 1;

@@ -1,0 +1,250 @@
+// Drop-in fp64 host entry of the GPF path: the engine behind gpf_filter_gpf
+// (proj/src/capi.cpp:176-192) and gpfilter::gpf (proj/src/core/bilateral.hpp:73-75).
+//
+// The reference call takes a host image of doubles and returns a new one. Here
+// one call = H2D of the frame, the filter on the GPU, D2H of the result, with
+// everything the call needs kept per device between calls:
+//   * an LRU of fp32 plans keyed by every filter parameter (a repeated call
+//     with the same shape and parameters performs no cudaMalloc and no
+//     tensor-map encode),
+//   * the fp64 precision mode's workspace, device in/out buffers, the fallback
+//     counter, a pinned scalar readback slot and a non-blocking stream.
+// Calls on one device are serialised by the context's mutex (each call fills
+// the GPU on its own); the host images of the C ABI are page-locked
+// (capi.cpp), so the copies run at PCIe speed.
+//
+// Precision: the fp32 plane kernels follow the reference within
+// 1e-3 inside a validated envelope of max |H| = max(f_max - t_c, t_c - f_min)
+// / sigma_r; outside it the reference's own degree-N series is ill-conditioned
+// (its outputs leave the input range, up to 1e5 on BASELINE C5) and only an fp64
+// replay of its arithmetic can follow it. AUTO measures t_c, f_min and f_max
+// on the device first and picks the fp64 replay outside the envelope.
+#include <atomic>
+#include <cmath>
+#include <cstdlib>
+#include <cstring>
+#include <list>
+#include <memory>
+#include <mutex>
+#include <string>
+#include <vector>
+
+#include <cuda_runtime.h>
+
+#include "gpf_internal.h"
+
+namespace gpfb {
+
+// Largest max|H| at which the fp32 kernels are held to the 1e-3 bar against
+// the reference (tests/test_gpu_fullsize.py).
+const double kH32Limit = 6.0;
+
+namespace {
+
+constexpr int kDropinPlans = 4;  // cached fp32 plans per device
+constexpr int kStatBlocks = 592;
+
+std::atomic<int> g_precision{-1};
+thread_local int t_last_precision = 0;
+thread_local double t_last_hmax = 0.0;
+
+void chk(cudaError_t e, const char* what) {
+  if (e != cudaSuccess) throw Error{9, std::string(what) + ": " + cudaGetErrorString(e)};
+}
+
+int precision_from_env() {
+  const char* e = std::getenv("GPF_B200_PRECISION");
+  if (!e) return kPrecAuto;
+  const std::string v(e);
+  if (v == "fp32") return kPrecFp32;
+  if (v == "fp64") return kPrecFp64;
+  return kPrecAuto;
+}
+
+bool same_params(const Params& a, const Params& b) {
+  return a.width == b.width && a.height == b.height && a.sigma_s == b.sigma_s &&
+         a.kernel_scale == b.kernel_scale && a.sigma_r == b.sigma_r && a.degree == b.degree &&
+         a.centering == b.centering && (a.centering != 2 || a.tc_fixed == b.tc_fixed);
+}
+
+struct DevCtx {
+  std::mutex mu;
+  int device = 0;
+  std::list<std::unique_ptr<Plan>> plans;  // most recently used first
+  F64Work f64;
+  double* din = nullptr;
+  double* dout = nullptr;
+  size_t cap = 0;  // pixels
+  unsigned long long* dfb = nullptr;
+  double* dscal = nullptr;  // [4] scalars + [2 * kStatBlocks] partials
+  double* hscal = nullptr;  // pinned: t_c, min, max, fallbacks
+  cudaStream_t st = nullptr;
+
+  void free_plans() {
+    for (auto& p : plans) plan_free(*p);
+    plans.clear();
+  }
+  void free_buffers() {
+    cudaFree(din);
+    cudaFree(dout);
+    din = dout = nullptr;
+    cap = 0;
+  }
+  void release_all() {
+    free_plans();
+    f64.release();
+    free_buffers();
+  }
+};
+
+std::mutex g_ctx_mu;
+std::vector<DevCtx*>& contexts() {
+  static auto* v = new std::vector<DevCtx*>();  // never destroyed (process-lifetime CUDA objects)
+  return *v;
+}
+
+DevCtx& context(int dev) {
+  std::lock_guard<std::mutex> lock(g_ctx_mu);
+  auto& v = contexts();
+  if ((int)v.size() <= dev) v.resize(dev + 1, nullptr);
+  if (!v[dev]) {
+    v[dev] = new DevCtx();
+    v[dev]->device = dev;
+  }
+  return *v[dev];
+}
+
+int current_device() {
+  int n = 0;
+  if (cudaGetDeviceCount(&n) != cudaSuccess || n == 0) {
+    cudaGetLastError();
+    throw Error{9, "no CUDA device available (the B200 library has no CPU path)"};
+  }
+  int d = 0;
+  chk(cudaGetDevice(&d), "cudaGetDevice");
+  return d;
+}
+
+// Runs `fn`; on an allocation failure frees everything cached on the device
+// and tries once more.
+template <typename Fn>
+void with_retry(DevCtx& c, Fn&& fn) {
+  try {
+    fn();
+  } catch (const Error&) {
+    cudaGetLastError();
+    chk(cudaStreamSynchronize(c.st), "cudaStreamSynchronize");
+    c.free_plans();
+    c.f64.release();
+    fn();
+  }
+}
+
+Plan& cached_plan(DevCtx& c, const Params& p) {
+  for (auto it = c.plans.begin(); it != c.plans.end(); ++it)
+    if (same_params((*it)->p, p)) {
+      c.plans.splice(c.plans.begin(), c.plans, it);
+      return *c.plans.front();
+    }
+  if ((int)c.plans.size() >= kDropinPlans) {
+    chk(cudaStreamSynchronize(c.st), "cudaStreamSynchronize");
+    plan_free(*c.plans.back());
+    c.plans.pop_back();
+  }
+  auto pl = std::make_unique<Plan>();
+  with_retry(c, [&] { plan_init(*pl, p, c.device); });
+  c.plans.push_front(std::move(pl));
+  return *c.plans.front();
+}
+
+}  // namespace
+
+void set_precision(int mode) { g_precision.store(mode); }
+
+int get_precision() {
+  int m = g_precision.load();
+  if (m < 0) {
+    int expected = -1;
+    g_precision.compare_exchange_strong(expected, precision_from_env());
+    m = g_precision.load();
+  }
+  return m;
+}
+
+int last_precision() { return t_last_precision; }
+double last_max_abs_h() { return t_last_hmax; }
+
+long long dropin_gpf(const double* h_in, double* h_out, const Params& p) {
+  const int dev = current_device();
+  DevCtx& c = context(dev);
+  std::lock_guard<std::mutex> lock(c.mu);
+  const long long n = (long long)p.width * p.height;
+  if (!c.st) {
+    chk(cudaStreamCreateWithFlags(&c.st, cudaStreamNonBlocking), "cudaStreamCreate");
+    chk(cudaMalloc(&c.dfb, sizeof(unsigned long long)), "cudaMalloc");
+    chk(cudaMalloc(&c.dscal, sizeof(double) * (4 + 2 * kStatBlocks)), "cudaMalloc");
+    chk(cudaMallocHost(&c.hscal, sizeof(double) * 4), "cudaMallocHost");
+  }
+  if ((size_t)n > c.cap) {
+    c.free_buffers();
+    with_retry(c, [&] {
+      c.free_buffers();
+      chk(cudaMalloc(&c.din, sizeof(double) * n), "cudaMalloc(input)");
+      chk(cudaMalloc(&c.dout, sizeof(double) * n), "cudaMalloc(output)");
+      c.cap = (size_t)n;
+    });
+  }
+  chk(cudaMemcpyAsync(c.din, h_in, sizeof(double) * n, cudaMemcpyHostToDevice, c.st), "H2D");
+  int mode = get_precision();
+  double hmax = 0.0;
+  if (mode == kPrecFp32 && p.degree > kMaxDegreeF32)
+    throw Error{1, "RangeParams: degree must be <= " + std::to_string(kMaxDegreeF32) +
+                       " with the fp32 precision mode"};
+  if (mode == kPrecAuto) {
+    if (p.degree > kMaxDegreeF32) {
+      mode = kPrecFp64;
+    } else {
+      double* partials = c.dscal + 4;
+      launch_mean_f64(c.din, n, p.centering, p.tc_fixed, partials, kStatBlocks, c.dscal, c.st);
+      launch_minmax_f64(c.din, n, partials, kStatBlocks, c.dscal, c.st);
+      chk(cudaMemcpyAsync(c.hscal, c.dscal, sizeof(double) * 3, cudaMemcpyDeviceToHost, c.st), "D2H");
+      chk(cudaStreamSynchronize(c.st), "cudaStreamSynchronize");
+      const double tc = c.hscal[0], lo = c.hscal[1], hi = c.hscal[2];
+      hmax = std::max(hi - tc, tc - lo) / p.sigma_r;
+      mode = (hmax > kH32Limit || std::isnan(hmax)) ? kPrecFp64 : kPrecFp32;
+    }
+  }
+  chk(cudaMemsetAsync(c.dfb, 0, sizeof(unsigned long long), c.st), "cudaMemsetAsync");
+  if (mode == kPrecFp64) {
+    with_retry(c, [&] { c.f64.ensure(f64_workspace_bytes(p.width, p.height, p.degree)); });
+    run_gpf_f64_exact(c.din, c.dout, p, c.f64, c.dfb, c.st);
+  } else {
+    Plan& pl = cached_plan(c, p);
+    run_frames_f64(pl, c.din, c.dout, 1, c.dfb, c.st);
+  }
+  chk(cudaMemcpyAsync(h_out, c.dout, sizeof(double) * n, cudaMemcpyDeviceToHost, c.st), "D2H");
+  chk(cudaMemcpyAsync(c.hscal + 3, c.dfb, sizeof(unsigned long long), cudaMemcpyDeviceToHost, c.st),
+      "D2H");
+  chk(cudaStreamSynchronize(c.st), "cudaStreamSynchronize");
+  t_last_precision = mode;
+  t_last_hmax = hmax;
+  unsigned long long fb;
+  std::memcpy(&fb, c.hscal + 3, sizeof(fb));
+  return static_cast<long long>(fb);
+}
+
+void dropin_release() {
+  std::lock_guard<std::mutex> lock(g_ctx_mu);
+  for (DevCtx* c : contexts()) {
+    if (!c) continue;
+    std::lock_guard<std::mutex> l2(c->mu);
+    int prev = 0;
+    cudaGetDevice(&prev);
+    cudaSetDevice(c->device);
+    if (c->st) cudaStreamSynchronize(c->st);
+    c->release_all();
+    cudaSetDevice(prev);
+  }
+}
+
+}  // namespace gpfb

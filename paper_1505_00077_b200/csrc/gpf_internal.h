@@ -11,6 +11,8 @@
 namespace gpfb {
 
 constexpr int kMaxPlanes = 64;  // N+2 <= 64  (degree <= 62)
+constexpr int kMaxDegreeF32 = 48;  // fp32 plane kernels (shared memory per CTA)
+constexpr int kMaxDegreeF64 = 62;  // reference-exact fp64 mode
 constexpr int kTile = 32;       // rows per column-pass chunk == columns per row-pass chunk
 
 // Per-call constants of the filter, computed on the host in fp64 from the
@@ -85,13 +87,15 @@ struct RangeConsts {
   int planes;         // N + 2
   int pairs;          // ceil(planes / 2)
   int degree;         // N
-  int centering;      // 0 / 1 (mean)
+  int centering;      // 0 none / 1 mean / 2 fixed t_c (midpoint)
+  double tc_fixed;    // t_c for centering 2
 };
 
 struct Params {
   int width = 0, height = 0;
   double sigma_s = 2.0, kernel_scale = 1.0, sigma_r = 30.0;
-  int degree = 20, centering = 1;
+  int degree = 20, centering = 1;  // centering: 0 none, 1 mean, 2 fixed t_c = tc_fixed
+  double tc_fixed = 0.0;           // CenteringMode::midpoint: (range.low + range.high) / 2
 };
 
 // Host-side constant builders (coeffs.cpp).
@@ -177,6 +181,46 @@ ErrorStats compare_f64(const double* d_ref, const double* d_test, int w, int h, 
 void run_taylor_f64(const double* d_in, double* d_out, int w, int h, double sigma_s,
                     double kernel_scale, double sigma_r, int degree, unsigned long long* d_fb,
                     cudaStream_t st);
+// t_c of one fp64 frame (K0 double-double mean; 0 / tc_fixed per centering) into
+// scalars[0]; partials holds 2*blocks doubles.
+void launch_mean_f64(const double* d_in, long long n, int centering, double tc_fixed,
+                     double* partials, int blocks, double* scalars, cudaStream_t st);
+// scalars[1], scalars[2] = min, max of the frame (the conditioning check of the
+// drop-in entry; scalars[0] = t_c from launch_mean_f64).
+void launch_minmax_f64(const double* d_in, long long n, double* partials, int blocks,
+                       double* scalars, cudaStream_t st);
+
+// Reference-exact fp64 GPF (gpf_f64.cu): the reference's own fp64 operation
+// sequence replayed on the GPU, for inputs whose degree-N series is too
+// ill-conditioned for fp32 planes. Workspace grown on demand and reused.
+constexpr int kF64MeanBlocks = 592;
+struct F64Work {
+  double* base = nullptr;
+  size_t cap = 0;
+  void ensure(size_t bytes);  // throws Error
+  void release();
+};
+size_t f64_workspace_bytes(int w, int h, int degree);
+void run_gpf_f64_exact(const double* d_in, double* d_out, const Params& p, F64Work& ws,
+                       unsigned long long* d_fb, cudaStream_t st);
+
+// Drop-in fp64 host entry (dropin.cpp): gpf_filter_gpf and gpfilter::gpf.
+// Per device: an LRU of fp32 plans, the fp64 workspace, device in/out
+// buffers and a stream, reused across calls (a repeated call allocates
+// nothing). Precision: kPrecFp32 = the fp32 plane kernels, kPrecFp64 = the
+// reference-exact fp64 replay, kPrecAuto = fp64 exactly when the frame lies
+// outside the envelope where the fp32 kernels are validated against the
+// reference (max |H| = max(f_max - t_c, t_c - f_min) / sigma_r > kH32Limit),
+// or when the degree exceeds the fp32 kernels' limit.
+enum Precision { kPrecAuto = 0, kPrecFp32 = 1, kPrecFp64 = 2 };
+extern const double kH32Limit;
+void set_precision(int mode);
+int get_precision();
+int last_precision();       // mode this thread's last drop-in call ran (1 or 2; 0 = none)
+double last_max_abs_h();    // max |H| this thread's last drop-in call measured (auto mode)
+long long dropin_gpf(const double* h_in, double* h_out, const Params& p);  // throws Error
+void dropin_release();
+
 // Single-plane recursive Gaussian (gpf_gaussian_recursive), fp64 in/out.
 void run_gaussian_f64(const double* d_in, double* d_out, double* d_tmp, int w, int h,
                       double sigma_s, double scale, cudaStream_t st);

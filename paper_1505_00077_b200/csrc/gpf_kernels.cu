@@ -128,7 +128,7 @@ __global__ void __launch_bounds__(kMeanThreads) k_mean_partial(const T* __restri
 
 __global__ void __launch_bounds__(kMeanThreads) k_mean_final(const double* __restrict__ partials,
                                                              int nblocks, long long n,
-                                                             int centering,
+                                                             int centering, double tc_fixed,
                                                              double* __restrict__ scalars) {
   partials += (size_t)blockIdx.x * nblocks * 2;
   double hi = 0.0, lo = 0.0;
@@ -136,7 +136,9 @@ __global__ void __launch_bounds__(kMeanThreads) k_mean_final(const double* __res
     dd_add(hi, lo, partials[2 * b], partials[2 * b + 1]);
   block_dd_reduce(hi, lo);
   if (threadIdx.x == 0)
-    scalars[2 * blockIdx.x] = centering ? (hi + lo) / static_cast<double>(n) : 0.0;
+    // centering 1: mean; 2: a fixed t_c (CenteringMode::midpoint, bilateral.cpp:77-82); 0: none
+    scalars[2 * blockIdx.x] =
+        centering == 1 ? (hi + lo) / static_cast<double>(n) : (centering == 2 ? tc_fixed : 0.0);
 }
 
 // ----------------------------------------------------------------------------
@@ -591,7 +593,9 @@ __global__ void __launch_bounds__(256) k_seed(const Tin* __restrict__ in_all,
   const Tin* in = in_all + (size_t)f * w * h;
   float2* EM = EM_all + (size_t)f * h * w_pad;
   const double t_c = scalars[2 * f];
-  const bool vec = sizeof(Tin) == 4 && (w & 3) == 0 && x + 4 <= w;
+  // 16-B loads need a 16-B aligned frame base (a torch view may start at any float)
+  const bool vec = sizeof(Tin) == 4 && (w & 3) == 0 && x + 4 <= w &&
+                   (reinterpret_cast<uintptr_t>(in_all) & 15) == 0;
   for (int y = blockIdx.y; y < h; y += gridDim.y) {
     const Tin* src = in + (size_t)y * w + x;
     float2* dst = EM + (size_t)y * w_pad + x;
@@ -1304,7 +1308,7 @@ static void run_frames(Plan& plan, const Tin* d_in, Tout* d_out, int count,
   stage_mark(plan, kStageMean, st);
   k_mean_partial<Tin><<<dim3(plan.mean_blocks, count), kMeanThreads, 0, st>>>(d_in, npx, plan.partials);
   k_mean_final<<<count, kMeanThreads, 0, st>>>(plan.partials, plan.mean_blocks, npx,
-                                               plan.rc.centering, plan.scalars);
+                                               plan.rc.centering, plan.rc.tc_fixed, plan.scalars);
   const int nthr = 32 * plan.rc.pairs;
   if (nthr <= 352) launch_passes<352>(plan, d_in, d_out, count, d_fb, st);  // N <= 20
   else if (nthr <= 384) launch_passes<384>(plan, d_in, d_out, count, d_fb, st);
@@ -1359,6 +1363,13 @@ void stage_reset(Plan& plan) {
   for (auto& m : plan.timer->marks) cudaEventDestroy(m.ev);
   delete plan.timer;
   plan.timer = nullptr;
+}
+
+void launch_mean_f64(const double* d_in, long long n, int centering, double tc_fixed,
+                     double* partials, int blocks, double* scalars, cudaStream_t st) {
+  k_mean_partial<double><<<dim3(blocks, 1), kMeanThreads, 0, st>>>(d_in, n, partials);
+  k_mean_final<<<1, kMeanThreads, 0, st>>>(partials, blocks, n, centering, tc_fixed, scalars);
+  check(cudaGetLastError(), "kernel launch (mean)");
 }
 
 void run_frames_f32(Plan& plan, const float* d_in, float* d_out, int count,

@@ -195,6 +195,36 @@ def write_pgm(img: np.ndarray, path: str) -> None:
     _check(_lib.lib().gpf_write_pgm(src.h, path.encode()))
 
 
+PRECISIONS = {"auto": _lib.PRECISION_AUTO, "fp32": _lib.PRECISION_FP32, "fp64": _lib.PRECISION_FP64}
+
+
+def set_precision(mode: str) -> None:
+    """Precision of gpf_filter_gpf: "auto" (default), "fp32" or "fp64" (gpfilter_b200.h)."""
+    _check(_lib.lib().gpf_b200_set_precision(PRECISIONS[mode]))
+
+
+def get_precision() -> str:
+    inv = {v: k for k, v in PRECISIONS.items()}
+    return inv[_lib.lib().gpf_b200_get_precision()]
+
+
+def last_precision() -> str | None:
+    """Mode ("fp32"/"fp64") this thread's last gpf_filter_gpf call ran."""
+    return {1: "fp32", 2: "fp64"}.get(_lib.lib().gpf_b200_last_precision())
+
+
+def last_max_abs_h() -> float:
+    return _lib.lib().gpf_b200_last_max_abs_h()
+
+
+def fp32_h_limit() -> float:
+    return _lib.lib().gpf_b200_fp32_h_limit()
+
+
+def dropin_release() -> None:
+    _lib.lib().gpf_b200_dropin_release()
+
+
 def set_num_threads(n: int) -> None:
     _check(_lib.lib().gpf_set_num_threads(n))
 

@@ -12,6 +12,8 @@ image and the reference's missing astronaut_256.pgm. Generator (numpy PCG64):
 
 Seeds: rectangles use config_id*1000 + channel, noise uses
 config_id*1000 + frame*3 + channel + 500 (C4 rectangles drift +4 px per frame).
+Frame k > 0 of a still-image config (C1/C2/C3 batches) uses seed
+config_id*1000 + channel + 17k for both; frame 0 is the canonical image.
 """
 from __future__ import annotations
 
@@ -99,7 +101,9 @@ def make(cfg: Config, frame: int = 0, channel: int = 0) -> np.ndarray:
     if cfg.kind == "video":
         return rects_image(cfg.width, cfg.height, 48, cfg.noise, base + channel,
                            noise_seed=base + frame * 3 + channel + 500, dx=4 * frame)
-    return rects_image(cfg.width, cfg.height, cfg.rects, cfg.noise, base + channel)
+    # further frames of a still-image config (a frame batch: C3's per-sigma_s
+    # frames, the frames each rank shards) draw fresh rectangles and noise
+    return rects_image(cfg.width, cfg.height, cfg.rects, cfg.noise, base + channel + 17 * frame)
 
 
 def scaled(cfg: Config, width: int, height: int) -> Config:

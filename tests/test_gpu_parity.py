@@ -4,11 +4,12 @@ Bar (north_star): max |gpu - reference| <= 1e-3 on the [0,255] scale, equal
 fallback counts. The oracle is the compiled reference's output (golden
 fixtures) or the bitwise-equal C restatement (oracle/liboracle.so).
 
-Inputs whose degree-N series diverges in the reference itself (sigma_r = 20
-with bright pixels far from the mean, the C2 family): the reference output
-leaves the input range there and is ill-conditioned in any fp32 evaluation.
-For those we hold the 1e-3 bar on pixels whose reference output lies inside
-the input range, and a relative bar on the diverged ones.
+The drop-in gpf_filter_gpf runs in its default AUTO precision: inputs whose
+degree-N series is ill-conditioned in the reference itself (small sigma_r with
+pixels far from t_c, the C2/C5 family, where the reference output leaves the
+input range) run the reference-exact fp64 mode, so the bar holds on every
+pixel. The fp32 plan entries are held to the bar inside their
+validated envelope.
 """
 import numpy as np
 import pytest
@@ -18,7 +19,6 @@ from paper_1505_00077_b200 import synth
 pytestmark = pytest.mark.gpu
 
 TOL = 1e-3
-ILL_CONDITIONED = {"rects_160x96_ss5_sr20"}
 
 
 def split_report(out, ref, img):
@@ -44,11 +44,7 @@ def test_golden_cases(gpu, golden):
         assert fb == int(golden[f"{name}/fb"]), name
         dmax, din, rel, nout = split_report(out, ref, img)
         worst[name] = dmax
-        if name in ILL_CONDITIONED:
-            assert din <= TOL, (name, din)
-            assert rel <= 1e-2, (name, rel)
-        else:
-            assert dmax <= TOL, (name, dmax)
+        assert dmax <= TOL, (name, dmax, gpu.last_precision())
     print("golden max-abs:", {k: f"{v:.2e}" for k, v in worst.items()})
 
 
@@ -94,10 +90,7 @@ def test_configs_vs_oracle(gpu, oracle, cid, w, h):
         assert fb == rfb
         dmax, din, rel, nout = split_report(out, ref, img)
         print(f"C{cid} {w}x{h} ss={ss}: max {dmax:.2e} in-range {din:.2e} diverged px {nout} rel {rel:.2e}")
-        if cid == 2:
-            assert din <= 5 * TOL and rel <= 1e-2
-        else:
-            assert dmax <= TOL
+        assert dmax <= TOL, (cid, ss, gpu.last_precision())
 
 
 def test_full_size_c1_and_plan_path(gpu, oracle):
@@ -266,16 +259,19 @@ def test_sigma_s_sweep_basis_edges(gpu, oracle, ss):
     assert d <= TOL
 
 
-@pytest.mark.parametrize("sr,ss", [(3.0, 2.0), (3.0, 6.0), (5.0, 2.0), (5.0, 3.0)])
+@pytest.mark.parametrize("sr,ss", [(1.0, 2.0), (1.0, 6.0), (3.0, 2.0), (3.0, 6.0), (5.0, 2.0),
+                                   (5.0, 3.0)])
 def test_small_sigma_r(gpu, oracle, sr, ss):
-    """Small sigma_r (H = h / sigma_r up to ~85): planes F_n = H^n E span a huge
-    range across neighbouring pixels, the regime where fp32 rounding inside the
-    filter matters most (DESIGN.md 2). Within the bar down to sigma_r = 3;
-    sigma_r = 1 with sigma_s = 2 exceeds it (tools/small_sr_probe.py)."""
+    """Small sigma_r (H = h / sigma_r up to ~200): planes F_n = H^n E span far
+    more than fp32's range across neighbouring pixels and the reference's own
+    series diverges; AUTO runs the reference-exact fp64 mode here, so every
+    pixel is held to the bar (the sigma_r = 1 case of ADVICE r01)."""
     img = synth.rects_image(96, 64, 8, 10.0, 77).astype(np.float64)
     ref, rfb, _ = oracle.gpf(img, ss, sr, 20, threads=4)
     out, fb = run(gpu, img, ss, sr)
     assert fb == rfb
     dmax, din, rel, nout = split_report(out, ref, img)
-    print(f"sr {sr} ss {ss}: max {dmax:.2e} in-range {din:.2e} diverged px {nout}")
-    assert din <= TOL and rel <= 1e-2
+    print(f"sr {sr} ss {ss}: max {dmax:.2e} in-range {din:.2e} diverged px {nout} "
+          f"({gpu.last_precision()}, max|H| {gpu.last_max_abs_h():.1f})")
+    assert gpu.last_precision() == "fp64"
+    assert dmax <= TOL
