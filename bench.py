@@ -2,23 +2,37 @@
 """Benchmark of the B200 GPF hot path (BASELINE.json metric: Mpixel/s of the
 sigma_s-independent Gauss-polynomial bilateral filter, and % of roofline).
 
-Workload (BASELINE config 3): one 8192x8192 fp32 frame of the seeded
-generator (1024 rectangles, noise 10), sigma_r 30, N = 20, recursive backend,
-mean centering; a STEP filters it at every sigma_s of the sweep
-{2, 5, 10, 20, 50} (5 frames = 335.5 Mpixel per GPU), one plan and stream per
-sigma_s. Inputs are 256 MiB per frame (> 126 MB L2), so no L2 flush is needed.
+Workload (BASELINE config 3): 8192x8192 fp32 frames of the seeded generator
+(1024 rectangles, noise 10), sigma_r 30, N = 20, recursive backend, mean
+centering. A STEP filters five frames, frame k of the C3 batch at sigma_s[k]
+of the sweep {2, 5, 10, 20, 50} (335.5 Mpixel per GPU), one plan and stream
+per sigma_s. Inputs are 256 MiB per frame (> 126 MB L2), so no L2 flush is
+needed.
 
   python bench.py [--gpus N] [--steps K] [--warmup W] [--impl b200|reference]
 
-N > 1 runs one process per GPU under torch.distributed.run (weak scaling:
-every rank filters its own frame sweep; no collective on the data path);
-time = max over ranks of the CUDA-event time of the K steps.
+N > 1 runs one process per GPU under torch.distributed.run: the frame batch
+is sharded, rank r filtering frames 5r .. 5r+4 (weak scaling, no collective on
+the data path); time = max over ranks of the CUDA-event time of the K steps.
+`--workload c4` shards BASELINE C4's 192 problems instead (strong scaling).
 
 --impl reference times the reference's own CPU implementation
 (oracle/_ref/libgpfilter_ref.so, compiled unmodified from the reference
 sources; the oracle port if that build is absent) on the box's host cores, on
-a bounded sample of the same workload (one 2048x2048 frame of the generator at
-each sigma_s per step, ~5 s on 16 cores).
+the bench's own frames: each step filters one full 8192x8192 C3 frame at the
+next sigma_s of the sweep.
+
+Besides `value` (device-resident fp32 frames), the line carries:
+  roofline   the dominant kernel and the whole step against SURVEY 8(d)'s
+             algorithmic bytes (188 B/px per frame; 96 B/px for the row pass)
+  e2e        pinned host fp32 frames through gpf_b200_filter_f32_host
+  e2e_dropin the reference's own call, gpf_filter_gpf on fp64 host images
+             (what the reference's `gpf bench` times), per frame
+  fp64_exact the reference-exact fp64 precision mode on BASELINE C5 / C2
+  parity     max |out - reference| on the golden reference samples of the
+             bench's own frames (tests/golden/baseline_samples.npz)
+  cpu_baseline  the reference on one full C3 frame (nproc threads) and a
+             2048^2 crop (1 thread)
 """
 from __future__ import annotations
 
@@ -37,10 +51,10 @@ sys.path.insert(0, ROOT)
 METRIC = "Mpixel/s of Gauss-poly bilateral (sigma_s-independent) and % of HBM/FP32 roofline"
 UNIT = "Mpixel/s"
 CFG_ID = 3
-SAMPLE_W = SAMPLE_H = 2048  # 5 sigma_s x 4.2 MP: ~5 s per pass of the reference on 16 cores
+GOLDEN = os.path.join(ROOT, "tests", "golden", "baseline_samples.npz")
 
 
-def parse():
+def parse(argv=None):
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=20)
@@ -49,22 +63,78 @@ def parse():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-mse", action="store_true",
                     help="skip the (untimed) MSE-vs-exact report, e.g. for ncu launch lists")
+    ap.add_argument("--no-extras", action="store_true",
+                    help="only the timed device-resident step (no e2e / drop-in / fp64 / parity legs)")
     ap.add_argument("--workload", choices=["c3", "c4"], default="c3",
-                    help="c3 (default, the metric's config): 8192^2 sigma_s sweep, replicas per GPU; "
+                    help="c3 (default, the metric's config): 8192^2 sigma_s sweep, 5 frames per GPU; "
                          "c4: 64 frames x 3 channels of 3840x2160 sharded across the GPUs")
-    return ap.parse_args()
+    ap.add_argument("--size", type=int, default=0,
+                    help="frame side override (functional runs only; the metric is quoted at 8192)")
+    ap.add_argument("--share-gpu", action="store_true",
+                    help="every rank on GPU 0 with gloo for the scalar reductions (functional "
+                         "multi-rank run on one GPU; not a performance number)")
+    ap.add_argument("--selftest-cpu", action="store_true",
+                    help="CPU-only check of the launch / reduction plumbing with a stub filter (gloo)")
+    return ap.parse_args(argv)
 
 
+# ------------------------------------------------------------ process plumbing
 def dist_env():
     return (int(os.environ.get("RANK", 0)), int(os.environ.get("WORLD_SIZE", 1)),
             int(os.environ.get("LOCAL_RANK", 0)))
 
 
-def relaunch_under_torchrun(args):
+def relaunch_under_torchrun(args, port: int = 29531):
     cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
-           f"--nproc-per-node={args.gpus}", "--master-addr", "127.0.0.1", "--master-port", "29531",
-           os.path.abspath(__file__)] + sys.argv[1:]
+           f"--nproc-per-node={args.gpus}", "--master-addr", "127.0.0.1", "--master-port",
+           str(int(os.environ.get("GPF_BENCH_PORT", port))), os.path.abspath(__file__)] + sys.argv[1:]
     sys.exit(subprocess.call(cmd))
+
+
+class Job:
+    """One rank of the job: device selection, process group, and the scalar
+    reductions after the timed region (only scalars cross ranks)."""
+
+    def __init__(self, backend: str | None, device: str | None):
+        self.rank, self.world, self.local = dist_env()
+        self.device = device
+        self.pg = False
+        if self.world > 1:
+            import torch
+            import torch.distributed as dist
+            kw = {}
+            if backend == "nccl":
+                kw["device_id"] = torch.device("cuda", self.local)
+            dist.init_process_group(backend, **kw)
+            self.pg = True
+
+    def barrier(self):
+        if self.pg:
+            import torch.distributed as dist
+            dist.barrier()
+
+    def max(self, x: float) -> float:
+        if not self.pg:
+            return float(x)
+        import torch
+        import torch.distributed as dist
+        t = torch.tensor([float(x)], dtype=torch.float64, device=self.device)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item())
+
+    def sum(self, x: float) -> float:
+        if not self.pg:
+            return float(x)
+        import torch
+        import torch.distributed as dist
+        t = torch.tensor([float(x)], dtype=torch.float64, device=self.device)
+        dist.all_reduce(t, op=dist.ReduceOp.SUM)
+        return float(t.item())
+
+    def close(self):
+        if self.pg:
+            import torch.distributed as dist
+            dist.destroy_process_group()
 
 
 # ------------------------------------------------------------------ clocks
@@ -126,47 +196,84 @@ def cpu_threads() -> int:
         return os.cpu_count() or 1
 
 
-def cpu_reference_run(sigmas, sigma_r, degree, steps, threads):
-    """Times the reference CPU implementation on the bounded sample; returns
-    (Mpix/s, seconds per step, kind)."""
-    import numpy as np
+def cpu_model() -> str:
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
 
+
+def reference_filter(threads: int):
+    """(kind, fn(img, sigma_s, sigma_r, degree)): the unmodified reference
+    library when built (oracle/_ref), else the oracle port."""
     from oracle.oracle import LIB_REF, Oracle, Reference
-    from paper_1505_00077_b200 import synth
-    img = synth.rects_image(SAMPLE_W, SAMPLE_H, 16, 10.0, CFG_ID * 1000 + 7).astype(np.float64)
     if os.path.exists(LIB_REF):
         ref = Reference()
         ref.set_num_threads(threads)
-        kind = "reference"
 
-        def one(ss):
-            st, _, _ = ref.gpf(img, ss, sigma_r, degree)
+        def run(img, ss, sr, deg):
+            st, out, fb = ref.gpf(img, ss, sr, deg)
             assert st == 0
-    else:
-        orc = Oracle()
-        kind = "port"
+            return out, fb
+        return "reference", run
+    orc = Oracle()
 
-        def one(ss):
-            orc.gpf(img, ss, sigma_r, degree, threads=threads)
-    times = []
-    for _ in range(steps):
-        t0 = time.perf_counter()
-        for ss in sigmas:
-            one(ss)
-        times.append(time.perf_counter() - t0)
-    per_step = statistics.median(times)
-    return len(sigmas) * SAMPLE_W * SAMPLE_H / per_step / 1e6, per_step, kind
+    def run_port(img, ss, sr, deg):
+        out, fb, _ = orc.gpf(img, ss, sr, deg, threads=threads)
+        return out, fb
+    return "port", run_port
 
 
-def algorithmic_bytes_per_px(pairs: int) -> dict:
-    """HBM bytes each stage must move per pixel (fp32 frames, N+2 = 2*pairs
-    planes; carries every 32 samples: 32 B per (pair, line, chunk) = pairs B/px).
-      mean       f                                   4
-      col_carry  seeds: f in, EM out; carries: EM in, CA out   4 + 8 + 8 + pairs
-      colpass    EM + CA in; V + AH out              8 + pairs + 8 pairs + pairs
-      row_scan   AH in, CH out                       2 pairs
-      rowpass    V + CH + f in; out                  8 pairs + pairs + 4 + 4
-    (ncu dram__bytes of each launch agree to within 3%: profiles/r01_v26_traffic.csv)"""
+def cpu_baseline_leg(cfg, frames) -> dict:
+    """The reference on the host cores: one full frame of the bench's batch at
+    nproc threads (the same config as `value`), and a 2048^2 crop at 1 thread."""
+    thr = cpu_threads()
+    kind, run = reference_filter(thr)
+    img0 = frames[0].astype("float64")
+    t0 = time.perf_counter()
+    run(img0, cfg.sigma_s[0], cfg.sigma_r, cfg.degree)
+    sec = time.perf_counter() - t0
+    px = img0.size
+    out = {"value": round(px / sec / 1e6, 3), "unit": UNIT, "cores": thr, "kind": kind,
+           "cpu_model": cpu_model(),
+           "sample": f"one full {img0.shape[1]}x{img0.shape[0]} C3 frame (frame 0) at sigma_s "
+                     f"{cfg.sigma_s[0]:g}, sigma_r {cfg.sigma_r:g}, N {cfg.degree}, {thr} threads: "
+                     f"{sec:.1f} s"}
+    kind1, run1 = reference_filter(1)
+    crop = img0[:2048, :2048].copy()
+    t0 = time.perf_counter()
+    run1(crop, cfg.sigma_s[0], cfg.sigma_r, cfg.degree)
+    sec1 = time.perf_counter() - t0
+    out["single_thread"] = {"value": round(crop.size / sec1 / 1e6, 3), "unit": UNIT, "cores": 1,
+                            "sample": f"2048x2048 crop of frame 0, 1 thread: {sec1:.1f} s"}
+    return out
+
+
+# ------------------------------------------------------- roofline model
+def model_bytes_per_px(degree: int) -> dict:
+    """SURVEY 8(d) algorithmic HBM bytes per pixel (fp32 frames, N+2 planes):
+    the step reads f for the mean (4) and for the planes (4), writes and reads
+    every plane once between the separable passes (2 x 4 (N+2)) and writes the
+    output (4): 8 (N+2) + 12 = 188 at N = 20. The row pass's share: it reads
+    the N+2 column-pass planes (4 (N+2)), the input f for the fallback rule (4)
+    and writes the output (4): 4 (N+2) + 8 = 96."""
+    planes = degree + 2
+    return {"step": 8 * planes + 12, "rowpass": 4 * planes + 8, "colpass": 4 * planes + 4,
+            "col_carry": 4, "row_scan": 0, "mean": 4}
+
+
+def design_bytes_per_px(pairs: int) -> dict:
+    """HBM bytes each stage of THIS implementation moves per pixel (P = plane
+    pairs; carries every 32 samples: 32 B per (pair, line, chunk) = P B/px).
+      mean       f                                          4
+      col_carry  seeds: f in, EM out; carries: EM in, CA out   4 + 8 + 8 + P
+      colpass    EM + CA in; V + AH out                     8 + P + 8P + P
+      row_scan   AH in, CH out                              2P
+      rowpass    V + CH + f in; out                         8P + P + 4 + 4
+    (ncu dram__bytes per launch: profiles/ncu_traffic.json)"""
     return {"mean": 4, "col_carry": 20 + pairs, "colpass": 8 + 10 * pairs, "row_scan": 2 * pairs,
             "rowpass": 9 * pairs + 8}
 
@@ -175,10 +282,8 @@ def algorithmic_flops_per_px(pairs: int) -> dict:
     """FP32 FLOPs each stage issues per pixel (FMA = 2), P = plane pairs.
     One IIR step of one plane in the output-aligned section basis (DESIGN.md
     section 3): two sections advanced, 3 FMA each, in each direction = 24;
-    emits with normalised weights (causal 1 FMA, or ADD + FMA where the other
-    direction's parked value is added; anticausal MUL + FMA, or 2 FMA) ~6;
-    i.e. ~30 per plane, 60 per pair. Strip/chunk dot products: 4 FMA per
-    plane. Contraction: 2 FMA + 2 MUL per plane.
+    emits ~6; i.e. ~30 per plane, 60 per pair. Strip/chunk dot products: 4 FMA
+    per plane. Contraction: 2 FMA + 2 MUL per plane.
       carries    seeds ~20 + per pair: planes 2 MUL, dots 16          18 P + 20
       colpass    per pair: planes 2, sweeps 60, row dots 16           78 P
       row_scan   per pair: one chain step per 32 pixels              ~P
@@ -205,7 +310,163 @@ def roofline_of(px: int, ms: float, bpp: int, fpp: int, hbm_gbs: float, fp32_tf:
             "frac": round(ach / fp32_tf, 4)}
 
 
+def load_peaks() -> dict:
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    return json.load(open(p)) if os.path.exists(p) else {}
+
+
+def load_traffic(w: int, h: int):
+    """ncu dram__bytes per launch of each stage (profiles/ncu_traffic.json)."""
+    tpath = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+    if not os.path.exists(tpath):
+        return None
+    t = json.load(open(tpath))
+    if t.get("width") != w or t.get("height") != h:
+        return None
+    return t
+
+
+def roofline_block(px, frames, ms_step, stage_ms, degree, w, h) -> dict:
+    """`roofline` key: the dominant kernel against its SURVEY 8(d) share of the
+    algorithmic bytes, the whole step against 8(d)'s 188 B/px (the headline
+    fraction), and the implementation's own traffic beside them."""
+    pairs = (degree + 3) // 2
+    model = model_bytes_per_px(degree)
+    design = design_bytes_per_px(pairs)
+    fpp = algorithmic_flops_per_px(pairs)
+    peaks = load_peaks()
+    hbm_peak = peaks.get("hbm_gbs", 6460.5)
+    hbm_src = ("MEASURED_PEAKS.json hbm_gbs (burst copy)" if "hbm_gbs" in peaks
+               else "B200_PROFILING.md fallback")
+    fp32_tf = fp32_peak_tflops(peaks)
+    dom = "rowpass" if "rowpass" in stage_ms else max(stage_ms, key=stage_ms.get)
+    k_ms = stage_ms[dom]
+    roof = roofline_of(px, k_ms, model[dom], fpp[dom], hbm_peak, fp32_tf)
+    fp_k = fpp[dom] * px / (k_ms / 1e3) / 1e12
+    traffic = load_traffic(w, h)
+    t_launch = traffic["bytes_per_launch"].get(dom) if traffic else None
+    t_step = sum(traffic["bytes_per_launch"].values()) if traffic else None
+    step = roofline_of(px * frames, ms_step, model["step"], sum(fpp.values()), hbm_peak, fp32_tf)
+    return dict(
+        roof, kernel=dom, kernel_ms=round(k_ms, 4), traffic=t_launch,
+        algorithmic_bytes_per_px=model[dom],
+        algorithmic_what=f"SURVEY 8(d) share of the {dom}: N+2 plane reads 4(N+2) + f 4 + out 4",
+        traffic_over_algorithmic=round(t_launch / (model[dom] * px), 3) if t_launch else None,
+        design_bytes_per_px=design[dom], algorithmic_flops_per_px=fpp[dom],
+        fp32={"achieved_tflops": round(fp_k, 2), "peak_tflops": round(fp32_tf, 1),
+              "frac": round(fp_k / fp32_tf, 4),
+              "peak_source": "nominal 148 SM x 128 FMA/clk x 2 x sm_max_mhz"},
+        peak_source=hbm_src,
+        step=dict(step, bytes_per_px=model["step"],
+                  what="whole step at SURVEY 8(d)'s 188 B/px per frame (headline fraction)",
+                  traffic_bytes_per_px=round(t_step / px, 1) if t_step else None,
+                  traffic_over_algorithmic=round(t_step / (model["step"] * px), 3) if t_step else None,
+                  design_bytes_per_px=sum(design.values())))
+
+
 # ------------------------------------------------------------- B200 leg
+def golden_parity(outs, sigmas, n_frames) -> dict | None:
+    """max |out - reference| on the committed reference samples of the bench's
+    frames (frame k at sigma_s[k]; tests/golden/make_baseline_samples.py)."""
+    import numpy as np
+    if not os.path.exists(GOLDEN):
+        return None
+    g = np.load(GOLDEN)
+    res, worst = {}, 0.0
+    for k in range(n_frames):
+        key = f"c3_f{k}_ss{int(sigmas[k])}"
+        if f"{key}/samples" not in g.files:
+            continue
+        ref = g[f"{key}/samples"]
+        s = int(g[f"{key}/meta"][0])
+        got = outs[k][::s, ::s].double().cpu().numpy()
+        d = float(np.abs(got - ref).max())
+        worst = max(worst, d)
+        res[f"{sigmas[k]:g}"] = {"max_abs": float(f"{d:.3e}"), "samples": int(ref.size),
+                                 "ref_fallbacks": int(g[f"{key}/meta"][1])}
+    return {"per_sigma_s": res, "max_abs": float(f"{worst:.3e}"), "tol": 1e-3,
+            "what": "fp32 outputs of the timed step vs the unmodified reference (oracle/_ref) "
+                    "on a stride-64 grid of every frame (tests/golden/baseline_samples.npz); "
+                    "every pixel is compared in tests/test_gpu_fullsize.py"}
+
+
+def dropin_leg(frames, sigmas, cfg, steps) -> dict:
+    """The reference's own call, gpf_filter_gpf, on fp64 host images (the
+    reference's `gpf bench` protocol, proj/tools/gpf_cli.cpp:241-258): every
+    call copies the frame H2D, filters it and returns a new host image."""
+    import ctypes as C
+
+    import numpy as np
+
+    from paper_1505_00077_b200 import _lib, gpf
+    L = _lib.lib()
+    imgs = [gpf.Image.from_array(f.astype(np.float64)) for f in frames]
+    sps = [gpf.spatial_params(s) for s in sigmas]
+    rp = gpf.range_params(cfg.sigma_r, cfg.degree)
+
+    def call(i):
+        out = C.c_void_p()
+        fb = C.c_longlong(-1)
+        st = L.gpf_filter_gpf(imgs[i].h, C.byref(sps[i]), C.byref(rp), 1, 1, C.byref(fb), C.byref(out))
+        if st != 0:
+            raise RuntimeError(L.gpf_last_error().decode())
+        L.gpf_image_destroy(out)
+        return gpf.last_precision(), gpf.last_device_ms()
+
+    for i in range(len(frames)):  # first call per frame: plan + buffers (cached afterwards)
+        call(i)
+    t0 = time.perf_counter()
+    dev_ms, precs = 0.0, set()
+    for _ in range(steps):
+        for i in range(len(frames)):
+            p, ms = call(i)
+            precs.add(p)
+            dev_ms += ms
+    sec = (time.perf_counter() - t0) / steps
+    px = sum(f.size for f in frames)
+    return {"value": round(px / sec / 1e6, 1), "unit": UNIT, "ms_per_step": round(sec * 1e3, 2),
+            "device_ms_per_step": round(dev_ms / steps, 3), "precision": sorted(precs),
+            "h2d_bytes_per_step": px * 8, "d2h_bytes_per_step": px * 8 + 8 * len(frames),
+            "api": "gpf_filter_gpf (reference C ABI): fp64 host image in, new fp64 host image out, "
+                   f"one call per frame, {len(frames)} frames per step, AUTO precision"}
+
+
+def fp64_leg(steps) -> dict:
+    """The reference-exact fp64 mode through gpf_filter_gpf on BASELINE C5 (and
+    C2): the configs whose reference series leaves the input range."""
+    import ctypes as C
+
+    import numpy as np
+
+    from paper_1505_00077_b200 import _lib, gpf, synth
+    L = _lib.lib()
+    res = {}
+    for cid in (5, 2):
+        cfg = synth.CONFIGS[cid]
+        img = gpf.Image.from_array(synth.make(cfg).astype(np.float64))
+        sp, rp = gpf.spatial_params(cfg.sigma_s[0]), gpf.range_params(cfg.sigma_r, cfg.degree)
+
+        def call():
+            out = C.c_void_p()
+            fb = C.c_longlong(-1)
+            st = L.gpf_filter_gpf(img.h, C.byref(sp), C.byref(rp), 1, 1, C.byref(fb), C.byref(out))
+            if st != 0:
+                raise RuntimeError(L.gpf_last_error().decode())
+            L.gpf_image_destroy(out)
+            return gpf.last_device_ms()
+
+        call()
+        t0 = time.perf_counter()
+        dev = [call() for _ in range(steps)]
+        sec = (time.perf_counter() - t0) / steps
+        px = cfg.width * cfg.height
+        res[f"C{cid}"] = {"e2e": round(px / sec / 1e6, 1), "device": round(px / (min(dev) / 1e3) / 1e6, 1),
+                          "unit": UNIT, "device_ms": round(min(dev), 3), "precision": gpf.last_precision(),
+                          "frame": f"{cfg.width}x{cfg.height}, sigma_s {cfg.sigma_s[0]:g}, "
+                                   f"sigma_r {cfg.sigma_r:g}, max|H| {gpf.last_max_abs_h():.2f}"}
+    return res
+
+
 def bench_b200(args):
     import numpy as np
     import torch
@@ -213,55 +474,40 @@ def bench_b200(args):
     from paper_1505_00077_b200 import gpf, synth
 
     rank, world, local = dist_env()
-    torch.cuda.set_device(local)
-    if world > 1:
-        import torch.distributed as dist
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    dev_index = 0 if args.share_gpu else local
+    torch.cuda.set_device(dev_index)
+    job = Job("gloo" if args.share_gpu else "nccl", None if args.share_gpu else "cuda")
     cfg = synth.CONFIGS[CFG_ID]
-    W, H, sigmas, sr, N = cfg.width, cfg.height, cfg.sigma_s, cfg.sigma_r, cfg.degree
-    img = synth.make(cfg)
+    W = H = args.size or cfg.width
+    if args.size:
+        cfg = synth.scaled(cfg, W, H)
+    sigmas, sr, N = cfg.sigma_s, cfg.sigma_r, cfg.degree
+    n_fr = len(sigmas)
+    # this rank's shard of the frame batch: frames n_fr*rank .. n_fr*rank + n_fr - 1
+    frames = [synth.make(cfg, n_fr * rank + k) for k in range(n_fr)]
     px = W * H
-    d_in = torch.from_numpy(img).cuda()
+    d_ins = [torch.from_numpy(f).cuda() for f in frames]
     plans = [gpf.Plan(W, H, s, sr, N) for s in sigmas]
-    outs = [torch.empty_like(d_in) for _ in sigmas]
-    d_fb = torch.zeros(len(sigmas), dtype=torch.int64, device="cuda")
+    outs = [torch.empty_like(d) for d in d_ins]
+    d_fb = torch.zeros(n_fr, dtype=torch.int64, device="cuda")
     streams = [torch.cuda.Stream() for _ in sigmas]
     main = torch.cuda.current_stream()
 
-    # The five sigma_s frames run concurrently on five streams. (GPF_BENCH_CHAIN=1
-    # instead chains them -- frame j starts when frame j-1's column half is done,
-    # via gpf_b200_filter_f32_ev -- measured slower: 12.0 vs 13.8 Gpix/s.)
-    pipelined = os.environ.get("GPF_BENCH_CHAIN", "0") == "1"
-    front = [torch.cuda.Event() for _ in sigmas]
-    for ev, st in zip(front, streams):
-        ev.record(st)  # creates the events
-    chain = {"prev": None}
-
-    # A step enqueues the five frames; steps follow each other on the streams
-    # without a join in between (the timed region is still bracketed by a
-    # device-wide synchronize), so one frame's tail overlaps the next step.
-    join_each_step = os.environ.get("GPF_BENCH_JOIN", "0") == "1"
-
+    # A step enqueues the five frames on five streams; steps follow each other
+    # on the streams without a join in between (the timed region is bracketed
+    # by a device-wide synchronize), so one frame's tail overlaps the next step.
     def step():
-        for i, (plan, out, st) in enumerate(zip(plans, outs, streams)):
-            if pipelined and chain["prev"] is not None:
-                st.wait_event(chain["prev"])
-            plan.filter_device(d_in, out, 1, d_fb[i:i + 1], st.cuda_stream,
-                               front[i].cuda_event if pipelined else None)
-            chain["prev"] = front[i]
-        if join_each_step:
-            for st in streams:
-                main.wait_stream(st)
+        for i, (plan, st) in enumerate(zip(plans, streams)):
+            plan.filter_device(d_ins[i], outs[i], 1, d_fb[i:i + 1], st.cuda_stream)
 
     for st in streams:
         st.wait_stream(main)
     for _ in range(args.warmup):
         step()
     torch.cuda.synchronize()
-    if world > 1:
-        torch.distributed.barrier()
+    job.barrier()
     torch.cuda.synchronize()
-    clocks = ClockSampler(local)
+    clocks = ClockSampler(dev_index)
     clocks.start()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e0.record(main)
@@ -275,150 +521,127 @@ def bench_b200(args):
     torch.cuda.synchronize()
     ms = e0.elapsed_time(e1)
     clk = clocks.stop()
-    if world > 1:
-        t = torch.tensor([ms], device="cuda")
-        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
-        ms = float(t.item())
-        torch.distributed.barrier()
+    ms = job.max(ms)
+    job.barrier()
     ms_step = ms / args.steps
-    frames = len(sigmas)
-    value = world * frames * px / (ms_step / 1e3) / 1e6
+    value = world * n_fr * px / (ms_step / 1e3) / 1e6
+    launches = args.steps * n_fr * plans[0].launches_per_frame
     fallbacks = d_fb.cpu().tolist()
+    parity = golden_parity(outs, sigmas, n_fr) if (rank == 0 and not args.size) else None
 
     # GPF's error against the exact O(sigma_s^2) filter (north_star: reported
     # alongside), full frame, metrics::compare definitions; outside the timed region
     mse = {}
-    d_ex = torch.empty_like(d_in)
-    for s_, out in zip(sigmas, [] if args.no_mse else outs):
-        gpf.exact_device(d_in, d_ex, W, H, s_, sr, stream=main.cuda_stream)
-        rep = gpf.compare_device(d_ex, out, W, H, 0, main.cuda_stream)
-        mse[f"{s_:g}"] = {"mse": round(rep["mse"], 4), "mse_db": round(rep["mse_db"], 3),
-                          "max_abs": round(rep["max_abs"], 4)}
-    del d_ex
+    if not args.no_mse and not args.no_extras:
+        d_ex = torch.empty_like(d_ins[0])
+        for k, (s_, out) in enumerate(zip(sigmas, outs)):
+            gpf.exact_device(d_ins[k], d_ex, W, H, s_, sr, stream=main.cuda_stream)
+            rep = gpf.compare_device(d_ex, out, W, H, 0, main.cuda_stream)
+            mse[f"{s_:g}"] = {"mse": round(rep["mse"], 4), "mse_db": round(rep["mse_db"], 3),
+                              "max_abs": round(rep["max_abs"], 4)}
+        del d_ex
 
     # sigma_s independence: each plan alone on one stream
     per_sigma = {}
-    for s, plan, out in zip(sigmas, plans, outs):
+    for k, (s, plan) in enumerate(zip(sigmas, plans)):
         a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        plan.filter_device(d_in, out, 1, None, main.cuda_stream)
+        plan.filter_device(d_ins[k], outs[k], 1, None, main.cuda_stream)
         a.record(main)
         for _ in range(3):
-            plan.filter_device(d_in, out, 1, None, main.cuda_stream)
+            plan.filter_device(d_ins[k], outs[k], 1, None, main.cuda_stream)
         b.record(main)
         torch.cuda.synchronize()
         per_sigma[f"{s:g}"] = round(a.elapsed_time(b) / 3, 4)
 
     # per-stage timing of one plan (sigma_s = 5) on one stream: dominant kernel
-    p5 = plans[sigmas.index(5.0)]
+    k5 = list(sigmas).index(5.0)
+    p5 = plans[k5]
     p5.set_profiling(True)
     reps = max(3, min(args.steps, 10))
     for _ in range(reps):
-        p5.filter_device(d_in, outs[0], 1, None, main.cuda_stream)
+        p5.filter_device(d_ins[k5], outs[k5], 1, None, main.cuda_stream)
     torch.cuda.synchronize()
     stage_ms = {k: v / reps for k, v in p5.stage_times().items()}
     p5.set_profiling(False)
-    pairs = (N + 3) // 2
-    bpp = algorithmic_bytes_per_px(pairs)
-    fpp = algorithmic_flops_per_px(pairs)
-    dom = max(stage_ms, key=stage_ms.get)
-    peaks = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json"))) if os.path.exists(
-        os.path.join(ROOT, "MEASURED_PEAKS.json")) else {}
-    hbm_peak = peaks.get("hbm_gbs", 6650.0)
-    fp32_tf = fp32_peak_tflops(peaks)
-    traffic = None
-    tpath = os.path.join(ROOT, "profiles", "ncu_traffic.json")
-    if os.path.exists(tpath):
-        t = json.load(open(tpath))
-        if t.get("width") == W and t.get("height") == H and dom in t.get("bytes_per_launch", {}):
-            traffic = t["bytes_per_launch"][dom]
-    roof = roofline_of(px, stage_ms[dom], bpp[dom], fpp[dom], hbm_peak, fp32_tf)
-    fp_k = fpp[dom] * px / (stage_ms[dom] / 1e3) / 1e12
-    # whole step: all stages' bytes and FLOPs against the same peaks
-    design_bpp, design_fpp = sum(bpp.values()), sum(fpp.values())
-    step = roofline_of(px * frames, ms_step, design_bpp, design_fpp, hbm_peak, fp32_tf)
-    model_bpp = 8 * (N + 2) + 12  # SURVEY 8(d) streaming model
-    model_frac = (model_bpp * px * frames / (ms_step / 1e3) / 1e9) / hbm_peak
-    roofline = dict(roof, kernel=dom, traffic=traffic, algorithmic_bytes_per_px=bpp[dom],
-                    algorithmic_flops_per_px=fpp[dom],
-                    fp32={"achieved_tflops": round(fp_k, 2), "peak_tflops": round(fp32_tf, 1),
-                          "frac": round(fp_k / fp32_tf, 4),
-                          "peak_source": "nominal 148 SM x 128 FMA/clk x 2 x sm_max_mhz"},
-                    peak_source="MEASURED_PEAKS.json hbm_gbs (burst copy)",
-                    step=dict(step, bytes_per_px=design_bpp, flops_per_px=design_fpp,
-                              what="all stages of the step, slower of HBM bytes and FP32 FLOPs"),
-                    step_model_frac=round(model_frac, 4),
-                    step_model=f"SURVEY 8(d): {model_bpp} B/px at HBM peak")
+    roofline = roofline_block(px, n_fr, ms_step, stage_ms, N, W, H)
 
-    # end to end through the C ABI: pinned host fp32 in -> host fp32 out
-    # One host thread per sigma_s plan (the C call releases the GIL; each plan
-    # owns its streams), so one frame's upload/download overlaps the others'
-    # compute. Every step still moves its input H2D and its output D2H.
-    import threading
-    h_in = torch.from_numpy(img).pin_memory()
-    h_in_np = h_in.numpy()
-    h_outs = [torch.empty_like(h_in).pin_memory() for _ in plans]
-    h_outs_np = [o.numpy() for o in h_outs]
-    e2e_steps = max(3, min(args.steps, 10))  # amortise the pipeline fill (first upload) and drain (last download)
+    e2e = dropin = fp64 = None
+    if not args.no_extras:
+        # end to end through the C ABI: pinned host fp32 in -> host fp32 out.
+        # One host thread per sigma_s plan (the C call releases the GIL; each
+        # plan owns its streams), so one frame's upload/download overlaps the
+        # others' compute. Every step moves its inputs H2D and outputs D2H.
+        import threading
+        h_ins = [torch.from_numpy(f).pin_memory().numpy() for f in frames]
+        h_outs = [torch.empty((H, W), dtype=torch.float32).pin_memory().numpy() for _ in frames]
+        e2e_steps = max(3, min(args.steps, 10))
 
-    def host_run(n):
-        errs = []
+        def host_run(n):
+            errs = []
 
-        def worker(plan, o):
-            try:
-                for _ in range(n):
-                    plan.filter_host(h_in_np, o)
-            except Exception as e:  # surfaced below
-                errs.append(e)
-        ths = [threading.Thread(target=worker, args=(p, o)) for p, o in zip(plans, h_outs_np)]
-        t0 = time.perf_counter()
-        for t in ths:
-            t.start()
-        for t in ths:
-            t.join()
-        if errs:
-            raise errs[0]
-        return time.perf_counter() - t0
+            def worker(plan, i):
+                try:
+                    for _ in range(n):
+                        plan.filter_host(h_ins[i], h_outs[i])
+                except Exception as e:  # surfaced below
+                    errs.append(e)
+            ths = [threading.Thread(target=worker, args=(p, i)) for i, p in enumerate(plans)]
+            t0 = time.perf_counter()
+            for t in ths:
+                t.start()
+            for t in ths:
+                t.join()
+            if errs:
+                raise errs[0]
+            return time.perf_counter() - t0
 
-    host_run(1)
-    torch.cuda.synchronize()
-    if world > 1:
-        torch.distributed.barrier()
-    e2e_s = host_run(e2e_steps) / e2e_steps
-    if world > 1:
-        t = torch.tensor([e2e_s], device="cuda")
-        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
-        e2e_s = float(t.item())
-    e2e = {"value": round(world * frames * px / e2e_s / 1e6, 1), "unit": UNIT,
-           "h2d_bytes_per_step": frames * px * 4, "d2h_bytes_per_step": frames * px * 4 + frames * 8,
-           "api": "gpf_b200_filter_f32_host (pinned host fp32 in/out, one call per sigma_s per step, "
-                   f"{frames} host threads, one per sigma_s plan)"}
+        host_run(1)
+        torch.cuda.synchronize()
+        job.barrier()
+        e2e_s = job.max(host_run(e2e_steps) / e2e_steps)
+        e2e = {"value": round(world * n_fr * px / e2e_s / 1e6, 1), "unit": UNIT,
+               "h2d_bytes_per_step": n_fr * px * 4, "d2h_bytes_per_step": n_fr * px * 4 + n_fr * 8,
+               "api": "gpf_b200_filter_f32_host (pinned host fp32 in/out, one call per sigma_s per "
+                      f"step, {n_fr} host threads, one per sigma_s plan)"}
+        # the reference's own call on fp64 host images
+        for p in plans:
+            p.close()
+        del outs
+        torch.cuda.empty_cache()
+        dsteps = max(1, min(args.steps, 3))
+        dropin = dropin_leg(frames, sigmas, cfg, dsteps)
+        dropin["value"] = round(job.sum(dropin["value"]), 1)
+        if rank == 0 and world == 1 and not args.size:
+            fp64 = fp64_leg(max(1, min(args.steps, 3)))
+        gpf.dropin_release()
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        thr = cpu_threads()
-        v, sec, kind = cpu_reference_run(sigmas, sr, N, 2, thr)
-        cpu = {"value": round(v, 3), "unit": UNIT, "cores": thr, "kind": kind,
-               "sample": f"{SAMPLE_W}x{SAMPLE_H} generator frame at sigma_s {list(sigmas)}, "
-                         f"sigma_r {sr}, N {N}; median of 2 passes of {sec:.1f} s of CPU work"}
+        cpu = cpu_baseline_leg(cfg, frames)
 
-    launches = args.steps * frames * plans[0].launches_per_frame
     line = {
         "metric": METRIC, "value": round(value, 1), "unit": UNIT, "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms_step, 4),
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "fp32",
         "data": "synthetic (seeded generator, SURVEY.md 8(d))",
-        "config": {"workload": f"C3: {W}x{H} fp32 rects1024 noise10, sigma_r {sr}, N {N}, "
-                               f"sigma_s sweep {list(sigmas)} = {frames} frames/step/GPU",
-                   "frames_per_step_per_gpu": frames, "pixels_per_frame": px,
+        "config": {"workload": f"C3: {W}x{H} fp32 rects{cfg.rects} noise10, sigma_r {sr:g}, N {N}; "
+                               f"frame k of the C3 batch at sigma_s[k] of {list(sigmas)} = {n_fr} "
+                               "frames/step/GPU",
+                   "frames_per_step_per_gpu": n_fr, "pixels_per_frame": px,
                    "l2": "inputs larger than L2 (256 MiB per frame, 126 MB L2); no flush",
-                   "parallelism": f"frame replicas x{world}, no collective"},
+                   "parallelism": f"frame batch sharded x{world} (rank r: frames {n_fr}r..{n_fr}r+"
+                                  f"{n_fr - 1}), no collective on the data path"
+                                  + ("; all ranks on GPU 0 (functional run)" if args.share_gpu else "")},
         "sigma_s_ms_per_frame": per_sigma,
         "mse_vs_exact": {"per_sigma_s": mse, "pixels": px,
                          "what": "GPF output vs the exact O(sigma_s^2) bilateral (gpf_b200_exact_f32), "
                                  "full frame, metrics::compare (mse, 10 log10 mse, max |d|)"},
         "stage_ms_per_frame": {k: round(v, 4) for k, v in stage_ms.items()},
         "roofline": roofline,
+        "parity": parity,
         "e2e": e2e,
+        "e2e_dropin": dropin,
+        "fp64_exact": fp64,
         "cpu_baseline": cpu,
         "gpu_launches": launches,
         "fallbacks": fallbacks,
@@ -426,8 +649,7 @@ def bench_b200(args):
     }
     if rank == 0:
         print(json.dumps(line), flush=True)
-    if world > 1:
-        torch.distributed.destroy_process_group()
+    job.close()
 
 
 # ------------------------------------------------------------- C4 frame batch
@@ -465,10 +687,9 @@ def bench_c4(args):
     from paper_1505_00077_b200 import gpf, shard, synth
 
     rank, world, local = dist_env()
-    torch.cuda.set_device(local)
-    if world > 1:
-        import torch.distributed as dist
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    dev_index = 0 if args.share_gpu else local
+    torch.cuda.set_device(dev_index)
+    job = Job("gloo" if args.share_gpu else "nccl", None if args.share_gpu else "cuda")
     cfg = synth.CONFIGS[4]
     W, H, ss, sr, N = cfg.width, cfg.height, cfg.sigma_s[0], cfg.sigma_r, cfg.degree
     n_items = cfg.frames * cfg.channels
@@ -491,10 +712,9 @@ def bench_c4(args):
     for _ in range(args.warmup):
         step()
     torch.cuda.synchronize()
-    if world > 1:
-        torch.distributed.barrier()
+    job.barrier()
     torch.cuda.synchronize()
-    clocks = ClockSampler(local)
+    clocks = ClockSampler(dev_index)
     clocks.start()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e0.record(st)
@@ -504,10 +724,9 @@ def bench_c4(args):
     torch.cuda.synchronize()
     ms_local = e0.elapsed_time(e1)
     clk = clocks.stop()
-    if world > 1:
-        torch.distributed.barrier()
+    job.barrier()
     secs, fallbacks = shard.reduce_job(ms_local / 1e3, d_fb[:n_loc].cpu().tolist(), n_items, rank,
-                                       world, device="cuda")
+                                       world, device=job.device)
     ms_step = secs * 1e3 / args.steps
     value = n_items * px / (ms_step / 1e3) / 1e6
 
@@ -519,48 +738,41 @@ def bench_c4(args):
     torch.cuda.synchronize()
     stage_ms = {k: v / reps for k, v in plan.stage_times().items()}
     plan.set_profiling(False)
-    pairs = (N + 3) // 2
-    bpp, fpp = algorithmic_bytes_per_px(pairs), algorithmic_flops_per_px(pairs)
-    dom = max(stage_ms, key=stage_ms.get)
-    peaks = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json"))) if os.path.exists(
-        os.path.join(ROOT, "MEASURED_PEAKS.json")) else {}
-    hbm_peak, fp32_tf = peaks.get("hbm_gbs", 6650.0), fp32_peak_tflops(peaks)
-    roof = roofline_of(px, stage_ms[dom], bpp[dom], fpp[dom], hbm_peak, fp32_tf)
-    step_roof = roofline_of(n_items * px, ms_step, sum(bpp.values()), sum(fpp.values()),
-                            hbm_peak * world, fp32_tf * world)
-    roofline = dict(roof, kernel=dom, traffic=None, algorithmic_bytes_per_px=bpp[dom],
-                    algorithmic_flops_per_px=fpp[dom],
-                    peak_source="MEASURED_PEAKS.json hbm_gbs (burst copy)",
-                    step=dict(step_roof, what=f"whole job on {world} GPU(s), peaks x {world}"))
+    roofline = roofline_block(px, n_items / world, ms_step, stage_ms, N, W, H)
 
     # end to end: this rank's frames from pinned host memory through the
     # pipelined host entry (H2D of frame f+1 overlaps compute of f), every step
-    h_in = d_in[:max(n_loc, 1)].cpu().pin_memory()
-    h_out = torch.empty_like(h_in).pin_memory()
-    h_in_np, h_out_np = h_in.numpy(), h_out.numpy()
-    if n_loc:
-        plan.filter_host(h_in_np[:n_loc], h_out_np[:n_loc])
-    torch.cuda.synchronize()
-    if world > 1:
-        torch.distributed.barrier()
-    e2e_steps = max(1, min(args.steps, 3))
-    t0 = time.perf_counter()
-    for _ in range(e2e_steps):
+    e2e = None
+    if not args.no_extras:
+        h_in = d_in[:max(n_loc, 1)].cpu().pin_memory()
+        h_out = torch.empty_like(h_in).pin_memory()
+        h_in_np, h_out_np = h_in.numpy(), h_out.numpy()
         if n_loc:
             plan.filter_host(h_in_np[:n_loc], h_out_np[:n_loc])
-    e2e_s, _ = shard.reduce_job((time.perf_counter() - t0) / e2e_steps, [0] * n_loc, n_items, rank,
-                                world, device="cuda")
-    e2e = {"value": round(n_items * px / e2e_s / 1e6, 1), "unit": UNIT,
-           "h2d_bytes_per_step": n_items * px * 4, "d2h_bytes_per_step": n_items * (px * 4 + 8),
-           "api": "gpf_b200_filter_f32_host (pinned host fp32 in/out, all local frames per call, "
-                  "H2D/compute/D2H pipelined inside)"}
+        torch.cuda.synchronize()
+        job.barrier()
+        e2e_steps = max(1, min(args.steps, 3))
+        t0 = time.perf_counter()
+        for _ in range(e2e_steps):
+            if n_loc:
+                plan.filter_host(h_in_np[:n_loc], h_out_np[:n_loc])
+        e2e_s = job.max((time.perf_counter() - t0) / e2e_steps)
+        e2e = {"value": round(n_items * px / e2e_s / 1e6, 1), "unit": UNIT,
+               "h2d_bytes_per_step": n_items * px * 4, "d2h_bytes_per_step": n_items * (px * 4 + 8),
+               "api": "gpf_b200_filter_f32_host (pinned host fp32 in/out, all local frames per call, "
+                      "H2D/compute/D2H pipelined inside)"}
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         thr = cpu_threads()
-        v, sec, kind = cpu_reference_run((ss,), sr, N, 3, thr)
-        cpu = {"value": round(v, 3), "unit": UNIT, "cores": thr, "kind": kind,
-               "sample": f"{SAMPLE_W}x{SAMPLE_H} generator frame at sigma_s {ss}, sigma_r {sr}, N {N} "
-                         f"({sec:.1f} s of CPU work)"}
+        kind, run = reference_filter(thr)
+        img = d_in[0].double().cpu().numpy()
+        t0 = time.perf_counter()
+        run(img, ss, sr, N)
+        sec = time.perf_counter() - t0
+        cpu = {"value": round(px / sec / 1e6, 3), "unit": UNIT, "cores": thr, "kind": kind,
+               "cpu_model": cpu_model(),
+               "sample": f"one full C4 problem (frame 0, channel 0, {W}x{H}) at sigma_s {ss:g}, "
+                         f"sigma_r {sr:g}, N {N}: {sec:.1f} s"}
     line = {
         "metric": METRIC, "value": round(value, 1), "unit": UNIT, "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms_step, 4),
@@ -581,40 +793,95 @@ def bench_c4(args):
     }
     if rank == 0:
         print(json.dumps(line), flush=True)
-    if world > 1:
-        torch.distributed.destroy_process_group()
+    job.close()
 
 
+# ------------------------------------------------------------- reference arm
 def bench_reference(args):
+    """The reference's own CPU implementation on the bench's frames: each step
+    filters one full frame of the C3 batch (frame k at sigma_s[k], k = step mod
+    5) with all host threads; warm-up steps page the library and the frames in
+    on a 1024^2 crop. Under torchrun only rank 0 runs."""
     rank, world, _ = dist_env()
     if rank != 0:
         return
     from paper_1505_00077_b200 import synth
     cfg = synth.CONFIGS[4 if args.workload == "c4" else CFG_ID]
     thr = cpu_threads()
-    cpu_reference_run(cfg.sigma_s, cfg.sigma_r, cfg.degree, args.warmup, thr) if args.warmup else None
-    v, sec, kind = cpu_reference_run(cfg.sigma_s, cfg.sigma_r, cfg.degree, args.steps, thr)
+    kind, run = reference_filter(thr)
+    if args.workload == "c4":
+        imgs = [synth.make(cfg, 0, 0).astype("float64")]
+        sig = [cfg.sigma_s[0]]
+    else:
+        n = args.size or cfg.width
+        c = synth.scaled(cfg, n, n) if args.size else cfg
+        imgs = [synth.make(c, k).astype("float64") for k in range(len(cfg.sigma_s))]
+        sig = list(cfg.sigma_s)
+    for w in range(args.warmup):
+        run(imgs[0][:1024, :1024].copy(), sig[0], cfg.sigma_r, cfg.degree)
+    times, px = [], 0
+    for s in range(args.steps):
+        k = s % len(imgs)
+        t0 = time.perf_counter()
+        run(imgs[k], sig[k], cfg.sigma_r, cfg.degree)
+        times.append(time.perf_counter() - t0)
+        px += imgs[k].size
+    total = sum(times)
+    v = px / total / 1e6
+    h, w = imgs[0].shape
     line = {
         "impl": "reference", "metric": METRIC, "value": round(v, 3), "unit": UNIT, "n_gpus": world,
-        "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(sec * 1e3, 1),
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(total / args.steps * 1e3, 1),
         "higher_is_better": True, "scaling": "strong" if args.workload == "c4" else "weak",
         "vs_baseline": None, "dtype": "fp64",
         "data": "synthetic (seeded generator, SURVEY.md 8(d))",
-        "config": {"workload": f"C{cfg.cid} sample: {SAMPLE_W}x{SAMPLE_H} generator frame, sigma_r "
-                               f"{cfg.sigma_r}, N {cfg.degree}, sigma_s sweep {list(cfg.sigma_s)}",
+        "config": {"workload": (f"C{cfg.cid}: one full {w}x{h} frame per step (frame k of the batch at "
+                                f"sigma_s[k], k = step mod {len(imgs)}), sigma_r {cfg.sigma_r:g}, "
+                                f"N {cfg.degree}, sigma_s {sig}"),
                    "parallelism": f"{thr} host threads (gpf_set_num_threads)"},
         "cpu_baseline": {"value": round(v, 3), "unit": UNIT, "cores": thr, "kind": kind,
-                         "sample": f"{SAMPLE_W}x{SAMPLE_H} x {len(cfg.sigma_s)} sigma_s per step"},
+                         "cpu_model": cpu_model(),
+                         "sample": f"{args.steps} full {w}x{h} frames ({total:.1f} s)"},
         "e2e": {"value": round(v, 3), "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
+
+
+# ------------------------------------------------------------- CPU self-test
+def selftest_cpu(args):
+    """The launch and reduction plumbing of the B200 leg with a stub filter:
+    torchrun relaunch, gloo process group, frame shard per rank, max-over-ranks
+    time, whole-job value. No GPU and no library involved."""
+    import numpy as np
+    rank, world, _ = dist_env()
+    job = Job("gloo", None)
+    n_fr, n = 5, args.size or 64
+    frames = [np.full((n, n), float(n_fr * rank + k), np.float32) for k in range(n_fr)]
+    job.barrier()
+    t0 = time.perf_counter()
+    acc = 0.0
+    for _ in range(args.steps):
+        for f in frames:
+            acc += float(np.cumsum(f, axis=0)[-1].sum())  # stub work
+    ms = job.max((time.perf_counter() - t0) * 1e3)
+    total_frames = job.sum(n_fr)
+    ms_step = ms / args.steps
+    line = {"metric": METRIC, "value": round(world * n_fr * n * n / (ms_step / 1e3) / 1e6, 3),
+            "unit": UNIT, "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": ms_step, "scaling": "weak", "selftest": True,
+            "frames_total": int(total_frames), "checksum": job.sum(acc)}
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    job.close()
 
 
 def main():
     args = parse()
     if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
         relaunch_under_torchrun(args)
-    if args.impl == "reference":
+    if args.selftest_cpu:
+        selftest_cpu(args)
+    elif args.impl == "reference":
         bench_reference(args)
     elif args.workload == "c4":
         bench_c4(args)

@@ -64,6 +64,17 @@ gpf_status gpf_b200_filter_f32_ev(gpf_b200_plan* plan, const float* d_in, float*
                                   int count, long long* d_fallbacks, void* stream,
                                   void* front_done);
 
+/* Same as gpf_b200_filter_f32, and writes d_ill[f] (device memory, `count`
+ * ints) = 1 when frame f lies outside the envelope in which the fp32 kernels
+ * are held to the reference within 1e-3 (max|H| = max(f_max - t_c, t_c -
+ * f_min) / sigma_r > gpf_b200_fp32_h_limit(), measured on the device from the
+ * frame itself), else 0. Such a frame's fp32 output is still the fp32
+ * evaluation, but the reference's own degree-N series is ill-conditioned there
+ * (it may leave the input range); filter it through gpf_filter_gpf (AUTO runs
+ * the reference-exact fp64 mode for it). */
+gpf_status gpf_b200_filter_f32_checked(gpf_b200_plan* plan, const float* d_in, float* d_out,
+                                       int count, long long* d_fallbacks, int* d_ill, void* stream);
+
 /* Exact (direct O(sigma_s^2)) bilateral filter of `count` contiguous fp32
  * frames in device memory (the gpf_filter_exact definition), on `stream`. */
 gpf_status gpf_b200_exact_f32(const float* d_in, float* d_out, int width, int height, int count,
@@ -111,6 +122,9 @@ int gpf_b200_get_precision(void);
 int gpf_b200_last_precision(void);
 double gpf_b200_last_max_abs_h(void);
 double gpf_b200_fp32_h_limit(void);
+/* Device time (CUDA events on the drop-in stream) of the filter kernels of this
+ * thread's last gpf_filter_gpf call, copies excluded. */
+float gpf_b200_last_device_ms(void);
 
 /* gpf_filter_gpf keeps, per device, up to four fp32 plans (keyed by every
  * filter parameter), the fp64 workspace and its device buffers between calls,

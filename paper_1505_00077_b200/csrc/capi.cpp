@@ -488,6 +488,7 @@ gpf_status gpf_b200_set_precision(int mode) {
 int gpf_b200_get_precision(void) { return gpfb::get_precision(); }
 int gpf_b200_last_precision(void) { return gpfb::last_precision(); }
 double gpf_b200_last_max_abs_h(void) { return gpfb::last_max_abs_h(); }
+float gpf_b200_last_device_ms(void) { return gpfb::last_device_ms(); }
 double gpf_b200_fp32_h_limit(void) { return gpfb::kH32Limit; }
 void gpf_b200_dropin_release(void) { gpfb::dropin_release(); }
 
@@ -592,8 +593,11 @@ int gpf_b200_plan_launches_per_frame(const gpf_b200_plan* plan) {
   return plan ? plan->plan.launches_per_frame : 0;
 }
 
-gpf_status gpf_b200_filter_f32_ev(gpf_b200_plan* plan, const float* d_in, float* d_out, int count,
-                                  long long* d_fallbacks, void* stream, void* front_done) {
+}  // extern "C"
+
+namespace {
+gpf_status filter_f32_impl(gpf_b200_plan* plan, const float* d_in, float* d_out, int count,
+                           long long* d_fallbacks, int* d_ill, void* stream, void* front_done) {
   if (plan == nullptr || d_in == nullptr || d_out == nullptr)
     return fail(GPF_ERR_INVALID_ARGUMENT, "null argument");
   if (count < 0) return fail(GPF_ERR_INVALID_ARGUMENT, "count must be >= 0");
@@ -606,24 +610,43 @@ gpf_status gpf_b200_filter_f32_ev(gpf_b200_plan* plan, const float* d_in, float*
     if (fb) cuda_check(cudaMemsetAsync(fb, 0, sizeof(long long) * count, st), "cudaMemsetAsync");
     else if (plan->d_fb_cap < B) {
       cudaFree(plan->d_fb);
+      plan->d_fb = nullptr;
+      plan->d_fb_cap = 0;
       cuda_check(cudaMalloc(&plan->d_fb, sizeof(unsigned long long) * B), "cudaMalloc");
       plan->d_fb_cap = B;
     }
-    struct Reset {  // the event belongs to this call only
+    struct Reset {  // the event and the flag array belong to this call only
       gpfb::Plan& p;
-      ~Reset() { p.front_done = nullptr; }
+      ~Reset() {
+        p.front_done = nullptr;
+        p.ill_out = nullptr;
+      }
     } reset{plan->plan};
     for (int f = 0; f < count; f += B) {
       const int n = std::min(B, count - f);
       plan->plan.front_done = f + n >= count ? static_cast<cudaEvent_t>(front_done) : nullptr;
+      plan->plan.ill_out = d_ill ? d_ill + f : nullptr;
       gpfb::run_frames_f32(plan->plan, d_in + f * npx, d_out + f * npx, n, fb ? fb + f : plan->d_fb, st);
     }
   });
 }
+}  // namespace
+
+extern "C" {
+
+gpf_status gpf_b200_filter_f32_ev(gpf_b200_plan* plan, const float* d_in, float* d_out, int count,
+                                  long long* d_fallbacks, void* stream, void* front_done) {
+  return filter_f32_impl(plan, d_in, d_out, count, d_fallbacks, nullptr, stream, front_done);
+}
 
 gpf_status gpf_b200_filter_f32(gpf_b200_plan* plan, const float* d_in, float* d_out, int count,
                                long long* d_fallbacks, void* stream) {
-  return gpf_b200_filter_f32_ev(plan, d_in, d_out, count, d_fallbacks, stream, nullptr);
+  return filter_f32_impl(plan, d_in, d_out, count, d_fallbacks, nullptr, stream, nullptr);
+}
+
+gpf_status gpf_b200_filter_f32_checked(gpf_b200_plan* plan, const float* d_in, float* d_out, int count,
+                                       long long* d_fallbacks, int* d_ill, void* stream) {
+  return filter_f32_impl(plan, d_in, d_out, count, d_fallbacks, d_ill, stream, nullptr);
 }
 
 gpf_status gpf_b200_exact_f32(const float* d_in, float* d_out, int width, int height, int count,

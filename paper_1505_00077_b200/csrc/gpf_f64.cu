@@ -211,63 +211,15 @@ __global__ void k_f64_combine(const double* __restrict__ f, const double* __rest
   if ((threadIdx.x & 31) == 0 && my_fb) atomicAdd(fallbacks, (unsigned long long)my_fb);
 }
 
-__global__ void __launch_bounds__(256) k_minmax_partial(const double* __restrict__ in, long long n,
-                                                        double* __restrict__ partials) {
-  double lo = INFINITY, hi = -INFINITY;
-  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n;
-       i += (long long)gridDim.x * blockDim.x) {
-    const double v = in[i];
-    lo = fmin(lo, v);
-    hi = fmax(hi, v);
-  }
-  for (int o = 16; o; o >>= 1) {
-    lo = fmin(lo, __shfl_xor_sync(0xffffffffu, lo, o));
-    hi = fmax(hi, __shfl_xor_sync(0xffffffffu, hi, o));
-  }
-  __shared__ double slo[8], shi[8];
-  if ((threadIdx.x & 31) == 0) {
-    slo[threadIdx.x >> 5] = lo;
-    shi[threadIdx.x >> 5] = hi;
-  }
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    for (int k = 1; k < 8; ++k) {
-      lo = fmin(lo, slo[k]);
-      hi = fmax(hi, shi[k]);
-    }
-    partials[2 * blockIdx.x] = lo;
-    partials[2 * blockIdx.x + 1] = hi;
-  }
-}
-
-__global__ void k_minmax_final(const double* __restrict__ partials, int blocks,
-                               double* __restrict__ scalars) {
-  if (threadIdx.x != 0) return;
-  double lo = INFINITY, hi = -INFINITY;
-  for (int b = 0; b < blocks; ++b) {
-    lo = fmin(lo, partials[2 * b]);
-    hi = fmax(hi, partials[2 * b + 1]);
-  }
-  scalars[1] = lo;
-  scalars[2] = hi;
-}
-
 void chk(cudaError_t e, const char* what) {
   if (e != cudaSuccess) throw Error{9, std::string(what) + ": " + cudaGetErrorString(e)};
 }
 
 }  // namespace
 
-void launch_minmax_f64(const double* d_in, long long n, double* partials, int blocks,
-                       double* scalars, cudaStream_t st) {
-  k_minmax_partial<<<blocks, 256, 0, st>>>(d_in, n, partials);
-  k_minmax_final<<<1, 32, 0, st>>>(partials, blocks, scalars);
-  chk(cudaGetLastError(), "kernel launch (minmax)");
-}
-
 size_t f64_workspace_bytes(int w, int h, int degree) {
   const size_t n = (size_t)w * h;
-  return sizeof(double) * (n * (2 + 2 * (size_t)(degree + 2)) + 2 + 2 * kF64MeanBlocks);
+  return sizeof(double) * (n * (2 + 2 * (size_t)(degree + 2)) + 2 + 4 * kF64MeanBlocks);
 }
 
 void F64Work::ensure(size_t bytes_needed) {
@@ -295,7 +247,7 @@ void run_gpf_f64_exact(const double* d_in, double* d_out, const Params& p, F64Wo
   double* Cb = R + (size_t)planes * n;
   double* scalars = Cb + (size_t)planes * n;
   double* partials = scalars + 2;
-  launch_mean_f64(d_in, n, p.centering, p.tc_fixed, partials, kF64MeanBlocks, scalars, st);
+  launch_mean_f64(d_in, n, p.centering, p.tc_fixed, p.sigma_r, partials, kF64MeanBlocks, scalars, st);
   const int blocks = (int)std::min<long long>((n + 255) / 256, 148 * 16);
   // GpfState::init: inv2s2 = 1.0 / (2.0 * sr * sr) (bilateral.cpp:92)
   const double inv2s2 = 1.0 / (2.0 * p.sigma_r * p.sigma_r);

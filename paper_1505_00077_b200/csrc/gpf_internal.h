@@ -128,13 +128,15 @@ struct Plan {
   alignas(64) CUtensorMap vstore;  // TMA map of V for the column pass's staged chunk stores
   alignas(64) CUtensorMap emmap;   // TMA map of EM: 32x32-pixel tiles for the column pass
   alignas(64) CUtensorMap emcmap;  // TMA map of EM: 64-column x 32-row tiles for the carry walk
-  double* scalars = nullptr;   // [batch][2]  t_c
-  double* partials = nullptr;  // [batch][mean_blocks][2]
+  double* scalars = nullptr;   // [batch][2]  t_c, max|H|
+  double* partials = nullptr;  // [batch][mean_blocks][4]
   size_t bytes = 0;
   int mean_blocks = 0;
   int launches_per_frame = 0;  // kernels per launch group (independent of batch)
   // optional event recorded after the column pass (set per call by the C ABI)
   cudaEvent_t front_done = nullptr;
+  // optional per-frame ill-conditioned flags of this launch group (device, set per call)
+  int* ill_out = nullptr;
   // optional per-stage timing: events recorded on the launching stream
   bool profile = false;
   struct StageTimer* timer = nullptr;
@@ -182,13 +184,11 @@ void run_taylor_f64(const double* d_in, double* d_out, int w, int h, double sigm
                     double kernel_scale, double sigma_r, int degree, unsigned long long* d_fb,
                     cudaStream_t st);
 // t_c of one fp64 frame (K0 double-double mean; 0 / tc_fixed per centering) into
-// scalars[0]; partials holds 2*blocks doubles.
-void launch_mean_f64(const double* d_in, long long n, int centering, double tc_fixed,
+// scalars[0];
+// scalars[1] = max|H| = max(f_max - t_c, t_c - f_min) / sigma_r; partials
+// holds 4*blocks doubles.
+void launch_mean_f64(const double* d_in, long long n, int centering, double tc_fixed, double sigma_r,
                      double* partials, int blocks, double* scalars, cudaStream_t st);
-// scalars[1], scalars[2] = min, max of the frame (the conditioning check of the
-// drop-in entry; scalars[0] = t_c from launch_mean_f64).
-void launch_minmax_f64(const double* d_in, long long n, double* partials, int blocks,
-                       double* scalars, cudaStream_t st);
 
 // Reference-exact fp64 GPF (gpf_f64.cu): the reference's own fp64 operation
 // sequence replayed on the GPU, for inputs whose degree-N series is too
@@ -218,6 +218,7 @@ void set_precision(int mode);
 int get_precision();
 int last_precision();       // mode this thread's last drop-in call ran (1 or 2; 0 = none)
 double last_max_abs_h();    // max |H| this thread's last drop-in call measured (auto mode)
+float last_device_ms();     // device time of its filter kernels (CUDA events; copies excluded)
 long long dropin_gpf(const double* h_in, double* h_out, const Params& p);  // throws Error
 void dropin_release();
 

@@ -87,13 +87,36 @@ __device__ void block_dd_reduce(double& hi, double& lo) {
   lo = slo[0];
 }
 
+__device__ void block_minmax_reduce(double& mn, double& mx) {
+  for (int o = 16; o; o >>= 1) {
+    mn = fmin(mn, __shfl_xor_sync(0xffffffffu, mn, o));
+    mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+  }
+  __shared__ double smn[kMeanThreads / 32], smx[kMeanThreads / 32];
+  if ((threadIdx.x & 31) == 0) {
+    smn[threadIdx.x >> 5] = mn;
+    smx[threadIdx.x >> 5] = mx;
+  }
+  __syncthreads();
+  mn = smn[0];
+  mx = smx[0];
+  for (int k = 1; k < kMeanThreads / 32; ++k) {
+    mn = fmin(mn, smn[k]);
+    mx = fmax(mx, smx[k]);
+  }
+}
+
+// Per block: (hi, lo) of the double-double sum, and the min / max of f (for
+// the conditioning measure max|H| of the frame).
 template <typename T>
 __global__ void __launch_bounds__(kMeanThreads) k_mean_partial(const T* __restrict__ in,
                                                                long long n,
                                                                double* __restrict__ partials) {
   in += (size_t)blockIdx.y * n;
-  partials += (size_t)blockIdx.y * gridDim.x * 2;
+  partials += (size_t)blockIdx.y * gridDim.x * 4;
   double hi = 0.0, lo = 0.0;
+  float mn = INFINITY, mx = -INFINITY;
+  double mnd = INFINITY, mxd = -INFINITY;
   const long long stride = (long long)gridDim.x * kMeanThreads;
   long long i0 = 0;
   if (sizeof(T) == 4 && (reinterpret_cast<uintptr_t>(in) & 15) == 0) {
@@ -103,6 +126,8 @@ __global__ void __launch_bounds__(kMeanThreads) k_mean_partial(const T* __restri
     for (long long i = (long long)blockIdx.x * kMeanThreads + threadIdx.x; i < n4; i += stride) {
       const float4 v = __ldg(in4 + i);
       const double e4[4] = {v.x, v.y, v.z, v.w};
+      mn = fminf(fminf(mn, v.x), fminf(fminf(v.y, v.z), v.w));
+      mx = fmaxf(fmaxf(mx, v.x), fmaxf(fmaxf(v.y, v.z), v.w));
 #pragma unroll
       for (int k = 0; k < 4; ++k) {
         double s, e;
@@ -114,31 +139,52 @@ __global__ void __launch_bounds__(kMeanThreads) k_mean_partial(const T* __restri
     i0 = n4 * 4;
   }
   for (long long i = i0 + (long long)blockIdx.x * kMeanThreads + threadIdx.x; i < n; i += stride) {
+    const double v = static_cast<double>(in[i]);
     double s, e;
-    two_sum(hi, static_cast<double>(in[i]), s, e);
+    two_sum(hi, v, s, e);
     hi = s;
     lo += e;
+    mnd = fmin(mnd, v);
+    mxd = fmax(mxd, v);
   }
+  mnd = fmin(mnd, (double)mn);
+  mxd = fmax(mxd, (double)mx);
   block_dd_reduce(hi, lo);
+  block_minmax_reduce(mnd, mxd);
   if (threadIdx.x == 0) {
-    partials[2 * blockIdx.x] = hi;
-    partials[2 * blockIdx.x + 1] = lo;
+    partials[4 * blockIdx.x] = hi;
+    partials[4 * blockIdx.x + 1] = lo;
+    partials[4 * blockIdx.x + 2] = mnd;
+    partials[4 * blockIdx.x + 3] = mxd;
   }
 }
 
+// scalars[2 f] = t_c, scalars[2 f + 1] = max|H| = max(f_max - t_c, t_c - f_min) / sigma_r;
+// ill[f] (optional) = 1 when max|H| lies outside the fp32 envelope.
 __global__ void __launch_bounds__(kMeanThreads) k_mean_final(const double* __restrict__ partials,
                                                              int nblocks, long long n,
                                                              int centering, double tc_fixed,
-                                                             double* __restrict__ scalars) {
-  partials += (size_t)blockIdx.x * nblocks * 2;
-  double hi = 0.0, lo = 0.0;
-  for (int b = threadIdx.x; b < nblocks; b += kMeanThreads)
-    dd_add(hi, lo, partials[2 * b], partials[2 * b + 1]);
+                                                             double inv_sr, double h_limit,
+                                                             double* __restrict__ scalars,
+                                                             int* __restrict__ ill) {
+  partials += (size_t)blockIdx.x * nblocks * 4;
+  double hi = 0.0, lo = 0.0, mn = INFINITY, mx = -INFINITY;
+  for (int b = threadIdx.x; b < nblocks; b += kMeanThreads) {
+    dd_add(hi, lo, partials[4 * b], partials[4 * b + 1]);
+    mn = fmin(mn, partials[4 * b + 2]);
+    mx = fmax(mx, partials[4 * b + 3]);
+  }
   block_dd_reduce(hi, lo);
-  if (threadIdx.x == 0)
+  block_minmax_reduce(mn, mx);
+  if (threadIdx.x == 0) {
     // centering 1: mean; 2: a fixed t_c (CenteringMode::midpoint, bilateral.cpp:77-82); 0: none
-    scalars[2 * blockIdx.x] =
+    const double t_c =
         centering == 1 ? (hi + lo) / static_cast<double>(n) : (centering == 2 ? tc_fixed : 0.0);
+    const double hmax = fmax(mx - t_c, t_c - mn) * inv_sr;
+    scalars[2 * blockIdx.x] = t_c;
+    scalars[2 * blockIdx.x + 1] = hmax;
+    if (ill) ill[blockIdx.x] = !(hmax <= h_limit);
+  }
 }
 
 // ----------------------------------------------------------------------------
@@ -1102,12 +1148,12 @@ void plan_init(Plan& plan, const Params& p, int device, int batch) {
     check(cudaMalloc(&plan.AH, ahb), "cudaMalloc(AH)");
     check(cudaMalloc(&plan.CH, ahb), "cudaMalloc(CH)");
     check(cudaMalloc(&plan.scalars, sizeof(double) * 2 * B), "cudaMalloc(scalars)");
-    check(cudaMalloc(&plan.partials, sizeof(double) * 2 * B * plan.mean_blocks), "cudaMalloc(partials)");
+    check(cudaMalloc(&plan.partials, sizeof(double) * 4 * B * plan.mean_blocks), "cudaMalloc(partials)");
   } catch (...) {
     plan_free(plan);
     throw;
   }
-  plan.bytes = vb + cab + 2 * ahb + emb + sizeof(double) * 2 * B * (1 + plan.mean_blocks);
+  plan.bytes = vb + cab + 2 * ahb + emb + sizeof(double) * 2 * B * (1 + 2 * plan.mean_blocks);
   // mean (2), [seed,] carries, column pass, row scan, row pass
   plan.launches_per_frame = 32 * pairs <= 512 ? 7 : 6;
   // TMA tensor maps of the band-major V: fp32 dims (inner first)
@@ -1308,7 +1354,8 @@ static void run_frames(Plan& plan, const Tin* d_in, Tout* d_out, int count,
   stage_mark(plan, kStageMean, st);
   k_mean_partial<Tin><<<dim3(plan.mean_blocks, count), kMeanThreads, 0, st>>>(d_in, npx, plan.partials);
   k_mean_final<<<count, kMeanThreads, 0, st>>>(plan.partials, plan.mean_blocks, npx,
-                                               plan.rc.centering, plan.rc.tc_fixed, plan.scalars);
+                                               plan.rc.centering, plan.rc.tc_fixed, plan.rc.inv_sr,
+                                               kH32Limit, plan.scalars, plan.ill_out);
   const int nthr = 32 * plan.rc.pairs;
   if (nthr <= 352) launch_passes<352>(plan, d_in, d_out, count, d_fb, st);  // N <= 20
   else if (nthr <= 384) launch_passes<384>(plan, d_in, d_out, count, d_fb, st);
@@ -1365,10 +1412,11 @@ void stage_reset(Plan& plan) {
   plan.timer = nullptr;
 }
 
-void launch_mean_f64(const double* d_in, long long n, int centering, double tc_fixed,
+void launch_mean_f64(const double* d_in, long long n, int centering, double tc_fixed, double sigma_r,
                      double* partials, int blocks, double* scalars, cudaStream_t st) {
   k_mean_partial<double><<<dim3(blocks, 1), kMeanThreads, 0, st>>>(d_in, n, partials);
-  k_mean_final<<<1, kMeanThreads, 0, st>>>(partials, blocks, n, centering, tc_fixed, scalars);
+  k_mean_final<<<1, kMeanThreads, 0, st>>>(partials, blocks, n, centering, tc_fixed, 1.0 / sigma_r,
+                                           kH32Limit, scalars, nullptr);
   check(cudaGetLastError(), "kernel launch (mean)");
 }
 

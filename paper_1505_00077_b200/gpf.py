@@ -217,6 +217,11 @@ def last_max_abs_h() -> float:
     return _lib.lib().gpf_b200_last_max_abs_h()
 
 
+def last_device_ms() -> float:
+    """Device time of the filter kernels of this thread's last gpf_filter_gpf call."""
+    return _lib.lib().gpf_b200_last_device_ms()
+
+
 def fp32_h_limit() -> float:
     return _lib.lib().gpf_b200_fp32_h_limit()
 
@@ -283,6 +288,14 @@ class Plan:
         fb = _ptr(d_fallbacks) if d_fallbacks is not None else None
         _check(_lib.lib().gpf_b200_filter_f32_ev(self.h, _ptr(d_in), _ptr(d_out), count, fb, stream,
                                                  front_done))
+
+    def filter_device_checked(self, d_in, d_out, count: int, d_fallbacks, d_ill,
+                              stream: int = 0) -> None:
+        """filter_device plus per-frame ill-conditioned flags (int32 device array):
+        1 where the frame lies outside the fp32 envelope (gpf_b200_filter_f32_checked)."""
+        fb = _ptr(d_fallbacks) if d_fallbacks is not None else None
+        _check(_lib.lib().gpf_b200_filter_f32_checked(self.h, _ptr(d_in), _ptr(d_out), count, fb,
+                                                      _ptr(d_ill), stream))
 
     def filter_host(self, h_in: np.ndarray, h_out: np.ndarray | None = None, stream: int = 0):
         """Host fp32 frames -> host fp32 frames (copies inside). Returns (out, fallbacks)."""

@@ -1,0 +1,159 @@
+"""The drop-in entry's machinery (dropin.cpp, capi.cpp) and the plan entries'
+robustness fixes: precision modes, plan cache, per-frame conditioning flags,
+misaligned device pointers, failed re-batching, device restore."""
+import numpy as np
+import pytest
+
+from paper_1505_00077_b200 import synth
+
+pytestmark = pytest.mark.gpu
+
+TOL = 1e-3
+
+
+def test_precision_modes_and_envelope(gpu, oracle):
+    """AUTO picks fp32 inside the envelope and the reference-exact fp64 mode
+    outside it; both forced modes run; the limit is the documented one."""
+    assert gpu.fp32_h_limit() == pytest.approx(7.0)
+    inside = synth.rects_image(256, 192, 8, 10.0, 3).astype(np.float64)   # sigma_r 40: max|H| ~ 3.7
+    outside = synth.checker_image(256, 192, 5.0, 4).astype(np.float64)    # sigma_r 10: max|H| 12.75
+    for img, sr, want in ((inside, 40.0, "fp32"), (outside, 10.0, "fp64")):
+        ref, rfb, tc = oracle.gpf(img, 4.0, sr, 20)
+        for mode in ("auto", "fp32", "fp64"):
+            gpu.set_precision(mode)
+            try:
+                out, fb = gpu.gpf_filter_gpf(img, gpu.spatial_params(4.0), gpu.range_params(sr, 20))
+            finally:
+                gpu.set_precision("auto")
+            ran = gpu.last_precision()
+            assert ran == (want if mode == "auto" else mode)
+            if mode == "auto":
+                hm = max(img.max() - tc, tc - img.min()) / sr
+                assert gpu.last_max_abs_h() == pytest.approx(hm, rel=1e-12)
+            if ran == "fp64" or want == "fp32":
+                assert fb == rfb and np.abs(out - ref).max() <= TOL, (mode, want)
+
+
+def test_fp64_mode_large_degree(gpu, oracle):
+    """Degrees above the fp32 kernels' limit (48) run the fp64 mode (<= 62)."""
+    img = synth.rects_image(64, 48, 4, 10.0, 5).astype(np.float64)
+    for deg in (49, 62):
+        ref, rfb, _ = oracle.gpf(img, 3.0, 60.0, deg)
+        out, fb = gpu.gpf_filter_gpf(img, gpu.spatial_params(3.0), gpu.range_params(60.0, deg))
+        assert gpu.last_precision() == "fp64"
+        assert fb == rfb and np.abs(out - ref).max() <= 1e-9
+    with pytest.raises(gpu.GpfError):
+        gpu.gpf_filter_gpf(img, gpu.spatial_params(3.0), gpu.range_params(60.0, 63))
+    gpu.set_precision("fp32")
+    try:
+        with pytest.raises(gpu.GpfError):
+            gpu.gpf_filter_gpf(img, gpu.spatial_params(3.0), gpu.range_params(60.0, 49))
+    finally:
+        gpu.set_precision("auto")
+
+
+def test_fp64_mode_matches_reference_goldens(gpu, golden):
+    """The fp64 mode replays the reference's arithmetic: the golden cases agree
+    to round-off (only exp() differs), far inside the bar."""
+    gpu.set_precision("fp64")
+    try:
+        for name in [str(n) for n in golden["__names__"]]:
+            img = golden[f"{name}/in"]
+            ss, sr, deg, cen, ks = golden[f"{name}/params"]
+            out, fb = gpu.gpf_filter_gpf(img, gpu.spatial_params(ss, kernel_scale=ks),
+                                         gpu.range_params(sr, int(deg)), centering=int(cen))
+            ref = golden[f"{name}/out"]
+            assert fb == int(golden[f"{name}/fb"]), name
+            assert np.abs(out - ref).max() <= 1e-9 * max(1.0, np.abs(ref).max()), name
+    finally:
+        gpu.set_precision("auto")
+
+
+def test_dropin_repeated_call_allocates_nothing(gpu):
+    """A second call with the same shape and parameters reuses the cached plan,
+    buffers and pinned images: device free memory is unchanged."""
+    import torch
+    img = synth.rects_image(1024, 768, 16, 10.0, 8).astype(np.float64)
+    sp, rp = gpu.spatial_params(5.0), gpu.range_params(30.0, 20)
+    a, _ = gpu.gpf_filter_gpf(img, sp, rp)
+    torch.cuda.synchronize()
+    free0 = torch.cuda.mem_get_info()[0]
+    b, _ = gpu.gpf_filter_gpf(img, sp, rp)
+    free1 = torch.cuda.mem_get_info()[0]
+    assert free1 == free0
+    np.testing.assert_array_equal(a, b)
+    gpu.dropin_release()
+    assert torch.cuda.mem_get_info()[0] > free1
+
+
+def test_checked_entry_flags(gpu):
+    """gpf_b200_filter_f32_checked flags exactly the frames outside the fp32
+    envelope, computed on the device from each frame."""
+    import torch
+    w, h = 320, 200
+    good = synth.rects_image(w, h, 8, 10.0, 1)                       # sigma_r 10: rects ~ up to 15
+    calm = np.clip(good * 0.2 + 100.0, 0, 255).astype(np.float32)    # narrow range: inside
+    frames = np.stack([calm, good, calm])
+    plan = gpu.Plan(w, h, 3.0, 10.0, 20, batch=2)
+    d_in = torch.from_numpy(frames).cuda()
+    d_out = torch.empty_like(d_in)
+    d_ill = torch.full((3,), -1, dtype=torch.int32, device="cuda")
+    plan.filter_device_checked(d_in, d_out, 3, None, d_ill, torch.cuda.current_stream().cuda_stream)
+    torch.cuda.synchronize()
+    hm = [max(f.max() - f.astype(np.float64).mean(), f.astype(np.float64).mean() - f.min()) / 10.0
+          for f in frames]
+    want = [int(v > gpu.fp32_h_limit()) for v in hm]
+    assert d_ill.cpu().tolist() == want and want == [0, 1, 0]
+
+
+def test_misaligned_device_input(gpu):
+    """A frame starting 4 bytes past a 16-B boundary: no vector
+    load faults, same result as the aligned copy."""
+    import torch
+    w, h = 256, 64
+    img = torch.from_numpy(synth.rects_image(w, h, 4, 10.0, 2)).cuda()
+    buf = torch.empty(w * h + 1, device="cuda")
+    buf[1:].copy_(img.reshape(-1))
+    mis = buf[1:].view(h, w)
+    assert mis.data_ptr() % 16 == 4
+    plan = gpu.Plan(w, h, 3.0, 30.0, 20)
+    s = torch.cuda.current_stream().cuda_stream
+    a, b = torch.empty_like(img), torch.empty_like(img)
+    plan.filter_device(img, a, 1, None, s)
+    plan.filter_device(mis, b, 1, None, s)
+    torch.cuda.synchronize()
+    assert torch.equal(a, b)
+
+
+def test_failed_rebatch_keeps_plan_usable(gpu):
+    """plan_set_batch that cannot allocate returns an error and leaves the
+    plan's previous workspace intact."""
+    import ctypes as C
+    import torch
+    from paper_1505_00077_b200 import _lib
+    w = h = 4096
+    plan = gpu.Plan(w, h, 3.0, 30.0, 20)
+    st = _lib.lib().gpf_b200_plan_set_batch(plan.h, 100000)  # petabytes
+    assert st != 0
+    img = torch.from_numpy(synth.rects_image(512, 512, 4, 10.0, 2)).cuda()
+    img = torch.nn.functional.interpolate(img[None, None], size=(h, w))[0, 0].contiguous()
+    out = torch.empty_like(img)
+    plan.filter_device(img, out, 1, None, torch.cuda.current_stream().cuda_stream)
+    torch.cuda.synchronize()
+    assert torch.isfinite(out).all()
+    del C
+
+
+def test_plan_create_restores_current_device(gpu):
+    import ctypes as C
+    import torch
+    from paper_1505_00077_b200 import _lib
+    torch.cuda.set_device(0)
+    sp, rp = gpu.spatial_params(2.0), gpu.range_params(30.0, 20)
+    h = C.c_void_p()
+    assert _lib.lib().gpf_b200_plan_create(64, 64, C.byref(sp), C.byref(rp), 1, 0, C.byref(h)) == 0
+    assert torch.cuda.current_device() == 0
+    _lib.lib().gpf_b200_plan_destroy(h)
+    # the fp32 plan entries reject degrees above their kernels' limit with one message
+    with pytest.raises(gpu.GpfError, match="48"):
+        gpu.Plan(64, 64, 2.0, 30.0, 49)
