@@ -1,0 +1,111 @@
+// gpfilter.hpp -- C++ entry point of the B200 GPF path.
+//
+// The reference's C++ API for the Gauss-polynomial filter is
+//   gpfilter::gpf(const Image&, const SpatialParams&, const RangeParams&,
+//                 SpatialBackend, const GpfOptions& = {}) -> FilterResult
+// (/root/reference/proj/src/core/bilateral.hpp:73-75, "ref" below), the only
+// way to reach midpoint centering (ref bilateral.hpp:15-21). This header
+// declares the same names, members, defaults and exceptions in namespace
+// gpfilter, so C++ callers of that path recompile against libgpfilter_b200.so
+// unchanged:
+//   Image                ref image.hpp:14-41 (row-major doubles, w, h >= 1)
+//   IntensityRange       ref image.hpp:44-47
+//   Boundary, SpatialParams, SigmaTooSmallError, default_window_radius
+//                        ref spatial.hpp:13-34
+//   RangeParams          ref range_kernel.hpp:13-18
+//   SpatialBackend, CenteringMode, GpfOptions, FilterResult, gpf, kQMin
+//                        ref bilateral.hpp:13-28, 73-85
+// Errors are thrown as in the reference: std::invalid_argument for invalid
+// parameters (same messages), SigmaTooSmallError for sigma_s < 0.5 on the
+// recursive backend; GPU failures as std::runtime_error. The filter runs on the
+// current CUDA device through the drop-in engine of gpf_filter_gpf (plan cache,
+// AUTO precision: fp32 planes inside their validated envelope, the
+// reference-exact fp64 mode outside it; gpfilter_b200.h).
+#ifndef GPFILTER_B200_GPFILTER_HPP
+#define GPFILTER_B200_GPFILTER_HPP
+
+#include <cstddef>
+#include <stdexcept>
+#include <vector>
+
+namespace gpfilter {
+
+class Image {
+ public:
+  Image() = default;
+  Image(int width, int height, double fill = 0.0);  // throws std::invalid_argument if w or h < 1
+
+  int width() const { return width_; }
+  int height() const { return height_; }
+  std::size_t pixels() const { return samples_.size(); }
+
+  double* data() { return samples_.data(); }
+  const double* data() const { return samples_.data(); }
+
+  double& at(int row, int col) { return samples_[static_cast<std::size_t>(row) * width_ + col]; }
+  double at(int row, int col) const { return samples_[static_cast<std::size_t>(row) * width_ + col]; }
+
+  bool same_size(const Image& o) const { return width_ == o.width_ && height_ == o.height_; }
+
+ private:
+  int width_ = 0;
+  int height_ = 0;
+  std::vector<double> samples_;
+};
+
+struct IntensityRange {
+  double low = 0.0;
+  double high = 255.0;
+};
+
+enum class Boundary { replicate, reflect, zero };
+
+struct SigmaTooSmallError : std::invalid_argument {
+  using std::invalid_argument::invalid_argument;
+};
+
+struct SpatialParams {
+  double sigma_s = 2.0;
+  int window_radius = 6;
+  Boundary boundary = Boundary::replicate;
+  double kernel_scale = 1.0;
+
+  static SpatialParams make(double sigma_s);  // window_radius = ceil(3 sigma_s)
+  void validate() const;                      // throws std::invalid_argument
+};
+
+int default_window_radius(double sigma_s);
+
+struct RangeParams {
+  double sigma_r = 30.0;
+  int degree = 20;
+
+  void validate() const;  // throws std::invalid_argument
+};
+
+enum class SpatialBackend { direct, recursive };
+
+enum class CenteringMode { mean, midpoint };
+
+struct GpfOptions {
+  bool centering = true;
+  CenteringMode mode = CenteringMode::mean;
+  IntensityRange range;  // midpoint mode: t_c = (low + high) / 2
+};
+
+struct FilterResult {
+  Image image;
+  long long fallback_count = 0;
+};
+
+// Constant-time Gauss-polynomial bilateral filter on the GPU. The recursive
+// backend only (SpatialBackend::direct throws std::invalid_argument); degree
+// <= 62.
+FilterResult gpf(const Image& img, const SpatialParams& sp, const RangeParams& rp,
+                 SpatialBackend backend, const GpfOptions& opts = {});
+
+inline constexpr double kQMin = 1e-8;
+
+}  // namespace gpfilter
+
+#endif  // GPFILTER_B200_GPFILTER_HPP

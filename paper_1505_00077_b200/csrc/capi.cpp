@@ -135,7 +135,10 @@ gpf_status fail(gpf_status s, const std::string& msg) {
 }
 
 void cuda_check(cudaError_t e, const char* what) {
-  if (e != cudaSuccess) throw gpfb::Error{GPF_ERR_UNKNOWN, std::string(what) + ": " + cudaGetErrorString(e)};
+  if (e != cudaSuccess) {
+    cudaGetLastError();  // clear a non-sticky error (e.g. a failed allocation) for the caller
+    throw gpfb::Error{GPF_ERR_UNKNOWN, std::string(what) + ": " + cudaGetErrorString(e)};
+  }
 }
 
 template <typename Fn>
@@ -406,7 +409,8 @@ gpf_status gpf_filter_exact(const gpf_image* in, const gpf_spatial_params* sp,
     DevBuf din(n * sizeof(double)), dout(n * sizeof(double));
     cuda_check(cudaMemcpy(din.p, in->px, n * sizeof(double), cudaMemcpyHostToDevice), "H2D");
     gpfb::run_exact_f64(static_cast<const double*>(din.p), static_cast<double*>(dout.p), in->w, in->h,
-                        1, W, static_cast<int>(sp->boundary), sp->sigma_s, rp->sigma_r, nullptr);
+                        1, W, static_cast<int>(sp->boundary), sp->sigma_s, rp->sigma_r,
+                        sp->kernel_scale, nullptr);
     auto* res = new gpf_image(in->w, in->h);
     std::unique_ptr<gpf_image> hold(res);
     cuda_check(cudaMemcpy(res->px, dout.p, n * sizeof(double), cudaMemcpyDeviceToHost), "D2H");

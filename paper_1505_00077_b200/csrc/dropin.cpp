@@ -4,7 +4,8 @@
 // The reference call takes a host image of doubles and returns a new one. Here
 // one call = H2D of the frame, the filter on the GPU, D2H of the result, with
 // everything the call needs kept per device between calls:
-//   * an LRU of fp32 plans keyed by every filter parameter (a repeated call
+//   * an LRU of up to 8 fp32 plans (64 GiB of workspace) keyed by every filter
+//     parameter -- a C3 sigma_s sweep keeps all five plans -- (a repeated call
 //     with the same shape and parameters performs no cudaMalloc and no
 //     tensor-map encode),
 //   * the fp64 precision mode's workspace, device in/out buffers, the fallback
@@ -44,7 +45,8 @@ const double kH32Limit = 7.0;
 
 namespace {
 
-constexpr int kDropinPlans = 4;  // cached fp32 plans per device
+constexpr int kDropinPlans = 8;                        // cached fp32 plans per device
+constexpr size_t kDropinPlanBytes = size_t(64) << 30;  // and at most this much workspace
 constexpr int kStatBlocks = 592;
 
 std::atomic<int> g_precision{-1};
@@ -53,7 +55,10 @@ thread_local double t_last_hmax = 0.0;
 thread_local float t_last_device_ms = 0.f;
 
 void chk(cudaError_t e, const char* what) {
-  if (e != cudaSuccess) throw Error{9, std::string(what) + ": " + cudaGetErrorString(e)};
+  if (e != cudaSuccess) {
+    cudaGetLastError();  // clear a non-sticky error (e.g. a failed allocation) for the caller
+    throw Error{9, std::string(what) + ": " + cudaGetErrorString(e)};
+  }
 }
 
 int precision_from_env() {
@@ -145,14 +150,26 @@ void with_retry(DevCtx& c, Fn&& fn) {
   }
 }
 
+// device workspace of a single-frame fp32 plan (plan_init's allocation)
+size_t plan_bytes_estimate(const Params& p) {
+  const size_t pairs = (size_t)(p.degree + 3) / 2;
+  const size_t ny = (p.height + kTile - 1) / kTile, nx = (p.width + kTile - 1) / kTile;
+  return 8 * pairs * p.width * ny * kTile + 32 * ny * pairs * p.width + 64 * nx * pairs * p.height +
+         8 * (size_t)(p.width + 1) * p.height;
+}
+
 Plan& cached_plan(DevCtx& c, const Params& p) {
   for (auto it = c.plans.begin(); it != c.plans.end(); ++it)
     if (same_params((*it)->p, p)) {
       c.plans.splice(c.plans.begin(), c.plans, it);
       return *c.plans.front();
     }
-  if ((int)c.plans.size() >= kDropinPlans) {
+  size_t held = 0;
+  for (auto& q : c.plans) held += q->bytes;
+  while (!c.plans.empty() &&
+         ((int)c.plans.size() >= kDropinPlans || held + plan_bytes_estimate(p) > kDropinPlanBytes)) {
     chk(cudaStreamSynchronize(c.st), "cudaStreamSynchronize");
+    held -= c.plans.back()->bytes;
     plan_free(*c.plans.back());
     c.plans.pop_back();
   }

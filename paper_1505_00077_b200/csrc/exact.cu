@@ -16,6 +16,7 @@
 // (spatial and range exponents folded). Sums run in fp32 over one row of taps
 // (<= 2W+1 terms) and in fp64 across rows.
 #include <algorithm>
+#include <cmath>
 #include <cstdint>
 #include <string>
 
@@ -88,6 +89,58 @@ __global__ void __launch_bounds__(32 * kExactWarps) k_exact(const T* __restrict_
   if (x < w) out[(size_t)r * w + x] = static_cast<T>(static_cast<double>(fc) + num / den);
 }
 
+// fp64 form for the reference-facing gpf_filter_exact: the reference's own
+// operation sequence per pixel (bilateral.cpp:31-52) with explicitly rounded,
+// never-contracted fp64 operations; the spatial weight table ws[a][b] =
+// kernel_scale * spatial_weight(a, b, sigma_s) is the reference's own
+// expression evaluated once on the host (spatial.cpp:37-41), so only the range
+// factor's exp() is CUDA's instead of glibc's (<= 1 ulp). A warp owns 32
+// output pixels of one row and stages each boundary-mapped input row segment
+// in shared memory (coalesced loads); taps of zero padding are skipped.
+__device__ __forceinline__ double dm_(double a, double b) { return __dmul_rn(a, b); }
+__device__ __forceinline__ double da_(double a, double b) { return __dadd_rn(a, b); }
+
+__global__ void __launch_bounds__(32 * kExactWarps) k_exact64(const double* __restrict__ in_all,
+                                                              double* __restrict__ out_all, int w,
+                                                              int h, int W, int boundary,
+                                                              const double* __restrict__ ws,
+                                                              double inv2s2) {
+  extern __shared__ double seg64_all[];  // [warps][32 + 2W]
+  const int lane = threadIdx.x, warp = threadIdx.y, f = blockIdx.z;
+  const int span = 32 + 2 * W;
+  double* seg = seg64_all + warp * span;
+  int* ok = reinterpret_cast<int*>(seg64_all + kExactWarps * span) + warp * span;
+  const int x0 = blockIdx.x * 32, x = x0 + lane;
+  const int r = blockIdx.y * kExactWarps + warp;
+  if (r >= h) return;  // warp-uniform; no CTA barrier below
+  const double* in = in_all + (size_t)f * w * h;
+  double* out = out_all + (size_t)f * w * h;
+  const double fc = in[(size_t)r * w + min(x, w - 1)];
+  const int n = 2 * W + 1;
+  double num = 0.0, den = 0.0;
+  for (int a = -W; a <= W; ++a) {
+    const int rr = bidx(r + a, h, boundary);
+    if (rr < 0) continue;  // zero padding contributes nothing (bilateral.cpp:39)
+    const double* src = in + (size_t)rr * w;
+    __syncwarp();
+    for (int j = lane; j < span; j += 32) {
+      const int cc = bidx(x0 - W + j, w, boundary);
+      seg[j] = cc >= 0 ? src[cc] : 0.0;
+      ok[j] = cc >= 0;
+    }
+    __syncwarp();
+    const double* wrow = ws + (size_t)(a + W) * n;
+    for (int b = -W; b <= W; ++b) {
+      if (!ok[lane + W + b]) continue;  // bilateral.cpp:42
+      const double d = __dsub_rn(seg[lane + W + b], fc);
+      const double wgt = dm_(wrow[b + W], exp(dm_(-dm_(d, d), inv2s2)));
+      num = da_(num, dm_(wgt, d));
+      den = da_(den, wgt);
+    }
+  }
+  if (x < w) out[(size_t)r * w + x] = da_(fc, __ddiv_rn(num, den));
+}
+
 // ---------------------------------------------------------------- metrics
 // sum (ref - test)^2 and max |ref - test| over the interior, as exact
 // double-double partial sums per CTA (order-independent up to the final tree,
@@ -143,7 +196,10 @@ __global__ void __launch_bounds__(kCmpThreads) k_cmp_partial(const T* __restrict
 }
 
 void check_(cudaError_t e, const char* what) {
-  if (e != cudaSuccess) throw Error{9, std::string(what) + ": " + cudaGetErrorString(e)};
+  if (e != cudaSuccess) {
+    cudaGetLastError();  // clear a non-sticky error (e.g. a failed allocation) for the caller
+    throw Error{9, std::string(what) + ": " + cudaGetErrorString(e)};
+  }
 }
 
 template <typename T>
@@ -171,8 +227,42 @@ void run_exact_f32(const float* d_in, float* d_out, int w, int h, int count, int
 }
 
 void run_exact_f64(const double* d_in, double* d_out, int w, int h, int count, int W, int boundary,
-                   double sigma_s, double sigma_r, cudaStream_t st) {
-  run_exact<double>(d_in, d_out, w, h, count, W, boundary, sigma_s, sigma_r, st);
+                   double sigma_s, double sigma_r, double kernel_scale, cudaStream_t st) {
+  if (count <= 0) return;
+  const int n = 2 * W + 1;
+  // ws[a][b] = kernel_scale * spatial_weight(a, b, sigma_s) (bilateral.cpp:23-28, spatial.cpp:37-41)
+  double* hws = nullptr;
+  check_(cudaMallocHost(&hws, sizeof(double) * n * n), "cudaMallocHost");
+  for (int a = -W; a <= W; ++a)
+    for (int b = -W; b <= W; ++b) {
+      const double r2 = static_cast<double>(a) * a + static_cast<double>(b) * b;
+      hws[(a + W) * n + (b + W)] = kernel_scale * std::exp(-r2 / (2.0 * sigma_s * sigma_s));
+    }
+  double* dws = nullptr;
+  cudaError_t e = cudaMallocAsync(&dws, sizeof(double) * n * n, st);
+  if (e == cudaSuccess) e = cudaMemcpyAsync(dws, hws, sizeof(double) * n * n, cudaMemcpyHostToDevice, st);
+  if (e != cudaSuccess) {
+    cudaFreeHost(hws);
+    check_(e, "exact filter weights");
+  }
+  const double inv2s2 = 1.0 / (2.0 * sigma_r * sigma_r);  // bilateral.cpp:29
+  const size_t smem = (sizeof(double) + sizeof(int)) * kExactWarps * (32 + 2 * (size_t)W);
+  if (smem > 227 * 1024) {
+    cudaFreeAsync(dws, st);
+    cudaStreamSynchronize(st);
+    cudaFreeHost(hws);
+    throw Error{1, "exact filter: window radius too large for the GPU kernel"};
+  }
+  check_(cudaFuncSetAttribute(k_exact64, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem),
+         "cudaFuncSetAttribute");
+  const dim3 grid((w + 31) / 32, (h + kExactWarps - 1) / kExactWarps, count);
+  k_exact64<<<grid, dim3(32, kExactWarps), smem, st>>>(d_in, d_out, w, h, W, boundary, dws, inv2s2);
+  e = cudaGetLastError();
+  cudaFreeAsync(dws, st);
+  const cudaError_t e2 = cudaStreamSynchronize(st);  // the pinned table may be released
+  cudaFreeHost(hws);
+  check_(e, "kernel launch");
+  check_(e2, "exact filter");
 }
 
 // mse / max_abs / pixels of (ref, test) over the interior (metrics.cpp:20-56);

@@ -212,7 +212,10 @@ __global__ void k_f64_combine(const double* __restrict__ f, const double* __rest
 }
 
 void chk(cudaError_t e, const char* what) {
-  if (e != cudaSuccess) throw Error{9, std::string(what) + ": " + cudaGetErrorString(e)};
+  if (e != cudaSuccess) {
+    cudaGetLastError();  // clear a non-sticky error (e.g. a failed allocation) for the caller
+    throw Error{9, std::string(what) + ": " + cudaGetErrorString(e)};
+  }
 }
 
 }  // namespace

@@ -167,8 +167,9 @@ void run_frames_f64(Plan& plan, const double* d_in, double* d_out, int count,
 // `count` frames; boundary 0 replicate, 1 reflect, 2 zero (exact.cu).
 void run_exact_f32(const float* d_in, float* d_out, int w, int h, int count, int W, int boundary,
                    double sigma_s, double sigma_r, cudaStream_t st);
+// fp64 form: the reference's per-pixel operation sequence (fp64 taps).
 void run_exact_f64(const double* d_in, double* d_out, int w, int h, int count, int W, int boundary,
-                   double sigma_s, double sigma_r, cudaStream_t st);
+                   double sigma_s, double sigma_r, double kernel_scale, cudaStream_t st);
 // metrics::compare (metrics.cpp:20-56) on device images; synchronises st.
 struct ErrorStats {
   double mse = 0.0, max_abs = 0.0;

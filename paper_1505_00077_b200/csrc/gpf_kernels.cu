@@ -1059,7 +1059,10 @@ __global__ void k_gauss_cols(const double* __restrict__ tmp, double* __restrict_
 // Host side
 // ----------------------------------------------------------------------------
 static void check(cudaError_t e, const char* what) {
-  if (e != cudaSuccess) throw Error{9, std::string(what) + ": " + cudaGetErrorString(e)};
+  if (e != cudaSuccess) {
+    cudaGetLastError();  // clear a non-sticky error (e.g. a failed allocation) for the caller
+    throw Error{9, std::string(what) + ": " + cudaGetErrorString(e)};
+  }
 }
 
 template <typename Tin>

@@ -76,7 +76,10 @@ __global__ void k_taylor_combine(const double* __restrict__ f, const double* __r
 }
 
 void check_(cudaError_t e, const char* what) {
-  if (e != cudaSuccess) throw Error{9, std::string(what) + ": " + cudaGetErrorString(e)};
+  if (e != cudaSuccess) {
+    cudaGetLastError();  // clear a non-sticky error (e.g. a failed allocation) for the caller
+    throw Error{9, std::string(what) + ": " + cudaGetErrorString(e)};
+  }
 }
 
 }  // namespace
@@ -90,10 +93,15 @@ void run_taylor_f64(const double* d_in, double* d_out, int w, int h, double sigm
   const int K = degree / 2;
   const int planes = 2 * K + 2;
   double *mbar = nullptr, *mom = nullptr, *mom2 = nullptr, *tmp = nullptr;
-  check_(cudaMallocAsync(&mbar, sizeof(double) * n * planes, st), "cudaMallocAsync");
-  check_(cudaMallocAsync(&mom, sizeof(double) * n, st), "cudaMallocAsync");
-  check_(cudaMallocAsync(&mom2, sizeof(double) * n, st), "cudaMallocAsync");
-  check_(cudaMallocAsync(&tmp, sizeof(double) * n, st), "cudaMallocAsync");
+  cudaError_t e = cudaMallocAsync(&mbar, sizeof(double) * n * planes, st);
+  if (e == cudaSuccess) e = cudaMallocAsync(&mom, sizeof(double) * n, st);
+  if (e == cudaSuccess) e = cudaMallocAsync(&mom2, sizeof(double) * n, st);
+  if (e == cudaSuccess) e = cudaMallocAsync(&tmp, sizeof(double) * n, st);
+  if (e != cudaSuccess) {  // release what was allocated before the failure
+    for (double* p : {mbar, mom, mom2, tmp})
+      if (p) cudaFreeAsync(p, st);
+    check_(e, "cudaMallocAsync (Taylor workspace)");
+  }
   const double mass = kernel_mass_1d(sigma_s, default_window_radius(sigma_s));
   const double scale = mass * mass * kernel_scale;  // recursive_gaussian's output scale
   const int blocks = (int)std::min<long long>((n + 255) / 256, 148 * 8);

@@ -1,0 +1,66 @@
+// TEST INFRASTRUCTURE: one program, compiled twice -- against the reference's
+// C++ core (proj/src/core/bilateral.hpp, linked with oracle/_ref's library;
+// oracle/Makefile) and against the B200 library's C++ entry point
+// (include/gpfilter/gpfilter.hpp; paper_1505_00077_b200/Makefile) -- so that
+// tests/test_cxx_api.py runs the same gpfilter::gpf call through both.
+//
+//   driver IN.raw W H OUT.raw SIGMA_S SIGMA_R DEGREE CENTERING MODE LOW HIGH BACKEND
+//          KERNEL_SCALE WINDOW_RADIUS
+// IN/OUT: W*H little-endian doubles; MODE mean|midpoint; BACKEND direct|recursive.
+// Prints "ok <fallback_count>" or "error <exception type> <message>".
+#include <cstdio>
+#include <cstdlib>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#ifdef GPF_B200
+#include "gpfilter/gpfilter.hpp"
+#else
+#include "core/bilateral.hpp"
+#endif
+
+using namespace gpfilter;
+
+int main(int argc, char** argv) {
+  if (argc != 15) {
+    std::fprintf(stderr, "usage: see source\n");
+    return 2;
+  }
+  const int w = std::atoi(argv[2]), h = std::atoi(argv[3]);
+  SpatialParams sp;
+  sp.sigma_s = std::atof(argv[5]);
+  sp.kernel_scale = std::atof(argv[13]);
+  sp.window_radius = std::atoi(argv[14]);
+  RangeParams rp;
+  rp.sigma_r = std::atof(argv[6]);
+  rp.degree = std::atoi(argv[7]);
+  GpfOptions opts;
+  opts.centering = std::atoi(argv[8]) != 0;
+  opts.mode = std::strcmp(argv[9], "midpoint") == 0 ? CenteringMode::midpoint : CenteringMode::mean;
+  opts.range.low = std::atof(argv[10]);
+  opts.range.high = std::atof(argv[11]);
+  const SpatialBackend be =
+      std::strcmp(argv[12], "direct") == 0 ? SpatialBackend::direct : SpatialBackend::recursive;
+  try {
+    Image img;
+    if (w > 0 && h > 0) {
+      img = Image(w, h);
+      FILE* f = std::fopen(argv[1], "rb");
+      if (!f || std::fread(img.data(), sizeof(double), img.pixels(), f) != img.pixels()) return 3;
+      std::fclose(f);
+    }
+    const FilterResult r = gpf(img, sp, rp, be, opts);
+    FILE* o = std::fopen(argv[4], "wb");
+    std::fwrite(r.image.data(), sizeof(double), r.image.pixels(), o);
+    std::fclose(o);
+    std::printf("ok %lld\n", r.fallback_count);
+  } catch (const SigmaTooSmallError& e) {
+    std::printf("error SigmaTooSmallError %s\n", e.what());
+  } catch (const std::invalid_argument& e) {
+    std::printf("error invalid_argument %s\n", e.what());
+  } catch (const std::exception& e) {
+    std::printf("error runtime_error %s\n", e.what());
+  }
+  return 0;
+}

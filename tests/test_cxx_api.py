@@ -1,0 +1,91 @@
+"""The C++ entry point gpfilter::gpf (include/gpfilter/gpfilter.hpp) against the
+reference's own C++ core (proj/src/core/bilateral.hpp:73-75, built unmodified
+into oracle/_ref by oracle/Makefile): tests/cxx/gpf_cxx_driver.cpp is compiled
+against each, and both binaries get the same arguments and input.
+
+CPU: the exceptions (type and message) of the validation path, which runs
+before any device work. GPU: the filtered images, including the midpoint
+centering mode that only the C++ API reaches (ref bilateral.hpp:15-21).
+"""
+import os
+import subprocess
+import tempfile
+
+import numpy as np
+import pytest
+
+from paper_1505_00077_b200 import synth
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+OURS = os.path.join(ROOT, "tests", "cxx", "gpf_cxx_driver_b200")
+REF = os.path.join(ROOT, "oracle", "_ref", "gpf_cxx_driver_ref")
+
+
+def drive(binary, img, ss=3.0, sr=30.0, deg=20, cen=1, mode="mean", low=0.0, high=255.0,
+          backend="recursive", ks=1.0, radius=9):
+    if not os.path.exists(binary):
+        pytest.skip(f"{binary} not built")
+    with tempfile.TemporaryDirectory() as d:
+        src, dst = os.path.join(d, "in.raw"), os.path.join(d, "out.raw")
+        h, w = img.shape if img is not None else (0, 0)
+        if img is not None:
+            np.ascontiguousarray(img, dtype="<f8").tofile(src)
+        out = subprocess.run([binary, src, str(w), str(h), dst, repr(ss), repr(sr), str(deg), str(cen),
+                              mode, repr(low), repr(high), backend, repr(ks), str(radius)],
+                             capture_output=True, text=True, timeout=600)
+        assert out.returncode == 0, out.stderr
+        line = out.stdout.strip()
+        if line.startswith("ok"):
+            return int(line.split()[1]), np.fromfile(dst, dtype="<f8").reshape(h, w)
+        _, kind, msg = line.split(" ", 2)
+        return kind, msg
+
+
+ERROR_CASES = [
+    dict(ss=0.4),                    # SigmaTooSmallError, "direct" in the message
+    dict(ss=0.0),                    # SpatialParams: sigma_s must be > 0
+    dict(radius=0),                  # SpatialParams: window_radius must be >= 1
+    dict(ks=0.0),                    # SpatialParams: kernel_scale must be > 0
+    dict(sr=0.0),                    # RangeParams: sigma_r must be > 0
+    dict(deg=-1),                    # RangeParams: degree must be >= 0
+    dict(low=200.0, high=100.0),     # GpfOptions: range.low must be < range.high
+    dict(low=5.0, high=5.0, cen=0),  # checked even with centering off
+]
+
+
+@pytest.mark.parametrize("case", ERROR_CASES, ids=[str(c) for c in ERROR_CASES])
+def test_exceptions_match_reference(case):
+    img = synth.rects_image(16, 12, 2, 10.0, 1).astype(np.float64)
+    ref = drive(REF, img, **case)
+    ours = drive(OURS, img, **case)
+    assert isinstance(ref[0], str) and ref == ours, (ref, ours)
+
+
+def test_empty_image_rejected_like_reference():
+    ref = drive(REF, None)
+    ours = drive(OURS, None)
+    assert ref == ours == ("invalid_argument", "Image dimensions must be >= 1")
+
+
+def test_direct_backend_is_not_provided():
+    img = synth.rects_image(16, 12, 2, 10.0, 1).astype(np.float64)
+    kind, msg = drive(OURS, img, backend="direct")
+    assert kind == "invalid_argument" and "direct" in msg and "recursive" in msg
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("opts", [
+    dict(),                                        # mean centering (gpf_filter_gpf's default)
+    dict(mode="midpoint"),                         # t_c = 127.5
+    dict(mode="midpoint", low=20.0, high=120.0),   # t_c = 70
+    dict(cen=0),                                   # no centering (t_c = 0)
+    dict(ks=2.5, ss=5.0, sr=25.0),                 # kernel_scale cancels, fallback threshold moves
+    dict(sr=10.0, ss=6.0),                         # outside the fp32 envelope: fp64 mode
+    dict(deg=8, sr=40.0),
+])
+def test_gpf_matches_reference_cxx(gpu, opts):
+    img = synth.rects_image(320, 240, 12, 10.0, 11).astype(np.float64)
+    rfb, ref = drive(REF, img, **opts)
+    fb, out = drive(OURS, img, **opts)
+    assert fb == rfb
+    assert np.abs(out - ref).max() <= 1e-3, opts

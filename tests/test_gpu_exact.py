@@ -8,7 +8,8 @@ import pytest
 from paper_1505_00077_b200 import synth
 
 pytestmark = pytest.mark.gpu
-TOL = 1e-4  # fp32 taps with fp64 row sums vs the fp64 reference, on [0, 255]
+TOL = 1e-4    # device fp32 entry (gpf_b200_exact_f32): fp32 taps, fp64 row sums
+TOL64 = 1e-10  # gpf_filter_exact: the reference's fp64 operation sequence (only exp() differs)
 
 
 def _img(w, h, seed):
@@ -22,7 +23,7 @@ def test_exact_matches_oracle(gpu, oracle, boundary, w, h, ss, sr):
     out = gpu.gpf_filter_exact(img, gpu.spatial_params(ss, boundary=boundary), gpu.range_params(sr))
     idx = np.arange(w * h)  # every pixel
     ref = oracle.exact_bilateral_at(img, ss, sr, idx, boundary=boundary).reshape(h, w)
-    assert np.abs(out - ref).max() <= TOL
+    assert np.abs(out - ref).max() <= TOL64
 
 
 def test_exact_large_window_sampled(gpu, oracle):
@@ -32,7 +33,7 @@ def test_exact_large_window_sampled(gpu, oracle):
     rng = np.random.default_rng(3)
     idx = rng.choice(160 * 120, size=600, replace=False)
     ref = oracle.exact_bilateral_at(img, ss, sr, idx)
-    assert np.abs(out.ravel()[idx] - ref).max() <= TOL
+    assert np.abs(out.ravel()[idx] - ref).max() <= TOL64
 
 
 def test_exact_constant_and_reference_entry(gpu, reference):
@@ -41,7 +42,71 @@ def test_exact_constant_and_reference_entry(gpu, reference):
     img = _img(48, 40, 5)
     ref = reference.exact(img, 2.5, 30.0, boundary=1)
     out = gpu.gpf_filter_exact(img, gpu.spatial_params(2.5, boundary=1), gpu.range_params(30.0))
-    assert np.abs(out - ref).max() <= TOL
+    assert np.abs(out - ref).max() <= TOL64
+    # zero padding: skipped taps
+    ref = reference.exact(img, 2.5, 30.0, boundary=2)
+    out = gpu.gpf_filter_exact(img, gpu.spatial_params(2.5, boundary=2), gpu.range_params(30.0))
+    assert np.abs(out - ref).max() <= TOL64
+
+
+# ---- the reference's own exact_bilateral unit pins (proj/tests/test_bilateral.cpp:44-139)
+def _mt_uniform(seed, w, h, hi):
+    """testsupport::uniform_noise_image (proj/tests/noise.hpp:46-56): mt19937, (x + 0.5) / 2^32."""
+    raw = np.random.RandomState(seed).randint(0, 2**32, size=w * h, dtype=np.uint32).astype(np.float64)
+    u = (raw + 0.5) / 4294967296.0 * hi
+    return (np.floor(u) if hi > 1.0 else u).reshape(h, w)
+
+
+def test_exact_pin_constants(gpu):
+    img = np.full((7, 9), 42.0)
+    assert (gpu.gpf_filter_exact(img, gpu.spatial_params(2.0), gpu.range_params(30.0)) == 42.0).all()
+
+
+def test_exact_pin_impulse(gpu):
+    """3x3 zero image with a 255 impulse, sigma_s 1, W 1, sigma_r 30: the
+    high-precision oracle value 254.99999999999979655 within 3e-14."""
+    img = np.zeros((3, 3))
+    img[1, 1] = 255.0
+    out = gpu.gpf_filter_exact(img, gpu.spatial_params(1.0, window_radius=1), gpu.range_params(30.0))
+    assert abs(out[1, 1] - 254.99999999999979655) <= 3e-14
+    assert 0.0 <= out[0, 0] < 1.0
+
+
+def test_exact_pin_shift_invariance(gpu):
+    img = _mt_uniform(19, 16, 16, 255.0)
+    sp, rp = gpu.spatial_params(2.0), gpu.range_params(30.0)
+    base = gpu.gpf_filter_exact(img, sp, rp)
+    for c in (-100.0, 50.0, 127.5):
+        shifted = gpu.gpf_filter_exact(img - c, sp, rp)
+        assert np.abs(shifted + c - base).max() <= 1e-9
+
+
+def test_exact_pin_hard_step_and_convexity(gpu):
+    img = np.zeros((16, 16))
+    img[:, 8:] = 255.0
+    out = gpu.gpf_filter_exact(img, gpu.spatial_params(2.0), gpu.range_params(30.0))
+    for c in list(range(0, 2)) + list(range(14, 16)):
+        assert np.abs(out[:, c] - img[:, c]).max() < 1.0
+    img = _mt_uniform(23, 12, 12, 255.0)
+    out = gpu.gpf_filter_exact(img, gpu.spatial_params(1.5), gpu.range_params(20.0))
+    assert out.min() >= img.min() - 1e-12 and out.max() <= img.max() + 1e-12
+
+
+def test_exact_pin_huge_sigma_r_is_gaussian_smoothing(gpu):
+    """sigma_r = 1e9: the exact filter degenerates to normalised direct
+    Gaussian smoothing (epsilon 1e-6), computed here in fp64 numpy."""
+    img = _mt_uniform(17, 16, 16, 255.0)
+    out = gpu.gpf_filter_exact(img, gpu.spatial_params(2.0), gpu.range_params(1e9))
+    W = 6
+    k = np.exp(-np.arange(-W, W + 1) ** 2 / 8.0)
+    pad = np.pad(img, W, mode="edge")
+    num = np.zeros_like(img)
+    den = 0.0
+    for a in range(-W, W + 1):
+        for b in range(-W, W + 1):
+            num += k[a + W] * k[b + W] * pad[W + a:W + a + 16, W + b:W + b + 16]
+            den += k[a + W] * k[b + W]
+    assert np.abs(out - num / den).max() <= 1e-6 * np.abs(num / den).max()
 
 
 def test_exact_device_batch(gpu):
