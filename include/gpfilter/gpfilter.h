@@ -7,9 +7,13 @@
  * Each declaration cites the reference interface it replaces
  * (/root/reference/proj/include/gpfilter/gpfilter.h, "ref.h" below).
  *
- * Only the hot path and the handles/params/errors it needs are provided.
- * The exact filter, Taylor baseline, direct Gaussian, kernel evaluators,
- * metrics and PGM I/O stay in the reference library.
+ * Provided: the GPF hot path (gpf_filter_gpf) and the handles, params,
+ * status/error plumbing it needs; beside it the exact filter, the Taylor
+ * baseline, the single-plane recursive Gaussian, gpf_compare and PGM I/O
+ * (SURVEY 8(f)). Not provided (they stay in the reference library; see
+ * INTEGRATION.md): the direct (windowed) Gaussian backend and the range-kernel
+ * evaluators. The C++ entry point gpfilter::gpf is in gpfilter/gpfilter.hpp;
+ * device-resident batches and the precision modes in gpfilter/gpfilter_b200.h.
  */
 #ifndef GPFILTER_B200_GPFILTER_H
 #define GPFILTER_B200_GPFILTER_H
@@ -78,6 +82,11 @@ void gpf_spatial_params_init(gpf_spatial_params* sp); /* 2 / auto / replicate / 
 void gpf_range_params_init(gpf_range_params* rp);     /* 30 / 20 */
 
 /* The hot path (replaces ref.h:100-107, proj/src/capi.cpp:176-192).
+ * Runs on the current CUDA device; precision per gpf_b200_set_precision
+ * (default AUTO: the fp32 plane kernels inside their validated envelope, the
+ * reference-exact fp64 mode outside it -- gpfilter_b200.h). Degree <= 62.
+ * Plans and buffers are cached per device between calls; concurrent calls on
+ * one device are serialised. Host images of 4 MiB and more are page-locked.
  * Validation and status mapping follow the reference: NULL in/sp/rp/out ->
  * INVALID_ARGUMENT; *out is set to NULL before work starts; bad backend or
  * boundary enum, sigma_s <= 0, kernel_scale <= 0, sigma_r <= 0, degree < 0 ->
@@ -108,8 +117,11 @@ gpf_status gpf_filter_taylor(const gpf_image* in, const gpf_spatial_params* sp,
 /* Exact brute-force bilateral filter, Eq. (1) over the (2W+1)^2 window with
  * the boundary mode of sp (ref.h:97-98, proj/src/capi.cpp:164-174 ->
  * exact_bilateral, proj/src/core/bilateral.cpp:14-56). The MSE yardstick of
- * the GPF path; runs on the GPU (fp32 taps, fp64 row sums: within 1e-4 of the
- * fp64 reference on [0,255]). Same NULL / validation / status behaviour. */
+ * the GPF path; runs on the GPU in fp64 with the reference's operation order
+ * and weight table (only exp() differs by <= 1 ulp): passes the reference's
+ * own pins (impulse within 3e-14, shift invariance within 1e-9). The fp32
+ * device entry gpf_b200_exact_f32 is the fast form. Same NULL / validation /
+ * status behaviour. */
 gpf_status gpf_filter_exact(const gpf_image* in, const gpf_spatial_params* sp,
                             const gpf_range_params* rp, gpf_image** out);
 

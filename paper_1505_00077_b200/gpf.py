@@ -80,9 +80,12 @@ class Image:
         return self.view().copy()
 
     def __del__(self):
-        if getattr(self, "h", None):
-            _lib.lib().gpf_image_destroy(self.h)
-            self.h = None
+        try:
+            if getattr(self, "h", None):
+                _lib.lib().gpf_image_destroy(self.h)
+                self.h = None
+        except Exception:  # interpreter shutdown: module globals may already be gone
+            pass
 
 
 def gpf_filter_gpf(img: np.ndarray, sp: SpatialParams | None = None, rp: RangeParams | None = None,
