@@ -17,7 +17,8 @@
 //                   Q += (c G) Fbar_n, P += (c G) Fbar_{n+1}, G = H G, in step order
 //   GpfState::finalize (bilateral.cpp:131-148)                -> k_f64_combine
 // All N+2 planes are filtered concurrently (they are independent given H and
-// F_0), one thread per (line, plane group). The only non-replayed operation is
+// F_0): one lane per (row, 2 planes) in the row pass, one thread per
+// (column, plane) in the column pass. The only non-replayed operation is
 // exp(): CUDA's exp (<= 1 ulp) instead of glibc's, so F_0 may differ from the
 // reference by an ulp on some pixels; everything downstream is bitwise the
 // reference's evaluation of those inputs. t_c comes from the deterministic
@@ -46,7 +47,7 @@ struct Deriche64 {
   double csum, asum, den;  // (nc0+nc1+nc2+nc3), (na0+...), 1+d0+d1+d2+d3 in the reference's order
 };
 
-constexpr int kGP = 4;  // planes per row-pass thread
+constexpr int kGP = 2;  // planes per row-pass thread
 
 // GpfState::init (bilateral.cpp:92-101)
 __global__ void k_f64_prologue(const double* __restrict__ f, const double* __restrict__ scalars,
@@ -86,61 +87,108 @@ __device__ __forceinline__ double deriche_step(const double (&c)[4], const doubl
   return y;
 }
 
-// Row pass of recursive_gaussian (spatial.cpp:235-239) for kGP planes of one
-// row: thread = (row, plane group). The planes are regenerated from (H, F_0)
-// in both directions instead of being stored.
-__global__ void __launch_bounds__(64) k_f64_rows(const double* __restrict__ H,
+// Row pass of recursive_gaussian (spatial.cpp:235-239): CTA = one warp = 32
+// rows x kGP planes, lane = row. The row is walked in chunks of 32 columns
+// staged through shared memory, so every global access is a coalesced 256-B
+// row segment: the (H, F_0) chunk is loaded row by row, each lane runs its
+// row's recurrences out of the tile (planes regenerated from (H, F_0) by the
+// reference's multiply chain), and the chunk of outputs leaves through a
+// [plane][row][column] tile. The anticausal walk reloads the causal outputs
+// the same way and adds its own (dst[i] += y-, spatial.cpp:211).
+constexpr int kRowT = 32;  // rows per CTA == lanes == columns per chunk
+
+__global__ void __launch_bounds__(32) k_f64_rows(const double* __restrict__ H,
                                                  const double* __restrict__ F0,
                                                  double* __restrict__ R, int w, int h, int planes,
                                                  Deriche64 k) {
-  const int y = blockIdx.x * blockDim.x + threadIdx.x;
-  const int n0 = blockIdx.y * kGP;
-  if (y >= h) return;
-  const int np = min(kGP, planes - n0);
+  __shared__ double sH[kRowT][kRowT + 1], sF[kRowT][kRowT + 1];
+  __shared__ double sR[kGP][kRowT][kRowT + 1];
+  const int lane = threadIdx.x;
+  const int y0 = blockIdx.x * kRowT, rows = min(kRowT, h - y0);
+  const int n0 = blockIdx.y * kGP, np = min(kGP, planes - n0);
   const size_t ps = (size_t)w * h;
-  const double* hr = H + (size_t)y * w;
-  const double* fr = F0 + (size_t)y * w;
-  double* rr = R + (size_t)n0 * ps + (size_t)y * w;
+  const int nc = (w + kRowT - 1) / kRowT;
+  auto load_in = [&](int x0, int cols) {
+    for (int r = 0; r < rows; ++r)
+      if (lane < cols) {
+        sH[r][lane] = H[(size_t)(y0 + r) * w + x0 + lane];
+        sF[r][lane] = F0[(size_t)(y0 + r) * w + x0 + lane];
+      }
+  };
+  auto move_out = [&](int x0, int cols, bool store) {
+    for (int p = 0; p < np; ++p)
+      for (int r = 0; r < rows; ++r)
+        if (lane < cols) {
+          double* g = R + (size_t)(n0 + p) * ps + (size_t)(y0 + r) * w + x0 + lane;
+          if (store) *g = sR[p][r][lane];
+          else sR[p][r][lane] = *g;
+        }
+  };
+  const bool live = lane < rows;
   double x[kGP], xm1[kGP], xm2[kGP], xm3[kGP], ym1[kGP], ym2[kGP], ym3[kGP], ym4[kGP];
-  gen_planes<kGP>(hr[0], fr[0], n0, x);
+  // causal (spatial.cpp:190-202): warm start from column 0
+  for (int c = 0; c < nc; ++c) {
+    const int x0 = c * kRowT, cols = min(kRowT, w - x0);
+    load_in(x0, cols);
+    __syncwarp();
+    if (live) {
+      if (c == 0) {
+        gen_planes<kGP>(sH[lane][0], sF[lane][0], n0, x);
 #pragma unroll
-  for (int p = 0; p < kGP; ++p) {
-    const double ss = __ddiv_rn(m_(x[p], k.csum), k.den);
-    xm1[p] = xm2[p] = xm3[p] = x[p];
-    ym1[p] = ym2[p] = ym3[p] = ym4[p] = ss;
-  }
-  for (int i = 0; i < w; ++i) {
-    gen_planes<kGP>(hr[i], fr[i], n0, x);
+        for (int p = 0; p < kGP; ++p) {
+          const double ss = __ddiv_rn(m_(x[p], k.csum), k.den);
+          xm1[p] = xm2[p] = xm3[p] = x[p];
+          ym1[p] = ym2[p] = ym3[p] = ym4[p] = ss;
+        }
+      }
+      for (int j = 0; j < cols; ++j) {
+        gen_planes<kGP>(sH[lane][j], sF[lane][j], n0, x);
 #pragma unroll
-    for (int p = 0; p < kGP; ++p) {
-      const double yi = deriche_step(k.nc, k.d, x[p], xm1[p], xm2[p], xm3[p], ym1[p], ym2[p], ym3[p],
-                                     ym4[p]);
-      if (p < np) rr[(size_t)p * ps + i] = yi;
-      xm3[p] = xm2[p]; xm2[p] = xm1[p]; xm1[p] = x[p];
-      ym4[p] = ym3[p]; ym3[p] = ym2[p]; ym2[p] = ym1[p]; ym1[p] = yi;
+        for (int p = 0; p < kGP; ++p) {
+          const double yi = deriche_step(k.nc, k.d, x[p], xm1[p], xm2[p], xm3[p], ym1[p], ym2[p],
+                                         ym3[p], ym4[p]);
+          sR[p][lane][j] = yi;
+          xm3[p] = xm2[p]; xm2[p] = xm1[p]; xm1[p] = x[p];
+          ym4[p] = ym3[p]; ym3[p] = ym2[p]; ym2[p] = ym1[p]; ym1[p] = yi;
+        }
+      }
     }
+    __syncwarp();
+    move_out(x0, cols, true);
+    __syncwarp();
   }
-  // anticausal (spatial.cpp:204-215): xp = x[i+1..i+4], dst[i] += y-
-  gen_planes<kGP>(hr[w - 1], fr[w - 1], n0, x);
-#pragma unroll
-  for (int p = 0; p < kGP; ++p) {
-    const double ss = __ddiv_rn(m_(x[p], k.asum), k.den);
-    xm1[p] = xm2[p] = xm3[p] = x[p];  // xp1..xp3 (xp4 = ym4 slot below)
-    ym1[p] = ym2[p] = ym3[p] = ym4[p] = ss;
-  }
+  // anticausal (spatial.cpp:204-215): xp = x[i+1..i+4], warm start from column w-1
   double xp4[kGP];
+  for (int c = nc - 1; c >= 0; --c) {
+    const int x0 = c * kRowT, cols = min(kRowT, w - x0);
+    load_in(x0, cols);
+    move_out(x0, cols, false);
+    __syncwarp();
+    if (live) {
+      if (c == nc - 1) {
+        gen_planes<kGP>(sH[lane][cols - 1], sF[lane][cols - 1], n0, x);
 #pragma unroll
-  for (int p = 0; p < kGP; ++p) xp4[p] = x[p];
-  for (int i = w - 1; i >= 0; --i) {
-    gen_planes<kGP>(hr[i], fr[i], n0, x);
+        for (int p = 0; p < kGP; ++p) {
+          const double ss = __ddiv_rn(m_(x[p], k.asum), k.den);
+          xm1[p] = xm2[p] = xm3[p] = xp4[p] = x[p];  // xp1..xp4
+          ym1[p] = ym2[p] = ym3[p] = ym4[p] = ss;
+        }
+      }
+      for (int j = cols - 1; j >= 0; --j) {
+        gen_planes<kGP>(sH[lane][j], sF[lane][j], n0, x);
 #pragma unroll
-    for (int p = 0; p < kGP; ++p) {
-      const double yi = deriche_step(k.na, k.d, xm1[p], xm2[p], xm3[p], xp4[p], ym1[p], ym2[p], ym3[p],
-                                     ym4[p]);
-      if (p < np) rr[(size_t)p * ps + i] = a_(rr[(size_t)p * ps + i], yi);
-      xp4[p] = xm3[p]; xm3[p] = xm2[p]; xm2[p] = xm1[p]; xm1[p] = x[p];
-      ym4[p] = ym3[p]; ym3[p] = ym2[p]; ym2[p] = ym1[p]; ym1[p] = yi;
+        for (int p = 0; p < kGP; ++p) {
+          const double yi = deriche_step(k.na, k.d, xm1[p], xm2[p], xm3[p], xp4[p], ym1[p], ym2[p],
+                                         ym3[p], ym4[p]);
+          sR[p][lane][j] = a_(sR[p][lane][j], yi);
+          xp4[p] = xm3[p]; xm3[p] = xm2[p]; xm2[p] = xm1[p]; xm1[p] = x[p];
+          ym4[p] = ym3[p]; ym3[p] = ym2[p]; ym2[p] = ym1[p]; ym1[p] = yi;
+        }
+      }
     }
+    __syncwarp();
+    move_out(x0, cols, true);
+    __syncwarp();
   }
 }
 
@@ -260,7 +308,8 @@ void run_gpf_f64_exact(const double* d_in, double* d_out, const Params& p, F64Wo
   k.den = 1.0 + k.d[0] + k.d[1] + k.d[2] + k.d[3];
   k.csum = k.nc[0] + k.nc[1] + k.nc[2] + k.nc[3];
   k.asum = k.na[0] + k.na[1] + k.na[2] + k.na[3];
-  k_f64_rows<<<dim3((h + 63) / 64, (planes + kGP - 1) / kGP), 64, 0, st>>>(H, F0, R, w, h, planes, k);
+  k_f64_rows<<<dim3((h + kRowT - 1) / kRowT, (planes + kGP - 1) / kGP), kRowT, 0, st>>>(H, F0, R, w, h,
+                                                                                        planes, k);
   const double mass = kernel_mass_1d(p.sigma_s, default_window_radius(p.sigma_s));
   const double scale = mass * mass * p.kernel_scale;
   k_f64_cols<<<dim3((w + 127) / 128, planes), 128, 0, st>>>(R, Cb, w, h, k, scale);
