@@ -108,21 +108,55 @@ __global__ void __launch_bounds__(32) k_f64_rows(const double* __restrict__ H,
   const int n0 = blockIdx.y * kGP, np = min(kGP, planes - n0);
   const size_t ps = (size_t)w * h;
   const int nc = (w + kRowT - 1) / kRowT;
+  // global -> shared copies as cp.async (LDGSTS): all of a chunk's row
+  // segments in flight at once instead of one load latency per row
+  auto cp8 = [](double* smem, const double* gmem) {
+    const unsigned sa = static_cast<unsigned>(__cvta_generic_to_shared(smem));
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(sa), "l"(gmem));
+  };
   auto load_in = [&](int x0, int cols) {
-    for (int r = 0; r < rows; ++r)
-      if (lane < cols) {
-        sH[r][lane] = H[(size_t)(y0 + r) * w + x0 + lane];
-        sF[r][lane] = F0[(size_t)(y0 + r) * w + x0 + lane];
+    if (lane < cols)
+      for (int r = 0; r < rows; ++r) {
+        cp8(&sH[r][lane], H + (size_t)(y0 + r) * w + x0 + lane);
+        cp8(&sF[r][lane], F0 + (size_t)(y0 + r) * w + x0 + lane);
       }
   };
-  auto move_out = [&](int x0, int cols, bool store) {
-    for (int p = 0; p < np; ++p)
-      for (int r = 0; r < rows; ++r)
-        if (lane < cols) {
-          double* g = R + (size_t)(n0 + p) * ps + (size_t)(y0 + r) * w + x0 + lane;
-          if (store) *g = sR[p][r][lane];
-          else sR[p][r][lane] = *g;
-        }
+  auto load_r = [&](int x0, int cols) {
+    if (lane < cols)
+      for (int p = 0; p < np; ++p)
+        for (int r = 0; r < rows; ++r)
+          cp8(&sR[p][r][lane], R + (size_t)(n0 + p) * ps + (size_t)(y0 + r) * w + x0 + lane);
+  };
+  auto wait_loads = [] {
+    asm volatile("cp.async.commit_group;\n" ::);
+    asm volatile("cp.async.wait_group 0;\n" ::: "memory");
+  };
+  // base plane of this lane's row over the chunk: sF <- F_{n0} = H^{n0} F_0
+  // (the reference's multiply chain), eight independent chains interleaved
+  auto base_planes = [&](int cols) {
+    if (n0 == 0 || !(lane < rows)) return;
+    for (int j0 = 0; j0 < cols; j0 += 8) {
+      double v[8], hv[8];
+#pragma unroll
+      for (int q = 0; q < 8; ++q) {
+        const int j = min(j0 + q, cols - 1);
+        v[q] = sF[lane][j];
+        hv[q] = sH[lane][j];
+      }
+      for (int t = 0; t < n0; ++t) {
+#pragma unroll
+        for (int q = 0; q < 8; ++q) v[q] = m_(hv[q], v[q]);
+      }
+#pragma unroll
+      for (int q = 0; q < 8; ++q)
+        if (j0 + q < cols) sF[lane][j0 + q] = v[q];
+    }
+  };
+  auto store_r = [&](int x0, int cols) {
+    if (lane < cols)
+      for (int p = 0; p < np; ++p)
+        for (int r = 0; r < rows; ++r)
+          R[(size_t)(n0 + p) * ps + (size_t)(y0 + r) * w + x0 + lane] = sR[p][r][lane];
   };
   const bool live = lane < rows;
   double x[kGP], xm1[kGP], xm2[kGP], xm3[kGP], ym1[kGP], ym2[kGP], ym3[kGP], ym4[kGP];
@@ -130,10 +164,12 @@ __global__ void __launch_bounds__(32) k_f64_rows(const double* __restrict__ H,
   for (int c = 0; c < nc; ++c) {
     const int x0 = c * kRowT, cols = min(kRowT, w - x0);
     load_in(x0, cols);
+    wait_loads();
     __syncwarp();
+    base_planes(cols);
     if (live) {
       if (c == 0) {
-        gen_planes<kGP>(sH[lane][0], sF[lane][0], n0, x);
+        gen_planes<kGP>(sH[lane][0], sF[lane][0], 0, x);
 #pragma unroll
         for (int p = 0; p < kGP; ++p) {
           const double ss = __ddiv_rn(m_(x[p], k.csum), k.den);
@@ -142,7 +178,7 @@ __global__ void __launch_bounds__(32) k_f64_rows(const double* __restrict__ H,
         }
       }
       for (int j = 0; j < cols; ++j) {
-        gen_planes<kGP>(sH[lane][j], sF[lane][j], n0, x);
+        gen_planes<kGP>(sH[lane][j], sF[lane][j], 0, x);
 #pragma unroll
         for (int p = 0; p < kGP; ++p) {
           const double yi = deriche_step(k.nc, k.d, x[p], xm1[p], xm2[p], xm3[p], ym1[p], ym2[p],
@@ -154,7 +190,7 @@ __global__ void __launch_bounds__(32) k_f64_rows(const double* __restrict__ H,
       }
     }
     __syncwarp();
-    move_out(x0, cols, true);
+    store_r(x0, cols);
     __syncwarp();
   }
   // anticausal (spatial.cpp:204-215): xp = x[i+1..i+4], warm start from column w-1
@@ -162,11 +198,13 @@ __global__ void __launch_bounds__(32) k_f64_rows(const double* __restrict__ H,
   for (int c = nc - 1; c >= 0; --c) {
     const int x0 = c * kRowT, cols = min(kRowT, w - x0);
     load_in(x0, cols);
-    move_out(x0, cols, false);
+    load_r(x0, cols);
+    wait_loads();
     __syncwarp();
+    base_planes(cols);
     if (live) {
       if (c == nc - 1) {
-        gen_planes<kGP>(sH[lane][cols - 1], sF[lane][cols - 1], n0, x);
+        gen_planes<kGP>(sH[lane][cols - 1], sF[lane][cols - 1], 0, x);
 #pragma unroll
         for (int p = 0; p < kGP; ++p) {
           const double ss = __ddiv_rn(m_(x[p], k.asum), k.den);
@@ -175,7 +213,7 @@ __global__ void __launch_bounds__(32) k_f64_rows(const double* __restrict__ H,
         }
       }
       for (int j = cols - 1; j >= 0; --j) {
-        gen_planes<kGP>(sH[lane][j], sF[lane][j], n0, x);
+        gen_planes<kGP>(sH[lane][j], sF[lane][j], 0, x);
 #pragma unroll
         for (int p = 0; p < kGP; ++p) {
           const double yi = deriche_step(k.na, k.d, xm1[p], xm2[p], xm3[p], xp4[p], ym1[p], ym2[p],
@@ -187,7 +225,7 @@ __global__ void __launch_bounds__(32) k_f64_rows(const double* __restrict__ H,
       }
     }
     __syncwarp();
-    move_out(x0, cols, true);
+    store_r(x0, cols);
     __syncwarp();
   }
 }
