@@ -157,3 +157,55 @@ def test_plan_create_restores_current_device(gpu):
     # the fp32 plan entries reject degrees above their kernels' limit with one message
     with pytest.raises(gpu.GpfError, match="48"):
         gpu.Plan(64, 64, 2.0, 30.0, 49)
+
+
+@pytest.mark.parametrize("shape", [(1, 1), (1, 7), (5, 1), (2, 33), (33, 2), (31, 65), (64, 32),
+                                   (1, 1000), (1000, 1), (97, 131)])
+def test_fp64_mode_shapes(gpu, oracle, shape):
+    """The fp64 mode's row tiles (32 rows x 32-column chunks) and column
+    threads at every edge: partial tiles, single rows / columns."""
+    img = np.random.default_rng(sum(shape) + 7).uniform(0, 255, size=shape)
+    ref, rfb, _ = oracle.gpf(img, 2.0, 12.0, 20)
+    gpu.set_precision("fp64")
+    try:
+        out, fb = gpu.gpf_filter_gpf(img, gpu.spatial_params(2.0), gpu.range_params(12.0, 20))
+    finally:
+        gpu.set_precision("auto")
+    assert fb == rfb
+    assert np.abs(out - ref).max() <= 1e-9 * max(1.0, np.abs(ref).max()), shape
+
+
+@pytest.mark.parametrize("mode", ["fp32", "fp64"])
+@pytest.mark.parametrize("deg", [0, 1, 2])
+def test_low_degrees(gpu, oracle, mode, deg):
+    img = synth.rects_image(70, 45, 4, 10.0, 3 + deg).astype(np.float64)
+    ref, rfb, _ = oracle.gpf(img, 3.0, 40.0, deg)
+    gpu.set_precision(mode)
+    try:
+        out, fb = gpu.gpf_filter_gpf(img, gpu.spatial_params(3.0), gpu.range_params(40.0, deg))
+    finally:
+        gpu.set_precision("auto")
+    assert fb == rfb and np.abs(out - ref).max() <= TOL
+
+
+def test_dropin_concurrent_host_threads(gpu):
+    """gpf_filter_gpf from several host threads at once (the engine serialises
+    calls per device): every thread gets its sequential result, in both modes."""
+    import threading
+    cases = [(synth.rects_image(200 + 8 * k, 150, 6, 10.0, 30 + k).astype(np.float64),
+              2.0 + k, 30.0 if k % 2 == 0 else 10.0) for k in range(6)]
+    seq = [gpu.gpf_filter_gpf(img, gpu.spatial_params(ss), gpu.range_params(sr)) for img, ss, sr in cases]
+    got = [None] * len(cases)
+
+    def work(i):
+        img, ss, sr = cases[i]
+        for _ in range(3):
+            got[i] = gpu.gpf_filter_gpf(img, gpu.spatial_params(ss), gpu.range_params(sr))
+    ths = [threading.Thread(target=work, args=(i,)) for i in range(len(cases))]
+    for t in ths:
+        t.start()
+    for t in ths:
+        t.join()
+    for (a, fa), (b, fb) in zip(seq, got):
+        assert fa == fb
+        np.testing.assert_array_equal(a, b)
