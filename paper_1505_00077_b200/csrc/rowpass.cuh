@@ -261,7 +261,13 @@ namespace gpfb {
 // Two CTAs share an SM, so one's contraction / write-out / load phases
 // overlap the other's FMA-bound sweeps.
 // ----------------------------------------------------------------------------
-constexpr int kRow2Slots = 2;
+#ifndef GPF_ROW_SLOTS
+#define GPF_ROW_SLOTS 2
+#endif
+#ifndef GPF_ROW_CTAS
+#define GPF_ROW_CTAS 2
+#endif
+constexpr int kRow2Slots = GPF_ROW_SLOTS;  // V slots per CTA (2: the next strip prefetched)
 constexpr int kRow2MaxN = 22;  // pairs <= 12
 
 // Band height RB: 16 rows (half-warp per pair, 2 CTAs/SM) or 8 rows (quarter-warp
@@ -381,7 +387,7 @@ __device__ __forceinline__ unsigned contract_px(const float2* Ts, const Tin* Fs,
 // the caller's output), which drains under the next strip's sweeps; else the
 // warps write the tile out row by row.
 template <typename Tin, typename Tout, int NFIX, bool OTMA, int RB = kRowBand, bool AEV = true>
-__global__ void __launch_bounds__(RB == 8 ? 96 : 192, RB == 8 ? 4 : 2) k_rowpass2(const Tin* __restrict__ in_all,
+__global__ void __launch_bounds__(RB == 8 ? 96 : 192, RB == 8 ? 4 : GPF_ROW_CTAS) k_rowpass2(const Tin* __restrict__ in_all,
                                                       const double* __restrict__ scalars,
                                                       const float4* __restrict__ CH_all,
                                                       Tout* __restrict__ out_all,
@@ -474,7 +480,7 @@ __global__ void __launch_bounds__(RB == 8 ? 96 : 192, RB == 8 ? 4 : 2) k_rowpass
 #endif
 
   for (int b = 0; b < nx; ++b) {
-    const int s = b & 1, xs = b * 32, cols = min(32, w - xs);
+    const int s = b % kRow2Slots, xs = b * 32, cols = min(32, w - xs);
     PairState as;
     ps_from_carry(as, c0, c1, fc);
     if (b + 1 < nx) {
@@ -484,7 +490,7 @@ __global__ void __launch_bounds__(RB == 8 ? 96 : 192, RB == 8 ? 4 : 2) k_rowpass
     // ---- 1. sweeps (element [g][c][r] of slot s at tl[c * RB])
     float2* tl = T + (size_t)s * slot_elems + (size_t)gl * PC * RB + r;
     GPF_TICK(5);
-    mbar_wait(&full[s], (b >> 1) & 1);
+    mbar_wait(&full[s], (b / kRow2Slots) & 1);
     GPF_TICK(0);
     if (b == 0) ps_set_gain_sweep(cs, tl[0], fc);
 #ifdef GPF_DIAG_NO_SWEEP
@@ -541,7 +547,7 @@ __global__ void __launch_bounds__(RB == 8 ? 96 : 192, RB == 8 ? 4 : 2) k_rowpass
     GPF_TICK(1);
     // this strip's f tile: the newer group (strip b+1) may stay in flight
     if constexpr (!OTMA) {
-      if (b + 1 < nx) asm volatile("cp.async.wait_group 1;\n" ::: "memory");
+      if (kRow2Slots > 1 && b + 1 < nx) asm volatile("cp.async.wait_group 1;\n" ::: "memory");
       else asm volatile("cp.async.wait_group 0;\n" ::: "memory");
     }
     if (OTMA && tid == 0) bulk_wait_read_all();  // the previous strip's store has left O2
