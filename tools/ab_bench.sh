@@ -2,7 +2,7 @@
 # Same-box A/B of library variants on the bench (C3 five-sigma_s step):
 #   tools/ab_bench.sh OUTPREFIX base abtest/NAME1 abtest/NAME2 ...  (alternating, 2 rounds)
 OUT=$1; shift
-for round in 1 2; do
+for round in ${AB_ROUNDS:-1 2}; do
   for v in "$@"; do
     if [ "$v" = base ]; then lib=""; else lib="$v/libgpfilter_b200.so"; fi
     tag=$(basename "$v")
