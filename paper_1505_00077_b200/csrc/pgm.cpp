@@ -12,6 +12,7 @@
 // [0, 255] (NaN and non-positive values -> 0).
 #include "pgm.h"
 
+#include <algorithm>
 #include <cmath>
 #include <cstdio>
 #include <string>
@@ -40,48 +41,46 @@ const char* kind_name(gpf_status s) {
 
 inline bool space(uint8_t c) { return c == ' ' || (c >= '\t' && c <= '\r'); }
 
-class Tokens {
- public:
-  Tokens(const uint8_t* b, size_t n, size_t start) : b_(b), n_(n), at_(start) {}
-
-  size_t at() const { return at_; }
-  size_t token_start() const { return tok_; }
-  bool done() const { return at_ >= n_; }
-  uint8_t peek() const { return b_[at_]; }
-  void advance() { ++at_; }
-
-  // Next unsigned decimal token, bounded by `limit`; failures report `kind`.
-  long long number(gpf_status kind, const char* what, long long limit) {
-    skip();
-    if (at_ >= n_) parse_error(GPF_ERR_PGM_TRUNCATED, n_, std::string("missing ") + what);
-    tok_ = at_;
-    long long v = 0;
-    size_t digits = 0;
-    for (; at_ < n_ && b_[at_] >= '0' && b_[at_] <= '9'; ++at_, ++digits) {
-      v = 10 * v + (b_[at_] - '0');
-      if (v > limit) parse_error(kind, tok_, std::string(what) + " exceeds " + std::to_string(limit));
-    }
-    const bool ends = at_ >= n_ || space(b_[at_]) || b_[at_] == '#';
-    if (digits == 0 || !ends) parse_error(kind, tok_, std::string("malformed ") + what);
-    return v;
-  }
-
- private:
-  void skip() {
-    while (at_ < n_) {
-      if (space(b_[at_])) {
-        ++at_;
-      } else if (b_[at_] == '#') {
-        while (at_ < n_ && b_[at_] != '\n') ++at_;
-      } else {
-        return;
-      }
-    }
-  }
-
-  const uint8_t* b_;
-  size_t n_, at_, tok_ = 0;
+// Header scanner. A token is a maximal run of bytes that are neither
+// whitespace nor '#'; separators are whitespace and '#'-to-end-of-line
+// comments. next() returns the token's [begin, end) or begin == n at the end
+// of the input.
+struct Span {
+  size_t begin, end;
 };
+
+Span next_token(const uint8_t* b, size_t n, size_t& pos) {
+  for (;;) {
+    while (pos < n && space(b[pos])) ++pos;
+    if (pos < n && b[pos] == '#') {
+      while (pos < n && b[pos] != '\n') ++pos;
+      continue;
+    }
+    break;
+  }
+  const size_t begin = pos;
+  while (pos < n && !space(b[pos]) && b[pos] != '#') ++pos;
+  return {begin, pos};
+}
+
+// One header / ASCII-raster field: an unsigned decimal no larger than
+// `limit`. The value is checked digit by digit (a too-long number is reported
+// as exceeding the limit even if it is followed by garbage); a token that is
+// empty or not all digits is malformed. Errors carry the token's offset.
+long long field(const uint8_t* b, size_t n, size_t& pos, gpf_status kind, const char* what,
+                long long limit, size_t* where = nullptr) {
+  const Span t = next_token(b, n, pos);
+  if (t.begin == n) parse_error(GPF_ERR_PGM_TRUNCATED, n, std::string("missing ") + what);
+  if (where) *where = t.begin;
+  long long v = 0;
+  size_t k = t.begin;
+  while (k < t.end && b[k] >= '0' && b[k] <= '9') {
+    v = 10 * v + (b[k++] - '0');
+    if (v > limit) parse_error(kind, t.begin, std::string(what) + " exceeds " + std::to_string(limit));
+  }
+  if (k == t.begin || k != t.end) parse_error(kind, t.begin, std::string("malformed ") + what);
+  return v;
+}
 
 }  // namespace
 
@@ -89,34 +88,35 @@ Decoded decode(const uint8_t* bytes, size_t size) {
   if (size < 2 || bytes[0] != 'P' || (bytes[1] != '2' && bytes[1] != '5'))
     parse_error(GPF_ERR_PGM_BAD_MAGIC, 0, "expected magic \"P5\" or \"P2\"");
   const bool raw = bytes[1] == '5';
-  Tokens t(bytes, size, 2);
+  size_t pos = 2, at = 0;
   constexpr long long kMaxDim = 1 << 20;
-  const long long w = t.number(GPF_ERR_PGM_BAD_DIMS, "width", kMaxDim);
-  if (w < 1) parse_error(GPF_ERR_PGM_BAD_DIMS, t.token_start(), "width must be positive");
-  const long long h = t.number(GPF_ERR_PGM_BAD_DIMS, "height", kMaxDim);
-  if (h < 1) parse_error(GPF_ERR_PGM_BAD_DIMS, t.token_start(), "height must be positive");
-  const long long maxval = t.number(GPF_ERR_PGM_BAD_MAXVAL, "maxval", 255);
-  if (maxval != 255) parse_error(GPF_ERR_PGM_BAD_MAXVAL, t.token_start(), "only maxval 255 is supported");
-  Decoded d;
-  d.w = static_cast<int>(w);
-  d.h = static_cast<int>(h);
-  const size_t count = static_cast<size_t>(w) * static_cast<size_t>(h);
-  d.pixels.resize(count);
-  if (raw) {
-    if (t.done()) parse_error(GPF_ERR_PGM_TRUNCATED, size, "missing raster");
-    if (!space(t.peek()))
-      parse_error(GPF_ERR_PGM_BAD_MAXVAL, t.at(), "expected a single whitespace byte after maxval");
-    t.advance();
-    const size_t left = size - t.at();
-    if (left < count)
-      parse_error(GPF_ERR_PGM_TRUNCATED, size,
-                  "raster has " + std::to_string(left) + " of " + std::to_string(count) + " bytes");
-    const uint8_t* r = bytes + t.at();
-    for (size_t i = 0; i < count; ++i) d.pixels[i] = r[i];
-  } else {
-    for (size_t i = 0; i < count; ++i)
-      d.pixels[i] = static_cast<double>(t.number(GPF_ERR_PGM_BAD_PIXEL, "sample", 255));
+  long long dims[2];
+  const char* names[2] = {"width", "height"};
+  for (int k = 0; k < 2; ++k) {
+    dims[k] = field(bytes, size, pos, GPF_ERR_PGM_BAD_DIMS, names[k], kMaxDim, &at);
+    if (dims[k] < 1) parse_error(GPF_ERR_PGM_BAD_DIMS, at, std::string(names[k]) + " must be positive");
   }
+  if (field(bytes, size, pos, GPF_ERR_PGM_BAD_MAXVAL, "maxval", 255, &at) != 255)
+    parse_error(GPF_ERR_PGM_BAD_MAXVAL, at, "only maxval 255 is supported");
+  Decoded d;
+  d.w = static_cast<int>(dims[0]);
+  d.h = static_cast<int>(dims[1]);
+  const size_t count = static_cast<size_t>(dims[0]) * static_cast<size_t>(dims[1]);
+  d.pixels.resize(count);
+  if (!raw) {  // P2: every sample is a field of its own
+    for (double& v : d.pixels) v = static_cast<double>(field(bytes, size, pos, GPF_ERR_PGM_BAD_PIXEL, "sample", 255));
+    return d;
+  }
+  // P5: the maxval token is followed by exactly one whitespace byte, then the raster
+  if (pos == size) parse_error(GPF_ERR_PGM_TRUNCATED, size, "missing raster");
+  if (!space(bytes[pos]))
+    parse_error(GPF_ERR_PGM_BAD_MAXVAL, pos, "expected a single whitespace byte after maxval");
+  const uint8_t* raster = bytes + pos + 1;
+  const size_t avail = size - pos - 1;
+  if (avail < count)
+    parse_error(GPF_ERR_PGM_TRUNCATED, size,
+                "raster has " + std::to_string(avail) + " of " + std::to_string(count) + " bytes");
+  std::copy(raster, raster + count, d.pixels.begin());
   return d;
 }
 

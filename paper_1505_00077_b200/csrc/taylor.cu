@@ -47,12 +47,17 @@ __global__ void k_taylor_combine(const double* __restrict__ f, const double* __r
   unsigned my_fb = 0;
   for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n;
        i += (long long)gridDim.x * blockDim.x) {
+    // Order-K Taylor weight of the range Gaussian, sum_k a_k (f(q) - t)^{2k},
+    // expanded binomially over the smoothed moments f^m. Evaluated with the
+    // reference's recurrences and operation order (bitwise parity): the
+    // series coefficient a_k, the binomial C(2k, m) walked from m = 2k down,
+    // and the power (-t)^(2k-m) walked up alongside.
     const double t = f[i];
     double num = 0.0, den = 0.0;
-    double a = 1.0;  // a_k = (-1)^k / (2^k sigma_r^{2k} k!), running product
+    double a = 1.0;
     for (int k = 0; k <= K; ++k) {
-      double binom = 1.0;  // C(2k, m), m descending
-      double pw = 1.0;     // (-t)^{2k - m}
+      double binom = 1.0;
+      double pw = 1.0;
       for (int m = 2 * k; m >= 0; --m) {
         const double coef = m_(m_(a, binom), pw);
         den = a_(den, m_(coef, mbar[(size_t)m * n + i]));
@@ -64,8 +69,8 @@ __global__ void k_taylor_combine(const double* __restrict__ f, const double* __r
       }
       a = m_(a, d_(-1.0, m_(sr2x2, static_cast<double>(k + 1))));
     }
-    if (den <= 1e-8) {  // kQMin (bilateral.hpp:85); tiny or negative
-      out[i] = t;
+    if (den <= 1e-8) {  // kQMin (bilateral.hpp:85): a vanishing or negative
+      out[i] = t;       // denominator keeps the input sample
       ++my_fb;
     } else {
       out[i] = d_(num, den);
