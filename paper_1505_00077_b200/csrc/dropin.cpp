@@ -20,6 +20,7 @@
 // (its outputs leave the input range, up to 1e5 on BASELINE C5) and only an fp64
 // replay of its arithmetic can follow it. AUTO measures t_c, f_min and f_max
 // on the device first and picks the fp64 replay outside the envelope.
+#include <algorithm>
 #include <atomic>
 #include <cmath>
 #include <cstdlib>
@@ -48,6 +49,8 @@ namespace {
 constexpr int kDropinPlans = 8;                        // cached fp32 plans per device
 constexpr size_t kDropinPlanBytes = size_t(64) << 30;  // and at most this much workspace
 constexpr int kStatBlocks = 592;
+constexpr int kRanges = 4;                      // row-pass ranges of a large drop-in frame
+constexpr long long kSplitPixels = 1LL << 22;   // 4 MP and more
 
 std::atomic<int> g_precision{-1};
 thread_local int t_last_precision = 0;
@@ -88,7 +91,9 @@ struct DevCtx {
   double* dscal = nullptr;  // [4] scalars + [4 * kStatBlocks] partials
   double* hscal = nullptr;  // pinned: t_c, max|H|, -, fallbacks
   cudaStream_t st = nullptr;
+  cudaStream_t st_out = nullptr;             // D2H of finished row ranges
   cudaEvent_t ev0 = nullptr, ev1 = nullptr;  // brackets the filter kernels of a call
+  cudaEvent_t range_ev[Plan::kMaxRanges] = {};
 
   void free_plans() {
     for (auto& p : plans) plan_free(*p);
@@ -209,6 +214,8 @@ long long dropin_gpf(const double* h_in, double* h_out, const Params& p) {
     chk(cudaMallocHost(&c.hscal, sizeof(double) * 4), "cudaMallocHost");
     chk(cudaEventCreate(&c.ev0), "cudaEventCreate");
     chk(cudaEventCreate(&c.ev1), "cudaEventCreate");
+    chk(cudaStreamCreateWithFlags(&c.st_out, cudaStreamNonBlocking), "cudaStreamCreate");
+    for (auto& e : c.range_ev) chk(cudaEventCreateWithFlags(&e, cudaEventDisableTiming), "cudaEventCreate");
   }
   if ((size_t)n > c.cap) {
     c.free_buffers();
@@ -239,6 +246,7 @@ long long dropin_gpf(const double* h_in, double* h_out, const Params& p) {
     }
   }
   chk(cudaMemsetAsync(c.dfb, 0, sizeof(unsigned long long), c.st), "cudaMemsetAsync");
+  int ranges = 1, range_rows = 16;
   if (mode == kPrecFp64) {
     with_retry(c, [&] { c.f64.ensure(f64_workspace_bytes(p.width, p.height, p.degree)); });
     chk(cudaEventRecord(c.ev0, c.st), "cudaEventRecord");
@@ -246,13 +254,38 @@ long long dropin_gpf(const double* h_in, double* h_out, const Params& p) {
   } else {
     Plan& pl = cached_plan(c, p);
     chk(cudaEventRecord(c.ev0, c.st), "cudaEventRecord");
+    // large frames: the row pass goes out in kRanges band ranges and each
+    // range's rows start their D2H as soon as it is done
+    if (n >= kSplitPixels) {
+      pl.row_ranges = kRanges;
+      for (int i = 0; i < kRanges; ++i) pl.range_done[i] = c.range_ev[i];
+    }
+    struct Restore {  // the cached plan keeps no per-call state
+      Plan& q;
+      ~Restore() { q.row_ranges = 1; }
+    } restore{pl};
     run_frames_f64(pl, c.din, c.dout, 1, c.dfb, c.st);
+    ranges = pl.ranges_launched;
+    range_rows = pl.range_rows;
   }
   chk(cudaEventRecord(c.ev1, c.st), "cudaEventRecord");
-  chk(cudaMemcpyAsync(h_out, c.dout, sizeof(double) * n, cudaMemcpyDeviceToHost, c.st), "D2H");
+  if (ranges > 1) {
+    const int nbands = (p.height + range_rows - 1) / range_rows;
+    for (int i = 0; i < ranges; ++i) {
+      const long long r0 = (long long)(nbands * (long long)i / ranges) * range_rows;
+      const long long r1 = std::min<long long>((nbands * (long long)(i + 1) / ranges) * range_rows, p.height);
+      chk(cudaStreamWaitEvent(c.st_out, c.range_ev[i], 0), "cudaStreamWaitEvent");
+      chk(cudaMemcpyAsync(h_out + r0 * p.width, c.dout + r0 * p.width,
+                          sizeof(double) * (r1 - r0) * p.width, cudaMemcpyDeviceToHost, c.st_out),
+          "D2H");
+    }
+  } else {
+    chk(cudaMemcpyAsync(h_out, c.dout, sizeof(double) * n, cudaMemcpyDeviceToHost, c.st), "D2H");
+  }
   chk(cudaMemcpyAsync(c.hscal + 3, c.dfb, sizeof(unsigned long long), cudaMemcpyDeviceToHost, c.st),
       "D2H");
   chk(cudaStreamSynchronize(c.st), "cudaStreamSynchronize");
+  chk(cudaStreamSynchronize(c.st_out), "cudaStreamSynchronize");
   t_last_precision = mode;
   t_last_hmax = hmax;
   chk(cudaEventElapsedTime(&t_last_device_ms, c.ev0, c.ev1), "cudaEventElapsedTime");

@@ -137,6 +137,13 @@ struct Plan {
   cudaEvent_t front_done = nullptr;
   // optional per-frame ill-conditioned flags of this launch group (device, set per call)
   int* ill_out = nullptr;
+  // optional row ranges of the row pass for single-frame calls (drop-in D2H overlap):
+  // the bands are split into row_ranges launches, range_done[i] recorded after each;
+  // the launch reports how many it used and the rows per band
+  static constexpr int kMaxRanges = 8;
+  int row_ranges = 1;
+  cudaEvent_t range_done[kMaxRanges] = {};
+  int ranges_launched = 1, range_rows = 16;
   // optional per-stage timing: events recorded on the launching stream
   bool profile = false;
   struct StageTimer* timer = nullptr;

@@ -1336,14 +1336,26 @@ static void launch_passes(Plan& plan, const Tin* d_in, Tout* d_out, int count,
     }
     check(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, r2sm),
           "cudaFuncSetAttribute");
-    k<<<dim3((h + RB - 1) / RB, count), dim3(32, (pairs * RB + 31) / 32), r2sm, st>>>(
-        d_in, plan.scalars, plan.CH, d_out, d_fb, w, h, plan.nx, pairs, plan.fc, plan.rc,
-        RB == 8 ? plan.vmap8 : plan.vmap, omap, imap);
+    // Row ranges (single-frame host entries): the bands go out in plan.row_ranges
+    // launches, each followed by plan.range_done[i], so the caller's D2H of
+    // the finished rows overlaps the rest of the row pass.
+    const int nbands = (h + RB - 1) / RB;
+    const int nr = (count == 1 && plan.row_ranges > 1) ? std::min(plan.row_ranges, nbands) : 1;
+    for (int i = 0; i < nr; ++i) {
+      const int b0 = (int)((long long)nbands * i / nr), b1 = (int)((long long)nbands * (i + 1) / nr);
+      k<<<dim3(b1 - b0, count), dim3(32, (pairs * RB + 31) / 32), r2sm, st>>>(
+          d_in, plan.scalars, plan.CH, d_out, d_fb, w, h, plan.nx, pairs, plan.fc, plan.rc,
+          RB == 8 ? plan.vmap8 : plan.vmap, omap, imap, b0);
+      if (nr > 1) check(cudaEventRecord(plan.range_done[i], st), "cudaEventRecord");
+    }
+    plan.range_rows = RB;
+    plan.ranges_launched = nr;
   } else {
     k_rowpass<RMAXT, Tin, Tout><<<dim3((h + kRowBand - 1) / kRowBand, count),
                                   dim3(32, (pairs + 1) / 2 + kAux), rsm, st>>>(
         d_in, plan.scalars, plan.CH, d_out, d_fb, w, h, plan.nx, pairs, nbuf, plan.fc, plan.rc,
         plan.vmap);
+    plan.ranges_launched = 1;
   }
   stage_end(plan, st);
 }

@@ -396,12 +396,13 @@ __global__ void __launch_bounds__(RB == 8 ? 96 : 192, RB == 8 ? 4 : GPF_ROW_CTAS
                                                       FilterConsts fc, RangeConsts rc,
                                                       const __grid_constant__ CUtensorMap vmap,
                                                       const __grid_constant__ CUtensorMap omap,
-                                                      const __grid_constant__ CUtensorMap imap) {
+                                                      const __grid_constant__ CUtensorMap imap,
+                                                      int band0) {
   extern __shared__ float4 smem4[];
   const int f = blockIdx.y, lane = threadIdx.x, warp = threadIdx.y;
   const int tid = warp * 32 + lane, nthr = blockDim.x * blockDim.y;
   constexpr int PC = row2_pair_cols<RB>();  // columns per pair in a slot
-  const int y0 = blockIdx.x * RB;
+  const int y0 = (blockIdx.x + band0) * RB;  // band0: first band of this launch (row ranges)
   const int rows = min(RB, h - y0);
   const size_t tile_elems = (size_t)pairs * PC * RB;  // float2 per V box: [g][PC columns][RB rows]
   const size_t slot_elems = (tile_elems + 15) & ~size_t(15);  // slots 128-B aligned (TMA)
