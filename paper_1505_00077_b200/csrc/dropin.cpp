@@ -247,10 +247,16 @@ long long dropin_gpf(const double* h_in, double* h_out, const Params& p) {
   }
   chk(cudaMemsetAsync(c.dfb, 0, sizeof(unsigned long long), c.st), "cudaMemsetAsync");
   int ranges = 1, range_rows = 16;
+  bool pixel_ranges = false;  // fp64 mode: ranges of pixels rather than of row bands
   if (mode == kPrecFp64) {
     with_retry(c, [&] { c.f64.ensure(f64_workspace_bytes(p.width, p.height, p.degree)); });
     chk(cudaEventRecord(c.ev0, c.st), "cudaEventRecord");
-    run_gpf_f64_exact(c.din, c.dout, p, c.f64, c.dfb, c.st);
+    const bool split = n >= kSplitPixels;
+    run_gpf_f64_exact(c.din, c.dout, p, c.f64, c.dfb, c.st, split ? kRanges : 1, c.range_ev);
+    if (split) {
+      ranges = kRanges;
+      pixel_ranges = true;
+    }
   } else {
     Plan& pl = cached_plan(c, p);
     chk(cudaEventRecord(c.ev0, c.st), "cudaEventRecord");
@@ -272,11 +278,17 @@ long long dropin_gpf(const double* h_in, double* h_out, const Params& p) {
   if (ranges > 1) {
     const int nbands = (p.height + range_rows - 1) / range_rows;
     for (int i = 0; i < ranges; ++i) {
-      const long long r0 = (long long)(nbands * (long long)i / ranges) * range_rows;
-      const long long r1 = std::min<long long>((nbands * (long long)(i + 1) / ranges) * range_rows, p.height);
+      long long e0, e1;  // element range of range i
+      if (pixel_ranges) {
+        e0 = n * i / ranges;
+        e1 = n * (i + 1) / ranges;
+      } else {
+        e0 = (long long)(nbands * (long long)i / ranges) * range_rows * p.width;
+        e1 = std::min<long long>((nbands * (long long)(i + 1) / ranges) * range_rows, p.height) * p.width;
+      }
       chk(cudaStreamWaitEvent(c.st_out, c.range_ev[i], 0), "cudaStreamWaitEvent");
-      chk(cudaMemcpyAsync(h_out + r0 * p.width, c.dout + r0 * p.width,
-                          sizeof(double) * (r1 - r0) * p.width, cudaMemcpyDeviceToHost, c.st_out),
+      chk(cudaMemcpyAsync(h_out + e0, c.dout + e0, sizeof(double) * (e1 - e0), cudaMemcpyDeviceToHost,
+                          c.st_out),
           "D2H");
     }
   } else {

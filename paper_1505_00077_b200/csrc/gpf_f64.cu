@@ -270,11 +270,11 @@ struct Combine64 {
 
 __global__ void k_f64_combine(const double* __restrict__ f, const double* __restrict__ H,
                               const double* __restrict__ Cb, const double* __restrict__ scalars,
-                              double* __restrict__ out, long long n, Combine64 cb,
-                              unsigned long long* __restrict__ fallbacks) {
+                              double* __restrict__ out, long long n, long long i0, long long i1,
+                              Combine64 cb, unsigned long long* __restrict__ fallbacks) {
   const double t_c = scalars[0];
   unsigned my_fb = 0;
-  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+  for (long long i = i0 + (long long)blockIdx.x * blockDim.x + threadIdx.x; i < i1;
        i += (long long)gridDim.x * blockDim.x) {
     const double hv = H[i];
     double g = 1.0, q = 0.0, p = 0.0;
@@ -325,7 +325,8 @@ void F64Work::release() {
 }
 
 void run_gpf_f64_exact(const double* d_in, double* d_out, const Params& p, F64Work& ws,
-                       unsigned long long* d_fb, cudaStream_t st) {
+                       unsigned long long* d_fb, cudaStream_t st, int ranges,
+                       cudaEvent_t* range_done) {
   const int w = p.width, h = p.height, planes = p.degree + 2;
   if (planes > kMaxPlanes) throw Error{1, "RangeParams: degree must be <= 62 in the B200 library"};
   const long long n = (long long)w * h;
@@ -357,7 +358,14 @@ void run_gpf_f64_exact(const double* d_in, double* d_out, const Params& p, F64Wo
   cb.sigma_r = p.sigma_r;
   cb.degree = p.degree;
   chk(cudaMemsetAsync(d_fb, 0, sizeof(unsigned long long), st), "cudaMemsetAsync");
-  k_f64_combine<<<blocks, 256, 0, st>>>(d_in, H, Cb, scalars, d_out, n, cb, d_fb);
+  // pixel ranges (drop-in D2H overlap): event i once pixels [n i/R, n (i+1)/R) are final
+  const int nr = (ranges > 1 && range_done) ? ranges : 1;
+  for (int r = 0; r < nr; ++r) {
+    const long long i0 = n * r / nr, i1 = n * (r + 1) / nr;
+    const int rb = (int)std::min<long long>((i1 - i0 + 255) / 256, 148 * 16);
+    k_f64_combine<<<std::max(rb, 1), 256, 0, st>>>(d_in, H, Cb, scalars, d_out, n, i0, i1, cb, d_fb);
+    if (nr > 1) chk(cudaEventRecord(range_done[r], st), "cudaEventRecord");
+  }
   chk(cudaGetLastError(), "kernel launch (fp64 GPF)");
 }
 

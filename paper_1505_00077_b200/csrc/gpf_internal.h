@@ -209,8 +209,11 @@ struct F64Work {
   void release();
 };
 size_t f64_workspace_bytes(int w, int h, int degree);
+// ranges > 1: the final combine runs in that many pixel ranges, range_done[i]
+// recorded after range i (pixels [n i/ranges, n (i+1)/ranges)).
 void run_gpf_f64_exact(const double* d_in, double* d_out, const Params& p, F64Work& ws,
-                       unsigned long long* d_fb, cudaStream_t st);
+                       unsigned long long* d_fb, cudaStream_t st, int ranges = 1,
+                       cudaEvent_t* range_done = nullptr);
 
 // Drop-in fp64 host entry (dropin.cpp): gpf_filter_gpf and gpfilter::gpf.
 // Per device: an LRU of fp32 plans, the fp64 workspace, device in/out
