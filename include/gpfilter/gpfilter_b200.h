@@ -21,8 +21,11 @@ extern "C" {
 
 typedef struct gpf_b200_plan gpf_b200_plan;
 
-/* Validates like gpf_filter_gpf (backend is implied recursive) and allocates
- * the workspace on `device` (-1 = current device). */
+/* Validates like gpf_filter_gpf (backend is implied recursive; degree <= 48,
+ * the fp32 kernels' limit) and allocates the workspace on `device` (-1 =
+ * current device); the caller's current device is left unchanged. The plan
+ * entries always run the fp32 plane kernels (see the precision notes below
+ * and gpf_b200_filter_f32_checked). */
 gpf_status gpf_b200_plan_create(int width, int height, const gpf_spatial_params* sp,
                                 const gpf_range_params* rp, int centering, int device,
                                 gpf_b200_plan** out);
@@ -30,7 +33,10 @@ void gpf_b200_plan_destroy(gpf_b200_plan* plan);
 
 /* Re-sizes the workspace to hold `frames` frames, so that gpf_b200_filter_f32
  * filters up to that many frames per kernel launch (default 1). Frame-level
- * batching is what fills the 148 SMs for small frames (e.g. 3840x2160). */
+ * batching is what fills the 148 SMs for small frames (e.g. 3840x2160). The
+ * new workspace is built before the old one is released: on failure (e.g. the
+ * batch does not fit in HBM) the plan keeps its previous workspace and stays
+ * usable. */
 gpf_status gpf_b200_plan_set_batch(gpf_b200_plan* plan, int frames);
 
 /* Per-stage timing for benchmarks: when enabled, every launch group records
