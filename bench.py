@@ -490,10 +490,7 @@ def bench_b200(args):
     plans = [gpf.Plan(W, H, s, sr, N) for s in sigmas]
     outs = [torch.empty_like(d) for d in d_ins]
     d_fb = torch.zeros(n_fr, dtype=torch.int64, device="cuda")
-    # GPF_BENCH_PRIO=graded: stream k at priority -k (experiment; default: equal priorities)
-    prio = os.environ.get("GPF_BENCH_PRIO", "")
-    lo, hi = torch.cuda.Stream.priority_range() if hasattr(torch.cuda.Stream, "priority_range") else (0, -1)
-    streams = [torch.cuda.Stream(priority=max(hi, -k) if prio == "graded" else 0) for k in range(n_fr)]
+    streams = [torch.cuda.Stream() for _ in sigmas]
     main = torch.cuda.current_stream()
 
     # A step enqueues the five frames on five streams; steps follow each other
