@@ -226,12 +226,12 @@ long long dropin_gpf(const double* h_in, double* h_out, const Params& p) {
       c.cap = (size_t)n;
     });
   }
-  chk(cudaMemcpyAsync(c.din, h_in, sizeof(double) * n, cudaMemcpyHostToDevice, c.st), "H2D");
   int mode = get_precision();
   double hmax = 0.0;
   if (mode == kPrecFp32 && p.degree > kMaxDegreeF32)
     throw Error{1, "RangeParams: degree must be <= " + std::to_string(kMaxDegreeF32) +
                        " with the fp32 precision mode"};
+  chk(cudaMemcpyAsync(c.din, h_in, sizeof(double) * n, cudaMemcpyHostToDevice, c.st), "H2D");
   if (mode == kPrecAuto) {
     if (p.degree > kMaxDegreeF32) {
       mode = kPrecFp64;
