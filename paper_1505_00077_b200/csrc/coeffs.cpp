@@ -192,7 +192,19 @@ RangeConsts make_range_consts(const Params& p) {
   }
   const double mass = kernel_mass_1d(p.sigma_s, default_window_radius(p.sigma_s));
   rc.q_thresh = static_cast<float>(1e-8 / (mass * mass * p.kernel_scale));
+  finalize_range_consts(rc);
   return rc;
+}
+
+void finalize_range_consts(RangeConsts& rc) {
+  const double ei = std::floor(rc.e_log2);
+  rc.e_int = static_cast<int>(ei);
+  const double ef = rc.e_log2 - ei;
+  rc.e_frac_hi = static_cast<float>(ef);
+  rc.e_frac_lo = static_cast<float>(ef - rc.e_frac_hi);
+  rc.k_hi = static_cast<float>(rc.exp2_k);
+  rc.k_lo = static_cast<float>(rc.exp2_k - rc.k_hi);
+  rc.inv_sr_f = static_cast<float>(rc.inv_sr);
 }
 
 }  // namespace gpfb

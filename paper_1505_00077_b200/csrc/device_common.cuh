@@ -52,6 +52,69 @@ __device__ __forceinline__ float2 pixel_terms(double f, double t_c, const RangeC
   return r;
 }
 
+// fp32-only form of pixel_terms for fp32 frames (GPF_F32_PROLOGUE): no fp64
+// instructions. h = f - t_c as an unevaluated sum s + hl (TwoSum against the
+// split t_c = tc_hi + tc_lo); the exponent's integer part n and fraction
+// r = a - n are formed with one fused multiply-add of the rounded square
+// against an integer, plus the small correction terms (the square's rounding
+// pe, 2 s hl, the split constants' low parts), so r is accurate to ~1e-7
+// absolute as in the fp64 form. H comes from the same (s, hl) in both the
+// seeds and the row pass (h_f32), so the two agree bitwise.
+__device__ __forceinline__ void h_split(float f, float tc_hi, float tc_lo, float& s, float& hl) {
+  s = f - tc_hi;
+  const float bb = s - f;
+  const float e = (f - (s - bb)) + (-tc_hi - bb);  // exact rounding error of s
+  hl = e - tc_lo;
+}
+
+__device__ __forceinline__ float h_f32(float f, float tc_hi, float tc_lo, const RangeConsts& rc) {
+  float s, hl;
+  h_split(f, tc_hi, tc_lo, s, hl);
+  return fmaf(s, rc.inv_sr_f, hl * rc.inv_sr_f);  // H = h / sr
+}
+
+__device__ __forceinline__ float2 pixel_terms_f32(float f, float tc_hi, float tc_lo,
+                                                  const RangeConsts& rc) {
+  float s, hl;
+  h_split(f, tc_hi, tc_lo, s, hl);
+  float2 out;
+  out.y = fmaf(s, rc.inv_sr_f, hl * rc.inv_sr_f) * rc.h_step;
+  const float p = s * s;
+  const float q = p * rc.k_hi;  // ~ h^2 log2(e) / (2 sr^2)
+  if (!(q < 1000.f)) {          // E 2^(s0) below every fp32 (and its clamp at 2^-252)
+    out.x = 0.f;
+    return out;
+  }
+  const float pe = fmaf(s, s, -p);
+  const float nt = rintf(q);
+  float r = fmaf(-p, rc.k_hi, nt);  // nt - p k_hi, one rounding, |r| <= ~0.5
+  const float corr = fmaf(-p, rc.k_lo, -fmaf(2.f * s, hl, pe) * rc.k_hi) + rc.e_frac_lo;
+  r = (r + rc.e_frac_hi) + corr;   // a - (e_int - nt), in about [-0.5, 1.5]
+  const float n2 = rintf(r);
+  r -= n2;
+  const float pr = exp2_frac(r);
+  const int ni = max(rc.e_int - static_cast<int>(nt) + static_cast<int>(n2), -252);
+  const int k1 = max(ni, -126), k2 = ni - k1;
+  out.x = (pr * __int_as_float((k1 + 127) << 23)) * __int_as_float((k2 + 127) << 23);
+  return out;
+}
+
+// per-input-type prologue: fp32 frames use the fp32 form when enabled
+#ifndef GPF_F32_PROLOGUE
+#define GPF_F32_PROLOGUE 0
+#endif
+template <typename Tin>
+__device__ __forceinline__ float2 pixel_terms_t(Tin f, double t_c, float tc_hi, float tc_lo,
+                                                const RangeConsts& rc) {
+  if constexpr (sizeof(Tin) == 4 && GPF_F32_PROLOGUE) return pixel_terms_f32(f, tc_hi, tc_lo, rc);
+  else return pixel_terms(static_cast<double>(f), t_c, rc);
+}
+template <typename Tin>
+__device__ __forceinline__ float h_t(Tin f, double t_c, float tc_hi, float tc_lo, const RangeConsts& rc) {
+  if constexpr (sizeof(Tin) == 4 && GPF_F32_PROLOGUE) return h_f32(f, tc_hi, tc_lo, rc);
+  else return static_cast<float>((static_cast<double>(f) - t_c) * rc.inv_sr);
+}
+
 // ------------------------------------------------------- IIR section state
 // Two complex first-order sections k; each component packs the two planes.
 struct PairState {

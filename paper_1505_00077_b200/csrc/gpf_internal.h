@@ -87,6 +87,10 @@ struct RangeConsts {
   int planes;         // N + 2
   int pairs;          // ceil(planes / 2)
   int degree;         // N
+  // fp32 prologue (pixel_terms_f32): e_log2 = e_int + e_frac_hi + e_frac_lo,
+  // exp2_k = k_hi + k_lo, inv_sr_f = (float)inv_sr (finalize_range_consts)
+  int e_int;
+  float e_frac_hi, e_frac_lo, k_hi, k_lo, inv_sr_f;
   int centering;      // 0 none / 1 mean / 2 fixed t_c (midpoint)
   double tc_fixed;    // t_c for centering 2
 };
@@ -102,6 +106,7 @@ struct Params {
 FilterConsts make_filter_consts(double sigma_s);
 TileConsts make_tile_consts(double sigma_s, int width, int height);
 RangeConsts make_range_consts(const Params& p);
+void finalize_range_consts(RangeConsts& rc);  // after e_log2 is final: the fp32 prologue split
 double kernel_mass_1d(double sigma_s, int radius);
 int default_window_radius(double sigma_s);
 // The reference's normalised Deriche coefficients (spatial.cpp:140-181), fp64.

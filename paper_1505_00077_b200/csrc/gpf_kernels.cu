@@ -240,7 +240,8 @@ __device__ __forceinline__ void produce_planes(float2* buf, const Tin* ftile, do
       ok[k] = pk < 1024;
       const int pp = ok[k] ? pk : p0;
       const int j = pp >> 5, c = pp & 31;
-      const float2 t = pixel_terms(static_cast<double>(ftile[j * 33 + c]), t_c, rc);
+      const float tc_hi = static_cast<float>(t_c), tc_lo = static_cast<float>(t_c - tc_hi);
+      const float2 t = pixel_terms_t<Tin>(ftile[j * 33 + c], t_c, tc_hi, tc_lo, rc);
       x[k] = t.x;
       m[k] = t.y;
       dst[k] = buf + c * 33 + j;
@@ -639,6 +640,7 @@ __global__ void __launch_bounds__(256) k_seed(const Tin* __restrict__ in_all,
   const Tin* in = in_all + (size_t)f * w * h;
   float2* EM = EM_all + (size_t)f * h * w_pad;
   const double t_c = scalars[2 * f];
+  const float tc_hi = static_cast<float>(t_c), tc_lo = static_cast<float>(t_c - tc_hi);
   // 16-B loads need a 16-B aligned frame base (a torch view may start at any float)
   const bool vec = sizeof(Tin) == 4 && (w & 3) == 0 && x + 4 <= w &&
                    (reinterpret_cast<uintptr_t>(in_all) & 15) == 0;
@@ -647,12 +649,14 @@ __global__ void __launch_bounds__(256) k_seed(const Tin* __restrict__ in_all,
     float2* dst = EM + (size_t)y * w_pad + x;
     if (vec) {
       const float4 v = __ldg(reinterpret_cast<const float4*>(src));
-      const float2 a = pixel_terms(v.x, t_c, rc), b = pixel_terms(v.y, t_c, rc);
-      const float2 c = pixel_terms(v.z, t_c, rc), d = pixel_terms(v.w, t_c, rc);
+      const float2 a = pixel_terms_t<float>(v.x, t_c, tc_hi, tc_lo, rc);
+      const float2 b = pixel_terms_t<float>(v.y, t_c, tc_hi, tc_lo, rc);
+      const float2 c = pixel_terms_t<float>(v.z, t_c, tc_hi, tc_lo, rc);
+      const float2 d = pixel_terms_t<float>(v.w, t_c, tc_hi, tc_lo, rc);
       reinterpret_cast<float4*>(dst)[0] = make_float4(a.x, a.y, b.x, b.y);
       reinterpret_cast<float4*>(dst)[1] = make_float4(c.x, c.y, d.x, d.y);
     } else {
-      for (int k = 0; k < 4 && x + k < w; ++k) dst[k] = pixel_terms(static_cast<double>(src[k]), t_c, rc);
+      for (int k = 0; k < 4 && x + k < w; ++k) dst[k] = pixel_terms_t<Tin>(src[k], t_c, tc_hi, tc_lo, rc);
     }
   }
 }
@@ -1125,6 +1129,7 @@ void plan_init(Plan& plan, const Params& p, int device, int batch) {
   plan.tc = make_tile_consts(p.sigma_s, p.width, p.height);
   plan.rc = make_range_consts(p);
   plan.rc.e_log2 += plan.fc.seed_log2;  // column-pass input carries S^2 (emit normalisation)
+  finalize_range_consts(plan.rc);
   const int pairs = plan.rc.pairs;
   if (rowpass_nbuf<double, double>(pairs) == 0 || colpass_smem<double>(pairs) > 227 * 1024)
     throw Error{1, "RangeParams: degree must be <= 48 in the B200 library"};

@@ -198,7 +198,8 @@ __global__ void __launch_bounds__(MAXT, 1) k_rowpass(const Tin* __restrict__ in_
         const int p = min(p0 + k * nat, kRowBand * 32 - 1);
         const int r = p & (kRowBand - 1), c = p >> 4;
         fv[k] = static_cast<double>(Fs[r * 33 + c]);
-        Hf[k] = static_cast<float>((fv[k] - t_c) * rc.inv_sr);
+        Hf[k] = h_t<Tin>(Fs[r * 33 + c], t_c, static_cast<float>(t_c),
+                         static_cast<float>(t_c - static_cast<float>(t_c)), rc);
         cc[k] = rc.c0;
         qp[k] = make_float2(0.f, 0.f);
         col[k] = Ts + (size_t)c * kRowBand + r;
@@ -312,7 +313,7 @@ __device__ __forceinline__ unsigned contract_px(const float2* Ts, const Tin* Fs,
     const int p = min(p0 + k * nthr, RB * 32 - 1);
     off[k] = p;  // [col][row]: column p / RB, row p % RB
     // H as the column pass formed it (pixel_terms): fp64 difference, fp32 H
-    Hf[k] = static_cast<float>((static_cast<double>(Fs[f_at<OSW>(p % RB, p / RB)]) - t_c) * rc.inv_sr);
+    Hf[k] = h_t<Tin>(Fs[f_at<OSW>(p % RB, p / RB)], t_c, tc_hi, tc_lo, rc);
   }
   // Q = sum_{n<=N} c_n F_n and P = sum_{n<=N} c_n F_{n+1} with c_n = H^n k_n
   // share the coefficient polynomial: Horner in H over n = N..0 on the pair
