@@ -649,12 +649,22 @@ __global__ void __launch_bounds__(256) k_seed(const Tin* __restrict__ in_all,
     float2* dst = EM + (size_t)y * w_pad + x;
     if (vec) {
       const float4 v = __ldg(reinterpret_cast<const float4*>(src));
+#if defined(GPF_DIAG_SEED_COPY)  // diagnostic: the seed traffic without its arithmetic (wrong output)
+      const float2 a = make_float2(v.x, v.x), b = make_float2(v.y, v.y);
+      const float2 c = make_float2(v.z, v.z), d = make_float2(v.w, v.w);
+#else
       const float2 a = pixel_terms_t<float>(v.x, t_c, tc_hi, tc_lo, rc);
       const float2 b = pixel_terms_t<float>(v.y, t_c, tc_hi, tc_lo, rc);
       const float2 c = pixel_terms_t<float>(v.z, t_c, tc_hi, tc_lo, rc);
       const float2 d = pixel_terms_t<float>(v.w, t_c, tc_hi, tc_lo, rc);
-      reinterpret_cast<float4*>(dst)[0] = make_float4(a.x, a.y, b.x, b.y);
-      reinterpret_cast<float4*>(dst)[1] = make_float4(c.x, c.y, d.x, d.y);
+#endif
+#if defined(GPF_DIAG_SEED_NOSTORE)  // diagnostic: the arithmetic without the EM stores (stale seeds)
+      if (a.x == -1.f && b.x == -1.f && c.x == -1.f && d.x == -1.f)
+#endif
+      {
+        reinterpret_cast<float4*>(dst)[0] = make_float4(a.x, a.y, b.x, b.y);
+        reinterpret_cast<float4*>(dst)[1] = make_float4(c.x, c.y, d.x, d.y);
+      }
     } else {
       for (int k = 0; k < 4 && x + k < w; ++k) dst[k] = pixel_terms_t<Tin>(src[k], t_c, tc_hi, tc_lo, rc);
     }
