@@ -1283,7 +1283,10 @@ static void launch_passes(Plan& plan, const Tin* d_in, Tout* d_out, int count,
   if constexpr (kCanStage) {
     // seeds once per pixel, then the carries in pair groups
 #ifndef GPF_DIAG_NO_SEED  // diagnostic: reuse the previous call's seeds (bench-mix cost of K1a)
-    k_seed<Tin><<<dim3((w + 1023) / 1024, std::min(h, 1024), count), 256, 0, st>>>(
+#ifndef GPF_SEED_ROWS
+#define GPF_SEED_ROWS 1024
+#endif
+    k_seed<Tin><<<dim3((w + 1023) / 1024, std::min(h, GPF_SEED_ROWS), count), 256, 0, st>>>(
         d_in, plan.scalars, plan.EM, w, h, plan.w_pad, plan.rc);
 #endif
 #ifndef GPF_DIAG_NO_CARRY  // diagnostic: skip the carries (wrong output; bench-mix cost)
