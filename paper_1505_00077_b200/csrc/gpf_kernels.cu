@@ -662,8 +662,13 @@ __global__ void __launch_bounds__(256) k_seed(const Tin* __restrict__ in_all,
       if (a.x == -1.f && b.x == -1.f && c.x == -1.f && d.x == -1.f)
 #endif
       {
+#ifdef GPF_SEED_STCS  // streaming stores (evict-first)
+        __stcs(reinterpret_cast<float4*>(dst), make_float4(a.x, a.y, b.x, b.y));
+        __stcs(reinterpret_cast<float4*>(dst) + 1, make_float4(c.x, c.y, d.x, d.y));
+#else
         reinterpret_cast<float4*>(dst)[0] = make_float4(a.x, a.y, b.x, b.y);
         reinterpret_cast<float4*>(dst)[1] = make_float4(c.x, c.y, d.x, d.y);
+#endif
       }
     } else {
       for (int k = 0; k < 4 && x + k < w; ++k) dst[k] = pixel_terms_t<Tin>(src[k], t_c, tc_hi, tc_lo, rc);
