@@ -167,7 +167,7 @@ class ClockSampler:
         time.sleep(0.1)
         self.proc.terminate()
         self.proc.wait()
-        sm, smax, reasons = [], [], set()
+        sm, smax, pw, reasons = [], [], [], set()
         names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
         for line in open(self.path):
             parts = [p.strip() for p in line.split(",")]
@@ -178,6 +178,10 @@ class ClockSampler:
                 smax.append(float(parts[1]))
             except ValueError:
                 continue
+            try:
+                pw.append(float(parts[2]))
+            except ValueError:
+                pass
             for n, v in zip(names, parts[3:7]):
                 if v.lower().startswith("active"):
                     reasons.add(n)
@@ -185,7 +189,8 @@ class ClockSampler:
         # samples under load: the timed region keeps the GPU busy throughout
         return {"sm_mhz": statistics.median(sm) if sm else None,
                 "sm_max_mhz": max(smax) if smax else None,
-                "samples": len(sm), "reasons": sorted(reasons)}
+                "samples": len(sm), "power_w": statistics.median(pw) if pw else None,
+                "reasons": sorted(reasons)}
 
 
 # ------------------------------------------------------------- CPU leg

@@ -360,10 +360,68 @@ __device__ __forceinline__ float pow_group(float m2, int pair0) {
 // item = (column, row pair), four items (eight pixels) per thread in one
 // straight-line pass, so eight independent multiply chains are in flight.
 // x_{n0} = es m^{n0} by squarings, then the chain runs over the group's planes.
+// 8-B shared store kept as issued (the compiler would fuse two adjacent ones
+// into a 16-B store that needs an aligned register quad, i.e. register moves)
+__device__ __forceinline__ void sts64(float2* p, float2 v) {
+  asm volatile("st.shared.v2.f32 [%0], {%1, %2};\n" ::"r"(smem_u32(p)), "f"(v.x), "f"(v.y) : "memory");
+}
+
+#ifndef GPF_L2HINT
+#define GPF_L2HINT 0  // evict-first L2 policies: 1 V stores, 2 V loads, 4 EM loads (column pass), 8 row-pass f/out
+#endif
+#ifndef GPF_COL_STS64
+#define GPF_COL_STS64 1
+#endif
+#ifndef GPF_PROD_PAIRCHAIN
+#define GPF_PROD_PAIRCHAIN 1
+#endif
 __device__ __forceinline__ void produce_group(float* stage, const float2* emt, int pair0,
                                               int npairs) {
   constexpr int kIt = 4;  // 512 items = 4 x 128 threads (4-warp CTAs)
   const int tid = threadIdx.y * 32 + threadIdx.x;
+#if GPF_PROD_PAIRCHAIN
+  // Pair chain: an item's two pixels (rows j, j+1) keep their current plane
+  // pair (F_{2g}, F_{2g+1}) as float2 and step to the next pair with one
+  // packed multiply by the broadcast m^2 (the carry walk forms its planes the
+  // same way, carry_base). The pairs go to the stage as two 8-B stores, which
+  // leaves the multiplies' register pairs in place (a 16-B store of the two
+  // pixels needs an aligned quad and costs register moves).
+  float2 a[kIt], b[kIt];
+  float m2[2 * kIt];
+  float2* dst[kIt];
+#pragma unroll
+  for (int k = 0; k < kIt; ++k) {
+    const int it = tid + k * 128;
+    const int c = it & 31, j = (it >> 5) * 2;  // rows j, j+1
+    const float2 ta = emt[j * 32 + c], tb = emt[(j + 1) * 32 + c];
+    m2[2 * k] = ta.y * ta.y;
+    m2[2 * k + 1] = tb.y * tb.y;
+    float xa = ta.x, xb = tb.x;
+    if (pair0 > 0) {
+      xa *= pow_group(m2[2 * k], pair0);
+      xb *= pow_group(m2[2 * k + 1], pair0);
+    }
+    a[k] = make_float2(xa, xa * ta.y);
+    b[k] = make_float2(xb, xb * tb.y);
+    dst[k] = reinterpret_cast<float2*>(stage_at(stage + c * 32, j, c & 7));
+  }
+  // every pair slot of the stage is written (a group's missing pairs hold
+  // finite values no warp sweeps, and the TMA store clips them), so the
+  // chain is branch-free
+  (void)npairs;
+#pragma unroll
+  for (int gg = 0; gg < kColGroup; ++gg) {
+#pragma unroll
+    for (int k = 0; k < kIt; ++k) {
+      sts64(dst[k] + gg * 1024, a[k]);
+      sts64(dst[k] + gg * 1024 + 1, b[k]);
+      if (gg + 1 < kColGroup) {
+        a[k] = mul2(a[k], f2(m2[2 * k]));
+        b[k] = mul2(b[k], f2(m2[2 * k + 1]));
+      }
+    }
+  }
+#else
   float x[2 * kIt], m[2 * kIt];
   float4* dst[kIt];
 #pragma unroll
@@ -393,6 +451,7 @@ __device__ __forceinline__ void produce_group(float* stage, const float2* emt, i
       }
     }
   }
+#endif
 }
 
 // One CTA = 32 columns x kColGroup pairs (pair group blockIdx.z); several
@@ -416,7 +475,11 @@ template <bool AEV>
 __global__ void __launch_bounds__(32 * kColGroup, GPF_COL_CTAS) k_colpass_tma(
     const float4* __restrict__ CA_all, float4* __restrict__ AH_all, int w, int h, int ny, int nx,
     int pairs, int groups, FilterConsts fc, TileConsts tc,
-    const __grid_constant__ CUtensorMap emmap, const __grid_constant__ CUtensorMap vstore) {
+    const __grid_constant__ CUtensorMap emmap, const __grid_constant__ CUtensorMap vstore
+#ifdef GPF_DIAG_EXTRA_VW
+    , const __grid_constant__ CUtensorMap vstore_x
+#endif
+    ) {
   extern __shared__ float4 smem4[];
   __shared__ uint64_t em_full;
   const int f = blockIdx.y, lane = threadIdx.x, gl = threadIdx.y;
@@ -450,7 +513,8 @@ __global__ void __launch_bounds__(32 * kColGroup, GPF_COL_CTAS) k_colpass_tma(
   __syncthreads();
   if (tid == 0) {
     mbar_arrive_expect_tx(&em_full, 32 * 32 * sizeof(float2));
-    tma_load_3d(emt, &emmap, 2 * x0, 0, f, &em_full);
+    if constexpr (GPF_L2HINT & 4) tma_load_3d_hint(emt, &emmap, 2 * x0, 0, f, &em_full, l2_evict_first());
+    else tma_load_3d(emt, &emmap, 2 * x0, 0, f, &em_full);
   }
   PairState cs;  // causal state, carried across chunks
   ps_zero(cs);
@@ -490,7 +554,8 @@ __global__ void __launch_bounds__(32 * kColGroup, GPF_COL_CTAS) k_colpass_tma(
     GPF_TICK(3);
     if (tid == 0 && cy + 1 < ny) {  // the EM tile is free again: fetch the next chunk's
       mbar_arrive_expect_tx(&em_full, 32 * 32 * sizeof(float2));
-      tma_load_3d(emt, &emmap, 2 * x0, y0 + kTile, f, &em_full);
+      if constexpr (GPF_L2HINT & 4) tma_load_3d_hint(emt, &emmap, 2 * x0, y0 + kTile, f, &em_full, l2_evict_first());
+      else tma_load_3d(emt, &emmap, 2 * x0, y0 + kTile, f, &em_full);
     }
     float* mcol = stage + col_off;
     if (active && x < w && rows == kTile) {
@@ -554,8 +619,19 @@ __global__ void __launch_bounds__(32 * kColGroup, GPF_COL_CTAS) k_colpass_tma(
         ps_advance_a(as, make_float2(va.x, va.y), fc);
         ps_advance_c(cs, make_float2(vc.z, vc.w), fc);
         const float2 yc1 = ps_emit_c_acc(cs, fc, pa[u + 1]);
+#if GPF_COL_STS64
+        {  // 8-B stores (fused back into 16-B ones by ptxas, without register moves)
+          float2* pa2 = reinterpret_cast<float2*>(stage_at(mcol, 14 - u, cm));
+          float2* pc2 = reinterpret_cast<float2*>(stage_at(mcol, 16 + u, cm));
+          sts64(pa2, ya);
+          sts64(pa2 + 1, yb);
+          sts64(pc2, yc0);
+          sts64(pc2 + 1, yc1);
+        }
+#else
         *reinterpret_cast<float4*>(stage_at(mcol, 14 - u, cm)) = make_float4(ya.x, ya.y, yb.x, yb.y);
         *reinterpret_cast<float4*>(stage_at(mcol, 16 + u, cm)) = make_float4(yc0.x, yc0.y, yc1.x, yc1.y);
+#endif
         va = na;
         vc = nc;
       }
@@ -591,7 +667,11 @@ __global__ void __launch_bounds__(32 * kColGroup, GPF_COL_CTAS) k_colpass_tma(
     __syncthreads();
 #ifndef GPF_DIAG_NO_STORE
     if (tid == 0) {  // pairs past the last one fall outside the tensor and are clipped
-      tma_store_5d(&vstore, 0, x0, y0 >> 4, pair0, f, stage);
+      if constexpr (GPF_L2HINT & 1) tma_store_5d_hint(&vstore, 0, x0, y0 >> 4, pair0, f, stage, l2_evict_first());
+      else tma_store_5d(&vstore, 0, x0, y0 >> 4, pair0, f, stage);
+#ifdef GPF_DIAG_EXTRA_VW  // diagnostic: the chunk is stored a second time, to a scratch copy of V
+      tma_store_5d(&vstore_x, 0, x0, y0 >> 4, pair0, f, stage);
+#endif
       bulk_commit();
     }
 #endif
@@ -793,11 +873,96 @@ __device__ __forceinline__ float2 carry_base(float2 s, int half, float& m2) {
   return make_float2(xb, xb * s.y);
 }
 
+#ifndef GPF_CARRY_RS
+#define GPF_CARRY_RS 0
+#endif
+// Row-split lanes (GPF_CARRY_RS, kCarryLP == 2 geometry: 16 columns per warp):
+// lane = (column lane & 15, row half lane >> 4), every lane folds all four
+// pairs of the group over its 16 rows of the chunk -- one power chain per
+// seed and group instead of one per seed and half-warp -- and the two halves'
+// partial dot products are summed with one shuffle per state word (the
+// weights p^j already carry each row's absolute position in the chunk).
+template <int GRP>
+__device__ __forceinline__ void carry_walk_rs(float2* tiles, uint64_t* full, float4* CA,
+                                              const CUtensorMap* emcmap, int w, int h, int ny,
+                                              int pairs, int x0, int f, const FilterConsts& fc,
+                                              const TileConsts& tc) {
+  constexpr int kLanePairs = kColGroup;
+  const int lane = threadIdx.x, wi = threadIdx.y, tid = wi * 32 + lane;
+  const int rh = lane >> 4;
+  const int col = wi * 16 + (lane & 15), x = x0 + col;
+  const int pair0 = GRP * kColGroup;
+  const int npairs = min(kLanePairs, pairs - pair0);
+  const size_t pair_stride = (size_t)w * 2, chunk_stride = (size_t)pairs * w * 2;
+  float4* ca = CA + (size_t)x * 2;
+  PairState C[kLanePairs];
+  for (int k = 0; k < ny; ++k) {
+    const int cy = ny - 1 - k, s = k % kCarrySlots;
+    const float2* tile = tiles + (size_t)s * 32 * kCarryCols + col;  // [32 rows][kCarryCols columns]
+    mbar_wait(&full[s], (k / kCarrySlots) & 1);
+    if (k == 0) {  // replicate boundary: steady state of the bottom row
+      float m2;
+      float2 pl = carry_base<GRP>(tile[(h - 1 - cy * kTile) * kCarryCols], 0, m2);
+#pragma unroll
+      for (int gg = 0; gg < kLanePairs; ++gg) {
+        ps_set_gain(C[gg], pl, fc);
+        pl = mul2(pl, f2(m2));
+      }
+    }
+    if (x < w) {  // half 0 stores pairs 0, 1 and half 1 pairs 2, 3 (both hold every C)
+#pragma unroll
+      for (int gg = 0; gg < kLanePairs; ++gg)
+        if ((gg >> 1) == rh && gg < npairs) ps_store(ca + cy * chunk_stride + (pair0 + gg) * pair_stride, C[gg]);
+    }
+    if (cy == 0) break;
+    PairState agg[kLanePairs];
+#pragma unroll
+    for (int gg = 0; gg < kLanePairs; ++gg) ps_zero(agg[gg]);
+    // rows past the image (last, partial chunk) read as zero seeds (TMA fill)
+#pragma unroll
+    for (int jj = 0; jj < kTile / 2; ++jj) {
+      const int j = rh * (kTile / 2) + jj;
+      float m2;
+      float2 pl = carry_base<GRP>(tile[j * kCarryCols], 0, m2);
+      const float4 wj = tc.w4[j];
+#pragma unroll
+      for (int gg = 0; gg < kLanePairs; ++gg) {
+        ps_accum(agg[gg], pl, wj);
+        if (gg + 1 < kLanePairs) pl = mul2(pl, f2(m2));
+      }
+    }
+#pragma unroll
+    for (int gg = 0; gg < kLanePairs; ++gg) {
+#pragma unroll
+      for (int q = 0; q < 2; ++q) {
+        agg[gg].wr[q].x += __shfl_xor_sync(0xffffffffu, agg[gg].wr[q].x, 16);
+        agg[gg].wr[q].y += __shfl_xor_sync(0xffffffffu, agg[gg].wr[q].y, 16);
+        agg[gg].wi[q].x += __shfl_xor_sync(0xffffffffu, agg[gg].wi[q].x, 16);
+        agg[gg].wi[q].y += __shfl_xor_sync(0xffffffffu, agg[gg].wi[q].y, 16);
+      }
+    }
+    const bool last = k == 0;
+#pragma unroll
+    for (int gg = 0; gg < kLanePairs; ++gg)
+      ps_chain(C[gg], agg[gg], last ? tc.pYr2 : tc.pTr2, last ? tc.pYi2 : tc.pTi2);
+    __syncthreads();  // every warp is done with slot s
+    if (tid == 0 && k + kCarrySlots < ny) {
+      mbar_arrive_expect_tx(&full[s], 32 * kCarryCols * sizeof(float2));
+      tma_load_3d(tiles + (size_t)s * 32 * kCarryCols, emcmap, 2 * x0, (cy - kCarrySlots) * kTile, f,
+                  &full[s]);
+    }
+  }
+}
+
 template <int GRP>
 __device__ __forceinline__ void carry_walk(float2* tiles, uint64_t* full,
                                            float4* CA, const CUtensorMap* emcmap, int w, int h,
                                            int ny, int pairs, int x0, int f, const FilterConsts& fc,
                                            const TileConsts& tc) {
+  if constexpr (GPF_CARRY_RS && kCarryLP == 2) {
+    carry_walk_rs<GRP>(tiles, full, CA, emcmap, w, h, ny, pairs, x0, f, fc, tc);
+    return;
+  }
   // kCarryLP pairs per lane: 2 (half-warp per two pairs, 16 columns per warp)
   // or 4 (the whole group, 32 columns per warp: one power chain per seed)
   constexpr int kLanePairs = kCarryLP;
@@ -857,7 +1022,7 @@ __device__ __forceinline__ void carry_walk(float2* tiles, uint64_t* full,
   }
 }
 
-__global__ void __launch_bounds__(32 * kCarryWarps, (GPF_CARRY_SLOTS == 2 ? 6 : 4) * (4 / kCarryWarps)) k_col_carry_tma(float4* __restrict__ CA_all, int w, int h,
+__global__ void __launch_bounds__(32 * kCarryWarps, (GPF_CARRY_SLOTS == 2 ? (GPF_CARRY_RS ? 5 : 6) : 4) * (4 / kCarryWarps)) k_col_carry_tma(float4* __restrict__ CA_all, int w, int h,
                                                           int ny, int pairs, int groups,
                                                           FilterConsts fc, TileConsts tc,
                                                           const __grid_constant__ CUtensorMap emcmap) {
@@ -1212,6 +1377,15 @@ void plan_init(Plan& plan, const Params& p, int device, int batch) {
   const CUresult r2 = encode(&plan.vstore, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 5, plan.V, dims, strides,
                              sbox, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
                              CU_TENSOR_MAP_L2_PROMOTION_NONE, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+#ifdef GPF_DIAG_EXTRA_VW
+  {
+    float2* vx = nullptr;
+    check(cudaMalloc(&vx, vb), "cudaMalloc(Vx)");  // diagnostic only: never freed
+    encode(&plan.vmap8, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 5, vx, dims, strides, sbox, estr,
+           CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_NONE,
+           CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  }
+#endif
   if (r2 != CUDA_SUCCESS) {
     plan_free(plan);
     throw Error{9, "cuTensorMapEncodeTiled (store) failed (" + std::to_string((int)r2) + ")"};
@@ -1291,8 +1465,27 @@ static void launch_passes(Plan& plan, const Tin* d_in, Tout* d_out, int count,
 #ifndef GPF_SEED_ROWS
 #define GPF_SEED_ROWS 1024
 #endif
+#ifdef GPF_DIAG_SEED_DUMMY  // diagnostic: the seed stores go to a scratch buffer (consumers read stale EM)
+    static float2* dummy = nullptr;
+    if (!dummy) check(cudaMalloc(&dummy, sizeof(float2) * (size_t)h * plan.w_pad * count), "cudaMalloc");
+    k_seed<Tin><<<dim3((w + 1023) / 1024, std::min(h, GPF_SEED_ROWS), count), 256, 0, st>>>(
+        d_in, plan.scalars, dummy, w, h, plan.w_pad, plan.rc);
+#else
+#ifdef GPF_DIAG_SEED_ONCE  // diagnostic: seeds only on a plan's first call (valid while it keeps its frame)
+    static std::vector<const void*> seeded;
+    const bool once = std::find(seeded.begin(), seeded.end(), (const void*)plan.EM) != seeded.end();
+    if (!once) seeded.push_back(plan.EM);
+    if (!once)
+#endif
+#ifdef GPF_DIAG_SEED_EXTRA  // diagnostic: a second seed pass into a scratch buffer (real data kept)
+    static float2* dummy = nullptr;
+    if (!dummy) check(cudaMalloc(&dummy, sizeof(float2) * (size_t)h * plan.w_pad * count), "cudaMalloc");
+    k_seed<Tin><<<dim3((w + 1023) / 1024, std::min(h, GPF_SEED_ROWS), count), 256, 0, st>>>(
+        d_in, plan.scalars, dummy, w, h, plan.w_pad, plan.rc);
+#endif
     k_seed<Tin><<<dim3((w + 1023) / 1024, std::min(h, GPF_SEED_ROWS), count), 256, 0, st>>>(
         d_in, plan.scalars, plan.EM, w, h, plan.w_pad, plan.rc);
+#endif
 #endif
 #ifndef GPF_DIAG_NO_CARRY  // diagnostic: skip the carries (wrong output; bench-mix cost)
 #if GPF_CARRY_TMA
@@ -1318,7 +1511,11 @@ static void launch_passes(Plan& plan, const Tin* d_in, Tout* d_out, int count,
           "cudaFuncSetAttribute");
     kc<<<dim3(plan.nx * groups, count), dim3(32, kColGroup), psm, st>>>(
         plan.CA, plan.AH, w, h, plan.ny, plan.nx, pairs, groups, plan.fc, plan.tc, plan.emmap,
-        plan.vstore);
+        plan.vstore
+#ifdef GPF_DIAG_EXTRA_VW
+        , plan.vmap8
+#endif
+        );
   }
   if (!staged) {
     check(cudaFuncSetAttribute(k_colpass<MAXT, Tin>, cudaFuncAttributeMaxDynamicSharedMemorySize, psm),

@@ -437,9 +437,14 @@ __global__ void __launch_bounds__(RB == 8 ? 96 : 192, RB == 8 ? 4 : GPF_ROW_CTAS
 #ifdef GPF_DIAG_L2V  // diagnostic: V boxes from a small L2-resident region
       tma_load_5d(T + (size_t)s * slot_elems, &vmap, 0, (b & 3) * 32, blockIdx.x & 1, 0, f, &full[s]);
 #else
-      tma_load_5d(T + (size_t)s * slot_elems, &vmap, (y0 & 15) * 2, xs, y0 >> 4, 0, f, &full[s]);
+      if constexpr (GPF_L2HINT & 2)
+        tma_load_5d_hint(T + (size_t)s * slot_elems, &vmap, (y0 & 15) * 2, xs, y0 >> 4, 0, f, &full[s], l2_evict_first());
+      else tma_load_5d(T + (size_t)s * slot_elems, &vmap, (y0 & 15) * 2, xs, y0 >> 4, 0, f, &full[s]);
 #endif
-      if constexpr (OTMA) tma_load_3d(F2 + s * RB * 32, &imap, xs, y0, f, &full[s]);
+      if constexpr (OTMA) {
+        if constexpr (GPF_L2HINT & 8) tma_load_3d_hint(F2 + s * RB * 32, &imap, xs, y0, f, &full[s], l2_evict_first());
+        else tma_load_3d(F2 + s * RB * 32, &imap, xs, y0, f, &full[s]);
+      }
     }
     if constexpr (!OTMA) {
       Tin* Fs = F + s * RB * 33;
@@ -580,7 +585,8 @@ __global__ void __launch_bounds__(RB == 8 ? 96 : 192, RB == 8 ? 4 : GPF_ROW_CTAS
       fence_proxy_async();  // O2 writes -> visible to the TMA store
       __syncthreads();      // slot s, its f tile are free; O2 is complete
       if (tid == 0) {
-        tma_store_3d(&omap, xs, y0, f, O2);  // clipped to the image
+        if constexpr (GPF_L2HINT & 8) tma_store_3d_hint(&omap, xs, y0, f, O2, l2_evict_first());
+        else tma_store_3d(&omap, xs, y0, f, O2);  // clipped to the image
         bulk_commit();
       }
       GPF_TICK(4);

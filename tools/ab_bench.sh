@@ -11,7 +11,7 @@ for round in ${AB_ROUNDS:-1 2}; do
     python - "gpurun_out/${OUT}_${tag}_${round}.json" "$tag" <<'PY'
 import json, sys
 d = json.loads(open(sys.argv[1]).read().strip().splitlines()[-1])
-print(sys.argv[2], d["value"], "stage", d["stage_ms_per_frame"], "clk", d["clocks"]["sm_mhz"])
+print(sys.argv[2], d["value"], "stage", d["stage_ms_per_frame"], "clk", d["clocks"]["sm_mhz"], "W", d["clocks"].get("power_w"))
 PY
   done
 done
