@@ -46,6 +46,13 @@ gpf_status gpf_b200_plan_set_batch(gpf_b200_plan* plan, int frames);
  * milliseconds accumulated since profiling was (re)enabled. */
 gpf_status gpf_b200_plan_set_profiling(gpf_b200_plan* plan, int enable);
 int gpf_b200_plan_stage_times(gpf_b200_plan* plan, float* ms, int max_stages);
+/* Timeline of the recorded stage events (profiling enabled): for each mark
+ * since the last stage_times / stage_marks call, its stage id (0-4, or -1 for
+ * the end of a launch group) and its time in ms after `ref_event` (a
+ * cudaEvent_t recorded by the caller on the same device). Synchronises the
+ * events and consumes them; returns the number of marks written. */
+int gpf_b200_plan_stage_marks(gpf_b200_plan* plan, void* ref_event, float* t_ms, int* stage,
+                              int max_marks);
 
 /* Bytes of device workspace held by the plan. */
 size_t gpf_b200_plan_workspace_bytes(const gpf_b200_plan* plan);

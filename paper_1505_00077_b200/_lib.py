@@ -36,7 +36,7 @@ EXPORTED = (
     "gpf_free_bytes",
     "gpf_set_num_threads", "gpf_get_num_threads",
     "gpf_b200_plan_create", "gpf_b200_plan_destroy", "gpf_b200_plan_set_batch",
-    "gpf_b200_plan_set_profiling", "gpf_b200_plan_stage_times", "gpf_b200_plan_workspace_bytes",
+    "gpf_b200_plan_set_profiling", "gpf_b200_plan_stage_times", "gpf_b200_plan_stage_marks", "gpf_b200_plan_workspace_bytes",
     "gpf_b200_plan_launches_per_frame", "gpf_b200_filter_f32", "gpf_b200_filter_f32_ev",
     "gpf_b200_filter_f32_host", "gpf_b200_exact_f32", "gpf_b200_compare_f32",
     "gpf_b200_set_precision", "gpf_b200_get_precision", "gpf_b200_last_precision",
@@ -109,6 +109,7 @@ def _declare(lib: C.CDLL) -> C.CDLL:
     lib.gpf_b200_plan_set_batch.argtypes = [vp, C.c_int]
     lib.gpf_b200_plan_set_profiling.argtypes = [vp, C.c_int]
     lib.gpf_b200_plan_stage_times.argtypes = [vp, C.POINTER(C.c_float), C.c_int]
+    lib.gpf_b200_plan_stage_marks.argtypes = [vp, vp, C.POINTER(C.c_float), C.POINTER(C.c_int), C.c_int]
     lib.gpf_b200_plan_workspace_bytes.restype = C.c_size_t
     lib.gpf_b200_plan_workspace_bytes.argtypes = [vp]
     lib.gpf_b200_plan_launches_per_frame.argtypes = [vp]

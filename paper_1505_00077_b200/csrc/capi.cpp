@@ -591,6 +591,18 @@ int gpf_b200_plan_stage_times(gpf_b200_plan* plan, float* ms, int max_stages) {
   }
 }
 
+int gpf_b200_plan_stage_marks(gpf_b200_plan* plan, void* ref_event, float* t_ms, int* stage,
+                              int max_marks) {
+  if (plan == nullptr || ref_event == nullptr || t_ms == nullptr || stage == nullptr || max_marks <= 0)
+    return 0;
+  try {
+    return gpfb::stage_marks(plan->plan, static_cast<cudaEvent_t>(ref_event), t_ms, stage, max_marks);
+  } catch (const gpfb::Error& e) {
+    fail(static_cast<gpf_status>(e.status), e.msg);
+    return 0;
+  }
+}
+
 size_t gpf_b200_plan_workspace_bytes(const gpf_b200_plan* plan) { return plan ? plan->plan.bytes : 0; }
 
 int gpf_b200_plan_launches_per_frame(const gpf_b200_plan* plan) {

@@ -196,6 +196,22 @@ RangeConsts make_range_consts(const Params& p) {
   return rc;
 }
 
+void fill_gscale_consts(TileConsts& tc, RangeConsts& rc) {
+  // K_n = prod_{i<n} w_i = 2^{kn}/n! takes plane n from the seed chain
+  // (es m^n = F_n 2^{s0-kn} S^2) to G units (F_n 2^{s0} S^2 / n!)
+  double K[34];
+  K[0] = 1.0;
+  for (int n = 1; n < 34; ++n) K[n] = K[n - 1] * rc.w_step[n - 1];
+  for (int g = 0; g < 16; ++g) {
+    tc.gstep[g] = make_float2(static_cast<float>(static_cast<double>(rc.w_step[2 * g]) * rc.w_step[2 * g + 1]),
+                              static_cast<float>(static_cast<double>(rc.w_step[2 * g + 1]) * rc.w_step[2 * g + 2]));
+    tc.gpre[g] = static_cast<float>(K[2 * g]);
+    tc.gw[g] = rc.w_step[2 * g];
+    tc.gcar[g] = make_float2(static_cast<float>(K[2 * g]), static_cast<float>(K[2 * g + 1]));
+  }
+  rc.q_thresh_g = static_cast<float>(static_cast<double>(rc.q_thresh) * rc.e_scale);
+}
+
 void finalize_range_consts(RangeConsts& rc) {
   const double ei = std::floor(rc.e_log2);
   rc.e_int = static_cast<int>(ei);

@@ -66,7 +66,16 @@ struct TileConsts {
   float2 pTr2[2], pTi2[2];              // p_k^kTile
   float2 pYr2[2], pYi2[2];              // p_k^(rows in the last row chunk)
   float2 pXr2[2], pXi2[2];              // p_k^(columns in the last column strip)
+  // G-scaled planes (GPF_GSCALE, pairs <= kGsPairs): the column pass stores
+  // plane n as G_n = F_n 2^{s0} / n! (every 1/n! folded into the plane, so the
+  // row pass contracts with a joint Horner pass for Q and Q' = P and no
+  // per-plane weights). With w_n = 2^k/(n+1) (RangeConsts::w_step):
+  float2 gstep[16];                     // pair step: (w_2g w_2g+1, w_2g+1 w_2g+2) times m^2
+  float gpre[16];                       // prod_{i<2g} w_i: first plane of pair g from es m^{2g}
+  float gw[16];                         // w_2g: second plane of pair g from its first (times m)
+  float2 gcar[16];                      // (prod_{i<2g} w_i, prod_{i<2g+1} w_i): carry-walk states -> G units
 };
+constexpr int kGsPairs = 12;            // G-scaled contraction: the k_rowpass2 path (N <= 22)
 
 // Range / plane constants. Plane n holds F_n * 2^{s_n}, s_n = s0 - k*n, so
 // that every significant plane value stays in the fp32 normal range (the
@@ -84,6 +93,7 @@ struct RangeConsts {
   float w_step[kMaxPlanes];  // 2^k/(n+1): c_{n+1} = c_n * H * w_step[n]
   float k_coef[kMaxPlanes];  // 2^-s0 2^{kn} / n!: c_n = H^n k_coef[n] (Horner contraction)
   float q_thresh;     // kQMin / (mass^2 * kernel_scale)  (bilateral.hpp:85)
+  float q_thresh_g;   // the same threshold in G units (q_thresh 2^{s0}; GPF_GSCALE)
   int planes;         // N + 2
   int pairs;          // ceil(planes / 2)
   int degree;         // N
@@ -105,6 +115,7 @@ struct Params {
 // Host-side constant builders (coeffs.cpp).
 FilterConsts make_filter_consts(double sigma_s);
 TileConsts make_tile_consts(double sigma_s, int width, int height);
+void fill_gscale_consts(TileConsts& tc, RangeConsts& rc);  // G-scaled plane constants
 RangeConsts make_range_consts(const Params& p);
 void finalize_range_consts(RangeConsts& rc);  // after e_log2 is final: the fp32 prologue split
 double kernel_mass_1d(double sigma_s, int radius);
@@ -159,6 +170,7 @@ enum Stage { kStageMean = 0, kStageColCarry, kStageColPass, kStageRowScan, kStag
 void stage_mark(Plan& plan, int stage, cudaStream_t st);  // records "stage begins"
 void stage_end(Plan& plan, cudaStream_t st);              // records "last stage ends"
 int stage_times(Plan& plan, float* ms, int max_stages);   // accumulated ms per stage; syncs
+int stage_marks(Plan& plan, cudaEvent_t ref, float* t_ms, int* stage, int max_marks);  // timeline; syncs
 void stage_reset(Plan& plan);
 
 // Status-carrying error used inside the library.

@@ -366,6 +366,9 @@ __device__ __forceinline__ void sts64(float2* p, float2 v) {
   asm volatile("st.shared.v2.f32 [%0], {%1, %2};\n" ::"r"(smem_u32(p)), "f"(v.x), "f"(v.y) : "memory");
 }
 
+#ifndef GPF_GSCALE
+#define GPF_GSCALE 0  // G-scaled planes + joint Horner contraction (TileConsts::gstep)
+#endif
 #ifndef GPF_L2HINT
 #define GPF_L2HINT 0  // evict-first L2 policies: 1 V stores, 2 V loads, 4 EM loads (column pass), 8 row-pass f/out
 #endif
@@ -375,8 +378,9 @@ __device__ __forceinline__ void sts64(float2* p, float2 v) {
 #ifndef GPF_PROD_PAIRCHAIN
 #define GPF_PROD_PAIRCHAIN 1
 #endif
+template <bool GS = false>
 __device__ __forceinline__ void produce_group(float* stage, const float2* emt, int pair0,
-                                              int npairs) {
+                                              int npairs, const TileConsts* tcp = nullptr) {
   constexpr int kIt = 4;  // 512 items = 4 x 128 threads (4-warp CTAs)
   const int tid = threadIdx.y * 32 + threadIdx.x;
 #if GPF_PROD_PAIRCHAIN
@@ -401,8 +405,16 @@ __device__ __forceinline__ void produce_group(float* stage, const float2* emt, i
       xa *= pow_group(m2[2 * k], pair0);
       xb *= pow_group(m2[2 * k + 1], pair0);
     }
-    a[k] = make_float2(xa, xa * ta.y);
-    b[k] = make_float2(xb, xb * tb.y);
+    if constexpr (GS) {  // G units: plane n carries 1/n! (K_n = prod_{i<n} w_i)
+      const float pre = tcp->gpre[pair0], w0 = tcp->gw[pair0];
+      xa *= pre;
+      xb *= pre;
+      a[k] = make_float2(xa, xa * (ta.y * w0));
+      b[k] = make_float2(xb, xb * (tb.y * w0));
+    } else {
+      a[k] = make_float2(xa, xa * ta.y);
+      b[k] = make_float2(xb, xb * tb.y);
+    }
     dst[k] = reinterpret_cast<float2*>(stage_at(stage + c * 32, j, c & 7));
   }
   // every pair slot of the stage is written (a group's missing pairs hold
@@ -416,8 +428,14 @@ __device__ __forceinline__ void produce_group(float* stage, const float2* emt, i
       sts64(dst[k] + gg * 1024, a[k]);
       sts64(dst[k] + gg * 1024 + 1, b[k]);
       if (gg + 1 < kColGroup) {
-        a[k] = mul2(a[k], f2(m2[2 * k]));
-        b[k] = mul2(b[k], f2(m2[2 * k + 1]));
+        if constexpr (GS) {  // (G_{2g+2}, G_{2g+3}) = (G_2g, G_2g+1) * m^2 * gstep[g]
+          const float2 st2 = tcp->gstep[pair0 + gg];
+          a[k] = mul2(a[k], mul2(f2(m2[2 * k]), st2));
+          b[k] = mul2(b[k], mul2(f2(m2[2 * k + 1]), st2));
+        } else {
+          a[k] = mul2(a[k], f2(m2[2 * k]));
+          b[k] = mul2(b[k], f2(m2[2 * k + 1]));
+        }
       }
     }
   }
@@ -471,7 +489,7 @@ __device__ __forceinline__ void produce_group(float* stage, const float2* emt, i
 constexpr bool kColXreg = GPF_COL_XREG != 0;
 constexpr int kColStages = GPF_COL_STAGES;  // staging tiles per CTA (1: store drains under the H-dots)
 
-template <bool AEV>
+template <bool AEV, bool GS>
 __global__ void __launch_bounds__(32 * kColGroup, GPF_COL_CTAS) k_colpass_tma(
     const float4* __restrict__ CA_all, float4* __restrict__ AH_all, int w, int h, int ny, int nx,
     int pairs, int groups, FilterConsts fc, TileConsts tc,
@@ -541,11 +559,17 @@ __global__ void __launch_bounds__(32 * kColGroup, GPF_COL_CTAS) k_colpass_tma(
     mbar_wait(&em_full, cy & 1);  // this chunk's seeds have landed
     GPF_TICK(1);
 #ifndef GPF_DIAG_NO_PROD
-    produce_group(stage, emt, pair0, npairs);
+    produce_group<GS>(stage, emt, pair0, npairs, &tc);
 #endif
     GPF_TICK(2);
     PairState as;
-    ps_from_carry(as, ca0, ca1, fc);
+    if constexpr (GS) {  // the carry walk's states are in seed-chain units: scale to G units
+      const float2 kc = tc.gcar[min(g, 15)];
+      ps_from_carry(as, make_float4(ca0.x * kc.x, ca0.y * kc.y, ca0.z * kc.x, ca0.w * kc.y),
+                    make_float4(ca1.x * kc.x, ca1.y * kc.y, ca1.z * kc.x, ca1.w * kc.y), fc);
+    } else {
+      ps_from_carry(as, ca0, ca1, fc);
+    }
     if (cy + 1 < ny) {
       ca0 = __ldg(ca_ptr + (size_t)(cy + 1) * ca_stride);
       ca1 = __ldg(ca_ptr + (size_t)(cy + 1) * ca_stride + 1);
@@ -555,7 +579,11 @@ __global__ void __launch_bounds__(32 * kColGroup, GPF_COL_CTAS) k_colpass_tma(
     if (tid == 0 && cy + 1 < ny) {  // the EM tile is free again: fetch the next chunk's
       mbar_arrive_expect_tx(&em_full, 32 * 32 * sizeof(float2));
       if constexpr (GPF_L2HINT & 4) tma_load_3d_hint(emt, &emmap, 2 * x0, y0 + kTile, f, &em_full, l2_evict_first());
+#ifdef GPF_DIAG_EM_L2  // diagnostic: EM tiles from a 256x256-pixel (L2-resident) region
+      else tma_load_3d(emt, &emmap, 2 * (x0 & 255), (y0 + kTile) & 255, f, &em_full);
+#else
       else tma_load_3d(emt, &emmap, 2 * x0, y0 + kTile, f, &em_full);
+#endif
     }
     float* mcol = stage + col_off;
     if (active && x < w && rows == kTile) {
@@ -948,7 +976,11 @@ __device__ __forceinline__ void carry_walk_rs(float2* tiles, uint64_t* full, flo
     __syncthreads();  // every warp is done with slot s
     if (tid == 0 && k + kCarrySlots < ny) {
       mbar_arrive_expect_tx(&full[s], 32 * kCarryCols * sizeof(float2));
+#ifdef GPF_DIAG_EMC_L2
+      tma_load_3d(tiles + (size_t)s * 32 * kCarryCols, emcmap, 2 * (x0 & 255), ((cy - kCarrySlots) * kTile) & 255, f,
+#else
       tma_load_3d(tiles + (size_t)s * 32 * kCarryCols, emcmap, 2 * x0, (cy - kCarrySlots) * kTile, f,
+#endif
                   &full[s]);
     }
   }
@@ -1016,7 +1048,11 @@ __device__ __forceinline__ void carry_walk(float2* tiles, uint64_t* full,
     __syncthreads();  // every warp is done with slot s
     if (tid == 0 && k + kCarrySlots < ny) {
       mbar_arrive_expect_tx(&full[s], 32 * kCarryCols * sizeof(float2));
+#ifdef GPF_DIAG_EMC_L2
+      tma_load_3d(tiles + (size_t)s * 32 * kCarryCols, emcmap, 2 * (x0 & 255), ((cy - kCarrySlots) * kTile) & 255, f,
+#else
       tma_load_3d(tiles + (size_t)s * 32 * kCarryCols, emcmap, 2 * x0, (cy - kCarrySlots) * kTile, f,
+#endif
                   &full[s]);
     }
   }
@@ -1310,6 +1346,7 @@ void plan_init(Plan& plan, const Params& p, int device, int batch) {
   plan.rc = make_range_consts(p);
   plan.rc.e_log2 += plan.fc.seed_log2;  // column-pass input carries S^2 (emit normalisation)
   finalize_range_consts(plan.rc);
+  fill_gscale_consts(plan.tc, plan.rc);
   const int pairs = plan.rc.pairs;
   if (rowpass_nbuf<double, double>(pairs) == 0 || colpass_smem<double>(pairs) > 227 * 1024)
     throw Error{1, "RangeParams: degree must be <= 48 in the B200 library"};
@@ -1437,6 +1474,9 @@ void plan_free(Plan& plan) {
 #define GPF_CARRY_TMA 1
 #endif
 
+// G-scaled planes on the TMA column pass + k_rowpass2 path
+static bool plan_gscale(const Plan& plan) { return GPF_GSCALE && plan.rc.pairs <= kGsPairs; }
+
 template <int MAXT, typename Tin, typename Tout>
 static void launch_passes(Plan& plan, const Tin* d_in, Tout* d_out, int count,
                           unsigned long long* d_fb, cudaStream_t st) {
@@ -1506,7 +1546,9 @@ static void launch_passes(Plan& plan, const Tin* d_in, Tout* d_out, int count,
   }
   stage_mark(plan, kStageColPass, st);
   if constexpr (kCanStage) {
-    auto kc = plan.fc.aev.x != 0.f ? k_colpass_tma<true> : k_colpass_tma<false>;
+    const bool gs = plan_gscale(plan);
+    auto kc = plan.fc.aev.x != 0.f ? (gs ? k_colpass_tma<true, true> : k_colpass_tma<true, false>)
+                                   : (gs ? k_colpass_tma<false, true> : k_colpass_tma<false, false>);
     check(cudaFuncSetAttribute(kc, cudaFuncAttributeMaxDynamicSharedMemorySize, psm),
           "cudaFuncSetAttribute");
     kc<<<dim3(plan.nx * groups, count), dim3(32, kColGroup), psm, st>>>(
@@ -1639,6 +1681,25 @@ int stage_times(Plan& plan, float* ms, int max_stages) {
   }
   const int n = std::min(max_stages, static_cast<int>(kNumStages));
   for (int i = 0; i < n; ++i) ms[i] = t ? t->acc[i] : 0.f;
+  return n;
+}
+
+int stage_marks(Plan& plan, cudaEvent_t ref, float* t_ms, int* stage, int max_marks) {
+  StageTimer* t = plan.timer;
+  if (!t) return 0;
+  int n = 0;
+  for (auto& m : t->marks) {
+    if (n < max_marks) {
+      check(cudaEventSynchronize(m.ev), "cudaEventSynchronize");
+      float e = 0.f;
+      check(cudaEventElapsedTime(&e, ref, m.ev), "cudaEventElapsedTime");
+      t_ms[n] = e;
+      stage[n] = m.stage;
+      ++n;
+    }
+    cudaEventDestroy(m.ev);
+  }
+  t->marks.clear();
   return n;
 }
 

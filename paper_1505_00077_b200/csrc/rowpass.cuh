@@ -326,6 +326,46 @@ __device__ __forceinline__ unsigned contract_px(const float2* Ts, const Tin* Fs,
   // offsets and the k_n are immediates.
   constexpr int kTop = NFIX > 0 ? NFIX : kRow2MaxN;
   constexpr int kPS = row2_pair_cols<RB>() * RB;  // float2 per pair in a slot
+  float2 qp[kPx];
+  if constexpr (GPF_GSCALE) {
+    // G units: plane n holds Gbar_n = Fbar_n 2^{s0} / n!, so
+    //   Q 2^{s0} = sum_{n<=N} H^n Gbar_n = b,   P 2^{s0} = sum_{n<=N} (n+1) H^n Gbar_{n+1} = d,
+    // P being Q's derivative plus the top term: one joint Horner pass,
+    //   d <- d H + b,  b <- b H + Gbar_n     (b = Gbar_N, d = (N+1) Gbar_{N+1} first),
+    // taken two planes at a time from pair g = (Gbar_2g, Gbar_2g+1) = L:
+    //   (d, b) <- (d, b) H^2 + (2 b H + L.y, H L.y + L.x).
+    float2 db[kPx], h21[kPx];
+    float hsq[kPx];
+#pragma unroll
+    for (int k = 0; k < kPx; ++k) {
+      h21[k] = make_float2(2.f * Hf[k], Hf[k]);
+      hsq[k] = Hf[k] * Hf[k];
+      const float2 lo = Ts[off[k] + (nN >> 1) * kPS];
+      if (!(nN & 1)) {
+        db[k] = make_float2(static_cast<float>(nN + 1) * lo.y, lo.x);
+      } else {  // N odd: Gbar_N = lo.y, Gbar_{N+1} in the next pair; then plane N-1 alone
+        const float g1 = Ts[off[k] + ((nN + 1) >> 1) * kPS].x;
+        float d = static_cast<float>(nN + 1) * g1, b = lo.y;
+        d = fmaf(d, Hf[k], b);
+        b = fmaf(b, Hf[k], lo.x);
+        db[k] = make_float2(d, b);
+      }
+    }
+    constexpr int kTopG = (kTop >> 1) - 1;  // highest pair taken two planes at a time
+    const int gTop = (nN & 1) ? ((nN - 3) >> 1) : ((nN >> 1) - 1);
+#pragma unroll
+    for (int gq = kTopG; gq >= 0; --gq) {
+      if (gq > gTop) continue;
+#pragma unroll
+      for (int k = 0; k < kPx; ++k) {
+        const float2 L = Ts[off[k] + gq * kPS];
+        const float2 u = fma2(make_float2(db[k].y, L.y), h21[k], make_float2(L.y, L.x));
+        db[k] = fma2(db[k], f2(hsq[k]), u);
+      }
+    }
+#pragma unroll
+    for (int k = 0; k < kPx; ++k) qp[k] = make_float2(db[k].y, db[k].x);  // (Q, P) in G units
+  } else {
   float2 acc[kPx], hi[kPx];
   {  // n = N
     const float kn = rc.k_coef[nN];
@@ -350,9 +390,12 @@ __device__ __forceinline__ unsigned contract_px(const float2* Ts, const Tin* Fs,
       hi[k] = lo;
     }
   }
-  float2 qp[kPx];
 #pragma unroll
   for (int k = 0; k < kPx; ++k) qp[k] = acc[k];
+  }
+  // G units: no P scale, the threshold in G units
+  const float qth = GPF_GSCALE ? rc.q_thresh_g : rc.q_thresh;
+  const float psc = GPF_GSCALE ? 1.f : rc.p_scale;
   // out = sr P/Q + t_c (bilateral.cpp:139-147); |Q| <= threshold -> input.
   // fp32 output: fp32 quotient (|error| <= sr |P/Q| 2^-22 < 1e-4 on [0, 255]);
   // fp64 output keeps the fp64 quotient.
@@ -362,17 +405,16 @@ __device__ __forceinline__ unsigned contract_px(const float2* Ts, const Tin* Fs,
     const int pr = p % RB, pc = p / RB;
     if (p < RB * 32 && (OSW || (pr < rows && pc < cols))) {  // the TMA store clips
       Tout o;
-      if (!(fabsf(qp[k].x) > rc.q_thresh)) {
+      if (!(fabsf(qp[k].x) > qth)) {
         o = static_cast<Tout>(Fs[f_at<OSW>(pr, pc)]);
         if (pr < rows && pc < cols) ++nfb;
       } else if constexpr (sizeof(Tout) == sizeof(float)) {
         // fast quotient (2 ulp) inside its range; |Q| > threshold >> 2^-126 here
-        const float num = qp[k].y * rc.p_scale, den = qp[k].x;
+        const float num = qp[k].y * psc, den = qp[k].x;
         const float q = fabsf(den) < 1e37f ? __fdividef(num, den) : num / den;
         o = fmaf(sr_f, q, tc_hi) + tc_lo;
       } else {
-        o = rc.sigma_r * ((static_cast<double>(qp[k].y) * rc.p_scale) / static_cast<double>(qp[k].x)) +
-            t_c;
+        o = rc.sigma_r * ((static_cast<double>(qp[k].y) * psc) / static_cast<double>(qp[k].x)) + t_c;
       }
       if constexpr (OSW) O[pr * 32 + ((((pc >> 2) ^ (pr & 7))) << 2) + (pc & 3)] = o;
       else O[pr * 33 + pc] = o;

@@ -275,6 +275,14 @@ class Plan:
         n = _lib.lib().gpf_b200_plan_stage_times(self.h, buf, len(self.STAGES))
         return {self.STAGES[i]: float(buf[i]) for i in range(n)}
 
+    def stage_marks(self, ref_event: int, max_marks: int = 4096) -> list:
+        """[(stage, ms after ref_event)] of the recorded stage events (stage -1 =
+        end of a launch group); `ref_event` is a cudaEvent_t handle. Syncs."""
+        t = (C.c_float * max_marks)()
+        st = (C.c_int * max_marks)()
+        n = _lib.lib().gpf_b200_plan_stage_marks(self.h, C.c_void_p(ref_event), t, st, max_marks)
+        return [(int(st[i]), float(t[i])) for i in range(n)]
+
     @property
     def workspace_bytes(self) -> int:
         return _lib.lib().gpf_b200_plan_workspace_bytes(self.h)
