@@ -198,9 +198,14 @@ RangeConsts make_range_consts(const Params& p) {
 
 void fill_gscale_consts(TileConsts& tc, RangeConsts& rc) {
   // K_n = prod_{i<n} w_i = 2^{kn}/n! takes plane n from the seed chain
-  // (es m^n = F_n 2^{s0-kn} S^2) to G units (F_n 2^{s0} S^2 / n!)
+  // (es m^n = F_n 2^{s0-kn} S^2) to G units (F_n 2^{s0} S^2 / n!), times
+  // 2^-kGsShift: G units are 2^{s0-64} = 2^36 times the true plane / n!, so
+  // the contraction's Q and P (which reach ~1e8 in true units just past the
+  // fp32 envelope, where the truncated series diverges) stay far from the fp32
+  // maximum, while every significant plane value stays normal
+  constexpr int kGsShift = 64;
   double K[34];
-  K[0] = 1.0;
+  K[0] = std::ldexp(1.0, -kGsShift);
   for (int n = 1; n < 34; ++n) K[n] = K[n - 1] * rc.w_step[n - 1];
   for (int g = 0; g < 16; ++g) {
     tc.gstep[g] = make_float2(static_cast<float>(static_cast<double>(rc.w_step[2 * g]) * rc.w_step[2 * g + 1]),
@@ -209,7 +214,7 @@ void fill_gscale_consts(TileConsts& tc, RangeConsts& rc) {
     tc.gw[g] = rc.w_step[2 * g];
     tc.gcar[g] = make_float2(static_cast<float>(K[2 * g]), static_cast<float>(K[2 * g + 1]));
   }
-  rc.q_thresh_g = static_cast<float>(static_cast<double>(rc.q_thresh) * rc.e_scale);
+  rc.q_thresh_g = static_cast<float>(static_cast<double>(rc.q_thresh) * rc.e_scale * K[0]);
 }
 
 void finalize_range_consts(RangeConsts& rc) {

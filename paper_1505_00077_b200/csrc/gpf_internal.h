@@ -67,7 +67,7 @@ struct TileConsts {
   float2 pYr2[2], pYi2[2];              // p_k^(rows in the last row chunk)
   float2 pXr2[2], pXi2[2];              // p_k^(columns in the last column strip)
   // G-scaled planes (GPF_GSCALE, pairs <= kGsPairs): the column pass stores
-  // plane n as G_n = F_n 2^{s0} / n! (every 1/n! folded into the plane, so the
+  // plane n as G_n = F_n 2^{s0-64} / n! (every 1/n! folded into the plane, so the
   // row pass contracts with a joint Horner pass for Q and Q' = P and no
   // per-plane weights). With w_n = 2^k/(n+1) (RangeConsts::w_step):
   float2 gstep[16];                     // pair step: (w_2g w_2g+1, w_2g+1 w_2g+2) times m^2
@@ -93,7 +93,7 @@ struct RangeConsts {
   float w_step[kMaxPlanes];  // 2^k/(n+1): c_{n+1} = c_n * H * w_step[n]
   float k_coef[kMaxPlanes];  // 2^-s0 2^{kn} / n!: c_n = H^n k_coef[n] (Horner contraction)
   float q_thresh;     // kQMin / (mass^2 * kernel_scale)  (bilateral.hpp:85)
-  float q_thresh_g;   // the same threshold in G units (q_thresh 2^{s0}; GPF_GSCALE)
+  float q_thresh_g;   // the same threshold in G units (q_thresh 2^{s0-64}; GPF_GSCALE)
   int planes;         // N + 2
   int pairs;          // ceil(planes / 2)
   int degree;         // N

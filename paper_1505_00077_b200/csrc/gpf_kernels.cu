@@ -367,7 +367,7 @@ __device__ __forceinline__ void sts64(float2* p, float2 v) {
 }
 
 #ifndef GPF_GSCALE
-#define GPF_GSCALE 0  // G-scaled planes + joint Horner contraction (TileConsts::gstep)
+#define GPF_GSCALE 1  // G-scaled planes + joint Horner contraction (TileConsts::gstep); 0: per-plane weights
 #endif
 #ifndef GPF_L2HINT
 #define GPF_L2HINT 0  // evict-first L2 policies: 1 V stores, 2 V loads, 4 EM loads (column pass), 8 row-pass f/out
@@ -1289,8 +1289,12 @@ template <typename Tin>
 static size_t colpass_smem(int pairs) {  // k_colpass and k_col_carry
   return sizeof(float2) * (size_t)pairs * 32 * 33 + sizeof(Tin) * 2 * 32 * 33;
 }
+#ifndef GPF_COL_SMEM_KB
+#define GPF_COL_SMEM_KB 0  // > 0: pad the column pass's shared memory (fewer CTAs per SM, room for others)
+#endif
 static size_t colpass_tma_smem() {  // stages of a pair group + EM tile + alignment slack
-  return kStageAlign + sizeof(float) * kColStages * kColGroup * 2048 + sizeof(float2) * 32 * 32;
+  const size_t need = kStageAlign + sizeof(float) * kColStages * kColGroup * 2048 + sizeof(float2) * 32 * 32;
+  return std::max<size_t>(need, (size_t)GPF_COL_SMEM_KB * 1024);
 }
 template <typename Tin, typename Tout>
 static int rowpass_nbuf(int pairs) {  // deepest V ring that fits in 227 KB (0: none)

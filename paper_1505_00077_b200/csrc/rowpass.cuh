@@ -328,8 +328,8 @@ __device__ __forceinline__ unsigned contract_px(const float2* Ts, const Tin* Fs,
   constexpr int kPS = row2_pair_cols<RB>() * RB;  // float2 per pair in a slot
   float2 qp[kPx];
   if constexpr (GPF_GSCALE) {
-    // G units: plane n holds Gbar_n = Fbar_n 2^{s0} / n!, so
-    //   Q 2^{s0} = sum_{n<=N} H^n Gbar_n = b,   P 2^{s0} = sum_{n<=N} (n+1) H^n Gbar_{n+1} = d,
+    // G units: plane n holds Gbar_n = Fbar_n 2^{s0-64} / n! (coeffs.cpp), so with T = 2^{s0-64}
+    //   Q T = sum_{n<=N} H^n Gbar_n = b,   P T = sum_{n<=N} (n+1) H^n Gbar_{n+1} = d,
     // P being Q's derivative plus the top term: one joint Horner pass,
     //   d <- d H + b,  b <- b H + Gbar_n     (b = Gbar_N, d = (N+1) Gbar_{N+1} first),
     // taken two planes at a time from pair g = (Gbar_2g, Gbar_2g+1) = L:
