@@ -290,13 +290,14 @@ def algorithmic_flops_per_px(pairs: int) -> dict:
     One IIR step of one plane in the output-aligned section basis (DESIGN.md
     section 3): two sections advanced, 3 FMA each, in each direction = 24;
     emits ~6; i.e. ~30 per plane, 60 per pair. Strip/chunk dot products: 4 FMA
-    per plane. Contraction: 2 FMA + 2 MUL per plane.
+    per plane. Contraction on G-scaled planes: two packed FMAs
+    per plane pair (joint Horner of Q and P = Q'), i.e. 2 FMA per plane.
       carries    seeds ~20 + per pair: planes 2 MUL, dots 16          18 P + 20
-      colpass    per pair: planes 2, sweeps 60, row dots 16           78 P
+      colpass    per pair: planes 2 MUL + 2 (1/n!), sweeps 60, dots 16 80 P
       row_scan   per pair: one chain step per 32 pixels              ~P
-      rowpass    per pair: sweeps 60, contraction 12                  72 P + 10"""
-    return {"mean": 1, "col_carry": 18 * pairs + 20, "colpass": 78 * pairs, "row_scan": pairs,
-            "rowpass": 72 * pairs + 10}
+      rowpass    per pair: sweeps 60, contraction 8; setup ~12        68 P + 12"""
+    return {"mean": 1, "col_carry": 18 * pairs + 20, "colpass": 80 * pairs, "row_scan": pairs,
+            "rowpass": 68 * pairs + 12}
 
 
 def fp32_peak_tflops(peaks: dict) -> float:
@@ -346,8 +347,15 @@ def roofline_block(px, frames, ms_step, stage_ms, degree, w, h) -> dict:
     hbm_src = ("MEASURED_PEAKS.json hbm_gbs (burst copy)" if "hbm_gbs" in peaks
                else "B200_PROFILING.md fallback")
     fp32_tf = fp32_peak_tflops(peaks)
-    dom = "rowpass" if "rowpass" in stage_ms else max(stage_ms, key=stage_ms.get)
+    heavy = [k for k in ("colpass", "rowpass") if k in stage_ms]
+    dom = max(heavy, key=stage_ms.get) if heavy else max(stage_ms, key=stage_ms.get)
     k_ms = stage_ms[dom]
+    # both heavy passes against their own 8(d) shares (the dominant one is `frac`)
+    per_kernel = {}
+    for k in heavy:
+        rk = roofline_of(px, stage_ms[k], model[k], fpp[k], hbm_peak, fp32_tf)
+        per_kernel[k] = {"ms": round(stage_ms[k], 4), "achieved": rk["achieved"], "frac": rk["frac"],
+                         "algorithmic_bytes_per_px": model[k]}
     roof = roofline_of(px, k_ms, model[dom], fpp[dom], hbm_peak, fp32_tf)
     fp_k = fpp[dom] * px / (k_ms / 1e3) / 1e12
     traffic = load_traffic(w, h)
@@ -357,7 +365,10 @@ def roofline_block(px, frames, ms_step, stage_ms, degree, w, h) -> dict:
     return dict(
         roof, kernel=dom, kernel_ms=round(k_ms, 4), traffic=t_launch,
         algorithmic_bytes_per_px=model[dom],
-        algorithmic_what=f"SURVEY 8(d) share of the {dom}: N+2 plane reads 4(N+2) + f 4 + out 4",
+        algorithmic_what=(f"SURVEY 8(d) share of the {dom}: " +
+                          ("N+2 plane reads 4(N+2) + f 4 + out 4" if dom == "rowpass"
+                           else "f 4 + N+2 plane writes 4(N+2)")),
+        kernels=per_kernel,
         traffic_over_algorithmic=round(t_launch / (model[dom] * px), 3) if t_launch else None,
         design_bytes_per_px=design[dom], algorithmic_flops_per_px=fpp[dom],
         fp32={"achieved_tflops": round(fp_k, 2), "peak_tflops": round(fp32_tf, 1),
@@ -811,8 +822,8 @@ def bench_reference(args):
     about REF_BUDGET_S, a full-width band of rows of it (the reference's cost
     per pixel does not depend on the frame height; the band moves down the
     frame from step to step). Warm-up steps page the library and the frames in
-    on a 1024^2 crop and time it to size the band. Under torchrun only rank 0
-    runs."""
+    on a 512-row full-width band and time it to size the band. Under torchrun
+    only rank 0 runs."""
     rank, world, _ = dist_env()
     if rank != 0:
         return
@@ -830,14 +841,16 @@ def bench_reference(args):
         c = synth.scaled(cfg, n, n) if args.size else cfg
         imgs = [synth.make(c, k).astype("float64") for k in range(len(cfg.sigma_s))]
         sig = list(cfg.sigma_s)
-    t_crop = None
-    for w in range(max(1, args.warmup)):
-        t0 = time.perf_counter()
-        run(imgs[0][:1024, :1024].copy(), sig[0], cfg.sigma_r, cfg.degree)
-        t_crop = time.perf_counter() - t0
     h, w = imgs[0].shape
+    cal_rows = min(h, 512)
+    t_cal = None
+    for _ in range(max(1, args.warmup)):
+        t0 = time.perf_counter()
+        run(np.ascontiguousarray(imgs[0][:cal_rows]), sig[0], cfg.sigma_r, cfg.degree)
+        t_cal = time.perf_counter() - t0
     # rows per step: whole frames if K of them fit the budget, else a band
-    est_frame_s = t_crop / (1024 * 1024) * w * h
+    # (calibrated on a full-width band, with a 1.3x margin)
+    est_frame_s = 1.3 * t_cal * h / cal_rows
     rows = h
     if args.steps * est_frame_s > REF_BUDGET_S:
         rows = int(h * REF_BUDGET_S / (args.steps * est_frame_s)) // 64 * 64
