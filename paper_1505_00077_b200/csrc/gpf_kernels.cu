@@ -488,6 +488,10 @@ __device__ __forceinline__ void produce_group(float* stage, const float2* emt, i
 // second half (no re-reads from the stage; needs ~166 registers, 3 CTAs/SM)
 constexpr bool kColXreg = GPF_COL_XREG != 0;
 constexpr int kColStages = GPF_COL_STAGES;  // staging tiles per CTA (1: store drains under the H-dots)
+#ifndef GPF_COL_EMBUFS
+#define GPF_COL_EMBUFS 2
+#endif
+constexpr int kColEmBufs = GPF_COL_EMBUFS;  // EM seed tiles in flight (2: loaded two chunks ahead)
 
 template <bool AEV, bool GS>
 __global__ void __launch_bounds__(32 * kColGroup, GPF_COL_CTAS) k_colpass_tma(
@@ -499,7 +503,7 @@ __global__ void __launch_bounds__(32 * kColGroup, GPF_COL_CTAS) k_colpass_tma(
 #endif
     ) {
   extern __shared__ float4 smem4[];
-  __shared__ uint64_t em_full;
+  __shared__ uint64_t em_full[kColEmBufs];
   const int f = blockIdx.y, lane = threadIdx.x, gl = threadIdx.y;
   const int tid = gl * 32 + lane;
   // pair group fastest in the grid: a strip's groups run together and share
@@ -514,9 +518,18 @@ __global__ void __launch_bounds__(32 * kColGroup, GPF_COL_CTAS) k_colpass_tma(
   float* stages = reinterpret_cast<float*>(reinterpret_cast<char*>(smem4) +
                                            ((kStageAlign - smem_u32(smem4)) & (kStageAlign - 1)));
   constexpr int kStageFloats = kColGroup * 2048;
-  float2* emt = reinterpret_cast<float2*>(stages + kColStages * kStageFloats);  // [32][32]
+  float2* emts = reinterpret_cast<float2*>(stages + kColStages * kStageFloats);  // [kColEmBufs][32][32]
   const int x0 = strip * 32, x = x0 + lane;
   const int cols = min(32, w - x0);
+  // EM tile of the chunk starting at row y into buffer b (TMA, completion on em_full[b])
+  auto load_em = [&](int b, int y) {
+    mbar_arrive_expect_tx(&em_full[b], 32 * 32 * sizeof(float2));
+#ifdef GPF_DIAG_EM_L2  // diagnostic: EM tiles from a 256x256-pixel (L2-resident) region
+    tma_load_3d(emts + b * 1024, &emmap, 2 * (x0 & 255), y & 255, f, &em_full[b]);
+#else
+    tma_load_3d(emts + b * 1024, &emmap, 2 * x0, y, f, &em_full[b]);
+#endif
+  };
   const float4* CA = CA_all + (size_t)f * ny * pairs * w * 2;
   float4* AH = AH_all + (size_t)f * nx * pairs * h * 2;
   const int cm = lane & 7;
@@ -525,14 +538,12 @@ __global__ void __launch_bounds__(32 * kColGroup, GPF_COL_CTAS) k_colpass_tma(
   const int hq = (lane & 15) >> 1;
   const int hd_off = (gl * 64 + (lane >> 4) * 32) * 32 + (lane & 1) * 2;
   if (tid == 0) {
-    mbar_init(&em_full, 1);
+    for (int b = 0; b < kColEmBufs; ++b) mbar_init(&em_full[b], 1);
     mbar_fence_init();
   }
   __syncthreads();
-  if (tid == 0) {
-    mbar_arrive_expect_tx(&em_full, 32 * 32 * sizeof(float2));
-    if constexpr (GPF_L2HINT & 4) tma_load_3d_hint(emt, &emmap, 2 * x0, 0, f, &em_full, l2_evict_first());
-    else tma_load_3d(emt, &emmap, 2 * x0, 0, f, &em_full);
+  if (tid == 0) {  // the first kColEmBufs chunks' seeds
+    for (int b = 0; b < kColEmBufs && b < ny; ++b) load_em(b, b * kTile);
   }
   PairState cs;  // causal state, carried across chunks
   ps_zero(cs);
@@ -556,10 +567,11 @@ __global__ void __launch_bounds__(32 * kColGroup, GPF_COL_CTAS) k_colpass_tma(
     }
     __syncthreads();
     GPF_TICK(0);
-    mbar_wait(&em_full, cy & 1);  // this chunk's seeds have landed
+    const int eb = cy % kColEmBufs;
+    mbar_wait(&em_full[eb], (cy / kColEmBufs) & 1);  // this chunk's seeds have landed
     GPF_TICK(1);
 #ifndef GPF_DIAG_NO_PROD
-    produce_group<GS>(stage, emt, pair0, npairs, &tc);
+    produce_group<GS>(stage, emts + eb * 1024, pair0, npairs, &tc);
 #endif
     GPF_TICK(2);
     PairState as;
@@ -576,15 +588,8 @@ __global__ void __launch_bounds__(32 * kColGroup, GPF_COL_CTAS) k_colpass_tma(
     }
     __syncthreads();
     GPF_TICK(3);
-    if (tid == 0 && cy + 1 < ny) {  // the EM tile is free again: fetch the next chunk's
-      mbar_arrive_expect_tx(&em_full, 32 * 32 * sizeof(float2));
-      if constexpr (GPF_L2HINT & 4) tma_load_3d_hint(emt, &emmap, 2 * x0, y0 + kTile, f, &em_full, l2_evict_first());
-#ifdef GPF_DIAG_EM_L2  // diagnostic: EM tiles from a 256x256-pixel (L2-resident) region
-      else tma_load_3d(emt, &emmap, 2 * (x0 & 255), (y0 + kTile) & 255, f, &em_full);
-#else
-      else tma_load_3d(emt, &emmap, 2 * x0, y0 + kTile, f, &em_full);
-#endif
-    }
+    if (tid == 0 && cy + kColEmBufs < ny)  // EM buffer eb is free again: fetch chunk cy + kColEmBufs
+      load_em(eb, y0 + kColEmBufs * kTile);
     float* mcol = stage + col_off;
     if (active && x < w && rows == kTile) {
       // full chunk: both directions in one branch-free loop (two independent
@@ -1293,7 +1298,7 @@ static size_t colpass_smem(int pairs) {  // k_colpass and k_col_carry
 #define GPF_COL_SMEM_KB 0  // > 0: pad the column pass's shared memory (fewer CTAs per SM, room for others)
 #endif
 static size_t colpass_tma_smem() {  // stages of a pair group + EM tile + alignment slack
-  const size_t need = kStageAlign + sizeof(float) * kColStages * kColGroup * 2048 + sizeof(float2) * 32 * 32;
+  const size_t need = kStageAlign + sizeof(float) * kColStages * kColGroup * 2048 + sizeof(float2) * 32 * 32 * kColEmBufs;
   return std::max<size_t>(need, (size_t)GPF_COL_SMEM_KB * 1024);
 }
 template <typename Tin, typename Tout>
