@@ -95,19 +95,26 @@ __device__ __forceinline__ double deriche_step(const double (&c)[4], const doubl
 // reference's multiply chain), and the chunk of outputs leaves through a
 // [plane][row][column] tile. The anticausal walk reloads the causal outputs
 // the same way and adds its own (dst[i] += y-, spatial.cpp:211).
-constexpr int kRowT = 32;  // rows per CTA == lanes == columns per chunk
+constexpr int kRowT = 32;  // rows per CTA == lanes
+#ifndef GPF_F64_ROW_CHUNK
+#define GPF_F64_ROW_CHUNK 32
+#endif
+// columns per staged chunk (32: 256-B row segments, 34 KB of tiles per one-warp
+// CTA; 16 halves the tiles and doubles the CTAs per SM but measured slower:
+// C5 8.15 vs 7.89 ms, C2 3.08 vs 2.73 ms)
+constexpr int kRowC = GPF_F64_ROW_CHUNK;
 
 __global__ void __launch_bounds__(32) k_f64_rows(const double* __restrict__ H,
                                                  const double* __restrict__ F0,
                                                  double* __restrict__ R, int w, int h, int planes,
                                                  Deriche64 k) {
-  __shared__ double sH[kRowT][kRowT + 1], sF[kRowT][kRowT + 1];
-  __shared__ double sR[kGP][kRowT][kRowT + 1];
+  __shared__ double sH[kRowT][kRowC + 1], sF[kRowT][kRowC + 1];
+  __shared__ double sR[kGP][kRowT][kRowC + 1];
   const int lane = threadIdx.x;
   const int y0 = blockIdx.x * kRowT, rows = min(kRowT, h - y0);
   const int n0 = blockIdx.y * kGP, np = min(kGP, planes - n0);
   const size_t ps = (size_t)w * h;
-  const int nc = (w + kRowT - 1) / kRowT;
+  const int nc = (w + kRowC - 1) / kRowC;
   // global -> shared copies as cp.async (LDGSTS): all of a chunk's row
   // segments in flight at once instead of one load latency per row
   auto cp8 = [](double* smem, const double* gmem) {
@@ -162,7 +169,7 @@ __global__ void __launch_bounds__(32) k_f64_rows(const double* __restrict__ H,
   double x[kGP], xm1[kGP], xm2[kGP], xm3[kGP], ym1[kGP], ym2[kGP], ym3[kGP], ym4[kGP];
   // causal (spatial.cpp:190-202): warm start from column 0
   for (int c = 0; c < nc; ++c) {
-    const int x0 = c * kRowT, cols = min(kRowT, w - x0);
+    const int x0 = c * kRowC, cols = min(kRowC, w - x0);
     load_in(x0, cols);
     wait_loads();
     __syncwarp();
@@ -196,7 +203,7 @@ __global__ void __launch_bounds__(32) k_f64_rows(const double* __restrict__ H,
   // anticausal (spatial.cpp:204-215): xp = x[i+1..i+4], warm start from column w-1
   double xp4[kGP];
   for (int c = nc - 1; c >= 0; --c) {
-    const int x0 = c * kRowT, cols = min(kRowT, w - x0);
+    const int x0 = c * kRowC, cols = min(kRowC, w - x0);
     load_in(x0, cols);
     load_r(x0, cols);
     wait_loads();
