@@ -209,3 +209,34 @@ def test_dropin_concurrent_host_threads(gpu):
     for (a, fa), (b, fb) in zip(seq, got):
         assert fa == fb
         np.testing.assert_array_equal(a, b)
+
+
+def test_stage_timing_and_timeline(gpu):
+    """Per-stage profiling of a plan (bench.py's stage times, tools/timeline.py):
+    stage_times sums every recorded stage, stage_marks returns the timeline --
+    stages 0..4 then the end marker per launch group, non-decreasing times after
+    the caller's reference event -- and consumes the events."""
+    import torch
+
+    w, h = 512, 384
+    img = torch.from_numpy(synth.rects_image(w, h, 8, 10.0, 11)).cuda()
+    out = torch.empty_like(img)
+    plan = gpu.Plan(w, h, 3.0, 30.0, 20)
+    try:
+        st = torch.cuda.current_stream()
+        plan.set_profiling(True)
+        plan.filter_device(img, out, 1, None, st.cuda_stream)
+        times = plan.stage_times()
+        assert set(times) == set(plan.STAGES) and all(v > 0 for v in times.values()), times
+        ref = torch.cuda.Event(enable_timing=True)
+        ref.record(st)
+        for _ in range(2):
+            plan.filter_device(img, out, 1, None, st.cuda_stream)
+        marks = plan.stage_marks(ref.cuda_event)
+        assert [s for s, _ in marks] == [0, 1, 2, 3, 4, -1] * 2, marks
+        ts = [t for _, t in marks]
+        assert ts[0] >= 0 and all(b >= a for a, b in zip(ts, ts[1:])), ts
+        assert plan.stage_marks(ref.cuda_event) == []  # consumed
+    finally:
+        plan.set_profiling(False)
+        plan.close()
