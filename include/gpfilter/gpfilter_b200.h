@@ -80,7 +80,7 @@ gpf_status gpf_b200_filter_f32_ev(gpf_b200_plan* plan, const float* d_in, float*
 /* Same as gpf_b200_filter_f32, and writes d_ill[f] (device memory, `count`
  * ints) = 1 when frame f lies outside the envelope in which the fp32 kernels
  * are held to the reference within 1e-3 (max|H| = max(f_max - t_c, t_c -
- * f_min) / sigma_r > gpf_b200_fp32_h_limit(), measured on the device from the
+ * f_min) / sigma_r > gpf_b200_fp32_h_limit_degree(degree), measured on the device from the
  * frame itself), else 0. Such a frame's fp32 output is still the fp32
  * evaluation, but the reference's own degree-N series is ill-conditioned there
  * (it may leave the input range); filter it through gpf_filter_gpf (AUTO runs
@@ -111,7 +111,9 @@ gpf_status gpf_b200_filter_f32_host(gpf_b200_plan* plan, const float* h_in, floa
  *   FP32  the fp32 plane kernels (the throughput path of gpf_b200_filter_f32),
  *         fp64 input/output and prologue. Held to max |out - reference| <= 1e-3
  *         on [0,255] while max|H| = max(f_max - t_c, t_c - f_min) / sigma_r <=
- *         gpf_b200_fp32_h_limit() and degree <= 48.
+ *         gpf_b200_fp32_h_limit_degree(degree) (7.0 at the default N = 20;
+ *         1.5-10 for other degrees: the truncated series cancels sooner at low
+ *         and odd N) and degree <= 48.
  *   FP64  the reference's own fp64 arithmetic replayed on the GPU operation for
  *         operation (only exp() is CUDA's rather than glibc's): follows the
  *         reference also where its degree-N series is ill-conditioned and its
@@ -134,7 +136,8 @@ gpf_status gpf_b200_set_precision(int mode);
 int gpf_b200_get_precision(void);
 int gpf_b200_last_precision(void);
 double gpf_b200_last_max_abs_h(void);
-double gpf_b200_fp32_h_limit(void);
+double gpf_b200_fp32_h_limit(void);             /* the envelope at the default degree (20) */
+double gpf_b200_fp32_h_limit_degree(int degree); /* the envelope at `degree` (0 outside 0..48) */
 /* Device time (CUDA events on the drop-in stream) of the filter kernels of this
  * thread's last gpf_filter_gpf call, copies excluded. */
 float gpf_b200_last_device_ms(void);

@@ -40,7 +40,7 @@ EXPORTED = (
     "gpf_b200_plan_launches_per_frame", "gpf_b200_filter_f32", "gpf_b200_filter_f32_ev",
     "gpf_b200_filter_f32_host", "gpf_b200_exact_f32", "gpf_b200_compare_f32",
     "gpf_b200_set_precision", "gpf_b200_get_precision", "gpf_b200_last_precision",
-    "gpf_b200_last_max_abs_h", "gpf_b200_fp32_h_limit", "gpf_b200_dropin_release",
+    "gpf_b200_last_max_abs_h", "gpf_b200_fp32_h_limit", "gpf_b200_fp32_h_limit_degree", "gpf_b200_dropin_release",
     "gpf_b200_last_device_ms", "gpf_b200_filter_f32_checked",
 )
 
@@ -119,6 +119,8 @@ def _declare(lib: C.CDLL) -> C.CDLL:
     lib.gpf_b200_set_precision.argtypes = [C.c_int]
     lib.gpf_b200_last_max_abs_h.restype = C.c_double
     lib.gpf_b200_fp32_h_limit.restype = C.c_double
+    lib.gpf_b200_fp32_h_limit_degree.restype = C.c_double
+    lib.gpf_b200_fp32_h_limit_degree.argtypes = [C.c_int]
     lib.gpf_b200_last_device_ms.restype = C.c_float
     lib.gpf_b200_filter_f32_checked.argtypes = [vp, vp, vp, C.c_int, vp, vp, vp]
     return lib

@@ -494,6 +494,7 @@ int gpf_b200_last_precision(void) { return gpfb::last_precision(); }
 double gpf_b200_last_max_abs_h(void) { return gpfb::last_max_abs_h(); }
 float gpf_b200_last_device_ms(void) { return gpfb::last_device_ms(); }
 double gpf_b200_fp32_h_limit(void) { return gpfb::kH32Limit; }
+double gpf_b200_fp32_h_limit_degree(int degree) { return gpfb::fp32_h_limit(degree); }
 void gpf_b200_dropin_release(void) { gpfb::dropin_release(); }
 
 gpf_status gpf_set_num_threads(int n) {

@@ -44,6 +44,28 @@ namespace gpfb {
 // first failure at 8.2 (|d| = 50). 7.0 keeps a margin below that cliff.
 const double kH32Limit = 7.0;
 
+// The envelope depends on the degree: the reference truncates exp(H_x H_y) at
+// degree N, and for pixels whose neighbours sit on the other side of t_c the
+// truncated alternating series cancels (for odd N it changes sign) long before
+// max|H| = 7; its fp64 evaluation of that cancellation is what the fp32 planes
+// cannot follow. Measured per degree (tools/h32_calibrate_n.py: 5 layouts x
+// max|H| 0.5-12 x sigma_s 2/8 at 256^2, fp32 forced vs the reference; the
+// largest sampled max|H| whose cases all stay <= 2e-4, the next sample being
+// past the cliff; profiles/r02_h32_calibration_n.jsonl). Degrees between two
+// sampled ones take the smaller of their limits.
+double fp32_h_limit(int degree) {
+  static const struct { int n; double lim; } kSampled[] = {
+      {0, 3.5}, {1, 1.5}, {2, 4.0}, {3, 2.5}, {5, 3.5}, {8, 6.0}, {10, 7.0}, {12, 7.0},
+      {15, 5.0}, {20, kH32Limit}, {25, 6.0}, {30, 8.0}, {40, 8.0}, {48, 10.0}};
+  constexpr int kN = sizeof(kSampled) / sizeof(kSampled[0]);
+  if (degree < 0 || degree > kSampled[kN - 1].n) return 0.0;
+  for (int i = 0; i < kN; ++i) {
+    if (kSampled[i].n == degree) return kSampled[i].lim;
+    if (kSampled[i].n > degree) return std::min(kSampled[i].lim, kSampled[i - 1].lim);
+  }
+  return 0.0;
+}
+
 namespace {
 
 constexpr int kDropinPlans = 8;                        // cached fp32 plans per device
@@ -242,7 +264,7 @@ long long dropin_gpf(const double* h_in, double* h_out, const Params& p) {
       chk(cudaMemcpyAsync(c.hscal, c.dscal, sizeof(double) * 2, cudaMemcpyDeviceToHost, c.st), "D2H");
       chk(cudaStreamSynchronize(c.st), "cudaStreamSynchronize");
       hmax = c.hscal[1];
-      mode = (hmax > kH32Limit || std::isnan(hmax)) ? kPrecFp64 : kPrecFp32;
+      mode = (hmax > fp32_h_limit(p.degree) || std::isnan(hmax)) ? kPrecFp64 : kPrecFp32;
     }
   }
   chk(cudaMemsetAsync(c.dfb, 0, sizeof(unsigned long long), c.st), "cudaMemsetAsync");

@@ -241,7 +241,8 @@ void run_gpf_f64_exact(const double* d_in, double* d_out, const Params& p, F64Wo
 // reference (max |H| = max(f_max - t_c, t_c - f_min) / sigma_r > kH32Limit),
 // or when the degree exceeds the fp32 kernels' limit.
 enum Precision { kPrecAuto = 0, kPrecFp32 = 1, kPrecFp64 = 2 };
-extern const double kH32Limit;
+extern const double kH32Limit;          // the envelope at the default degree N = 20
+double fp32_h_limit(int degree);        // the envelope at degree N (dropin.cpp)
 void set_precision(int mode);
 int get_precision();
 int last_precision();       // mode this thread's last drop-in call ran (1 or 2; 0 = none)

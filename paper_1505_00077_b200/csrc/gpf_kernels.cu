@@ -1643,7 +1643,7 @@ static void run_frames(Plan& plan, const Tin* d_in, Tout* d_out, int count,
   k_mean_partial<Tin><<<dim3(plan.mean_blocks, count), kMeanThreads, 0, st>>>(d_in, npx, plan.partials);
   k_mean_final<<<count, kMeanThreads, 0, st>>>(plan.partials, plan.mean_blocks, npx,
                                                plan.rc.centering, plan.rc.tc_fixed, plan.rc.inv_sr,
-                                               kH32Limit, plan.scalars, plan.ill_out);
+                                               fp32_h_limit(plan.rc.degree), plan.scalars, plan.ill_out);
   const int nthr = 32 * plan.rc.pairs;
   if (nthr <= 352) launch_passes<352>(plan, d_in, d_out, count, d_fb, st);  // N <= 20
   else if (nthr <= 384) launch_passes<384>(plan, d_in, d_out, count, d_fb, st);

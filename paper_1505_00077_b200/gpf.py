@@ -225,8 +225,12 @@ def last_device_ms() -> float:
     return _lib.lib().gpf_b200_last_device_ms()
 
 
-def fp32_h_limit() -> float:
-    return _lib.lib().gpf_b200_fp32_h_limit()
+def fp32_h_limit(degree: int | None = None) -> float:
+    """The fp32 envelope (max|H| up to which AUTO runs the fp32 kernels) at
+    `degree`, or at the default degree 20."""
+    if degree is None:
+        return _lib.lib().gpf_b200_fp32_h_limit()
+    return _lib.lib().gpf_b200_fp32_h_limit_degree(int(degree))
 
 
 def dropin_release() -> None:

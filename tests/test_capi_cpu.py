@@ -176,3 +176,18 @@ def test_exact_and_compare_validation_before_device():
     assert L.gpf_compare(img.h, img.h, -1, C.byref(rep)) == _lib.GPF_ERR_INVALID_ARGUMENT
     assert L.gpf_compare(img.h, img.h, 2, C.byref(rep)) == _lib.GPF_ERR_INVALID_ARGUMENT
     assert b"no interior" in L.gpf_last_error()
+
+
+def test_fp32_envelope_per_degree():
+    """The AUTO precision envelope (dropin.cpp fp32_h_limit, calibrated by
+    tools/h32_calibrate_n.py): 7.0 at the default degree, smaller at low and odd
+    degrees where the reference's truncated series cancels sooner, the smaller
+    neighbour for unsampled degrees, 0 where the fp32 kernels do not run."""
+    import paper_1505_00077_b200 as g
+    assert g.fp32_h_limit() == 7.0 == g.fp32_h_limit(20)
+    sampled = {0: 3.5, 1: 1.5, 2: 4.0, 3: 2.5, 5: 3.5, 8: 6.0, 10: 7.0, 12: 7.0, 15: 5.0,
+               25: 6.0, 30: 8.0, 40: 8.0, 48: 10.0}
+    for n, lim in sampled.items():
+        assert g.fp32_h_limit(n) == lim, n
+    assert g.fp32_h_limit(4) == 2.5 and g.fp32_h_limit(19) == 5.0 and g.fp32_h_limit(21) == 6.0
+    assert g.fp32_h_limit(-1) == 0.0 and g.fp32_h_limit(49) == 0.0
