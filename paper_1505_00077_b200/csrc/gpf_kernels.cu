@@ -501,6 +501,9 @@ __global__ void __launch_bounds__(32 * kColGroup, GPF_COL_CTAS) k_colpass_tma(
 #ifdef GPF_DIAG_EXTRA_VW
     , const __grid_constant__ CUtensorMap vstore_x
 #endif
+#ifdef GPF_DIAG_V_ONCE  // diagnostic: V stored on a plan's first call only (valid while it keeps its frame)
+    , int vst
+#endif
     ) {
   extern __shared__ float4 smem4[];
   __shared__ uint64_t em_full[kColEmBufs];
@@ -699,7 +702,12 @@ __global__ void __launch_bounds__(32 * kColGroup, GPF_COL_CTAS) k_colpass_tma(
     fence_proxy_async();  // stage writes -> visible to the TMA store
     __syncthreads();
 #ifndef GPF_DIAG_NO_STORE
-    if (tid == 0) {  // pairs past the last one fall outside the tensor and are clipped
+#ifdef GPF_DIAG_V_ONCE
+    if (tid == 0 && vst) {
+#else
+    if (tid == 0) {
+#endif
+      // pairs past the last one fall outside the tensor and are clipped
       if constexpr (GPF_L2HINT & 1) tma_store_5d_hint(&vstore, 0, x0, y0 >> 4, pair0, f, stage, l2_evict_first());
       else tma_store_5d(&vstore, 0, x0, y0 >> 4, pair0, f, stage);
 #ifdef GPF_DIAG_EXTRA_VW  // diagnostic: the chunk is stored a second time, to a scratch copy of V
@@ -1484,6 +1492,14 @@ void plan_free(Plan& plan) {
 #endif
 
 // G-scaled planes on the TMA column pass + k_rowpass2 path
+#ifdef GPF_DIAG_V_ONCE
+static int vonce_first(const void* v) {  // 1 on the first call of a plan (its V buffer)
+  static std::vector<const void*> seen;
+  if (std::find(seen.begin(), seen.end(), v) != seen.end()) return 0;
+  seen.push_back(v);
+  return 1;
+}
+#endif
 static bool plan_gscale(const Plan& plan) { return GPF_GSCALE && plan.rc.pairs <= kGsPairs; }
 
 template <int MAXT, typename Tin, typename Tout>
@@ -1565,6 +1581,9 @@ static void launch_passes(Plan& plan, const Tin* d_in, Tout* d_out, int count,
         plan.vstore
 #ifdef GPF_DIAG_EXTRA_VW
         , plan.vmap8
+#endif
+#ifdef GPF_DIAG_V_ONCE
+        , vonce_first(plan.V)
 #endif
         );
   }
