@@ -442,11 +442,34 @@ def dropin_leg(frames, sigmas, cfg, steps) -> dict:
             dev_ms += ms
     sec = (time.perf_counter() - t0) / steps
     px = sum(f.size for f in frames)
+
+    # the same calls from one host thread per frame (a serving process with
+    # several callers): the engine pipelines one call's upload and another's
+    # download against the kernels of a third (dropin.cpp call slots)
+    def worker(i, n):
+        for _ in range(n):
+            call(i)
+    import threading
+    ths = [threading.Thread(target=worker, args=(i, 1)) for i in range(len(frames))]
+    for t in ths:
+        t.start()
+    for t in ths:
+        t.join()
+    t0 = time.perf_counter()
+    ths = [threading.Thread(target=worker, args=(i, steps)) for i in range(len(frames))]
+    for t in ths:
+        t.start()
+    for t in ths:
+        t.join()
+    csec = (time.perf_counter() - t0) / steps
     return {"value": round(px / sec / 1e6, 1), "unit": UNIT, "ms_per_step": round(sec * 1e3, 2),
             "device_ms_per_step": round(dev_ms / steps, 3), "precision": sorted(precs),
             "h2d_bytes_per_step": px * 8, "d2h_bytes_per_step": px * 8 + 8 * len(frames),
             "api": "gpf_filter_gpf (reference C ABI): fp64 host image in, new fp64 host image out, "
-                   f"one call per frame, {len(frames)} frames per step, AUTO precision"}
+                   f"one call per frame, {len(frames)} frames per step, AUTO precision",
+            "concurrent": {"value": round(px / csec / 1e6, 1), "unit": UNIT,
+                           "ms_per_step": round(csec * 1e3, 2), "host_threads": len(frames),
+                           "what": "the same calls, one host thread per frame calling concurrently"}}
 
 
 def fp64_leg(steps) -> dict:
@@ -629,6 +652,7 @@ def bench_b200(args):
         dsteps = max(1, min(args.steps, 3))
         dropin = dropin_leg(frames, sigmas, cfg, dsteps)
         dropin["value"] = round(job.sum(dropin["value"]), 1)
+        dropin["concurrent"]["value"] = round(job.sum(dropin["concurrent"]["value"]), 1)
         if rank == 0 and world == 1 and not args.size:
             fp64 = fp64_leg(max(1, min(args.steps, 3)))
         gpf.dropin_release()

@@ -8,11 +8,16 @@
 //     parameter -- a C3 sigma_s sweep keeps all five plans -- (a repeated call
 //     with the same shape and parameters performs no cudaMalloc and no
 //     tensor-map encode),
-//   * the fp64 precision mode's workspace, device in/out buffers, the fallback
-//     counter, a pinned scalar readback slot and a non-blocking stream.
-// Calls on one device are serialised by the context's mutex (each call fills
-// the GPU on its own); the host images of the C ABI are page-locked
-// (capi.cpp), so the copies run at PCIe speed.
+//   * the fp64 precision mode's workspace, a compute stream and one FIFO copy
+//     stream per direction,
+//   * up to max_slots() call slots (device in/out buffers, the fallback counter, the
+//     call's events), one per call in flight.
+// Concurrent callers pipeline: a call uploads its frame on the H2D FIFO while
+// the previous call computes, and downloads on the D2H FIFO while the next one
+// computes. The filter kernels of all calls run in order on the one compute
+// stream (each fills the GPU), so plans and the fp64 workspace are shared
+// without copies; the launch mutex covers only the launches. The host images
+// of the C ABI are page-locked (capi.cpp), so the copies run at PCIe speed.
 //
 // Precision: the fp32 plane kernels follow the reference within
 // 1e-3 inside a validated envelope of max |H| = max(f_max - t_c, t_c - f_min)
@@ -22,6 +27,7 @@
 // on the device first and picks the fp64 replay outside the envelope.
 #include <algorithm>
 #include <atomic>
+#include <condition_variable>
 #include <cmath>
 #include <cstdlib>
 #include <cstring>
@@ -101,31 +107,59 @@ bool same_params(const Params& a, const Params& b) {
          a.centering == b.centering && (a.centering != 2 || a.tc_fixed == b.tc_fixed);
 }
 
-struct DevCtx {
-  std::mutex mu;
-  int device = 0;
-  std::list<std::unique_ptr<Plan>> plans;  // most recently used first
-  F64Work f64;
+// One call in flight: its device buffers and events (the D2H FIFO is shared,
+// so a call waits on its own ev_done, never on the stream).
+struct Slot {
   double* din = nullptr;
   double* dout = nullptr;
   size_t cap = 0;  // pixels
   unsigned long long* dfb = nullptr;
-  double* dscal = nullptr;  // [4] scalars + [4 * kStatBlocks] partials
-  double* hscal = nullptr;  // pinned: t_c, max|H|, -, fallbacks
-  cudaStream_t st = nullptr;
-  cudaStream_t st_out = nullptr;             // D2H of finished row ranges
-  cudaEvent_t ev0 = nullptr, ev1 = nullptr;  // brackets the filter kernels of a call
+  unsigned long long* hfb = nullptr;  // pinned fallback readback
+  cudaEvent_t ev_in = nullptr;        // the frame is on the device
+  cudaEvent_t ev0 = nullptr, ev1 = nullptr;  // bracket the filter kernels
+  cudaEvent_t ev_done = nullptr;      // the result and fallback count are on the host
   cudaEvent_t range_ev[Plan::kMaxRanges] = {};
+
+  void free_buffers() {
+    cudaFree(din);
+    cudaFree(dout);
+    din = dout = nullptr;
+    cap = 0;
+  }
+};
+
+// calls in flight per device (uploading, computing, downloading, waiting);
+// GPF_B200_DROPIN_SLOTS overrides (1 serialises the calls)
+int max_slots() {
+  static const int n = [] {
+    const char* e = std::getenv("GPF_B200_DROPIN_SLOTS");
+    const int v = e ? std::atoi(e) : 0;
+    return v > 0 ? std::min(v, 16) : 4;
+  }();
+  return n;
+}
+
+struct DevCtx {
+  std::mutex mu;  // launches on the compute stream, plans, fp64 workspace, slot buffers
+  int device = 0;
+  std::list<std::unique_ptr<Plan>> plans;  // most recently used first
+  F64Work f64;
+  double* dscal = nullptr;  // [4] scalars + [4 * kStatBlocks] partials (AUTO statistics)
+  double* hscal = nullptr;  // pinned: t_c, max|H|
+  cudaStream_t st = nullptr;      // compute (every call's kernels, in call order)
+  cudaStream_t st_in = nullptr;   // H2D FIFO
+  cudaStream_t st_out = nullptr;  // D2H FIFO
+  std::mutex slot_mu;
+  std::condition_variable slot_cv;
+  std::vector<Slot*> slots;       // all created slots
+  std::vector<Slot*> free_slots;  // most recently released last
 
   void free_plans() {
     for (auto& p : plans) plan_free(*p);
     plans.clear();
   }
   void free_buffers() {
-    cudaFree(din);
-    cudaFree(dout);
-    din = dout = nullptr;
-    cap = 0;
+    for (Slot* sl : slots) sl->free_buffers();
   }
   void release_all() {
     free_plans();
@@ -206,6 +240,44 @@ Plan& cached_plan(DevCtx& c, const Params& p) {
   return *c.plans.front();
 }
 
+Slot& acquire_slot(DevCtx& c) {
+  std::unique_lock<std::mutex> lock(c.slot_mu);
+  if (c.free_slots.empty() && (int)c.slots.size() < max_slots()) {
+    auto* sl = new Slot();  // lives as long as the context
+    chk(cudaMalloc(&sl->dfb, sizeof(unsigned long long)), "cudaMalloc");
+    chk(cudaMallocHost(&sl->hfb, sizeof(unsigned long long)), "cudaMallocHost");
+    chk(cudaEventCreateWithFlags(&sl->ev_in, cudaEventDisableTiming), "cudaEventCreate");
+    chk(cudaEventCreate(&sl->ev0), "cudaEventCreate");
+    chk(cudaEventCreate(&sl->ev1), "cudaEventCreate");
+    chk(cudaEventCreateWithFlags(&sl->ev_done, cudaEventDisableTiming), "cudaEventCreate");
+    for (auto& e : sl->range_ev) chk(cudaEventCreateWithFlags(&e, cudaEventDisableTiming), "cudaEventCreate");
+    c.slots.push_back(sl);
+    c.free_slots.push_back(sl);
+  }
+  c.slot_cv.wait(lock, [&] { return !c.free_slots.empty(); });
+  Slot* sl = c.free_slots.back();
+  c.free_slots.pop_back();
+  return *sl;
+}
+
+struct SlotGuard {  // returns the slot when the call ends (normally or by an exception)
+  DevCtx& c;
+  Slot& s;
+  bool done = false;  // the call recorded and waited on its ev_done
+  ~SlotGuard() {
+    if (!done) {  // a failed call: nothing it queued may still use the slot's buffers
+      if (c.st) cudaStreamSynchronize(c.st);
+      if (c.st_in) cudaStreamSynchronize(c.st_in);
+      if (c.st_out) cudaStreamSynchronize(c.st_out);
+    }
+    {
+      std::lock_guard<std::mutex> lock(c.slot_mu);
+      c.free_slots.push_back(&s);
+    }
+    c.slot_cv.notify_one();
+  }
+};
+
 }  // namespace
 
 void set_precision(int mode) { g_precision.store(mode); }
@@ -227,105 +299,115 @@ float last_device_ms() { return t_last_device_ms; }
 long long dropin_gpf(const double* h_in, double* h_out, const Params& p) {
   const int dev = current_device();
   DevCtx& c = context(dev);
-  std::lock_guard<std::mutex> lock(c.mu);
   const long long n = (long long)p.width * p.height;
-  if (!c.st) {
-    chk(cudaStreamCreateWithFlags(&c.st, cudaStreamNonBlocking), "cudaStreamCreate");
-    chk(cudaMalloc(&c.dfb, sizeof(unsigned long long)), "cudaMalloc");
-    chk(cudaMalloc(&c.dscal, sizeof(double) * (4 + 4 * kStatBlocks)), "cudaMalloc");
-    chk(cudaMallocHost(&c.hscal, sizeof(double) * 4), "cudaMallocHost");
-    chk(cudaEventCreate(&c.ev0), "cudaEventCreate");
-    chk(cudaEventCreate(&c.ev1), "cudaEventCreate");
-    chk(cudaStreamCreateWithFlags(&c.st_out, cudaStreamNonBlocking), "cudaStreamCreate");
-    for (auto& e : c.range_ev) chk(cudaEventCreateWithFlags(&e, cudaEventDisableTiming), "cudaEventCreate");
-  }
-  if ((size_t)n > c.cap) {
-    c.free_buffers();
-    with_retry(c, [&] {
-      c.free_buffers();
-      chk(cudaMalloc(&c.din, sizeof(double) * n), "cudaMalloc(input)");
-      chk(cudaMalloc(&c.dout, sizeof(double) * n), "cudaMalloc(output)");
-      c.cap = (size_t)n;
-    });
-  }
   int mode = get_precision();
-  double hmax = 0.0;
   if (mode == kPrecFp32 && p.degree > kMaxDegreeF32)
     throw Error{1, "RangeParams: degree must be <= " + std::to_string(kMaxDegreeF32) +
                        " with the fp32 precision mode"};
-  chk(cudaMemcpyAsync(c.din, h_in, sizeof(double) * n, cudaMemcpyHostToDevice, c.st), "H2D");
-  if (mode == kPrecAuto) {
-    if (p.degree > kMaxDegreeF32) {
-      mode = kPrecFp64;
-    } else {
-      double* partials = c.dscal + 4;
-      launch_mean_f64(c.din, n, p.centering, p.tc_fixed, p.sigma_r, partials, kStatBlocks, c.dscal,
-                      c.st);
-      chk(cudaMemcpyAsync(c.hscal, c.dscal, sizeof(double) * 2, cudaMemcpyDeviceToHost, c.st), "D2H");
-      chk(cudaStreamSynchronize(c.st), "cudaStreamSynchronize");
-      hmax = c.hscal[1];
-      mode = (hmax > fp32_h_limit(p.degree) || std::isnan(hmax)) ? kPrecFp64 : kPrecFp32;
+  {
+    std::lock_guard<std::mutex> lock(c.mu);
+    if (!c.st) {
+      chk(cudaStreamCreateWithFlags(&c.st, cudaStreamNonBlocking), "cudaStreamCreate");
+      chk(cudaStreamCreateWithFlags(&c.st_in, cudaStreamNonBlocking), "cudaStreamCreate");
+      chk(cudaStreamCreateWithFlags(&c.st_out, cudaStreamNonBlocking), "cudaStreamCreate");
+      chk(cudaMalloc(&c.dscal, sizeof(double) * (4 + 4 * kStatBlocks)), "cudaMalloc");
+      chk(cudaMallocHost(&c.hscal, sizeof(double) * 4), "cudaMallocHost");
     }
   }
-  chk(cudaMemsetAsync(c.dfb, 0, sizeof(unsigned long long), c.st), "cudaMemsetAsync");
+  Slot& s = acquire_slot(c);
+  SlotGuard guard{c, s};
+  if ((size_t)n > s.cap) {
+    std::lock_guard<std::mutex> lock(c.mu);
+    s.free_buffers();
+    with_retry(c, [&] {
+      s.free_buffers();
+      chk(cudaMalloc(&s.din, sizeof(double) * n), "cudaMalloc(input)");
+      chk(cudaMalloc(&s.dout, sizeof(double) * n), "cudaMalloc(output)");
+      s.cap = (size_t)n;
+    });
+  }
+  // upload on the H2D FIFO: overlaps the kernels of the call before this one
+  chk(cudaMemcpyAsync(s.din, h_in, sizeof(double) * n, cudaMemcpyHostToDevice, c.st_in), "H2D");
+  chk(cudaEventRecord(s.ev_in, c.st_in), "cudaEventRecord");
+  double hmax = 0.0;
   int ranges = 1, range_rows = 16;
   bool pixel_ranges = false;  // fp64 mode: ranges of pixels rather than of row bands
-  if (mode == kPrecFp64) {
-    with_retry(c, [&] { c.f64.ensure(f64_workspace_bytes(p.width, p.height, p.degree)); });
-    chk(cudaEventRecord(c.ev0, c.st), "cudaEventRecord");
-    const bool split = n >= kSplitPixels;
-    run_gpf_f64_exact(c.din, c.dout, p, c.f64, c.dfb, c.st, split ? kRanges : 1, c.range_ev);
-    if (split) {
-      ranges = kRanges;
-      pixel_ranges = true;
-    }
-  } else {
-    Plan& pl = cached_plan(c, p);
-    chk(cudaEventRecord(c.ev0, c.st), "cudaEventRecord");
-    // large frames: the row pass goes out in kRanges band ranges and each
-    // range's rows start their D2H as soon as it is done
-    if (n >= kSplitPixels) {
-      pl.row_ranges = kRanges;
-      for (int i = 0; i < kRanges; ++i) pl.range_done[i] = c.range_ev[i];
-    }
-    struct Restore {  // the cached plan keeps no per-call state
-      Plan& q;
-      ~Restore() { q.row_ranges = 1; }
-    } restore{pl};
-    run_frames_f64(pl, c.din, c.dout, 1, c.dfb, c.st);
-    ranges = pl.ranges_launched;
-    range_rows = pl.range_rows;
-  }
-  chk(cudaEventRecord(c.ev1, c.st), "cudaEventRecord");
-  if (ranges > 1) {
-    const int nbands = (p.height + range_rows - 1) / range_rows;
-    for (int i = 0; i < ranges; ++i) {
-      long long e0, e1;  // element range of range i
-      if (pixel_ranges) {
-        e0 = n * i / ranges;
-        e1 = n * (i + 1) / ranges;
+  {
+    std::lock_guard<std::mutex> lock(c.mu);
+    chk(cudaStreamWaitEvent(c.st, s.ev_in, 0), "cudaStreamWaitEvent");
+    if (mode == kPrecAuto) {
+      if (p.degree > kMaxDegreeF32) {
+        mode = kPrecFp64;
       } else {
-        e0 = (long long)(nbands * (long long)i / ranges) * range_rows * p.width;
-        e1 = std::min<long long>((nbands * (long long)(i + 1) / ranges) * range_rows, p.height) * p.width;
+        double* partials = c.dscal + 4;
+        launch_mean_f64(s.din, n, p.centering, p.tc_fixed, p.sigma_r, partials, kStatBlocks, c.dscal,
+                        c.st);
+        chk(cudaMemcpyAsync(c.hscal, c.dscal, sizeof(double) * 2, cudaMemcpyDeviceToHost, c.st), "D2H");
+        chk(cudaStreamSynchronize(c.st), "cudaStreamSynchronize");
+        hmax = c.hscal[1];
+        mode = (hmax > fp32_h_limit(p.degree) || std::isnan(hmax)) ? kPrecFp64 : kPrecFp32;
       }
-      chk(cudaStreamWaitEvent(c.st_out, c.range_ev[i], 0), "cudaStreamWaitEvent");
-      chk(cudaMemcpyAsync(h_out + e0, c.dout + e0, sizeof(double) * (e1 - e0), cudaMemcpyDeviceToHost,
-                          c.st_out),
-          "D2H");
     }
-  } else {
-    chk(cudaMemcpyAsync(h_out, c.dout, sizeof(double) * n, cudaMemcpyDeviceToHost, c.st), "D2H");
+    chk(cudaMemsetAsync(s.dfb, 0, sizeof(unsigned long long), c.st), "cudaMemsetAsync");
+    if (mode == kPrecFp64) {
+      if (f64_workspace_bytes(p.width, p.height, p.degree) > c.f64.cap)
+        chk(cudaStreamSynchronize(c.st), "cudaStreamSynchronize");  // earlier calls may use it
+      with_retry(c, [&] { c.f64.ensure(f64_workspace_bytes(p.width, p.height, p.degree)); });
+      chk(cudaEventRecord(s.ev0, c.st), "cudaEventRecord");
+      const bool split = n >= kSplitPixels;
+      run_gpf_f64_exact(s.din, s.dout, p, c.f64, s.dfb, c.st, split ? kRanges : 1, s.range_ev);
+      if (split) {
+        ranges = kRanges;
+        pixel_ranges = true;
+      }
+    } else {
+      Plan& pl = cached_plan(c, p);
+      chk(cudaEventRecord(s.ev0, c.st), "cudaEventRecord");
+      // large frames: the row pass goes out in kRanges band ranges and each
+      // range's rows start their D2H as soon as it is done
+      if (n >= kSplitPixels) {
+        pl.row_ranges = kRanges;
+        for (int i = 0; i < kRanges; ++i) pl.range_done[i] = s.range_ev[i];
+      }
+      struct Restore {  // the cached plan keeps no per-call state
+        Plan& q;
+        ~Restore() { q.row_ranges = 1; }
+      } restore{pl};
+      run_frames_f64(pl, s.din, s.dout, 1, s.dfb, c.st);
+      ranges = pl.ranges_launched;
+      range_rows = pl.range_rows;
+    }
+    chk(cudaEventRecord(s.ev1, c.st), "cudaEventRecord");
+    // downloads on the D2H FIFO, queued in call order while the launch order is held
+    if (ranges > 1) {
+      const int nbands = (p.height + range_rows - 1) / range_rows;
+      for (int i = 0; i < ranges; ++i) {
+        long long e0, e1;  // element range of range i
+        if (pixel_ranges) {
+          e0 = n * i / ranges;
+          e1 = n * (i + 1) / ranges;
+        } else {
+          e0 = (long long)(nbands * (long long)i / ranges) * range_rows * p.width;
+          e1 = std::min<long long>((nbands * (long long)(i + 1) / ranges) * range_rows, p.height) * p.width;
+        }
+        chk(cudaStreamWaitEvent(c.st_out, s.range_ev[i], 0), "cudaStreamWaitEvent");
+        chk(cudaMemcpyAsync(h_out + e0, s.dout + e0, sizeof(double) * (e1 - e0), cudaMemcpyDeviceToHost,
+                            c.st_out),
+            "D2H");
+      }
+    }
+    chk(cudaStreamWaitEvent(c.st_out, s.ev1, 0), "cudaStreamWaitEvent");
+    if (ranges <= 1)
+      chk(cudaMemcpyAsync(h_out, s.dout, sizeof(double) * n, cudaMemcpyDeviceToHost, c.st_out), "D2H");
+    chk(cudaMemcpyAsync(s.hfb, s.dfb, sizeof(unsigned long long), cudaMemcpyDeviceToHost, c.st_out), "D2H");
+    chk(cudaEventRecord(s.ev_done, c.st_out), "cudaEventRecord");
   }
-  chk(cudaMemcpyAsync(c.hscal + 3, c.dfb, sizeof(unsigned long long), cudaMemcpyDeviceToHost, c.st),
-      "D2H");
-  chk(cudaStreamSynchronize(c.st), "cudaStreamSynchronize");
-  chk(cudaStreamSynchronize(c.st_out), "cudaStreamSynchronize");
+  chk(cudaEventSynchronize(s.ev_done), "cudaEventSynchronize");
+  guard.done = true;
   t_last_precision = mode;
   t_last_hmax = hmax;
-  chk(cudaEventElapsedTime(&t_last_device_ms, c.ev0, c.ev1), "cudaEventElapsedTime");
-  unsigned long long fb;
-  std::memcpy(&fb, c.hscal + 3, sizeof(fb));
-  return static_cast<long long>(fb);
+  chk(cudaEventElapsedTime(&t_last_device_ms, s.ev0, s.ev1), "cudaEventElapsedTime");
+  return static_cast<long long>(*s.hfb);
 }
 
 void dropin_release() {
@@ -336,7 +418,8 @@ void dropin_release() {
     int prev = 0;
     cudaGetDevice(&prev);
     cudaSetDevice(c->device);
-    if (c->st) cudaStreamSynchronize(c->st);
+    for (cudaStream_t st : {c->st, c->st_in, c->st_out})
+      if (st) cudaStreamSynchronize(st);
     c->release_all();
     cudaSetDevice(prev);
   }

@@ -607,7 +607,7 @@ __global__ void __launch_bounds__(32 * kColGroup, GPF_COL_CTAS) k_colpass_tma(
         ps_set_gain_sweep(cs, make_float2(v0.x, v0.y), fc);
       }
       float2 pa[kTile / 2], pc[kTile / 2];
-      float4 xa[kColXreg ? kTile / 4 : 1], xc[kColXreg ? kTile / 4 : 1];  // inputs kept for the second half
+      [[maybe_unused]] float4 xa[kColXreg ? kTile / 4 : 1], xc[kColXreg ? kTile / 4 : 1];  // inputs kept for the second half
 #pragma unroll
       for (int t = 0; t < kTile / 2; t += 2) {
         const float4 va = *reinterpret_cast<const float4*>(stage_at(mcol, 30 - t, cm));

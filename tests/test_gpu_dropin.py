@@ -240,3 +240,33 @@ def test_stage_timing_and_timeline(gpu):
     finally:
         plan.set_profiling(False)
         plan.close()
+
+
+@pytest.mark.gpu
+def test_dropin_concurrent_large_frames_pipeline(gpu):
+    """Concurrent calls on >= 4 MP frames (the band/pixel-range D2H path of the
+    call slots), fp32 and fp64 modes mixed: every thread's result is bitwise its
+    sequential one, fallback counts included."""
+    import threading
+    cases = [(synth.rects_image(2048, 2048, 64, 15.0, 700 + k).astype(np.float64), 5.0 + k,
+              30.0 if k % 2 == 0 else 10.0) for k in range(4)]
+    seq = [gpu.gpf_filter_gpf(img, gpu.spatial_params(ss), gpu.range_params(sr)) for img, ss, sr in cases]
+    got = [None] * len(cases)
+    errs = []
+
+    def work(i):
+        try:
+            img, ss, sr = cases[i]
+            for _ in range(2):
+                got[i] = gpu.gpf_filter_gpf(img, gpu.spatial_params(ss), gpu.range_params(sr))
+        except Exception as e:  # surfaced below
+            errs.append(e)
+    ths = [threading.Thread(target=work, args=(i,)) for i in range(len(cases))]
+    for t in ths:
+        t.start()
+    for t in ths:
+        t.join()
+    assert not errs, errs
+    for (a, fa), (b, fb) in zip(seq, got):
+        assert fa == fb
+        np.testing.assert_array_equal(a, b)
