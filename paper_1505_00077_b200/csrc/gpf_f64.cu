@@ -28,6 +28,7 @@
 // HBM per frame (doubles): H, F_0 [w h]; R [planes][w h] row-pass output;
 // C [planes][w h] column-pass output (the filtered planes Fbar_n).
 #include <algorithm>
+#include <cstdlib>
 #include <string>
 
 #include <cuda_runtime.h>
@@ -268,6 +269,401 @@ __global__ void __launch_bounds__(128) k_f64_cols(const double* __restrict__ R, 
   }
 }
 
+// ----------------------------------------------------------------------------
+// Chunked form of the same two passes (the default). The reference's line
+// filter runs the causal recurrence over the whole line, then the anticausal
+// one adding into it; replayed literally (k_f64_rows / k_f64_cols above) that
+// is a read-modify-write of every plane per axis. Here a line is cut into
+// chunks of kF64Chunk samples:
+//   states kernel : the anticausal recurrence alone, walked from the far end
+//                   of the line; its register state (x[i+1..i+4], y-[i+1..i+4])
+//                   is recorded where it enters each chunk.
+//   chunk kernel  : walks the chunks in causal order; per chunk the causal
+//                   recurrence (state carried in registers), then the
+//                   anticausal one restarted from the recorded state, summed
+//                   and written once.
+// Every output is produced by the same operations on the same operands in the
+// same order as in the sequential form, so the two are bitwise equal
+// (tests/test_gpu_dropin.py compares them); the planes cross HBM once per
+// axis instead of being re-read and re-written.
+// ----------------------------------------------------------------------------
+constexpr int kF64Chunk = 32;  // samples per chunk on both axes
+constexpr int kRB2 = 8;        // rows per CTA of the chunked row pass
+constexpr int kTP = kF64Chunk + 1;  // padded tile pitch (doubles)
+constexpr int kYP = kRB2 * kTP + 4;  // Y plane stride: consecutive plane pairs 8 doubles apart in the bank space
+
+__device__ __forceinline__ void cp8(double* smem, const double* gmem) {
+  const unsigned sa = static_cast<unsigned>(__cvta_generic_to_shared(smem));
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(sa), "l"(gmem));
+}
+
+// Chunked row pass, shared by its two kernels. A CTA owns kRB2 rows and ALL
+// planes: thread = (row, plane pair), so a chunk's (H, F_0) tile is loaded once
+// for every plane and the even planes F_2g = H (H F_{2g-2}) are formed once per
+// pixel by the reference's multiply chain (X2), the odd ones as H F_2g by their
+// owner. Shared memory (doubles): sH, sF [kRB2][kTP]; X2 [pg][kRB2][kTP];
+// Y [planes][kRB2][kTP] (chunk kernel only).
+struct RowCtx {
+  double *sH, *sF, *X2;
+  int tid, nthr, row, pg, PG, rows, y0;
+};
+
+// Chunk pipeline: while a chunk's recurrences run, the next chunk's F_0 tile
+// streams into sF by cp.async (sF is free once the even planes are formed) and
+// its H values wait in registers (sH is still being read); rows_finish_load
+// lands both. kHR H values per thread cover the tile for CTAs of >= 64 threads.
+constexpr int kHR = 4;
+struct RowPrefetch {
+  double hreg[kHR];
+};
+__device__ __forceinline__ void rows_issue_load(const RowCtx& c, RowPrefetch& pf,
+                                                const double* __restrict__ H,
+                                                const double* __restrict__ F0, int w, int x0, int cols) {
+#pragma unroll
+  for (int q = 0; q < kHR; ++q) {
+    const int e = c.tid + q * c.nthr;
+    const int r = e / kF64Chunk, j = e % kF64Chunk;
+    if (e < kRB2 * kF64Chunk && r < c.rows && j < cols) {
+      const size_t g = (size_t)(c.y0 + r) * w + x0 + j;
+      pf.hreg[q] = __ldg(H + g);
+      cp8(&c.sF[r * kTP + j], F0 + g);
+    }
+  }
+  asm volatile("cp.async.commit_group;\n" ::);
+}
+// lands the issued chunk in sH / sF and forms the even planes of its pixels
+__device__ __forceinline__ void rows_finish_load(const RowCtx& c, const RowPrefetch& pf, int cols) {
+#pragma unroll
+  for (int q = 0; q < kHR; ++q) {
+    const int e = c.tid + q * c.nthr;
+    const int r = e / kF64Chunk, j = e % kF64Chunk;
+    if (e < kRB2 * kF64Chunk && r < c.rows && j < cols) c.sH[r * kTP + j] = pf.hreg[q];
+  }
+  asm volatile("cp.async.wait_group 0;\n" ::: "memory");
+  __syncthreads();
+  // even planes of every pixel of the chunk, four pixels' chains interleaved
+  constexpr int kE = 4;
+  for (int e0 = c.tid; e0 < kRB2 * kF64Chunk; e0 += c.nthr * kE) {
+    double hv[kE], v[kE];
+    int off[kE];
+    bool ok[kE];
+#pragma unroll
+    for (int q = 0; q < kE; ++q) {
+      const int e = e0 + q * c.nthr;
+      const int r = e / kF64Chunk, j = e % kF64Chunk;
+      ok[q] = e < kRB2 * kF64Chunk && r < c.rows && j < cols;
+      off[q] = ok[q] ? r * kTP + j : 0;
+      hv[q] = c.sH[off[q]];
+      v[q] = c.sF[off[q]];
+      if (ok[q]) c.X2[off[q]] = v[q];
+    }
+    for (int g = 1; g < c.PG; ++g) {
+#pragma unroll
+      for (int q = 0; q < kE; ++q) {
+        v[q] = m_(hv[q], m_(hv[q], v[q]));
+        if (ok[q]) c.X2[g * kRB2 * kTP + off[q]] = v[q];
+      }
+    }
+  }
+  __syncthreads();
+}
+
+// this thread's plane pair at column j of the chunk: (F_2pg, F_2pg+1); xe / hr
+// are the thread's rows of X2 and sH (immediate offsets in the unrolled loops)
+__device__ __forceinline__ void rows_x(const double* xe, const double* hr, int j, double (&x)[kGP]) {
+  x[0] = xe[j];
+  x[1] = m_(hr[j], x[0]);
+}
+
+struct Anti64 {  // anticausal register state of one line
+  double xp1, xp2, xp3, xp4, yp1, yp2, yp3, yp4;
+};
+__device__ __forceinline__ void anti_warm(Anti64& a, double xl, const Deriche64& k) {
+  const double ss = __ddiv_rn(m_(xl, k.asum), k.den);
+  a.xp1 = a.xp2 = a.xp3 = a.xp4 = xl;
+  a.yp1 = a.yp2 = a.yp3 = a.yp4 = ss;
+}
+__device__ __forceinline__ double anti_step(Anti64& a, double xi, const Deriche64& k) {
+  const double yi = deriche_step(k.na, k.d, a.xp1, a.xp2, a.xp3, a.xp4, a.yp1, a.yp2, a.yp3, a.yp4);
+  a.xp4 = a.xp3; a.xp3 = a.xp2; a.xp2 = a.xp1; a.xp1 = xi;
+  a.yp4 = a.yp3; a.yp3 = a.yp2; a.yp2 = a.yp1; a.yp1 = yi;
+  return yi;
+}
+struct Caus64 {
+  double xm1, xm2, xm3, ym1, ym2, ym3, ym4;
+};
+__device__ __forceinline__ void caus_warm(Caus64& s, double x0, const Deriche64& k) {
+  const double ss = __ddiv_rn(m_(x0, k.csum), k.den);
+  s.xm1 = s.xm2 = s.xm3 = x0;
+  s.ym1 = s.ym2 = s.ym3 = s.ym4 = ss;
+}
+__device__ __forceinline__ double caus_step(Caus64& s, double xi, const Deriche64& k) {
+  const double yi = deriche_step(k.nc, k.d, xi, s.xm1, s.xm2, s.xm3, s.ym1, s.ym2, s.ym3, s.ym4);
+  s.xm3 = s.xm2; s.xm2 = s.xm1; s.xm1 = xi;
+  s.ym4 = s.ym3; s.ym3 = s.ym2; s.ym2 = s.ym1; s.ym1 = yi;
+  return yi;
+}
+// recorded states: component k of line `line` at p[k * stride]
+__device__ __forceinline__ void anti_store(const Anti64& a, double* p, size_t stride) {
+  p[0] = a.xp1; p[stride] = a.xp2; p[2 * stride] = a.xp3; p[3 * stride] = a.xp4;
+  p[4 * stride] = a.yp1; p[5 * stride] = a.yp2; p[6 * stride] = a.yp3; p[7 * stride] = a.yp4;
+}
+__device__ __forceinline__ void anti_load(Anti64& a, const double* p, size_t stride) {
+  a.xp1 = p[0]; a.xp2 = p[stride]; a.xp3 = p[2 * stride]; a.xp4 = p[3 * stride];
+  a.yp1 = p[4 * stride]; a.yp2 = p[5 * stride]; a.yp3 = p[6 * stride]; a.yp4 = p[7 * stride];
+}
+
+__device__ __forceinline__ RowCtx rows_ctx(double* smem, int h, int planes) {
+  RowCtx c;
+  c.sH = smem;
+  c.sF = smem + kRB2 * kTP;
+  c.X2 = smem + 2 * kRB2 * kTP;
+  c.tid = threadIdx.x;
+  c.nthr = blockDim.x;
+  c.row = c.tid % kRB2;
+  c.pg = c.tid / kRB2;
+  c.PG = (planes + kGP - 1) / kGP;
+  c.y0 = blockIdx.x * kRB2;
+  c.rows = min(kRB2, h - c.y0);
+  return c;
+}
+
+// S layout (row pass): [band][chunk][8 components][planes][kRB2 rows]
+__global__ void k_f64_rows_states(const double* __restrict__ H, const double* __restrict__ F0,
+                                  double* __restrict__ S, int w, int h, int planes, Deriche64 k) {
+  extern __shared__ double smem_d[];
+  const RowCtx c = rows_ctx(smem_d, h, planes);
+  const int nc = (w + kF64Chunk - 1) / kF64Chunk;
+  const bool live = c.pg < c.PG && c.row < c.rows;
+  const size_t comp = (size_t)planes * kRB2;
+  const double* xe = c.X2 + (c.pg < c.PG ? c.pg : 0) * kRB2 * kTP + c.row * kTP;
+  const double* hr = c.sH + c.row * kTP;
+  Anti64 a[kGP];
+  double x[kGP];
+  RowPrefetch pf;
+  if (nc > 1) rows_issue_load(c, pf, H, F0, w, (nc - 1) * kF64Chunk, w - (nc - 1) * kF64Chunk);
+  for (int ch = nc - 1; ch >= 1; --ch) {  // chunk 0's walk would record nothing
+    const int x0 = ch * kF64Chunk, cols = min(kF64Chunk, w - x0);
+    rows_finish_load(c, pf, cols);
+    if (ch > 1) rows_issue_load(c, pf, H, F0, w, x0 - kF64Chunk, kF64Chunk);
+    if (live) {
+      if (ch == nc - 1) {
+        rows_x(xe, hr, cols - 1, x);
+#pragma unroll
+        for (int p = 0; p < kGP; ++p) anti_warm(a[p], x[p], k);
+      }
+      if (cols == kF64Chunk) {  // full chunk: unrolled, the state rotation renames registers
+#pragma unroll 8
+        for (int j = kF64Chunk - 1; j >= 0; --j) {
+          rows_x(xe, hr, j, x);
+#pragma unroll
+          for (int p = 0; p < kGP; ++p) anti_step(a[p], x[p], k);
+        }
+      } else {
+        for (int j = cols - 1; j >= 0; --j) {
+          rows_x(xe, hr, j, x);
+#pragma unroll
+          for (int p = 0; p < kGP; ++p) anti_step(a[p], x[p], k);
+        }
+      }
+      double* dst = S + ((size_t)blockIdx.x * nc + (ch - 1)) * 8 * comp + c.row;
+#pragma unroll
+      for (int p = 0; p < kGP; ++p)
+        if (c.pg * kGP + p < planes) anti_store(a[p], dst + (size_t)(c.pg * kGP + p) * kRB2, comp);
+    }
+    __syncthreads();  // sH and X2 are free again
+  }
+}
+
+__global__ void k_f64_rows_chunked(const double* __restrict__ H, const double* __restrict__ F0,
+                                   const double* __restrict__ S, double* __restrict__ R, int w, int h,
+                                   int planes, Deriche64 k) {
+  extern __shared__ double smem_d[];
+  const RowCtx c = rows_ctx(smem_d, h, planes);
+  double* Y = c.X2 + (size_t)c.PG * kRB2 * kTP;  // [planes][kRB2][kTP]
+  const int nc = (w + kF64Chunk - 1) / kF64Chunk;
+  const bool live = c.pg < c.PG && c.row < c.rows;
+  const size_t comp = (size_t)planes * kRB2, ps = (size_t)w * h;
+  const int lane = c.tid & 31, warp = c.tid >> 5, nwarp = c.nthr >> 5;
+  const double* xe = c.X2 + (c.pg < c.PG ? c.pg : 0) * kRB2 * kTP + c.row * kTP;
+  const double* hr = c.sH + c.row * kTP;
+  Caus64 cs[kGP];
+  double x[kGP];
+  RowPrefetch pf;
+  rows_issue_load(c, pf, H, F0, w, 0, min(kF64Chunk, w));
+  for (int ch = 0; ch < nc; ++ch) {
+    const int x0 = ch * kF64Chunk, cols = min(kF64Chunk, w - x0);
+    // the anticausal state entering this chunk, in flight under the even-plane chains
+    Anti64 a[kGP];
+    if (live && ch + 1 < nc) {
+      const double* src = S + ((size_t)blockIdx.x * nc + ch) * 8 * comp + c.row;
+#pragma unroll
+      for (int p = 0; p < kGP; ++p)
+        if (c.pg * kGP + p < planes) anti_load(a[p], src + (size_t)(c.pg * kGP + p) * kRB2, comp);
+    }
+    rows_finish_load(c, pf, cols);
+    if (ch + 1 < nc) rows_issue_load(c, pf, H, F0, w, x0 + kF64Chunk, min(kF64Chunk, w - x0 - kF64Chunk));
+    if (live) {
+      double* yt = Y + (size_t)(c.pg * kGP) * kYP + c.row * kTP;
+      const bool two = c.pg * kGP + 1 < planes;
+      if (ch == 0) {
+        rows_x(xe, hr, 0, x);
+#pragma unroll
+        for (int p = 0; p < kGP; ++p) caus_warm(cs[p], x[p], k);
+      }
+      if (ch + 1 == nc) {
+        rows_x(xe, hr, cols - 1, x);
+#pragma unroll
+        for (int p = 0; p < kGP; ++p) anti_warm(a[p], x[p], k);
+      }
+      if (cols == kF64Chunk && two) {  // full chunk: unrolled, the state rotations rename registers
+#pragma unroll 8
+        for (int j = 0; j < kF64Chunk; ++j) {
+          rows_x(xe, hr, j, x);
+          yt[j] = caus_step(cs[0], x[0], k);
+          yt[kYP + j] = caus_step(cs[1], x[1], k);
+        }
+#pragma unroll 8
+        for (int j = kF64Chunk - 1; j >= 0; --j) {
+          rows_x(xe, hr, j, x);
+          yt[j] = a_(yt[j], anti_step(a[0], x[0], k));
+          yt[kYP + j] = a_(yt[kYP + j], anti_step(a[1], x[1], k));
+        }
+      } else {
+        for (int j = 0; j < cols; ++j) {
+          rows_x(xe, hr, j, x);
+          yt[j] = caus_step(cs[0], x[0], k);
+          const double y1 = caus_step(cs[1], x[1], k);
+          if (two) yt[kYP + j] = y1;
+        }
+        for (int j = cols - 1; j >= 0; --j) {
+          rows_x(xe, hr, j, x);
+          yt[j] = a_(yt[j], anti_step(a[0], x[0], k));
+          const double y1 = anti_step(a[1], x[1], k);
+          if (two) yt[kYP + j] = a_(yt[kYP + j], y1);
+        }
+      }
+    }
+    __syncthreads();
+    // the chunk leaves as 256-B row segments, one (plane, row) per warp and turn
+    for (int sgm = warp; sgm < planes * kRB2; sgm += nwarp) {
+      const int n = sgm / kRB2, r = sgm % kRB2;
+      if (r < c.rows && lane < cols)
+        R[(size_t)n * ps + (size_t)(c.y0 + r) * w + x0 + lane] = Y[(size_t)n * kYP + r * kTP + lane];
+    }
+    __syncthreads();
+  }
+}
+
+size_t rows2_smem_bytes(int planes) {
+  const int PG = (planes + kGP - 1) / kGP;
+  return sizeof(double) * ((size_t)(2 + PG) * kRB2 * kTP + (size_t)planes * kYP);
+}
+
+// Chunked column pass: thread = (column, plane), coalesced across columns. A
+// thread's chunk of inputs arrives in its own shared-memory column by
+// cp.async, double-buffered: the next chunk's 32 loads are in flight while the
+// current one is filtered, and no value waits in registers. No barriers: a
+// thread only touches its own column of the tiles.
+// S layout: [plane][chunk][8 components][w].
+constexpr int kColT = 128;
+struct ColTiles {
+  double x[2][kF64Chunk][kColT];  // inputs, two chunks
+  double y[kF64Chunk][kColT];     // causal outputs of the current chunk (chunk kernel)
+};
+__device__ __forceinline__ void cols_load_chunk(double (*sx)[kColT], const double* src, int w, int y0,
+                                                int rows) {
+#pragma unroll
+  for (int j = 0; j < kF64Chunk; ++j)
+    if (j < rows) cp8(&sx[j][threadIdx.x], src + (size_t)(y0 + j) * w);
+  asm volatile("cp.async.commit_group;\n" ::);
+}
+__device__ __forceinline__ void cols_wait_chunk(bool newer_in_flight) {
+  if (newer_in_flight) asm volatile("cp.async.wait_group 1;\n" ::: "memory");
+  else asm volatile("cp.async.wait_group 0;\n" ::: "memory");
+}
+
+__global__ void __launch_bounds__(kColT) k_f64_cols_states(const double* __restrict__ R,
+                                                           double* __restrict__ S, int w, int h,
+                                                           Deriche64 k) {
+  extern __shared__ double smem_d[];
+  double(*sx)[kF64Chunk][kColT] = reinterpret_cast<double(*)[kF64Chunk][kColT]>(smem_d);
+  const int x = blockIdx.x * kColT + threadIdx.x;
+  if (x >= w) return;
+  const size_t ps = (size_t)w * h;
+  const int ncy = (h + kF64Chunk - 1) / kF64Chunk;
+  const double* src = R + (size_t)blockIdx.y * ps + x;
+  Anti64 a;
+  anti_warm(a, src[(size_t)(h - 1) * w], k);
+  cols_load_chunk(sx[(ncy - 1) & 1], src, w, (ncy - 1) * kF64Chunk, h - (ncy - 1) * kF64Chunk);
+  for (int cy = ncy - 1; cy >= 1; --cy) {  // chunk 0's walk would record nothing
+    const int rows = min(kF64Chunk, h - cy * kF64Chunk);
+    if (cy > 1) cols_load_chunk(sx[(cy - 1) & 1], src, w, (cy - 1) * kF64Chunk, kF64Chunk);
+    cols_wait_chunk(cy > 1);
+    const double* cx = &sx[cy & 1][0][threadIdx.x];
+    if (rows == kF64Chunk) {
+#pragma unroll 8
+      for (int j = kF64Chunk - 1; j >= 0; --j) anti_step(a, cx[j * kColT], k);
+    } else {
+      for (int j = rows - 1; j >= 0; --j) anti_step(a, cx[j * kColT], k);
+    }
+    anti_store(a, S + ((size_t)blockIdx.y * ncy + (cy - 1)) * 8 * w + x, w);
+  }
+}
+
+__global__ void __launch_bounds__(kColT) k_f64_cols_chunked(const double* __restrict__ R,
+                                                            const double* __restrict__ S,
+                                                            double* __restrict__ C, int w, int h,
+                                                            Deriche64 k, double scale) {
+  extern __shared__ double smem_d[];
+  ColTiles& t = *reinterpret_cast<ColTiles*>(smem_d);
+  const int x = blockIdx.x * kColT + threadIdx.x;
+  if (x >= w) return;
+  const size_t ps = (size_t)w * h;
+  const int ncy = (h + kF64Chunk - 1) / kF64Chunk;
+  const double* src = R + (size_t)blockIdx.y * ps + x;
+  double* dst = C + (size_t)blockIdx.y * ps + x;
+  Caus64 cs;
+  cols_load_chunk(t.x[0], src, w, 0, min(kF64Chunk, h));
+  for (int cy = 0; cy < ncy; ++cy) {
+    const int y0 = cy * kF64Chunk, rows = min(kF64Chunk, h - y0);
+    const bool more = cy + 1 < ncy;
+    Anti64 a;
+    if (more) {
+      cols_load_chunk(t.x[(cy + 1) & 1], src, w, y0 + kF64Chunk, min(kF64Chunk, h - y0 - kF64Chunk));
+      anti_load(a, S + ((size_t)blockIdx.y * ncy + cy) * 8 * w + x, w);
+    }
+    cols_wait_chunk(more);
+    const double* cx = &t.x[cy & 1][0][threadIdx.x];
+    double* cyo = &t.y[0][threadIdx.x];
+    double* dd = dst + (size_t)y0 * w;
+    if (cy == 0) caus_warm(cs, cx[0], k);
+    if (!more) anti_warm(a, cx[(rows - 1) * kColT], k);
+    if (rows == kF64Chunk) {
+#pragma unroll 8
+      for (int j = 0; j < kF64Chunk; ++j) cyo[j * kColT] = caus_step(cs, cx[j * kColT], k);
+#pragma unroll 8
+      for (int j = kF64Chunk - 1; j >= 0; --j) {
+        const double yi = anti_step(a, cx[j * kColT], k);
+        dd[(size_t)j * w] = m_(a_(cyo[j * kColT], yi), scale);
+      }
+    } else {
+      for (int j = 0; j < rows; ++j) cyo[j * kColT] = caus_step(cs, cx[j * kColT], k);
+      for (int j = rows - 1; j >= 0; --j) {
+        const double yi = anti_step(a, cx[j * kColT], k);
+        dd[(size_t)j * w] = m_(a_(cyo[j * kColT], yi), scale);
+      }
+    }
+  }
+}
+
+size_t f64_state_doubles(int w, int h, int planes) {
+  const size_t nc = (w + kF64Chunk - 1) / kF64Chunk, ncy = (h + kF64Chunk - 1) / kF64Chunk;
+  const size_t bands = (h + kRB2 - 1) / kRB2;
+  const size_t rows_s = bands * nc * 8 * planes * kRB2, cols_s = (size_t)planes * ncy * 8 * w;
+  return std::max(rows_s, cols_s);
+}
+
 // Accumulation in step order and finalize (bilateral.cpp:117-148).
 struct Combine64 {
   double c[kMaxPlanes];  // c_n = c_{n-1} / n, as step() updates it
@@ -315,7 +711,15 @@ void chk(cudaError_t e, const char* what) {
 
 size_t f64_workspace_bytes(int w, int h, int degree) {
   const size_t n = (size_t)w * h;
-  return sizeof(double) * (n * (2 + 2 * (size_t)(degree + 2)) + 2 + 4 * kF64MeanBlocks);
+  return sizeof(double) * (n * (2 + 2 * (size_t)(degree + 2)) + 2 + 4 * kF64MeanBlocks +
+                           f64_state_doubles(w, h, degree + 2));
+}
+
+// GPF_B200_F64_SEQUENTIAL=1 runs the literal sequential replay instead of the
+// chunked form (same bits; kept as the cross-check of tests/test_gpu_dropin.py)
+static bool f64_sequential() {
+  const char* e = std::getenv("GPF_B200_F64_SEQUENTIAL");
+  return e != nullptr && e[0] != '\0' && e[0] != '0';
 }
 
 void F64Work::ensure(size_t bytes_needed) {
@@ -354,11 +758,34 @@ void run_gpf_f64_exact(const double* d_in, double* d_out, const Params& p, F64Wo
   k.den = 1.0 + k.d[0] + k.d[1] + k.d[2] + k.d[3];
   k.csum = k.nc[0] + k.nc[1] + k.nc[2] + k.nc[3];
   k.asum = k.na[0] + k.na[1] + k.na[2] + k.na[3];
-  k_f64_rows<<<dim3((h + kRowT - 1) / kRowT, (planes + kGP - 1) / kGP), kRowT, 0, st>>>(H, F0, R, w, h,
-                                                                                        planes, k);
   const double mass = kernel_mass_1d(p.sigma_s, default_window_radius(p.sigma_s));
   const double scale = mass * mass * p.kernel_scale;
-  k_f64_cols<<<dim3((w + 127) / 128, planes), 128, 0, st>>>(R, Cb, w, h, k, scale);
+  if (f64_sequential()) {
+    k_f64_rows<<<dim3((h + kRowT - 1) / kRowT, (planes + kGP - 1) / kGP), kRowT, 0, st>>>(H, F0, R, w, h,
+                                                                                          planes, k);
+    k_f64_cols<<<dim3((w + 127) / 128, planes), 128, 0, st>>>(R, Cb, w, h, k, scale);
+  } else {
+    double* S = partials + 4 * kF64MeanBlocks;  // recorded anticausal states (rows, then columns)
+    const size_t smA = rows2_smem_bytes(planes) - sizeof(double) * (size_t)planes * kYP;
+    const size_t smB = rows2_smem_bytes(planes);
+    chk(cudaFuncSetAttribute(k_f64_rows_states, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smA),
+        "cudaFuncSetAttribute");
+    chk(cudaFuncSetAttribute(k_f64_rows_chunked, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smB),
+        "cudaFuncSetAttribute");
+    const int PG = (planes + kGP - 1) / kGP;
+    const int thr = std::max(64, ((PG * kRB2 + 31) / 32) * 32);  // >= 64: kHR loads per thread cover a tile
+    const int bands = (h + kRB2 - 1) / kRB2;
+    if (w > kF64Chunk) k_f64_rows_states<<<bands, thr, smA, st>>>(H, F0, S, w, h, planes, k);
+    k_f64_rows_chunked<<<bands, thr, smB, st>>>(H, F0, S, R, w, h, planes, k);
+    const dim3 cg((w + kColT - 1) / kColT, planes);
+    const size_t smCA = sizeof(double) * 2 * kF64Chunk * kColT, smCB = sizeof(ColTiles);
+    chk(cudaFuncSetAttribute(k_f64_cols_states, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smCA),
+        "cudaFuncSetAttribute");
+    chk(cudaFuncSetAttribute(k_f64_cols_chunked, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smCB),
+        "cudaFuncSetAttribute");
+    if (h > kF64Chunk) k_f64_cols_states<<<cg, kColT, smCA, st>>>(R, S, w, h, k);
+    k_f64_cols_chunked<<<cg, kColT, smCB, st>>>(R, S, Cb, w, h, k, scale);
+  }
   Combine64 cb;
   cb.c[0] = 1.0;
   for (int s = 0; s + 1 < kMaxPlanes; ++s) cb.c[s + 1] = cb.c[s] / (s + 1);  // c = c / (n + 1)

@@ -270,3 +270,21 @@ def test_dropin_concurrent_large_frames_pipeline(gpu):
     for (a, fa), (b, fb) in zip(seq, got):
         assert fa == fb
         np.testing.assert_array_equal(a, b)
+
+
+@pytest.mark.parametrize("shape,deg,ss", [((97, 131), 20, 2.0), ((64, 64), 7, 0.7), ((33, 200), 49, 6.0),
+                                          ((300, 40), 20, 25.0), ((1, 77), 3, 3.0), ((520, 515), 20, 9.0)])
+def test_fp64_chunked_equals_sequential_bitwise(gpu, shape, deg, ss, monkeypatch):
+    """The chunked fp64 passes (anticausal states recorded per 32-sample chunk,
+    chunks restarted from them) against the literal sequential replay
+    (GPF_B200_F64_SEQUENTIAL=1): same operations in the same order, equal bits."""
+    img = np.random.default_rng(shape[0] * 1000 + shape[1]).uniform(0, 255, size=shape)
+    gpu.set_precision("fp64")
+    try:
+        out, fb = gpu.gpf_filter_gpf(img, gpu.spatial_params(ss), gpu.range_params(11.0, deg))
+        monkeypatch.setenv("GPF_B200_F64_SEQUENTIAL", "1")
+        seq, fbs = gpu.gpf_filter_gpf(img, gpu.spatial_params(ss), gpu.range_params(11.0, deg))
+    finally:
+        gpu.set_precision("auto")
+    assert fb == fbs
+    assert np.array_equal(out.view(np.uint64), seq.view(np.uint64)), shape
