@@ -287,10 +287,20 @@ __global__ void __launch_bounds__(128) k_f64_cols(const double* __restrict__ R, 
 // (tests/test_gpu_dropin.py compares them); the planes cross HBM once per
 // axis instead of being re-read and re-written.
 // ----------------------------------------------------------------------------
-constexpr int kF64Chunk = 32;  // samples per chunk on both axes
-constexpr int kRB2 = 8;        // rows per CTA of the chunked row pass
-constexpr int kTP = kF64Chunk + 1;  // padded tile pitch (doubles)
-constexpr int kYP = kRB2 * kTP + 4;  // Y plane stride: consecutive plane pairs 8 doubles apart in the bank space
+constexpr int kF64Chunk = 32;  // samples per chunk of the column pass
+#ifndef GPF_F64_RB
+#define GPF_F64_RB 8
+#endif
+#ifndef GPF_F64_RCH
+#define GPF_F64_RCH 32
+#endif
+constexpr int kRB2 = GPF_F64_RB;     // rows per CTA of the chunked row pass (4 or 8)
+constexpr int kRowCh = GPF_F64_RCH;  // samples per chunk of the row pass (<= 32)
+constexpr int kTP = kRowCh + 1;      // padded tile pitch (doubles)
+// Y plane stride: a half-warp's 16 / kRB2 plane pairs land kRB2 doubles apart in the bank space
+constexpr int kYP = kRB2 * kTP + ((kRB2 / 2 - (kRB2 * kTP) % 8 + 8) % 8);
+static_assert(kRB2 == 4 || kRB2 == 8, "rows per CTA");
+static_assert(kRowCh == 8 || kRowCh == 16 || kRowCh == 32, "row chunk");
 
 __device__ __forceinline__ void cp8(double* smem, const double* gmem) {
   const unsigned sa = static_cast<unsigned>(__cvta_generic_to_shared(smem));
@@ -322,8 +332,8 @@ __device__ __forceinline__ void rows_issue_load(const RowCtx& c, RowPrefetch& pf
 #pragma unroll
   for (int q = 0; q < kHR; ++q) {
     const int e = c.tid + q * c.nthr;
-    const int r = e / kF64Chunk, j = e % kF64Chunk;
-    if (e < kRB2 * kF64Chunk && r < c.rows && j < cols) {
+    const int r = e / kRowCh, j = e % kRowCh;
+    if (e < kRB2 * kRowCh && r < c.rows && j < cols) {
       const size_t g = (size_t)(c.y0 + r) * w + x0 + j;
       pf.hreg[q] = __ldg(H + g);
       cp8(&c.sF[r * kTP + j], F0 + g);
@@ -336,22 +346,22 @@ __device__ __forceinline__ void rows_finish_load(const RowCtx& c, const RowPrefe
 #pragma unroll
   for (int q = 0; q < kHR; ++q) {
     const int e = c.tid + q * c.nthr;
-    const int r = e / kF64Chunk, j = e % kF64Chunk;
-    if (e < kRB2 * kF64Chunk && r < c.rows && j < cols) c.sH[r * kTP + j] = pf.hreg[q];
+    const int r = e / kRowCh, j = e % kRowCh;
+    if (e < kRB2 * kRowCh && r < c.rows && j < cols) c.sH[r * kTP + j] = pf.hreg[q];
   }
   asm volatile("cp.async.wait_group 0;\n" ::: "memory");
   __syncthreads();
   // even planes of every pixel of the chunk, four pixels' chains interleaved
   constexpr int kE = 4;
-  for (int e0 = c.tid; e0 < kRB2 * kF64Chunk; e0 += c.nthr * kE) {
+  for (int e0 = c.tid; e0 < kRB2 * kRowCh; e0 += c.nthr * kE) {
     double hv[kE], v[kE];
     int off[kE];
     bool ok[kE];
 #pragma unroll
     for (int q = 0; q < kE; ++q) {
       const int e = e0 + q * c.nthr;
-      const int r = e / kF64Chunk, j = e % kF64Chunk;
-      ok[q] = e < kRB2 * kF64Chunk && r < c.rows && j < cols;
+      const int r = e / kRowCh, j = e % kRowCh;
+      ok[q] = e < kRB2 * kRowCh && r < c.rows && j < cols;
       off[q] = ok[q] ? r * kTP + j : 0;
       hv[q] = c.sH[off[q]];
       v[q] = c.sF[off[q]];
@@ -433,7 +443,7 @@ __global__ void k_f64_rows_states(const double* __restrict__ H, const double* __
                                   double* __restrict__ S, int w, int h, int planes, Deriche64 k) {
   extern __shared__ double smem_d[];
   const RowCtx c = rows_ctx(smem_d, h, planes);
-  const int nc = (w + kF64Chunk - 1) / kF64Chunk;
+  const int nc = (w + kRowCh - 1) / kRowCh;
   const bool live = c.pg < c.PG && c.row < c.rows;
   const size_t comp = (size_t)planes * kRB2;
   const double* xe = c.X2 + (c.pg < c.PG ? c.pg : 0) * kRB2 * kTP + c.row * kTP;
@@ -441,23 +451,30 @@ __global__ void k_f64_rows_states(const double* __restrict__ H, const double* __
   Anti64 a[kGP];
   double x[kGP];
   RowPrefetch pf;
-  if (nc > 1) rows_issue_load(c, pf, H, F0, w, (nc - 1) * kF64Chunk, w - (nc - 1) * kF64Chunk);
+  if (nc > 1) rows_issue_load(c, pf, H, F0, w, (nc - 1) * kRowCh, w - (nc - 1) * kRowCh);
   for (int ch = nc - 1; ch >= 1; --ch) {  // chunk 0's walk would record nothing
-    const int x0 = ch * kF64Chunk, cols = min(kF64Chunk, w - x0);
+    const int x0 = ch * kRowCh, cols = min(kRowCh, w - x0);
     rows_finish_load(c, pf, cols);
-    if (ch > 1) rows_issue_load(c, pf, H, F0, w, x0 - kF64Chunk, kF64Chunk);
+    if (ch > 1) rows_issue_load(c, pf, H, F0, w, x0 - kRowCh, kRowCh);
     if (live) {
       if (ch == nc - 1) {
         rows_x(xe, hr, cols - 1, x);
 #pragma unroll
         for (int p = 0; p < kGP; ++p) anti_warm(a[p], x[p], k);
       }
-      if (cols == kF64Chunk) {  // full chunk: unrolled, the state rotation renames registers
-#pragma unroll 8
-        for (int j = kF64Chunk - 1; j >= 0; --j) {
-          rows_x(xe, hr, j, x);
+      if (cols == kRowCh) {  // full chunk: eight samples' inputs at a time, rotations rename registers
+        for (int j0 = kRowCh - 8; j0 >= 0; j0 -= 8) {
+          double xs[8], hs[8];
 #pragma unroll
-          for (int p = 0; p < kGP; ++p) anti_step(a[p], x[p], k);
+          for (int q = 0; q < 8; ++q) {
+            xs[q] = xe[j0 + q];
+            hs[q] = hr[j0 + q];
+          }
+#pragma unroll
+          for (int q = 7; q >= 0; --q) {
+            anti_step(a[0], xs[q], k);
+            anti_step(a[1], m_(hs[q], xs[q]), k);
+          }
         }
       } else {
         for (int j = cols - 1; j >= 0; --j) {
@@ -481,7 +498,7 @@ __global__ void k_f64_rows_chunked(const double* __restrict__ H, const double* _
   extern __shared__ double smem_d[];
   const RowCtx c = rows_ctx(smem_d, h, planes);
   double* Y = c.X2 + (size_t)c.PG * kRB2 * kTP;  // [planes][kRB2][kTP]
-  const int nc = (w + kF64Chunk - 1) / kF64Chunk;
+  const int nc = (w + kRowCh - 1) / kRowCh;
   const bool live = c.pg < c.PG && c.row < c.rows;
   const size_t comp = (size_t)planes * kRB2, ps = (size_t)w * h;
   const int lane = c.tid & 31, warp = c.tid >> 5, nwarp = c.nthr >> 5;
@@ -490,19 +507,19 @@ __global__ void k_f64_rows_chunked(const double* __restrict__ H, const double* _
   Caus64 cs[kGP];
   double x[kGP];
   RowPrefetch pf;
-  rows_issue_load(c, pf, H, F0, w, 0, min(kF64Chunk, w));
+  rows_issue_load(c, pf, H, F0, w, 0, min(kRowCh, w));
   for (int ch = 0; ch < nc; ++ch) {
-    const int x0 = ch * kF64Chunk, cols = min(kF64Chunk, w - x0);
+    const int x0 = ch * kRowCh, cols = min(kRowCh, w - x0);
     // the anticausal state entering this chunk, in flight under the even-plane chains
-    Anti64 a[kGP];
+    Anti64 a[kGP], an[kGP];
     if (live && ch + 1 < nc) {
       const double* src = S + ((size_t)blockIdx.x * nc + ch) * 8 * comp + c.row;
 #pragma unroll
       for (int p = 0; p < kGP; ++p)
-        if (c.pg * kGP + p < planes) anti_load(a[p], src + (size_t)(c.pg * kGP + p) * kRB2, comp);
+        if (c.pg * kGP + p < planes) anti_load(an[p], src + (size_t)(c.pg * kGP + p) * kRB2, comp);
     }
     rows_finish_load(c, pf, cols);
-    if (ch + 1 < nc) rows_issue_load(c, pf, H, F0, w, x0 + kF64Chunk, min(kF64Chunk, w - x0 - kF64Chunk));
+    if (ch + 1 < nc) rows_issue_load(c, pf, H, F0, w, x0 + kRowCh, min(kRowCh, w - x0 - kRowCh));
     if (live) {
       double* yt = Y + (size_t)(c.pg * kGP) * kYP + c.row * kTP;
       const bool two = c.pg * kGP + 1 < planes;
@@ -515,19 +532,41 @@ __global__ void k_f64_rows_chunked(const double* __restrict__ H, const double* _
         rows_x(xe, hr, cols - 1, x);
 #pragma unroll
         for (int p = 0; p < kGP; ++p) anti_warm(a[p], x[p], k);
+      } else {
+#pragma unroll
+        for (int p = 0; p < kGP; ++p) a[p] = an[p];
       }
-      if (cols == kF64Chunk && two) {  // full chunk: unrolled, the state rotations rename registers
-#pragma unroll 8
-        for (int j = 0; j < kF64Chunk; ++j) {
-          rows_x(xe, hr, j, x);
-          yt[j] = caus_step(cs[0], x[0], k);
-          yt[kYP + j] = caus_step(cs[1], x[1], k);
+      if (cols == kRowCh && two) {
+        // full chunk, eight samples at a time: their inputs are read before the
+        // outputs are stored (the tiles share one array, so the compiler keeps
+        // loads behind earlier stores), and the state rotations rename registers
+        for (int j0 = 0; j0 < kRowCh; j0 += 8) {
+          double xs[8], hs[8];
+#pragma unroll
+          for (int q = 0; q < 8; ++q) {
+            xs[q] = xe[j0 + q];
+            hs[q] = hr[j0 + q];
+          }
+#pragma unroll
+          for (int q = 0; q < 8; ++q) {
+            yt[j0 + q] = caus_step(cs[0], xs[q], k);
+            yt[kYP + j0 + q] = caus_step(cs[1], m_(hs[q], xs[q]), k);
+          }
         }
-#pragma unroll 8
-        for (int j = kF64Chunk - 1; j >= 0; --j) {
-          rows_x(xe, hr, j, x);
-          yt[j] = a_(yt[j], anti_step(a[0], x[0], k));
-          yt[kYP + j] = a_(yt[kYP + j], anti_step(a[1], x[1], k));
+        for (int j0 = kRowCh - 8; j0 >= 0; j0 -= 8) {
+          double xs[8], hs[8], y0s[8], y1s[8];
+#pragma unroll
+          for (int q = 0; q < 8; ++q) {
+            xs[q] = xe[j0 + q];
+            hs[q] = hr[j0 + q];
+            y0s[q] = yt[j0 + q];
+            y1s[q] = yt[kYP + j0 + q];
+          }
+#pragma unroll
+          for (int q = 7; q >= 0; --q) {
+            yt[j0 + q] = a_(y0s[q], anti_step(a[0], xs[q], k));
+            yt[kYP + j0 + q] = a_(y1s[q], anti_step(a[1], m_(hs[q], xs[q]), k));
+          }
         }
       } else {
         for (int j = 0; j < cols; ++j) {
@@ -545,11 +584,17 @@ __global__ void k_f64_rows_chunked(const double* __restrict__ H, const double* _
       }
     }
     __syncthreads();
-    // the chunk leaves as 256-B row segments, one (plane, row) per warp and turn
-    for (int sgm = warp; sgm < planes * kRB2; sgm += nwarp) {
-      const int n = sgm / kRB2, r = sgm % kRB2;
-      if (r < c.rows && lane < cols)
-        R[(size_t)n * ps + (size_t)(c.y0 + r) * w + x0 + lane] = Y[(size_t)n * kYP + r * kTP + lane];
+    // the chunk leaves as coalesced row segments of kRowCh doubles
+    // a warp takes whole rows and walks their planes with constant strides
+    constexpr int kSW = 32 / kRowCh;  // row segments per warp and turn
+    const int l = lane % kRowCh;
+    for (int r = warp * kSW + lane / kRowCh; r < c.rows; r += nwarp * kSW) {
+      const double* ys = Y + r * kTP + l;
+      double* rd = R + (size_t)(c.y0 + r) * w + x0 + l;
+      if (l < cols) {
+#pragma unroll 4
+        for (int n = 0; n < planes; ++n) rd[(size_t)n * ps] = ys[n * kYP];
+      }
     }
     __syncthreads();
   }
@@ -639,13 +684,24 @@ __global__ void __launch_bounds__(kColT) k_f64_cols_chunked(const double* __rest
     double* dd = dst + (size_t)y0 * w;
     if (cy == 0) caus_warm(cs, cx[0], k);
     if (!more) anti_warm(a, cx[(rows - 1) * kColT], k);
-    if (rows == kF64Chunk) {
-#pragma unroll 8
-      for (int j = 0; j < kF64Chunk; ++j) cyo[j * kColT] = caus_step(cs, cx[j * kColT], k);
-#pragma unroll 8
-      for (int j = kF64Chunk - 1; j >= 0; --j) {
-        const double yi = anti_step(a, cx[j * kColT], k);
-        dd[(size_t)j * w] = m_(a_(cyo[j * kColT], yi), scale);
+    if (rows == kF64Chunk) {  // eight samples' inputs read ahead of the outputs' stores
+      for (int j0 = 0; j0 < kF64Chunk; j0 += 8) {
+        double xs[8];
+#pragma unroll
+        for (int q = 0; q < 8; ++q) xs[q] = cx[(j0 + q) * kColT];
+#pragma unroll
+        for (int q = 0; q < 8; ++q) cyo[(j0 + q) * kColT] = caus_step(cs, xs[q], k);
+      }
+      for (int j0 = kF64Chunk - 8; j0 >= 0; j0 -= 8) {
+        double xs[8], ys[8];
+#pragma unroll
+        for (int q = 0; q < 8; ++q) {
+          xs[q] = cx[(j0 + q) * kColT];
+          ys[q] = cyo[(j0 + q) * kColT];
+        }
+#pragma unroll
+        for (int q = 7; q >= 0; --q)
+          dd[(size_t)(j0 + q) * w] = m_(a_(ys[q], anti_step(a, xs[q], k)), scale);
       }
     } else {
       for (int j = 0; j < rows; ++j) cyo[j * kColT] = caus_step(cs, cx[j * kColT], k);
@@ -658,7 +714,7 @@ __global__ void __launch_bounds__(kColT) k_f64_cols_chunked(const double* __rest
 }
 
 size_t f64_state_doubles(int w, int h, int planes) {
-  const size_t nc = (w + kF64Chunk - 1) / kF64Chunk, ncy = (h + kF64Chunk - 1) / kF64Chunk;
+  const size_t nc = (w + kRowCh - 1) / kRowCh, ncy = (h + kF64Chunk - 1) / kF64Chunk;
   const size_t bands = (h + kRB2 - 1) / kRB2;
   const size_t rows_s = bands * nc * 8 * planes * kRB2, cols_s = (size_t)planes * ncy * 8 * w;
   return std::max(rows_s, cols_s);
@@ -775,7 +831,7 @@ void run_gpf_f64_exact(const double* d_in, double* d_out, const Params& p, F64Wo
     const int PG = (planes + kGP - 1) / kGP;
     const int thr = std::max(64, ((PG * kRB2 + 31) / 32) * 32);  // >= 64: kHR loads per thread cover a tile
     const int bands = (h + kRB2 - 1) / kRB2;
-    if (w > kF64Chunk) k_f64_rows_states<<<bands, thr, smA, st>>>(H, F0, S, w, h, planes, k);
+    if (w > kRowCh) k_f64_rows_states<<<bands, thr, smA, st>>>(H, F0, S, w, h, planes, k);
     k_f64_rows_chunked<<<bands, thr, smB, st>>>(H, F0, S, R, w, h, planes, k);
     const dim3 cg((w + kColT - 1) / kColT, planes);
     const size_t smCA = sizeof(double) * 2 * kF64Chunk * kColT, smCB = sizeof(ColTiles);

@@ -52,5 +52,18 @@ int main() {
   run<1, 1>("DMUL->DADD dependent", 32, 1, 2);
   run<1, 2>("DMUL+DADD 2 chains, 3 warps", 96, 3, 2);
   run<1, 2>("DMUL+DADD 2 chains, 4 warps", 128, 4, 2);
+  // occupancy x ILP grid (independent dependent-chains per thread; warps per SM = thr/32 * CTAs)
+  run<1, 1>("grid: 1 chain", 128, 1, 2);
+  run<1, 2>("grid: 2 chains", 128, 1, 2);
+  run<1, 4>("grid: 4 chains", 128, 1, 2);
+  run<1, 8>("grid: 8 chains", 128, 1, 2);
+  run<1, 1>("grid: 1 chain", 128, 2, 2);
+  run<1, 2>("grid: 2 chains", 128, 2, 2);
+  run<1, 4>("grid: 4 chains", 128, 2, 2);
+  run<1, 8>("grid: 8 chains", 128, 2, 2);
+  run<1, 1>("grid: 1 chain", 128, 4, 2);
+  run<1, 4>("grid: 4 chains", 128, 4, 2);
+  run<1, 1>("grid: 1 chain", 128, 8, 2);
+  run<1, 2>("grid: 2 chains", 128, 8, 2);
   return 0;
 }
