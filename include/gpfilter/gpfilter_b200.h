@@ -118,7 +118,11 @@ gpf_status gpf_b200_filter_f32_host(gpf_b200_plan* plan, const float* h_in, floa
  *         operation (only exp() is CUDA's rather than glibc's): follows the
  *         reference also where its degree-N series is ill-conditioned and its
  *         output leaves the input range (BASELINE C2/C5). Degree <= 62; about
- *         (degree + 2) x 16 B of extra device memory per pixel.
+ *         (degree + 2) x 18 B of extra device memory per pixel. Each axis runs
+ *         in chunks of 32 samples restarted from recorded recurrence states,
+ *         bitwise equal to the line-by-line order of the reference
+ *         (environment GPF_B200_F64_SEQUENTIAL=1 selects the literal
+ *         sequential replay, the cross-check of the tests).
  *   AUTO  (default; environment GPF_B200_PRECISION=auto|fp32|fp64 sets the
  *         initial mode) measures t_c, f_min and f_max on the device and runs
  *         FP64 outside the FP32 envelope, FP32 inside it.
