@@ -88,6 +88,20 @@ gpf_status gpf_b200_filter_f32_ev(gpf_b200_plan* plan, const float* d_in, float*
 gpf_status gpf_b200_filter_f32_checked(gpf_b200_plan* plan, const float* d_in, float* d_out,
                                        int count, long long* d_fallbacks, int* d_ill, void* stream);
 
+/* One-shot batched device entry: gpf_b200_filter_f32 without a
+ * plan handle. Filters `count` contiguous fp32 frames (each width*height,
+ * row-major) in device memory on the current device with the parameters of
+ * gpf_filter_gpf (recursive backend; `centering` as there). The library
+ * creates a plan for (device, size, parameters, count) on first use and keeps
+ * the four most recently used, so a repeated call allocates nothing; calls
+ * that share a cached plan run one after the other on the device (their
+ * streams are chained by an event). d_fallbacks: device memory, `count` long
+ * longs, may be NULL. Enqueued on `stream`, no synchronisation.
+ * gpf_b200_dropin_release() frees the cached plans. */
+gpf_status gpf_b200_filter_batch(const float* d_in, float* d_out, int width, int height, int count,
+                                 const gpf_spatial_params* sp, const gpf_range_params* rp,
+                                 int centering, long long* d_fallbacks, void* stream);
+
 /* Exact (direct O(sigma_s^2)) bilateral filter of `count` contiguous fp32
  * frames in device memory (the gpf_filter_exact definition), on `stream`. */
 gpf_status gpf_b200_exact_f32(const float* d_in, float* d_out, int width, int height, int count,

@@ -41,7 +41,7 @@ EXPORTED = (
     "gpf_b200_filter_f32_host", "gpf_b200_exact_f32", "gpf_b200_compare_f32",
     "gpf_b200_set_precision", "gpf_b200_get_precision", "gpf_b200_last_precision",
     "gpf_b200_last_max_abs_h", "gpf_b200_fp32_h_limit", "gpf_b200_fp32_h_limit_degree", "gpf_b200_dropin_release",
-    "gpf_b200_last_device_ms", "gpf_b200_filter_f32_checked",
+    "gpf_b200_last_device_ms", "gpf_b200_filter_f32_checked", "gpf_b200_filter_batch",
 )
 
 # gpf_b200_precision (include/gpfilter/gpfilter_b200.h)
@@ -123,6 +123,8 @@ def _declare(lib: C.CDLL) -> C.CDLL:
     lib.gpf_b200_fp32_h_limit_degree.argtypes = [C.c_int]
     lib.gpf_b200_last_device_ms.restype = C.c_float
     lib.gpf_b200_filter_f32_checked.argtypes = [vp, vp, vp, C.c_int, vp, vp, vp]
+    lib.gpf_b200_filter_batch.argtypes = [vp, vp, C.c_int, C.c_int, C.c_int, C.POINTER(SpatialParams),
+                                          C.POINTER(RangeParams), C.c_int, vp, vp]
     return lib
 
 

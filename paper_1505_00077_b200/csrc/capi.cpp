@@ -127,6 +127,7 @@ struct gpf_b200_plan {
 namespace {
 
 thread_local std::string g_last_error;
+void batch_release();  // cached plans of gpf_b200_filter_batch (defined with it)
 std::atomic<int> g_threads{1};
 
 gpf_status fail(gpf_status s, const std::string& msg) {
@@ -495,7 +496,10 @@ double gpf_b200_last_max_abs_h(void) { return gpfb::last_max_abs_h(); }
 float gpf_b200_last_device_ms(void) { return gpfb::last_device_ms(); }
 double gpf_b200_fp32_h_limit(void) { return gpfb::kH32Limit; }
 double gpf_b200_fp32_h_limit_degree(int degree) { return gpfb::fp32_h_limit(degree); }
-void gpf_b200_dropin_release(void) { gpfb::dropin_release(); }
+void gpf_b200_dropin_release(void) {
+  batch_release();
+  gpfb::dropin_release();
+}
 
 gpf_status gpf_set_num_threads(int n) {
   if (n < 1) return fail(GPF_ERR_INVALID_ARGUMENT, "thread count must be >= 1");
@@ -647,6 +651,38 @@ gpf_status filter_f32_impl(gpf_b200_plan* plan, const float* d_in, float* d_out,
     }
   });
 }
+
+// One-shot batched entry: plans cached per device and parameter set, most
+// recently used first. A plan's workspace serves one call at a time, so a call
+// makes its stream wait for the plan's previous user (`last`).
+struct BatchEntry {
+  int device, count;
+  gpfb::Params p;
+  gpf_b200_plan* plan;
+  cudaEvent_t last;
+};
+std::mutex g_batch_mu;
+std::list<BatchEntry> g_batch;
+constexpr int kBatchPlans = 4;
+constexpr size_t kBatchWorkspace = (size_t)16 << 30;  // bound on one plan's batch workspace
+
+bool batch_same(const BatchEntry& e, int device, int count, const gpfb::Params& p) {
+  return e.device == device && e.count == count && e.p.width == p.width && e.p.height == p.height &&
+         e.p.sigma_s == p.sigma_s && e.p.kernel_scale == p.kernel_scale && e.p.sigma_r == p.sigma_r &&
+         e.p.degree == p.degree && e.p.centering == p.centering;
+}
+
+void batch_drop(BatchEntry& e) {  // the plan's queued work finishes first
+  cudaEventSynchronize(e.last);
+  cudaEventDestroy(e.last);
+  gpf_b200_plan_destroy(e.plan);
+}
+
+void batch_release() {
+  std::lock_guard<std::mutex> lock(g_batch_mu);
+  for (auto& e : g_batch) batch_drop(e);
+  g_batch.clear();
+}
 }  // namespace
 
 extern "C" {
@@ -664,6 +700,55 @@ gpf_status gpf_b200_filter_f32(gpf_b200_plan* plan, const float* d_in, float* d_
 gpf_status gpf_b200_filter_f32_checked(gpf_b200_plan* plan, const float* d_in, float* d_out, int count,
                                        long long* d_fallbacks, int* d_ill, void* stream) {
   return filter_f32_impl(plan, d_in, d_out, count, d_fallbacks, d_ill, stream, nullptr);
+}
+
+gpf_status gpf_b200_filter_batch(const float* d_in, float* d_out, int width, int height, int count,
+                                 const gpf_spatial_params* sp, const gpf_range_params* rp, int centering,
+                                 long long* d_fallbacks, void* stream) {
+  if (d_in == nullptr || d_out == nullptr || sp == nullptr || rp == nullptr)
+    return fail(GPF_ERR_INVALID_ARGUMENT, "null argument");
+  if (count < 0) return fail(GPF_ERR_INVALID_ARGUMENT, "count must be >= 0");
+  gpf_status inner = GPF_OK;
+  const gpf_status st = guarded([&] {
+    const gpfb::Params p =
+        validate(width, height, *sp, *rp, GPF_BACKEND_RECURSIVE, centering, gpfb::kMaxDegreeF32);
+    if (count == 0) return;
+    const int dev = current_device();
+    std::lock_guard<std::mutex> lock(g_batch_mu);
+    auto it = g_batch.begin();
+    while (it != g_batch.end() && !batch_same(*it, dev, count, p)) ++it;
+    if (it != g_batch.end()) {
+      g_batch.splice(g_batch.begin(), g_batch, it);
+    } else {
+      while ((int)g_batch.size() >= kBatchPlans) {
+        batch_drop(g_batch.back());
+        g_batch.pop_back();
+      }
+      BatchEntry e{dev, count, p, nullptr, nullptr};
+      inner = gpf_b200_plan_create(width, height, sp, rp, centering, dev, &e.plan);
+      if (inner != GPF_OK) return;
+      // frames filtered per launch: the whole batch when its workspace fits the bound
+      const size_t per = std::max<size_t>(e.plan->plan.bytes, 1);
+      const int frames = (int)std::max<size_t>(1, std::min<size_t>((size_t)count, kBatchWorkspace / per));
+      if (frames > 1) inner = gpf_b200_plan_set_batch(e.plan, frames);
+      if (inner == GPF_OK && cudaEventCreateWithFlags(&e.last, cudaEventDisableTiming) != cudaSuccess) {
+        cudaGetLastError();
+        inner = fail(GPF_ERR_UNKNOWN, "cudaEventCreate failed");
+      }
+      if (inner != GPF_OK) {
+        gpf_b200_plan_destroy(e.plan);
+        return;
+      }
+      cuda_check(cudaEventRecord(e.last, static_cast<cudaStream_t>(stream)), "cudaEventRecord");
+      g_batch.push_front(e);
+    }
+    BatchEntry& e = g_batch.front();
+    auto cs = static_cast<cudaStream_t>(stream);
+    cuda_check(cudaStreamWaitEvent(cs, e.last, 0), "cudaStreamWaitEvent");
+    inner = gpf_b200_filter_f32(e.plan, d_in, d_out, count, d_fallbacks, stream);
+    cuda_check(cudaEventRecord(e.last, cs), "cudaEventRecord");
+  });
+  return st != GPF_OK ? st : inner;
 }
 
 gpf_status gpf_b200_exact_f32(const float* d_in, float* d_out, int width, int height, int count,

@@ -159,6 +159,18 @@ def exact_device(d_in, d_out, width: int, height: int, sigma_s: float, sigma_r: 
                                          C.byref(rp), stream))
 
 
+def filter_batch_device(d_in, d_out, width: int, height: int, count: int,
+                        sp: SpatialParams | None = None, rp: RangeParams | None = None,
+                        centering: int = 1, d_fallbacks=None, stream: int = 0) -> None:
+    """gpf_b200_filter_batch: `count` contiguous device fp32 frames, no plan handle
+    (the library caches one per device, size and parameter set). Enqueued on `stream`."""
+    sp = sp or spatial_params()
+    rp = rp or range_params()
+    fb = _ptr(d_fallbacks) if d_fallbacks is not None else None
+    _check(_lib.lib().gpf_b200_filter_batch(_ptr(d_in), _ptr(d_out), width, height, count, C.byref(sp),
+                                            C.byref(rp), centering, fb, stream))
+
+
 def compare_device(d_ref, d_test, width: int, height: int, exclude_border: int = 0,
                    stream: int = 0) -> dict:
     """gpf_compare on fp32 device images (synchronises `stream`)."""

@@ -288,3 +288,45 @@ def test_fp64_chunked_equals_sequential_bitwise(gpu, shape, deg, ss, monkeypatch
         gpu.set_precision("auto")
     assert fb == fbs
     assert np.array_equal(out.view(np.uint64), seq.view(np.uint64)), shape
+
+
+def test_filter_batch_one_shot(gpu, oracle):
+    """gpf_b200_filter_batch (SURVEY 8(b)'s plan-less device entry): equals the plan
+    entry bitwise, holds the bar against the oracle, allocates nothing on a repeated
+    call, keeps several parameter sets cached and rejects what the plan entry rejects."""
+    import torch
+
+    w, h, n = 160, 96, 3
+    frames = np.stack([synth.rects_image(w, h, 6, 10.0, 20 + k) for k in range(n)]).astype(np.float32)
+    d_in = torch.from_numpy(frames).cuda()
+    d_out = torch.empty_like(d_in)
+    d_fb = torch.zeros(n, dtype=torch.int64, device="cuda")
+    sp, rp = gpu.spatial_params(4.0), gpu.range_params(35.0, 20)
+    gpu.filter_batch_device(d_in, d_out, w, h, n, sp, rp, 1, d_fb)
+    torch.cuda.synchronize()
+    out = d_out.cpu().numpy()
+    plan = gpu.Plan(w, h, 4.0, 35.0, 20)
+    d_ref = torch.empty_like(d_in)
+    plan.filter_device(d_in, d_ref, n)
+    torch.cuda.synchronize()
+    plan.close()
+    assert np.array_equal(out, d_ref.cpu().numpy())
+    for k in range(n):
+        ref, rfb, _ = oracle.gpf(frames[k].astype(np.float64), 4.0, 35.0, 20)
+        assert int(d_fb[k]) == rfb and np.abs(out[k] - ref).max() <= TOL
+    # a second parameter set, then the first again: both stay cached, nothing is allocated
+    sp2 = gpu.spatial_params(9.0)
+    gpu.filter_batch_device(d_in, d_out, w, h, n, sp2, rp)
+    torch.cuda.synchronize()
+    free0 = torch.cuda.mem_get_info()[0]
+    for s in (sp, sp2, sp):
+        gpu.filter_batch_device(d_in, d_out, w, h, n, s, rp, 1, d_fb)
+    torch.cuda.synchronize()
+    assert torch.cuda.mem_get_info()[0] == free0
+    assert np.array_equal(d_out.cpu().numpy(), out)
+    gpu.filter_batch_device(d_in, d_out, w, h, 0, sp, rp)  # empty batch: nothing to do
+    with pytest.raises(gpu.GpfError, match="sigma_s"):
+        gpu.filter_batch_device(d_in, d_out, w, h, n, gpu.spatial_params(-1.0), rp)
+    with pytest.raises(gpu.GpfError, match="48"):
+        gpu.filter_batch_device(d_in, d_out, w, h, n, sp, gpu.range_params(35.0, 49))
+    gpu.dropin_release()
