@@ -738,12 +738,21 @@ __global__ void k_f64_combine(const double* __restrict__ f, const double* __rest
     const double hv = H[i];
     double g = 1.0, q = 0.0, p = 0.0;
     double fb = Cb[i];
-    for (int s = 0; s <= cb.degree; ++s) {
-      const double cg = m_(cb.c[s], g);
-      q = a_(q, m_(cg, fb));
-      fb = Cb[(size_t)(s + 1) * n + i];
-      p = a_(p, m_(cg, fb));
-      g = m_(hv, g);
+    // eight planes' loads in flight per pixel, then their steps in step order
+    for (int s0 = 0; s0 <= cb.degree; s0 += 8) {
+      double nx[8];
+#pragma unroll
+      for (int k = 0; k < 8; ++k)
+        if (s0 + k <= cb.degree) nx[k] = Cb[(size_t)(s0 + k + 1) * n + i];
+#pragma unroll
+      for (int k = 0; k < 8; ++k)
+        if (s0 + k <= cb.degree) {
+          const double cg = m_(cb.c[s0 + k], g);
+          q = a_(q, m_(cg, fb));
+          fb = nx[k];
+          p = a_(p, m_(cg, fb));
+          g = m_(hv, g);
+        }
     }
     if (fabs(q) <= 1e-8) {  // kQMin (bilateral.hpp:85)
       out[i] = f[i];
