@@ -501,7 +501,7 @@ __global__ void k_f64_rows_chunked(const double* __restrict__ H, const double* _
   const int nc = (w + kRowCh - 1) / kRowCh;
   const bool live = c.pg < c.PG && c.row < c.rows;
   const size_t comp = (size_t)planes * kRB2, ps = (size_t)w * h;
-  const int lane = c.tid & 31, warp = c.tid >> 5, nwarp = c.nthr >> 5;
+  const int lane = c.tid & 31, warp = c.tid >> 5;
   const double* xe = c.X2 + (c.pg < c.PG ? c.pg : 0) * kRB2 * kTP + c.row * kTP;
   const double* hr = c.sH + c.row * kTP;
   Caus64 cs[kGP];
@@ -583,17 +583,20 @@ __global__ void k_f64_rows_chunked(const double* __restrict__ H, const double* _
         }
       }
     }
-    __syncthreads();
-    // the chunk leaves as coalesced row segments of kRowCh doubles
-    // a warp takes whole rows and walks their planes with constant strides
-    constexpr int kSW = 32 / kRowCh;  // row segments per warp and turn
+    // The chunk leaves as coalesced row segments of kRowCh doubles. A warp owns whole
+    // planes of Y (its plane pairs), so it stores them as soon as its own recurrences are
+    // done; the CTA barrier below only guards the tiles the next chunk overwrites.
+    __syncwarp();
+    constexpr int kSW = 32 / kRowCh;       // row segments per warp and turn
+    constexpr int kPW = kGP * 32 / kRB2;  // planes of one warp
     const int l = lane % kRowCh;
-    for (int r = warp * kSW + lane / kRowCh; r < c.rows; r += nwarp * kSW) {
+    const int n0w = warp * kPW, n1w = min(n0w + kPW, planes);
+    for (int r = lane / kRowCh; r < c.rows; r += kSW) {
       const double* ys = Y + r * kTP + l;
       double* rd = R + (size_t)(c.y0 + r) * w + x0 + l;
       if (l < cols) {
 #pragma unroll 4
-        for (int n = 0; n < planes; ++n) rd[(size_t)n * ps] = ys[n * kYP];
+        for (int n = n0w; n < n1w; ++n) rd[(size_t)n * ps] = ys[n * kYP];
       }
     }
     __syncthreads();
