@@ -7,13 +7,14 @@
  * Each declaration cites the reference interface it replaces
  * (/root/reference/proj/include/gpfilter/gpfilter.h, "ref.h" below).
  *
- * Provided: the GPF hot path (gpf_filter_gpf) and the handles, params,
- * status/error plumbing it needs; beside it the exact filter, the Taylor
- * baseline, the single-plane recursive Gaussian, gpf_compare and PGM I/O
- * (SURVEY 8(f)). Not provided (they stay in the reference library; see
- * INTEGRATION.md): the direct (windowed) Gaussian backend and the range-kernel
- * evaluators. The C++ entry point gpfilter::gpf is in gpfilter/gpfilter.hpp;
- * device-resident batches and the precision modes in gpfilter/gpfilter_b200.h.
+ * Provided: every function of the reference header -- the GPF hot path
+ * (gpf_filter_gpf, recursive backend) and the handles, params, status/error
+ * plumbing it needs; beside it the exact filter, the Taylor baseline, the
+ * single-plane Gaussians, the direct (windowed) backend (fp64 on the GPU,
+ * bitwise the reference's), gpf_compare, PGM I/O and the scalar
+ * range-kernel evaluators (host). The C++ entry point gpfilter::gpf is in
+ * gpfilter/gpfilter.hpp; device-resident batches and the precision modes in
+ * gpfilter/gpfilter_b200.h.
  */
 #ifndef GPFILTER_B200_GPFILTER_H
 #define GPFILTER_B200_GPFILTER_H
@@ -61,15 +62,16 @@ typedef enum gpf_boundary {
 } gpf_boundary;
 
 typedef enum gpf_backend {
-  GPF_BACKEND_DIRECT = 0,   /* not provided on the GPU: returns GPF_ERR_INVALID_ARGUMENT */
+  GPF_BACKEND_DIRECT = 0,   /* windowed Gaussian, O(window_radius) per pixel; fp64 mode only */
   GPF_BACKEND_RECURSIVE = 1 /* the O(1) Deriche path, sigma_s >= 0.5 */
 } gpf_backend;
 
 typedef struct gpf_spatial_params {
   double sigma_s;     /* > 0 */
   int window_radius;  /* <= 0 selects ceil(3 sigma_s); unused by the recursive path */
-  gpf_boundary boundary; /* validated; the recursive path always uses the
-                            replicate steady state, as the reference does */
+  gpf_boundary boundary; /* direct backend and exact filter; the recursive path
+                            always uses the replicate steady state, as the
+                            reference does */
   double kernel_scale;   /* > 0 */
 } gpf_spatial_params;
 
@@ -90,14 +92,27 @@ void gpf_range_params_init(gpf_range_params* rp);     /* 30 / 20 */
  * Validation and status mapping follow the reference: NULL in/sp/rp/out ->
  * INVALID_ARGUMENT; *out is set to NULL before work starts; bad backend or
  * boundary enum, sigma_s <= 0, kernel_scale <= 0, sigma_r <= 0, degree < 0 ->
- * INVALID_ARGUMENT (detail names the field); sigma_s < 0.5 ->
- * GPF_ERR_SIGMA_TOO_SMALL with "direct" in the detail. fallback_count may be
+ * INVALID_ARGUMENT (detail names the field); sigma_s < 0.5 with the recursive
+ * backend -> GPF_ERR_SIGMA_TOO_SMALL with "direct" in the detail.
+ * GPF_BACKEND_DIRECT (apply_spatial -> direct_gaussian,
+ * proj/src/core/bilateral.cpp:58-62) filters the planes with the windowed
+ * passes of gpf_gaussian_direct, any sigma_s > 0, in the fp64 mode (the fp32
+ * mode forced by gpf_b200_set_precision rejects it). fallback_count may be
  * NULL and is written only on success. Pixels with |Q| <= 1e-8 (reference
  * units, proj/src/core/bilateral.hpp:85) keep their input value. */
 gpf_status gpf_filter_gpf(const gpf_image* in, const gpf_spatial_params* sp,
                           const gpf_range_params* rp, gpf_backend backend,
                           int centering, long long* fallback_count,
                           gpf_image** out);
+
+/* Spatial windowed Gaussian alone (ref.h:116-117, proj/src/capi.cpp:209-217 ->
+ * direct_gaussian, proj/src/core/spatial.cpp:112-129): 2W+1 taps per axis
+ * (W = sp->window_radius, or ceil(3 sigma_s) when <= 0), rows then columns,
+ * kernel_scale on the row taps, the boundary mode of sp; unnormalised, like
+ * the reference. fp64 on the GPU in the reference's accumulation order:
+ * bitwise equal to the reference. */
+gpf_status gpf_gaussian_direct(const gpf_image* in, const gpf_spatial_params* sp,
+                               gpf_image** out);
 
 /* Spatial recursive Gaussian alone (ref.h:118-119, proj/src/capi.cpp:219-228):
  * same Deriche filter, output scaled by kernel_mass_1d(sigma_s)^2*kernel_scale. */
@@ -108,8 +123,8 @@ gpf_status gpf_gaussian_recursive(const gpf_image* in, double sigma_s,
  * K = degree / 2 (ref.h:109-113, proj/src/capi.cpp:194-207 -> taylor_bilateral,
  * proj/src/core/bilateral.cpp:160-220): the 2K+2 moment images f^m smoothed by
  * the recursive Gaussian and recombined per pixel; fp64 on the GPU, bitwise
- * equal to the reference. Same NULL / validation / status behaviour and
- * fallback rule as gpf_filter_gpf; GPF_BACKEND_DIRECT is rejected. */
+ * equal to the reference, with either backend. Same NULL / validation /
+ * status behaviour and fallback rule as gpf_filter_gpf. */
 gpf_status gpf_filter_taylor(const gpf_image* in, const gpf_spatial_params* sp,
                              const gpf_range_params* rp, gpf_backend backend,
                              long long* fallback_count, gpf_image** out);
@@ -124,6 +139,23 @@ gpf_status gpf_filter_taylor(const gpf_image* in, const gpf_spatial_params* sp,
  * status behaviour. */
 gpf_status gpf_filter_exact(const gpf_image* in, const gpf_spatial_params* sp,
                             const gpf_range_params* rp, gpf_image** out);
+
+/* Range-kernel evaluation (ref.h:123-143, proj/src/capi.cpp:230-286 ->
+ * proj/src/core/range_kernel.cpp): scalar, on the host. NULL out, sigma_r <= 0,
+ * degree < 0, low >= high, step <= 0 or a bad `which` -> INVALID_ARGUMENT. */
+typedef enum gpf_range_approx {
+  GPF_RANGE_APPROX_GAUSS_POLY = 0,
+  GPF_RANGE_APPROX_TAYLOR = 1
+} gpf_range_approx;
+/* exp(-(t - tau)^2 / (2 sigma_r^2)) */
+gpf_status gpf_kernel_gauss(double t, double tau, double sigma_r, double* out);
+/* its degree-N Gauss-polynomial (Eq. (4)) and Taylor approximations */
+gpf_status gpf_kernel_gauss_poly(double t, double tau, double sigma_r, int degree, double* out);
+gpf_status gpf_kernel_taylor(double t, double tau, double sigma_r, int degree, double* out);
+/* sup over t in [low, high] (stepped by `step`, endpoint included) of the
+ * absolute error of the chosen approximation against the exact kernel */
+gpf_status gpf_kernel_sup_error(double sigma_r, int degree, double tau, double low, double high,
+                                double step, gpf_range_approx which, double* out);
 
 /* Error statistics between equally sized images (ref.h:149-159,
  * proj/src/capi.cpp:288-301 -> metrics::compare, proj/src/core/metrics.cpp). */

@@ -98,9 +98,9 @@ struct FilterResult {
   long long fallback_count = 0;
 };
 
-// Constant-time Gauss-polynomial bilateral filter on the GPU. The recursive
-// backend only (SpatialBackend::direct throws std::invalid_argument); degree
-// <= 62.
+// Gauss-polynomial bilateral filter on the GPU: constant time per pixel with
+// SpatialBackend::recursive (the hot path), O(window_radius) with
+// SpatialBackend::direct (windowed passes, fp64 mode); degree <= 62.
 FilterResult gpf(const Image& img, const SpatialParams& sp, const RangeParams& rp,
                  SpatialBackend backend, const GpfOptions& opts = {});
 

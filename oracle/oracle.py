@@ -164,9 +164,10 @@ class Reference:
         self.lib.gpf_set_num_threads(n)
 
     def gpf(self, img: np.ndarray, sigma_s: float, sigma_r: float, degree: int = 20,
-            centering: int = 1, kernel_scale: float = 1.0, backend: int = 1):
+            centering: int = 1, kernel_scale: float = 1.0, backend: int = 1,
+            window_radius: int = 0, boundary: int = 0):
         """Returns (status, out or None, fallback_count)."""
-        sp = self.SpatialParams(sigma_s, 0, 0, kernel_scale)
+        sp = self.SpatialParams(sigma_s, window_radius, boundary, kernel_scale)
         rp = self.RangeParams(sigma_r, degree)
         src = self._img(img)
         out = C.c_void_p()
@@ -193,6 +194,31 @@ class Reference:
         if st != 0:
             return st, None
         return st, {"mse": rep.mse, "mse_db": rep.mse_db, "max_abs": rep.max_abs, "pixels": rep.pixels}
+
+    def gaussian_direct(self, img: np.ndarray, sigma_s: float, window_radius: int = 0,
+                        boundary: int = 0, kernel_scale: float = 1.0):
+        """Reference gpf_gaussian_direct (capi.cpp:209-217): (status, out or None)."""
+        self.lib.gpf_gaussian_direct.argtypes = [C.c_void_p, C.c_void_p, C.POINTER(C.c_void_p)]
+        sp = self.SpatialParams(sigma_s, window_radius, boundary, kernel_scale)
+        src = self._img(img)
+        out = C.c_void_p()
+        st = self.lib.gpf_gaussian_direct(src, C.byref(sp), C.byref(out))
+        self.lib.gpf_image_destroy(src)
+        if st != 0:
+            return st, None
+        return st, self._take(out, img.shape)
+
+    def kernel(self, name: str, *args):
+        """Reference gpf_kernel_<name> (capi.cpp:230-286) with the C argument order:
+        (status, value)."""
+        fn = getattr(self.lib, "gpf_kernel_" + name)
+        sig = {"gauss": [C.c_double] * 3, "gauss_poly": [C.c_double] * 3 + [C.c_int],
+               "taylor": [C.c_double] * 3 + [C.c_int],
+               "sup_error": [C.c_double, C.c_int] + [C.c_double] * 4 + [C.c_int]}[name]
+        fn.argtypes = sig + [C.POINTER(C.c_double)]
+        v = C.c_double(float("nan"))
+        st = fn(*args, C.byref(v))
+        return st, v.value
 
     def taylor(self, img: np.ndarray, sigma_s: float, sigma_r: float, degree: int = 20,
                backend: int = 1):

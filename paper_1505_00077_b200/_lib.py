@@ -31,7 +31,8 @@ EXPORTED = (
     "gpf_image_create", "gpf_image_destroy", "gpf_image_width", "gpf_image_height",
     "gpf_image_data", "gpf_image_cdata",
     "gpf_spatial_params_init", "gpf_range_params_init",
-    "gpf_filter_gpf", "gpf_gaussian_recursive", "gpf_filter_exact", "gpf_compare",
+    "gpf_filter_gpf", "gpf_gaussian_recursive", "gpf_gaussian_direct", "gpf_filter_exact", "gpf_compare",
+    "gpf_kernel_gauss", "gpf_kernel_gauss_poly", "gpf_kernel_taylor", "gpf_kernel_sup_error",
     "gpf_filter_taylor", "gpf_read_pgm", "gpf_decode_pgm", "gpf_write_pgm", "gpf_encode_pgm",
     "gpf_free_bytes",
     "gpf_set_num_threads", "gpf_get_num_threads",
@@ -90,6 +91,13 @@ def _declare(lib: C.CDLL) -> C.CDLL:
     lib.gpf_filter_gpf.argtypes = [vp, C.POINTER(SpatialParams), C.POINTER(RangeParams), C.c_int,
                                    C.c_int, C.POINTER(C.c_longlong), pvp]
     lib.gpf_gaussian_recursive.argtypes = [vp, C.c_double, C.c_double, pvp]
+    lib.gpf_gaussian_direct.argtypes = [vp, C.POINTER(SpatialParams), pvp]
+    pd = C.POINTER(C.c_double)
+    lib.gpf_kernel_gauss.argtypes = [C.c_double, C.c_double, C.c_double, pd]
+    lib.gpf_kernel_gauss_poly.argtypes = [C.c_double, C.c_double, C.c_double, C.c_int, pd]
+    lib.gpf_kernel_taylor.argtypes = [C.c_double, C.c_double, C.c_double, C.c_int, pd]
+    lib.gpf_kernel_sup_error.argtypes = [C.c_double, C.c_int, C.c_double, C.c_double, C.c_double,
+                                         C.c_double, C.c_int, pd]
     lib.gpf_filter_exact.argtypes = [vp, C.POINTER(SpatialParams), C.POINTER(RangeParams), pvp]
     lib.gpf_read_pgm.argtypes = [C.c_char_p, pvp]
     lib.gpf_decode_pgm.argtypes = [C.c_void_p, C.c_size_t, pvp]

@@ -176,11 +176,8 @@ gpfb::Params validate(int w, int h, const gpf_spatial_params& sp, const gpf_rang
   // RangeParams::validate (range_kernel.cpp:22-29)
   if (!(rp.sigma_r > 0.0)) invalid("RangeParams: sigma_r must be > 0");
   if (rp.degree < 0) invalid("RangeParams: degree must be >= 0");
-  if (backend == GPF_BACKEND_DIRECT)
-    invalid("the direct (windowed) backend is not provided by the B200 library; "
-            "use GPF_BACKEND_RECURSIVE");
-  // recursive_gaussian (spatial.cpp:222-230)
-  if (sp.sigma_s < 0.5)
+  // recursive_gaussian (spatial.cpp:222-230); the direct backend takes any sigma_s > 0
+  if (backend == GPF_BACKEND_RECURSIVE && sp.sigma_s < 0.5)
     throw gpfb::Error{GPF_ERR_SIGMA_TOO_SMALL,
                       "recursive_gaussian: sigma_s < 0.5 is not supported; use the direct backend"};
   if (rp.degree > max_degree)
@@ -196,6 +193,9 @@ gpfb::Params validate(int w, int h, const gpf_spatial_params& sp, const gpf_rang
   p.sigma_r = rp.sigma_r;
   p.degree = rp.degree;
   p.centering = centering != 0 ? 1 : 0;
+  p.backend = backend == GPF_BACKEND_DIRECT ? 0 : 1;
+  p.window_radius = radius;
+  p.boundary = static_cast<int>(sp.boundary);
   return p;
 }
 
@@ -347,6 +347,34 @@ gpf_status gpf_filter_gpf(const gpf_image* in, const gpf_spatial_params* sp,
     *out = hold.release();
   });
 }
+gpf_status gpf_gaussian_direct(const gpf_image* in, const gpf_spatial_params* sp, gpf_image** out) {
+  if (in == nullptr || sp == nullptr || out == nullptr)
+    return fail(GPF_ERR_INVALID_ARGUMENT, "null argument");
+  *out = nullptr;
+  return guarded([&] {
+    // to_spatial (capi.cpp:65-80), SpatialParams::validate (spatial.cpp:25-35)
+    if (sp->boundary != GPF_BOUNDARY_REPLICATE && sp->boundary != GPF_BOUNDARY_REFLECT &&
+        sp->boundary != GPF_BOUNDARY_ZERO)
+      invalid("boundary must be replicate, reflect, or zero");
+    const int radius =
+        sp->window_radius > 0 ? sp->window_radius : gpfb::default_window_radius(sp->sigma_s);
+    if (!(sp->sigma_s > 0.0)) invalid("SpatialParams: sigma_s must be > 0");
+    if (radius < 1) invalid("SpatialParams: window_radius must be >= 1");
+    if (!(sp->kernel_scale > 0.0)) invalid("SpatialParams: kernel_scale must be > 0");
+    current_device();
+    const size_t n = (size_t)in->w * in->h;
+    DevBuf din(n * sizeof(double)), dtmp(n * sizeof(double));
+    cuda_check(cudaMemcpy(din.p, in->px, n * sizeof(double), cudaMemcpyHostToDevice), "H2D");
+    gpfb::run_direct_gaussian_f64(static_cast<const double*>(din.p), static_cast<double*>(din.p),
+                                  static_cast<double*>(dtmp.p), in->w, in->h, 1, sp->sigma_s,
+                                  sp->kernel_scale, radius, static_cast<int>(sp->boundary), nullptr);
+    auto* res = new gpf_image(in->w, in->h);
+    std::unique_ptr<gpf_image> hold(res);
+    cuda_check(cudaMemcpy(res->px, din.p, n * sizeof(double), cudaMemcpyDeviceToHost), "D2H");
+    *out = hold.release();
+  });
+}
+
 gpf_status gpf_gaussian_recursive(const gpf_image* in, double sigma_s, double kernel_scale,
                                   gpf_image** out) {
   if (in == nullptr || out == nullptr) return fail(GPF_ERR_INVALID_ARGUMENT, "null argument");
@@ -385,8 +413,7 @@ gpf_status gpf_filter_taylor(const gpf_image* in, const gpf_spatial_params* sp,
     const size_t n = (size_t)in->w * in->h;
     DevBuf din(n * sizeof(double)), dout(n * sizeof(double)), dfb(sizeof(unsigned long long));
     cuda_check(cudaMemcpy(din.p, in->px, n * sizeof(double), cudaMemcpyHostToDevice), "H2D");
-    gpfb::run_taylor_f64(static_cast<const double*>(din.p), static_cast<double*>(dout.p), in->w, in->h,
-                         p.sigma_s, p.kernel_scale, p.sigma_r, p.degree,
+    gpfb::run_taylor_f64(static_cast<const double*>(din.p), static_cast<double*>(dout.p), p,
                          static_cast<unsigned long long*>(dfb.p), nullptr);
     auto* res = new gpf_image(in->w, in->h);
     std::unique_ptr<gpf_image> hold(res);
@@ -416,6 +443,33 @@ gpf_status gpf_filter_exact(const gpf_image* in, const gpf_spatial_params* sp,
     std::unique_ptr<gpf_image> hold(res);
     cuda_check(cudaMemcpy(res->px, dout.p, n * sizeof(double), cudaMemcpyDeviceToHost), "D2H");
     *out = hold.release();
+  });
+}
+
+// ------------------------------------------------- range-kernel evaluators
+gpf_status gpf_kernel_gauss(double t, double tau, double sigma_r, double* out) {
+  if (out == nullptr) return fail(GPF_ERR_INVALID_ARGUMENT, "out is null");
+  return guarded([&] { *out = gpfb::kernel_gauss(t, tau, sigma_r); });
+}
+
+gpf_status gpf_kernel_gauss_poly(double t, double tau, double sigma_r, int degree, double* out) {
+  if (out == nullptr) return fail(GPF_ERR_INVALID_ARGUMENT, "out is null");
+  return guarded([&] { *out = gpfb::kernel_gauss_poly(t, tau, sigma_r, degree); });
+}
+
+gpf_status gpf_kernel_taylor(double t, double tau, double sigma_r, int degree, double* out) {
+  if (out == nullptr) return fail(GPF_ERR_INVALID_ARGUMENT, "out is null");
+  return guarded([&] { *out = gpfb::kernel_taylor(t, tau, sigma_r, degree); });
+}
+
+gpf_status gpf_kernel_sup_error(double sigma_r, int degree, double tau, double low, double high,
+                                double step, gpf_range_approx which, double* out) {
+  if (out == nullptr) return fail(GPF_ERR_INVALID_ARGUMENT, "out is null");
+  return guarded([&] {
+    if (which != GPF_RANGE_APPROX_GAUSS_POLY && which != GPF_RANGE_APPROX_TAYLOR)
+      invalid("which must be gauss_poly or taylor");
+    *out = gpfb::kernel_sup_error(sigma_r, degree, tau, low, high, step,
+                                  which == GPF_RANGE_APPROX_TAYLOR);
   });
 }
 

@@ -45,16 +45,15 @@ FilterResult gpf(const Image& img, const SpatialParams& sp, const RangeParams& r
   if (!(opts.range.low < opts.range.high))
     throw std::invalid_argument("GpfOptions: range.low must be < range.high");
   if (img.pixels() == 0) throw std::invalid_argument("Image dimensions must be >= 1");
-  // apply_spatial (bilateral.cpp:58-62) -> recursive_gaussian (spatial.cpp:222-230)
-  if (backend == SpatialBackend::direct)
-    throw std::invalid_argument(
-        "the direct (windowed) backend is not provided by the B200 library; use "
-        "SpatialBackend::recursive");
-  if (!(sp.sigma_s > 0.0) || !(sp.kernel_scale > 0.0))
-    throw std::invalid_argument("recursive_gaussian: sigma_s and kernel_scale must be > 0");
-  if (sp.sigma_s < 0.5)
-    throw SigmaTooSmallError(
-        "recursive_gaussian: sigma_s < 0.5 is not supported; use the direct backend");
+  // apply_spatial (bilateral.cpp:58-62): direct_gaussian (spatial.cpp:112-129)
+  // or recursive_gaussian (spatial.cpp:222-230)
+  if (backend == SpatialBackend::recursive) {
+    if (!(sp.sigma_s > 0.0) || !(sp.kernel_scale > 0.0))
+      throw std::invalid_argument("recursive_gaussian: sigma_s and kernel_scale must be > 0");
+    if (sp.sigma_s < 0.5)
+      throw SigmaTooSmallError(
+          "recursive_gaussian: sigma_s < 0.5 is not supported; use the direct backend");
+  }
   if (rp.degree > gpfb::kMaxDegreeF64)
     throw std::invalid_argument("RangeParams: degree must be <= " +
                                 std::to_string(gpfb::kMaxDegreeF64) + " in the B200 library");
@@ -65,6 +64,9 @@ FilterResult gpf(const Image& img, const SpatialParams& sp, const RangeParams& r
   p.kernel_scale = sp.kernel_scale;
   p.sigma_r = rp.sigma_r;
   p.degree = rp.degree;
+  p.backend = backend == SpatialBackend::direct ? 0 : 1;
+  p.window_radius = sp.window_radius;
+  p.boundary = static_cast<int>(sp.boundary);
   // t_c (bilateral.cpp:77-82): mean, midpoint (low + high) / 2, or 0
   p.centering = !opts.centering ? 0 : (opts.mode == CenteringMode::mean ? 1 : 2);
   p.tc_fixed = (opts.range.low + opts.range.high) / 2.0;

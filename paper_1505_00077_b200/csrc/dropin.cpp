@@ -301,6 +301,12 @@ long long dropin_gpf(const double* h_in, double* h_out, const Params& p) {
   DevCtx& c = context(dev);
   const long long n = (long long)p.width * p.height;
   int mode = get_precision();
+  if (p.backend == 0) {
+    // the windowed backend exists in the reference-exact fp64 mode only
+    if (mode == kPrecFp32)
+      throw Error{1, "the direct (windowed) backend runs in the fp64 precision mode only"};
+    mode = kPrecFp64;
+  }
   if (mode == kPrecFp32 && p.degree > kMaxDegreeF32)
     throw Error{1, "RangeParams: degree must be <= " + std::to_string(kMaxDegreeF32) +
                        " with the fp32 precision mode"};

@@ -821,14 +821,23 @@ void run_gpf_f64_exact(const double* d_in, double* d_out, const Params& p, F64Wo
   // GpfState::init: inv2s2 = 1.0 / (2.0 * sr * sr) (bilateral.cpp:92)
   const double inv2s2 = 1.0 / (2.0 * p.sigma_r * p.sigma_r);
   k_f64_prologue<<<blocks, 256, 0, st>>>(d_in, scalars, H, F0, n, p.sigma_r, inv2s2);
-  Deriche64 k;
-  deriche_coeffs_f64(p.sigma_s, k.nc, k.na, k.d);
+  if (p.backend == 0) {
+    // SpatialBackend::direct: the planes are materialised (into C), filtered
+    // rows-then-columns by the windowed passes (C -> R -> C)
+    direct_gen_planes_f64(H, F0, Cb, n, planes, st);
+    run_direct_gaussian_f64(Cb, Cb, R, w, h, planes, p.sigma_s, p.kernel_scale, p.window_radius,
+                            p.boundary, st);
+  }
+  Deriche64 k = {};
+  if (p.backend != 0) deriche_coeffs_f64(p.sigma_s, k.nc, k.na, k.d);
   k.den = 1.0 + k.d[0] + k.d[1] + k.d[2] + k.d[3];
   k.csum = k.nc[0] + k.nc[1] + k.nc[2] + k.nc[3];
   k.asum = k.na[0] + k.na[1] + k.na[2] + k.na[3];
   const double mass = kernel_mass_1d(p.sigma_s, default_window_radius(p.sigma_s));
   const double scale = mass * mass * p.kernel_scale;
-  if (f64_sequential()) {
+  if (p.backend == 0) {
+    // filtered above
+  } else if (f64_sequential()) {
     k_f64_rows<<<dim3((h + kRowT - 1) / kRowT, (planes + kGP - 1) / kGP), kRowT, 0, st>>>(H, F0, R, w, h,
                                                                                           planes, k);
     k_f64_cols<<<dim3((w + 127) / 128, planes), 128, 0, st>>>(R, Cb, w, h, k, scale);

@@ -110,6 +110,10 @@ struct Params {
   double sigma_s = 2.0, kernel_scale = 1.0, sigma_r = 30.0;
   int degree = 20, centering = 1;  // centering: 0 none, 1 mean, 2 fixed t_c = tc_fixed
   double tc_fixed = 0.0;           // CenteringMode::midpoint: (range.low + range.high) / 2
+  // apply_spatial (bilateral.cpp:58-62): 1 recursive (the hot path), 0 direct
+  // (windowed, fp64 mode only: window_radius taps per side, boundary 0
+  // replicate / 1 reflect / 2 zero)
+  int backend = 1, window_radius = 0, boundary = 0;
 };
 
 // Host-side constant builders (coeffs.cpp).
@@ -205,8 +209,7 @@ ErrorStats compare_f64(const double* d_ref, const double* d_test, int w, int h, 
                        cudaStream_t st);
 // Taylor-polynomial baseline (taylor_bilateral, bilateral.cpp:160-220), fp64,
 // bitwise equal to the reference; *d_fb receives the fallback count (taylor.cu).
-void run_taylor_f64(const double* d_in, double* d_out, int w, int h, double sigma_s,
-                    double kernel_scale, double sigma_r, int degree, unsigned long long* d_fb,
+void run_taylor_f64(const double* d_in, double* d_out, const Params& p, unsigned long long* d_fb,
                     cudaStream_t st);
 // t_c of one fp64 frame (K0 double-double mean; 0 / tc_fixed per centering) into
 // scalars[0];
@@ -254,5 +257,21 @@ void dropin_release();
 // Single-plane recursive Gaussian (gpf_gaussian_recursive), fp64 in/out.
 void run_gaussian_f64(const double* d_in, double* d_out, double* d_tmp, int w, int h,
                       double sigma_s, double scale, cudaStream_t st);
+
+// The direct (windowed) backend in fp64 (direct.cu): `planes` images of w x h
+// (plane stride w h) d_src -> d_dst through d_tmp (d_dst may alias d_src),
+// bitwise the reference's direct_gaussian (spatial.cpp:112-129).
+void run_direct_gaussian_f64(const double* d_src, double* d_dst, double* d_tmp, int w, int h,
+                             int planes, double sigma_s, double kernel_scale, int window_radius,
+                             int boundary, cudaStream_t st);
+// Scalar range-kernel evaluators (range_kernel.cpp; host fp64, throw Error{1, ...})
+double kernel_gauss(double t, double tau, double sigma_r);
+double kernel_gauss_poly(double t, double tau, double sigma_r, int degree);
+double kernel_taylor(double t, double tau, double sigma_r, int degree);
+double kernel_sup_error(double sigma_r, int degree, double tau, double low, double high, double step,
+                        int taylor);
+// F[p] = H^p F0, p < planes, by step()'s multiply chain (bilateral.cpp:108-129)
+void direct_gen_planes_f64(const double* H, const double* F0, double* F, long long n, int planes,
+                           cudaStream_t st);
 
 }  // namespace gpfb

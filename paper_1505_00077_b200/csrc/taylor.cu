@@ -91,9 +91,10 @@ void check_(cudaError_t e, const char* what) {
 
 // d_in (w x h fp64) -> d_out; d_fb (one counter, zeroed here); workspace
 // allocated here: (2K+2) filtered moments + two moment/temp planes.
-void run_taylor_f64(const double* d_in, double* d_out, int w, int h, double sigma_s,
-                    double kernel_scale, double sigma_r, int degree,
-                    unsigned long long* d_fb, cudaStream_t st) {
+void run_taylor_f64(const double* d_in, double* d_out, const Params& p, unsigned long long* d_fb,
+                    cudaStream_t st) {
+  const int w = p.width, h = p.height, degree = p.degree;
+  const double sigma_s = p.sigma_s, kernel_scale = p.kernel_scale, sigma_r = p.sigma_r;
   const long long n = (long long)w * h;
   const int K = degree / 2;
   const int planes = 2 * K + 2;
@@ -112,7 +113,12 @@ void run_taylor_f64(const double* d_in, double* d_out, int w, int h, double sigm
   const int blocks = (int)std::min<long long>((n + 255) / 256, 148 * 8);
   k_fill<<<blocks, 256, 0, st>>>(mom, 1.0, n);
   for (int m = 0; m < planes; ++m) {
-    run_gaussian_f64(mom, mbar + (size_t)m * n, tmp, w, h, sigma_s, scale, st);
+    // filt (bilateral.cpp:168-172)
+    if (p.backend == 0)
+      run_direct_gaussian_f64(mom, mbar + (size_t)m * n, tmp, w, h, 1, sigma_s, kernel_scale,
+                              p.window_radius, p.boundary, st);
+    else
+      run_gaussian_f64(mom, mbar + (size_t)m * n, tmp, w, h, sigma_s, scale, st);
     if (m + 1 < planes) {
       k_moment_next<<<blocks, 256, 0, st>>>(d_in, mom, mom2, n);
       std::swap(mom, mom2);

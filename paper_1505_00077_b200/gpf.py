@@ -113,6 +113,47 @@ def gpf_gaussian_recursive(img: np.ndarray, sigma_s: float, kernel_scale: float 
     return Image(out).numpy()
 
 
+def gpf_gaussian_direct(img: np.ndarray, sp: SpatialParams | None = None) -> np.ndarray:
+    """Single-plane windowed Gaussian (reference gpf_gaussian_direct), fp64 on the GPU."""
+    sp = sp or spatial_params()
+    src = Image.from_array(img)
+    out = C.c_void_p()
+    _check(_lib.lib().gpf_gaussian_direct(src.h, C.byref(sp), C.byref(out)))
+    return Image(out).numpy()
+
+
+GPF_RANGE_APPROX_GAUSS_POLY, GPF_RANGE_APPROX_TAYLOR = 0, 1
+
+
+def kernel_gauss(t: float, tau: float, sigma_r: float) -> float:
+    """exp(-(t - tau)^2 / 2 sigma_r^2) (reference gpf_kernel_gauss)."""
+    v = C.c_double()
+    _check(_lib.lib().gpf_kernel_gauss(t, tau, sigma_r, C.byref(v)))
+    return v.value
+
+
+def kernel_gauss_poly(t: float, tau: float, sigma_r: float, degree: int) -> float:
+    """Degree-N Gauss-polynomial range kernel (reference gpf_kernel_gauss_poly)."""
+    v = C.c_double()
+    _check(_lib.lib().gpf_kernel_gauss_poly(t, tau, sigma_r, degree, C.byref(v)))
+    return v.value
+
+
+def kernel_taylor(t: float, tau: float, sigma_r: float, degree: int) -> float:
+    """Degree-N Taylor range kernel (reference gpf_kernel_taylor)."""
+    v = C.c_double()
+    _check(_lib.lib().gpf_kernel_taylor(t, tau, sigma_r, degree, C.byref(v)))
+    return v.value
+
+
+def kernel_sup_error(sigma_r: float, degree: int, tau: float, low: float, high: float, step: float,
+                     which: int = GPF_RANGE_APPROX_GAUSS_POLY) -> float:
+    """sup |exact - approximation| over the closed grid (reference gpf_kernel_sup_error)."""
+    v = C.c_double()
+    _check(_lib.lib().gpf_kernel_sup_error(sigma_r, degree, tau, low, high, step, which, C.byref(v)))
+    return v.value
+
+
 def gpf_filter_taylor(img: np.ndarray, sp: SpatialParams | None = None, rp: RangeParams | None = None,
                       backend: int = GPF_BACKEND_RECURSIVE):
     """Taylor-polynomial baseline (reference gpf_filter_taylor), on the GPU.

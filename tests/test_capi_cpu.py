@@ -86,7 +86,8 @@ def _call(img, sp, rp, backend=1, centering=1, out_ptr=True):
     (dict(degree=63), 1, "degree"),
     (dict(boundary=9), 1, "boundary"),
     (dict(backend=7), 1, "backend"),
-    (dict(backend=0), 1, "direct"),
+    (dict(backend=0, sigma_s=0.0), 1, "sigma_s"),
+    (dict(backend=0, degree=-1), 1, "degree"),
     (dict(sigma_s=0.49), 3, "direct"),
     (dict(sigma_s=0.3), 3, "direct"),
 ])
@@ -99,6 +100,32 @@ def test_validation_statuses(case, status, needle):
     assert needle in msg
     assert out.value is None          # *out set to NULL before work
     assert fb.value == -7             # fallback_count untouched on error
+
+
+def test_direct_backend_passes_validation():
+    """GPF_BACKEND_DIRECT is provided (fp64 mode on the GPU) and takes any
+    sigma_s > 0: validation passes, so the only failure left is a missing
+    device (no CPU path: GPF_ERR_UNKNOWN, never INVALID_ARGUMENT / SIGMA_TOO_SMALL)."""
+    sp, rp = gpf.spatial_params(0.3), gpf.range_params(30.0, 4)
+    st, out, fb, msg = _call(np.zeros((8, 8)), sp, rp, backend=0)
+    assert st in (0, 9), (st, msg)
+    if st != 0:
+        assert "CUDA" in msg and out.value is None
+
+
+def test_gaussian_direct_and_kernel_null_and_validation():
+    L = _lib.lib()
+    src = gpf.Image.from_array(np.ones((8, 8)))
+    out = C.c_void_p(1)
+    sp = gpf.spatial_params(2.0)
+    assert L.gpf_gaussian_direct(None, C.byref(sp), C.byref(out)) == 1
+    assert L.gpf_gaussian_direct(src.h, None, C.byref(out)) == 1
+    assert L.gpf_gaussian_direct(src.h, C.byref(sp), None) == 1
+    for bad, needle in [(gpf.spatial_params(0.0), "sigma_s"), (gpf.spatial_params(2.0, kernel_scale=-1.0), "kernel_scale"),
+                        (gpf.spatial_params(2.0, boundary=5), "boundary")]:
+        out = C.c_void_p(1)
+        assert L.gpf_gaussian_direct(src.h, C.byref(bad), C.byref(out)) == 1
+        assert needle in L.gpf_last_error().decode() and out.value is None
 
 
 def test_null_arguments():

@@ -67,10 +67,28 @@ def test_empty_image_rejected_like_reference():
     assert ref == ours == ("invalid_argument", "Image dimensions must be >= 1")
 
 
-def test_direct_backend_is_not_provided():
+def test_direct_backend_validates_like_reference():
+    """SpatialBackend::direct: same parameter exceptions as the reference, and
+    no SigmaTooSmallError below 0.5 (only the recursive backend has that limit)."""
     img = synth.rects_image(16, 12, 2, 10.0, 1).astype(np.float64)
-    kind, msg = drive(OURS, img, backend="direct")
-    assert kind == "invalid_argument" and "direct" in msg and "recursive" in msg
+    for case in [dict(ss=0.0), dict(radius=0), dict(ks=0.0), dict(deg=-1)]:
+        ref = drive(REF, img, backend="direct", **case)
+        ours = drive(OURS, img, backend="direct", **case)
+        assert isinstance(ref[0], str) and ref == ours, (ref, ours)
+    ours = drive(OURS, img, backend="direct", ss=0.4)
+    assert ours[0] not in ("SigmaTooSmallError", "invalid_argument"), ours
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("case", [dict(ss=2.0, radius=6), dict(ss=0.4, radius=2),
+                                  dict(ss=3.0, radius=9, mode="midpoint", ks=0.5)])
+def test_direct_backend_matches_reference_core(case):
+    """gpfilter::gpf(..., SpatialBackend::direct) against the reference's C++ core."""
+    img = synth.rects_image(40, 28, 3, 10.0, 5).astype(np.float64)
+    rfb, ref = drive(REF, img, backend="direct", **case)
+    fb, out = drive(OURS, img, backend="direct", **case)
+    assert fb == rfb
+    assert np.abs(out - ref).max() <= 1e-9
 
 
 @pytest.mark.gpu

@@ -35,6 +35,20 @@ def test_taylor_fallbacks_and_constant(gpu, reference):
     assert fb == rfb
 
 
-def test_taylor_direct_backend_rejected(gpu):
-    with pytest.raises(gpu.GpfError, match="direct"):
-        gpu.gpf_filter_taylor(np.zeros((4, 4)), backend=0)
+@pytest.mark.parametrize("degree,ss,radius,boundary", [(4, 2.0, 0, 0), (10, 0.4, 2, 1), (20, 3.0, 5, 2)])
+def test_taylor_direct_backend_bitwise_vs_reference(gpu, reference, degree, ss, radius, boundary):
+    """filt = direct_gaussian (bilateral.cpp:168-172)."""
+    img = synth.rects_image(41, 30, 5, 10.0, 3 + degree).astype(np.float64)
+    sp = reference.SpatialParams(ss, radius, boundary, 1.0)
+    rp = reference.RangeParams(30.0, degree)
+    import ctypes as C
+    src, outp, rfb = reference._img(img), C.c_void_p(), C.c_longlong(-1)
+    reference.lib.gpf_filter_taylor.argtypes = [C.c_void_p, C.c_void_p, C.c_void_p, C.c_int,
+                                                C.POINTER(C.c_longlong), C.POINTER(C.c_void_p)]
+    assert reference.lib.gpf_filter_taylor(src, C.byref(sp), C.byref(rp), 0, C.byref(rfb), C.byref(outp)) == 0
+    reference.lib.gpf_image_destroy(src)
+    ref = reference._take(outp, img.shape)
+    out, fb = gpu.gpf_filter_taylor(img, gpu.spatial_params(ss, radius, boundary), gpu.range_params(30.0, degree),
+                                    backend=0)
+    assert fb == rfb.value
+    np.testing.assert_array_equal(out, ref)
