@@ -1,11 +1,11 @@
 // gpf_b200: command-line front end of libgpfilter_b200 with the reference CLI's
-// `filter`, `compare` and `bench` subcommands (proj/tools/gpf_cli.cpp:53-110,
-// 112-137, 200-285): same flags, same CSV protocol
+// `filter`, `compare`, `kernel-error` and `bench` subcommands
+// (proj/tools/gpf_cli.cpp:53-110, 112-137, 145-199, 200-285; SURVEY.md 8(f)
+// row 4): same flags, same CSV protocol
 //   method,backend,sigma_s,sigma_r,degree,pixels,repeats,median_seconds
 // (only the filter call inside the clock; warm-up runs discarded; median of
-// the timed runs), same "error: <flag>: <detail>" diagnostics. The
-// `kernel-error` subcommand belongs to the range-kernel evaluators, which the
-// B200 library does not provide.
+// the timed runs), same "error: <flag>: <detail>" diagnostics;
+// `kernel-error` writes "tau,approx,sup_error" rows.
 #include <algorithm>
 #include <chrono>
 #include <cmath>
@@ -186,6 +186,49 @@ int cmd_compare(const Args& a) {
   return 0;
 }
 
+// kernel-error: sup |exact - approximation| of the range kernel per tau
+// (reference gpf kernel-error, proj/tools/gpf_cli.cpp:145-199): CSV
+// "tau,approx,sup_error", approx in {gp, taylor}, rows in tau order, gp first.
+int cmd_kernel_error(const Args& a) {
+  for (const char* k : {"--sigma-r", "--degree", "--tau-list", "--range", "--step", "--which", "--csv"})
+    if (!a.has(k)) return fail(k, "is required");
+  double sigma_r, step, lo, hi;
+  int degree;
+  if (!to_double(a.str("--sigma-r"), &sigma_r) || !(sigma_r > 0)) return fail("--sigma-r", "must be a positive number");
+  if (!to_int(a.str("--degree"), &degree) || degree < 0) return fail("--degree", "must be a non-negative integer");
+  if (!to_double(a.str("--step"), &step) || !(step > 0)) return fail("--step", "must be a positive number");
+  const std::string which = a.str("--which");
+  if (which != "gp" && which != "taylor" && which != "both") return fail("--which", "must be one of gp, taylor, both");
+  std::vector<double> taus;
+  for (const auto& t : split(a.str("--tau-list"))) {
+    double v;
+    if (!to_double(t, &v)) return fail("--tau-list", "must be numbers");
+    taus.push_back(v);
+  }
+  const std::string range = a.str("--range");
+  const size_t colon = range.find(':');
+  if (colon == std::string::npos || !to_double(range.substr(0, colon), &lo) ||
+      !to_double(range.substr(colon + 1), &hi) || !(lo < hi))
+    return fail("--range", "expected LO:HI with LO < HI");
+  FILE* csv = std::fopen(a.str("--csv").c_str(), "w");
+  if (!csv) return fail("--csv", "cannot open for writing");
+  std::fprintf(csv, "tau,approx,sup_error\n");
+  for (const double tau : taus) {
+    for (const gpf_range_approx ap : {GPF_RANGE_APPROX_GAUSS_POLY, GPF_RANGE_APPROX_TAYLOR}) {
+      if (which != "both" && (which == "gp") != (ap == GPF_RANGE_APPROX_GAUSS_POLY)) continue;
+      double sup = 0.0;
+      if (gpf_kernel_sup_error(sigma_r, degree, tau, lo, hi, step, ap, &sup) != GPF_OK) {
+        std::fclose(csv);
+        return fail("--range", gpf_last_error());
+      }
+      std::fprintf(csv, "%s,%s,%s\n", num(tau).c_str(), ap == GPF_RANGE_APPROX_GAUSS_POLY ? "gp" : "taylor",
+                   num(sup).c_str());
+    }
+  }
+  if (std::fclose(csv) != 0) return fail("--csv", "write failure");
+  return 0;
+}
+
 int cmd_bench(const Args& a) {
   for (const char* k : {"--input", "--method", "--sigma-s-list", "--sigma-r", "--degree", "--backend", "--csv"})
     if (!a.has(k)) return fail(k, "is required");
@@ -254,13 +297,15 @@ int cmd_bench(const Args& a) {
 
 void usage() {
   std::fprintf(stderr,
-               "usage: gpf_b200 {filter|compare|bench} --flag value ...\n"
+               "usage: gpf_b200 {filter|compare|kernel-error|bench} --flag value ...\n"
                "  filter  --input P --output P --method exact|gpf|taylor --sigma-s S --sigma-r R\n"
-               "          [--degree N] [--backend recursive] [--window W] [--boundary B]\n"
+               "          [--degree N] [--backend recursive|direct] [--window W] [--boundary B]\n"
                "          [--no-centering] [--threads T]\n"
                "  compare --ref P --test P [--exclude-border B]\n"
+               "  kernel-error --sigma-r R --degree N --tau-list T[,T..] --range LO:HI --step S\n"
+               "          --which gp|taylor|both --csv P\n"
                "  bench   --input P --method M[,M..] --sigma-s-list S[,S..] --sigma-r R --degree N\n"
-               "          --backend recursive --csv P [--repeats K] [--warmup W] [--threads T]\n");
+               "          --backend recursive|direct --csv P [--repeats K] [--warmup W] [--threads T]\n");
 }
 
 }  // namespace
@@ -280,8 +325,7 @@ int main(int argc, char** argv) {
   if (cmd == "filter") return cmd_filter(a);
   if (cmd == "compare") return cmd_compare(a);
   if (cmd == "bench") return cmd_bench(a);
-  if (cmd == "kernel-error")
-    return fail("kernel-error", "the range-kernel evaluators are not provided by the B200 library");
+  if (cmd == "kernel-error") return cmd_kernel_error(a);
   usage();
   return 1;
 }

@@ -38,8 +38,31 @@ def test_cli_argument_errors(cli, tmp_path):
             "--degree", "20", "--backend", "recursive", "--csv", "o.csv")
     assert r.returncode == 1 and "--sigma-s-list" in r.stderr
     r = run("kernel-error")
-    assert r.returncode == 1 and "not provided" in r.stderr
+    assert r.returncode == 1 and "error: --sigma-r: is required" in r.stderr
+    r = run("kernel-error", "--sigma-r", "30", "--degree", "20", "--tau-list", "0,40", "--range", "255:0",
+            "--step", "1", "--which", "both", "--csv", str(tmp_path / "k.csv"))
+    assert r.returncode == 1 and "error: --range: expected LO:HI with LO < HI" in r.stderr
     assert run("--version").stdout.strip().endswith("b200")
+
+
+def test_cli_kernel_error_csv(cli, reference, tmp_path):
+    """kernel-error (host only): the reference CLI's CSV (proj/tools/gpf_cli.cpp:165-199),
+    values equal to the reference library's gpf_kernel_sup_error."""
+    path = tmp_path / "k.csv"
+    r = run("kernel-error", "--sigma-r", "30", "--degree", "12", "--tau-list", "0,40,-100.5", "--range",
+            "0:255", "--step", "0.5", "--which", "both", "--csv", str(path))
+    assert r.returncode == 0, r.stderr
+    rows = list(csv.reader(open(path)))
+    assert rows[0] == ["tau", "approx", "sup_error"]
+    assert [(a, b) for a, b, _ in rows[1:]] == [("0.0", "gp"), ("0.0", "taylor"), ("40.0", "gp"), ("40.0", "taylor"),
+                                                ("-100.5", "gp"), ("-100.5", "taylor")]
+    for tau, ap, v in rows[1:]:
+        st, want = reference.kernel("sup_error", 30.0, 12, float(tau), 0.0, 255.0, 0.5, 0 if ap == "gp" else 1)
+        assert st == 0 and float(v) == want
+    assert rows[1][2] == "0.0"
+    r = run("kernel-error", "--sigma-r", "30", "--degree", "12", "--tau-list", "40", "--range", "0:255",
+            "--step", "1", "--which", "taylor", "--csv", str(path))
+    assert r.returncode == 0 and [x[1] for x in csv.reader(open(path))][1:] == ["taylor"]
 
 
 @pytest.mark.gpu
@@ -76,3 +99,12 @@ def test_cli_filter_compare_bench(cli, gpu, reference, tmp_path):
                                               ("exact", "4.5"), ("taylor", "2.0"), ("taylor", "4.5")]
     assert all(x[1] == "recursive" and x[3] == "30.0" and x[4] == "20" and x[5] == str(96 * 64)
                and x[6] == "2" and float(x[7]) > 0 for x in rows[1:])
+    # the direct backend through the CLI (reference flags --backend / --window / --boundary)
+    dout = tmp_path / "direct.pgm"
+    r = run("filter", "--input", str(src), "--output", str(dout), "--method", "gpf", "--sigma-s", "2",
+            "--sigma-r", "30", "--backend", "direct", "--window", "4", "--boundary", "reflect")
+    assert r.returncode == 0, r.stderr
+    st, ref, _ = reference.gpf(img, 2.0, 30.0, 20, backend=0, window_radius=4, boundary=1)
+    want = np.frombuffer(reference.encode_pgm(ref)[-96 * 64:], np.uint8).astype(int)
+    got = np.frombuffer(dout.read_bytes()[-96 * 64:], np.uint8).astype(int)
+    assert st == 0 and np.abs(got - want).max() <= 1 and (got == want).mean() > 0.999
