@@ -115,3 +115,123 @@ def test_recursive_tracks_wide_direct_window(gpu):
     rec = gpu.gpf_gaussian_recursive(img, ss)
     rel = np.abs(rec / mass9 ** 2 - wide / mass15 ** 2).max() / 255.0
     assert rel <= 5e-3, rel
+
+
+# --- the reference unit suite's direct-backend pins (proj/tests/test_bilateral.cpp), restated.
+# Inputs: the reference's own generators restated (proj/tests/noise.hpp): the pins on noise
+# images hold for those images, not for any image (the degree sweep below fails in the
+# reference itself on a numpy-normal image of the same moments).
+
+def _mt_uniform(seed, w, h, hi):
+    # proj/tests/noise.hpp:46-56 restated: mt19937, (x + 0.5) / 2^32 * hi, floored for hi > 1
+    raw = np.random.RandomState(seed).randint(0, 2**32, size=w * h, dtype=np.uint32).astype(np.float64)
+    u = (raw + 0.5) / 4294967296.0 * hi
+    return (np.floor(u) if hi > 1.0 else u).reshape(h, w)
+
+
+def _gauss_noise(seed, w, h, mean=128.0, sigma=40.0):
+    # proj/tests/noise.hpp:22-44 restated: Box-Muller pairs from the mt19937 stream,
+    # clamp(round(mean + sigma z)) to [0, 255]
+    n = w * h
+    m = n + (n & 1)
+    raw = np.random.RandomState(seed).randint(0, 2**32, size=m, dtype=np.uint32).astype(np.float64)
+    u = (raw + 0.5) / 4294967296.0
+    r = np.sqrt(-2.0 * np.log(u[0::2]))
+    z = np.empty(m)
+    z[0::2] = r * np.cos(6.283185307179586 * u[1::2])
+    z[1::2] = r * np.sin(6.283185307179586 * u[1::2])
+    return np.clip(np.floor(mean + sigma * z + 0.5), 0.0, 255.0)[:n].reshape(h, w)
+
+
+def _gpf_direct(gpu, img, ss=2.0, sr=30.0, deg=20, cen=1, ks=1.0, radius=0):
+    return gpu.gpf_filter_gpf(img, gpu.spatial_params(ss, radius, 0, ks), gpu.range_params(sr, deg),
+                              backend=0, centering=cen)
+
+
+def test_pin_constants_preserved_exactly(gpu):
+    """test_bilateral.cpp:141-152."""
+    out, fb = _gpf_direct(gpu, np.full((32, 32), 137.0))
+    assert fb == 0 and (out == 137.0).all()
+
+
+def test_pin_approaches_exact_for_large_sigma_r(gpu):
+    """test_bilateral.cpp:203-216: matched direct windows, sigma_r 80 -> <= -20 dB."""
+    img = _mt_uniform(2, 32, 32, 256.0)
+    ex = gpu.gpf_filter_exact(img, gpu.spatial_params(2.0), gpu.range_params(80.0))
+    out, fb = _gpf_direct(gpu, img, sr=80.0)
+    assert fb == 0 and gpu.gpf_compare(ex, out)["mse_db"] <= -20.0
+
+
+def test_pin_error_non_increasing_in_degree(gpu):
+    """test_bilateral.cpp:218-232."""
+    img = _gauss_noise(2, 32, 32)
+    ex = gpu.gpf_filter_exact(img, gpu.spatial_params(2.0), gpu.range_params(30.0))
+    prev = 1e300
+    for deg in (5, 10, 20, 30):
+        db = gpu.gpf_compare(ex, _gpf_direct(gpu, img, deg=deg)[0])["mse_db"]
+        assert db <= prev + 0.1
+        prev = db
+
+
+def test_pin_centering_consistency_bitwise(gpu, oracle):
+    """test_bilateral.cpp:234-258: centred == shift by t_c, centering off, add t_c back (bitwise)."""
+    img = _mt_uniform(13, 16, 16, 256.0)
+    out, fb = _gpf_direct(gpu, img)
+    t_c = oracle.mean(img)
+    raw, rfb = _gpf_direct(gpu, img - t_c, cen=0)
+    assert fb == rfb == 0
+    np.testing.assert_array_equal(out, raw + t_c)
+
+
+def test_pin_kernel_scale_invariance(gpu):
+    """test_bilateral.cpp:272-289: kernel_scale cancels in P/Q to 1e-10."""
+    img = _mt_uniform(43, 16, 16, 256.0)
+    base, _ = _gpf_direct(gpu, img)
+    scaled, _ = _gpf_direct(gpu, img, ks=5.25)
+    assert np.abs(base - scaled).max() <= 1e-10
+
+
+def test_pin_backends_agree_away_from_border(gpu):
+    """test_bilateral.cpp:291-315: direct (W = 4 sigma) vs recursive within 0.5 inside the 3 sigma band."""
+    img = _gauss_noise(9, 64, 64)
+    for sigma in (2.0, 5.0):
+        d, _ = _gpf_direct(gpu, img, ss=sigma, radius=int(math.ceil(4.0 * sigma)))
+        r, _ = gpu.gpf_filter_gpf(img, gpu.spatial_params(sigma), gpu.range_params(30.0, 20))
+        b = int(math.ceil(3.0 * sigma))
+        assert np.abs(d[b:64 - b, b:64 - b] - r[b:64 - b, b:64 - b]).max() <= 0.5
+
+
+def test_pin_fallback_count_and_values(gpu):
+    """test_bilateral.cpp:317-333: sigma_r 1, degree 5 on a two-level image: all 64 pixels fall back."""
+    img = np.zeros((8, 8))
+    img[:, 4:] = 255.0
+    out, fb = _gpf_direct(gpu, img, sr=1.0, deg=5)
+    assert fb == 64
+    np.testing.assert_array_equal(out, img)
+
+
+def test_pin_taylor_direct(gpu):
+    """test_bilateral.cpp:335-356 (constants), 358-374 (K = 0 is num / den of direct_gaussian,
+    bitwise), 376-391 (worse than gpf on noise), 393-409 (falls back on the two-level image)."""
+    sp = gpu.spatial_params(2.0)
+    one, fb = gpu.gpf_filter_taylor(np.full((8, 8), 1.0), sp, gpu.range_params(30.0, 20), backend=0)
+    assert fb == 0 and np.abs(one - 1.0).max() <= 1e-12
+    mid, fb = gpu.gpf_filter_taylor(np.full((8, 8), 100.0), sp, gpu.range_params(30.0, 20), backend=0)
+    assert fb == 0 and np.abs(mid - 100.0).max() <= 1e-6
+    img = _mt_uniform(47, 16, 16, 256.0)
+    num = gpu.gpf_gaussian_direct(img, sp)
+    den = gpu.gpf_gaussian_direct(np.ones((16, 16)), sp)
+    for deg in (0, 1):
+        out, fb = gpu.gpf_filter_taylor(img, sp, gpu.range_params(30.0, deg), backend=0)
+        assert fb == 0
+        np.testing.assert_array_equal(out, num / den)
+    noisy = _gauss_noise(2, 32, 32)
+    ex = gpu.gpf_filter_exact(noisy, sp, gpu.range_params(30.0))
+    gp, _ = _gpf_direct(gpu, noisy)
+    ty, _ = gpu.gpf_filter_taylor(noisy, sp, gpu.range_params(30.0, 20), backend=0)
+    assert np.isfinite(ty).all()
+    assert gpu.gpf_compare(ex, ty)["mse_db"] > gpu.gpf_compare(ex, gp)["mse_db"]
+    two = np.zeros((8, 8))
+    two[:, 4:] = 255.0
+    out, fb = gpu.gpf_filter_taylor(two, sp, gpu.range_params(1.0, 2), backend=0)
+    assert fb > 0 and np.isfinite(out).all()
