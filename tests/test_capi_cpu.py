@@ -31,6 +31,30 @@ def test_library_exports_every_declared_symbol():
         assert hasattr(L, name), name
 
 
+REFERENCE_ABI = [  # every function of proj/include/gpfilter/gpfilter.h (28)
+    "gpf_compare", "gpf_decode_pgm", "gpf_encode_pgm", "gpf_filter_exact", "gpf_filter_gpf",
+    "gpf_filter_taylor", "gpf_free_bytes", "gpf_gaussian_direct", "gpf_gaussian_recursive",
+    "gpf_get_num_threads", "gpf_image_cdata", "gpf_image_create", "gpf_image_data",
+    "gpf_image_destroy", "gpf_image_height", "gpf_image_width", "gpf_kernel_gauss",
+    "gpf_kernel_gauss_poly", "gpf_kernel_sup_error", "gpf_kernel_taylor", "gpf_last_error",
+    "gpf_range_params_init", "gpf_read_pgm", "gpf_set_num_threads", "gpf_spatial_params_init",
+    "gpf_status_name", "gpf_version", "gpf_write_pgm",
+]
+
+
+def test_library_exports_the_whole_reference_abi():
+    """Link-level drop-in: every function the reference header declares is exported
+    (and, when the reference tree is present, the list above is the header's)."""
+    L = _lib.lib()
+    assert len(REFERENCE_ABI) == 28
+    for name in REFERENCE_ABI:
+        assert hasattr(L, name), name
+    hdr = "/root/reference/proj/include/gpfilter/gpfilter.h"
+    if os.path.exists(hdr):
+        text = re.sub(r"/\*.*?\*/", "", open(hdr).read(), flags=re.S)
+        assert sorted(set(re.findall(r"\b(gpf_\w+)\s*\(", text))) == REFERENCE_ABI
+
+
 def test_version_and_status_names():
     L = _lib.lib()
     assert L.gpf_version().decode().startswith("1.0.0")
