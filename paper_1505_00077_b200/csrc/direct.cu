@@ -17,6 +17,7 @@
 // (W <= kMaxApron), read through L1/L2 otherwise.
 #include <algorithm>
 #include <cmath>
+#include <cstdlib>
 #include <string>
 #include <vector>
 
@@ -133,6 +134,128 @@ __global__ void __launch_bounds__(kColTX * 8) k_direct_cols(const double* __rest
   }
 }
 
+
+// ---- register-tiled passes (W <= kMaxApron): one thread owns R consecutive
+// outputs of a line and walks the R + 2W samples they touch once; sample j
+// meets output r with tap j - r, so every output still accumulates its taps in
+// the order k = -W..W (bitwise the simple kernels above, which stay as the
+// path for wider windows). The last R taps live in registers (a rotating
+// window, resolved statically by unrolling R samples per trip), so a
+// multiply-add costs 2/R shared-memory loads instead of 2.
+constexpr int kTileT = 128;  // threads per CTA of the tiled row pass
+
+template <int R>
+__global__ void __launch_bounds__(kTileT) k_direct_rows_tiled(const double* __restrict__ src,
+                                                             double* __restrict__ dst,
+                                                             const double* __restrict__ taps, int w,
+                                                             long long lines, int W, int boundary) {
+  extern __shared__ double sm[];
+  const int nt = 2 * W + 1;
+  const int span = kTileT * R;                  // outputs per segment
+  const int P = kTileT + (2 * W + R - 1) / R + 1;  // pitch of the sample planes
+  double* st = sm;                              // taps, padded to a multiple of R past nt
+  double* sx = sm + ((nt + 2 * R) & ~1);        // samples, transposed: i -> (i % R) P + i / R
+  for (int k = threadIdx.x; k < nt + R; k += kTileT) st[k] = k < nt ? taps[k] : 0.0;
+  const int segs = (w + span - 1) / span;
+  const int trips = (nt + R - 1 + R - 1) / R;   // ceil((2W + R) / R)
+  for (long long item = blockIdx.x; item < lines * segs; item += gridDim.x) {
+    const long long line = item / segs;
+    const int x0 = (int)(item % segs) * span;
+    const double* row = src + line * w;
+    __syncthreads();
+    for (int i = threadIdx.x; i < trips * R + span; i += kTileT) {
+      const int m = bidx(x0 - W + i, w, boundary);
+      sx[(i % R) * P + i / R] = m >= 0 ? row[m] : 0.0;
+    }
+    __syncthreads();
+    const int xb = x0 + threadIdx.x * R;  // first output of this thread
+    double acc[R], t[R];
+#pragma unroll
+    for (int r = 0; r < R; ++r) acc[r] = 0.0, t[r] = 0.0;
+    for (int j0 = 0; j0 < trips * R; j0 += R) {
+#pragma unroll
+      for (int jj = 0; jj < R; ++jj) {
+        const int j = j0 + jj;          // sample xb - W + j, tap index j - r for output r
+        t[jj] = st[min(j, nt + R - 1)];
+        const double s = sx[jj * P + threadIdx.x + j0 / R];
+        const int pos = xb - W + j;
+        const bool live = boundary != 2 || (pos >= 0 && pos < w);
+#pragma unroll
+        for (int r = 0; r < R; ++r) {
+          const int k = j - r;
+          if (live && k >= 0 && k < nt) acc[r] = __dadd_rn(acc[r], __dmul_rn(t[(jj - r + R) % R], s));
+        }
+      }
+    }
+#pragma unroll
+    for (int r = 0; r < R; ++r)
+      if (xb + r < w) dst[line * w + xb + r] = acc[r];
+  }
+}
+
+template <int R>
+__global__ void __launch_bounds__(kColTX * 8) k_direct_cols_tiled(const double* __restrict__ src,
+                                                                 double* __restrict__ dst,
+                                                                 const double* __restrict__ taps, int w,
+                                                                 int h, int planes, int W, int boundary) {
+  extern __shared__ double sm[];
+  const int nt = 2 * W + 1;
+  for (int k = threadIdx.y * kColTX + threadIdx.x; k < nt + R; k += kColTX * 8) sm[k] = k < nt ? taps[k] : 0.0;
+  __syncthreads();
+  const int TY = 8 * R;
+  const int tx = (w + kColTX - 1) / kColTX, ty = (h + TY - 1) / TY;
+  const long long tiles = (long long)tx * ty * planes;
+  const int trips = (nt + R - 1 + R - 1) / R;
+  for (long long tl = blockIdx.x; tl < tiles; tl += gridDim.x) {
+    const int plane = (int)(tl / ((long long)tx * ty));
+    const int rem = (int)(tl % ((long long)tx * ty));
+    const int x = (rem % tx) * kColTX + threadIdx.x;
+    const int yb = (rem / tx) * TY + threadIdx.y * R;
+    if (x >= w || yb >= h) continue;
+    const double* sp = src + (size_t)plane * w * h + x;
+    double* dp = dst + (size_t)plane * w * h + x;
+    double acc[R], t[R];
+#pragma unroll
+    for (int r = 0; r < R; ++r) acc[r] = 0.0, t[r] = 0.0;
+    for (int j0 = 0; j0 < trips * R; j0 += R) {
+#pragma unroll
+      for (int jj = 0; jj < R; ++jj) {
+        const int j = j0 + jj;
+        t[jj] = sm[min(j, nt + R - 1)];
+        const int m = bidx(yb - W + j, h, boundary);
+        const double s = m >= 0 ? __ldg(sp + (size_t)m * w) : 0.0;
+#pragma unroll
+        for (int r = 0; r < R; ++r) {
+          const int k = j - r;
+          if (m >= 0 && k >= 0 && k < nt) acc[r] = __dadd_rn(acc[r], __dmul_rn(t[(jj - r + R) % R], s));
+        }
+      }
+    }
+#pragma unroll
+    for (int r = 0; r < R; ++r)
+      if (yb + r < h) dp[(size_t)(yb + r) * w] = acc[r];
+  }
+}
+
+template <int R>
+cudaError_t launch_tiled(const double* d_src, double* d_dst, double* d_tmp, const double* d_taps, int w,
+                         int h, int planes, int W, int boundary, cudaStream_t st) {
+  const int nt = 2 * W + 1;
+  const long long lines = (long long)planes * h;
+  const int span = kTileT * R;
+  const int trips = (nt + 2 * R - 2) / R;
+  const int P = kTileT + (2 * W + R - 1) / R + 1;
+  const size_t smr = sizeof(double) * (((nt + 2 * R) & ~1) + (size_t)R * P + trips);
+  const size_t smc = sizeof(double) * (nt + R);
+  const long long segs = lines * ((w + span - 1) / span);
+  k_direct_rows_tiled<R><<<(int)std::min<long long>(segs, 148 * 16), kTileT, smr, st>>>(
+      d_src, d_tmp, d_taps, w, lines, W, boundary);
+  const long long tiles = (long long)((w + kColTX - 1) / kColTX) * ((h + 8 * R - 1) / (8 * R)) * planes;
+  k_direct_cols_tiled<R><<<(int)std::min<long long>(tiles, 148 * 32), dim3(kColTX, 8), smc, st>>>(
+      d_tmp, d_dst, d_taps + nt, w, h, planes, W, boundary);
+  return cudaGetLastError();
+}
+
 // GpfState::step's plane chain (bilateral.cpp:108-129): F_0, F_{n+1} = H F_n
 __global__ void k_direct_gen_planes(const double* __restrict__ H, const double* __restrict__ F0,
                                     double* __restrict__ F, long long n, int planes) {
@@ -145,6 +268,13 @@ __global__ void k_direct_gen_planes(const double* __restrict__ H, const double* 
       v = __dmul_rn(hv, v);
     }
   }
+}
+
+// GPF_B200_DIRECT_SIMPLE=1: the one-output-per-thread kernels for every window
+// (the cross-check of the tiled kernels in tests/test_gpu_direct.py)
+bool direct_simple() {
+  const char* e = std::getenv("GPF_B200_DIRECT_SIMPLE");
+  return e != nullptr && e[0] != '\0' && e[0] != '0';
 }
 
 void chk_(cudaError_t e, const char* what) {
@@ -185,6 +315,13 @@ void run_direct_gaussian_f64(const double* d_src, double* d_dst, double* d_tmp, 
                                   cudaMemcpyHostToDevice, st);
   if (e == cudaSuccess) {
     const long long lines = (long long)planes * h;
+    if (W <= kMaxApron && !direct_simple()) {
+      e = W <= 12 ? launch_tiled<4>(d_src, d_dst, d_tmp, d_taps, w, h, planes, W, boundary, st)
+                  : launch_tiled<8>(d_src, d_dst, d_tmp, d_taps, w, h, planes, W, boundary, st);
+      cudaFreeAsync(d_taps, st);
+      chk_(e, "direct_gaussian launch");
+      return;
+    }
     const int use_smem = W <= kMaxApron;
     const size_t smc = sizeof(double) * (W <= kMaxTapW ? nt : 0);  // <= 32 KB
     const size_t smr = smc + sizeof(double) * (use_smem ? kDirT + 2 * W : 0);

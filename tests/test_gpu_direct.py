@@ -235,3 +235,22 @@ def test_pin_taylor_direct(gpu):
     two[:, 4:] = 255.0
     out, fb = gpu.gpf_filter_taylor(two, sp, gpu.range_params(1.0, 2), backend=0)
     assert fb > 0 and np.isfinite(out).all()
+
+
+def test_tiled_and_simple_kernels_agree_bitwise(gpu, reference, monkeypatch):
+    """W <= 512 runs the register-tiled passes (R outputs per thread); GPF_B200_DIRECT_SIMPLE=1
+    forces the one-output-per-thread kernels. Both are the reference's bits."""
+    img = _noise(1100, 37, 5)
+    for ss, radius, boundary in [(2.0, 0, 0), (2.0, 0, 2), (4.0, 12, 1), (4.5, 13, 2), (30.0, 90, 1), (170.0, 512, 0)]:
+        st, ref = reference.gaussian_direct(img, ss, radius, boundary, 1.0)
+        assert st == 0
+        monkeypatch.delenv("GPF_B200_DIRECT_SIMPLE", raising=False)
+        tiled = gpu.gpf_gaussian_direct(img, gpu.spatial_params(ss, radius, boundary))
+        monkeypatch.setenv("GPF_B200_DIRECT_SIMPLE", "1")
+        simple = gpu.gpf_gaussian_direct(img, gpu.spatial_params(ss, radius, boundary))
+        monkeypatch.delenv("GPF_B200_DIRECT_SIMPLE")
+        np.testing.assert_array_equal(tiled, ref)
+        np.testing.assert_array_equal(simple, ref)
+    tall = _noise(37, 1100, 6)
+    st, ref = reference.gaussian_direct(tall, 6.0, 0, 1, 1.0)
+    np.testing.assert_array_equal(gpu.gpf_gaussian_direct(tall, gpu.spatial_params(6.0, 0, 1)), ref)
