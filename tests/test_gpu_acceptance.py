@@ -30,7 +30,7 @@ def _run(binary):
     out = subprocess.run([binary], cwd=ROOT, capture_output=True, text=True, timeout=900)
     lines = {}
     for ln in out.stdout.splitlines():
-        m = re.match(r"\[(PASS|FAIL)\] (\d)\. (.*) \((.*)\)$", ln)
+        m = re.match(r"\[(PASS|FAIL)\] (\d)\. (.*?) \((.*)\)$", ln)
         if m:
             lines[int(m.group(2))] = (m.group(1), m.group(4))
     assert len(lines) == 9, out.stdout + out.stderr
