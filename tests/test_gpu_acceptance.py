@@ -61,3 +61,42 @@ def test_reference_acceptance_harness_against_the_b200_library(gpu):
         for x, y in zip(a, b):
             assert abs(x - y) <= 2e-3 * max(1.0, abs(y)), report
     print(report)
+
+
+def test_constant_time_property_at_gpu_scale(gpu):
+    """Criterion 5 (acceptance.cpp:265-308) restated where a B200 can show it: device time of a
+    2048x2048 frame instead of the wall time of a 256x256 call (which is launch- and copy-bound
+    on a GPU). The gpf call's device time is flat from sigma_s 2 to 15 (ratio <= 1.5); the exact
+    filter's grows with its (2W+1)^2 window (sigma_s 2 -> 4: ratio >= 2.5)."""
+    import numpy as np
+    import torch
+
+    from paper_1505_00077_b200 import synth
+    img = np.round(synth.rects_image(2048, 2048, 64, 10.0, 9)).astype(np.float64)
+    rp = gpu.range_params(30.0, 20)
+
+    def gpf_ms(ss):
+        best = 1e9
+        for _ in range(4):
+            gpu.gpf_filter_gpf(img, gpu.spatial_params(ss), rp)
+            best = min(best, gpu.last_device_ms())
+        return best
+
+    d_in = torch.from_numpy(img.astype(np.float32)).cuda()
+    d_out = torch.empty_like(d_in)
+
+    def exact_ms(ss):
+        best = 1e9
+        for _ in range(3):
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record()
+            gpu.exact_device(d_in, d_out, 2048, 2048, ss, 30.0, stream=torch.cuda.current_stream().cuda_stream)
+            e1.record()
+            torch.cuda.synchronize()
+            best = min(best, e0.elapsed_time(e1))
+        return best
+
+    g2, g15, e2, e4 = gpf_ms(2.0), gpf_ms(15.0), exact_ms(2.0), exact_ms(4.0)
+    print(f"device ms: gpf {g2:.3f} / {g15:.3f} (ratio {g15 / g2:.3f}); exact {e2:.3f} / {e4:.3f} (ratio {e4 / e2:.3f})")
+    assert g15 / g2 <= 1.5
+    assert e4 / e2 >= 2.5
