@@ -13,8 +13,8 @@
 //   Boundary, SpatialParams, SigmaTooSmallError, default_window_radius
 //                        ref spatial.hpp:13-34
 //   RangeParams          ref range_kernel.hpp:13-18
-//   SpatialBackend, CenteringMode, GpfOptions, FilterResult, gpf, kQMin
-//                        ref bilateral.hpp:13-28, 73-85
+//   SpatialBackend, CenteringMode, GpfOptions, FilterResult, GpfState, gpf, kQMin
+//                        ref bilateral.hpp:13-28, 38-68, 73-85
 // Errors are thrown as in the reference: std::invalid_argument for invalid
 // parameters (same messages), SigmaTooSmallError for sigma_s < 0.5 on the
 // recursive backend; GPU failures as std::runtime_error. The filter runs on the
@@ -105,6 +105,36 @@ FilterResult gpf(const Image& img, const SpatialParams& sp, const RangeParams& r
                  SpatialBackend backend, const GpfOptions& opts = {});
 
 inline constexpr double kQMin = 1e-8;
+
+// Step-wise form of gpf (ref bilateral.hpp:38-68): init, then degree + 1 calls
+// of step(), then finalize(); after n steps c = 1/n!, G = H^n, F = H^n F_0.
+// The state images are public host images, as in the reference; every phase
+// runs on the GPU in the reference-exact fp64 arithmetic (the reference's
+// operation order; only exp() may differ by an ulp) on the images as they
+// stand, so a caller may inspect or edit them between steps. It is the
+// inspection tool, not the fast path: each step round-trips its images over
+// PCIe (gpf() keeps the planes on the device).
+struct GpfState {
+  Image G;     // running power image H^n
+  Image F;     // Gaussian-weighted moment image
+  Image Fbar;  // spatially filtered F
+  Image P;     // numerator accumulator
+  Image Q;     // denominator accumulator
+  Image H;     // h / sigma_r
+  double c = 1.0;
+  int n = 0;  // completed steps
+  double t_c = 0.0;
+
+  static GpfState init(const Image& img, const SpatialParams& sp, const RangeParams& rp,
+                       SpatialBackend backend, const GpfOptions& opts);
+  void step();
+  FilterResult finalize(const Image& input) const;  // sigma_r (P / Q) + t_c, fallback rule
+
+ private:
+  SpatialParams sp_;
+  RangeParams rp_;
+  SpatialBackend backend_ = SpatialBackend::recursive;
+};
 
 }  // namespace gpfilter
 

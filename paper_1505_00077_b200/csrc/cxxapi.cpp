@@ -4,6 +4,9 @@
 // 220-230; range_kernel.cpp:22-29; image.cpp:11-18).
 #include <cmath>
 #include <string>
+#include <utility>
+
+#include <cuda_runtime.h>
 
 #include "gpf_internal.h"
 #include "gpfilter/gpfilter.hpp"
@@ -78,6 +81,149 @@ FilterResult gpf(const Image& img, const SpatialParams& sp, const RangeParams& r
     if (e.status == 1) throw std::invalid_argument(e.msg);
     if (e.status == 3) throw SigmaTooSmallError(e.msg);
     throw std::runtime_error(e.msg);
+  }
+  return res;
+}
+
+// ------------------------------------------------------------------ GpfState
+namespace {
+
+[[noreturn]] void rethrow(const gpfb::Error& e) {
+  if (e.status == 1) throw std::invalid_argument(e.msg);
+  if (e.status == 3) throw SigmaTooSmallError(e.msg);
+  throw std::runtime_error(e.msg);
+}
+
+void cu(cudaError_t e, const char* what) {
+  if (e != cudaSuccess) {
+    cudaGetLastError();
+    throw gpfb::Error{9, std::string(what) + ": " + cudaGetErrorString(e)};
+  }
+}
+
+// n doubles on the device, optionally filled from a host image
+struct Dev {
+  double* p = nullptr;
+  size_t n = 0;
+  explicit Dev(size_t count, const double* host = nullptr) : n(count) {
+    cu(cudaMalloc(&p, sizeof(double) * count), "cudaMalloc");
+    if (host) up(host);
+  }
+  ~Dev() { cudaFree(p); }
+  Dev(const Dev&) = delete;
+  Dev& operator=(const Dev&) = delete;
+  void up(const double* host) { cu(cudaMemcpy(p, host, sizeof(double) * n, cudaMemcpyHostToDevice), "H2D"); }
+  void down(double* host) const { cu(cudaMemcpy(host, p, sizeof(double) * n, cudaMemcpyDeviceToHost), "D2H"); }
+};
+
+gpfb::Params state_params(int w, int h, const SpatialParams& sp, const RangeParams& rp,
+                          SpatialBackend backend) {
+  gpfb::Params p;
+  p.width = w;
+  p.height = h;
+  p.sigma_s = sp.sigma_s;
+  p.kernel_scale = sp.kernel_scale;
+  p.sigma_r = rp.sigma_r;
+  p.degree = rp.degree;
+  p.backend = backend == SpatialBackend::direct ? 0 : 1;
+  p.window_radius = sp.window_radius;
+  p.boundary = static_cast<int>(sp.boundary);
+  return p;
+}
+
+void require_device() {
+  int count = 0;
+  if (cudaGetDeviceCount(&count) != cudaSuccess || count == 0) {
+    cudaGetLastError();
+    throw std::runtime_error("no CUDA device available (the B200 library has no CPU path)");
+  }
+}
+
+}  // namespace
+
+GpfState GpfState::init(const Image& img, const SpatialParams& sp, const RangeParams& rp,
+                        SpatialBackend backend, const GpfOptions& opts) {
+  // bilateral.cpp:67-72, then the first apply_spatial's checks (spatial.cpp:222-230)
+  sp.validate();
+  rp.validate();
+  if (!(opts.range.low < opts.range.high))
+    throw std::invalid_argument("GpfOptions: range.low must be < range.high");
+  if (img.pixels() == 0) throw std::invalid_argument("Image dimensions must be >= 1");
+  if (backend == SpatialBackend::recursive && sp.sigma_s < 0.5)
+    throw SigmaTooSmallError(
+        "recursive_gaussian: sigma_s < 0.5 is not supported; use the direct backend");
+  require_device();
+  GpfState s;
+  s.sp_ = sp;
+  s.rp_ = rp;
+  s.backend_ = backend;
+  const int w = img.width(), h = img.height();
+  const size_t n = img.pixels();
+  s.G = Image(w, h, 1.0);
+  s.P = Image(w, h, 0.0);
+  s.Q = Image(w, h, 0.0);
+  s.H = Image(w, h);
+  s.F = Image(w, h);
+  s.Fbar = Image(w, h);
+  gpfb::Params p = state_params(w, h, sp, rp, backend);
+  // t_c (bilateral.cpp:77-82): mean, midpoint (low + high) / 2, or 0
+  p.centering = !opts.centering ? 0 : (opts.mode == CenteringMode::mean ? 1 : 2);
+  p.tc_fixed = (opts.range.low + opts.range.high) / 2.0;
+  try {
+    Dev in(n, img.data()), dH(n), dF(n), dFbar(n), tmp(n), scal(2 + 4 * (size_t)gpfb::kF64MeanBlocks);
+    gpfb::state_init_f64(in.p, dH.p, dF.p, scal.p, scal.p + 2, p, nullptr);
+    gpfb::state_spatial_f64(dF.p, dFbar.p, tmp.p, p, nullptr);
+    cu(cudaMemcpy(&s.t_c, scal.p, sizeof(double), cudaMemcpyDeviceToHost), "D2H");
+    dH.down(s.H.data());
+    dF.down(s.F.data());
+    dFbar.down(s.Fbar.data());
+  } catch (const gpfb::Error& e) {
+    rethrow(e);
+  }
+  s.c = 1.0;
+  s.n = 0;
+  return s;
+}
+
+void GpfState::step() {
+  require_device();
+  const size_t count = F.pixels();
+  const gpfb::Params p = state_params(F.width(), F.height(), sp_, rp_, backend_);
+  try {
+    Dev dG(count, G.data()), dF(count, F.data()), dFbar(count, Fbar.data()), dP(count, P.data()),
+        dQ(count, Q.data()), dH(count, H.data()), tmp(count);
+    gpfb::state_step_a_f64(dQ.p, dF.p, dG.p, dFbar.p, dH.p, c, (long long)count, nullptr);
+    gpfb::state_spatial_f64(dF.p, dFbar.p, tmp.p, p, nullptr);
+    gpfb::state_step_b_f64(dP.p, dG.p, dFbar.p, dH.p, c, (long long)count, nullptr);
+    dQ.down(Q.data());
+    dF.down(F.data());
+    dFbar.down(Fbar.data());
+    dP.down(P.data());
+    dG.down(G.data());
+  } catch (const gpfb::Error& e) {
+    rethrow(e);
+  }
+  c = c / (n + 1);
+  ++n;
+}
+
+FilterResult GpfState::finalize(const Image& input) const {
+  if (!input.same_size(P) || !input.same_size(Q))
+    throw std::invalid_argument("GpfState::finalize: input and state images differ in size");
+  require_device();
+  FilterResult res;
+  res.image = Image(input.width(), input.height());
+  const size_t count = input.pixels();
+  try {
+    Dev in(count, input.data()), dP(count, P.data()), dQ(count, Q.data()), out(count), fb(1);
+    gpfb::state_finalize_f64(in.p, dP.p, dQ.p, out.p, (long long)count, rp_.sigma_r, t_c,
+                             reinterpret_cast<unsigned long long*>(fb.p), nullptr);
+    out.down(res.image.data());
+    unsigned long long f = 0;
+    cu(cudaMemcpy(&f, fb.p, sizeof(f), cudaMemcpyDeviceToHost), "D2H");
+    res.fallback_count = static_cast<long long>(f);
+  } catch (const gpfb::Error& e) {
+    rethrow(e);
   }
   return res;
 }

@@ -777,6 +777,93 @@ void chk(cudaError_t e, const char* what) {
 
 }  // namespace
 
+// ---- GpfState stepping (cxxapi.cpp; bilateral.cpp:64-148), one call per phase
+namespace {
+
+// step(), first loop (bilateral.cpp:117-120): q += c g fbar; f = h f
+__global__ void k_state_step_a(double* __restrict__ Q, double* __restrict__ F,
+                               const double* __restrict__ G, const double* __restrict__ Fbar,
+                               const double* __restrict__ H, double c, long long n) {
+  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+       i += (long long)gridDim.x * blockDim.x) {
+    Q[i] = a_(Q[i], m_(m_(c, G[i]), Fbar[i]));
+    F[i] = m_(H[i], F[i]);
+  }
+}
+
+// step(), second loop (bilateral.cpp:123-126): p += c g fbar; g = h g
+__global__ void k_state_step_b(double* __restrict__ P, double* __restrict__ G,
+                               const double* __restrict__ Fbar, const double* __restrict__ H,
+                               double c, long long n) {
+  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+       i += (long long)gridDim.x * blockDim.x) {
+    P[i] = a_(P[i], m_(m_(c, G[i]), Fbar[i]));
+    G[i] = m_(H[i], G[i]);
+  }
+}
+
+// finalize() (bilateral.cpp:131-148)
+__global__ void k_state_finalize(const double* __restrict__ in, const double* __restrict__ P,
+                                 const double* __restrict__ Q, double* __restrict__ out, long long n,
+                                 double sigma_r, double t_c, unsigned long long* __restrict__ fallbacks) {
+  unsigned my_fb = 0;
+  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+       i += (long long)gridDim.x * blockDim.x) {
+    if (fabs(Q[i]) <= 1e-8) {  // kQMin
+      out[i] = in[i];
+      ++my_fb;
+    } else {
+      out[i] = a_(m_(sigma_r, __ddiv_rn(P[i], Q[i])), t_c);
+    }
+  }
+  for (int o = 16; o; o >>= 1) my_fb += __shfl_xor_sync(0xffffffffu, my_fb, o);
+  if ((threadIdx.x & 31) == 0 && my_fb) atomicAdd(fallbacks, (unsigned long long)my_fb);
+}
+
+int state_blocks(long long n) { return (int)std::max<long long>(1, std::min<long long>((n + 255) / 256, 148 * 16)); }
+
+}  // namespace
+
+// t_c -> scalars[0] (scalars: 2 doubles; partials: 4 kF64MeanBlocks doubles), H, F_0
+void state_init_f64(const double* d_in, double* H, double* F, double* scalars, double* partials,
+                    const Params& p, cudaStream_t st) {
+  const long long n = (long long)p.width * p.height;
+  launch_mean_f64(d_in, n, p.centering, p.tc_fixed, p.sigma_r, partials, kF64MeanBlocks, scalars, st);
+  const double inv2s2 = 1.0 / (2.0 * p.sigma_r * p.sigma_r);
+  k_f64_prologue<<<state_blocks(n), 256, 0, st>>>(d_in, scalars, H, F, n, p.sigma_r, inv2s2);
+  chk(cudaGetLastError(), "kernel launch (GpfState::init)");
+}
+
+// apply_spatial (bilateral.cpp:58-62): src -> dst through tmp
+void state_spatial_f64(const double* src, double* dst, double* tmp, const Params& p, cudaStream_t st) {
+  if (p.backend == 0) {
+    run_direct_gaussian_f64(src, dst, tmp, p.width, p.height, 1, p.sigma_s, p.kernel_scale,
+                            p.window_radius, p.boundary, st);
+  } else {
+    const double mass = kernel_mass_1d(p.sigma_s, default_window_radius(p.sigma_s));
+    run_gaussian_f64(src, dst, tmp, p.width, p.height, p.sigma_s, mass * mass * p.kernel_scale, st);
+  }
+}
+
+void state_step_a_f64(double* Q, double* F, const double* G, const double* Fbar, const double* H,
+                      double c, long long n, cudaStream_t st) {
+  k_state_step_a<<<state_blocks(n), 256, 0, st>>>(Q, F, G, Fbar, H, c, n);
+  chk(cudaGetLastError(), "kernel launch (GpfState::step)");
+}
+
+void state_step_b_f64(double* P, double* G, const double* Fbar, const double* H, double c, long long n,
+                      cudaStream_t st) {
+  k_state_step_b<<<state_blocks(n), 256, 0, st>>>(P, G, Fbar, H, c, n);
+  chk(cudaGetLastError(), "kernel launch (GpfState::step)");
+}
+
+void state_finalize_f64(const double* in, const double* P, const double* Q, double* out, long long n,
+                        double sigma_r, double t_c, unsigned long long* d_fb, cudaStream_t st) {
+  chk(cudaMemsetAsync(d_fb, 0, sizeof(unsigned long long), st), "cudaMemsetAsync");
+  k_state_finalize<<<state_blocks(n), 256, 0, st>>>(in, P, Q, out, n, sigma_r, t_c, d_fb);
+  chk(cudaGetLastError(), "kernel launch (GpfState::finalize)");
+}
+
 size_t f64_workspace_bytes(int w, int h, int degree) {
   const size_t n = (size_t)w * h;
   return sizeof(double) * (n * (2 + 2 * (size_t)(degree + 2)) + 2 + 4 * kF64MeanBlocks +

@@ -235,6 +235,19 @@ void run_gpf_f64_exact(const double* d_in, double* d_out, const Params& p, F64Wo
                        unsigned long long* d_fb, cudaStream_t st, int ranges = 1,
                        cudaEvent_t* range_done = nullptr);
 
+// GpfState stepping on device buffers (gpf_f64.cu; bilateral.cpp:64-148), fp64,
+// the reference's operation order: init (t_c into scalars[0], H, F_0),
+// apply_spatial with either backend, the two loops of step(), finalize.
+void state_init_f64(const double* d_in, double* H, double* F, double* scalars, double* partials,
+                    const Params& p, cudaStream_t st);
+void state_spatial_f64(const double* src, double* dst, double* tmp, const Params& p, cudaStream_t st);
+void state_step_a_f64(double* Q, double* F, const double* G, const double* Fbar, const double* H,
+                      double c, long long n, cudaStream_t st);
+void state_step_b_f64(double* P, double* G, const double* Fbar, const double* H, double c, long long n,
+                      cudaStream_t st);
+void state_finalize_f64(const double* in, const double* P, const double* Q, double* out, long long n,
+                        double sigma_r, double t_c, unsigned long long* d_fb, cudaStream_t st);
+
 // Drop-in fp64 host entry (dropin.cpp): gpf_filter_gpf and gpfilter::gpf.
 // Per device: an LRU of fp32 plans, the fp64 workspace, device in/out
 // buffers and a stream, reused across calls (a repeated call allocates

@@ -5,9 +5,12 @@
 // tests/test_cxx_api.py runs the same gpfilter::gpf call through both.
 //
 //   driver IN.raw W H OUT.raw SIGMA_S SIGMA_R DEGREE CENTERING MODE LOW HIGH BACKEND
-//          KERNEL_SCALE WINDOW_RADIUS
+//          KERNEL_SCALE WINDOW_RADIUS [state:K]
 // IN/OUT: W*H little-endian doubles; MODE mean|midpoint; BACKEND direct|recursive.
 // Prints "ok <fallback_count>" or "error <exception type> <message>".
+// With state:K the run goes through GpfState (init, K steps, finalize) and OUT
+// holds the doubles t_c, c, n, then the images G, F, Fbar, P, Q, H, then the
+// finalize image.
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
@@ -23,7 +26,7 @@
 using namespace gpfilter;
 
 int main(int argc, char** argv) {
-  if (argc != 15) {
+  if (argc != 15 && argc != 16) {
     std::fprintf(stderr, "usage: see source\n");
     return 2;
   }
@@ -49,6 +52,21 @@ int main(int argc, char** argv) {
       FILE* f = std::fopen(argv[1], "rb");
       if (!f || std::fread(img.data(), sizeof(double), img.pixels(), f) != img.pixels()) return 3;
       std::fclose(f);
+    }
+    if (argc == 16) {
+      const int steps = std::atoi(argv[15] + 6);
+      GpfState st = GpfState::init(img, sp, rp, be, opts);
+      for (int k = 0; k < steps; ++k) st.step();
+      const FilterResult r = st.finalize(img);
+      FILE* o = std::fopen(argv[4], "wb");
+      const double head[3] = {st.t_c, st.c, static_cast<double>(st.n)};
+      std::fwrite(head, sizeof(double), 3, o);
+      const Image* dump[7] = {&st.G, &st.F, &st.Fbar, &st.P, &st.Q, &st.H, &r.image};
+      for (const Image* im : dump)
+        std::fwrite(im->data(), sizeof(double), im->pixels(), o);
+      std::fclose(o);
+      std::printf("ok %lld\n", r.fallback_count);
+      return 0;
     }
     const FilterResult r = gpf(img, sp, rp, be, opts);
     FILE* o = std::fopen(argv[4], "wb");

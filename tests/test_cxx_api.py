@@ -22,7 +22,7 @@ REF = os.path.join(ROOT, "oracle", "_ref", "gpf_cxx_driver_ref")
 
 
 def drive(binary, img, ss=3.0, sr=30.0, deg=20, cen=1, mode="mean", low=0.0, high=255.0,
-          backend="recursive", ks=1.0, radius=9):
+          backend="recursive", ks=1.0, radius=9, state=None):
     if not os.path.exists(binary):
         pytest.skip(f"{binary} not built")
     with tempfile.TemporaryDirectory() as d:
@@ -31,10 +31,17 @@ def drive(binary, img, ss=3.0, sr=30.0, deg=20, cen=1, mode="mean", low=0.0, hig
         if img is not None:
             np.ascontiguousarray(img, dtype="<f8").tofile(src)
         out = subprocess.run([binary, src, str(w), str(h), dst, repr(ss), repr(sr), str(deg), str(cen),
-                              mode, repr(low), repr(high), backend, repr(ks), str(radius)],
+                              mode, repr(low), repr(high), backend, repr(ks), str(radius)]
+                             + ([f"state:{state}"] if state is not None else []),
                              capture_output=True, text=True, timeout=600)
         assert out.returncode == 0, out.stderr
         line = out.stdout.strip()
+        if line.startswith("ok") and state is not None:
+            raw = np.fromfile(dst, dtype="<f8")
+            names = ["G", "F", "Fbar", "P", "Q", "H", "out"]
+            res = {"t_c": raw[0], "c": raw[1], "n": int(raw[2])}
+            res.update({k: raw[3 + i * h * w: 3 + (i + 1) * h * w].reshape(h, w) for i, k in enumerate(names)})
+            return int(line.split()[1]), res
         if line.startswith("ok"):
             return int(line.split()[1]), np.fromfile(dst, dtype="<f8").reshape(h, w)
         _, kind, msg = line.split(" ", 2)
@@ -107,3 +114,45 @@ def test_gpf_matches_reference_cxx(gpu, opts):
     fb, out = drive(OURS, img, **opts)
     assert fb == rfb
     assert np.abs(out - ref).max() <= 1e-3, opts
+
+
+def test_gpf_state_validates_like_reference():
+    """GpfState::init (bilateral.cpp:64-72): the same exceptions as the reference."""
+    img = synth.rects_image(16, 12, 2, 10.0, 1).astype(np.float64)
+    for case in [dict(ss=0.4), dict(ss=0.0), dict(radius=0), dict(sr=0.0), dict(deg=-1),
+                 dict(low=200.0, high=100.0)]:
+        ref = drive(REF, img, state=2, **case)
+        ours = drive(OURS, img, state=2, **case)
+        assert isinstance(ref[0], str) and ref == ours, (ref, ours)
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("backend,steps,opts", [
+    ("direct", 0, dict()), ("direct", 6, dict()), ("recursive", 3, dict()),
+    ("recursive", 21, dict()), ("direct", 21, dict(mode="midpoint")), ("recursive", 11, dict(cen=0, deg=10)),
+])
+def test_gpf_state_stepping_matches_reference_core(backend, steps, opts):
+    """GpfState (ref bilateral.hpp:38-68; test_bilateral.cpp:154-201): every state image after
+    K steps against the reference's own GpfState -- t_c, c and n equal, G and H bitwise (pure
+    fp64 products of the input), F / Fbar / P / Q to the ulp of exp() -- and finalize()."""
+    img = synth.rects_image(40, 28, 3, 10.0, 5).astype(np.float64)
+    rfb, ref = drive(REF, img, backend=backend, state=steps, radius=9, **opts)
+    fb, out = drive(OURS, img, backend=backend, state=steps, radius=9, **opts)
+    assert fb == rfb
+    assert out["n"] == ref["n"] == steps and out["c"] == ref["c"] and out["t_c"] == ref["t_c"]
+    np.testing.assert_array_equal(out["H"], ref["H"])
+    np.testing.assert_array_equal(out["G"], ref["G"])
+    for k in ("F", "Fbar", "P", "Q"):
+        scale = max(float(np.abs(ref[k]).max()), 1e-300)
+        assert float(np.abs(out[k] - ref[k]).max()) <= 1e-13 * scale, k
+    assert float(np.abs(out["out"] - ref["out"]).max()) <= 1e-9
+
+
+@pytest.mark.gpu
+def test_gpf_state_full_run_equals_gpf():
+    """init + (degree + 1) steps + finalize is gpf() (bilateral.cpp:150-158): against the
+    reference's gpf on the reference side, and ours within 1e-9 of it."""
+    img = synth.rects_image(40, 28, 3, 10.0, 7).astype(np.float64)
+    rfb, ref = drive(REF, img, deg=12)
+    fb, st = drive(OURS, img, deg=12, state=13)
+    assert fb == rfb and float(np.abs(st["out"] - ref).max()) <= 1e-9
