@@ -106,6 +106,43 @@ FilterResult gpf(const Image& img, const SpatialParams& sp, const RangeParams& r
 
 inline constexpr double kQMin = 1e-8;
 
+// The other entry points of the reference core, same signatures and exceptions,
+// each running on the GPU through the C ABI entry of the same name (gpfilter.h):
+//   exact_bilateral, taylor_bilateral            ref bilateral.hpp:30-36, 76-80
+//   direct_gaussian, recursive_gaussian, kernel_mass_1d
+//                                                ref spatial.hpp:46-64
+//   mean_intensity, shift, max_abs_diff          ref image.hpp:49-57
+//   ErrorReport, compare, mse_db, kMseDbFloor    ref metrics.hpp:11-33
+//   gaussian_range, gauss_polynomial, taylor_polynomial, RangeApprox, sup_error
+//                                                ref range_kernel.hpp:20-43 (host scalar)
+Image exact_bilateral(const Image& img, const SpatialParams& sp, const RangeParams& rp);
+FilterResult taylor_bilateral(const Image& img, const SpatialParams& sp, const RangeParams& rp,
+                              SpatialBackend backend);
+Image direct_gaussian(const Image& img, const SpatialParams& p);
+Image recursive_gaussian(const Image& img, double sigma_s, double kernel_scale = 1.0);
+double kernel_mass_1d(double sigma_s, int window_radius);
+
+double mean_intensity(const Image& img);         // deterministic double-double mean on the GPU
+Image shift(const Image& img, double c);         // every sample decreased by c
+double max_abs_diff(const Image& a, const Image& b);  // throws std::invalid_argument on size mismatch
+
+struct ErrorReport {
+  double mse = 0.0;
+  double mse_db = 0.0;  // 10 log10(mse), kMseDbFloor when mse == 0
+  double max_abs = 0.0;
+  long long pixels = 0;
+};
+inline constexpr double kMseDbFloor = -400.0;
+double mse_db(double mse);
+ErrorReport compare(const Image& ref, const Image& test, int exclude_border = 0);
+
+double gaussian_range(double t, double tau, const RangeParams& p);
+double gauss_polynomial(double t, double tau, const RangeParams& p);
+double taylor_polynomial(double t, double tau, const RangeParams& p);
+enum class RangeApprox { gauss_polynomial, taylor };
+double sup_error(const RangeParams& p, double tau, const IntensityRange& range, double step,
+                 RangeApprox which);
+
 // Step-wise form of gpf (ref bilateral.hpp:38-68): init, then degree + 1 calls
 // of step(), then finalize(); after n steps c = 1/n!, G = H^n, F = H^n F_0.
 // The state images are public host images, as in the reference; every phase

@@ -2,6 +2,7 @@
 // drop-in engine (dropin.cpp), with the reference's validation order and
 // exceptions (proj/src/core/bilateral.cpp:64-106, 150-158; spatial.cpp:25-35,
 // 220-230; range_kernel.cpp:22-29; image.cpp:11-18).
+#include <algorithm>
 #include <cmath>
 #include <string>
 #include <utility>
@@ -9,6 +10,7 @@
 #include <cuda_runtime.h>
 
 #include "gpf_internal.h"
+#include "gpfilter/gpfilter.h"
 #include "gpfilter/gpfilter.hpp"
 
 namespace gpfilter {
@@ -83,6 +85,147 @@ FilterResult gpf(const Image& img, const SpatialParams& sp, const RangeParams& r
     throw std::runtime_error(e.msg);
   }
   return res;
+}
+
+// ------------------------------------- the other entry points, over the C ABI
+namespace {
+
+// a gpf_image handle holding a copy of `img` (or an output of the C ABI)
+struct Handle {
+  gpf_image* h = nullptr;
+  Handle() = default;
+  explicit Handle(const Image& img) {
+    if (img.pixels() == 0) throw std::invalid_argument("Image dimensions must be >= 1");
+    if (gpf_image_create(img.width(), img.height(), &h) != GPF_OK) throw std::runtime_error(gpf_last_error());
+    std::copy(img.data(), img.data() + img.pixels(), gpf_image_data(h));
+  }
+  ~Handle() { gpf_image_destroy(h); }
+  Handle(const Handle&) = delete;
+  Handle& operator=(const Handle&) = delete;
+  Image take() const {
+    Image out(gpf_image_width(h), gpf_image_height(h));
+    std::copy(gpf_image_cdata(h), gpf_image_cdata(h) + out.pixels(), out.data());
+    return out;
+  }
+};
+
+// status -> the exception the reference core throws for it
+void raise(gpf_status st) {
+  if (st == GPF_OK) return;
+  const std::string msg = gpf_last_error();
+  if (st == GPF_ERR_INVALID_ARGUMENT) throw std::invalid_argument(msg);
+  if (st == GPF_ERR_SIGMA_TOO_SMALL) throw SigmaTooSmallError(msg);
+  throw std::runtime_error(msg);
+}
+
+gpf_spatial_params c_spatial(const SpatialParams& sp) {
+  sp.validate();  // window_radius >= 1 here: the C struct's "<= 0 selects the default" never applies
+  gpf_spatial_params c;
+  c.sigma_s = sp.sigma_s;
+  c.window_radius = sp.window_radius;
+  c.boundary = static_cast<gpf_boundary>(static_cast<int>(sp.boundary));
+  c.kernel_scale = sp.kernel_scale;
+  return c;
+}
+
+gpf_range_params c_range(const RangeParams& rp) {
+  rp.validate();
+  return gpf_range_params{rp.sigma_r, rp.degree};
+}
+
+}  // namespace
+
+Image exact_bilateral(const Image& img, const SpatialParams& sp, const RangeParams& rp) {
+  const gpf_spatial_params csp = c_spatial(sp);
+  const gpf_range_params crp = c_range(rp);
+  Handle in(img), out;
+  raise(gpf_filter_exact(in.h, &csp, &crp, &out.h));
+  return out.take();
+}
+
+FilterResult taylor_bilateral(const Image& img, const SpatialParams& sp, const RangeParams& rp,
+                              SpatialBackend backend) {
+  const gpf_spatial_params csp = c_spatial(sp);
+  const gpf_range_params crp = c_range(rp);
+  Handle in(img), out;
+  FilterResult res;
+  raise(gpf_filter_taylor(in.h, &csp, &crp,
+                          backend == SpatialBackend::direct ? GPF_BACKEND_DIRECT : GPF_BACKEND_RECURSIVE,
+                          &res.fallback_count, &out.h));
+  res.image = out.take();
+  return res;
+}
+
+Image direct_gaussian(const Image& img, const SpatialParams& p) {
+  const gpf_spatial_params csp = c_spatial(p);
+  Handle in(img), out;
+  raise(gpf_gaussian_direct(in.h, &csp, &out.h));
+  return out.take();
+}
+
+Image recursive_gaussian(const Image& img, double sigma_s, double kernel_scale) {
+  if (!(sigma_s > 0.0) || !(kernel_scale > 0.0))
+    throw std::invalid_argument("recursive_gaussian: sigma_s and kernel_scale must be > 0");
+  if (sigma_s < 0.5)
+    throw SigmaTooSmallError(
+        "recursive_gaussian: sigma_s < 0.5 is not supported; use the direct backend");
+  Handle in(img), out;
+  raise(gpf_gaussian_recursive(in.h, sigma_s, kernel_scale, &out.h));
+  return out.take();
+}
+
+double kernel_mass_1d(double sigma_s, int window_radius) { return gpfb::kernel_mass_1d(sigma_s, window_radius); }
+
+Image shift(const Image& img, double c) {
+  Image out = img;
+  for (std::size_t i = 0; i < out.pixels(); ++i) out.data()[i] -= c;
+  return out;
+}
+
+double max_abs_diff(const Image& a, const Image& b) {
+  if (!a.same_size(b)) throw std::invalid_argument("max_abs_diff: image dimensions differ");
+  double worst = 0.0;
+  for (std::size_t i = 0; i < a.pixels(); ++i) worst = std::fmax(worst, std::fabs(a.data()[i] - b.data()[i]));
+  return worst;
+}
+
+double mse_db(double mse) { return mse == 0.0 ? kMseDbFloor : std::fmax(10.0 * std::log10(mse), kMseDbFloor); }
+
+ErrorReport compare(const Image& ref, const Image& test, int exclude_border) {
+  if (!ref.same_size(test)) throw std::invalid_argument("compare: images differ in size");
+  Handle a(ref), b(test);
+  gpf_error_report r;
+  raise(gpf_compare(a.h, b.h, exclude_border, &r));
+  return ErrorReport{r.mse, r.mse_db, r.max_abs, r.pixels};
+}
+
+namespace {
+template <class F>
+double scalar(F&& f) {
+  try {
+    return f();
+  } catch (const gpfb::Error& e) {
+    throw std::invalid_argument(e.msg);
+  }
+}
+}  // namespace
+
+double gaussian_range(double t, double tau, const RangeParams& p) {
+  p.validate();
+  return scalar([&] { return gpfb::kernel_gauss(t, tau, p.sigma_r); });
+}
+double gauss_polynomial(double t, double tau, const RangeParams& p) {
+  return scalar([&] { return gpfb::kernel_gauss_poly(t, tau, p.sigma_r, p.degree); });
+}
+double taylor_polynomial(double t, double tau, const RangeParams& p) {
+  return scalar([&] { return gpfb::kernel_taylor(t, tau, p.sigma_r, p.degree); });
+}
+double sup_error(const RangeParams& p, double tau, const IntensityRange& range, double step,
+                 RangeApprox which) {
+  return scalar([&] {
+    return gpfb::kernel_sup_error(p.sigma_r, p.degree, tau, range.low, range.high, step,
+                                  which == RangeApprox::taylor);
+  });
 }
 
 // ------------------------------------------------------------------ GpfState
@@ -226,6 +369,24 @@ FilterResult GpfState::finalize(const Image& input) const {
     rethrow(e);
   }
   return res;
+}
+
+// mean_intensity (image.cpp:20-37): the deterministic double-double mean of the
+// GPF path (K0), equal to the reference's compensated sum whenever that is
+// correctly rounded
+double mean_intensity(const Image& img) {
+  if (img.pixels() == 0) throw std::invalid_argument("Image dimensions must be >= 1");
+  require_device();
+  double t_c = 0.0;
+  try {
+    Dev in(img.pixels(), img.data()), scal(2 + 4 * (size_t)gpfb::kF64MeanBlocks);
+    gpfb::launch_mean_f64(in.p, (long long)img.pixels(), 1, 0.0, 1.0, scal.p + 2, gpfb::kF64MeanBlocks,
+                          scal.p, nullptr);
+    cu(cudaMemcpy(&t_c, scal.p, sizeof(double), cudaMemcpyDeviceToHost), "D2H");
+  } catch (const gpfb::Error& e) {
+    rethrow(e);
+  }
+  return t_c;
 }
 
 }  // namespace gpfilter

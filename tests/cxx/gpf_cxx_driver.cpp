@@ -10,7 +10,11 @@
 // Prints "ok <fallback_count>" or "error <exception type> <message>".
 // With state:K the run goes through GpfState (init, K steps, finalize) and OUT
 // holds the doubles t_c, c, n, then the images G, F, Fbar, P, Q, H, then the
-// finalize image.
+// finalize image. With fn:NAME (exact|taylor|direct|recursive|misc) the named
+// core function runs instead of gpf (misc: OUT = mean_intensity, kernel_mass_1d,
+// compare(img, shift(img, 1.5), 1).{mse, mse_db, max_abs, pixels}, max_abs_diff,
+// gaussian_range / gauss_polynomial / taylor_polynomial / sup_error x 2 at fixed
+// arguments).
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
@@ -21,6 +25,7 @@
 #include "gpfilter/gpfilter.hpp"
 #else
 #include "core/bilateral.hpp"
+#include "core/metrics.hpp"
 #endif
 
 using namespace gpfilter;
@@ -52,6 +57,36 @@ int main(int argc, char** argv) {
       FILE* f = std::fopen(argv[1], "rb");
       if (!f || std::fread(img.data(), sizeof(double), img.pixels(), f) != img.pixels()) return 3;
       std::fclose(f);
+    }
+    if (argc == 16 && std::strncmp(argv[15], "fn:", 3) == 0) {
+      const std::string fn = argv[15] + 3;
+      FILE* o = std::fopen(argv[4], "wb");
+      long long fb = 0;
+      if (fn == "misc") {
+        const ErrorReport rep = compare(img, shift(img, 1.5), 1);
+        const IntensityRange rg{opts.range.low, opts.range.high};
+        const double v[12] = {mean_intensity(img), kernel_mass_1d(sp.sigma_s, sp.window_radius), rep.mse,
+                              rep.mse_db, rep.max_abs, static_cast<double>(rep.pixels),
+                              max_abs_diff(img, shift(img, -2.25)), gaussian_range(100.0, 40.0, rp),
+                              gauss_polynomial(100.0, 40.0, rp), taylor_polynomial(100.0, 40.0, rp),
+                              sup_error(rp, 40.0, rg, 0.5, RangeApprox::gauss_polynomial),
+                              sup_error(rp, 40.0, rg, 0.5, RangeApprox::taylor)};
+        std::fwrite(v, sizeof(double), 12, o);
+      } else {
+        Image out;
+        if (fn == "exact") out = exact_bilateral(img, sp, rp);
+        else if (fn == "direct") out = direct_gaussian(img, sp);
+        else if (fn == "recursive") out = recursive_gaussian(img, sp.sigma_s, sp.kernel_scale);
+        else {
+          FilterResult r = taylor_bilateral(img, sp, rp, be);
+          out = r.image;
+          fb = r.fallback_count;
+        }
+        std::fwrite(out.data(), sizeof(double), out.pixels(), o);
+      }
+      std::fclose(o);
+      std::printf("ok %lld\n", fb);
+      return 0;
     }
     if (argc == 16) {
       const int steps = std::atoi(argv[15] + 6);

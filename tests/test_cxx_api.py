@@ -22,7 +22,7 @@ REF = os.path.join(ROOT, "oracle", "_ref", "gpf_cxx_driver_ref")
 
 
 def drive(binary, img, ss=3.0, sr=30.0, deg=20, cen=1, mode="mean", low=0.0, high=255.0,
-          backend="recursive", ks=1.0, radius=9, state=None):
+          backend="recursive", ks=1.0, radius=9, state=None, fn=None):
     if not os.path.exists(binary):
         pytest.skip(f"{binary} not built")
     with tempfile.TemporaryDirectory() as d:
@@ -32,7 +32,8 @@ def drive(binary, img, ss=3.0, sr=30.0, deg=20, cen=1, mode="mean", low=0.0, hig
             np.ascontiguousarray(img, dtype="<f8").tofile(src)
         out = subprocess.run([binary, src, str(w), str(h), dst, repr(ss), repr(sr), str(deg), str(cen),
                               mode, repr(low), repr(high), backend, repr(ks), str(radius)]
-                             + ([f"state:{state}"] if state is not None else []),
+                             + ([f"state:{state}"] if state is not None else [])
+                             + ([f"fn:{fn}"] if fn is not None else []),
                              capture_output=True, text=True, timeout=600)
         assert out.returncode == 0, out.stderr
         line = out.stdout.strip()
@@ -42,6 +43,8 @@ def drive(binary, img, ss=3.0, sr=30.0, deg=20, cen=1, mode="mean", low=0.0, hig
             res = {"t_c": raw[0], "c": raw[1], "n": int(raw[2])}
             res.update({k: raw[3 + i * h * w: 3 + (i + 1) * h * w].reshape(h, w) for i, k in enumerate(names)})
             return int(line.split()[1]), res
+        if line.startswith("ok") and fn == "misc":
+            return int(line.split()[1]), np.fromfile(dst, dtype="<f8")
         if line.startswith("ok"):
             return int(line.split()[1]), np.fromfile(dst, dtype="<f8").reshape(h, w)
         _, kind, msg = line.split(" ", 2)
@@ -156,3 +159,49 @@ def test_gpf_state_full_run_equals_gpf():
     rfb, ref = drive(REF, img, deg=12)
     fb, st = drive(OURS, img, deg=12, state=13)
     assert fb == rfb and float(np.abs(st["out"] - ref).max()) <= 1e-9
+
+
+def test_core_functions_validate_like_reference():
+    """exact_bilateral / taylor_bilateral / direct_gaussian / recursive_gaussian: the reference
+    core's exceptions (type and message) for bad parameters, before any device work."""
+    img = synth.rects_image(16, 12, 2, 10.0, 1).astype(np.float64)
+    for fn, case in [("exact", dict(ss=0.0)), ("exact", dict(sr=0.0)), ("exact", dict(radius=0)),
+                     ("taylor", dict(deg=-1)), ("taylor", dict(ss=0.3)), ("direct", dict(ks=0.0)),
+                     ("recursive", dict(ss=0.4)), ("recursive", dict(ss=-1.0))]:
+        ref = drive(REF, img, fn=fn, **case)
+        ours = drive(OURS, img, fn=fn, **case)
+        assert isinstance(ref[0], str) and ref == ours, (fn, case, ref, ours)
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("fn,case,tol", [
+    ("exact", dict(ss=2.0, radius=6), 1e-10), ("taylor", dict(ss=2.5, deg=10), 0.0),
+    ("taylor", dict(ss=2.0, deg=8, backend="direct", radius=5), 0.0),
+    ("direct", dict(ss=3.0, radius=7, ks=0.5), 0.0), ("recursive", dict(ss=4.0, ks=2.0), 0.0),
+])
+def test_core_functions_match_reference_core(fn, case, tol):
+    """The other C++ entry points against the reference's C++ core: the Gaussians and the Taylor
+    baseline bitwise (fallback counts equal), the exact filter to 1e-10."""
+    img = synth.rects_image(40, 28, 3, 10.0, 5).astype(np.float64)
+    rfb, ref = drive(REF, img, fn=fn, **case)
+    fb, out = drive(OURS, img, fn=fn, **case)
+    assert fb == rfb
+    if tol == 0.0:
+        np.testing.assert_array_equal(out, ref)
+    else:
+        assert float(np.abs(out - ref).max()) <= tol
+
+
+@pytest.mark.gpu
+def test_core_scalars_and_metrics_match_reference_core():
+    """mean_intensity, kernel_mass_1d, compare, max_abs_diff, the range-kernel evaluators."""
+    img = synth.rects_image(40, 28, 3, 10.0, 5).astype(np.float64)
+    _, ref = drive(REF, img, fn="misc", deg=12)
+    _, out = drive(OURS, img, fn="misc", deg=12)
+    names = ["mean", "mass", "mse", "mse_db", "max_abs", "pixels", "max_abs_diff", "gauss", "gauss_poly",
+             "taylor", "sup_gp", "sup_taylor"]
+    for k, a, b in zip(names, out, ref):
+        if k in ("mse", "mse_db"):
+            assert a == pytest.approx(b, rel=1e-12), k
+        else:
+            assert a == b, (k, a, b)
