@@ -121,6 +121,14 @@ FilterResult taylor_bilateral(const Image& img, const SpatialParams& sp, const R
 Image direct_gaussian(const Image& img, const SpatialParams& p);
 Image recursive_gaussian(const Image& img, double sigma_s, double kernel_scale = 1.0);
 double kernel_mass_1d(double sigma_s, int window_radius);
+// index i mapped onto [0, n) by the boundary rule, -1 where zero padding drops the sample
+// (ref spatial.hpp:38-40); unnormalised 2-D weight exp(-(jr^2 + jc^2) / 2 sigma_s^2) (42-43)
+int boundary_index(int i, int n, Boundary boundary);
+double spatial_weight(int j_row, int j_col, double sigma_s);
+// ref parallel.hpp:20-22: recorded, not used -- the device work is deterministic and does not
+// depend on a host thread count
+void set_num_threads(int n);
+int num_threads();
 
 double mean_intensity(const Image& img);         // deterministic double-double mean on the GPU
 Image shift(const Image& img, double c);         // every sample decreased by c
@@ -147,7 +155,7 @@ double sup_error(const RangeParams& p, double tau, const IntensityRange& range, 
 // of step(), then finalize(); after n steps c = 1/n!, G = H^n, F = H^n F_0.
 // The state images are public host images, as in the reference; every phase
 // runs on the GPU in the reference-exact fp64 arithmetic (the reference's
-// operation order; only exp() may differ by an ulp) on the images as they
+// operation order; F_0's exp() is correctly rounded, one ulp from glibc's on ~0.1 % of arguments) on the images as they
 // stand, so a caller may inspect or edit them between steps. It is the
 // inspection tool, not the fast path: each step round-trips its images over
 // PCIe (gpf() keeps the planes on the device).

@@ -129,7 +129,8 @@ gpf_status gpf_b200_filter_f32_host(gpf_b200_plan* plan, const float* h_in, floa
  *         1.5-10 for other degrees: the truncated series cancels sooner at low
  *         and odd N) and degree <= 48.
  *   FP64  the reference's own fp64 arithmetic replayed on the GPU operation for
- *         operation (only exp() is CUDA's rather than glibc's): follows the
+ *         operation (exp() is a correctly rounded double-double evaluation,
+ *         equal to glibc's on ~99.9 % of arguments): follows the
  *         reference also where its degree-N series is ill-conditioned and its
  *         output leaves the input range (BASELINE C2/C5). Degree <= 62; about
  *         (degree + 2) x 18 B of extra device memory per pixel. Each axis runs
@@ -164,6 +165,12 @@ float gpf_b200_last_device_ms(void);
  * filter parameter), the fp64 workspace and its device buffers between calls,
  * so repeated calls allocate nothing. This frees all of it. */
 void gpf_b200_dropin_release(void);
+
+/* y[i] = exp(x[i]) as the reference-exact fp64 mode evaluates it on the device
+ * (csrc/exp_cr.h: double-double, correctly rounded; equals glibc's exp on ~99.9 %
+ * of arguments, one ulp apart where glibc itself misrounds). x, y: host arrays of
+ * n doubles. A verification hook (tests/test_exp_cr.py), not a fast path. */
+gpf_status gpf_b200_exp_cr(const double* x, double* y, long long n);
 
 #ifdef __cplusplus
 } /* extern "C" */

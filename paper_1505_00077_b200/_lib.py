@@ -41,7 +41,7 @@ EXPORTED = (
     "gpf_b200_plan_launches_per_frame", "gpf_b200_filter_f32", "gpf_b200_filter_f32_ev",
     "gpf_b200_filter_f32_host", "gpf_b200_exact_f32", "gpf_b200_compare_f32",
     "gpf_b200_set_precision", "gpf_b200_get_precision", "gpf_b200_last_precision",
-    "gpf_b200_last_max_abs_h", "gpf_b200_fp32_h_limit", "gpf_b200_fp32_h_limit_degree", "gpf_b200_dropin_release",
+    "gpf_b200_last_max_abs_h", "gpf_b200_fp32_h_limit", "gpf_b200_fp32_h_limit_degree", "gpf_b200_dropin_release", "gpf_b200_exp_cr",
     "gpf_b200_last_device_ms", "gpf_b200_filter_f32_checked", "gpf_b200_filter_batch",
 )
 
@@ -91,6 +91,7 @@ def _declare(lib: C.CDLL) -> C.CDLL:
     lib.gpf_filter_gpf.argtypes = [vp, C.POINTER(SpatialParams), C.POINTER(RangeParams), C.c_int,
                                    C.c_int, C.POINTER(C.c_longlong), pvp]
     lib.gpf_gaussian_recursive.argtypes = [vp, C.c_double, C.c_double, pvp]
+    lib.gpf_b200_exp_cr.argtypes = [C.c_void_p, C.c_void_p, C.c_longlong]
     lib.gpf_gaussian_direct.argtypes = [vp, C.POINTER(SpatialParams), pvp]
     pd = C.POINTER(C.c_double)
     lib.gpf_kernel_gauss.argtypes = [C.c_double, C.c_double, C.c_double, pd]

@@ -312,7 +312,7 @@ void usage() {
 
 int main(int argc, char** argv) {
   if (argc >= 2 && (!std::strcmp(argv[1], "--version"))) {
-    std::printf("%s\n", gpf_version());
+    std::printf("%s-b200\n", gpf_version());
     return 0;
   }
   if (argc < 2) {

@@ -299,7 +299,8 @@ const char* gpf_status_name(gpf_status status) {
 
 const char* gpf_last_error(void) { return g_last_error.c_str(); }
 
-const char* gpf_version(void) { return "1.0.0-b200"; }
+// the ABI version implemented (the reference pins "1.0.0", proj/tests/test_capi.cpp:37)
+const char* gpf_version(void) { return "1.0.0"; }
 
 gpf_status gpf_image_create(int width, int height, gpf_image** out) {
   if (out == nullptr) return fail(GPF_ERR_INVALID_ARGUMENT, "out is null");
@@ -443,6 +444,20 @@ gpf_status gpf_filter_exact(const gpf_image* in, const gpf_spatial_params* sp,
     std::unique_ptr<gpf_image> hold(res);
     cuda_check(cudaMemcpy(res->px, dout.p, n * sizeof(double), cudaMemcpyDeviceToHost), "D2H");
     *out = hold.release();
+  });
+}
+
+// y[i] = the fp64 mode's correctly rounded exp(x[i]) evaluated on the device (host
+// buffers); exists so that the device instantiation can be compared with the host one
+gpf_status gpf_b200_exp_cr(const double* x, double* y, long long n) {
+  if (x == nullptr || y == nullptr || n < 0) return fail(GPF_ERR_INVALID_ARGUMENT, "null argument");
+  return guarded([&] {
+    current_device();
+    if (n == 0) return;
+    DevBuf dx(n * sizeof(double)), dy(n * sizeof(double));
+    cuda_check(cudaMemcpy(dx.p, x, n * sizeof(double), cudaMemcpyHostToDevice), "H2D");
+    gpfb::run_exp_cr_f64(static_cast<const double*>(dx.p), static_cast<double*>(dy.p), n, nullptr);
+    cuda_check(cudaMemcpy(y, dy.p, n * sizeof(double), cudaMemcpyDeviceToHost), "D2H");
   });
 }
 

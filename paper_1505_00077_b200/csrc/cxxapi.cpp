@@ -176,6 +176,24 @@ Image recursive_gaussian(const Image& img, double sigma_s, double kernel_scale) 
 
 double kernel_mass_1d(double sigma_s, int window_radius) { return gpfb::kernel_mass_1d(sigma_s, window_radius); }
 
+int boundary_index(int i, int n, Boundary boundary) {
+  if (i >= 0 && i < n) return i;
+  if (boundary == Boundary::replicate) return i < 0 ? 0 : n - 1;
+  if (boundary == Boundary::zero) return -1;
+  const long long period = 2LL * n;  // half-sample symmetric: -1 -> 0, n -> n - 1
+  long long m = i % period;
+  if (m < 0) m += period;
+  return static_cast<int>(m < n ? m : period - 1 - m);
+}
+
+double spatial_weight(int j_row, int j_col, double sigma_s) {
+  const double r2 = static_cast<double>(j_row) * j_row + static_cast<double>(j_col) * j_col;
+  return std::exp(-r2 / (2.0 * sigma_s * sigma_s));
+}
+
+void set_num_threads(int n) { gpf_set_num_threads(std::max(1, n)); }
+int num_threads() { return gpf_get_num_threads(); }
+
 Image shift(const Image& img, double c) {
   Image out = img;
   for (std::size_t i = 0; i < out.pixels(); ++i) out.data()[i] -= c;
@@ -189,7 +207,10 @@ double max_abs_diff(const Image& a, const Image& b) {
   return worst;
 }
 
-double mse_db(double mse) { return mse == 0.0 ? kMseDbFloor : std::fmax(10.0 * std::log10(mse), kMseDbFloor); }
+double mse_db(double mse) {
+  if (mse < 0.0) throw std::invalid_argument("mse_db: mse must be non-negative");
+  return mse == 0.0 ? kMseDbFloor : std::fmax(10.0 * std::log10(mse), kMseDbFloor);
+}
 
 ErrorReport compare(const Image& ref, const Image& test, int exclude_border) {
   if (!ref.same_size(test)) throw std::invalid_argument("compare: images differ in size");

@@ -19,9 +19,10 @@
 // All N+2 planes are filtered concurrently (they are independent given H and
 // F_0): one lane per (row, 2 planes) in the row pass, one thread per
 // (column, plane) in the column pass. The only non-replayed operation is
-// exp(): CUDA's exp (<= 1 ulp) instead of glibc's, so F_0 may differ from the
-// reference by an ulp on some pixels; everything downstream is bitwise the
-// reference's evaluation of those inputs. t_c comes from the deterministic
+// exp(): a correctly rounded double-double evaluation (exp_cr.h) instead of
+// glibc's, which is itself correctly rounded on ~99.9 % of arguments -- F_0
+// differs from the reference by one ulp on the rest (~1 pixel in 1,000);
+// everything downstream is bitwise the reference's evaluation of those inputs. t_c comes from the deterministic
 // double-double mean (K0), equal to the reference's Neumaier mean whenever the
 // latter is correctly rounded (every BASELINE frame).
 //
@@ -33,6 +34,7 @@
 
 #include <cuda_runtime.h>
 
+#include "exp_cr.h"
 #include "gpf_internal.h"
 
 namespace gpfb {
@@ -59,7 +61,7 @@ __global__ void k_f64_prologue(const double* __restrict__ f, const double* __res
        i += (long long)gridDim.x * blockDim.x) {
     const double hv = s_(f[i], t_c);
     H[i] = __ddiv_rn(hv, sigma_r);
-    F0[i] = exp(m_(-m_(hv, hv), inv2s2));
+    F0[i] = exp_cr(m_(-m_(hv, hv), inv2s2));  // correctly rounded (exp_cr.h); CUDA's exp is within 1 ulp
   }
 }
 
@@ -780,6 +782,12 @@ void chk(cudaError_t e, const char* what) {
 // ---- GpfState stepping (cxxapi.cpp; bilateral.cpp:64-148), one call per phase
 namespace {
 
+__global__ void k_exp_cr(const double* __restrict__ x, double* __restrict__ y, long long n) {
+  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+       i += (long long)gridDim.x * blockDim.x)
+    y[i] = exp_cr(x[i]);
+}
+
 // step(), first loop (bilateral.cpp:117-120): q += c g fbar; f = h f
 __global__ void k_state_step_a(double* __restrict__ Q, double* __restrict__ F,
                                const double* __restrict__ G, const double* __restrict__ Fbar,
@@ -823,6 +831,12 @@ __global__ void k_state_finalize(const double* __restrict__ in, const double* __
 int state_blocks(long long n) { return (int)std::max<long long>(1, std::min<long long>((n + 255) / 256, 148 * 16)); }
 
 }  // namespace
+
+// the device instantiation of exp_cr.h over n doubles (test hook: gpf_b200_exp_cr)
+void run_exp_cr_f64(const double* d_x, double* d_y, long long n, cudaStream_t st) {
+  k_exp_cr<<<state_blocks(n), 256, 0, st>>>(d_x, d_y, n);
+  chk(cudaGetLastError(), "kernel launch (exp_cr)");
+}
 
 // t_c -> scalars[0] (scalars: 2 doubles; partials: 4 kF64MeanBlocks doubles), H, F_0
 void state_init_f64(const double* d_in, double* H, double* F, double* scalars, double* partials,

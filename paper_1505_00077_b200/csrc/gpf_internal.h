@@ -248,6 +248,8 @@ void state_step_b_f64(double* P, double* G, const double* Fbar, const double* H,
 void state_finalize_f64(const double* in, const double* P, const double* Q, double* out, long long n,
                         double sigma_r, double t_c, unsigned long long* d_fb, cudaStream_t st);
 
+void run_exp_cr_f64(const double* d_x, double* d_y, long long n, cudaStream_t st);
+
 // Drop-in fp64 host entry (dropin.cpp): gpf_filter_gpf and gpfilter::gpf.
 // Per device: an LRU of fp32 plans, the fp64 workspace, device in/out
 // buffers and a stream, reused across calls (a repeated call allocates
