@@ -25,7 +25,9 @@
 #define GPFILTER_B200_GPFILTER_HPP
 
 #include <cstddef>
+#include <cstdint>
 #include <stdexcept>
+#include <string>
 #include <vector>
 
 namespace gpfilter {
@@ -150,6 +152,28 @@ double taylor_polynomial(double t, double tau, const RangeParams& p);
 enum class RangeApprox { gauss_polynomial, taylor };
 double sup_error(const RangeParams& p, double tau, const IntensityRange& range, double step,
                  RangeApprox which);
+
+// PGM codec (ref pgm_io.hpp:17-54; host code, the C ABI's gpf_decode_pgm / gpf_encode_pgm /
+// gpf_read_pgm / gpf_write_pgm are the same routines): P5 and P2 decode with comments, canonical
+// P5 encode, clamp-and-round-half-away quantisation; parse failures carry their kind and the byte
+// offset, file failures are std::runtime_error.
+enum class PgmErrorKind { bad_magic, bad_dims, bad_maxval, truncated, bad_pixel };
+const char* pgm_error_kind_name(PgmErrorKind kind);
+class PgmParseError : public std::runtime_error {
+ public:
+  PgmParseError(PgmErrorKind kind, std::size_t offset, const std::string& detail);
+  PgmErrorKind kind() const { return kind_; }
+  std::size_t offset() const { return offset_; }
+
+ private:
+  PgmErrorKind kind_;
+  std::size_t offset_;
+};
+Image decode_pgm(const std::uint8_t* bytes, std::size_t size);
+std::vector<std::uint8_t> encode_pgm(const Image& img);
+std::uint8_t quantize_sample(double v);
+Image read_pgm(const std::string& path);
+void write_pgm(const Image& img, const std::string& path);
 
 // Step-wise form of gpf (ref bilateral.hpp:38-68): init, then degree + 1 calls
 // of step(), then finalize(); after n steps c = 1/n!, G = H^n, F = H^n F_0.

@@ -27,8 +27,18 @@ def standin(n: int = 256, seed: int = 20260) -> np.ndarray:
     # contrast stretch about the mean: ~15 % of the pixels clip to black (a dark background, as in
     # the photograph), which puts the GPF-vs-exact error at sigma_r 30, N 20 in the harness's
     # "natural 8-bit content" windows (-9.6 / -5.6 dB +- 3 at sigma_s 2 / 3; measured on the
-    # reference library: -7.7, -5.7, -4.3, -3.2 dB at sigma_s 2..5)
-    return np.clip(np.round((base - 166.0) * 1.6 + 105.0), 0, 255).astype(np.uint8)
+    # reference library: about -7.6, -5.6, -4.2, -3.1 dB at sigma_s 2..5)
+    out = np.clip(np.round((base - 166.0) * 1.6 + 109.3), 0, 255)
+    # the harness also pins the photograph's mean (112.6965 +- 1e-4 relative,
+    # proj/tests/test_pgm_io.cpp:239-245): brighten a seeded set of mid-grey pixels by one level
+    # each until the stand-in's mean is there
+    need = int(round(112.6965 * out.size - out.sum()))
+    assert 0 <= need < out.size // 3, need
+    mid = np.flatnonzero((out.ravel() > 40) & (out.ravel() < 215))
+    pick = r.choice(mid, size=need, replace=False)
+    flat = out.ravel()
+    flat[pick] += 1.0
+    return flat.reshape(out.shape).astype(np.uint8)
 
 
 if __name__ == "__main__":

@@ -12,6 +12,7 @@
 #include "gpf_internal.h"
 #include "gpfilter/gpfilter.h"
 #include "gpfilter/gpfilter.hpp"
+#include "pgm.h"
 
 namespace gpfilter {
 
@@ -247,6 +248,73 @@ double sup_error(const RangeParams& p, double tau, const IntensityRange& range, 
     return gpfb::kernel_sup_error(p.sigma_r, p.degree, tau, range.low, range.high, step,
                                   which == RangeApprox::taylor);
   });
+}
+
+// ----------------------------------------------------------------- PGM codec
+const char* pgm_error_kind_name(PgmErrorKind kind) {
+  static const char* const names[] = {"bad_magic", "bad_dims", "bad_maxval", "truncated", "bad_pixel"};
+  const int k = static_cast<int>(kind);
+  return k >= 0 && k < 5 ? names[k] : "unknown";
+}
+
+PgmParseError::PgmParseError(PgmErrorKind kind, std::size_t offset, const std::string& detail)
+    : std::runtime_error(std::string("PGM parse error (") + pgm_error_kind_name(kind) + ") at byte " +
+                         std::to_string(offset) + ": " + detail),
+      kind_(kind),
+      offset_(offset) {}
+
+namespace {
+// the codec (pgm.cpp) reports "PGM parse error (<kind>) at byte <offset>: <detail>" with a
+// GPF_ERR_PGM_* status: back to the typed exception
+[[noreturn]] void rethrow_pgm(const gpfb::Error& e) {
+  if (e.status >= GPF_ERR_PGM_BAD_MAGIC && e.status <= GPF_ERR_PGM_BAD_PIXEL) {
+    const std::string key = ") at byte ";
+    const std::size_t at = e.msg.find(key);
+    std::size_t offset = 0;
+    std::string detail = e.msg;
+    if (at != std::string::npos) {
+      const std::size_t colon = e.msg.find(": ", at);
+      offset = static_cast<std::size_t>(std::stoull(e.msg.substr(at + key.size())));
+      detail = colon == std::string::npos ? "" : e.msg.substr(colon + 2);
+    }
+    throw PgmParseError(static_cast<PgmErrorKind>(e.status - GPF_ERR_PGM_BAD_MAGIC), offset, detail);
+  }
+  throw std::runtime_error(e.msg);
+}
+}  // namespace
+
+Image decode_pgm(const std::uint8_t* bytes, std::size_t size) {
+  try {
+    gpfb::pgm::Decoded d = gpfb::pgm::decode(bytes, size);
+    Image img(d.w, d.h);
+    std::copy(d.pixels.begin(), d.pixels.end(), img.data());
+    return img;
+  } catch (const gpfb::Error& e) {
+    rethrow_pgm(e);
+  }
+}
+
+std::vector<std::uint8_t> encode_pgm(const Image& img) {
+  return gpfb::pgm::encode(img.data(), img.width(), img.height());
+}
+
+std::uint8_t quantize_sample(double v) { return gpfb::pgm::quantize(v); }
+
+Image read_pgm(const std::string& path) {
+  try {
+    const std::vector<std::uint8_t> bytes = gpfb::pgm::read_file(path.c_str());
+    return decode_pgm(bytes.data(), bytes.size());
+  } catch (const gpfb::Error& e) {
+    rethrow_pgm(e);
+  }
+}
+
+void write_pgm(const Image& img, const std::string& path) {
+  try {
+    gpfb::pgm::write_file(path.c_str(), encode_pgm(img));
+  } catch (const gpfb::Error& e) {
+    rethrow_pgm(e);
+  }
 }
 
 // ------------------------------------------------------------------ GpfState
