@@ -228,8 +228,9 @@ __global__ void __launch_bounds__(MAXT, 1) k_rowpass(const Tin* __restrict__ in_
             o = fv[k];
             ++my_fb;
           } else {
-            o = rc.sigma_r * ((static_cast<double>(qp[k].y) * rc.p_scale) /
-                              static_cast<double>(qp[k].x)) + t_c;
+            // sigma_r * (p / q) + t_c as the reference rounds it (bilateral.cpp:144): no FMA
+            o = __dadd_rn(__dmul_rn(rc.sigma_r, __ddiv_rn(static_cast<double>(qp[k].y) * rc.p_scale,
+                                                          static_cast<double>(qp[k].x))), t_c);
           }
           O[r * 33 + c] = static_cast<Tout>(o);
         }
@@ -414,7 +415,11 @@ __device__ __forceinline__ unsigned contract_px(const float2* Ts, const Tin* Fs,
         const float q = fabsf(den) < 1e37f ? __fdividef(num, den) : num / den;
         o = fmaf(sr_f, q, tc_hi) + tc_lo;
       } else {
-        o = rc.sigma_r * ((static_cast<double>(qp[k].y) * psc) / static_cast<double>(qp[k].x)) + t_c;
+        // sigma_r * (p / q) + t_c as the reference rounds it (bilateral.cpp:144): product, then
+        // sum, no FMA -- so that the centred call equals the pre-shifted, uncentred one plus t_c
+        // bit for bit (proj/tests/test_bilateral.cpp:234-258) in this mode too
+        o = __dadd_rn(__dmul_rn(rc.sigma_r, __ddiv_rn(static_cast<double>(qp[k].y) * psc,
+                                                      static_cast<double>(qp[k].x))), t_c);
       }
       if constexpr (OSW) O[pr * 32 + ((((pc >> 2) ^ (pr & 7))) << 2) + (pc & 3)] = o;
       else O[pr * 33 + pc] = o;
