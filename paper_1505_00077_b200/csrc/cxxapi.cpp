@@ -418,6 +418,10 @@ GpfState GpfState::init(const Image& img, const SpatialParams& sp, const RangePa
 }
 
 void GpfState::step() {
+  // the state images are public: a caller may have replaced one
+  for (const Image* im : {&G, &Fbar, &P, &Q, &H})
+    if (!im->same_size(F) || F.pixels() == 0)
+      throw std::invalid_argument("GpfState::step: state images differ in size");
   require_device();
   const size_t count = F.pixels();
   const gpfb::Params p = state_params(F.width(), F.height(), sp_, rp_, backend_);
