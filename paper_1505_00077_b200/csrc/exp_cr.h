@@ -11,8 +11,8 @@
 // returns the same bits as the device one and can be checked against libm and
 // mpmath without a GPU.
 //   x = k ln2 + r, |r| <= ln2 / 2, ln2 = L1 + L2 + L3 (L1: 32 bits, k L1 exact)
-//   exp(r) = exp(r / 256)^256: degree-10 Taylor in double-double (truncation
-//   < 2^-120), then eight double-double squarings
+//   exp(r) = exp(r / 256)^256: degree-9 Taylor (orders 0-4 in double-double, the
+//   tail in double; truncation < 2^-117), then eight double-double squarings
 //   result = round(E_hi + E_lo) 2^k, one rounding also when the result is subnormal
 #ifndef GPFB_EXP_CR_H
 #define GPFB_EXP_CR_H
@@ -91,14 +91,20 @@ GPFB_HD double exp_cr(double x) {
   DD r = two_sum(t1, -ph);
   r = fast_two_sum(r.hi, GPFB_XADD(GPFB_XADD(r.lo, -pl), -GPFB_XMUL(kd, 0x1.cc01f97b57a08p-87)));
   const DD s = DD{GPFB_XMUL(r.hi, 0.00390625), GPFB_XMUL(r.lo, 0.00390625)};  // r / 256, exact
-  // 1/n!, n = 10 .. 2, as double-doubles
-  const DD c[9] = {{0x1.27e4fb7789f5cp-22, 0x1.cbbc05b4fa99ap-76},  {0x1.71de3a556c734p-19, -0x1.c154f8ddc6c00p-73},
-                   {0x1.a01a01a01a01ap-16, 0x1.a01a01a01a01ap-76},  {0x1.a01a01a01a01ap-13, 0x1.a01a01a01a01ap-73},
-                   {0x1.6c16c16c16c17p-10, -0x1.f49f49f49f49fp-65}, {0x1.1111111111111p-7, 0x1.1111111111111p-63},
-                   {0x1.5555555555555p-5, 0x1.5555555555555p-59},   {0x1.5555555555555p-3, 0x1.5555555555555p-57},
-                   {0.5, 0.0}};
-  DD q = c[0];
-  for (int i = 1; i < 9; ++i) q = dd_add(dd_mul(q, s), c[i]);
+  // exp(s) = 1 + s (1 + s (1/2 + s (1/3! + s (1/4! + s T)))), |s| <= 0.00136.
+  // T = 1/5! + s/6! + ... + s^4/9! in plain double: its term enters the sum below 2^-54, so a
+  // 2^-52 relative error in T is below 2^-106 of the result; truncation after s^9/9! < 2^-117
+  const double sh = s.hi;
+  double t = 0x1.71de3a556c734p-19;                              // 1/9!
+  t = GPFB_XFMA(t, sh, 0x1.a01a01a01a01ap-16);                   // 1/8!
+  t = GPFB_XFMA(t, sh, 0x1.a01a01a01a01ap-13);                   // 1/7!
+  t = GPFB_XFMA(t, sh, 0x1.6c16c16c16c17p-10);                   // 1/6!
+  t = GPFB_XFMA(t, sh, 0x1.1111111111111p-7);                    // 1/5!
+  // the low orders in double-double: 1/4!, 1/3!, 1/2
+  const DD c4{0x1.5555555555555p-5, 0x1.5555555555555p-59}, c3{0x1.5555555555555p-3, 0x1.5555555555555p-57};
+  DD q = dd_add(dd_mul(DD{t, 0.0}, s), c4);
+  q = dd_add(dd_mul(q, s), c3);
+  q = dd_add(dd_mul(q, s), DD{0.5, 0.0});
   q = dd_add(dd_mul(q, s), DD{1.0, 0.0});
   DD e = dd_add(dd_mul(q, s), DD{1.0, 0.0});  // exp(r / 256)
   for (int i = 0; i < 8; ++i) e = dd_mul(e, e);
